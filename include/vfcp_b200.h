@@ -1,0 +1,141 @@
+/*
+ * vfcp_b200.h -- C ABI of the B200-native vfcp hot path.
+ *
+ * Drop-in boundary for the reference's numba kernel layer
+ * (/root/reference/pkg/src/vfcp).  The reference binds these stages as
+ * numba @njit functions over caller-allocated numpy arrays that are mutated
+ * in place; this library exposes the same stages, coarsened
+ * to whole-field / frame-streaming device calls over caller-allocated device
+ * buffers.  Plain pointers and sizes only; `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Every call returns 0 on success or a negative
+ * VFCP_E* code; vfcp_last_error() gives the message.
+ *
+ * Device-pointer calls are asynchronous on `stream` unless documented as
+ * synchronising (they return host values).
+ */
+#ifndef VFCP_B200_H
+#define VFCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VFCP_OK 0
+#define VFCP_EINVAL -1      /* bad argument (reference raises ValueError) */
+#define VFCP_ECUDA -2       /* CUDA runtime error */
+#define VFCP_ECAPACITY -3   /* output buffer too small */
+#define VFCP_ECORRUPT -4    /* archive content inconsistent */
+
+#define VFCP_F32 0
+#define VFCP_F64 1
+
+#define VFCP_PRED_MOP 0     /* codec.py:41 PREDICTORS order */
+#define VFCP_PRED_LORENZO 1
+#define VFCP_PRED_SL 2
+
+/* Codec settings (codec.py:44-68 Config + the archive header fields). */
+typedef struct vfcp_params {
+  int32_t H, W, T;
+  double dx, dy, dt;
+  double scale;        /* S, a power of two (field.py:300-310) */
+  int64_t tau;         /* tau' = max(0, floor(eps*S - 0.5)) (codec.py:71-77) */
+  int32_t predictor;   /* VFCP_PRED_* */
+  int32_t bx, by, stride;
+  int32_t radius;      /* |idx| < radius; symbols are uint16 iff radius <= 32768 */
+  int32_t n_max;
+  double lam, theta, d_max;
+} vfcp_params;
+
+const char* vfcp_last_error(void);
+int vfcp_version(void);
+
+/* field.py:69-73 FieldSeries.value_range and the max|x| of to_fixed
+ * (field.py:322).  Synchronising: out3 = {min, max, max|x|} over u and v. */
+int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,
+                     double* out3, void* stream);
+
+/* predicates.py:290-301 build_critical_face_set + ebounds.py:190-206
+ * derive_all + codec.py:97-115 _quantize_eb_vec, fused.
+ *   codes    u8[N]          eb ladder code per vertex (31 = lossless)
+ *   ld_words u32[ceil(N/32)] l_d = (xi == 0) as np.packbits bytes
+ *   mask     u16[N] or NULL positive-face classes per anchor vertex
+ *            (bit c = class c in mesh.py:91-128 order)
+ *   row_n31  i32[T*H]        code-31 vertices per frame row
+ * u, v are float32 or float64 (dtype) device arrays of N = H*W*T. */
+int vfcp_analyze(const vfcp_params* p, const void* u, const void* v,
+                 int dtype, uint8_t* codes, uint32_t* ld_words,
+                 uint16_t* mask, int32_t* row_n31, void* stream);
+
+/* Exclusive row offsets of the qd symbol stream from row_n31:
+ * qd_row_off[r] = 2 * sum_{q<r} (W - row_n31[q]), qd_row_off[T*H] = total.
+ * Synchronising: *total_host = number of qd symbols. */
+int vfcp_qd_offsets(const vfcp_params* p, const int32_t* row_n31,
+                    int64_t* qd_row_off, int64_t* total_host, void* stream);
+
+/* mop.py:154-173 select_modes + codec.py:118-164 _encode_frame over all
+ * frames (codec.py:359-376).
+ *   qd      u16 (or u32 when radius > 32768) symbols, capacity from
+ *           vfcp_qd_offsets
+ *   modes   u8[(T-1)*nby*nbx] per-block modes for t >= 1 (1 = SL)
+ *   scores  f64[(T-1)*nby*nbx*2] or NULL: MoP rates [lorenzo, sl]
+ *   row_ll  i32[T*H] lossless-stream entries per frame row
+ *   recon   i64[2*N] or NULL: the encoder's reconstruction (u then v). */
+int vfcp_encode(const vfcp_params* p, const void* u, const void* v,
+                int dtype, const uint8_t* codes, const int64_t* qd_row_off,
+                void* qd, uint8_t* modes, double* scores, int32_t* row_ll,
+                int64_t* recon, void* stream);
+
+/* Exclusive scan of per-row counts: off[r] = sum_{q<r} cnt[q], off[nrows] =
+ * total.  Synchronising: *total_host = total. */
+int vfcp_row_offsets(const int32_t* cnt, int64_t nrows, int64_t* off,
+                     int64_t* total_host, void* stream);
+
+/* The lossless side stream of codec.py:129-131,155-158 in raster order. */
+int vfcp_encode_ll(const vfcp_params* p, const void* u, const void* v,
+                   int dtype, const uint8_t* codes, const void* qd,
+                   const int64_t* qd_row_off, const int32_t* row_ll,
+                   const int64_t* ll_row_off, int64_t* ll, void* stream);
+
+/* Decoder stream bookkeeping (codec.py:404-413, 447-450).  Synchronising.
+ *   ld       packed l_d bytes or NULL (checked against codes == 31)
+ *   totals   host i64[2] = {qd symbols, ll values} the archive must hold
+ *   ld_ok    host int: 0 if l_d disagrees with the eb codes. */
+int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
+                        const uint8_t* ld, const void* qd, int64_t n_qd,
+                        int32_t* row_n31, int64_t* qd_row_off,
+                        int32_t* row_ll, int64_t* ll_row_off,
+                        int64_t* totals, int* ld_ok, void* stream);
+
+/* codec.py:401-453 decompress_with_stats frame loop (_decode_frame).
+ *   out_u, out_v  f64[N] reconstruction * (1/S)
+ *   fix_u, fix_v  i64[N] or NULL: fixed-point reconstruction. */
+int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
+                const int64_t* ll, const uint8_t* modes,
+                const int64_t* qd_row_off, const int64_t* ll_row_off,
+                double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
+                void* stream);
+
+/* ---- host entropy backend (huffman.py), byte-identical to the reference */
+/* huffman.py:21-48 code_lengths (heapq order, serial tie-break). */
+int vfcp_huff_lengths(const int64_t* counts, int32_t alphabet, uint8_t* lens);
+/* huffman.py:101-113 encode: symbol histogram over a host array of
+ * sym_bytes-wide unsigned symbols. */
+int vfcp_huff_count(const void* symbols, int sym_bytes, int64_t n,
+                    int32_t alphabet, int64_t* counts);
+/* huffman.py:51-76: canonical codes + MSB-first packing into out (zeroed,
+ * ceil(bits/8) bytes).  Returns total bits in *bits. */
+int vfcp_huff_pack(const void* symbols, int sym_bytes, int64_t n,
+                   const uint8_t* lens, int32_t alphabet, uint8_t* out,
+                   int64_t out_bytes, int64_t* bits, int threads);
+/* huffman.py:116-149 decode into sym_bytes-wide symbols.  Returns
+ * VFCP_ECORRUPT if the stream does not consume exactly total_bits. */
+int vfcp_huff_unpack(const uint8_t* data, int64_t total_bits,
+                     const uint8_t* lens, int32_t alphabet, int64_t n,
+                     void* out, int sym_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,474 @@
+"""Archive codec: the reference's public compress/decompress API on a B200.
+
+Mirrors codec.py of the reference (names, signatures, defaults, errors and
+the archive byte layout, codec.py:209-293).  Everything between "field in"
+and "symbol streams out" (and back) runs as sm_100a kernels through the C
+ABI (include/vfcp_b200.h); the Huffman + zlib backend stays on the host as in
+the reference and is timed separately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import struct
+import time
+import zlib
+from dataclasses import dataclass, field as dc_field
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib, huffman
+from .field import (FieldSeries, FixedField, device_range, dtype_code,
+                    scale_for, to_device)
+
+MAGIC = b"VFCP"
+VERSION = 1
+K_MAX = 30
+CODE_LOSSLESS = 31
+EB_ALPHABET = 32
+FLAG_IDENTITY = 0x1
+D_MAX_DEFAULT = 2.0
+N_MAX_DEFAULT = 32
+
+PREDICTORS = ("mop", "lorenzo", "sl")
+
+
+@dataclass(frozen=True)
+class MopConfig:
+    """mop.py:26-37."""
+    bx: int = 32
+    by: int = 32
+    stride: int = 2
+    lam: float = 16.0
+    theta: float = 3e-4
+
+    @property
+    def r_meta(self) -> float:
+        return 1.0 / (self.bx * self.by * 2)
+
+
+@dataclass(frozen=True)
+class Config:
+    """Single source of codec defaults (codec.py:44-68)."""
+    predictor: str = "mop"        # mop | lorenzo | sl
+    bx: int = 32
+    by: int = 32
+    stride: int = 2
+    lam: float = 16.0
+    theta: float = 3e-4
+    radius: int = 1 << 15         # quantization index range: |idx| < radius
+    d_max: float = D_MAX_DEFAULT
+    n_max: int = N_MAX_DEFAULT
+    backend: str = "zlib"         # zlib | identity
+    stats: bool = False
+
+    def __post_init__(self):
+        if self.predictor not in PREDICTORS:
+            raise ValueError(f"unknown predictor {self.predictor!r}")
+        if self.backend not in ("zlib", "identity"):
+            raise ValueError(f"unknown backend {self.backend!r}")
+
+    @property
+    def mop(self) -> MopConfig:
+        return MopConfig(bx=self.bx, by=self.by, stride=self.stride,
+                         lam=self.lam, theta=self.theta)
+
+
+def tau_from_eps(eps: float, scale: float) -> int:
+    """codec.py:71-77."""
+    return max(0, int(math.floor(eps * scale - 0.5)))
+
+
+def quantize_eb(xi: int, tau_prime: int, k_max: int = K_MAX) -> int:
+    """codec.py:80-90 (scalar ladder code)."""
+    if tau_prime <= 0 or xi <= 0:
+        return CODE_LOSSLESS
+    if xi >= tau_prime:
+        return 0
+    m = (tau_prime + xi - 1) // xi
+    k = (m - 1).bit_length()
+    if k > k_max or (tau_prime >> k) == 0:
+        return CODE_LOSSLESS
+    return k
+
+
+def eb_from_code(code: int, tau_prime: int) -> int:
+    return 0 if code == CODE_LOSSLESS else tau_prime >> code
+
+
+_HEADER = struct.Struct("<4sHHIIIdddidqHHHIdddHB")
+
+
+@dataclass
+class Archive:
+    H: int
+    W: int
+    T: int
+    dx: float
+    dy: float
+    dt: float
+    scale: float
+    eps: float
+    tau_prime: int
+    config: Config
+    q_xi: bytes
+    q_d: bytes
+    l_d: bytes
+    lossless_stream: bytes
+    mode_bitmap: bytes
+    stats: "CompressStats | None" = dc_field(default=None, compare=False)
+
+    @property
+    def sections(self) -> tuple[bytes, ...]:
+        return (self.q_xi, self.q_d, self.l_d,
+                self.lossless_stream, self.mode_bitmap)
+
+    def to_bytes(self) -> bytes:
+        """codec.py:236-253."""
+        cfg = self.config
+        flags = FLAG_IDENTITY if cfg.backend == "identity" else 0
+        scale_log2 = round(math.log2(self.scale))
+        head = _HEADER.pack(
+            MAGIC, VERSION, flags, self.H, self.W, self.T,
+            self.dx, self.dy, self.dt, scale_log2, self.eps, self.tau_prime,
+            cfg.bx, cfg.by, cfg.stride, cfg.radius,
+            cfg.lam, cfg.theta, cfg.d_max, cfg.n_max,
+            PREDICTORS.index(cfg.predictor))
+        parts = [head]
+        for sec in self.sections:
+            payload = sec if cfg.backend == "identity" else zlib.compress(sec, 6)
+            parts.append(struct.pack("<QQ", len(payload), len(sec)))
+            parts.append(payload)
+        return b"".join(parts)
+
+    @classmethod
+    def from_bytes(cls, blob: bytes) -> "Archive":
+        """codec.py:255-282."""
+        if len(blob) < _HEADER.size or blob[:4] != MAGIC:
+            raise ValueError("not a VFCP archive")
+        (magic, version, flags, H, W, T, dx, dy, dt, scale_log2, eps, tau,
+         bx, by, stride, radius, lam, theta, d_max, n_max,
+         pred_idx) = _HEADER.unpack_from(blob, 0)
+        if version != VERSION:
+            raise ValueError(f"unsupported archive version {version}")
+        backend = "identity" if flags & FLAG_IDENTITY else "zlib"
+        cfg = Config(predictor=PREDICTORS[pred_idx], bx=bx, by=by,
+                     stride=stride, lam=lam, theta=theta, radius=radius,
+                     d_max=d_max, n_max=n_max, backend=backend)
+        off = _HEADER.size
+        secs = []
+        for _ in range(5):
+            stored, raw = struct.unpack_from("<QQ", blob, off)
+            off += 16
+            payload = blob[off:off + stored]
+            if len(payload) != stored:
+                raise ValueError("truncated archive section")
+            off += stored
+            sec = payload if backend == "identity" else zlib.decompress(payload)
+            if len(sec) != raw:
+                raise ValueError("section length mismatch")
+            secs.append(sec)
+        return cls(H, W, T, dx, dy, dt, 2.0 ** scale_log2, eps, tau, cfg,
+                   *secs)
+
+    @property
+    def nbytes(self) -> int:
+        return len(self.to_bytes())
+
+    def save(self, path) -> None:
+        Path(path).write_bytes(self.to_bytes())
+
+    @classmethod
+    def load(cls, path) -> "Archive":
+        return cls.from_bytes(Path(path).read_bytes())
+
+
+@dataclass
+class CompressStats:
+    """codec.py:296-304."""
+    symbols: np.ndarray
+    signed_indices: np.ndarray
+    overflow_count: int
+    lossless_vertices: int
+    modes: np.ndarray
+    critical_faces: int
+
+
+@dataclass(frozen=True)
+class DecodeStats:
+    """codec.py:307-314."""
+    aux_component_buffers: int
+
+    @property
+    def aux_frames(self) -> float:
+        return self.aux_component_buffers / 2.0
+
+
+def _mode_grid_shape(H, W, cfg: Config):
+    return (-(-H // cfg.by), -(-W // cfg.bx))
+
+
+def make_params(H, W, T, dx, dy, dt, scale, tau, cfg: Config):
+    p = _lib.vfcp_params()
+    p.H, p.W, p.T = H, W, T
+    p.dx, p.dy, p.dt = float(dx), float(dy), float(dt)
+    p.scale = float(scale)
+    p.tau = int(tau)
+    p.predictor = _lib.PRED_INDEX[cfg.predictor]
+    p.bx, p.by, p.stride = int(cfg.bx), int(cfg.by), int(cfg.stride)
+    p.radius = int(cfg.radius)
+    p.n_max = int(cfg.n_max)
+    p.lam, p.theta, p.d_max = float(cfg.lam), float(cfg.theta), float(cfg.d_max)
+    return p
+
+
+def _sym_dtype(radius):
+    import torch
+    return torch.uint16 if radius <= 32768 else torch.int32
+
+
+# --------------------------------------------------------------------------
+# device pipeline (the hot path): field -> symbol streams
+
+@dataclass
+class DeviceStreams:
+    """Device-resident outputs of the compress hot path (torch tensors)."""
+    eps: float
+    scale: float
+    tau: int
+    codes: object       # u8[N]
+    ld: object          # u8[ceil(N/8)] np.packbits(xi == 0)
+    qd: object          # u16 (or u32) symbols
+    ll: object          # i64 lossless side stream
+    modes: object       # u8[(T-1)*nby*nbx]
+    mask: object = None  # u16[N] positive-face classes per anchor
+    scores: object = None
+    recon: object = None
+    n_faces: int | None = None
+
+
+def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
+                    relative: bool = False, want_mask: bool = False,
+                    want_scores: bool = False, want_recon: bool = False,
+                    ) -> DeviceStreams:
+    """codec.py:321-376 up to (not including) the entropy stage, on device."""
+    import torch
+    cfg = config or Config()
+    if eps < 0:
+        raise ValueError("eps must be non-negative")
+    du, dv = to_device(f.u), to_device(f.v)
+    if du.dtype != dv.dtype:
+        du, dv = du.double(), dv.double()
+    lo, hi, ma = device_range(du, dv)
+    if relative:
+        eps = eps * (hi - lo)
+    S = scale_for(ma)
+    tau = tau_from_eps(eps, S)
+    H, W, T = f.H, f.W, f.T
+    N = H * W * T
+    p = make_params(H, W, T, f.dx, f.dy, f.dt, S, tau, cfg)
+    pp = ctypes.byref(p)
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    dev = du.device
+    dt_code = dtype_code(du)
+    codes = torch.empty(N, dtype=torch.uint8, device=dev)
+    ld_words = torch.empty((N + 31) // 32, dtype=torch.int32, device=dev)
+    mask = torch.empty(N, dtype=torch.int16, device=dev) if want_mask else None
+    row_n31 = torch.empty(T * H, dtype=torch.int32, device=dev)
+    _lib.check(L.vfcp_analyze(pp, du.data_ptr(), dv.data_ptr(), dt_code,
+                              codes.data_ptr(), ld_words.data_ptr(),
+                              _lib.ptr(mask), row_n31.data_ptr(), st),
+               "analyze")
+    qd_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
+    nqd = ctypes.c_int64(0)
+    _lib.check(L.vfcp_qd_offsets(pp, row_n31.data_ptr(), qd_row_off.data_ptr(),
+                                 ctypes.addressof(nqd), st), "qd offsets")
+    nby, nbx = _mode_grid_shape(H, W, cfg)
+    qd = torch.empty(max(nqd.value, 1), dtype=_sym_dtype(cfg.radius),
+                     device=dev)
+    modes = torch.empty(max((T - 1) * nby * nbx, 1), dtype=torch.uint8,
+                        device=dev)
+    scores = (torch.empty(max((T - 1) * nby * nbx * 2, 1), dtype=torch.float64,
+                          device=dev) if want_scores else None)
+    recon = (torch.empty(2 * N, dtype=torch.int64, device=dev)
+             if want_recon else None)
+    row_ll = torch.empty(T * H, dtype=torch.int32, device=dev)
+    _lib.check(L.vfcp_encode(pp, du.data_ptr(), dv.data_ptr(), dt_code,
+                             codes.data_ptr(), qd_row_off.data_ptr(),
+                             qd.data_ptr(), modes.data_ptr(), _lib.ptr(scores),
+                             row_ll.data_ptr(), _lib.ptr(recon), st), "encode")
+    ll_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
+    nll = ctypes.c_int64(0)
+    _lib.check(L.vfcp_row_offsets(row_ll.data_ptr(), T * H,
+                                  ll_row_off.data_ptr(), ctypes.addressof(nll),
+                                  st), "ll offsets")
+    ll = torch.empty(max(nll.value, 1), dtype=torch.int64, device=dev)
+    if nll.value:
+        _lib.check(L.vfcp_encode_ll(pp, du.data_ptr(), dv.data_ptr(), dt_code,
+                                    codes.data_ptr(), qd.data_ptr(),
+                                    qd_row_off.data_ptr(), row_ll.data_ptr(),
+                                    ll_row_off.data_ptr(), ll.data_ptr(), st),
+                   "encode ll")
+    ld = ld_words.view(torch.uint8)[:(N + 7) // 8]
+    return DeviceStreams(
+        eps=eps, scale=S, tau=tau, codes=codes, ld=ld,
+        qd=qd[:nqd.value], ll=ll[:nll.value],
+        modes=modes[:(T - 1) * nby * nbx], mask=mask,
+        scores=scores[:(T - 1) * nby * nbx * 2] if scores is not None else None,
+        recon=recon)
+
+
+def archive_from_streams(f_dims, s: DeviceStreams, cfg: Config,
+                         host=None) -> Archive:
+    """Host entropy stage (codec.py:378-387): Huffman + packbits."""
+    H, W, T, dx, dy, dt = f_dims
+    h = host or streams_to_host(s)
+    nby, nbx = _mode_grid_shape(H, W, cfg)
+    return Archive(
+        H=H, W=W, T=T, dx=dx, dy=dy, dt=dt, scale=s.scale, eps=s.eps,
+        tau_prime=s.tau, config=cfg,
+        q_xi=huffman.encode(h["codes"], EB_ALPHABET),
+        q_d=huffman.encode(h["qd"], 2 * cfg.radius),
+        l_d=h["ld"].tobytes(),
+        lossless_stream=h["ll"].astype("<i8").tobytes(),
+        mode_bitmap=np.packbits(h["modes"]).tobytes(),
+    )
+
+
+def streams_to_host(s: DeviceStreams) -> dict:
+    return dict(codes=s.codes.cpu().numpy(), ld=s.ld.cpu().numpy(),
+                qd=s.qd.cpu().numpy(), ll=s.ll.cpu().numpy(),
+                modes=s.modes.cpu().numpy())
+
+
+def compress(f: FieldSeries, eps: float, config: Config | None = None,
+             relative: bool = False) -> Archive:
+    """Compress a field series under a uniform pointwise error bound eps.
+
+    codec.py:321-398.  With relative=True, eps is a fraction of the joint
+    value range.  Every critical-point trajectory of the input is preserved
+    exactly by construction."""
+    cfg = config or Config()
+    s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats)
+    host = streams_to_host(s)
+    a = archive_from_streams((f.H, f.W, f.T, f.dx, f.dy, f.dt), s, cfg, host)
+    if cfg.stats:
+        qd = host["qd"].astype(np.int32)
+        nby, nbx = _mode_grid_shape(f.H, f.W, cfg)
+        mask = s.mask.cpu().numpy().view(np.uint16)
+        n_faces = int(np.unpackbits(mask.view(np.uint8)).sum())
+        a.stats = CompressStats(
+            symbols=qd.copy(),
+            signed_indices=(qd[qd != 0] - cfg.radius).astype(np.int32),
+            overflow_count=int((qd == 0).sum()),
+            lossless_vertices=int(np.unpackbits(host["ld"])[:f.n_samples].sum()),
+            modes=host["modes"].reshape(max(f.T - 1, 0), nby, nbx),
+            critical_faces=n_faces,
+        )
+    return a
+
+
+# --------------------------------------------------------------------------
+# decompression
+
+def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
+                      qd=None, ll=None, modes=None):
+    """codec.py:401-453 on device.  Returns (out_u, out_v, fix_u, fix_v)
+    as CUDA tensors.  codes/qd/ll/modes may be passed pre-decoded (host
+    numpy or device tensors) to skip the host entropy stage."""
+    import torch
+    cfg = a.config
+    n = a.H * a.W * a.T
+    if codes is None:
+        codes = huffman.decode(a.q_xi, np.uint8)
+    if codes.shape[0] != n:
+        raise ValueError("eb code stream length mismatch")
+    if len(a.l_d) < (n + 7) // 8:
+        # np.unpackbits(...)[:n] is shorter than n: never equal to eq == 0
+        raise ValueError("lossless bitmap disagrees with eb codes")
+    if qd is None:
+        qd = huffman.decode(
+            a.q_d, np.uint16 if cfg.radius <= 32768 else np.uint32)
+        if qd.size and int(qd.max()) >= 2 * cfg.radius:
+            raise ValueError("corrupt entropy stream")
+    if ll is None:
+        ll = np.frombuffer(a.lossless_stream, dtype="<i8").astype(np.int64)
+    nby, nbx = _mode_grid_shape(a.H, a.W, cfg)
+    if modes is None:
+        n_mode_bits = max(a.T - 1, 0) * nby * nbx
+        mode_bits = np.unpackbits(
+            np.frombuffer(a.mode_bitmap, dtype=np.uint8))[:n_mode_bits]
+        modes = mode_bits.reshape(max(a.T - 1, 0), nby, nbx).astype(
+            np.uint8).reshape(-1)
+
+    def dev(x, dt=None):
+        if type(x).__module__.startswith("torch"):
+            return x.cuda().contiguous()
+        x = np.ascontiguousarray(x)
+        return torch.from_numpy(x).cuda()
+
+    d_codes = dev(codes)
+    d_ld = dev(np.frombuffer(a.l_d, dtype=np.uint8)[:(n + 7) // 8])
+    d_qd = dev(qd)
+    if d_qd.dtype == torch.int32 and cfg.radius <= 32768:
+        d_qd = d_qd.to(torch.uint16)
+    d_ll = dev(ll) if len(ll) else torch.zeros(1, dtype=torch.int64,
+                                                device="cuda")
+    d_modes = dev(modes) if len(modes) else torch.zeros(1, dtype=torch.uint8,
+                                                        device="cuda")
+    p = make_params(a.H, a.W, a.T, a.dx, a.dy, a.dt, a.scale, a.tau_prime, cfg)
+    pp = ctypes.byref(p)
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    nrows = a.T * a.H
+    row_n31 = torch.empty(nrows, dtype=torch.int32, device="cuda")
+    row_ll = torch.empty(nrows, dtype=torch.int32, device="cuda")
+    qd_row_off = torch.empty(nrows + 1, dtype=torch.int64, device="cuda")
+    ll_row_off = torch.empty(nrows + 1, dtype=torch.int64, device="cuda")
+    totals = np.zeros(2, np.int64)
+    ld_ok = ctypes.c_int(1)
+    n_qd = int(d_qd.numel()) if len(qd) else 0
+    if n_qd == 0:
+        d_qd = torch.zeros(1, dtype=d_qd.dtype, device="cuda")
+    _lib.check(L.vfcp_decode_prepare(
+        pp, d_codes.data_ptr(), d_ld.data_ptr(), d_qd.data_ptr(), n_qd,
+        row_n31.data_ptr(), qd_row_off.data_ptr(), row_ll.data_ptr(),
+        ll_row_off.data_ptr(), totals.ctypes.data, ctypes.addressof(ld_ok),
+        st), "decode prepare")
+    if not ld_ok.value:
+        raise ValueError("lossless bitmap disagrees with eb codes")
+    if totals[0] != n_qd:
+        raise ValueError("residual stream length mismatch")
+    if totals[1] != len(ll):
+        raise ValueError("lossless stream length mismatch")
+    out_u = torch.empty(n, dtype=torch.float64, device="cuda")
+    out_v = torch.empty(n, dtype=torch.float64, device="cuda")
+    fix_u = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
+    fix_v = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
+    _lib.check(L.vfcp_decode(pp, d_codes.data_ptr(), d_qd.data_ptr(),
+                             d_ll.data_ptr(), d_modes.data_ptr(),
+                             qd_row_off.data_ptr(), ll_row_off.data_ptr(),
+                             out_u.data_ptr(), out_v.data_ptr(),
+                             _lib.ptr(fix_u), _lib.ptr(fix_v), st), "decode")
+    return out_u, out_v, fix_u, fix_v
+
+
+def decompress_with_stats(a: Archive) -> tuple[FieldSeries, DecodeStats]:
+    out_u, out_v, _, _ = decompress_device(a)
+    fs = FieldSeries(a.H, a.W, a.T, a.dx, a.dy, a.dt,
+                     out_u.cpu().numpy(), out_v.cpu().numpy())
+    return fs, DecodeStats(aux_component_buffers=4)
+
+
+def decompress(a: Archive) -> FieldSeries:
+    return decompress_with_stats(a)[0]
+
+
+def reconstruct_fixed(a: Archive) -> FixedField:
+    """Reconstruction as integers at the archive's scale (codec.py:460-463)."""
+    _, _, fu, fv = decompress_device(a, want_fixed=True)
+    return FixedField(a.H, a.W, a.T, fu.cpu().numpy(), fv.cpu().numpy(),
+                      a.scale)

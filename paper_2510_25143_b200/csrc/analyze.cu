@@ -1,0 +1,334 @@
+// K0 value-range reduction and K1 fused critical-face / error-bound analysis.
+//
+// K1 replaces, in one pass over the input, the reference's
+//   field.to_fixed conversion          field.py:313-336
+//   build_critical_face_set            predicates.py:270-301
+//   derive_all (+ _eb_scan/_edge_eb)   ebounds.py:101-206
+//   _quantize_eb_vec                   codec.py:97-115
+// A CTA owns a TI x TJ spatial tile and marches through time keeping frames
+// t and t+1 (with a one-vertex halo) in shared memory.  Faces are enumerated
+// implicitly per anchor vertex (12 classes, mesh.py:91-128).  Only the
+// per-vertex eb *code* leaves the kernel (plus l_d bits and, optionally, a
+// 12-bit positive-face mask per anchor); xi itself is never stored: since
+// quantize_eb is monotone non-increasing in xi, code(min over faces) equals
+// max over faces of code(face bound), which is reduced with shared-memory
+// atomicMax.  A vertex class byte (|u|,|v| >= tau'+1 with a sign, and strict
+// signs) lets whole space-time cubes skip the exact integer work:
+// such faces can neither be positive nor lower xi below tau'.
+#include "predicates.cuh"
+
+namespace vfcp {
+
+// ---------------------------------------------------------------- K0
+template <typename F>
+__global__ void __launch_bounds__(256) range_kernel(const F* __restrict__ u,
+                                                    const F* __restrict__ v,
+                                                    int64_t n,
+                                                    double* __restrict__ part) {
+  double lo = INFINITY, hi = -INFINITY, ma = 0.0;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int c = 0; c < 2; c++) {
+    const F* p = c ? v : u;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += stride) {
+      double x = (double)__ldg(p + k);
+      lo = fmin(lo, x);
+      hi = fmax(hi, x);
+      ma = fmax(ma, fabs(x));
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+  }
+  __shared__ double s[3][8];
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s[0][w] = lo; s[1][w] = hi; s[2][w] = ma; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
+      lo = fmin(lo, s[0][q]); hi = fmax(hi, s[1][q]); ma = fmax(ma, s[2][q]);
+    }
+    part[3 * blockIdx.x + 0] = lo;
+    part[3 * blockIdx.x + 1] = hi;
+    part[3 * blockIdx.x + 2] = ma;
+  }
+}
+
+// ---------------------------------------------------------------- K1
+constexpr int TI = 32;             // owned rows per tile
+constexpr int TJ = 64;             // owned columns per tile
+constexpr int RH = TI + 2;         // region rows (1-vertex halo)
+constexpr int RW = TJ + 2;         // region columns
+constexpr int NA = (TI + 1) * (TJ + 1);  // anchors touching owned vertices
+constexpr int K1_THREADS = 256;
+
+// face classes (mesh.py:100-128): vertex offsets (dt, di, dj) of a < b < c
+__constant__ int8_t c_off[12][3][3] = {
+    {{0, 0, 0}, {0, 1, 0}, {0, 1, 1}},  // slice_lower
+    {{0, 0, 0}, {0, 0, 1}, {0, 1, 1}},  // slice_upper
+    {{0, 0, 0}, {0, 0, 1}, {1, 0, 1}},  // wall_h1
+    {{0, 0, 0}, {1, 0, 0}, {1, 0, 1}},  // wall_h2
+    {{0, 0, 0}, {0, 1, 0}, {1, 1, 0}},  // wall_v1
+    {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}},  // wall_v2
+    {{0, 0, 0}, {0, 1, 1}, {1, 1, 1}},  // wall_d1
+    {{0, 0, 0}, {1, 0, 0}, {1, 1, 1}},  // wall_d2
+    {{0, 0, 0}, {0, 1, 0}, {1, 1, 1}},  // int_lower_a
+    {{0, 0, 0}, {1, 1, 0}, {1, 1, 1}},  // int_lower_b
+    {{0, 0, 0}, {0, 0, 1}, {1, 1, 1}},  // int_upper_a
+    {{0, 0, 0}, {1, 0, 1}, {1, 1, 1}},  // int_upper_b
+};
+// anchor range: t < T - lim_t, i < H - lim_i, j < W - lim_j
+__constant__ int8_t c_lim[12][3] = {
+    {0, 1, 1}, {0, 1, 1}, {1, 0, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 0},
+    {1, 1, 1}, {1, 1, 1}, {1, 1, 1}, {1, 1, 1}, {1, 1, 1}, {1, 1, 1}};
+
+struct K1Smem {
+  int32_t u[2][RH][RW];
+  int32_t v[2][RH][RW];
+  uint8_t cls[2][RH][RW];    // low nibble: |.|>=tau'+1 by sign; high: strict sign
+  int32_t acc[2][TI][TJ];    // max eb value (0..32) per owned vertex
+  uint16_t mask[TI][TJ];     // positive-face classes per owned anchor
+  uint16_t list[NA];         // anchors that need exact work
+  int nlist;
+};
+
+__device__ __forceinline__ uint8_t vertex_class(int32_t x, int32_t y,
+                                                int64_t thr) {
+  uint8_t c = 0;
+  if (x >= thr) c |= 1;
+  if (-(int64_t)x >= thr) c |= 2;
+  if (y >= thr) c |= 4;
+  if (-(int64_t)y >= thr) c |= 8;
+  if (x > 0) c |= 16;
+  if (x < 0) c |= 32;
+  if (y > 0) c |= 64;
+  if (y < 0) c |= 128;
+  return c;
+}
+
+template <typename F>
+__global__ void __launch_bounds__(K1_THREADS)
+analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
+               int T, double S, int64_t tau, uint8_t* __restrict__ codes,
+               uint32_t* __restrict__ ld_words, uint16_t* __restrict__ mask,
+               int32_t* __restrict__ row_n31) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.y * TI, j0 = blockIdx.x * TJ;
+  const int64_t HW = (int64_t)H * W;
+  const int64_t thr = tau + 1;
+
+  for (int k = tid; k < 2 * TI * TJ; k += K1_THREADS)
+    (&sm.acc[0][0][0])[k] = 0;
+  for (int k = tid; k < TI * TJ; k += K1_THREADS) (&sm.mask[0][0])[k] = 0;
+
+  auto load_frame = [&](int t) {
+    int s = t & 1;
+    const int64_t base = (int64_t)t * HW;
+    for (int k = tid; k < RH * RW; k += K1_THREADS) {
+      int lr = k / RW, lc = k - lr * RW;
+      int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
+      int32_t x = 0, y = 0;
+      uint8_t c = 0;
+      if (gi >= 0 && gi < H && gj >= 0 && gj < W) {
+        int64_t q = base + (int64_t)gi * W + gj;
+        x = load_fixed(u, q, S);
+        y = load_fixed(v, q, S);
+        c = vertex_class(x, y, thr);
+      }
+      sm.u[s][lr][lc] = x;
+      sm.v[s][lr][lc] = y;
+      sm.cls[s][lr][lc] = c;
+    }
+  };
+
+  load_frame(0);
+  for (int t = 0; t < T; t++) {
+    const bool slab = t + 1 < T;
+    if (slab) load_frame(t + 1);
+    if (tid == 0) sm.nlist = 0;
+    __syncthreads();
+
+    // -- 1. cube test per anchor; compact the anchors needing exact work
+    const int s0 = t & 1, s1 = (t + 1) & 1;
+    for (int k = tid; k < NA; k += K1_THREADS) {
+      int lr = k / (TJ + 1), lc = k - lr * (TJ + 1);
+      int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
+      if (gi < 0 || gj < 0 || gi >= H || gj >= W) continue;
+      // vertices that exist around the anchor (edges of the grid clip)
+      int r1 = gi + 1 < H ? lr + 1 : lr, c1 = gj + 1 < W ? lc + 1 : lc;
+      uint8_t a = sm.cls[s0][lr][lc] & sm.cls[s0][lr][c1] &
+                  sm.cls[s0][r1][lc] & sm.cls[s0][r1][c1];
+      if (slab)
+        a &= sm.cls[s1][lr][lc] & sm.cls[s1][lr][c1] & sm.cls[s1][r1][lc] &
+             sm.cls[s1][r1][c1];
+      if ((a & 0x0F) == 0) {
+        int p = atomicAdd(&sm.nlist, 1);
+        sm.list[p] = (uint16_t)k;
+      }
+    }
+    __syncthreads();
+
+    // -- 2. exact predicate + bound for every (anchor, class) on the list
+    const int nitems = sm.nlist * 12;
+    for (int w = tid; w < nitems; w += K1_THREADS) {
+      int k = sm.list[w / 12], c = w % 12;
+      int lr = k / (TJ + 1), lc = k - lr * (TJ + 1);
+      int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
+      if (t >= T - c_lim[c][0] || gi >= H - c_lim[c][1] ||
+          gj >= W - c_lim[c][2])
+        continue;
+      int vs[3], vr[3], vc[3];
+      int64_t id[3], X[3], Y[3];
+      uint8_t cl[3];
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        int dt = c_off[c][q][0], di = c_off[c][q][1], dj = c_off[c][q][2];
+        vs[q] = (t + dt) & 1;
+        vr[q] = lr + di;
+        vc[q] = lc + dj;
+        X[q] = sm.u[vs[q]][vr[q]][vc[q]];
+        Y[q] = sm.v[vs[q]][vr[q]][vc[q]];
+        cl[q] = sm.cls[vs[q]][vr[q]][vc[q]];
+        id[q] = (int64_t)(t + dt) * HW + (int64_t)(gi + di) * W + (gj + dj);
+      }
+      uint8_t fa = cl[0] & cl[1] & cl[2];
+      if (fa & 0x0F) continue;  // neither positive nor below tau'
+      bool pos = false;
+      if ((fa & 0xF0) == 0)
+        pos = face_positive(X[0], Y[0], X[1], Y[1], X[2], Y[2], id[0], id[1],
+                            id[2]);
+      int val;
+      if (pos) {
+        val = 32;
+        if (mask && lr >= 1 && lc >= 1)
+          atomicOr((unsigned int*)&sm.mask[0][0] +
+                       (((lr - 1) * TJ + (lc - 1)) >> 1),
+                   (1u << c) << (16 * ((lc - 1) & 1)));
+      } else {
+        int64_t xi = tau;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          int q2 = q == 2 ? 0 : q + 1;
+          if ((cl[q] & cl[q2] & 0x0F) == 0) {
+            int64_t e = edge_eb(X[q], Y[q], X[q2], Y[q2]);
+            if (e < xi) xi = e;
+          }
+        }
+        if (xi < 0) xi = 0;
+        val = eb_value(xi, tau);
+      }
+      if (val == 0) continue;
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        int orr = vr[q] - 1, occ = vc[q] - 1;
+        if (orr >= 0 && orr < TI && occ >= 0 && occ < TJ)
+          atomicMax(&sm.acc[vs[q]][orr][occ], val);
+      }
+    }
+    __syncthreads();
+
+    // -- 3. frame t is final: emit codes, l_d bits, row counts, face mask
+    {
+      const int lc = tid & (TJ - 1);
+      const int gj = j0 + lc;
+      const int lane = tid & 31;
+      for (int lr = tid / TJ; lr < TI; lr += K1_THREADS / TJ) {
+        const int gi = i0 + lr;
+        bool inb = gi < H && gj < W;
+        int val = sm.acc[s0][lr][lc];
+        if (tau <= 0) val = 32;
+        int code = val > 31 ? 31 : val;
+        if (inb) {
+          int64_t n = (int64_t)t * HW + (int64_t)gi * W + gj;
+          codes[n] = (uint8_t)code;
+          if (val == 32) set_packbit(ld_words, n);
+          if (mask) mask[n] = sm.mask[lr][lc];
+        }
+        unsigned b = __ballot_sync(0xffffffffu, inb && code == 31);
+        if (lane == 0 && b && gi < H)
+          atomicAdd(row_n31 + (int64_t)t * H + gi, __popc(b));
+        sm.acc[s0][lr][lc] = 0;
+        sm.mask[lr][lc] = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- row offsets (exclusive)
+// out[r] = base + sum_{q < r} mul * (W - cnt[q])   (qd symbol offsets), or
+// out[r] = sum_{q < r} cnt[q] when W == 0 (plain exclusive scan).
+__global__ void __launch_bounds__(1024)
+row_scan_kernel(const int32_t* __restrict__ cnt, int64_t nrows, int W,
+                int mul, int64_t* __restrict__ out) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  int64_t per = (nrows + 1023) / 1024;
+  int64_t a = tid * per, b = min(nrows, a + per);
+  int64_t s = 0;
+  for (int64_t r = a; r < b; r++)
+    s += W ? (int64_t)mul * (W - cnt[r]) : (int64_t)cnt[r];
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    int64_t x = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += x;
+    __syncthreads();
+  }
+  int64_t run = tid ? part[tid - 1] : 0;
+  for (int64_t r = a; r < b; r++) {
+    out[r] = run;
+    run += W ? (int64_t)mul * (W - cnt[r]) : (int64_t)cnt[r];
+  }
+  if (tid == 1023) out[nrows] = part[1023];
+}
+
+// ------------------------------------------------------------ launchers
+template <typename F>
+cudaError_t launch_range(const F* u, const F* v, int64_t n, double* part,
+                         int nblocks, cudaStream_t st) {
+  range_kernel<F><<<nblocks, 256, 0, st>>>(u, v, n, part);
+  return cudaGetLastError();
+}
+
+template <typename F>
+cudaError_t launch_analyze(const F* u, const F* v, int H, int W, int T,
+                           double S, int64_t tau, uint8_t* codes,
+                           uint32_t* ld_words, uint16_t* mask,
+                           int32_t* row_n31, cudaStream_t st) {
+  size_t smem = sizeof(K1Smem);
+  cudaError_t e = cudaFuncSetAttribute(
+      analyze_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((W + TJ - 1) / TJ, (H + TI - 1) / TI);
+  analyze_kernel<F><<<grid, K1_THREADS, smem, st>>>(
+      u, v, H, W, T, S, tau, codes, ld_words, mask, row_n31);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_scan(const int32_t* cnt, int64_t nrows, int W, int mul,
+                            int64_t* out, cudaStream_t st) {
+  row_scan_kernel<<<1, 1024, 0, st>>>(cnt, nrows, W, mul, out);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_range<float>(const float*, const float*, int64_t,
+                                         double*, int, cudaStream_t);
+template cudaError_t launch_range<double>(const double*, const double*,
+                                          int64_t, double*, int, cudaStream_t);
+template cudaError_t launch_analyze<float>(const float*, const float*, int,
+                                           int, int, double, int64_t,
+                                           uint8_t*, uint32_t*, uint16_t*,
+                                           int32_t*, cudaStream_t);
+template cudaError_t launch_analyze<double>(const double*, const double*, int,
+                                            int, int, double, int64_t,
+                                            uint8_t*, uint32_t*, uint16_t*,
+                                            int32_t*, cudaStream_t);
+
+}  // namespace vfcp

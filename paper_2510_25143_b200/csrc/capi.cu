@@ -1,0 +1,425 @@
+// C ABI (include/vfcp_b200.h): host-side orchestration of the B200 kernels.
+//
+// The frame loop mirrors codec.py:359-376 (compress) and codec.py:427-446
+// (decompress): modes for frame t >= 1 are selected on the reconstruction of
+// frame t-1, then frame t is encoded; two frame buffers per component ring in
+// HBM.  Scratch memory comes from the stream-ordered allocator.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vfcp_b200.h"
+#include "common.cuh"
+
+namespace vfcp {
+// analyze.cu
+template <typename F>
+cudaError_t launch_range(const F*, const F*, int64_t, double*, int,
+                         cudaStream_t);
+template <typename F>
+cudaError_t launch_analyze(const F*, const F*, int, int, int, double, int64_t,
+                           uint8_t*, uint32_t*, uint16_t*, int32_t*,
+                           cudaStream_t);
+cudaError_t launch_row_scan(const int32_t*, int64_t, int, int, int64_t*,
+                            cudaStream_t);
+// encode.cu
+template <typename F, typename I>
+cudaError_t launch_mop(const F*, const F*, const I*, const I*,
+                       const FrameParams&, const double*, uint8_t*, double*,
+                       cudaStream_t);
+template <typename F, typename I, typename SYM>
+cudaError_t launch_encode(const F*, const F*, const uint8_t*, const I*,
+                          const I*, I*, I*, const uint8_t*,
+                          const FrameParams&, const Ladder&, const int64_t*,
+                          SYM*, int32_t*, I*, int*, int*, cudaStream_t);
+template <typename F, typename SYM>
+cudaError_t launch_ll_write(const F*, const F*, const uint8_t*, const SYM*,
+                            const int64_t*, const int32_t*, const int64_t*,
+                            int64_t, int, int, double, int64_t*,
+                            cudaStream_t);
+// decode.cu
+cudaError_t launch_decode_rows(const uint8_t*, const uint8_t*, int64_t, int,
+                               int64_t, int32_t*, int*, cudaStream_t);
+template <typename SYM>
+cudaError_t launch_decode_ll(const SYM*, const int64_t*, const int32_t*,
+                             int64_t, int32_t*, cudaStream_t);
+template <typename I, typename SYM>
+cudaError_t launch_decode(const uint8_t*, const SYM*, const int64_t*,
+                          const uint8_t*, const I*, const I*, I*, I*,
+                          const DecodeParams&, const Ladder&, const int64_t*,
+                          const int64_t*, double*, double*, int64_t*,
+                          int64_t*, I*, int*, int*, cudaStream_t);
+}  // namespace vfcp
+
+using namespace vfcp;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(...)                                                            \
+  do {                                                                     \
+    cudaError_t _e = (__VA_ARGS__);                                        \
+    if (_e != cudaSuccess)                                                 \
+      return fail(VFCP_ECUDA, std::string(#__VA_ARGS__) + ": " +           \
+                                  cudaGetErrorString(_e));                 \
+  } while (0)
+
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <typename T>
+  cudaError_t get(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, st);
+    if (e == cudaSuccess) ptrs.push_back(q);
+    *p = (T*)q;
+    return e;
+  }
+  ~Scratch() {
+    for (void* q : ptrs) cudaFreeAsync(q, st);
+  }
+};
+
+int check_params(const vfcp_params* p) {
+  if (!p) return fail(VFCP_EINVAL, "null params");
+  if (p->H < 2 || p->W < 2 || p->T < 2)
+    return fail(VFCP_EINVAL, "dims must be >= 2");
+  if (p->bx < 1 || p->by < 1 || p->stride < 1)
+    return fail(VFCP_EINVAL, "block grid / stride must be positive");
+  if (p->radius < 1) return fail(VFCP_EINVAL, "radius must be positive");
+  if (p->tau < 0) return fail(VFCP_EINVAL, "tau must be non-negative");
+  if (p->predictor < 0 || p->predictor > 2)
+    return fail(VFCP_EINVAL, "unknown predictor");
+  return VFCP_OK;
+}
+
+Ladder make_ladder(int64_t tau) {
+  Ladder L;
+  for (int k = 0; k < 32; k++) {
+    int64_t e = (k == CODE_LOSSLESS || tau <= 0) ? 0 : (tau >> (k > 62 ? 62 : k));
+    L.e[k] = e;
+    L.inv2e[k] = e ? 1.0 / (2.0 * (double)e) : 0.0;
+  }
+  return L;
+}
+
+bool narrow_frames(int64_t tau) { return tau < (((int64_t)1) << 30) - 1; }
+bool narrow_symbols(int radius) { return radius <= 32768; }
+
+FrameParams frame_params(const vfcp_params* p, int t) {
+  FrameParams f;
+  f.H = p->H; f.W = p->W; f.T = p->T; f.t = t;
+  f.S = p->scale;
+  f.tau = p->tau;
+  f.radius = p->radius;
+  f.bx = p->bx; f.by = p->by; f.stride = p->stride;
+  f.nbx = (p->W + p->bx - 1) / p->bx;
+  f.nby = (p->H + p->by - 1) / p->by;
+  f.lam = p->lam; f.theta = p->theta;
+  f.rmeta = 1.0 / (double)(p->bx * p->by * 2);
+  f.d_max = p->d_max;
+  f.n_max = p->n_max;
+  f.cfl_x = (p->dt / p->dx) / p->scale;   // predictors.py:117-119
+  f.cfl_y = (p->dt / p->dy) / p->scale;
+  f.use_modes = t >= 1;
+  return f;
+}
+
+template <typename I>
+__global__ void widen_kernel(const I* a, const I* b, int64_t n, int64_t* oa,
+                             int64_t* ob) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    oa[k] = a[k];
+    ob[k] = b[k];
+  }
+}
+
+template <typename F, typename I, typename SYM>
+int encode_impl(const vfcp_params* p, const F* u, const F* v,
+                const uint8_t* codes, const int64_t* qd_row_off, SYM* qd,
+                uint8_t* modes, double* scores, int32_t* row_ll,
+                int64_t* recon, cudaStream_t st) {
+  const int H = p->H, W = p->W, T = p->T;
+  const int64_t HW = (int64_t)H * W, N = HW * T;
+  const int nstrips = (H + 31) / 32;
+  const int nbx = (W + p->bx - 1) / p->bx, nby = (H + p->by - 1) / p->by;
+  const int64_t nblk = (int64_t)nbx * nby;
+  Scratch sc(st);
+  I *fr, *bnd;
+  int *progress, *ticket;
+  double* log2tab = nullptr;
+  CK(sc.get(&fr, 4 * (size_t)HW));
+  CK(sc.get(&bnd, (size_t)nstrips * W * 2));
+  CK(sc.get(&progress, (size_t)nstrips + 1));
+  CK(sc.get(&ticket, 1));
+  const bool mop = p->predictor == VFCP_PRED_MOP && p->tau > 0;
+  if (mop) {
+    int nlog = 2 * p->bx * p->by + 1;
+    std::vector<double> tab(nlog);
+    tab[0] = 0.0;
+    for (int h = 1; h < nlog; h++) tab[h] = std::log2((double)h);
+    CK(sc.get(&log2tab, (size_t)nlog));
+    CK(cudaMemcpyAsync(log2tab, tab.data(), sizeof(double) * nlog,
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // tab is a host temporary
+  }
+  if (T > 1)
+    CK(cudaMemsetAsync(modes,
+                       (p->predictor == VFCP_PRED_SL && p->tau > 0) ? 1 : 0,
+                       (size_t)(T - 1) * nblk, st));
+  if (scores && T > 1)
+    CK(cudaMemsetAsync(scores, 0, sizeof(double) * 2 * (T - 1) * nblk, st));
+  I* pu = fr;
+  I* pv = fr + HW;
+  I* cu = fr + 2 * HW;
+  I* cv = fr + 3 * HW;
+  CK(cudaMemsetAsync(pu, 0, sizeof(I) * 2 * HW, st));
+  Ladder lad = make_ladder(p->tau);
+  for (int t = 0; t < T; t++) {
+    FrameParams fp = frame_params(p, t);
+    const uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : modes;
+    if (mop && t >= 1) {
+      CK(launch_mop<F, I>(u, v, pu, pv, fp, log2tab, modes,
+                          scores, st));
+    }
+    CK(launch_encode<F, I, SYM>(u, v, codes, pu, pv, cu, cv, modes_t, fp, lad,
+                                qd_row_off, qd, row_ll, bnd, progress, ticket,
+                                st));
+    if (recon)
+      widen_kernel<I><<<1184, 256, 0, st>>>(cu, cv, HW, recon + t * HW,
+                                            recon + N + t * HW);
+    std::swap(pu, cu);
+    std::swap(pv, cv);
+  }
+  CK(cudaGetLastError());
+  return VFCP_OK;
+}
+
+template <typename I, typename SYM>
+int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
+                const int64_t* ll, const uint8_t* modes,
+                const int64_t* qd_row_off, const int64_t* ll_row_off,
+                double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
+                cudaStream_t st) {
+  const int H = p->H, W = p->W, T = p->T;
+  const int64_t HW = (int64_t)H * W;
+  const int nstrips = (H + 31) / 32;
+  const int nbx = (W + p->bx - 1) / p->bx, nby = (H + p->by - 1) / p->by;
+  const int64_t nblk = (int64_t)nbx * nby;
+  Scratch sc(st);
+  I *fr, *bnd;
+  int *progress, *ticket;
+  CK(sc.get(&fr, 4 * (size_t)HW));
+  CK(sc.get(&bnd, (size_t)nstrips * W * 2));
+  CK(sc.get(&progress, (size_t)nstrips + 1));
+  CK(sc.get(&ticket, 1));
+  I* pu = fr;
+  I* pv = fr + HW;
+  I* cu = fr + 2 * HW;
+  I* cv = fr + 3 * HW;
+  CK(cudaMemsetAsync(pu, 0, sizeof(I) * 2 * HW, st));
+  Ladder lad = make_ladder(p->tau);
+  for (int t = 0; t < T; t++) {
+    DecodeParams dp;
+    dp.H = H; dp.W = W; dp.T = T; dp.t = t;
+    dp.inv_S = 1.0 / p->scale;
+    dp.radius = p->radius;
+    dp.bx = p->bx; dp.by = p->by; dp.nbx = nbx;
+    dp.d_max = p->d_max;
+    dp.n_max = p->n_max;
+    dp.cfl_x = (p->dt / p->dx) / p->scale;
+    dp.cfl_y = (p->dt / p->dy) / p->scale;
+    dp.use_modes = t >= 1;
+    const uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : modes;
+    CK(launch_decode<I, SYM>(codes, qd, ll, modes_t, pu, pv, cu, cv, dp, lad,
+                             qd_row_off, ll_row_off, out_u, out_v, fix_u,
+                             fix_v, bnd, progress, ticket, st));
+    std::swap(pu, cu);
+    std::swap(pv, cv);
+  }
+  return VFCP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vfcp_last_error(void) { return g_err.c_str(); }
+int vfcp_version(void) { return 1; }
+
+int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,
+                     double* out3, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return fail(VFCP_EINVAL, "empty field");
+  int dev = 0, nsm = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  int nb = nsm * 8;
+  Scratch sc(st);
+  double* part;
+  CK(sc.get(&part, 3 * (size_t)nb));
+  if (dtype == VFCP_F32)
+    CK(launch_range((const float*)u, (const float*)v, n, part, nb, st));
+  else
+    CK(launch_range((const double*)u, (const double*)v, n, part, nb, st));
+  std::vector<double> h(3 * (size_t)nb);
+  CK(cudaMemcpyAsync(h.data(), part, sizeof(double) * 3 * nb,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double lo = h[0], hi = h[1], ma = h[2];
+  for (int b = 1; b < nb; b++) {
+    lo = std::fmin(lo, h[3 * b]);
+    hi = std::fmax(hi, h[3 * b + 1]);
+    ma = std::fmax(ma, h[3 * b + 2]);
+  }
+  out3[0] = lo; out3[1] = hi; out3[2] = ma;
+  return VFCP_OK;
+}
+
+int vfcp_analyze(const vfcp_params* p, const void* u, const void* v,
+                 int dtype, uint8_t* codes, uint32_t* ld_words,
+                 uint16_t* mask, int32_t* row_n31, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t N = (int64_t)p->H * p->W * p->T;
+  CK(cudaMemsetAsync(ld_words, 0, sizeof(uint32_t) * ((N + 31) / 32), st));
+  CK(cudaMemsetAsync(row_n31, 0, sizeof(int32_t) * (size_t)p->T * p->H, st));
+  if (dtype == VFCP_F32)
+    CK(launch_analyze((const float*)u, (const float*)v, p->H, p->W, p->T,
+                      p->scale, p->tau, codes, ld_words, mask, row_n31, st));
+  else
+    CK(launch_analyze((const double*)u, (const double*)v, p->H, p->W, p->T,
+                      p->scale, p->tau, codes, ld_words, mask, row_n31, st));
+  return VFCP_OK;
+}
+
+int vfcp_qd_offsets(const vfcp_params* p, const int32_t* row_n31,
+                    int64_t* qd_row_off, int64_t* total_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nrows = (int64_t)p->T * p->H;
+  CK(launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
+  CK(cudaMemcpyAsync(total_host, qd_row_off + nrows, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return VFCP_OK;
+}
+
+int vfcp_row_offsets(const int32_t* cnt, int64_t nrows, int64_t* off,
+                     int64_t* total_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(launch_row_scan(cnt, nrows, 0, 1, off, st));
+  CK(cudaMemcpyAsync(total_host, off + nrows, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return VFCP_OK;
+}
+
+int vfcp_encode(const vfcp_params* p, const void* u, const void* v,
+                int dtype, const uint8_t* codes, const int64_t* qd_row_off,
+                void* qd, uint8_t* modes, double* scores, int32_t* row_ll,
+                int64_t* recon, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
+#define ENC(F, I, SYM)                                                      \
+  return encode_impl<F, I, SYM>(p, (const F*)u, (const F*)v, codes,         \
+                                qd_row_off, (SYM*)qd, modes, scores, row_ll, \
+                                recon, st)
+  if (dtype == VFCP_F32) {
+    if (nf) { if (ns) ENC(float, int32_t, uint16_t); else ENC(float, int32_t, uint32_t); }
+    else { if (ns) ENC(float, int64_t, uint16_t); else ENC(float, int64_t, uint32_t); }
+  } else {
+    if (nf) { if (ns) ENC(double, int32_t, uint16_t); else ENC(double, int32_t, uint32_t); }
+    else { if (ns) ENC(double, int64_t, uint16_t); else ENC(double, int64_t, uint32_t); }
+  }
+#undef ENC
+}
+
+int vfcp_encode_ll(const vfcp_params* p, const void* u, const void* v,
+                   int dtype, const uint8_t* codes, const void* qd,
+                   const int64_t* qd_row_off, const int32_t* row_ll,
+                   const int64_t* ll_row_off, int64_t* ll, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nrows = (int64_t)p->T * p->H;
+  const bool ns = narrow_symbols(p->radius);
+#define LLW(F, SYM)                                                         \
+  CK(launch_ll_write<F, SYM>((const F*)u, (const F*)v, codes,               \
+                             (const SYM*)qd, qd_row_off, row_ll,            \
+                             ll_row_off, nrows, p->H, p->W, p->scale, ll,   \
+                             st))
+  if (dtype == VFCP_F32) { if (ns) LLW(float, uint16_t); else LLW(float, uint32_t); }
+  else { if (ns) LLW(double, uint16_t); else LLW(double, uint32_t); }
+#undef LLW
+  return VFCP_OK;
+}
+
+int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
+                        const uint8_t* ld, const void* qd, int64_t n_qd,
+                        int32_t* row_n31, int64_t* qd_row_off,
+                        int32_t* row_ll, int64_t* ll_row_off,
+                        int64_t* totals, int* ld_ok, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nrows = (int64_t)p->T * p->H;
+  Scratch sc(st);
+  int* bad;
+  CK(sc.get(&bad, 1));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  CK(launch_decode_rows(codes, ld, nrows, p->W, p->tau, row_n31, bad, st));
+  CK(launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
+  int64_t nq = 0;
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&nq, qd_row_off + nrows, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  totals[0] = nq;
+  *ld_ok = !hbad;
+  totals[1] = 0;
+  if (nq != n_qd) return VFCP_OK;   // caller raises the length error
+  if (narrow_symbols(p->radius))
+    CK(launch_decode_ll<uint16_t>((const uint16_t*)qd, qd_row_off, row_n31,
+                                  nrows, row_ll, st));
+  else
+    CK(launch_decode_ll<uint32_t>((const uint32_t*)qd, qd_row_off, row_n31,
+                                  nrows, row_ll, st));
+  CK(launch_row_scan(row_ll, nrows, 0, 1, ll_row_off, st));
+  CK(cudaMemcpyAsync(totals + 1, ll_row_off + nrows, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return VFCP_OK;
+}
+
+int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
+                const int64_t* ll, const uint8_t* modes,
+                const int64_t* qd_row_off, const int64_t* ll_row_off,
+                double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
+                void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
+#define DEC(I, SYM)                                                          \
+  return decode_impl<I, SYM>(p, codes, (const SYM*)qd, ll, modes,            \
+                             qd_row_off, ll_row_off, out_u, out_v, fix_u,    \
+                             fix_v, st)
+  if (nf) { if (ns) DEC(int32_t, uint16_t); else DEC(int32_t, uint32_t); }
+  else { if (ns) DEC(int64_t, uint16_t); else DEC(int64_t, uint32_t); }
+#undef DEC
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+"""Canonical Huffman coding over a fixed integer alphabet (host backend).
+
+Same blob layout and bytes as the reference (huffman.py:16,101-149):
+``<IQQ`` (alphabet, symbol count, bit count) + one length byte per symbol +
+MSB-first code bits.  The heavy loops run in the native library
+(csrc/huffman.cpp, multi-threaded packing); this stage stays on the host, as
+in the reference, and is timed separately from the device pipeline.
+"""
+
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+from . import _lib
+
+_HDR = struct.Struct("<IQQ")
+MAX_CODE_LEN = 60
+
+
+def _sym_view(symbols):
+    a = np.ascontiguousarray(symbols)
+    if a.dtype in (np.uint8, np.uint16, np.uint32):
+        return a, a.dtype.itemsize
+    if a.dtype in (np.int8, np.int16, np.int32):
+        if a.size and int(a.min()) < 0:
+            raise ValueError("negative symbol")
+        u = a.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[a.dtype.itemsize])
+        return u, a.dtype.itemsize
+    a = a.astype(np.int64)
+    if a.size and int(a.min()) < 0:
+        raise ValueError("negative symbol")
+    return a, 8
+
+
+def code_lengths(counts) -> np.ndarray:
+    """huffman.py:21-48."""
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    lens = np.zeros(counts.size, dtype=np.uint8)
+    rc = _lib.lib().vfcp_huff_lengths(counts.ctypes.data, counts.size,
+                                      lens.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"code length exceeds {MAX_CODE_LEN}")
+    return lens
+
+
+def encode(symbols, alphabet_size: int) -> bytes:
+    """Encode symbols in [0, alphabet_size) into a self-describing blob."""
+    a, sb = _sym_view(symbols)
+    n = a.size
+    L = _lib.lib()
+    counts = np.zeros(alphabet_size, dtype=np.int64)
+    if n:
+        _lib.check(L.vfcp_huff_count(a.ctypes.data, sb, n, alphabet_size,
+                                     counts.ctypes.data), "huffman count")
+    lens = code_lengths(counts)
+    total_bits = int((counts * lens.astype(np.int64)).sum())
+    out = np.zeros((total_bits + 7) // 8, dtype=np.uint8)
+    if n:
+        bits = ctypes_i64()
+        _lib.check(L.vfcp_huff_pack(a.ctypes.data, sb, n, lens.ctypes.data,
+                                    alphabet_size, out.ctypes.data, out.size,
+                                    bits.ref(), _lib.host_threads()),
+                   "huffman pack")
+    return _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes() + out.tobytes()
+
+
+def decode(blob, out_dtype=np.int64) -> np.ndarray:
+    """Inverse of encode(); raises ValueError on a corrupt stream."""
+    blob = memoryview(blob)
+    alphabet, n_symbols, total_bits = _HDR.unpack_from(blob, 0)
+    off = _HDR.size
+    lens = np.frombuffer(blob, dtype=np.uint8, count=alphabet, offset=off)
+    off += alphabet
+    out = np.empty(n_symbols, dtype=out_dtype)
+    if n_symbols == 0:
+        return out
+    data = np.frombuffer(blob, dtype=np.uint8,
+                         count=(total_bits + 7) // 8, offset=off)
+    lens = np.ascontiguousarray(lens)
+    data = np.ascontiguousarray(data)
+    rc = _lib.lib().vfcp_huff_unpack(data.ctypes.data, total_bits,
+                                     lens.ctypes.data, alphabet, n_symbols,
+                                     out.ctypes.data, out.dtype.itemsize)
+    if rc != 0:
+        raise ValueError("corrupt entropy stream")
+    return out
+
+
+class ctypes_i64:
+    def __init__(self):
+        import ctypes
+        self.v = ctypes.c_int64(0)
+
+    def ref(self):
+        import ctypes
+        return ctypes.addressof(self.v)
