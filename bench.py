@@ -1,0 +1,368 @@
+"""Benchmark: compress / decompress throughput of the B200 hot path.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  A step is one full compress of the workload field
+(config 5 of BASELINE.json: 8192 x 8192 x 16, fp32 u,v, default eps 1e-3 of
+the value range, MoP predictor) with inputs resident in HBM; the value is
+input GB/s = 8 * N bytes / step time (device time, CUDA events, max over
+ranks).  Decompression of the same archive streams is timed the same way and
+reported under "decompress".  `--impl reference` times the CPU oracle port
+of the reference path (oracle/, the test-side restatement; the reference
+itself is Python + numba and does not travel to the GPU box) on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("compress/decompress GB/s (fp32 u,v input) on 1 B200; "
+          "fraction of HBM roofline")
+UNIT = "GB/s"
+
+# algorithmic bytes per vertex
+ALGO_BYTES = {
+    "pipeline_compress": 21.125,
+    "pipeline_decompress": 21.125,
+    "analyze": 8.0 + 1.0 + 0.125,      # fp32 u,v in; code + l_d out
+    "encode": 8.0 + 1.0 + 4.0,         # fp32 u,v + code in; 2 x u16 out
+    "mop": 8.0,                        # fp32 u,v of the frame
+    "decode": 1.0 + 4.0 + 16.0,        # code + 2 x u16 in; 2 x f64 out
+}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_workload(cfg_id, H=None, W=None, T=None):
+    from paper_2510_25143_b200 import synth
+    return synth.generate(cfg_id, H, W, T)
+
+
+def cpu_baseline(cfg_id, eps, sample_hw, sample_t):
+    """The oracle port timed on this host on a bounded crop of the workload."""
+    from oracle import cpu_oracle as O
+    from paper_2510_25143_b200 import Config
+    h, w = sample_hw
+    H, W, T, u, v = load_workload(cfg_id, h, w, sample_t)
+    cfg = Config()
+    O.lib()
+    t0 = time.perf_counter()
+    O.compress_streams(u, v, H, W, T, 1.0, 1.0, 1.0, eps, cfg, relative=True)
+    dt = time.perf_counter() - t0
+    n = H * W * T
+    return {"value": round(8.0 * n / dt / 1e9, 6), "unit": UNIT, "cores": 1,
+            "kind": "port",
+            "sample": f"config {cfg_id} generator at {H}x{W}x{T} "
+                      f"({8 * n / 1e6:.1f} MB fp32 input), eps_rel {eps:g}, "
+                      f"MoP, single-threaded C oracle, {dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on bounded samples (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import cpu_oracle as O
+    from paper_2510_25143_b200 import Config
+    h, w, t = args.ref_sample
+    H, W, T, u, v = load_workload(args.config, h, w, t)
+    cfg = Config()
+    O.lib()
+    for _ in range(args.warmup):
+        O.compress_streams(u, v, H, W, T, 1.0, 1.0, 1.0, args.eps, cfg,
+                           relative=True)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.compress_streams(u, v, H, W, T, 1.0, 1.0, 1.0, args.eps, cfg,
+                           relative=True)
+        times.append(time.perf_counter() - t0)
+    n = H * W * T
+    dt = statistics.mean(times)
+    val = 8.0 * n / dt / 1e9
+    sample = (f"config {args.config} generator at {H}x{W}x{T}, eps_rel "
+              f"{args.eps:g}, MoP; single-threaded C port of the reference "
+              "path (the reference is single-threaded numba)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "sample": sample},
+        "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": 1,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(val, 6), "unit": UNIT,
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(args):
+    from paper_2510_25143_b200 import synth
+    c = synth.CONFIGS[args.config]
+    H = args.H or c["H"]
+    W = args.W or c["W"]
+    T = args.T or c["T"]
+    return f"config{args.config}_{W}x{H}x{T}_fp32_eps{args.eps:g}_mop"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--eps", type=float, default=1e-3)
+    ap.add_argument("--H", type=int, default=None)
+    ap.add_argument("--W", type=int, default=None)
+    ap.add_argument("--T", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decompress", action="store_true")
+    ap.add_argument("--ref-sample", type=int, nargs=3, default=(2048, 2048, 4))
+    ap.add_argument("--cpu-sample", type=int, nargs=3, default=(2048, 2048, 4))
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import _lib, codec
+
+    tg = time.perf_counter()
+    H, W, T, u_h, v_h = load_workload(args.config, args.H, args.W, args.T)
+    gen_s = time.perf_counter() - tg
+    N = H * W * T
+    cfg = vg.Config()
+    du = torch.from_numpy(u_h).cuda()
+    dv = torch.from_numpy(v_h).cuda()
+    f_dev = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, du, dv)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- compress (device-resident inputs)
+    for _ in range(args.warmup):
+        s = vg.compress_device(f_dev, args.eps, cfg, relative=True)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = _lib.launch_count()
+    _lib.prof_enable(True)
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        s = vg.compress_device(f_dev, args.eps, cfg, relative=True)
+    e1.record(st)
+    barrier()
+    comp_ms = e0.elapsed_time(e1) / args.steps
+    prof = _lib.prof_collect()
+    _lib.prof_enable(False)
+    launches = _lib.launch_count() - l0
+    clk = clocks.stop()
+    comp_ms = max_over_ranks(comp_ms)
+
+    # ---- decompress the same streams (device-resident inputs)
+    dec = None
+    if not args.no_decompress:
+        a_meta = codec.Archive(H, W, T, 1.0, 1.0, 1.0, s.scale, s.eps, s.tau,
+                               cfg, b"", b"", s.ld.cpu().numpy().tobytes(),
+                               b"", b"")
+        kw = dict(codes=s.codes, qd=s.qd, ll=s.ll, modes=s.modes, ld=s.ld)
+        for _ in range(args.warmup):
+            vg.decompress_device(a_meta, **kw)
+        barrier()
+        _lib.prof_enable(True)
+        l1 = _lib.launch_count()
+        e0.record(st)
+        for _ in range(args.steps):
+            out = vg.decompress_device(a_meta, **kw)
+        e1.record(st)
+        barrier()
+        dec_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        dprof = _lib.prof_collect()
+        _lib.prof_enable(False)
+        dlaunch = _lib.launch_count() - l1
+        del out
+        dec = {"value": round(8.0 * N * world / (dec_ms * 1e-3) / 1e9, 3),
+               "unit": UNIT, "ms_per_step": round(dec_ms, 3),
+               "gpu_launches": dlaunch,
+               "kernels_ms": {k: round(v[0] / args.steps, 3)
+                              for k, v in dprof.items() if v[1]}}
+
+    # ---- end to end through the public API from pinned host buffers
+    u_pin = torch.from_numpy(u_h).pin_memory()
+    v_pin = torch.from_numpy(v_h).pin_memory()
+    f_host = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u_pin, v_pin)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        s2 = vg.compress_device(f_host, args.eps, cfg, relative=True)
+        host = codec.streams_to_host(s2)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
+    e2e_s = max_over_ranks(e2e_s)
+    d2h = sum(int(x.nbytes) for x in host.values())
+    # host entropy backend (Huffman + zlib), timed on frame 0's streams
+    nq0 = 2 * (H * W) if s.qd.numel() >= 2 * H * W else s.qd.numel()
+    t0 = time.perf_counter()
+    from paper_2510_25143_b200 import huffman
+    import zlib
+    b1 = huffman.encode(host["codes"][:H * W], 32)
+    b2 = huffman.encode(host["qd"][:nq0], 2 * cfg.radius)
+    zlib.compress(b1, 6)
+    zlib.compress(b2, 6)
+    ent_s = time.perf_counter() - t0
+
+    peak, peak_src = measured_peak()
+    # dominant kernel roofline
+    steps = args.steps
+    dom = max((k for k in prof if prof[k][1]), key=lambda k: prof[k][0])
+    dom_ms_per_launch = prof[dom][0] / prof[dom][1]
+    units_per_launch = {"analyze": N, "encode": H * W, "mop": H * W,
+                        "range": N, "scan": T * H, "ll_write": N,
+                        "aux": H * W}.get(dom, N)
+    algo = ALGO_BYTES.get(dom, 0.0) * units_per_launch
+    achieved = algo / (dom_ms_per_launch * 1e-3) / 1e9
+    value = 8.0 * N * world / (comp_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(comp_ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(args), "H": H, "W": W, "T": T,
+                   "eps_rel": args.eps, "predictor": "mop",
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs (8.6 GB) larger than L2",
+                   "generator_s": round(gen_s, 1)},
+        "roofline": {"bound": "hbm", "kernel": dom,
+                     "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None,
+                     "algo_bytes_per_vertex": ALGO_BYTES.get(dom),
+                     "peak_source": peak_src,
+                     "pipeline_frac": round(
+                         ALGO_BYTES["pipeline_compress"] * N
+                         / (comp_ms * 1e-3) / 1e9 / peak, 5)},
+        "kernels_ms": {k: round(v[0] / steps, 3) for k, v in prof.items()
+                       if v[1]},
+        "gpu_launches": launches // max(1, steps),
+        "e2e": {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
+                "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                "d2h_bytes_per_step": d2h},
+        "host_entropy": {"sample": "frame 0 codes + qd: Huffman + zlib(6)",
+                         "seconds": round(ent_s, 3),
+                         "MBps_fp32_input": round(8.0 * H * W / ent_s / 1e6, 2)},
+        "clocks": clk,
+    }
+    if dec is not None:
+        dec["roofline_frac"] = round(
+            ALGO_BYTES["pipeline_decompress"] * N / (dec["ms_per_step"] * 1e-3)
+            / 1e9 / peak, 5)
+        line["decompress"] = dec
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.eps,
+                                            args.cpu_sample[:2],
+                                            args.cpu_sample[2])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -51,6 +51,14 @@ typedef struct vfcp_params {
 const char* vfcp_last_error(void);
 int vfcp_version(void);
 
+/* Instrumentation: number of kernels this library has launched, and
+ * per-kernel-class CUDA-event timings (classes: 0 range, 1 analyze, 2 scan,
+ * 3 mop, 4 encode, 5 ll write, 6 decode rows, 7 decode ll, 8 decode,
+ * 9 aux).  vfcp_prof_collect synchronises on the recorded events. */
+int64_t vfcp_launch_count(void);
+int vfcp_prof_enable(int on);
+int vfcp_prof_collect(double* ms, int64_t* counts, int ncls);
+
 /* field.py:69-73 FieldSeries.value_range and the max|x| of to_fixed
  * (field.py:322).  Synchronising: out3 = {min, max, max|x|} over u and v. */
 int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,

@@ -44,6 +44,9 @@ _PP = ctypes.POINTER(vfcp_params)
 _SIGS = {
     "vfcp_last_error": (ctypes.c_char_p, []),
     "vfcp_version": (_I, []),
+    "vfcp_launch_count": (_I64, []),
+    "vfcp_prof_enable": (_I, [_I]),
+    "vfcp_prof_collect": (_I, [_P, _P, _I]),
     "vfcp_value_range": (_I, [_P, _P, _I, _I64, _P, _P]),
     "vfcp_analyze": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P]),
     "vfcp_qd_offsets": (_I, [_PP, _P, _P, _P, _P]),
@@ -60,6 +63,27 @@ _SIGS = {
 }
 
 EXPORTED = tuple(_SIGS)
+
+KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
+                  "decode_rows", "decode_ll", "decode", "aux")
+
+
+def prof_enable(on=True):
+    lib().vfcp_prof_enable(1 if on else 0)
+
+
+def prof_collect():
+    """{class: (total ms, launches)} since prof_enable (synchronising)."""
+    n = len(KERNEL_CLASSES)
+    ms = np.zeros(n, np.float64)
+    cnt = np.zeros(n, np.int64)
+    check(lib().vfcp_prof_collect(ms.ctypes.data, cnt.ctypes.data, n),
+          "prof_collect")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def launch_count() -> int:
+    return int(lib().vfcp_launch_count())
 
 
 class VfcpError(RuntimeError):

@@ -375,7 +375,7 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
 # decompression
 
 def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
-                      qd=None, ll=None, modes=None):
+                      qd=None, ll=None, modes=None, ld=None):
     """codec.py:401-453 on device.  Returns (out_u, out_v, fix_u, fix_v)
     as CUDA tensors.  codes/qd/ll/modes may be passed pre-decoded (host
     numpy or device tensors) to skip the host entropy stage."""
@@ -408,10 +408,13 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
         if type(x).__module__.startswith("torch"):
             return x.cuda().contiguous()
         x = np.ascontiguousarray(x)
+        if not x.flags.writeable:
+            x = x.copy()
         return torch.from_numpy(x).cuda()
 
     d_codes = dev(codes)
-    d_ld = dev(np.frombuffer(a.l_d, dtype=np.uint8)[:(n + 7) // 8])
+    d_ld = dev(ld if ld is not None else
+               np.frombuffer(a.l_d, dtype=np.uint8)[:(n + 7) // 8])
     d_qd = dev(qd)
     if d_qd.dtype == torch.int32 and cfg.radius <= 32768:
         d_qd = d_qd.to(torch.uint16)

@@ -71,6 +71,34 @@ int fail(int code, const std::string& msg) {
                                   cudaGetErrorString(_e));                 \
   } while (0)
 
+// ---- launch accounting: every kernel launch goes through LAUNCH(), which
+// counts it and, when profiling is on, brackets it with CUDA events on the
+// launching stream (vfcp_prof_*).
+enum KClass { K_RANGE, K_ANALYZE, K_SCAN, K_MOP, K_ENCODE, K_LLW, K_DROWS,
+              K_DLL, K_DECODE, K_AUX, K_NCLS };
+struct Prof {
+  bool on = false;
+  int64_t launches = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+};
+Prof g_prof;
+
+#define LAUNCH(cls, st, ...)                                               \
+  do {                                                                     \
+    cudaEvent_t _a = nullptr, _b = nullptr;                                \
+    if (g_prof.on) {                                                       \
+      cudaEventCreate(&_a);                                                \
+      cudaEventCreate(&_b);                                                \
+      cudaEventRecord(_a, st);                                             \
+    }                                                                      \
+    CK(__VA_ARGS__);                                                       \
+    g_prof.launches++;                                                     \
+    if (g_prof.on) {                                                       \
+      cudaEventRecord(_b, st);                                             \
+      g_prof.ev.push_back({(int)(cls), {_a, _b}});                         \
+    }                                                                      \
+  } while (0)
+
 struct Scratch {
   cudaStream_t st;
   std::vector<void*> ptrs;
@@ -188,15 +216,18 @@ int encode_impl(const vfcp_params* p, const F* u, const F* v,
     FrameParams fp = frame_params(p, t);
     const uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : modes;
     if (mop && t >= 1) {
-      CK(launch_mop<F, I>(u, v, pu, pv, fp, log2tab, modes,
-                          scores, st));
+      LAUNCH(K_MOP, st, launch_mop<F, I>(u, v, pu, pv, fp, log2tab, modes,
+                                        scores, st));
     }
-    CK(launch_encode<F, I, SYM>(u, v, codes, pu, pv, cu, cv, modes_t, fp, lad,
-                                qd_row_off, qd, row_ll, bnd, progress, ticket,
-                                st));
+    LAUNCH(K_ENCODE, st,
+           launch_encode<F, I, SYM>(u, v, codes, pu, pv, cu, cv, modes_t, fp,
+                                    lad, qd_row_off, qd, row_ll, bnd,
+                                    progress, ticket, st));
     if (recon)
-      widen_kernel<I><<<1184, 256, 0, st>>>(cu, cv, HW, recon + t * HW,
-                                            recon + N + t * HW);
+      LAUNCH(K_AUX, st,
+             (widen_kernel<I><<<1184, 256, 0, st>>>(cu, cv, HW, recon + t * HW,
+                                                    recon + N + t * HW),
+              cudaGetLastError()));
     std::swap(pu, cu);
     std::swap(pv, cv);
   }
@@ -240,9 +271,10 @@ int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
     dp.cfl_y = (p->dt / p->dy) / p->scale;
     dp.use_modes = t >= 1;
     const uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : modes;
-    CK(launch_decode<I, SYM>(codes, qd, ll, modes_t, pu, pv, cu, cv, dp, lad,
-                             qd_row_off, ll_row_off, out_u, out_v, fix_u,
-                             fix_v, bnd, progress, ticket, st));
+    LAUNCH(K_DECODE, st,
+           launch_decode<I, SYM>(codes, qd, ll, modes_t, pu, pv, cu, cv, dp,
+                                 lad, qd_row_off, ll_row_off, out_u, out_v,
+                                 fix_u, fix_v, bnd, progress, ticket, st));
     std::swap(pu, cu);
     std::swap(pv, cv);
   }
@@ -256,6 +288,32 @@ extern "C" {
 const char* vfcp_last_error(void) { return g_err.c_str(); }
 int vfcp_version(void) { return 1; }
 
+int64_t vfcp_launch_count(void) { return g_prof.launches; }
+
+int vfcp_prof_enable(int on) {
+  for (auto& e : g_prof.ev) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  g_prof.ev.clear();
+  g_prof.on = on != 0;
+  return VFCP_OK;
+}
+
+int vfcp_prof_collect(double* ms, int64_t* counts, int ncls) {
+  for (int c = 0; c < ncls; c++) { ms[c] = 0.0; counts[c] = 0; }
+  for (auto& e : g_prof.ev) {
+    CK(cudaEventSynchronize(e.second.second));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+    if (e.first < ncls) { ms[e.first] += t; counts[e.first] += 1; }
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  g_prof.ev.clear();
+  return VFCP_OK;
+}
+
 int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,
                      double* out3, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -268,9 +326,9 @@ int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,
   double* part;
   CK(sc.get(&part, 3 * (size_t)nb));
   if (dtype == VFCP_F32)
-    CK(launch_range((const float*)u, (const float*)v, n, part, nb, st));
+    LAUNCH(K_RANGE, st, launch_range((const float*)u, (const float*)v, n, part, nb, st));
   else
-    CK(launch_range((const double*)u, (const double*)v, n, part, nb, st));
+    LAUNCH(K_RANGE, st, launch_range((const double*)u, (const double*)v, n, part, nb, st));
   std::vector<double> h(3 * (size_t)nb);
   CK(cudaMemcpyAsync(h.data(), part, sizeof(double) * 3 * nb,
                      cudaMemcpyDeviceToHost, st));
@@ -295,11 +353,15 @@ int vfcp_analyze(const vfcp_params* p, const void* u, const void* v,
   CK(cudaMemsetAsync(ld_words, 0, sizeof(uint32_t) * ((N + 31) / 32), st));
   CK(cudaMemsetAsync(row_n31, 0, sizeof(int32_t) * (size_t)p->T * p->H, st));
   if (dtype == VFCP_F32)
-    CK(launch_analyze((const float*)u, (const float*)v, p->H, p->W, p->T,
-                      p->scale, p->tau, codes, ld_words, mask, row_n31, st));
+    LAUNCH(K_ANALYZE, st,
+           launch_analyze((const float*)u, (const float*)v, p->H, p->W, p->T,
+                          p->scale, p->tau, codes, ld_words, mask, row_n31,
+                          st));
   else
-    CK(launch_analyze((const double*)u, (const double*)v, p->H, p->W, p->T,
-                      p->scale, p->tau, codes, ld_words, mask, row_n31, st));
+    LAUNCH(K_ANALYZE, st,
+           launch_analyze((const double*)u, (const double*)v, p->H, p->W,
+                          p->T, p->scale, p->tau, codes, ld_words, mask,
+                          row_n31, st));
   return VFCP_OK;
 }
 
@@ -307,7 +369,7 @@ int vfcp_qd_offsets(const vfcp_params* p, const int32_t* row_n31,
                     int64_t* qd_row_off, int64_t* total_host, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   int64_t nrows = (int64_t)p->T * p->H;
-  CK(launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
+  LAUNCH(K_SCAN, st, launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
   CK(cudaMemcpyAsync(total_host, qd_row_off + nrows, sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -317,7 +379,7 @@ int vfcp_qd_offsets(const vfcp_params* p, const int32_t* row_n31,
 int vfcp_row_offsets(const int32_t* cnt, int64_t nrows, int64_t* off,
                      int64_t* total_host, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  CK(launch_row_scan(cnt, nrows, 0, 1, off, st));
+  LAUNCH(K_SCAN, st, launch_row_scan(cnt, nrows, 0, 1, off, st));
   CK(cudaMemcpyAsync(total_host, off + nrows, sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -356,7 +418,7 @@ int vfcp_encode_ll(const vfcp_params* p, const void* u, const void* v,
   int64_t nrows = (int64_t)p->T * p->H;
   const bool ns = narrow_symbols(p->radius);
 #define LLW(F, SYM)                                                         \
-  CK(launch_ll_write<F, SYM>((const F*)u, (const F*)v, codes,               \
+  LAUNCH(K_LLW, st, launch_ll_write<F, SYM>((const F*)u, (const F*)v, codes,               \
                              (const SYM*)qd, qd_row_off, row_ll,            \
                              ll_row_off, nrows, p->H, p->W, p->scale, ll,   \
                              st))
@@ -379,8 +441,8 @@ int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
   int* bad;
   CK(sc.get(&bad, 1));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  CK(launch_decode_rows(codes, ld, nrows, p->W, p->tau, row_n31, bad, st));
-  CK(launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
+  LAUNCH(K_DROWS, st, launch_decode_rows(codes, ld, nrows, p->W, p->tau, row_n31, bad, st));
+  LAUNCH(K_SCAN, st, launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
   int64_t nq = 0;
   int hbad = 0;
   CK(cudaMemcpyAsync(&nq, qd_row_off + nrows, sizeof(int64_t),
@@ -392,12 +454,12 @@ int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
   totals[1] = 0;
   if (nq != n_qd) return VFCP_OK;   // caller raises the length error
   if (narrow_symbols(p->radius))
-    CK(launch_decode_ll<uint16_t>((const uint16_t*)qd, qd_row_off, row_n31,
+    LAUNCH(K_DLL, st, launch_decode_ll<uint16_t>((const uint16_t*)qd, qd_row_off, row_n31,
                                   nrows, row_ll, st));
   else
-    CK(launch_decode_ll<uint32_t>((const uint32_t*)qd, qd_row_off, row_n31,
+    LAUNCH(K_DLL, st, launch_decode_ll<uint32_t>((const uint32_t*)qd, qd_row_off, row_n31,
                                   nrows, row_ll, st));
-  CK(launch_row_scan(row_ll, nrows, 0, 1, ll_row_off, st));
+  LAUNCH(K_SCAN, st, launch_row_scan(row_ll, nrows, 0, 1, ll_row_off, st));
   CK(cudaMemcpyAsync(totals + 1, ll_row_off + nrows, sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
