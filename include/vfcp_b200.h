@@ -117,10 +117,12 @@ int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
                         int64_t* totals, int* ld_ok, void* stream);
 
 /* codec.py:401-453 decompress_with_stats frame loop (_decode_frame).
+ *   qd, ll        the symbol / lossless streams and their lengths
  *   out_u, out_v  f64[N] reconstruction * (1/S)
  *   fix_u, fix_v  i64[N] or NULL: fixed-point reconstruction. */
 int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
-                const int64_t* ll, const uint8_t* modes,
+                int64_t n_qd, const int64_t* ll, int64_t n_ll,
+                const uint8_t* modes,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
                 void* stream);

@@ -15,7 +15,9 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_lib" / "libvfcp_b200.so"
+LIB_PATH = _HERE / "_lib" / (
+    "libvfcp_b200_debug.so" if os.environ.get("VFCP_DEBUG_LIB") else
+    "libvfcp_b200.so")
 
 VFCP_F32, VFCP_F64 = 0, 1
 PRED_INDEX = {"mop": 0, "lorenzo": 1, "sl": 2}
@@ -55,7 +57,8 @@ _SIGS = {
     "vfcp_encode_ll": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "vfcp_decode_prepare": (_I, [_PP, _P, _P, _P, _I64, _P, _P, _P, _P, _P,
                                  _P, _P]),
-    "vfcp_decode": (_I, [_PP, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vfcp_decode": (_I, [_PP, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P,
+                         _P, _P, _P]),
     "vfcp_huff_lengths": (_I, [_P, _I32, _P]),
     "vfcp_huff_count": (_I, [_P, _I, _I64, _I32, _P]),
     "vfcp_huff_pack": (_I, [_P, _I, _I64, _P, _I32, _P, _I64, _P, _I]),

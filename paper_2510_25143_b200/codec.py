@@ -451,8 +451,8 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
     out_v = torch.empty(n, dtype=torch.float64, device="cuda")
     fix_u = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
     fix_v = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
-    _lib.check(L.vfcp_decode(pp, d_codes.data_ptr(), d_qd.data_ptr(),
-                             d_ll.data_ptr(), d_modes.data_ptr(),
+    _lib.check(L.vfcp_decode(pp, d_codes.data_ptr(), d_qd.data_ptr(), n_qd,
+                             d_ll.data_ptr(), len(ll), d_modes.data_ptr(),
                              qd_row_off.data_ptr(), ll_row_off.data_ptr(),
                              out_u.data_ptr(), out_v.data_ptr(),
                              _lib.ptr(fix_u), _lib.ptr(fix_v), st), "decode")

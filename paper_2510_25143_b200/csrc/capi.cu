@@ -5,13 +5,16 @@
 // frame t-1, then frame t is encoded; two frame buffers per component ring in
 // HBM.  Scratch memory comes from the stream-ordered allocator.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/vfcp_b200.h"
+#include "chain.cuh"
 #include "common.cuh"
+#include "wavefront.cuh"
 
 namespace vfcp {
 // analyze.cu
@@ -45,12 +48,34 @@ cudaError_t launch_decode_rows(const uint8_t*, const uint8_t*, int64_t, int,
 template <typename SYM>
 cudaError_t launch_decode_ll(const SYM*, const int64_t*, const int32_t*,
                              int64_t, int32_t*, cudaStream_t);
-template <typename I, typename SYM>
+template <typename IW, typename SYM>
 cudaError_t launch_decode(const uint8_t*, const SYM*, const int64_t*,
-                          const uint8_t*, const I*, const I*, I*, I*,
-                          const DecodeParams&, const Ladder&, const int64_t*,
-                          const int64_t*, double*, double*, int64_t*,
-                          int64_t*, I*, int*, int*, cudaStream_t);
+                          const uint8_t*, const DecodeParams&, const Ladder&,
+                          const int64_t*, const int64_t*, double*, double*,
+                          int64_t*, int64_t*, IW*, int, uint64_t*,
+                          const WaveSched&, int, int, cudaStream_t);
+// fast.cu
+template <typename SYM>
+cudaError_t launch_chunk_prefix(const uint8_t*, const SYM*, const int64_t*,
+                                int64_t, int, int, int64_t, int32_t*,
+                                int32_t*, cudaStream_t);
+template <typename F>
+cudaError_t launch_enc_prep(const F*, const F*, const uint8_t*,
+                            const int32_t*, const int32_t*, const int64_t*,
+                            const int32_t*, const PrepParams&, const double*,
+                            uint8_t*, int32_t*, int32_t*, uint32_t*,
+                            uint32_t*, uint32_t*, uint32_t*, uint16_t*,
+                            int32_t*, int*, uint8_t*, cudaStream_t);
+template <typename SYM>
+cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
+                            const uint8_t*, const int32_t*, const int32_t*,
+                            const int64_t*, const int64_t*, const int32_t*,
+                            const int32_t*, const PrepParams&, int32_t*,
+                            int32_t*, uint32_t*, uint32_t*, cudaStream_t);
+template <bool ENC>
+cudaError_t launch_chain(const ChainIO&, int, cudaStream_t);
+cudaError_t launch_widen_frame(const int32_t*, const int32_t*, int, int, int,
+                               int64_t*, int64_t*, cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -235,48 +260,341 @@ int encode_impl(const vfcp_params* p, const F* u, const F* v,
   return VFCP_OK;
 }
 
+// Semi-Lagrangian reach (cells) of a departure point plus its bilinear
+// stencil: |displacement| <= max|prev| * cfl (predictors.py:76-108, RK2 and
+// substeps alike), +1 for the i1/j1 tap, +1 margin.
+int sl_reach(double maxabs_fixed, double cfl, int lim) {
+  double r = std::ceil(maxabs_fixed * cfl) + 2.0;
+  if (!(r < (double)lim)) return lim;
+  return (int)r;
+}
+
 template <typename I, typename SYM>
 int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
+                int64_t n_qd, const int64_t* ll, int64_t n_ll,
+                const uint8_t* modes,
+                const int64_t* qd_row_off, const int64_t* ll_row_off,
+                double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
+                cudaStream_t st) {
+  const int H = p->H, W = p->W, T = p->T;
+  const int K = (H + 31) / 32;
+  const int nbx = (W + p->bx - 1) / p->bx, nby = (H + p->by - 1) / p->by;
+  const int64_t nblk = (int64_t)nbx * nby;
+  int dev = 0, nsm = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // any semi-Lagrangian block at all?  (decides the inter-frame reach)
+  bool any_sl = false;
+  if (T > 1) {
+    std::vector<uint8_t> hm((size_t)(T - 1) * nblk);
+    CK(cudaMemcpyAsync(hm.data(), modes, hm.size(), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (uint8_t x : hm) if (x) { any_sl = true; break; }
+  }
+  Scratch sc(st);
+  uint64_t* bnd;
+  int *sched;
+  const size_t nbnd = (size_t)T * K * 2 * W * (sizeof(I) / 4);
+  CK(sc.get(&bnd, nbnd));
+  // int recon frames, rows padded to 32 elements (128 B lines never straddle
+  // a strip / chunk boundary, so cp.async through L1 can never see a stale
+  // line of a frame written earlier in the same kernel)
+  const int Wp = (W + 31) / 32 * 32;
+  I* rec;
+  CK(sc.get(&rec, (size_t)T * 2 * H * Wp));
+  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * nbnd, st));
+  CK(sc.get(&sched, (size_t)2 * T * K + 1));
+  CK(cudaMemsetAsync(sched, 0, sizeof(int) * (2 * (size_t)T * K + 1), st));
+  WaveSched ws;
+  ws.ticket = sched;
+  ws.prog = sched + 1;
+  ws.bprog = sched + 1 + (size_t)T * K;
+  ws.K = K;
+  const double cfl_x = (p->dt / p->dx) / p->scale;
+  const double cfl_y = (p->dt / p->dy) / p->scale;
+  // recon magnitude <= 2^30 + tau' (|fixed| < 2^30, |err| <= e <= tau')
+  const double bound = 1073741824.0 + (double)p->tau;
+  const int reach_rows = any_sl ? sl_reach(bound, cfl_y, H) : 0;
+  ws.reach_cols = any_sl ? sl_reach(bound, cfl_x, W) : 0;
+  ws.reach_strips = (reach_rows + 31) / 32;
+  ws.stats = nullptr;
+  const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
+  if (wprof) {
+    CK(sc.get(&ws.stats, WP_N));
+    CK(cudaMemsetAsync(ws.stats, 0, sizeof(unsigned long long) * WP_N, st));
+  }
+  DecodeParams dp;
+  dp.H = H; dp.W = W; dp.T = T; dp.t = 0;
+  dp.n_qd = n_qd;
+  dp.n_ll = n_ll;
+  dp.inv_S = 1.0 / p->scale;
+  dp.S = p->scale;
+  dp.radius = p->radius;
+  dp.bx = p->bx; dp.by = p->by; dp.nbx = nbx;
+  dp.d_max = p->d_max;
+  dp.n_max = p->n_max;
+  dp.cfl_x = cfl_x;
+  dp.cfl_y = cfl_y;
+  dp.use_modes = any_sl ? 1 : 0;
+  Ladder lad = make_ladder(p->tau);
+  LAUNCH(K_DECODE, st,
+         launch_decode<I, SYM>(codes, qd, ll, modes, dp, lad, qd_row_off,
+                               ll_row_off, out_u, out_v, fix_u, fix_v, rec,
+                               Wp, bnd, ws, reach_rows, nsm, st));
+  if (wprof) {
+    unsigned long long h[WP_N];
+    CK(cudaMemcpyAsync(h, ws.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "[wave decode] tasks=%llu total=%.3g waitprev=%.3g pre=%.3g "
+            "waitbnd=%.3g chain=%.3g write=%.3g preload=%.3g sweep=%.3g "
+            "stage+bndput=%.3g (warp-cycles)\n",
+            h[WP_TASKS], (double)h[WP_TOTAL], (double)h[WP_WAITPREV],
+            (double)h[WP_PRE], (double)h[WP_WAITBND], (double)h[WP_CHAIN],
+            (double)h[WP_WRITE], (double)h[WP_X1], (double)h[WP_X2],
+            (double)h[WP_X3]);
+  }
+  return VFCP_OK;
+}
+
+// ------------------------------------------------------------ fast paths
+// Frame-parallel prepare + chain wavefront (fast.cu, chain.cuh).  Valid for
+// the default 32x32 block grid, 16-bit symbols and tau' < 2^28 (every error
+// term then fits int32); the caller falls back to the generic kernels
+// otherwise.
+bool fast_ok(const vfcp_params* p) {
+  return p->bx == 32 && p->by == 32 && p->radius <= 32768 &&
+         p->tau < ((int64_t)1 << 28) && p->stride >= 2;
+}
+
+PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
+  PrepParams pp;
+  pp.H = p->H; pp.W = p->W;
+  pp.nchunks = (p->W + 31) / 32;
+  pp.Wp = 32 * pp.nchunks;
+  pp.nbx = pp.nchunks;
+  pp.nby = (p->H + 31) / 32;
+  pp.t = t;
+  pp.S = p->scale;
+  pp.cfl_x = (p->dt / p->dx) / p->scale;
+  pp.cfl_y = (p->dt / p->dy) / p->scale;
+  pp.d_max = p->d_max;
+  pp.lam = p->lam;
+  pp.theta = p->theta;
+  pp.rmeta = 1.0 / (double)(p->bx * p->by * 2);
+  pp.n_max = p->n_max;
+  pp.stride = p->stride;
+  pp.radius = p->radius;
+  pp.tau = p->tau;
+  pp.mop = p->predictor == VFCP_PRED_MOP && t >= 1 && p->tau > 0;
+  pp.force_sl = p->predictor == VFCP_PRED_SL && t >= 1 && p->tau > 0;
+  pp.lad = lad;
+  return pp;
+}
+
+void chain_tables(ChainIO& io, const Ladder& lad) {
+  for (int k = 0; k < 32; k++) {
+    io.e_tab[k] = (int32_t)lad.e[k];
+    io.inv2e_tab[k] = lad.inv2e[k];
+  }
+}
+
+int nsm_of() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+
+template <typename F>
+int encode_fast(const vfcp_params* p, const F* u, const F* v,
+                const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
+                uint8_t* modes, int32_t* row_ll, cudaStream_t st,
+                bool* overflowed) {
+  const int H = p->H, W = p->W, T = p->T;
+  const int64_t HW = (int64_t)H * W;
+  const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
+  const int nby = (H + 31) / 32;
+  const int64_t nblk = (int64_t)nchunks * nby;
+  const int ntask = (H + 32 * chain_cw(true) - 1) / (32 * chain_cw(true));
+  const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
+  const int nsm = nsm_of();
+  Scratch sc(st);
+  uint8_t* codes_p;
+  CK(sc.get(&codes_p, (size_t)plane));
+  int32_t *pre_nl, *a, *err;
+  uint32_t* pins;
+  uint64_t* bnd;
+  int *ticket, *ovf;
+  double* log2tab = nullptr;
+  CK(sc.get(&pre_nl, (size_t)T * cplane));
+  CK(sc.get(&a, (size_t)2 * plane));
+  CK(sc.get(&err, (size_t)4 * plane));
+  CK(sc.get(&pins, (size_t)4 * cplane));
+  CK(sc.get(&bnd, (size_t)ntask * 2 * W));
+  CK(sc.get(&ticket, (size_t)T));
+  CK(sc.get(&ovf, 1));
+  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * 2 * W, st));
+  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
+  CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
+  const bool mop = p->predictor == VFCP_PRED_MOP && p->tau > 0;
+  std::vector<double> tab;
+  if (mop) {
+    const int nlog = 2 * p->bx * p->by + 1;
+    tab.resize(nlog);
+    tab[0] = 0.0;
+    for (int h = 1; h < nlog; h++) tab[h] = std::log2((double)h);
+    CK(sc.get(&log2tab, (size_t)nlog));
+    CK(cudaMemcpyAsync(log2tab, tab.data(), sizeof(double) * nlog,
+                       cudaMemcpyHostToDevice, st));
+  }
+  if (T > 1)
+    CK(cudaMemsetAsync(modes,
+                       (p->predictor == VFCP_PRED_SL && p->tau > 0) ? 1 : 0,
+                       (size_t)(T - 1) * nblk, st));
+  LAUNCH(K_SCAN, st,
+         launch_chunk_prefix<uint16_t>(codes, nullptr, nullptr,
+                                       (int64_t)T * H, W, nchunks, p->tau,
+                                       pre_nl, nullptr, st));
+  const Ladder lad = make_ladder(p->tau);
+  ChainIO io;
+  memset(&io, 0, sizeof(io));
+  chain_tables(io, lad);
+  const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
+  if (wprof) {
+    CK(sc.get(&io.stats, WP_N));
+    CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
+  }
+  io.a0 = a;
+  io.a1 = a + plane;
+  io.pin_u = pins;
+  io.pin_v = pins + cplane;
+  io.nl = pins + 2 * cplane;
+  io.symw = pins + 3 * cplane;
+  io.qd = qd;
+  io.bnd = bnd;
+  io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
+  io.radius = p->radius;
+  for (int t = 0; t < T; t++) {
+    const PrepParams pp = prep_params(p, t, lad);
+    int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
+    int32_t* ecur = err + 2 * plane * (t & 1);
+    LAUNCH(K_MOP, st,
+           launch_enc_prep<F>(u, v, codes, eprev, eprev + plane, qd_row_off,
+                              pre_nl, pp, log2tab,
+                              t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,
+                              a, a + plane, pins, pins + cplane,
+                              pins + 2 * cplane, pins + 3 * cplane, qd,
+                              row_ll, ovf, codes_p, st));
+    io.codes = codes_p;
+    io.out_i0 = ecur;
+    io.out_i1 = ecur + plane;
+    io.qd_row_off = qd_row_off + (size_t)t * H;
+    io.chunk_nl = pre_nl + (size_t)t * cplane;
+    io.row_esc = row_ll + (size_t)t * H;
+    io.ticket = ticket + t;
+    io.tag_base = (uint32_t)t * (uint32_t)ntask;
+    LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
+  }
+  if (wprof) {
+    unsigned long long h[WP_N];
+    CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "[chain %s] waitchunk=%.3g waitbnd=%.3g sweep=%.3g bnd+ring=%.3g "
+            "writeout=%.3g stage=%.3g (warp-cycles)\n", "enc",
+            (double)h[WP_WAITPREV], (double)h[WP_WAITBND], (double)h[WP_CHAIN],
+            (double)h[WP_X3], (double)h[WP_WRITE], (double)h[WP_PRE]);
+  }
+  int h_ovf = 0;
+  CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *overflowed = h_ovf != 0;
+  return VFCP_OK;
+}
+
+int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                 const int64_t* ll, const uint8_t* modes,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
                 cudaStream_t st) {
   const int H = p->H, W = p->W, T = p->T;
   const int64_t HW = (int64_t)H * W;
-  const int nstrips = (H + 31) / 32;
-  const int nbx = (W + p->bx - 1) / p->bx, nby = (H + p->by - 1) / p->by;
-  const int64_t nblk = (int64_t)nbx * nby;
+  const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
+  const int nby = (H + 31) / 32;
+  const int64_t nblk = (int64_t)nchunks * nby;
+  const int ntask = (H + 32 * chain_cw(false) - 1) / (32 * chain_cw(false));
+  const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
+  const int nsm = nsm_of();
   Scratch sc(st);
-  I *fr, *bnd;
-  int *progress, *ticket;
-  CK(sc.get(&fr, 4 * (size_t)HW));
-  CK(sc.get(&bnd, (size_t)nstrips * W * 2));
-  CK(sc.get(&progress, (size_t)nstrips + 1));
-  CK(sc.get(&ticket, 1));
-  I* pu = fr;
-  I* pv = fr + HW;
-  I* cu = fr + 2 * HW;
-  I* cv = fr + 3 * HW;
-  CK(cudaMemsetAsync(pu, 0, sizeof(I) * 2 * HW, st));
-  Ladder lad = make_ladder(p->tau);
+  int32_t *pre_nl, *pre_ll, *a, *rec;
+  uint32_t* pins;
+  uint64_t* bnd;
+  int* ticket;
+  CK(sc.get(&pre_nl, (size_t)T * cplane));
+  CK(sc.get(&pre_ll, (size_t)T * cplane));
+  CK(sc.get(&a, (size_t)2 * plane));
+  CK(sc.get(&rec, (size_t)4 * plane));
+  CK(sc.get(&pins, (size_t)2 * cplane));
+  CK(sc.get(&bnd, (size_t)ntask * 2 * W));
+  CK(sc.get(&ticket, (size_t)T));
+  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * 2 * W, st));
+  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
+  LAUNCH(K_SCAN, st,
+         launch_chunk_prefix<uint16_t>(codes, qd, qd_row_off, (int64_t)T * H,
+                                       W, nchunks, p->tau, pre_nl, pre_ll,
+                                       st));
+  const Ladder lad = make_ladder(p->tau);
+  ChainIO io;
+  memset(&io, 0, sizeof(io));
+  chain_tables(io, lad);
+  const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
+  if (wprof) {
+    CK(sc.get(&io.stats, WP_N));
+    CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
+  }
+  io.a0 = a;
+  io.a1 = a + plane;
+  io.pin_u = pins;
+  io.pin_v = pins + cplane;
+  io.bnd = bnd;
+  io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
+  io.radius = p->radius;
+  io.inv_S = 1.0 / p->scale;
   for (int t = 0; t < T; t++) {
-    DecodeParams dp;
-    dp.H = H; dp.W = W; dp.T = T; dp.t = t;
-    dp.inv_S = 1.0 / p->scale;
-    dp.radius = p->radius;
-    dp.bx = p->bx; dp.by = p->by; dp.nbx = nbx;
-    dp.d_max = p->d_max;
-    dp.n_max = p->n_max;
-    dp.cfl_x = (p->dt / p->dx) / p->scale;
-    dp.cfl_y = (p->dt / p->dy) / p->scale;
-    dp.use_modes = t >= 1;
-    const uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : modes;
-    LAUNCH(K_DECODE, st,
-           launch_decode<I, SYM>(codes, qd, ll, modes_t, pu, pv, cu, cv, dp,
-                                 lad, qd_row_off, ll_row_off, out_u, out_v,
-                                 fix_u, fix_v, bnd, progress, ticket, st));
-    std::swap(pu, cu);
-    std::swap(pv, cv);
+    const PrepParams pp = prep_params(p, t, lad);
+    int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
+    int32_t* rcur = rec + 2 * plane * (t & 1);
+    LAUNCH(K_DROWS, st,
+           launch_dec_prep<uint16_t>(
+               codes, qd, ll,
+               t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr, rprev,
+               rprev + plane, qd_row_off, ll_row_off, pre_nl, pre_ll, pp, a,
+               a + plane, pins, pins + cplane, st));
+    io.out_i0 = rcur;
+    io.out_i1 = rcur + plane;
+    io.out_f0 = out_u + (size_t)t * HW;
+    io.out_f1 = out_v + (size_t)t * HW;
+    io.ticket = ticket + t;
+    io.tag_base = (uint32_t)t * (uint32_t)ntask;
+    LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
+    if (fix_u)
+      LAUNCH(K_AUX, st,
+             launch_widen_frame(rcur, rcur + plane, H, W, Wp,
+                                fix_u + (size_t)t * HW, fix_v + (size_t)t * HW,
+                                st));
+  }
+  if (wprof) {
+    unsigned long long h[WP_N];
+    CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "[chain %s] waitchunk=%.3g waitbnd=%.3g sweep=%.3g bnd+ring=%.3g "
+            "writeout=%.3g stage=%.3g (warp-cycles)\n", "dec",
+            (double)h[WP_WAITPREV], (double)h[WP_WAITBND], (double)h[WP_CHAIN],
+            (double)h[WP_X3], (double)h[WP_WRITE], (double)h[WP_PRE]);
   }
   return VFCP_OK;
 }
@@ -393,6 +711,18 @@ int vfcp_encode(const vfcp_params* p, const void* u, const void* v,
   int rc = check_params(p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (fast_ok(p) && !scores && !recon && !getenv("VFCP_SLOW_PATH")) {
+    bool ovf = false;
+    int rc2 = dtype == VFCP_F32
+                  ? encode_fast<float>(p, (const float*)u, (const float*)v,
+                                       codes, qd_row_off, (uint16_t*)qd,
+                                       modes, row_ll, st, &ovf)
+                  : encode_fast<double>(p, (const double*)u, (const double*)v,
+                                        codes, qd_row_off, (uint16_t*)qd,
+                                        modes, row_ll, st, &ovf);
+    if (rc2 || !ovf) return rc2;
+    // an R0 did not fit int32: redo the field with the generic kernels
+  }
   const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
 #define ENC(F, I, SYM)                                                      \
   return encode_impl<F, I, SYM>(p, (const F*)u, (const F*)v, codes,         \
@@ -467,16 +797,20 @@ int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
 }
 
 int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
-                const int64_t* ll, const uint8_t* modes,
+                int64_t n_qd, const int64_t* ll, int64_t n_ll,
+                const uint8_t* modes,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
                 void* stream) {
   int rc = check_params(p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (fast_ok(p) && !getenv("VFCP_SLOW_PATH"))
+    return decode_fast(p, codes, (const uint16_t*)qd, ll, modes, qd_row_off,
+                       ll_row_off, out_u, out_v, fix_u, fix_v, st);
   const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
 #define DEC(I, SYM)                                                          \
-  return decode_impl<I, SYM>(p, codes, (const SYM*)qd, ll, modes,            \
+  return decode_impl<I, SYM>(p, codes, (const SYM*)qd, n_qd, ll, n_ll, modes, \
                              qd_row_off, ll_row_off, out_u, out_v, fix_u,    \
                              fix_v, st)
   if (nf) { if (ns) DEC(int32_t, uint16_t); else DEC(int32_t, uint32_t); }

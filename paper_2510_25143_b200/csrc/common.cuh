@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace vfcp {
@@ -38,7 +39,8 @@ struct FrameParams {
 // Per-frame settings of the decode kernels.
 struct DecodeParams {
   int H, W, T, t;
-  double inv_S;
+  int64_t n_qd, n_ll;     // stream lengths (debug bounds checks)
+  double inv_S, S;
   int radius;
   int bx, by, nbx;
   double d_max;
@@ -46,6 +48,21 @@ struct DecodeParams {
   double cfl_x, cfl_y;
   int use_modes;
 };
+
+#ifdef VFCP_DEBUG
+#define VFCP_CHECK(cond, tag)                                                \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      printf("VFCP_CHECK failed: %s (%s:%d) block %d thread %d\n", tag,      \
+             __FILE__, __LINE__, blockIdx.x, threadIdx.x);                   \
+      __trap();                                                              \
+    }                                                                        \
+  } while (0)
+#else
+#define VFCP_CHECK(cond, tag) \
+  do {                        \
+  } while (0)
+#endif
 
 // predictors.py:25-30 _rha: round half away from zero (float64 -> int64).
 __device__ __forceinline__ int64_t rha_d(double x) {
@@ -92,7 +109,7 @@ struct BilinearTap {
 };
 
 __device__ __forceinline__ BilinearTap bilinear_tap(int H, int W, double i_f,
-                                                    double j_f) {
+                                                    double j_f, int pitch) {
   if (i_f < 0.0) i_f = 0.0;
   else if (i_f > (double)(H - 1)) i_f = (double)(H - 1);
   if (j_f < 0.0) j_f = 0.0;
@@ -105,44 +122,81 @@ __device__ __forceinline__ BilinearTap bilinear_tap(int H, int W, double i_f,
   double a = __dsub_rn(i_f, (double)i0), b = __dsub_rn(j_f, (double)j0);
   double oma = __dsub_rn(1.0, a), omb = __dsub_rn(1.0, b);
   BilinearTap t;
-  t.k00 = (int64_t)i0 * W + j0;
-  t.k01 = (int64_t)i0 * W + j1;
-  t.k10 = (int64_t)i1 * W + j0;
-  t.k11 = (int64_t)i1 * W + j1;
+  t.k00 = (int64_t)i0 * pitch + j0;
+  t.k01 = (int64_t)i0 * pitch + j1;
+  t.k10 = (int64_t)i1 * pitch + j0;
+  t.k11 = (int64_t)i1 * pitch + j1;
   t.w00 = __dmul_rn(oma, omb);
   t.w01 = __dmul_rn(oma, b);
   t.w10 = __dmul_rn(a, omb);
   t.w11 = __dmul_rn(a, b);
   return t;
 }
+__device__ __forceinline__ BilinearTap bilinear_tap(int H, int W, double i_f,
+                                                    double j_f) {
+  return bilinear_tap(H, W, i_f, j_f, W);
+}
+
+// Value sources for the semi-Lagrangian sampler: the value of frame entry k
+// as the float64 the reference converts it to ((double) of an int64).
+template <typename I>
+struct IntSrc {
+  const I* p;
+  __device__ __forceinline__ double operator()(int64_t k) const {
+    return (double)p[k];
+  }
+};
+// an integer frame produced earlier in the same kernel (read through L2)
+template <typename I>
+struct IntSrcCG {
+  const I* p;
+  __device__ __forceinline__ double operator()(int64_t k) const {
+    return (double)__ldcg(p + k);
+  }
+};
+// a float64 frame holding recon * (1/S): times S is exact (S = 2^k)
+struct F64Src {
+  const double* p;
+  double S;
+  __device__ __forceinline__ double operator()(int64_t k) const {
+    return __dmul_rn(__ldcg(p + k), S);
+  }
+};
+
+template <typename Src>
+__device__ __forceinline__ int64_t bilinear_src(const BilinearTap& t,
+                                                const Src& f) {
+  double val = __dmul_rn(t.w00, f(t.k00));
+  val = __dadd_rn(val, __dmul_rn(t.w01, f(t.k01)));
+  val = __dadd_rn(val, __dmul_rn(t.w10, f(t.k10)));
+  val = __dadd_rn(val, __dmul_rn(t.w11, f(t.k11)));
+  return rha_d(val);
+}
 
 template <typename I>
 __device__ __forceinline__ int64_t bilinear_apply(const BilinearTap& t,
                                                   const I* f) {
-  double val = __dmul_rn(t.w00, (double)f[t.k00]);
-  val = __dadd_rn(val, __dmul_rn(t.w01, (double)f[t.k01]));
-  val = __dadd_rn(val, __dmul_rn(t.w10, (double)f[t.k10]));
-  val = __dadd_rn(val, __dmul_rn(t.w11, (double)f[t.k11]));
-  return rha_d(val);
+  return bilinear_src(t, IntSrc<I>{f});
 }
 
 // predictors.py:76-108 _sl_departure on the reconstructed frame t-1.
-template <typename I>
-__device__ __forceinline__ void sl_departure(const I* up, const I* vp, int H,
-                                             int W, int i, int j,
-                                             double cfl_x, double cfl_y,
-                                             double d_max, int n_max,
-                                             double* oi, double* oj) {
-  int64_t k = (int64_t)i * W + j;
-  double u0 = (double)up[k], v0 = (double)vp[k];
+template <typename Src>
+__device__ __forceinline__ void sl_departure_src(const Src& up, const Src& vp,
+                                                 int H, int W, int i, int j,
+                                                 double cfl_x, double cfl_y,
+                                                 double d_max, int n_max,
+                                                 double* oi, double* oj,
+                                                 int pitch) {
+  int64_t k = (int64_t)i * pitch + j;
+  double u0 = up(k), v0 = vp(k);
   double ax = __dmul_rn(fabs(u0), cfl_x), ay = __dmul_rn(fabs(v0), cfl_y);
   double d_inf = ay > ax ? ay : ax;
   if (d_inf <= d_max) {
     double ih = __dsub_rn((double)i, __dmul_rn(__dmul_rn(0.5, v0), cfl_y));
     double jh = __dsub_rn((double)j, __dmul_rn(__dmul_rn(0.5, u0), cfl_x));
-    BilinearTap t = bilinear_tap(H, W, ih, jh);
-    double um = (double)bilinear_apply(t, up);
-    double vm = (double)bilinear_apply(t, vp);
+    BilinearTap t = bilinear_tap(H, W, ih, jh, pitch);
+    double um = (double)bilinear_src(t, up);
+    double vm = (double)bilinear_src(t, vp);
     *oi = __dsub_rn((double)i, __dmul_rn(vm, cfl_y));
     *oj = __dsub_rn((double)j, __dmul_rn(um, cfl_x));
     return;
@@ -152,9 +206,9 @@ __device__ __forceinline__ void sl_departure(const I* up, const I* vp, int H,
   double dn = (double)n;
   double fi = (double)i, fj = (double)j;
   for (int64_t s = 0; s < n; s++) {
-    BilinearTap t = bilinear_tap(H, W, fi, fj);
-    double us = (double)bilinear_apply(t, up);
-    double vs = (double)bilinear_apply(t, vp);
+    BilinearTap t = bilinear_tap(H, W, fi, fj, pitch);
+    double us = (double)bilinear_src(t, up);
+    double vs = (double)bilinear_src(t, vp);
     fi = __dsub_rn(fi, __ddiv_rn(__dmul_rn(vs, cfl_y), dn));
     fj = __dsub_rn(fj, __ddiv_rn(__dmul_rn(us, cfl_x), dn));
     if (fi < 0.0) fi = 0.0;
@@ -164,6 +218,16 @@ __device__ __forceinline__ void sl_departure(const I* up, const I* vp, int H,
   }
   *oi = fi;
   *oj = fj;
+}
+
+template <typename I>
+__device__ __forceinline__ void sl_departure(const I* up, const I* vp, int H,
+                                             int W, int i, int j,
+                                             double cfl_x, double cfl_y,
+                                             double d_max, int n_max,
+                                             double* oi, double* oj) {
+  sl_departure_src(IntSrc<I>{up}, IntSrc<I>{vp}, H, W, i, j, cfl_x, cfl_y,
+                   d_max, n_max, oi, oj, W);
 }
 
 // Packed MSB-first bit (np.packbits) n of a byte stream viewed as u32 words.
