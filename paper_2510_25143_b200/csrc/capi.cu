@@ -417,7 +417,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
   const int64_t nblk = (int64_t)nchunks * nby;
-  const int ntask = (H + 32 * chain_cw(true) - 1) / (32 * chain_cw(true));
+  const int ntask = chain_ntask(true, H);
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
@@ -432,10 +432,10 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   CK(sc.get(&a, (size_t)2 * plane));
   CK(sc.get(&err, (size_t)4 * plane));
   CK(sc.get(&pins, (size_t)4 * cplane));
-  CK(sc.get(&bnd, (size_t)ntask * 2 * W));
+  CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
   CK(sc.get(&ovf, 1));
-  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * 2 * W, st));
+  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
   CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
   CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
@@ -503,10 +503,11 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     fprintf(stderr,
-            "[chain %s] waitchunk=%.3g waitbnd=%.3g sweep=%.3g bnd+ring=%.3g "
-            "writeout=%.3g stage=%.3g (warp-cycles)\n", "enc",
-            (double)h[WP_WAITPREV], (double)h[WP_WAITBND], (double)h[WP_CHAIN],
-            (double)h[WP_X3], (double)h[WP_WRITE], (double)h[WP_PRE]);
+            "[chain %s] C: waitchunk=%.3g waitbnd=%.3g sweep=%.3g handoff=%.3g"
+            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)\n",
+            "enc", (double)h[WP_WAITPREV], (double)h[WP_WAITBND],
+            (double)h[WP_CHAIN], (double)h[WP_X3], (double)h[WP_X1],
+            (double)h[WP_WRITE], (double)h[WP_PRE]);
   }
   int h_ovf = 0;
   CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -525,7 +526,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
   const int64_t nblk = (int64_t)nchunks * nby;
-  const int ntask = (H + 32 * chain_cw(false) - 1) / (32 * chain_cw(false));
+  const int ntask = chain_ntask(false, H);
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
@@ -538,9 +539,9 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   CK(sc.get(&a, (size_t)2 * plane));
   CK(sc.get(&rec, (size_t)4 * plane));
   CK(sc.get(&pins, (size_t)2 * cplane));
-  CK(sc.get(&bnd, (size_t)ntask * 2 * W));
+  CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
-  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * 2 * W, st));
+  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
   LAUNCH(K_SCAN, st,
          launch_chunk_prefix<uint16_t>(codes, qd, qd_row_off, (int64_t)T * H,
@@ -591,10 +592,11 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     fprintf(stderr,
-            "[chain %s] waitchunk=%.3g waitbnd=%.3g sweep=%.3g bnd+ring=%.3g "
-            "writeout=%.3g stage=%.3g (warp-cycles)\n", "dec",
-            (double)h[WP_WAITPREV], (double)h[WP_WAITBND], (double)h[WP_CHAIN],
-            (double)h[WP_X3], (double)h[WP_WRITE], (double)h[WP_PRE]);
+            "[chain %s] C: waitchunk=%.3g waitbnd=%.3g sweep=%.3g handoff=%.3g"
+            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)\n",
+            "dec", (double)h[WP_WAITPREV], (double)h[WP_WAITBND],
+            (double)h[WP_CHAIN], (double)h[WP_X3], (double)h[WP_X1],
+            (double)h[WP_WRITE], (double)h[WP_PRE]);
   }
   return VFCP_OK;
 }

@@ -17,14 +17,20 @@
 // [-4e, 4e] and q = Q0 + g with g in {-2..2} found by four comparisons
 // (ties -- y = +-e, +-3e -- round away from zero by the sign of x).
 //
-// A warp owns a 32-row strip (lane = row) and sweeps the columns with a
-// one-column skew per lane, so the neighbours are final when read; a step
-// is shfl -> a few integer ops -> select.  A CTA of CW warps owns CW
-// consecutive strips and hands each strip's last row to the next warp
-// through shared memory; CTAs (taken in row order by an atomic ticket, so a
-// CTA only waits on an earlier, resident one) hand off through tagged
-// global slots.  Inputs are staged per 32-column chunk with cp.async one
-// chunk ahead of the sweep.
+// The two components are independent recurrences.  A task is one
+// component of one 32-row strip, run by a warp PAIR:
+//   C (chain warp): lane = row, sweeps the columns with a one-column skew
+//     per lane so the three neighbours are final when read; a step is
+//     shfl -> a few integer ops -> select, nothing else.  It hands the
+//     strip's last row to the strip below (shared memory inside the CTA,
+//     tagged global slots across CTAs).
+//   P (producer warp): stages 32-column chunks of the prepared plane with
+//     coalesced cp.async into a 4-slot ring, splits R0 (encoder), and writes
+//     finished chunks back out coalesced (recon / err, float64 output,
+//     symbols).
+// A CTA holds NPAIR consecutive strips of one component; CTAs take tickets
+// in (strip group, component) order, so a CTA only ever waits on an
+// earlier, resident one.
 #pragma once
 
 #include <type_traits>
@@ -78,38 +84,6 @@ struct PrepParams {
   Ladder lad;
 };
 
-// warps (32-row strips) per chain CTA.  The per-frame chain is latency
-// bound on its strip pipeline; one warp per CTA spreads the strips over all
-// SMs (handoffs then go through the tagged global slots).
-__host__ __device__ constexpr int chain_cw(bool enc) { return enc ? 1 : 1; }
-constexpr int CNS = 3;   // chunk slots per warp: sweep uses m-1, m; m+1
-                         // in flight; write-out reuses m-1 before m+2 lands
-template <int CW>
-struct ChainEncExtra {
-  uint32_t sym[CW][CNS][32][32];      // symbol pair, ring layout
-  uint32_t nl[CW][CNS][32];
-  uint32_t symw[CW][CNS][32];
-  uint32_t code[CW][CNS][32][8];      // [warp][slot][row][word] 4 codes/word
-};
-// decoder: never touched (the encoder branches are compiled but not run)
-struct ChainNoExtra {
-  uint32_t sym[1][1][1][1];
-  uint32_t nl[1][1][1];
-  uint32_t symw[1][1][1];
-  uint32_t code[1][1][1][1];
-};
-
-template <int CW, bool ENC>
-struct ChainSmem {
-  int32_t ring[CW][CNS][2][32][32];   // [warp][slot][comp][row][col ^ row]
-  uint32_t pin[CW][CNS][2][32];       // [warp][slot][comp][row]
-  int32_t bnd[CW][4][2][32];          // [warp][chunk & 3][comp][col]: row 31
-  int bdone[CW];                      // blocks whose row 31 is in bnd
-  int bread[CW];                      // chunks of bnd[w-1] warp w consumed
-  int task;
-  typename std::conditional<ENC, ChainEncExtra<CW>, ChainNoExtra>::type x;
-};
-
 // exact rha(x / 2e) for integer x, e > 0, |x| < 2^31
 __device__ __forceinline__ int32_t quant32(int32_t x, int32_t e, double inv2e) {
   const int32_t two_e = 2 * e;
@@ -122,354 +96,395 @@ __device__ __forceinline__ int32_t quant32(int32_t x, int32_t e, double inv2e) {
   return q;
 }
 
-// Encoder step in error form.  rho, q0: R0 = q0*2e + rho, rho in [-e, e];
-// d = errU + errL - errUL.  With y = rho - d, x = q0*2e + y and
+// Exact encoder step in error form.  rho, q0: R0 = q0*2e + rho; d = errU +
+// errL - errUL.  With y = rho - d, x = q0*2e + y and
 //   q = rha(x / 2e) = q0 + g,  g = floor((y+e)/2e)  (x >= 0)
 //                              g = ceil((y-e)/2e)   (x <  0),
-// err = g*2e - y (0 on escape).  Fast path: |y| < 4e (the neighbours share
-// this pixel's step), g from four comparisons; otherwise the exact divisions.
+// err = g*2e - y (0 on escape).  The chain uses a comparison form of this
+// while |y| < 4e (the neighbours share this pixel's step) and this one
+// otherwise.
 __device__ __forceinline__ int32_t floordiv_p(int32_t a, int32_t d) {  // d > 0
   int32_t q = a / d;
   if ((a % d != 0) && (a < 0)) q--;
   return q;
 }
-__device__ __forceinline__ bool enc_in_fast_range(int32_t rho, int32_t e,
-                                                  int32_t d) {
-  const int32_t y = rho - d;
-  return y < 4 * e && y > -4 * e;
-}
-template <bool FAST>
-__device__ __forceinline__ int32_t enc_step(int32_t rho, int32_t q0,
-                                            int32_t e, int32_t d,
-                                            int32_t radius, uint32_t* sym) {
+__device__ __forceinline__ int32_t enc_step_exact(int32_t rho, int32_t q0,
+                                                  int32_t e, int32_t d,
+                                                  int32_t radius, uint32_t* sym) {
   const int32_t y = rho - d;
   const bool xneg = (int64_t)q0 * (2 * (int64_t)e) + y < 0;
-  int32_t g;
-  if (FAST) {
-    const int32_t e3 = 3 * e;
-    g = (y >= e) + (y >= e3) - (y < -e) - (y < -e3);
-    const bool tie = (y == e) | (y == -e) | (y == e3) | (y == -e3);
-    g -= (tie && xneg) ? 1 : 0;
-  } else {
-    g = xneg ? -floordiv_p(e - y, 2 * e) : floordiv_p(y + e, 2 * e);
-  }
+  const int32_t g = xneg ? -floordiv_p(e - y, 2 * e) : floordiv_p(y + e, 2 * e);
   const int64_t q = (int64_t)q0 + g;
   const bool esc = q <= -radius || q >= radius;
   *sym = esc ? 0u : (uint32_t)(q + radius);
   return esc ? 0 : g * 2 * e - y;
 }
 
-template <bool ENC, int CW>
-__global__ void __launch_bounds__(32 * CW, 1)
+// strips (warp pairs) per CTA; tasks per frame
+__host__ __device__ constexpr int chain_pairs(bool enc) { return 2; }
+__host__ __device__ inline int chain_ntask(bool enc, int H) {
+  return 2 * ((H + 32 * chain_pairs(enc) - 1) / (32 * chain_pairs(enc)));
+}
+constexpr int CNS = 4;   // chunk slots: the sweep of block m uses chunks m-1
+                         // and m; P stages m+1, m+2 meanwhile
+
+template <bool ENC>
+struct PairRing {
+  int32_t v[CNS][32][32];   // [slot][row][col ^ row]: A -> recon; rho0 -> err
+  uint32_t pin[CNS][32];
+  int32_t q0[ENC ? CNS : 1][32][32];   // encoder: Q0, then the symbol
+  int32_t e[ENC ? CNS : 1][32][32];    // encoder: e per pixel
+  uint32_t code[ENC ? CNS : 1][32][8]; // encoder: codes, 4 per word
+  uint32_t nl[ENC ? CNS : 1][32];
+  uint32_t symw[ENC ? CNS : 1][32];
+};
+
+template <bool ENC>
+struct ChainSmem {
+  PairRing<ENC> r[chain_pairs(ENC)];
+  int32_t bnd[chain_pairs(ENC)][4][32];   // row 31 of strip p, [chunk & 3]
+  int32_t etab[32];
+  double inv2e[32];
+  int bdone[chain_pairs(ENC)];   // blocks of C_p whose row 31 is in bnd
+  int bread[chain_pairs(ENC)];   // chunks of bnd[p-1] C_p has consumed
+  int full[chain_pairs(ENC)];    // chunks P_p has staged (and split)
+  int done[chain_pairs(ENC)];    // blocks C_p has swept
+  int task;
+};
+
+__device__ __forceinline__ void spin_ge(const int* p, int need) {
+  while (!__all_sync(0xffffffffu, ld_volatile(p) >= need)) __nanosleep(20);
+  __threadfence_block();
+}
+__device__ __forceinline__ void signal_set(int* p, int v, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    *(volatile int*)p = v;
+  }
+  __syncwarp();
+}
+
+template <bool ENC>
+__global__ void __launch_bounds__(64 * chain_pairs(ENC))
 chain_kernel(ChainIO io) {
+  constexpr int NPAIR = chain_pairs(ENC);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ChainSmem<CW, ENC>& sm = *reinterpret_cast<ChainSmem<CW, ENC>*>(smem_raw);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  ChainSmem<ENC>& sm = *reinterpret_cast<ChainSmem<ENC>*>(smem_raw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pr = wid >> 1;
+  const bool producer = (wid & 1) == 0;
+  PairRing<ENC>& R = sm.r[pr];
   const unsigned FULL = 0xffffffffu;
   const int H = io.H, W = io.W, Wp = io.Wp, nchunks = io.nchunks;
   const int nblocks = (W + 31 + 31) / 32;
-  const int ntask = (H + 32 * CW - 1) / (32 * CW);
+  const int ntask = chain_ntask(ENC, H);
+  if (threadIdx.x < 32) {
+    sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
+    sm.inv2e[threadIdx.x] = io.inv2e_tab[threadIdx.x];
+  }
 
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
-    if (threadIdx.x < CW) { sm.bdone[threadIdx.x] = 0; sm.bread[threadIdx.x] = 0; }
+    if (threadIdx.x < NPAIR) {
+      sm.bdone[threadIdx.x] = 0; sm.bread[threadIdx.x] = 0;
+      sm.full[threadIdx.x] = 0; sm.done[threadIdx.x] = 0;
+    }
     __syncthreads();
-    const int g = sm.task;
-    if (g >= ntask) break;
-    const int i0 = 32 * (CW * g + w);
+    const int task = sm.task;
+    if (task >= ntask) break;
+    const int g = task >> 1, comp = task & 1;
+    const int i0 = 32 * (NPAIR * g + pr);
     const bool wact = i0 < H;
     const int nrows = wact ? min(32, H - i0) : 0;
     const int my_i = i0 + lane;
     const bool rowok = my_i < H;
-    const bool has_next = i0 + 32 < H;
-    const bool next_in_cta = w + 1 < CW;
-    const uint32_t tag = io.tag_base + (uint32_t)g + 1u;
-    uint64_t* my_gb = io.bnd + (int64_t)g * 2 * W;
-    const uint64_t* up_gb = io.bnd + (int64_t)(g - 1) * 2 * W;
+    PhaseClock pc(io.stats);
 
-    // coalesced staging of chunk m (lane = column; one row per iteration)
-    auto stage = [&](int m) {
-      const int s = m % CNS;
-#pragma unroll 4
-      for (int r = 0; r < 32; r++) {
-        const bool rv = r < nrows;
-        const int64_t rb = (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * m + lane;
-        cp_async<4>(&sm.ring[w][s][0][r][lane ^ r], io.a0 + rb, rv);
-        cp_async<4>(&sm.ring[w][s][1][r][lane ^ r], io.a1 + rb, rv);
-      }
-      const int64_t pb = (int64_t)(rowok ? my_i : i0) * nchunks + m;
-      cp_async<4>(&sm.pin[w][s][0][lane], io.pin_u + pb, rowok);
-      cp_async<4>(&sm.pin[w][s][1][lane], io.pin_v + pb, rowok);
-      if (ENC) {
-        cp_async<4>(&sm.x.nl[w][s][lane], io.nl + pb, rowok);
-        cp_async<4>(&sm.x.symw[w][s][lane], io.symw + pb, rowok);
-        // codes: 32 bytes per row, lanes (row r = lane >> 3 + 4 k, word lane & 7)
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const int r = (lane >> 3) + 4 * k, q = lane & 7;
+    if (producer && wact) {
+      // ===================================================== producer
+      const int32_t* a = comp ? io.a1 : io.a0;
+      const uint32_t* pinp = comp ? io.pin_v : io.pin_u;
+      int32_t* out_i = comp ? io.out_i1 : io.out_i0;
+      double* out_f = comp ? io.out_f1 : io.out_f0;
+      auto stage = [&](int x) {
+        const int s = x % CNS;
+        const int c = 32 * x + lane;
+#pragma unroll 8
+        for (int r = 0; r < 32; r++) {
           const bool rv = r < nrows;
-          cp_async<4>(&sm.x.code[w][s][r][q],
-                      io.codes + (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * m + 4 * q,
-                      rv);
+          cp_async<4>(&R.v[s][r][lane ^ r],
+                      a + (int64_t)(i0 + (rv ? r : 0)) * Wp + c, rv);
         }
-      }
-    };
-    // coalesced write-out of chunk x (complete) from its slot; escapes of
-    // row r are added to esc_row of lane r
-    int32_t esc_row = 0;
-    auto write_out = [&](int x) {
-      const int s = x % CNS;
-      const int c = 32 * x + lane;
-      const bool cv = c < W;
-      uint32_t nl_r = 0, sw_r = 0;
-      int32_t pre_r = 0;
-      int64_t qrow_r = 0;
-      if (ENC && rowok) {
-        nl_r = sm.x.nl[w][s][lane];
-        sw_r = sm.x.symw[w][s][lane];
-        pre_r = io.chunk_nl[(int64_t)my_i * nchunks + x];
-        qrow_r = io.qd_row_off[my_i];
-      }
-#pragma unroll 4
-      for (int r = 0; r < 32; r++) {
-        if (r >= nrows) break;
-        const int32_t vu = sm.ring[w][s][0][r][lane ^ r];
-        const int32_t vv = sm.ring[w][s][1][r][lane ^ r];
-        if (cv) {
-          const int64_t nr = (int64_t)(i0 + r) * Wp + c;
-          io.out_i0[nr] = vu;
-          io.out_i1[nr] = vv;
-          if (!ENC) {
-            const int64_t n = (int64_t)(i0 + r) * W + c;
-            io.out_f0[n] = __dmul_rn((double)vu, io.inv_S);
-            io.out_f1[n] = __dmul_rn((double)vv, io.inv_S);
-          }
-        }
+        const int64_t pb = (int64_t)(rowok ? my_i : i0) * nchunks + x;
+        cp_async<4>(&R.pin[s][lane], pinp + pb, rowok);
         if (ENC) {
-          const uint32_t nlw = __shfl_sync(FULL, nl_r, r);
-          const uint32_t sww = __shfl_sync(FULL, sw_r, r);
-          const int32_t pre = __shfl_sync(FULL, pre_r, r);
-          const int64_t qrow = __shfl_sync(FULL, qrow_r, r);
-          const uint32_t bit = 1u << lane;
-          int ne = 0;
-          if (cv && (sww & bit)) {
-            const uint32_t sy = sm.x.sym[w][s][r][lane ^ r];
-            const int64_t pos = qrow + 2 * ((int64_t)pre + __popc(nlw & (bit - 1u)));
-            *reinterpret_cast<uint32_t*>(io.qd + pos) = sy;
-            ne = ((sy & 0xffffu) == 0) + ((sy >> 16) == 0);
+          cp_async<4>(&R.nl[s][lane], io.nl + pb, rowok);
+          cp_async<4>(&R.symw[s][lane], io.symw + pb, rowok);
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            const int r = (lane >> 3) + 4 * k, q = lane & 7;
+            const bool rv = r < nrows;
+            cp_async<4>(&R.code[s][r][q],
+                        io.codes + (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * x + 4 * q,
+                        rv);
           }
-          const int tot = __reduce_add_sync(FULL, ne);
-          if (lane == r) esc_row += tot;
         }
-      }
-    };
-
-    int32_t l_u = 0, l_v = 0, ul_u = 0, ul_v = 0, last_u = 0, last_v = 0;
-    // one cp.async group per chunk (empty groups keep the count aligned):
-    // at block m the newest group is chunk m+1, which may stay in flight
-    if (wact) {
+      };
+      // encoder: e per pixel and R0 = Q0*2e + rho0 (lane = column)
+      auto split = [&](int x) {
+        if (!ENC) return;
+        const int s = x % CNS;
+        const uint32_t bit = 1u << lane;
+        const unsigned char* cb = reinterpret_cast<const unsigned char*>(&R.code[s][0][0]);
+#pragma unroll 4
+        for (int r = 0; r < 32; r++) {
+          if (r >= nrows) break;
+          const int cd = cb[32 * r + lane] & 31;
+          const int32_t e = sm.etab[cd];
+          const bool pin = (R.pin[s][r] & bit) != 0;
+          const int32_t av = R.v[s][r][lane ^ r];
+          const int32_t q = (!pin && e != 0) ? quant32(av, e, sm.inv2e[cd]) : 0;
+          R.v[s][r][lane ^ r] = av - q * 2 * e;
+          R.q0[s][r][lane ^ r] = q;
+          R.e[s][r][lane ^ r] = e;
+        }
+      };
+      int32_t esc_row = 0;   // lane r: escapes of row r in this component
+      auto write_out = [&](int x) {
+        const int s = x % CNS;
+        const int c = 32 * x + lane;
+        const bool cv = c < W;
+        int64_t base_r = 0;
+        if (ENC && rowok)
+          base_r = io.qd_row_off[my_i] + comp +
+                   2 * (int64_t)io.chunk_nl[(int64_t)my_i * nchunks + x];
+#pragma unroll 4
+        for (int r = 0; r < 32; r++) {
+          if (r >= nrows) break;
+          const int32_t val = R.v[s][r][lane ^ r];
+          if (cv) {
+            out_i[(int64_t)(i0 + r) * Wp + c] = val;
+            if (!ENC)
+              out_f[(int64_t)(i0 + r) * W + c] = __dmul_rn((double)val, io.inv_S);
+          }
+          if (ENC) {
+            const int64_t base = __shfl_sync(FULL, base_r, r);
+            const uint32_t nlw = R.nl[s][r], sww = R.symw[s][r];
+            const uint32_t bit = 1u << lane;
+            int ne = 0;
+            if (cv && (sww & bit)) {
+              const uint32_t sy = (uint32_t)R.q0[s][r][lane ^ r];
+              io.qd[base + 2 * __popc(nlw & (bit - 1u))] = (uint16_t)sy;
+              ne = sy == 0;
+            }
+            const int tot = __reduce_add_sync(FULL, ne);
+            if (lane == r) esc_row += tot;
+          }
+        }
+      };
+      // chunk x lives in slot x % CNS from its staging to its write-out;
+      // it is complete once C has swept blocks x and x+1 (done >= x+2)
+      int next_out = 0;
+      auto retire_before = [&](int x) {   // free the slot chunk x needs
+        while (next_out <= x - CNS) {
+          spin_ge(&sm.done[pr], min(next_out + 2, nblocks));
+          pc.lap(WP_X1, lane);
+          write_out(next_out);
+          next_out++;
+          pc.lap(WP_WRITE, lane);
+        }
+      };
       stage(0);
       cp_async_commit();
-      if (nchunks > 1) stage(1);
-      cp_async_commit();
-    }
-    PhaseClock pc(io.stats);
-    for (int m = 0; m < nblocks && wact; m++) {
-      const int c0 = 32 * m;
-      cp_async_wait_group<1>();   // chunks <= m have landed
-      __syncwarp();
-      pc.lap(WP_WAITPREV, lane);
-      // ---- boundary row (row i0-1) for columns c0..c0+31
-      int32_t bu = 0, bv = 0;
-      if (i0 > 0 && c0 < W) {
-        if (w > 0) {
-          const int need = min(m + 2, nblocks);
-          while (!__all_sync(FULL, ld_volatile(&sm.bdone[w - 1]) >= need))
-            __nanosleep(20);
-          __threadfence_block();
-          bu = sm.bnd[w - 1][m & 3][0][lane];
-          bv = sm.bnd[w - 1][m & 3][1][lane];
-          __syncwarp();
-          if (lane == 0) *(volatile int*)&sm.bread[w] = m + 1;
-        } else {
-          const int c = c0 + lane;
-          const bool v = c < W;
-          const int cc = v ? c : 0;
-          bu = TaggedSlot<int32_t>::get(up_gb + cc, tag - 1, v);
-          bv = TaggedSlot<int32_t>::get(up_gb + W + cc, tag - 1, v);
+      for (int x = 1; x <= nchunks; x++) {
+        if (x < nchunks) {
+          retire_before(x);
+          stage(x);
         }
-      }
-      // ---- this lane's 32 columns c = c0 - lane + jj (two chunks)
-      pc.lap(WP_WAITBND, lane);
-      const int cbase = c0 - lane;
-      const int x_lo = cbase >> 5;   // -1 for the first block's lanes > 0
-      const int s_lo = (x_lo + CNS) % CNS, s_hi = (x_lo + 1) % CNS;
-      const uint32_t split = 32 - (cbase & 31);
-      uint32_t pu_lo = 0, pv_lo = 0, pu_hi = 0, pv_hi = 0;
-      if (rowok) {
-        pu_lo = sm.pin[w][s_lo][0][lane]; pv_lo = sm.pin[w][s_lo][1][lane];
-        pu_hi = sm.pin[w][s_hi][0][lane]; pv_hi = sm.pin[w][s_hi][1][lane];
-      }
-      const bool top = i0 > 0;
-      if (!ENC) {
-        int32_t av_u[32], av_v[32];
-#pragma unroll
-        for (int jj = 0; jj < 32; jj++) {
-          const int c = cbase + jj;
-          const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-          const int col = c & 31;
-          av_u[jj] = sm.ring[w][sl][0][lane][col ^ lane];
-          av_v[jj] = sm.ring[w][sl][1][lane][col ^ lane];
-        }
+        cp_async_commit();
+        cp_async_wait_group<1>();   // chunk x-1 has landed
         __syncwarp();
-#pragma unroll
-        for (int jj = 0; jj < 32; jj++) {
-          const int c = cbase + jj;
-          const int32_t b_u = __shfl_sync(FULL, bu, jj);
-          const int32_t b_v = __shfl_sync(FULL, bv, jj);
-          const int32_t up_u = __shfl_up_sync(FULL, last_u, 1);
-          const int32_t up_v = __shfl_up_sync(FULL, last_v, 1);
-          const bool inb = c < W;
-          const int32_t nu_u = lane == 0 ? ((top && inb) ? b_u : 0) : up_u;
-          const int32_t nu_v = lane == 0 ? ((top && inb) ? b_v : 0) : up_v;
-          const bool act = rowok && c >= 0 && inb;
-          const bool lo = (uint32_t)jj < split;
-          const uint32_t bit = 1u << (c & 31);
-          const bool pu_ = ((lo ? pu_lo : pu_hi) & bit) != 0;
-          const bool pv_ = ((lo ? pv_lo : pv_hi) & bit) != 0;
-          const bool first = c == 0;
-          const int32_t l0_u = first ? 0 : l_u, l0_v = first ? 0 : l_v;
-          const int32_t ul0_u = first ? 0 : ul_u, ul0_v = first ? 0 : ul_v;
-          const int32_t r_u = pu_ ? av_u[jj]
-              : (int32_t)((uint32_t)nu_u + ((uint32_t)l0_u +
-                                            ((uint32_t)av_u[jj] - (uint32_t)ul0_u)));
-          const int32_t r_v = pv_ ? av_v[jj]
-              : (int32_t)((uint32_t)nu_v + ((uint32_t)l0_v +
-                                            ((uint32_t)av_v[jj] - (uint32_t)ul0_v)));
-          av_u[jj] = act ? r_u : av_u[jj];
-          av_v[jj] = act ? r_v : av_v[jj];
-          l_u = act ? r_u : l_u;
-          l_v = act ? r_v : l_v;
-          last_u = l_u;
-          last_v = l_v;
-          ul_u = nu_u;
-          ul_v = nu_v;
+        split(x - 1);
+        signal_set(&sm.full[pr], x, lane);
+        pc.lap(WP_PRE, lane);
+      }
+      retire_before(nchunks + CNS - 1);
+      if (ENC && rowok && esc_row) atomicAdd(io.row_esc + my_i, esc_row);
+    } else if (wact) {
+      // ===================================================== chain warp
+      const bool has_next = i0 + 32 < H;
+      const bool next_in_cta = pr + 1 < NPAIR;
+      const uint32_t tag = io.tag_base + (uint32_t)task + 1u;
+      uint64_t* my_gb = io.bnd + (int64_t)task * W;
+      const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
+      const bool top = i0 > 0;
+      int32_t l = 0, ul = 0;
+      for (int m = 0; m < nblocks; m++) {
+        const int c0 = 32 * m;
+        spin_ge(&sm.full[pr], min(m + 1, nchunks));
+        pc.lap(WP_WAITPREV, lane);
+        // ---- boundary row (row i0-1) for columns c0..c0+31
+        int32_t b = 0;
+        if (top && c0 < W) {
+          if (pr > 0) {
+            spin_ge(&sm.bdone[pr - 1], min(m + 2, nblocks));
+            b = c0 + lane < W ? sm.bnd[pr - 1][m & 3][lane] : 0;
+            signal_set(&sm.bread[pr], m + 1, lane);
+          } else {
+            const int c = c0 + lane;
+            const bool v = c < W;
+            b = TaggedSlot<int32_t>::get(up_gb + (v ? c : 0), tag - 2, v);
+          }
         }
-        if (rowok) {
+        pc.lap(WP_WAITBND, lane);
+        // ---- this lane's 32 columns c = c0 - lane + jj (two chunks).
+        // vm: bit jj = pixel (my_i, cbase+jj) exists; pm: pinned or not
+        // existing (those take their prepared value, 0 left of column 0, so
+        // the left / up-left state entering column 0 is 0 with no test).
+        const int cbase = c0 - lane;
+        const int x_lo = cbase >> 5;   // -1 for the first block's lanes > 0
+        const int s_lo = (x_lo + CNS) % CNS, s_hi = (x_lo + 1) % CNS;
+        const uint32_t split = 32 - (cbase & 31);
+        const int jlo = max(0, -cbase), jhi = min(32, W - cbase);
+        const uint32_t vm =
+            (rowok && jhi > jlo)
+                ? ((jhi >= 32 ? 0xffffffffu : ((1u << jhi) - 1u)) & ~((1u << jlo) - 1u))
+                : 0u;
+        const uint32_t pm =
+            __funnelshift_r(R.pin[s_lo][lane], R.pin[s_hi][lane], cbase & 31) | ~vm;
+        const bool lane0 = lane == 0;
+        if (!ENC) {
+          int32_t av[32];
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
             const int c = cbase + jj;
-            if (c >= 0 && c < W) {
+            const int sl = (uint32_t)jj < split ? s_lo : s_hi;
+            const int32_t x = R.v[sl][lane][(c & 31) ^ lane];
+            av[jj] = c < 0 ? 0 : x;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 32; jj++) {
+            const int32_t bb = __shfl_sync(FULL, b, jj);
+            const int32_t up = __shfl_up_sync(FULL, l, 1);
+            const int32_t nu = lane0 ? bb : up;
+            const int32_t t = (int32_t)((uint32_t)av[jj] - (uint32_t)ul);
+            const int32_t r = ((pm >> jj) & 1u) ? av[jj]
+                : (int32_t)((uint32_t)nu + (uint32_t)l + (uint32_t)t);
+            av[jj] = r;
+            l = r;
+            ul = nu;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 32; jj++) {
+            const int c = cbase + jj;
+            const int sl = (uint32_t)jj < split ? s_lo : s_hi;
+            if ((vm >> jj) & 1u) R.v[sl][lane][(c & 31) ^ lane] = av[jj];
+          }
+        } else {
+          const int32_t radius = io.radius;
+          const int32_t l_s = l, ul_s = ul;
+          // operands into registers first: the sweep's stores would
+          // otherwise keep later loads from being hoisted past them.
+          // ee = 0 where pinned / absent (no slow-path trigger there).
+          int32_t rr[32], qq[32], ee[32];
+#pragma unroll
+          for (int jj = 0; jj < 32; jj++) {
+            const int c = cbase + jj;
+            const int sl = (uint32_t)jj < split ? s_lo : s_hi;
+            const int col = (c & 31) ^ lane;
+            const int32_t x = R.v[sl][lane][col];
+            rr[jj] = c < 0 ? 0 : x;
+            qq[jj] = R.q0[sl][lane][col];
+            const int32_t e = R.e[sl][lane][col];
+            ee[jj] = ((pm >> jj) & 1u) ? 0 : e;
+          }
+          bool slow = false;
+#pragma unroll
+          for (int jj = 0; jj < 32; jj++) {
+            const int32_t rho = rr[jj], q0 = qq[jj], e = ee[jj];
+            const int32_t bb = __shfl_sync(FULL, b, jj);
+            const int32_t up = __shfl_up_sync(FULL, l, 1);
+            const int32_t nu = lane0 ? bb : up;
+            const int32_t d = nu + l - ul;
+            // q = rha(x / 2e), x = q0*2e + y, valid while |y| < 4e: count
+            // the thresholds +-e, +-3e passed (ties upward), then a tie
+            // rounds away from zero
+            const int32_t y = rho - d;
+            const int32_t e3 = 3 * e;
+            const int32_t gf = (y >= e) + (y >= e3) - (y < -e) - (y < -e3);
+            const int32_t ay = y < 0 ? -y : y;
+            const bool tie = (ay == e) | (ay == e3);
+            const int32_t qf = q0 + gf;
+            const int32_t q = qf - ((tie && qf <= 0) ? 1 : 0);
+            const bool esc = (uint32_t)(q + radius - 1) >= (uint32_t)(2 * radius - 1);
+            const bool pin = (pm >> jj) & 1u;
+            const int32_t r = pin ? rho : (esc ? 0 : (q - q0) * 2 * e - y);
+            qq[jj] = (pin || esc) ? 0 : q + radius;
+            slow |= (e != 0) & (ay >= 4 * e);
+            rr[jj] = r;
+            l = r;
+            ul = nu;
+          }
+          if (__any_sync(FULL, slow)) {
+            // mixed steps: redo the block with the exact step
+            l = l_s; ul = ul_s;
+#pragma unroll 1
+            for (int jj = 0; jj < 32; jj++) {
+              const int c = cbase + jj;
               const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-              sm.ring[w][sl][0][lane][(c & 31) ^ lane] = av_u[jj];
-              sm.ring[w][sl][1][lane][(c & 31) ^ lane] = av_v[jj];
+              const int col = (c & 31) ^ lane;
+              const bool valid = (vm >> jj) & 1u, pin = (pm >> jj) & 1u;
+              const int32_t rho = c < 0 ? 0 : R.v[sl][lane][col];
+              const int32_t q0 = R.q0[sl][lane][col];
+              const int32_t e = pin ? 0 : R.e[sl][lane][col];
+              const int32_t bb = __shfl_sync(FULL, b, jj);
+              const int32_t up = __shfl_up_sync(FULL, l, 1);
+              const int32_t nu = lane0 ? bb : up;
+              const int32_t d = nu + l - ul;
+              uint32_t sy = 0;
+              const int32_t er = e != 0 ? enc_step_exact(rho, q0, e, d, radius, &sy) : 0;
+              const int32_t r = pin ? rho : er;
+              if (valid) {
+                R.v[sl][lane][col] = r;
+                R.q0[sl][lane][col] = pin ? 0 : (int32_t)sy;
+              }
+              l = r;
+              ul = nu;
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; jj++) {
+              const int c = cbase + jj;
+              const int sl = (uint32_t)jj < split ? s_lo : s_hi;
+              const int col = (c & 31) ^ lane;
+              if ((vm >> jj) & 1u) {
+                R.v[sl][lane][col] = rr[jj];
+                R.q0[sl][lane][col] = qq[jj];
+              }
             }
           }
         }
-      } else {
-        // encoder: per-step shared-memory operands (register budget); the
-        // loads and the R0 split are independent of the chain and are
-        // scheduled ahead by the unrolled loop
         __syncwarp();
-#pragma unroll
-        for (int jj = 0; jj < 32; jj++) {
-          const int c = cbase + jj;
-          const bool lo = (uint32_t)jj < split;
-          const int sl = lo ? s_lo : s_hi;
-          const int col = c & 31;
-          const int32_t a_u = sm.ring[w][sl][0][lane][col ^ lane];
-          const int32_t a_v = sm.ring[w][sl][1][lane][col ^ lane];
-          const int cd = (sm.x.code[w][sl][lane][col >> 2] >> (8 * (col & 3))) & 31;
-          const int32_t e = io.e_tab[cd];
-          const double inv = io.inv2e_tab[cd];
-          const uint32_t bit = 1u << col;
-          const bool pu_ = ((lo ? pu_lo : pu_hi) & bit) != 0;
-          const bool pv_ = ((lo ? pv_lo : pv_hi) & bit) != 0;
-          const bool live = e != 0;
-          const int32_t q0u = (!pu_ && live) ? quant32(a_u, e, inv) : 0;
-          const int32_t q0v = (!pv_ && live) ? quant32(a_v, e, inv) : 0;
-          const int32_t rho_u = a_u - q0u * 2 * e, rho_v = a_v - q0v * 2 * e;
-          const int32_t b_u = __shfl_sync(FULL, bu, jj);
-          const int32_t b_v = __shfl_sync(FULL, bv, jj);
-          const int32_t up_u = __shfl_up_sync(FULL, last_u, 1);
-          const int32_t up_v = __shfl_up_sync(FULL, last_v, 1);
-          const bool inb = c < W;
-          const int32_t nu_u = lane == 0 ? ((top && inb) ? b_u : 0) : up_u;
-          const int32_t nu_v = lane == 0 ? ((top && inb) ? b_v : 0) : up_v;
-          const bool act = rowok && c >= 0 && inb;
-          const bool first = c == 0;
-          const int32_t l0_u = first ? 0 : l_u, l0_v = first ? 0 : l_v;
-          const int32_t ul0_u = first ? 0 : ul_u, ul0_v = first ? 0 : ul_v;
-          uint32_t su, sv;
-          const int32_t d_u = nu_u + l0_u - ul0_u, d_v = nu_v + l0_v - ul0_v;
-          int32_t eu_ = enc_step<true>(rho_u, q0u, e, d_u, io.radius, &su);
-          int32_t ev_ = enc_step<true>(rho_v, q0v, e, d_v, io.radius, &sv);
-          const bool slow = live && !(enc_in_fast_range(rho_u, e, d_u) &&
-                                      enc_in_fast_range(rho_v, e, d_v));
-          if (__any_sync(FULL, slow)) {   // warp-uniform branch, rare
-            uint32_t su2, sv2;
-            const int32_t e1 = live ? e : 1;
-            const int32_t eu2 = enc_step<false>(rho_u, q0u, e1, d_u, io.radius, &su2);
-            const int32_t ev2 = enc_step<false>(rho_v, q0v, e1, d_v, io.radius, &sv2);
-            if (slow) { eu_ = eu2; ev_ = ev2; su = su2; sv = sv2; }
+        pc.lap(WP_CHAIN, lane);
+        // ---- row 31 of this strip for the strip below (from the ring)
+        if (has_next) {
+          const int c = c0 - 31 + lane;   // the columns row 31 did now
+          const bool cv = c >= 0 && c < W;
+          const int sl = cv ? (c >> 5) % CNS : 0;
+          const int32_t val = cv ? R.v[sl][31][(c & 31) ^ 31] : 0;
+          if (next_in_cta) {
+            spin_ge(&sm.bread[pr + 1], m - 3);   // slot (m+1)&3 reused
+            if (cv) sm.bnd[pr][(c >> 5) & 3][c & 31] = val;
+            signal_set(&sm.bdone[pr], m + 1, lane);
+          } else if (cv) {
+            TaggedSlot<int32_t>::put(my_gb + c, tag, val);
           }
-          const int32_t r_u = pu_ ? a_u : eu_;
-          const int32_t r_v = pv_ ? a_v : ev_;
-          if (act) {
-            sm.ring[w][sl][0][lane][col ^ lane] = r_u;
-            sm.ring[w][sl][1][lane][col ^ lane] = r_v;
-            sm.x.sym[w][sl][lane][col ^ lane] =
-                ((pu_ ? 0u : su) & 0xffffu) | ((pv_ ? 0u : sv) << 16);
-          }
-          l_u = act ? r_u : l_u;
-          l_v = act ? r_v : l_v;
-          last_u = l_u;
-          last_v = l_v;
-          ul_u = nu_u;
-          ul_v = nu_v;
         }
+        signal_set(&sm.done[pr], m + 1, lane);
+        pc.lap(WP_X3, lane);
       }
-      __syncwarp();
-      pc.lap(WP_CHAIN, lane);
-      // ---- row 31 of this strip for the strip below (from the ring)
-      if (has_next) {
-        const int c = c0 - 31 + lane;        // the columns row 31 did now
-        const bool cv = c >= 0 && c < W;
-        const int sl = cv ? (c >> 5) % CNS : 0;
-        const int32_t vu = cv ? sm.ring[w][sl][0][31][(c & 31) ^ 31] : 0;
-        const int32_t vv = cv ? sm.ring[w][sl][1][31][(c & 31) ^ 31] : 0;
-        if (next_in_cta) {
-          // the consumer must be done with chunk m-3 (same slot as m+1)
-          const int need = m - 3;
-          while (!__all_sync(FULL, ld_volatile(&sm.bread[w + 1]) >= need))
-            __nanosleep(20);
-          if (cv) {
-            sm.bnd[w][(c >> 5) & 3][0][c & 31] = vu;
-            sm.bnd[w][(c >> 5) & 3][1][c & 31] = vv;
-          }
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence_block();
-            *(volatile int*)&sm.bdone[w] = m + 1;
-          }
-          __syncwarp();
-        } else if (cv) {
-          TaggedSlot<int32_t>::put(my_gb + c, tag, vu);
-          TaggedSlot<int32_t>::put(my_gb + W + c, tag, vv);
-        }
-      }
-      // ---- chunk m-1 is complete: write it out, then reuse its slot for
-      //      chunk m+2
-      pc.lap(WP_X3, lane);
-      if (m >= 1) write_out(m - 1);
-      if (m == nblocks - 1 && 32 * m < W) write_out(m);
-      __syncwarp();
-      pc.lap(WP_WRITE, lane);
-      if (m + 2 < nchunks) stage(m + 2);
-      cp_async_commit();
-      pc.lap(WP_PRE, lane);
     }
-    if (ENC && rowok && esc_row) io.row_esc[my_i] += esc_row;
     cp_async_wait_all();
     __syncthreads();
   }

@@ -606,15 +606,18 @@ cudaError_t launch_widen_frame(const int32_t* ru, const int32_t* rv, int H,
 
 template <bool ENC>
 cudaError_t launch_chain(const ChainIO& io, int nsm, cudaStream_t st) {
-  constexpr int CWn = chain_cw(ENC);
-  const size_t smem = sizeof(ChainSmem<CWn, ENC>);
+  const size_t smem = sizeof(ChainSmem<ENC>);
   cudaError_t e = cudaFuncSetAttribute(
-      chain_kernel<ENC, CWn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      chain_kernel<ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)smem);
   if (e != cudaSuccess) return e;
-  const int ntask = (io.H + 32 * CWn - 1) / (32 * CWn);
-  // up to 8 resident CTAs per SM (the smem of CW = 1 allows it)
-  chain_kernel<ENC, CWn><<<min(8 * nsm, ntask), 32 * CWn, smem, st>>>(io);
+  const int threads = 64 * chain_pairs(ENC);
+  int occ = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chain_kernel<ENC>,
+                                                    threads, smem);
+  if (e != cudaSuccess) return e;
+  const int ntask = chain_ntask(ENC, io.H);
+  chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), threads, smem, st>>>(io);
   return cudaGetLastError();
 }
 
