@@ -68,7 +68,7 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
-                  "decode_rows", "decode_ll", "decode", "aux")
+                  "decode_rows", "decode_ll", "decode", "aux", "prep")
 
 
 def prof_enable(on=True):

@@ -60,12 +60,20 @@ cudaError_t launch_chunk_prefix(const uint8_t*, const SYM*, const int64_t*,
                                 int64_t, int, int, int64_t, int32_t*,
                                 int32_t*, cudaStream_t);
 template <typename F>
-cudaError_t launch_enc_prep(const F*, const F*, const uint8_t*,
-                            const int32_t*, const int32_t*, const int64_t*,
-                            const int32_t*, const PrepParams&, const double*,
-                            uint8_t*, int32_t*, int32_t*, uint32_t*,
-                            uint32_t*, uint32_t*, uint32_t*, uint16_t*,
-                            int32_t*, int*, uint8_t*, cudaStream_t);
+cudaError_t launch_enc_r0(const F*, const F*, const uint8_t*, const int32_t*,
+                          const int32_t*, const PrepParams&, int32_t*,
+                          int32_t*, int32_t*, int32_t*, int32_t*, uint8_t*,
+                          int*, cudaStream_t);
+template <typename F>
+cudaError_t launch_enc_mop(const F*, const F*, const int32_t*, const int32_t*,
+                           const int32_t*, const PrepParams&, const double*,
+                           uint8_t*, cudaStream_t);
+template <typename F>
+cudaError_t launch_enc_pix(const F*, const F*, const uint8_t*, const int32_t*,
+                           const int64_t*, const int32_t*, const PrepParams&,
+                           const uint8_t*, int32_t*, int32_t*, uint32_t*,
+                           uint32_t*, uint32_t*, uint32_t*, uint16_t*,
+                           int32_t*, cudaStream_t);
 template <typename SYM>
 cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
                             const uint8_t*, const int32_t*, const int32_t*,
@@ -74,8 +82,13 @@ cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
                             int32_t*, uint32_t*, uint32_t*, cudaStream_t);
 template <bool ENC>
 cudaError_t launch_chain(const ChainIO&, int, cudaStream_t);
-cudaError_t launch_widen_frame(const int32_t*, const int32_t*, int, int, int,
-                               int64_t*, int64_t*, cudaStream_t);
+cudaError_t launch_emit_frame(const int32_t*, const int32_t*, int, int, int,
+                              double, double*, double*, int64_t*, int64_t*,
+                              cudaStream_t);
+cudaError_t launch_sym_scatter(const uint16_t*, const uint16_t*,
+                               const uint32_t*, const uint32_t*,
+                               const int64_t*, const int32_t*, int, int, int,
+                               int, uint16_t*, int32_t*, cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -100,7 +113,7 @@ int fail(int code, const std::string& msg) {
 // counts it and, when profiling is on, brackets it with CUDA events on the
 // launching stream (vfcp_prof_*).
 enum KClass { K_RANGE, K_ANALYZE, K_SCAN, K_MOP, K_ENCODE, K_LLW, K_DROWS,
-              K_DLL, K_DECODE, K_AUX, K_NCLS };
+              K_DLL, K_DECODE, K_AUX, K_PREP, K_NCLS };
 struct Prof {
   bool on = false;
   int64_t launches = 0;
@@ -396,7 +409,6 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
 void chain_tables(ChainIO& io, const Ladder& lad) {
   for (int k = 0; k < 32; k++) {
     io.e_tab[k] = (int32_t)lad.e[k];
-    io.inv2e_tab[k] = lad.inv2e[k];
   }
 }
 
@@ -429,8 +441,13 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   int *ticket, *ovf;
   double* log2tab = nullptr;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
+  int32_t *prevrec, *q0;
+  uint16_t* syms;
   CK(sc.get(&a, (size_t)2 * plane));
+  CK(sc.get(&q0, (size_t)2 * plane));
   CK(sc.get(&err, (size_t)4 * plane));
+  CK(sc.get(&prevrec, (size_t)2 * plane));
+  CK(sc.get(&syms, (size_t)2 * plane));
   CK(sc.get(&pins, (size_t)4 * cplane));
   CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
@@ -471,9 +488,10 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   io.a1 = a + plane;
   io.pin_u = pins;
   io.pin_v = pins + cplane;
-  io.nl = pins + 2 * cplane;
-  io.symw = pins + 3 * cplane;
-  io.qd = qd;
+  io.q0_0 = q0;
+  io.q0_1 = q0 + plane;
+  io.sym0 = syms;
+  io.sym1 = syms + plane;
   io.bnd = bnd;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
@@ -481,22 +499,30 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
     int32_t* ecur = err + 2 * plane * (t & 1);
-    LAUNCH(K_MOP, st,
-           launch_enc_prep<F>(u, v, codes, eprev, eprev + plane, qd_row_off,
-                              pre_nl, pp, log2tab,
-                              t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,
-                              a, a + plane, pins, pins + cplane,
-                              pins + 2 * cplane, pins + 3 * cplane, qd,
-                              row_ll, ovf, codes_p, st));
+    uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
+    LAUNCH(K_PREP, st,
+           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, a, a + plane,
+                            q0, q0 + plane, prevrec, codes_p, ovf, st));
+    if (pp.mop)
+      LAUNCH(K_MOP, st,
+             launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
+                               modes_t, st));
+    LAUNCH(K_PREP, st,
+           launch_enc_pix<F>(u, v, codes_p, prevrec, qd_row_off, pre_nl, pp,
+                             modes_t, a, a + plane, pins, pins + cplane,
+                             pins + 2 * cplane, pins + 3 * cplane, qd, row_ll,
+                             st));
     io.codes = codes_p;
     io.out_i0 = ecur;
     io.out_i1 = ecur + plane;
-    io.qd_row_off = qd_row_off + (size_t)t * H;
-    io.chunk_nl = pre_nl + (size_t)t * cplane;
-    io.row_esc = row_ll + (size_t)t * H;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
     LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
+    LAUNCH(K_LLW, st,
+           launch_sym_scatter(syms, syms + plane, pins + 2 * cplane,
+                              pins + 3 * cplane, qd_row_off + (size_t)t * H,
+                              pre_nl + (size_t)t * cplane, H, W, Wp, nchunks,
+                              qd, row_ll + (size_t)t * H, st));
   }
   if (wprof) {
     unsigned long long h[WP_N];
@@ -504,10 +530,11 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     CK(cudaStreamSynchronize(st));
     fprintf(stderr,
             "[chain %s] C: waitchunk=%.3g waitbnd=%.3g sweep=%.3g handoff=%.3g"
-            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)\n",
+            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)"
+            " redo-blocks=%llu preload=%.3g\n",
             "enc", (double)h[WP_WAITPREV], (double)h[WP_WAITBND],
             (double)h[WP_CHAIN], (double)h[WP_X3], (double)h[WP_X1],
-            (double)h[WP_WRITE], (double)h[WP_PRE]);
+            (double)h[WP_WRITE], (double)h[WP_PRE], h[WP_X2], (double)h[WP_TASKS]);
   }
   int h_ovf = 0;
   CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -563,7 +590,6 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   io.bnd = bnd;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
-  io.inv_S = 1.0 / p->scale;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
@@ -576,16 +602,14 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                a + plane, pins, pins + cplane, st));
     io.out_i0 = rcur;
     io.out_i1 = rcur + plane;
-    io.out_f0 = out_u + (size_t)t * HW;
-    io.out_f1 = out_v + (size_t)t * HW;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
     LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
-    if (fix_u)
-      LAUNCH(K_AUX, st,
-             launch_widen_frame(rcur, rcur + plane, H, W, Wp,
-                                fix_u + (size_t)t * HW, fix_v + (size_t)t * HW,
-                                st));
+    LAUNCH(K_AUX, st,
+           launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
+                             out_u + (size_t)t * HW, out_v + (size_t)t * HW,
+                             fix_u ? fix_u + (size_t)t * HW : nullptr,
+                             fix_v ? fix_v + (size_t)t * HW : nullptr, st));
   }
   if (wprof) {
     unsigned long long h[WP_N];

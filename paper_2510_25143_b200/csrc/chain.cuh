@@ -3,8 +3,8 @@
 // Shared by the encoder (codec.py:118-164 _encode_frame) and the decoder
 // (codec.py:167-206 _decode_frame).  Everything that does not depend on the
 // current frame's reconstructed neighbours is computed beforehand, fully in
-// parallel, by a prepare kernel; what is left is the recurrence through the
-// up / left / up-left neighbours:
+// parallel, by the prepare kernels (fast.cu); what is left is the
+// recurrence through the up / left / up-left neighbours:
 //
 //   decoder (value form):  r = rU + rL - rUL + A,   A = Pd + (sym-radius)*2e
 //   encoder (error form):  with err = recon - orig and
@@ -13,27 +13,25 @@
 //     sym = q + radius  (0 on escape)
 //
 // The encoder never divides on the critical path: R0 is split once per
-// pixel as R0 = Q0*2e + rho0, rho0 in [-e, e]; then y = rho0 - D lies in
-// [-4e, 4e] and q = Q0 + g with g in {-2..2} found by four comparisons
-// (ties -- y = +-e, +-3e -- round away from zero by the sign of x).
+// pixel (prepare kernel) as R0 = Q0*2e + rho0, rho0 in [-e, e]; with
+// y = rho0 - D, q = Q0 + g and, while |y| <= 4e, g follows from the signs
+// of y -+ e, y -+ 3e (see enc_fast_g).  Blocks where some |y| > 4e (step
+// sizes differ between neighbours) are redone with exact divisions.
 //
 // The two components are independent recurrences.  A task is one
 // component of one 32-row strip, run by a warp PAIR:
 //   C (chain warp): lane = row, sweeps the columns with a one-column skew
 //     per lane so the three neighbours are final when read; a step is
-//     shfl -> a few integer ops -> select, nothing else.  It hands the
+//     shfl -> integer ops -> select on register operands.  It hands the
 //     strip's last row to the strip below (shared memory inside the CTA,
 //     tagged global slots across CTAs).
-//   P (producer warp): stages 32-column chunks of the prepared plane with
-//     coalesced cp.async into a 4-slot ring, splits R0 (encoder), and writes
-//     finished chunks back out coalesced (recon / err, float64 output,
-//     symbols).
+//   P (producer warp): stages 32-column chunks of the prepared planes with
+//     coalesced cp.async into a 4-slot ring and writes finished chunks back
+//     out coalesced (recon / err, symbol planes).
 // A CTA holds NPAIR consecutive strips of one component; CTAs take tickets
 // in (strip group, component) order, so a CTA only ever waits on an
 // earlier, resident one.
 #pragma once
-
-#include <type_traits>
 
 #include "common.cuh"
 #include "wavefront.cuh"
@@ -41,37 +39,30 @@
 namespace vfcp {
 
 // Prepared planes (frame layout, row pitch Wp = 32 * nchunks):
-//   a0, a1  int32 per component: decoder -- A or the pinned recon;
-//           encoder -- R0 or the pinned err
+//   a0, a1    int32 per component: decoder -- A or the pinned recon;
+//             encoder -- R0 or the pinned err
+//   q0_0, q0_1  encoder: Q0 = rha(R0 / 2e) per component (0 where pinned)
+//   codes     encoder: frame t codes (pitch Wp)
 //   pin_u, pin_v  uint32 per (row, chunk): bit j = pixel c0+j is pinned
-//   nl      uint32 per (row, chunk): non-lossless (encoder: symbol slots)
-//   symw    uint32 per (row, chunk): encoder: pixels whose symbols the chain
-//           writes (non-lossless Lorenzo pixels)
 struct ChainIO {
   const int32_t* a0;
   const int32_t* a1;
+  const int32_t* q0_0;
+  const int32_t* q0_1;
+  const uint8_t* codes;
   const uint32_t* pin_u;
   const uint32_t* pin_v;
-  const uint32_t* nl;
-  const uint32_t* symw;
-  const uint8_t* codes;      // frame t codes (pitch Wp), encoder
   int32_t* out_i0;           // decoder: recon; encoder: err (pitch Wp)
   int32_t* out_i1;
-  double* out_f0;            // decoder: recon * inv_S (pitch W)
-  double* out_f1;
-  uint16_t* qd;              // encoder symbols
-  const int64_t* qd_row_off; // per frame row
-  const int32_t* chunk_nl;   // encoder: non-lossless count before each chunk
-  int32_t* row_esc;          // encoder: escapes found by the chain, per row
-  uint64_t* bnd;             // tagged last-row slots [ntask][2][W]
+  uint16_t* sym0;            // encoder: symbol planes (pitch Wp)
+  uint16_t* sym1;
+  uint64_t* bnd;             // tagged last-row slots [ntask][W]
   unsigned long long* stats; // optional phase timers (WavePhase)
   int* ticket;
-  uint32_t tag_base;          // tags unique across frames sharing `bnd`
+  uint32_t tag_base;         // tags unique across frames sharing `bnd`
   int H, W, Wp, nchunks;
   int radius;
-  double inv_S;
   int32_t e_tab[32];         // e per code (encoder; requires tau' < 2^28)
-  double inv2e_tab[32];
 };
 
 struct PrepParams {
@@ -100,9 +91,7 @@ __device__ __forceinline__ int32_t quant32(int32_t x, int32_t e, double inv2e) {
 // errL - errUL.  With y = rho - d, x = q0*2e + y and
 //   q = rha(x / 2e) = q0 + g,  g = floor((y+e)/2e)  (x >= 0)
 //                              g = ceil((y-e)/2e)   (x <  0),
-// err = g*2e - y (0 on escape).  The chain uses a comparison form of this
-// while |y| < 4e (the neighbours share this pixel's step) and this one
-// otherwise.
+// err = g*2e - y (0 on escape).
 __device__ __forceinline__ int32_t floordiv_p(int32_t a, int32_t d) {  // d > 0
   int32_t q = a / d;
   if ((a % d != 0) && (a < 0)) q--;
@@ -120,23 +109,44 @@ __device__ __forceinline__ int32_t enc_step_exact(int32_t rho, int32_t q0,
   return esc ? 0 : g * 2 * e - y;
 }
 
+// One encoder step without divisions, valid while |y| <= 4e (y = rho - d).
+// With the breakpoints B = rho -+ e, rho -+ 3e (y = +-e, +-3e), g rounds
+// ties downward in d* = d - [d < R0]: a tie rounds away from zero in
+// x = R0 - d, i.e. toward the larger g iff x > 0, and g_up(d) = g_dn(d-1).
+//   g = -2 - sum_k sign(d* - B_k)   (sign = arithmetic shift by 31)
+// No overflow: |R0| < 2^31 is compared, never subtracted; |d| <= 3 * 2^28,
+// |B_k| <= 4 * 2^28 (e < 2^28).  Returns the pixel's new err (0 on escape)
+// and its symbol (0 on escape).
+__device__ __forceinline__ int32_t enc_step_fast(int32_t R0, int32_t q0,
+                                                 int32_t rho, int32_t e,
+                                                 int32_t d, int32_t radius,
+                                                 uint32_t* sym) {
+  const int32_t ds = d - (d < R0 ? 1 : 0);
+  const int32_t b1 = rho - 3 * e, b2 = rho - e, b3 = rho + e, b4 = rho + 3 * e;
+  const int32_t g = -2 - (((ds - b1) >> 31) + ((ds - b2) >> 31)) -
+                    (((ds - b3) >> 31) + ((ds - b4) >> 31));
+  const int32_t q = q0 + g;
+  const bool esc = (uint32_t)(q + radius - 1) >= (uint32_t)(2 * radius - 1);
+  *sym = esc ? 0u : (uint32_t)(q + radius);
+  return esc ? 0 : g * (2 * e) + (d - rho);
+}
+
 // strips (warp pairs) per CTA; tasks per frame
 __host__ __device__ constexpr int chain_pairs(bool enc) { return 2; }
 __host__ __device__ inline int chain_ntask(bool enc, int H) {
   return 2 * ((H + 32 * chain_pairs(enc) - 1) / (32 * chain_pairs(enc)));
 }
-constexpr int CNS = 4;   // chunk slots: the sweep of block m uses chunks m-1
+constexpr int CNS = 6;   // chunk slots: the sweep of block m uses chunks m-1
                          // and m; P stages m+1, m+2 meanwhile
 
 template <bool ENC>
 struct PairRing {
-  int32_t v[CNS][32][32];   // [slot][row][col ^ row]: A -> recon; rho0 -> err
+  // [slot][row][col]: A -> recon; R0 -> err.  No swizzle: the chain warp
+  // reads column c0 - lane + jj in row lane, distinct banks across lanes.
+  int32_t v[CNS][32][32];
   uint32_t pin[CNS][32];
   int32_t q0[ENC ? CNS : 1][32][32];   // encoder: Q0, then the symbol
-  int32_t e[ENC ? CNS : 1][32][32];    // encoder: e per pixel
   uint32_t code[ENC ? CNS : 1][32][8]; // encoder: codes, 4 per word
-  uint32_t nl[ENC ? CNS : 1][32];
-  uint32_t symw[ENC ? CNS : 1][32];
 };
 
 template <bool ENC>
@@ -144,16 +154,16 @@ struct ChainSmem {
   PairRing<ENC> r[chain_pairs(ENC)];
   int32_t bnd[chain_pairs(ENC)][4][32];   // row 31 of strip p, [chunk & 3]
   int32_t etab[32];
-  double inv2e[32];
   int bdone[chain_pairs(ENC)];   // blocks of C_p whose row 31 is in bnd
   int bread[chain_pairs(ENC)];   // chunks of bnd[p-1] C_p has consumed
-  int full[chain_pairs(ENC)];    // chunks P_p has staged (and split)
+  int full[chain_pairs(ENC)];    // chunks P_p has staged
   int done[chain_pairs(ENC)];    // blocks C_p has swept
   int task;
 };
 
 __device__ __forceinline__ void spin_ge(const int* p, int need) {
-  while (!__all_sync(0xffffffffu, ld_volatile(p) >= need)) __nanosleep(20);
+  while (!__all_sync(0xffffffffu, ld_volatile(p) >= need)) {
+  }
   __threadfence_block();
 }
 __device__ __forceinline__ void signal_set(int* p, int v, int lane) {
@@ -179,10 +189,7 @@ chain_kernel(ChainIO io) {
   const int H = io.H, W = io.W, Wp = io.Wp, nchunks = io.nchunks;
   const int nblocks = (W + 31 + 31) / 32;
   const int ntask = chain_ntask(ENC, H);
-  if (threadIdx.x < 32) {
-    sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
-    sm.inv2e[threadIdx.x] = io.inv2e_tab[threadIdx.x];
-  }
+  if (threadIdx.x < 32) sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
 
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
@@ -204,23 +211,23 @@ chain_kernel(ChainIO io) {
     if (producer && wact) {
       // ===================================================== producer
       const int32_t* a = comp ? io.a1 : io.a0;
+      const int32_t* q0p = comp ? io.q0_1 : io.q0_0;
       const uint32_t* pinp = comp ? io.pin_v : io.pin_u;
       int32_t* out_i = comp ? io.out_i1 : io.out_i0;
-      double* out_f = comp ? io.out_f1 : io.out_f0;
+      uint16_t* symp = comp ? io.sym1 : io.sym0;
       auto stage = [&](int x) {
         const int s = x % CNS;
         const int c = 32 * x + lane;
 #pragma unroll 8
         for (int r = 0; r < 32; r++) {
           const bool rv = r < nrows;
-          cp_async<4>(&R.v[s][r][lane ^ r],
-                      a + (int64_t)(i0 + (rv ? r : 0)) * Wp + c, rv);
+          const int64_t k = (int64_t)(i0 + (rv ? r : 0)) * Wp + c;
+          cp_async<4>(&R.v[s][r][lane], a + k, rv);
+          if (ENC) cp_async<4>(&R.q0[s][r][lane], q0p + k, rv);
         }
         const int64_t pb = (int64_t)(rowok ? my_i : i0) * nchunks + x;
         cp_async<4>(&R.pin[s][lane], pinp + pb, rowok);
         if (ENC) {
-          cp_async<4>(&R.nl[s][lane], io.nl + pb, rowok);
-          cp_async<4>(&R.symw[s][lane], io.symw + pb, rowok);
 #pragma unroll
           for (int k = 0; k < 8; k++) {
             const int r = (lane >> 3) + 4 * k, q = lane & 7;
@@ -231,55 +238,28 @@ chain_kernel(ChainIO io) {
           }
         }
       };
-      // encoder: e per pixel and R0 = Q0*2e + rho0 (lane = column)
-      auto split = [&](int x) {
-        if (!ENC) return;
-        const int s = x % CNS;
-        const uint32_t bit = 1u << lane;
-        const unsigned char* cb = reinterpret_cast<const unsigned char*>(&R.code[s][0][0]);
-#pragma unroll 4
-        for (int r = 0; r < 32; r++) {
-          if (r >= nrows) break;
-          const int cd = cb[32 * r + lane] & 31;
-          const int32_t e = sm.etab[cd];
-          const bool pin = (R.pin[s][r] & bit) != 0;
-          const int32_t av = R.v[s][r][lane ^ r];
-          const int32_t q = (!pin && e != 0) ? quant32(av, e, sm.inv2e[cd]) : 0;
-          R.v[s][r][lane ^ r] = av - q * 2 * e;
-          R.q0[s][r][lane ^ r] = q;
-          R.e[s][r][lane ^ r] = e;
-        }
-      };
-      int32_t esc_row = 0;   // lane r: escapes of row r in this component
+      // batched 16 rows at a time so the loads of a batch overlap
       auto write_out = [&](int x) {
         const int s = x % CNS;
         const int c = 32 * x + lane;
         const bool cv = c < W;
-        int64_t base_r = 0;
-        if (ENC && rowok)
-          base_r = io.qd_row_off[my_i] + comp +
-                   2 * (int64_t)io.chunk_nl[(int64_t)my_i * nchunks + x];
-#pragma unroll 4
-        for (int r = 0; r < 32; r++) {
-          if (r >= nrows) break;
-          const int32_t val = R.v[s][r][lane ^ r];
-          if (cv) {
-            out_i[(int64_t)(i0 + r) * Wp + c] = val;
-            if (!ENC)
-              out_f[(int64_t)(i0 + r) * W + c] = __dmul_rn((double)val, io.inv_S);
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {
+          int32_t val[16], sy[16];
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            const int r = h + k;
+            val[k] = R.v[s][r][lane];
+            if (ENC) sy[k] = R.q0[s][r][lane];
           }
-          if (ENC) {
-            const int64_t base = __shfl_sync(FULL, base_r, r);
-            const uint32_t nlw = R.nl[s][r], sww = R.symw[s][r];
-            const uint32_t bit = 1u << lane;
-            int ne = 0;
-            if (cv && (sww & bit)) {
-              const uint32_t sy = (uint32_t)R.q0[s][r][lane ^ r];
-              io.qd[base + 2 * __popc(nlw & (bit - 1u))] = (uint16_t)sy;
-              ne = sy == 0;
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            const int r = h + k;
+            if (cv && r < nrows) {
+              const int64_t kk = (int64_t)(i0 + r) * Wp + c;
+              out_i[kk] = val[k];
+              if (ENC) symp[kk] = (uint16_t)sy[k];
             }
-            const int tot = __reduce_add_sync(FULL, ne);
-            if (lane == r) esc_row += tot;
           }
         }
       };
@@ -304,13 +284,10 @@ chain_kernel(ChainIO io) {
         }
         cp_async_commit();
         cp_async_wait_group<1>();   // chunk x-1 has landed
-        __syncwarp();
-        split(x - 1);
         signal_set(&sm.full[pr], x, lane);
         pc.lap(WP_PRE, lane);
       }
       retire_before(nchunks + CNS - 1);
-      if (ENC && rowok && esc_row) atomicAdd(io.row_esc + my_i, esc_row);
     } else if (wact) {
       // ===================================================== chain warp
       const bool has_next = i0 + 32 < H;
@@ -319,6 +296,7 @@ chain_kernel(ChainIO io) {
       uint64_t* my_gb = io.bnd + (int64_t)task * W;
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
       const bool top = i0 > 0;
+      const bool lane0 = lane == 0;
       int32_t l = 0, ul = 0;
       for (int m = 0; m < nblocks; m++) {
         const int c0 = 32 * m;
@@ -353,14 +331,13 @@ chain_kernel(ChainIO io) {
                 : 0u;
         const uint32_t pm =
             __funnelshift_r(R.pin[s_lo][lane], R.pin[s_hi][lane], cbase & 31) | ~vm;
-        const bool lane0 = lane == 0;
         if (!ENC) {
           int32_t av[32];
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
             const int c = cbase + jj;
             const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-            const int32_t x = R.v[sl][lane][(c & 31) ^ lane];
+            const int32_t x = R.v[sl][lane][c & 31];
             av[jj] = c < 0 ? 0 : x;
           }
 #pragma unroll
@@ -379,72 +356,75 @@ chain_kernel(ChainIO io) {
           for (int jj = 0; jj < 32; jj++) {
             const int c = cbase + jj;
             const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-            if ((vm >> jj) & 1u) R.v[sl][lane][(c & 31) ^ lane] = av[jj];
+            if ((vm >> jj) & 1u) R.v[sl][lane][c & 31] = av[jj];
           }
         } else {
           const int32_t radius = io.radius;
           const int32_t l_s = l, ul_s = ul;
-          // operands into registers first: the sweep's stores would
-          // otherwise keep later loads from being hoisted past them.
-          // ee = 0 where pinned / absent (no slow-path trigger there).
+          const unsigned char* cb_lo =
+              reinterpret_cast<const unsigned char*>(&R.code[s_lo][lane][0]);
+          const unsigned char* cb_hi =
+              reinterpret_cast<const unsigned char*>(&R.code[s_hi][lane][0]);
+          // operands into registers first (the sweep's stores would keep
+          // later loads from being hoisted past them): rr = R0 (or the
+          // pinned err; 0 left of column 0), qq = Q0, ee = e (0 where
+          // pinned / absent: no slow-path trigger there)
           int32_t rr[32], qq[32], ee[32];
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
             const int c = cbase + jj;
-            const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-            const int col = (c & 31) ^ lane;
+            const bool lo = (uint32_t)jj < split;
+            const int sl = lo ? s_lo : s_hi;
+            const int col = c & 31;
             const int32_t x = R.v[sl][lane][col];
             rr[jj] = c < 0 ? 0 : x;
             qq[jj] = R.q0[sl][lane][col];
-            const int32_t e = R.e[sl][lane][col];
+            const int e = sm.etab[(lo ? cb_lo : cb_hi)[c & 31] & 31];
             ee[jj] = ((pm >> jj) & 1u) ? 0 : e;
           }
+          pc.lap(WP_TASKS, lane);
           bool slow = false;
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
-            const int32_t rho = rr[jj], q0 = qq[jj], e = ee[jj];
+            const int32_t R0 = rr[jj], q0 = qq[jj], e = ee[jj];
+            const int32_t rho = R0 - q0 * (2 * e);
             const int32_t bb = __shfl_sync(FULL, b, jj);
             const int32_t up = __shfl_up_sync(FULL, l, 1);
             const int32_t nu = lane0 ? bb : up;
             const int32_t d = nu + l - ul;
-            // q = rha(x / 2e), x = q0*2e + y, valid while |y| < 4e: count
-            // the thresholds +-e, +-3e passed (ties upward), then a tie
-            // rounds away from zero
-            const int32_t y = rho - d;
-            const int32_t e3 = 3 * e;
-            const int32_t gf = (y >= e) + (y >= e3) - (y < -e) - (y < -e3);
-            const int32_t ay = y < 0 ? -y : y;
-            const bool tie = (ay == e) | (ay == e3);
-            const int32_t qf = q0 + gf;
-            const int32_t q = qf - ((tie && qf <= 0) ? 1 : 0);
-            const bool esc = (uint32_t)(q + radius - 1) >= (uint32_t)(2 * radius - 1);
+            uint32_t sy;
+            const int32_t er = enc_step_fast(R0, q0, rho, e, d, radius, &sy);
             const bool pin = (pm >> jj) & 1u;
-            const int32_t r = pin ? rho : (esc ? 0 : (q - q0) * 2 * e - y);
-            qq[jj] = (pin || esc) ? 0 : q + radius;
-            slow |= (e != 0) & (ay >= 4 * e);
+            const int32_t r = pin ? R0 : er;
+            qq[jj] = pin ? 0 : (int32_t)sy;
+            // |y| > 4e: y + 4e outside [0, 8e] (no overflow for e < 2^28)
+            slow |= (e != 0) & ((uint32_t)(rho - d + 4 * e) > (uint32_t)(8 * e));
             rr[jj] = r;
             l = r;
             ul = nu;
           }
           if (__any_sync(FULL, slow)) {
             // mixed steps: redo the block with the exact step
+            if (io.stats && lane == 0) atomicAdd(io.stats + WP_X2, 1ull);
             l = l_s; ul = ul_s;
 #pragma unroll 1
             for (int jj = 0; jj < 32; jj++) {
               const int c = cbase + jj;
-              const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-              const int col = (c & 31) ^ lane;
+              const bool lo = (uint32_t)jj < split;
+              const int sl = lo ? s_lo : s_hi;
+              const int col = c & 31;
               const bool valid = (vm >> jj) & 1u, pin = (pm >> jj) & 1u;
-              const int32_t rho = c < 0 ? 0 : R.v[sl][lane][col];
+              const int32_t R0 = c < 0 ? 0 : R.v[sl][lane][col];
               const int32_t q0 = R.q0[sl][lane][col];
-              const int32_t e = pin ? 0 : R.e[sl][lane][col];
+              const int32_t e = pin ? 0 : sm.etab[(lo ? cb_lo : cb_hi)[c & 31] & 31];
               const int32_t bb = __shfl_sync(FULL, b, jj);
               const int32_t up = __shfl_up_sync(FULL, l, 1);
               const int32_t nu = lane0 ? bb : up;
               const int32_t d = nu + l - ul;
               uint32_t sy = 0;
-              const int32_t er = e != 0 ? enc_step_exact(rho, q0, e, d, radius, &sy) : 0;
-              const int32_t r = pin ? rho : er;
+              const int32_t er =
+                  e != 0 ? enc_step_exact(R0 - q0 * 2 * e, q0, e, d, radius, &sy) : 0;
+              const int32_t r = pin ? R0 : er;
               if (valid) {
                 R.v[sl][lane][col] = r;
                 R.q0[sl][lane][col] = pin ? 0 : (int32_t)sy;
@@ -457,7 +437,7 @@ chain_kernel(ChainIO io) {
             for (int jj = 0; jj < 32; jj++) {
               const int c = cbase + jj;
               const int sl = (uint32_t)jj < split ? s_lo : s_hi;
-              const int col = (c & 31) ^ lane;
+              const int col = c & 31;
               if ((vm >> jj) & 1u) {
                 R.v[sl][lane][col] = rr[jj];
                 R.q0[sl][lane][col] = qq[jj];
@@ -472,7 +452,7 @@ chain_kernel(ChainIO io) {
           const int c = c0 - 31 + lane;   // the columns row 31 did now
           const bool cv = c >= 0 && c < W;
           const int sl = cv ? (c >> 5) % CNS : 0;
-          const int32_t val = cv ? R.v[sl][31][(c & 31) ^ 31] : 0;
+          const int32_t val = cv ? R.v[sl][31][c & 31] : 0;
           if (next_in_cta) {
             spin_ge(&sm.bread[pr + 1], m - 3);   // slot (m+1)&3 reused
             if (cv) sm.bnd[pr][(c >> 5) & 3][c & 31] = val;

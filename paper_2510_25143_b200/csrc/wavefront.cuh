@@ -130,7 +130,7 @@ struct TaggedSlot {
       uint64_t w = valid ? ld_relaxed_u64(s + h) : 0;
       bool ok = !valid || (uint32_t)(w >> 32) == tag;
       while (!__all_sync(0xffffffffu, ok)) {
-        __nanosleep(20);
+        // poll again (no sleep: wake-up granularity exceeds the handoff)
         if (!ok) {
           w = ld_relaxed_u64(s + h);
           ok = (uint32_t)(w >> 32) == tag;
