@@ -217,18 +217,13 @@ def main():
     dv = torch.from_numpy(v_h).cuda()
     f_dev = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, du, dv)
 
+    from paper_2510_25143_b200 import replicas
+
     def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-            torch.cuda.synchronize()
+        replicas.barrier(dist)
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return replicas.max_over_ranks(x, dist)
 
     # ---- compress (device-resident inputs)
     for _ in range(args.warmup):

@@ -53,8 +53,9 @@ int vfcp_version(void);
 
 /* Instrumentation: number of kernels this library has launched, and
  * per-kernel-class CUDA-event timings (classes: 0 range, 1 analyze, 2 scan,
- * 3 mop, 4 encode, 5 ll write, 6 decode rows, 7 decode ll, 8 decode,
- * 9 aux).  vfcp_prof_collect synchronises on the recorded events. */
+ * 3 mop, 4 encode chain, 5 ll write / symbol scatter, 6 decode prep,
+ * 7 decode ll, 8 decode chain, 9 aux (frame emit), 10 encode prep).
+ * vfcp_prof_collect synchronises on the recorded events. */
 int64_t vfcp_launch_count(void);
 int vfcp_prof_enable(int on);
 int vfcp_prof_collect(double* ms, int64_t* counts, int ncls);

@@ -113,7 +113,7 @@ def lib():
 def check(rc: int, what: str):
     if rc != 0:
         msg = lib().vfcp_last_error().decode(errors="replace")
-        if rc == -1:
+        if rc in (-1, -4):   # VFCP_EINVAL, VFCP_ECORRUPT: the reference's ValueError
             raise ValueError(f"{what}: {msg}")
         raise VfcpError(f"{what} failed ({rc}): {msg}")
 
