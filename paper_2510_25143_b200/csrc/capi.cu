@@ -137,10 +137,26 @@ Prof g_prof;
     }                                                                      \
   } while (0)
 
+// Stream-ordered scratch from the device's default memory pool.  The pool
+// keeps freed memory (release threshold = max) so repeated calls do not
+// re-map gigabytes of scratch at every synchronisation.
+void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+
 struct Scratch {
   cudaStream_t st;
   std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t s) : st(s) {}
+  explicit Scratch(cudaStream_t s) : st(s) { keep_pool_memory(); }
   template <typename T>
   cudaError_t get(T** p, size_t count) {
     void* q = nullptr;
