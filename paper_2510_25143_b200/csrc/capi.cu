@@ -394,7 +394,7 @@ int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
 // otherwise.
 bool fast_ok(const vfcp_params* p) {
   return p->bx == 32 && p->by == 32 && p->radius <= 32768 &&
-         p->tau < ((int64_t)1 << 28) && p->stride >= 2;
+         p->tau < ((int64_t)1 << 28) && p->stride >= 2 && p->H <= 65535;
 }
 
 PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
@@ -425,6 +425,23 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
 void chain_tables(ChainIO& io, const Ladder& lad) {
   for (int k = 0; k < 32; k++) {
     io.e_tab[k] = (int32_t)lad.e[k];
+  }
+}
+
+// VFCP_WAVE_PROFILE: per-strip start / first-block / end times of one frame
+void print_stamps(const char* tag, unsigned long long* d, int H, cudaStream_t st) {
+  const int K = (H + 31) / 32;
+  std::vector<unsigned long long> h((size_t)3 * 2 * K);
+  if (cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
+                      cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return;
+  unsigned long long t0 = ~0ull;
+  for (auto x : h) if (x && x < t0) t0 = x;
+  fprintf(stderr, "[stamps %s] strip: first-block-start end (us, comp u)\n", tag);
+  for (int k = 0; k < K; k += (K > 16 ? K / 16 : 1)) {
+    const unsigned long long* e = &h[(size_t)(2 * k) * 3];
+    fprintf(stderr, "  %4d %9.1f %9.1f\n", k, (e[1] - t0) * 1e-3, (e[2] - t0) * 1e-3);
   }
 }
 
@@ -496,9 +513,12 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   memset(&io, 0, sizeof(io));
   chain_tables(io, lad);
   const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
+  std::vector<unsigned long long> tsv;
   if (wprof) {
     CK(sc.get(&io.stats, WP_N));
     CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
+    CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
+    CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
   }
   io.a0 = a;
   io.a1 = a + plane;
@@ -534,6 +554,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
     LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
+    if (wprof && t == 1) print_stamps("enc", io.tstamp, H, st);
     LAUNCH(K_LLW, st,
            launch_sym_scatter(syms, syms + plane, pins + 2 * cplane,
                               pins + 3 * cplane, qd_row_off + (size_t)t * H,
@@ -595,9 +616,12 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   memset(&io, 0, sizeof(io));
   chain_tables(io, lad);
   const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
+  std::vector<unsigned long long> tsv;
   if (wprof) {
     CK(sc.get(&io.stats, WP_N));
     CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
+    CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
+    CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
   }
   io.a0 = a;
   io.a1 = a + plane;
@@ -621,6 +645,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
     LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
+    if (wprof && t == 1) print_stamps("dec", io.tstamp, H, st);
     LAUNCH(K_AUX, st,
            launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
                              out_u + (size_t)t * HW, out_v + (size_t)t * HW,

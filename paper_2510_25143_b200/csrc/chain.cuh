@@ -58,6 +58,7 @@ struct ChainIO {
   uint16_t* sym1;
   uint64_t* bnd;             // tagged last-row slots [ntask][W]
   unsigned long long* stats; // optional phase timers (WavePhase)
+  unsigned long long* tstamp; // optional per-task [start, first block, end] ns
   int* ticket;
   uint32_t tag_base;         // tags unique across frames sharing `bnd`
   int H, W, Wp, nchunks;
@@ -132,11 +133,11 @@ __device__ __forceinline__ int32_t enc_step_fast(int32_t R0, int32_t q0,
 }
 
 // strips (warp pairs) per CTA; tasks per frame
-__host__ __device__ constexpr int chain_pairs(bool enc) { return 2; }
+__host__ __device__ constexpr int chain_pairs(bool enc) { return enc ? 4 : 4; }
 __host__ __device__ inline int chain_ntask(bool enc, int H) {
   return 2 * ((H + 32 * chain_pairs(enc) - 1) / (32 * chain_pairs(enc)));
 }
-constexpr int CNS = 6;   // chunk slots: the sweep of block m uses chunks m-1
+constexpr int CNS = 4;   // chunk slots: the sweep of block m uses chunks m-1
                          // and m; P stages m+1, m+2 meanwhile
 
 template <bool ENC>
@@ -149,20 +150,27 @@ struct PairRing {
   uint32_t code[ENC ? CNS : 1][32][8]; // encoder: codes, 4 per word
 };
 
+constexpr int HRING = 128;   // boundary-row ring (columns), power of two
+
 template <bool ENC>
 struct ChainSmem {
   PairRing<ENC> r[chain_pairs(ENC)];
-  int32_t bnd[chain_pairs(ENC)][4][32];   // row 31 of strip p, [chunk & 3]
+  int32_t hin[chain_pairs(ENC) + 1][HRING];   // row i0-1 of strip p
   int32_t etab[32];
-  int bdone[chain_pairs(ENC)];   // blocks of C_p whose row 31 is in bnd
-  int bread[chain_pairs(ENC)];   // chunks of bnd[p-1] C_p has consumed
-  int full[chain_pairs(ENC)];    // chunks P_p has staged
-  int done[chain_pairs(ENC)];    // blocks C_p has swept
+  int hprog[chain_pairs(ENC) + 1];   // columns of hin[p] available
+  int full[chain_pairs(ENC)];        // chunks P_p has staged
+  int done[chain_pairs(ENC)];        // blocks C_p has swept
   int task;
 };
 
+// Warp-uniform wait for a shared-memory counter.  The chain warps poll
+// tightly (they are on the critical path); the producers back off so their
+// polling does not take issue slots and shared-memory bandwidth from the
+// chain warp on the same sub-partition.
+template <int SLEEP_NS = 0>
 __device__ __forceinline__ void spin_ge(const int* p, int need) {
   while (!__all_sync(0xffffffffu, ld_volatile(p) >= need)) {
+    if (SLEEP_NS) __nanosleep(SLEEP_NS);
   }
   __threadfence_block();
 }
@@ -182,8 +190,10 @@ chain_kernel(ChainIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChainSmem<ENC>& sm = *reinterpret_cast<ChainSmem<ENC>*>(smem_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int pr = wid >> 1;
-  const bool producer = (wid & 1) == 0;
+  // chain warps 0..NPAIR-1, producers NPAIR..2*NPAIR-1: with NPAIR = 4 every
+  // SM sub-partition (warp % 4) holds one chain and one producer warp
+  const int pr = wid % NPAIR;
+  const bool producer = wid >= NPAIR;
   PairRing<ENC>& R = sm.r[pr];
   const unsigned FULL = 0xffffffffu;
   const int H = io.H, W = io.W, Wp = io.Wp, nchunks = io.nchunks;
@@ -194,7 +204,7 @@ chain_kernel(ChainIO io) {
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
     if (threadIdx.x < NPAIR) {
-      sm.bdone[threadIdx.x] = 0; sm.bread[threadIdx.x] = 0;
+      sm.hprog[threadIdx.x] = 0;
       sm.full[threadIdx.x] = 0; sm.done[threadIdx.x] = 0;
     }
     __syncthreads();
@@ -268,7 +278,7 @@ chain_kernel(ChainIO io) {
       int next_out = 0;
       auto retire_before = [&](int x) {   // free the slot chunk x needs
         while (next_out <= x - CNS) {
-          spin_ge(&sm.done[pr], min(next_out + 2, nblocks));
+          spin_ge<200>(&sm.done[pr], min(next_out + 2, nblocks));
           pc.lap(WP_X1, lane);
           write_out(next_out);
           next_out++;
@@ -290,32 +300,73 @@ chain_kernel(ChainIO io) {
       retire_before(nchunks + CNS - 1);
     } else if (wact) {
       // ===================================================== chain warp
+      // Row i0-1 (the strip above's last row) arrives in hin[pr] (a ring of
+      // HRING columns) with hprog[pr] = columns available: streamed every 8
+      // steps by the chain warp above when it is in this CTA, fetched per
+      // block from the tagged global slots otherwise.  This strip's last
+      // row is streamed the same way into hin[pr+1], or put to the global
+      // slots after each block for the next CTA.
       const bool has_next = i0 + 32 < H;
-      const bool next_in_cta = pr + 1 < NPAIR;
+      const bool stream_out = has_next && pr + 1 < NPAIR;
       const uint32_t tag = io.tag_base + (uint32_t)task + 1u;
       uint64_t* my_gb = io.bnd + (int64_t)task * W;
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
       const bool top = i0 > 0;
-      const bool lane0 = lane == 0;
+      const bool lane0 = lane == 0, lane31 = lane == 31;
+      int32_t* hin = sm.hin[pr];
+      int32_t* hout = sm.hin[pr + (stream_out ? 1 : 0)];
+      int* hprog_out = &sm.hprog[pr + (stream_out ? 1 : 0)];
       int32_t l = 0, ul = 0;
+      uint64_t bpre = 0;   // prefetched tagged boundary slot (pr == 0)
+      if (top && pr == 0 && lane < W) bpre = ld_relaxed_u64(up_gb + lane);
+      auto stamp = [&](int k) {
+        if (io.tstamp && lane == 0) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          io.tstamp[(int64_t)(2 * g * NPAIR + 2 * pr + comp) * 3 + k] = t;
+        }
+      };
+      stamp(0);
       for (int m = 0; m < nblocks; m++) {
         const int c0 = 32 * m;
         spin_ge(&sm.full[pr], min(m + 1, nchunks));
         pc.lap(WP_WAITPREV, lane);
-        // ---- boundary row (row i0-1) for columns c0..c0+31
-        int32_t b = 0;
-        if (top && c0 < W) {
-          if (pr > 0) {
-            spin_ge(&sm.bdone[pr - 1], min(m + 2, nblocks));
-            b = c0 + lane < W ? sm.bnd[pr - 1][m & 3][lane] : 0;
-            signal_set(&sm.bread[pr], m + 1, lane);
-          } else {
-            const int c = c0 + lane;
-            const bool v = c < W;
-            b = TaggedSlot<int32_t>::get(up_gb + (v ? c : 0), tag - 2, v);
+        if (m == 1) stamp(1);
+        if (top && pr == 0 && c0 < W) {
+          // tagged slots of the strip above (other CTA); the load for this
+          // block was issued during the previous block's sweep
+          const int c = c0 + lane;
+          const bool v = c < W;
+          uint64_t w = v ? bpre : 0;
+          bool ok = !v || (uint32_t)(w >> 32) == tag - 2;
+          while (!__all_sync(FULL, ok)) {
+            if (!ok) {
+              w = ld_relaxed_u64(up_gb + c);
+              ok = (uint32_t)(w >> 32) == tag - 2;
+            }
           }
+          hin[c & (HRING - 1)] = (int32_t)(uint32_t)w;
+          __syncwarp();
+          const int cn = c + 32;
+          if (cn < W) bpre = ld_relaxed_u64(up_gb + cn);
         }
+        // the consumer below must be done with the ring entries we reuse
+        if (stream_out) spin_ge(&sm.done[pr + 1], m - (HRING / 32 - 1));
         pc.lap(WP_WAITBND, lane);
+        // wait for the boundary columns c0+jj .. c0+jj+7 (pr > 0)
+        auto need_bnd = [&](int jj) {
+          if (top && pr > 0) spin_ge(&sm.hprog[pr], min(c0 + jj + 8, W));
+        };
+        auto bnd_at = [&](int jj) -> int32_t {
+          return top ? hin[(c0 + jj) & (HRING - 1)] : 0;
+        };
+        // after step jj, row 31 has finished column c0-31+jj
+        auto publish = [&](int jj) {
+          if (lane31) {
+            __threadfence_block();
+            *(volatile int*)hprog_out = min(max(c0 - 31 + jj + 1, 0), W);
+          }
+        };
         // ---- this lane's 32 columns c = c0 - lane + jj (two chunks).
         // vm: bit jj = pixel (my_i, cbase+jj) exists; pm: pinned or not
         // existing (those take their prepared value, 0 left of column 0, so
@@ -331,6 +382,7 @@ chain_kernel(ChainIO io) {
                 : 0u;
         const uint32_t pm =
             __funnelshift_r(R.pin[s_lo][lane], R.pin[s_hi][lane], cbase & 31) | ~vm;
+        const int hcol = (c0 - 31) & (HRING - 1);   // lane 31's ring column at jj = 0
         if (!ENC) {
           int32_t av[32];
 #pragma unroll
@@ -340,9 +392,18 @@ chain_kernel(ChainIO io) {
             const int32_t x = R.v[sl][lane][c & 31];
             av[jj] = c < 0 ? 0 : x;
           }
+          int32_t bbv[8];
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
-            const int32_t bb = __shfl_sync(FULL, b, jj);
+            if ((jj & 7) == 0) {
+              // the group's boundary values into registers up front: the
+              // ring stores below may alias, so loads inside the loop would
+              // wait for the previous step's result
+              need_bnd(jj);
+#pragma unroll
+              for (int k = 0; k < 8; k++) bbv[k] = bnd_at(jj + k);
+            }
+            const int32_t bb = bbv[jj & 7];
             const int32_t up = __shfl_up_sync(FULL, l, 1);
             const int32_t nu = lane0 ? bb : up;
             const int32_t t = (int32_t)((uint32_t)av[jj] - (uint32_t)ul);
@@ -351,6 +412,10 @@ chain_kernel(ChainIO io) {
             av[jj] = r;
             l = r;
             ul = nu;
+            if (stream_out) {
+              if (lane31) hout[(hcol + jj) & (HRING - 1)] = r;
+              if ((jj & 7) == 7) publish(jj);
+            }
           }
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
@@ -383,30 +448,47 @@ chain_kernel(ChainIO io) {
             ee[jj] = ((pm >> jj) & 1u) ? 0 : e;
           }
           pc.lap(WP_TASKS, lane);
-          bool slow = false;
+          // fast steps 8 at a time; results before the first step with
+          // |y| > 4e are exact, so completed groups are published at once
+          bool redo = false;
 #pragma unroll
-          for (int jj = 0; jj < 32; jj++) {
-            const int32_t R0 = rr[jj], q0 = qq[jj], e = ee[jj];
-            const int32_t rho = R0 - q0 * (2 * e);
-            const int32_t bb = __shfl_sync(FULL, b, jj);
-            const int32_t up = __shfl_up_sync(FULL, l, 1);
-            const int32_t nu = lane0 ? bb : up;
-            const int32_t d = nu + l - ul;
-            uint32_t sy;
-            const int32_t er = enc_step_fast(R0, q0, rho, e, d, radius, &sy);
-            const bool pin = (pm >> jj) & 1u;
-            const int32_t r = pin ? R0 : er;
-            qq[jj] = pin ? 0 : (int32_t)sy;
-            // |y| > 4e: y + 4e outside [0, 8e] (no overflow for e < 2^28)
-            slow |= (e != 0) & ((uint32_t)(rho - d + 4 * e) > (uint32_t)(8 * e));
-            rr[jj] = r;
-            l = r;
-            ul = nu;
+          for (int g8 = 0; g8 < 32; g8 += 8) {
+            if (!redo) {
+              need_bnd(g8);
+              int32_t bbv[8];   // see the decoder sweep
+#pragma unroll
+              for (int k = 0; k < 8; k++) bbv[k] = bnd_at(g8 + k);
+              bool slow = false;
+#pragma unroll
+              for (int k = 0; k < 8; k++) {
+                const int jj = g8 + k;
+                const int32_t R0 = rr[jj], q0 = qq[jj], e = ee[jj];
+                const int32_t rho = R0 - q0 * (2 * e);
+                const int32_t bb = bbv[k];
+                const int32_t up = __shfl_up_sync(FULL, l, 1);
+                const int32_t nu = lane0 ? bb : up;
+                const int32_t d = nu + l - ul;
+                uint32_t sy;
+                const int32_t er = enc_step_fast(R0, q0, rho, e, d, radius, &sy);
+                const bool pin = (pm >> jj) & 1u;
+                const int32_t r = pin ? R0 : er;
+                qq[jj] = pin ? 0 : (int32_t)sy;
+                // |y| > 4e: y + 4e outside [0, 8e] (no overflow, e < 2^28)
+                slow |= (e != 0) & ((uint32_t)(rho - d + 4 * e) > (uint32_t)(8 * e));
+                rr[jj] = r;
+                l = r;
+                ul = nu;
+                if (stream_out && lane31) hout[(hcol + jj) & (HRING - 1)] = r;
+              }
+              if (__any_sync(FULL, slow)) redo = true;
+              else if (stream_out) publish(g8 + 7);
+            }
           }
-          if (__any_sync(FULL, slow)) {
+          if (redo) {
             // mixed steps: redo the block with the exact step
             if (io.stats && lane == 0) atomicAdd(io.stats + WP_X2, 1ull);
             l = l_s; ul = ul_s;
+            if (top && pr > 0) spin_ge(&sm.hprog[pr], min(c0 + 32, W));
 #pragma unroll 1
             for (int jj = 0; jj < 32; jj++) {
               const int c = cbase + jj;
@@ -417,7 +499,7 @@ chain_kernel(ChainIO io) {
               const int32_t R0 = c < 0 ? 0 : R.v[sl][lane][col];
               const int32_t q0 = R.q0[sl][lane][col];
               const int32_t e = pin ? 0 : sm.etab[(lo ? cb_lo : cb_hi)[c & 31] & 31];
-              const int32_t bb = __shfl_sync(FULL, b, jj);
+              const int32_t bb = bnd_at(jj);
               const int32_t up = __shfl_up_sync(FULL, l, 1);
               const int32_t nu = lane0 ? bb : up;
               const int32_t d = nu + l - ul;
@@ -429,9 +511,11 @@ chain_kernel(ChainIO io) {
                 R.v[sl][lane][col] = r;
                 R.q0[sl][lane][col] = pin ? 0 : (int32_t)sy;
               }
+              if (stream_out && lane31) hout[(hcol + jj) & (HRING - 1)] = r;
               l = r;
               ul = nu;
             }
+            if (stream_out) publish(31);
           } else {
 #pragma unroll
             for (int jj = 0; jj < 32; jj++) {
@@ -447,23 +531,18 @@ chain_kernel(ChainIO io) {
         }
         __syncwarp();
         pc.lap(WP_CHAIN, lane);
-        // ---- row 31 of this strip for the strip below (from the ring)
-        if (has_next) {
+        // ---- row 31 for the strip below in the next CTA (from the ring)
+        if (has_next && !stream_out) {
           const int c = c0 - 31 + lane;   // the columns row 31 did now
           const bool cv = c >= 0 && c < W;
           const int sl = cv ? (c >> 5) % CNS : 0;
           const int32_t val = cv ? R.v[sl][31][c & 31] : 0;
-          if (next_in_cta) {
-            spin_ge(&sm.bread[pr + 1], m - 3);   // slot (m+1)&3 reused
-            if (cv) sm.bnd[pr][(c >> 5) & 3][c & 31] = val;
-            signal_set(&sm.bdone[pr], m + 1, lane);
-          } else if (cv) {
-            TaggedSlot<int32_t>::put(my_gb + c, tag, val);
-          }
+          if (cv) TaggedSlot<int32_t>::put(my_gb + c, tag, val);
         }
         signal_set(&sm.done[pr], m + 1, lane);
         pc.lap(WP_X3, lane);
       }
+      stamp(2);
     }
     cp_async_wait_all();
     __syncthreads();

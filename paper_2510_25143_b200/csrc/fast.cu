@@ -161,6 +161,28 @@ __device__ __forceinline__ void sl_predict2(const Src& s, int H, int W, int i,
   bilinear2(s, H, W, fi, fj, pu, pv);
 }
 
+// The RK2 branch of sl_predict2 only (d_inf <= d_max), branch-free so a
+// batch of samples overlaps its gathers; returns false (outputs unset) when
+// the sample needs the Euler-substep branch.
+template <typename Src>
+__device__ __forceinline__ bool sl_predict_rk2(const Src& s, int H, int W,
+                                               int i, int j, double cfl_x,
+                                               double cfl_y, double d_max,
+                                               int64_t* pu, int64_t* pv) {
+  double u0, v0;
+  s.get(i, j, u0, v0);
+  const double ax = __dmul_rn(fabs(u0), cfl_x), ay = __dmul_rn(fabs(v0), cfl_y);
+  const double d_inf = ay > ax ? ay : ax;
+  const double ih = __dsub_rn((double)i, __dmul_rn(__dmul_rn(0.5, v0), cfl_y));
+  const double jh = __dsub_rn((double)j, __dmul_rn(__dmul_rn(0.5, u0), cfl_x));
+  int64_t um, vm;
+  bilinear2(s, H, W, ih, jh, &um, &vm);
+  const double fi = __dsub_rn((double)i, __dmul_rn((double)vm, cfl_y));
+  const double fj = __dsub_rn((double)j, __dmul_rn((double)um, cfl_x));
+  bilinear2(s, H, W, fi, fj, pu, pv);
+  return d_inf <= d_max;
+}
+
 // ------------------------------------------------ first-touch block entropy
 // mop.py:118-138.  samp[sp] = |idx| of sample sp (sequence order: raster
 // (i, j), u then v) or -1 for an overflow sample.
@@ -244,65 +266,70 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
               int32_t* __restrict__ q0u, int32_t* __restrict__ q0v,
               int2* __restrict__ prevrec, uint8_t* __restrict__ codes_p,
               int* __restrict__ overflow) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wg >= (int64_t)p.H * p.nchunks) return;
-  const int i = (int)(wg / p.nchunks), bj = (int)(wg - (int64_t)i * p.nchunks);
+  // one 32x32 tile per CTA; every input value is converted to fixed point
+  // once, into shared memory with a one-pixel halo above and to the left
+  __shared__ int32_t so[2][33][33];   // orig(t)
+  __shared__ int32_t sp[2][33][33];   // recon(t-1) = orig(t-1) + err(t-1)
   const int H = p.H, W = p.W, Wp = p.Wp;
-  const int c0 = 32 * bj, j = c0 + lane;
-  const bool colok = j < W;
+  const int c0 = 32 * blockIdx.x, r0 = 32 * blockIdx.y;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int64_t HW = (int64_t)H * W;
   const F* uo = u + (int64_t)p.t * HW;
   const F* vo = v + (int64_t)p.t * HW;
   const bool has_prev = p.t > 0;
   const F* up_ = u + (int64_t)(p.t - 1) * HW;
   const F* vp_ = v + (int64_t)(p.t - 1) * HW;
-  const unsigned FULL = 0xffffffffu;
-  auto orig = [&](const F* f, int ii, int jj) -> int64_t {
-    return (ii >= 0 && jj >= 0) ? (int64_t)load_fixed(f, (int64_t)ii * W + jj, p.S) : 0;
-  };
-  auto prev = [&](const F* f, const int32_t* e, int ii, int jj) -> int64_t {
-    return (has_prev && ii >= 0 && jj >= 0)
-               ? (int64_t)load_fixed(f, (int64_t)ii * W + jj, p.S) +
-                     e[(int64_t)ii * Wp + jj]
-               : 0;
-  };
-  // lane l < 32 holds column j; lane 0 also fetches column c0-1
-  int64_t o_u = 0, o_v = 0, oU_u = 0, oU_v = 0, p_u = 0, p_v = 0, pU_u = 0, pU_v = 0;
-  if (colok) {
-    o_u = orig(uo, i, j); o_v = orig(vo, i, j);
-    oU_u = orig(uo, i - 1, j); oU_v = orig(vo, i - 1, j);
-    p_u = prev(up_, err_prev_u, i, j); p_v = prev(vp_, err_prev_v, i, j);
-    pU_u = prev(up_, err_prev_u, i - 1, j); pU_v = prev(vp_, err_prev_v, i - 1, j);
+#pragma unroll 5
+  for (int k = tid; k < 33 * 33; k += 256) {
+    const int rr = k / 33, cc = k - rr * 33;
+    const int i = r0 - 1 + rr, j = c0 - 1 + cc;
+    const bool ok = i >= 0 && j >= 0 && i < H && j < W;
+    const int64_t n = (int64_t)i * W + j;
+    so[0][rr][cc] = ok ? load_fixed(uo, n, p.S) : 0;
+    so[1][rr][cc] = ok ? load_fixed(vo, n, p.S) : 0;
+    int32_t pu = 0, pv = 0;
+    if (has_prev && ok) {
+      const int64_t m = (int64_t)i * Wp + j;
+      pu = load_fixed(up_, n, p.S) + __ldg(err_prev_u + m);
+      pv = load_fixed(vp_, n, p.S) + __ldg(err_prev_v + m);
+    }
+    sp[0][rr][cc] = pu;
+    sp[1][rr][cc] = pv;
   }
-  int64_t oL_u = __shfl_up_sync(FULL, o_u, 1), oL_v = __shfl_up_sync(FULL, o_v, 1);
-  int64_t oUL_u = __shfl_up_sync(FULL, oU_u, 1), oUL_v = __shfl_up_sync(FULL, oU_v, 1);
-  int64_t pL_u = __shfl_up_sync(FULL, p_u, 1), pL_v = __shfl_up_sync(FULL, p_v, 1);
-  int64_t pUL_u = __shfl_up_sync(FULL, pU_u, 1), pUL_v = __shfl_up_sync(FULL, pU_v, 1);
-  if (lane == 0) {
-    oL_u = orig(uo, i, c0 - 1); oL_v = orig(vo, i, c0 - 1);
-    oUL_u = orig(uo, i - 1, c0 - 1); oUL_v = orig(vo, i - 1, c0 - 1);
-    pL_u = prev(up_, err_prev_u, i, c0 - 1); pL_v = prev(vp_, err_prev_v, i, c0 - 1);
-    pUL_u = prev(up_, err_prev_u, i - 1, c0 - 1);
-    pUL_v = prev(vp_, err_prev_v, i - 1, c0 - 1);
-  }
-  const int64_t R_u = o_u - (oU_u + oL_u - oUL_u) - (p_u - pU_u - pL_u + pUL_u);
-  const int64_t R_v = o_v - (oU_v + oL_v - oUL_v) - (p_v - pU_v - pL_v + pUL_v);
-  const bool ovf = colok && (R_u >= 2147483647LL || R_u <= -2147483647LL ||
+  __syncthreads();
+  bool ovf = false;
+  const int j = c0 + tx;
+  const bool colok = j < W;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int rr = ty + 8 * q;
+    const int i = r0 + rr;
+    if (i >= H) break;
+    const int64_t R_u = (int64_t)so[0][rr + 1][tx + 1] -
+                        ((int64_t)so[0][rr][tx + 1] + so[0][rr + 1][tx] - so[0][rr][tx]) -
+                        ((int64_t)sp[0][rr + 1][tx + 1] - sp[0][rr][tx + 1] -
+                         sp[0][rr + 1][tx] + sp[0][rr][tx]);
+    const int64_t R_v = (int64_t)so[1][rr + 1][tx + 1] -
+                        ((int64_t)so[1][rr][tx + 1] + so[1][rr + 1][tx] - so[1][rr][tx]) -
+                        ((int64_t)sp[1][rr + 1][tx + 1] - sp[1][rr][tx + 1] -
+                         sp[1][rr + 1][tx] + sp[1][rr][tx]);
+    const bool o = colok && (R_u >= 2147483647LL || R_u <= -2147483647LL ||
                              R_v >= 2147483647LL || R_v <= -2147483647LL);
-  if (__any_sync(FULL, ovf) && lane == 0) atomicOr(overflow, 1);
-  const int64_t pr = (int64_t)i * Wp + j;
-  const int cd = colok ? codes[(int64_t)p.t * HW + (int64_t)i * W + j] : CODE_LOSSLESS;
-  // the chain's split R0 = Q0*2e + rho (e < 2^28 on this path)
-  const int32_t e = (int32_t)p.lad.e[cd];
-  const double inv = p.lad.inv2e[cd];
-  const int32_t ru = colok ? (int32_t)R_u : 0, rv = colok ? (int32_t)R_v : 0;
-  a0[pr] = ru;
-  a1[pr] = rv;
-  q0u[pr] = (e != 0 && !ovf) ? quant32(ru, e, inv) : 0;
-  q0v[pr] = (e != 0 && !ovf) ? quant32(rv, e, inv) : 0;
-  if (has_prev) prevrec[pr] = make_int2((int32_t)p_u, (int32_t)p_v);
-  codes_p[pr] = (uint8_t)cd;
+    ovf |= o;
+    const int64_t pr = (int64_t)i * Wp + j;
+    const int cd = colok ? codes[(int64_t)p.t * HW + (int64_t)i * W + j] : CODE_LOSSLESS;
+    // the chain's split R0 = Q0*2e + rho (e < 2^28 on this path)
+    const int32_t e = (int32_t)p.lad.e[cd];
+    const double inv = p.lad.inv2e[cd];
+    const int32_t ru = colok ? (int32_t)R_u : 0, rv = colok ? (int32_t)R_v : 0;
+    a0[pr] = ru;
+    a1[pr] = rv;
+    q0u[pr] = (e != 0 && !o) ? quant32(ru, e, inv) : 0;
+    q0v[pr] = (e != 0 && !o) ? quant32(rv, e, inv) : 0;
+    if (has_prev) prevrec[pr] = make_int2(sp[0][rr + 1][tx + 1], sp[1][rr + 1][tx + 1]);
+    codes_p[pr] = (uint8_t)cd;
+  }
+  if (__syncthreads_or(ovf) && tid == 0) atomicOr(overflow, 1);
 }
 
 // MoP trial step with one step size e for the whole block (mop.py:88-110):
@@ -401,16 +428,38 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const F* vo = v + (int64_t)p.t * HW;
   const PairPlane src{prevrec, Wp};
   const int64_t tau = p.tau;
-  for (int sidx = lane; sidx < nsx * nsy; sidx += 32) {
-    const int si = sidx / nsx, sj = sidx - si * nsx;
-    const int i = r0 + si * p.stride, jj = c0 + sj * p.stride;
-    int64_t pr_u, pr_v;
-    sl_predict2(src, H, W, i, jj, p.cfl_x, p.cfl_y, p.d_max, p.n_max, &pr_u, &pr_v);
-    const int64_t ru = (int64_t)load_fixed(uo, (int64_t)i * W + jj, p.S) - pr_u;
-    const int64_t rv = (int64_t)load_fixed(vo, (int64_t)i * W + jj, p.S) - pr_v;
-    const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
-    sm.samp[2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
-    sm.samp[2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
+  // NB samples per lane in lockstep: the departure-point gathers of the
+  // batch are independent and overlap; samples needing Euler substeps
+  // (d_inf > d_max) take the general path afterwards
+  constexpr int NB = 4;
+  const int nsamp = nsx * nsy;
+  for (int base = 0; base < nsamp; base += 32 * NB) {
+    int64_t pr_u[NB], pr_v[NB];
+    int si_i[NB], si_j[NB];
+    bool slow[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+      const int sidx = min(base + lane + 32 * b, nsamp - 1);
+      const int si = sidx / nsx, sj = sidx - si * nsx;
+      si_i[b] = r0 + si * p.stride;
+      si_j[b] = c0 + sj * p.stride;
+      slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
+                                p.d_max, &pr_u[b], &pr_v[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+      const int sidx = base + lane + 32 * b;
+      if (sidx >= nsamp) continue;
+      const int i = si_i[b], jj = si_j[b];
+      if (slow[b])
+        sl_predict2(src, H, W, i, jj, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
+                    &pr_u[b], &pr_v[b]);
+      const int64_t ru = (int64_t)load_fixed(uo, (int64_t)i * W + jj, p.S) - pr_u[b];
+      const int64_t rv = (int64_t)load_fixed(vo, (int64_t)i * W + jj, p.S) - pr_v[b];
+      const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
+      sm.samp[2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
+      sm.samp[2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
+    }
   }
   __syncwarp();
   const double r_sl = block_rate(sm.samp, ns, sm.first, sm.cnt, log2tab,
@@ -433,9 +482,9 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
                uint32_t* __restrict__ symw, uint16_t* __restrict__ qd,
                int32_t* __restrict__ row_ll) {
   const int lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wg >= (int64_t)p.H * p.nchunks) return;
-  const int i = (int)(wg / p.nchunks), bj = (int)(wg - (int64_t)i * p.nchunks);
+  // grid (chunk groups of 8, rows): warp = one (row, 32-column chunk)
+  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (bj >= p.nchunks) return;
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
   const int j = 32 * bj + lane;
   const bool colok = j < W;
@@ -509,9 +558,9 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
                 int32_t* __restrict__ a0, int32_t* __restrict__ a1,
                 uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v) {
   const int lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wg >= (int64_t)p.H * p.nchunks) return;
-  const int i = (int)(wg / p.nchunks), bj = (int)(wg - (int64_t)i * p.nchunks);
+  // grid (chunk groups of 8, rows): warp = one (row, 32-column chunk)
+  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (bj >= p.nchunks) return;
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
   const int c0 = 32 * bj, j = c0 + lane;
   const bool colok = j < W;
@@ -592,9 +641,8 @@ enc_sym_scatter_kernel(const uint16_t* __restrict__ s0,
                        int Wp, int nchunks, uint16_t* __restrict__ qd,
                        int32_t* __restrict__ row_ll) {
   const int lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wg >= (int64_t)H * nchunks) return;
-  const int i = (int)(wg / nchunks), bj = (int)(wg - (int64_t)i * nchunks);
+  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (bj >= nchunks) return;
   const int64_t pb = (int64_t)i * nchunks + bj;
   const uint32_t sw = symw[pb];
   if (sw == 0) return;   // warp-uniform
@@ -648,8 +696,8 @@ cudaError_t launch_enc_r0(const F* u, const F* v, const uint8_t* codes,
                           const PrepParams& p, int32_t* a0, int32_t* a1,
                           int32_t* q0u, int32_t* q0v, int32_t* prevrec,
                           uint8_t* codes_p, int* overflow, cudaStream_t st) {
-  const int64_t nw = (int64_t)p.H * p.nchunks;
-  enc_r0_kernel<F><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+  const dim3 grid(p.nchunks, p.nby);
+  enc_r0_kernel<F><<<grid, 256, 0, st>>>(
       u, v, codes, eu, ev, p, a0, a1, q0u, q0v,
       reinterpret_cast<int2*>(prevrec), codes_p, overflow);
   return cudaGetLastError();
@@ -678,8 +726,8 @@ cudaError_t launch_enc_pix(const F* u, const F* v, const uint8_t* codes_p,
                            uint32_t* pin_u, uint32_t* pin_v, uint32_t* nlw,
                            uint32_t* symw, uint16_t* qd, int32_t* row_ll,
                            cudaStream_t st) {
-  const int64_t nw = (int64_t)p.H * p.nchunks;
-  enc_pix_kernel<F><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+  const dim3 grid((p.nchunks + 7) / 8, p.H);
+  enc_pix_kernel<F><<<grid, 256, 0, st>>>(
       u, v, codes_p, reinterpret_cast<const int2*>(prevrec), qd_row_off,
       pre_nl, p, modes_t, a0, a1, pin_u, pin_v, nlw, symw, qd, row_ll);
   return cudaGetLastError();
@@ -694,8 +742,8 @@ cudaError_t launch_dec_prep(const uint8_t* codes, const SYM* qd,
                             const int32_t* pre_ll, const PrepParams& p,
                             int32_t* a0, int32_t* a1, uint32_t* pin_u,
                             uint32_t* pin_v, cudaStream_t st) {
-  const int64_t nw = (int64_t)p.H * p.nchunks;
-  dec_prep_kernel<SYM><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+  const dim3 grid((p.nchunks + 7) / 8, p.H);
+  dec_prep_kernel<SYM><<<grid, 256, 0, st>>>(
       codes, qd, ll, modes_t, ru, rv, qd_row_off, ll_row_off, pre_nl, pre_ll,
       p, a0, a1, pin_u, pin_v);
   return cudaGetLastError();
@@ -715,8 +763,8 @@ cudaError_t launch_sym_scatter(const uint16_t* s0, const uint16_t* s1,
                                const int32_t* pre_nl, int H, int W, int Wp,
                                int nchunks, uint16_t* qd, int32_t* row_ll,
                                cudaStream_t st) {
-  const int64_t nw = (int64_t)H * nchunks;
-  enc_sym_scatter_kernel<<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+  const dim3 grid((nchunks + 7) / 8, H);
+  enc_sym_scatter_kernel<<<grid, 256, 0, st>>>(
       s0, s1, nlw, symw, qd_row_off, pre_nl, H, W, Wp, nchunks, qd, row_ll);
   return cudaGetLastError();
 }

@@ -8,7 +8,7 @@ __global__ void enc_sweep(const int32_t* in, int nblk, uint32_t pm, long long* o
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   int32_t rr[32], qq[32], ee[32];
-  for (int jj = 0; jj < 32; jj++) { rr[jj] = in[lane * 32 + jj] % 100000; qq[jj] = in[lane * 32 + jj] % 7; ee[jj] = 1000 + (in[jj] & 3); }
+  for (int jj = 0; jj < 32; jj++) { rr[jj] = in[lane * 32 + jj] % 100000; qq[jj] = in[lane * 32 + jj] % 7; ee[jj] = 1000 + (in[lane * 32 + jj] & 3); }
   int32_t l = 0, ul = 0, b = in[lane] % 100;
   const int32_t radius = in[5] | 32768;
   const bool lane0 = lane == 0;
