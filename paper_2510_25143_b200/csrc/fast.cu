@@ -350,123 +350,147 @@ __device__ __forceinline__ int32_t trial_step(int32_t rho, int32_t q0,
   return esc ? 0 : (q - q0) * 2 * e - y;
 }
 
-constexpr int MOP_WARPS = 4;
+// One CTA of 4 warps per 32x32 block: warps 0 / 1 run the Lorenzo trial of
+// u / v (lane = row, skewed sweep), warps 2 / 3 the semi-Lagrangian trial at
+// the stride samples; then warp 0 rates the Lorenzo samples while warp 2
+// rates the SL samples (first-touch order, mop.py:118-138).
 struct MopSmem {
-  int32_t r0[2][32][32];   // [comp][row][col]: lane = row reads col s-lane
-  int32_t samp[512];
-  int32_t first[ETB];
-  int32_t cnt[ETB];
+  int32_t r0[2][32][33];   // [comp][row][col] R0 tile, then rho
+  int32_t q0[2][32][33];   // [comp][row][col] Q0 = rha(R0 / 2 tau')
+  int32_t samp[2][512];    // [trial] |idx| per sample (-1: escape)
+  int32_t first[2][ETB];
+  int32_t cnt[2][ETB];
+  double rate[2];
 };
 
 template <typename F>
-__global__ void __launch_bounds__(32 * MOP_WARPS)
+__global__ void __launch_bounds__(128, 8)
 enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
                const int32_t* __restrict__ a0, const int32_t* __restrict__ a1,
                const int2* __restrict__ prevrec, PrepParams p,
                const double* __restrict__ log2tab,
                uint8_t* __restrict__ modes_t) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ MopSmem sm;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  MopSmem& sm = reinterpret_cast<MopSmem*>(smem_raw)[wid];
-  const int blk = blockIdx.x * MOP_WARPS + wid;
-  if (blk >= p.nbx * p.nby) return;
-  const int bi = blk / p.nbx, bj = blk - bi * p.nbx;
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  const int blk = bi * p.nbx + bj;
   const int H = p.H, W = p.W, Wp = p.Wp;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, H - r0), ncl = min(32, W - c0);
   const unsigned FULL = 0xffffffffu;
-  // R0 tile, all rows in flight
-#pragma unroll 8
-  for (int r = 0; r < 32; r++) {
-    const bool rv = r < nr;
-    const int64_t k = (int64_t)(r0 + (rv ? r : 0)) * Wp + c0 + lane;
-    cp_async<4>(&sm.r0[0][r][lane], a0 + k, rv);
-    cp_async<4>(&sm.r0[1][r][lane], a1 + k, rv);
-  }
-  cp_async_commit();
-  for (int k = lane; k < ETB; k += 32) { sm.first[k] = 0x7fffffff; sm.cnt[k] = 0; }
   const int nsx = (ncl + p.stride - 1) / p.stride;
   const int nsy = (nr + p.stride - 1) / p.stride;
-  const int ns = 2 * nsx * nsy;
+  const int nsamp = nsx * nsy;
+  const int ns = 2 * nsamp;
   const int32_t e = (int32_t)p.tau;     // fast path: tau' < 2^28
   const double inv = 1.0 / (double)(2 * p.tau);
   const int32_t radius = p.radius;
-  cp_async_wait_all();
-  __syncwarp();
-  // Lorenzo trial (lane = row), block-local errors, skewed sweep
-  {
-    int32_t eL[2] = {0, 0}, eUL[2] = {0, 0};
+  const int64_t tau = p.tau;
+  // R0 tile (all 4 warps; lane = column)
+  for (int r = wid; r < 32; r += 4) {
+    const bool rv = r < nr;
+    const int64_t k = (int64_t)(r0 + (rv ? r : 0)) * Wp + c0 + lane;
+    sm.r0[0][r][lane] = rv ? __ldg(a0 + k) : 0;
+    sm.r0[1][r][lane] = rv ? __ldg(a1 + k) : 0;
+  }
+  for (int k = threadIdx.x; k < 2 * ETB; k += 128) {
+    (&sm.first[0][0])[k] = 0x7fffffff;
+    (&sm.cnt[0][0])[k] = 0;
+  }
+  __syncthreads();
+  if (wid < 2) {
+    // split R0 = Q0*2e + rho for the whole tile first (independent per
+    // pixel, lane = column), so the sweep below is only the recurrence
+    {
+      const int comp = wid;
+#pragma unroll 8
+      for (int r = 0; r < 32; r++) {
+        const int32_t x0 = sm.r0[comp][r][lane];
+        const int32_t q0 = quant32(x0, e, inv);
+        sm.q0[comp][r][lane] = q0;
+        sm.r0[comp][r][lane] = x0 - q0 * 2 * e;
+      }
+      __syncwarp();
+    }
+    // Lorenzo trial of component wid, block-local errors (mop.py:88-110)
+    const int comp = wid;
     const int i = lane;
     const bool rowok = i < nr;
-    for (int s = 0; s < ncl + 31; s++) {
+    int32_t eL = 0, eUL = 0;
+    // sample bookkeeping without divisions in the loop: row i is a sample
+    // row iff i % stride == 0; the column phase advances with jj
+    const bool srow = (i % p.stride) == 0;
+    const int sbase = 2 * ((i / p.stride) * nsx) + comp;
+    int jm = 0, jq = 0;   // jj % stride, jj / stride once jj >= 0
+#pragma unroll 7
+    for (int s = 0; s < 63; s++) {
       const int jj = s - lane;
       const bool act = rowok && jj >= 0 && jj < ncl;
-      const bool smp = act && (i % p.stride == 0) && (jj % p.stride == 0);
-      const int sidx = smp ? 2 * ((i / p.stride) * nsx + jj / p.stride) : 0;
+      const int32_t rho = act ? sm.r0[comp][i][jj] : 0;
+      const int32_t q0 = act ? sm.q0[comp][i][jj] : 0;
+      const int32_t up = __shfl_up_sync(FULL, eL, 1);
+      const int32_t eU = (lane == 0 || !act) ? 0 : up;
+      const int32_t d = eU + (jj > 0 ? eL : 0) - ((jj > 0 && lane > 0) ? eUL : 0);
+      int32_t qa;
+      const int32_t er = trial_step(rho, q0, e, d, radius, &qa);
+      eUL = eU;
+      if (act) eL = er;
+      if (act && srow && jm == 0) sm.samp[0][sbase + 2 * jq] = qa;
+      if (jj >= 0) {
+        if (++jm == p.stride) { jm = 0; jq++; }
+      }
+    }
+  } else {
+    // semi-Lagrangian trial at the stride samples, 64 threads; samples of
+    // a thread in lockstep so their departure-point gathers overlap
+    const int64_t HW = (int64_t)H * W;
+    const F* uo = u + (int64_t)p.t * HW;
+    const F* vo = v + (int64_t)p.t * HW;
+    const PairPlane src{prevrec, Wp};
+    const int tt = threadIdx.x - 64;
+    constexpr int NB = 2;   // 64 threads x 2 x 2 rounds = 256 samples (stride 2)
+    for (int base = 0; base < nsamp; base += 64 * NB) {
+      int64_t pr_u[NB], pr_v[NB];
+      int si_i[NB], si_j[NB];
+      bool slow[NB];
 #pragma unroll
-      for (int comp = 0; comp < 2; comp++) {
-        const int32_t x0 = act ? sm.r0[comp][i][jj] : 0;
-        const int32_t up = __shfl_up_sync(FULL, eL[comp], 1);
-        const int32_t eU = (lane == 0 || !act) ? 0 : up;
-        const int32_t q0 = quant32(x0, e, inv);
-        const int32_t rho = x0 - q0 * 2 * e;
-        const int32_t d = eU + (jj > 0 ? eL[comp] : 0) - ((jj > 0 && lane > 0) ? eUL[comp] : 0);
-        int32_t qa;
-        const int32_t er = trial_step(rho, q0, e, d, radius, &qa);
-        eUL[comp] = eU;
-        if (act) eL[comp] = er;
-        if (smp) sm.samp[sidx + comp] = qa;
+      for (int b = 0; b < NB; b++) {
+        const int sidx = min(base + tt + 64 * b, nsamp - 1);
+        const int si = sidx / nsx, sj = sidx - si * nsx;
+        si_i[b] = r0 + si * p.stride;
+        si_j[b] = c0 + sj * p.stride;
+        slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
+                                  p.d_max, &pr_u[b], &pr_v[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const int sidx = base + tt + 64 * b;
+        if (sidx >= nsamp) continue;
+        const int i = si_i[b], jj = si_j[b];
+        if (slow[b])
+          sl_predict2(src, H, W, i, jj, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
+                      &pr_u[b], &pr_v[b]);
+        const int64_t ru = (int64_t)load_fixed(uo, (int64_t)i * W + jj, p.S) - pr_u[b];
+        const int64_t rv = (int64_t)load_fixed(vo, (int64_t)i * W + jj, p.S) - pr_v[b];
+        const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
+        sm.samp[1][2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
+        sm.samp[1][2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
       }
     }
   }
-  __syncwarp();
-  const double r_lor = block_rate(sm.samp, ns, sm.first, sm.cnt, log2tab,
-                                  p.lam, p.rmeta, lane);
-  // semi-Lagrangian trial at the stride samples
-  const int64_t HW = (int64_t)H * W;
-  const F* uo = u + (int64_t)p.t * HW;
-  const F* vo = v + (int64_t)p.t * HW;
-  const PairPlane src{prevrec, Wp};
-  const int64_t tau = p.tau;
-  // NB samples per lane in lockstep: the departure-point gathers of the
-  // batch are independent and overlap; samples needing Euler substeps
-  // (d_inf > d_max) take the general path afterwards
-  constexpr int NB = 4;
-  const int nsamp = nsx * nsy;
-  for (int base = 0; base < nsamp; base += 32 * NB) {
-    int64_t pr_u[NB], pr_v[NB];
-    int si_i[NB], si_j[NB];
-    bool slow[NB];
-#pragma unroll
-    for (int b = 0; b < NB; b++) {
-      const int sidx = min(base + lane + 32 * b, nsamp - 1);
-      const int si = sidx / nsx, sj = sidx - si * nsx;
-      si_i[b] = r0 + si * p.stride;
-      si_j[b] = c0 + sj * p.stride;
-      slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
-                                p.d_max, &pr_u[b], &pr_v[b]);
-    }
-#pragma unroll
-    for (int b = 0; b < NB; b++) {
-      const int sidx = base + lane + 32 * b;
-      if (sidx >= nsamp) continue;
-      const int i = si_i[b], jj = si_j[b];
-      if (slow[b])
-        sl_predict2(src, H, W, i, jj, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
-                    &pr_u[b], &pr_v[b]);
-      const int64_t ru = (int64_t)load_fixed(uo, (int64_t)i * W + jj, p.S) - pr_u[b];
-      const int64_t rv = (int64_t)load_fixed(vo, (int64_t)i * W + jj, p.S) - pr_v[b];
-      const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
-      sm.samp[2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
-      sm.samp[2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
-    }
+  __syncthreads();
+  if (wid == 0 || wid == 2) {
+    const int tr = wid >> 1;
+    const double r = block_rate(sm.samp[tr], ns, sm.first[tr], sm.cnt[tr],
+                                log2tab, p.lam, p.rmeta, lane);
+    if (lane == 0) sm.rate[tr] = r;
   }
-  __syncwarp();
-  const double r_sl = block_rate(sm.samp, ns, sm.first, sm.cnt, log2tab,
-                                 p.lam, p.rmeta, lane);
-  const int mode =
-      (r_lor > 0.0 && __ddiv_rn(__dsub_rn(r_lor, r_sl), r_lor) > p.theta) ? 1 : 0;
-  if (lane == 0) modes_t[blk] = (uint8_t)mode;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double r_lor = sm.rate[0], r_sl = sm.rate[1];
+    modes_t[blk] =
+        (r_lor > 0.0 && __ddiv_rn(__dsub_rn(r_lor, r_sl), r_lor) > p.theta) ? 1 : 0;
+  }
 }
 
 template <typename F>
@@ -542,8 +566,11 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
 }
 
 // ---------------------------------------------------------- decoder prep
-// warp per (row, 32-column chunk): pins (lossless, escapes, semi-Lagrangian
-// pixels) and A = Pd + (sym-radius)*2e for the others
+// One 32x32 tile per CTA (8 warps x 4 rows, lane = column): the frame t-1
+// reconstruction of the tile and its halo is staged in shared memory once;
+// per row: pins (lossless, escapes, semi-Lagrangian pixels) and
+// A = Pd + (sym-radius)*2e for the others.  The four rows of a warp are
+// processed together so their stream loads overlap.
 template <typename SYM>
 __global__ void __launch_bounds__(256)
 dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
@@ -557,73 +584,101 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
                 const int32_t* __restrict__ pre_ll, PrepParams p,
                 int32_t* __restrict__ a0, int32_t* __restrict__ a1,
                 uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v) {
-  const int lane = threadIdx.x & 31;
-  // grid (chunk groups of 8, rows): warp = one (row, 32-column chunk)
-  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (bj >= p.nchunks) return;
+  __shared__ int32_t sp[2][33][33];   // recon(t-1), rows r0-1.., cols c0-1..
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
-  const int c0 = 32 * bj, j = c0 + lane;
-  const bool colok = j < W;
+  const int bj = blockIdx.x, bi = blockIdx.y;
+  const int c0 = 32 * bj, r0 = 32 * bi;
+  const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
   const int64_t HW = (int64_t)H * W;
   const bool has_prev = p.t > 0;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  const bool sl_blk = has_prev && modes_t && modes_t[(i >> 5) * p.nbx + bj] == 1;
-  auto prevv = [&](const int32_t* r, int ii, int jj) -> uint32_t {
-    return (has_prev && ii >= 0 && jj >= 0) ? (uint32_t)__ldg(r + (int64_t)ii * Wp + jj) : 0u;
-  };
-  uint32_t pp_u = 0, pp_v = 0, pU_u = 0, pU_v = 0;
-  if (colok) {
-    pp_u = prevv(rec_prev_u, i, j); pp_v = prevv(rec_prev_v, i, j);
-    pU_u = prevv(rec_prev_u, i - 1, j); pU_v = prevv(rec_prev_v, i - 1, j);
+  const bool sl_blk = has_prev && modes_t && modes_t[bi * p.nbx + bj] == 1;
+  {
+#pragma unroll 5
+    for (int k = tid; k < 33 * 33; k += 256) {
+      const int rr = k / 33, cc = k - rr * 33;
+      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
+      const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
+      const int64_t m = (int64_t)i * Wp + j;
+      sp[0][rr][cc] = ok ? __ldg(rec_prev_u + m) : 0;
+      sp[1][rr][cc] = ok ? __ldg(rec_prev_v + m) : 0;
+    }
   }
-  uint32_t tl_u = __shfl_up_sync(FULL, pp_u, 1), tl_v = __shfl_up_sync(FULL, pp_v, 1);
-  uint32_t tul_u = __shfl_up_sync(FULL, pU_u, 1), tul_v = __shfl_up_sync(FULL, pU_v, 1);
-  if (lane == 0) {
-    tl_u = prevv(rec_prev_u, i, c0 - 1); tl_v = prevv(rec_prev_v, i, c0 - 1);
-    tul_u = prevv(rec_prev_u, i - 1, c0 - 1); tul_v = prevv(rec_prev_v, i - 1, c0 - 1);
+  __syncthreads();
+  const int j = c0 + lane;
+  const bool colok = j < W;
+  constexpr int NR = 4;
+  int cd[NR];
+  int64_t qrow[NR], lrow[NR];
+  int32_t pnl[NR], pll[NR];
+  bool rv[NR];
+#pragma unroll
+  for (int q = 0; q < NR; q++) {
+    const int i = r0 + ty + 8 * q;
+    rv[q] = i < H;
+    const int ic = rv[q] ? i : r0;
+    const int64_t row = (int64_t)p.t * H + ic;
+    cd[q] = (colok && rv[q]) ? codes[(int64_t)p.t * HW + (int64_t)ic * W + j] : CODE_LOSSLESS;
+    qrow[q] = qd_row_off[row];
+    lrow[q] = ll_row_off[row];
+    pnl[q] = pre_nl[row * nchunks + bj];
+    pll[q] = pre_ll[row * nchunks + bj];
   }
-  const int64_t row = (int64_t)p.t * H + i;
-  const int cd = colok ? codes[(int64_t)p.t * HW + (int64_t)i * W + j] : CODE_LOSSLESS;
-  const int64_t e = p.lad.e[cd];
-  const bool nl = colok && e != 0;
-  const unsigned bnl = __ballot_sync(FULL, nl);
-  int64_t syu = 0, syv = 0;
-  if (nl) {
-    const int64_t q = qd_row_off[row] +
-                      2 * ((int64_t)pre_nl[row * nchunks + bj] + __popc(bnl & lt));
-    syu = qd[q];
-    syv = qd[q + 1];
+  int64_t syu[NR], syv[NR];
+  unsigned bnl[NR];
+#pragma unroll
+  for (int q = 0; q < NR; q++) {
+    const bool nl = colok && p.lad.e[cd[q]] != 0;
+    bnl[q] = __ballot_sync(FULL, nl);
+    syu[q] = 0; syv[q] = 0;
+    if (nl) {
+      const int64_t k = qrow[q] + 2 * ((int64_t)pnl[q] + __popc(bnl[q] & lt));
+      syu[q] = qd[k];
+      syv[q] = qd[k + 1];
+    }
   }
-  const bool eu = (colok && !nl) || (nl && syu == 0);
-  const bool ev = (colok && !nl) || (nl && syv == 0);
-  const unsigned b_eu = __ballot_sync(FULL, eu);
-  const unsigned b_ev = __ballot_sync(FULL, ev);
-  int64_t lidx = ll_row_off[row] + pre_ll[row * nchunks + bj] +
-                 __popc(b_eu & lt) + __popc(b_ev & lt);
-  const int64_t two_e = 2 * e;
-  const int64_t qu = syu - p.radius, qv = syv - p.radius;
-  uint32_t val_u = (pp_u - pU_u - tl_u + tul_u) + (uint32_t)(qu * two_e);
-  uint32_t val_v = (pp_v - pU_v - tl_v + tul_v) + (uint32_t)(qv * two_e);
-  const bool sl = nl && sl_blk;
-  if (sl) {
-    int64_t pr_u, pr_v;
-    sl_predict2(TwoPlanes{rec_prev_u, rec_prev_v, Wp}, H, W, i, j, p.cfl_x,
-                p.cfl_y, p.d_max, p.n_max, &pr_u, &pr_v);
-    val_u = (uint32_t)(pr_u + qu * two_e);
-    val_v = (uint32_t)(pr_v + qv * two_e);
-  }
-  if (eu) { val_u = (uint32_t)ll[lidx]; lidx++; }
-  if (ev) val_v = (uint32_t)ll[lidx];
-  const unsigned b_pu = __ballot_sync(FULL, colok && (eu || sl));
-  const unsigned b_pv = __ballot_sync(FULL, colok && (ev || sl));
-  const int64_t pr = (int64_t)i * Wp + j;
-  a0[pr] = colok ? (int32_t)val_u : 0;
-  a1[pr] = colok ? (int32_t)val_v : 0;
-  if (lane == 0) {
-    const int64_t pb = (int64_t)i * nchunks + bj;
-    pin_u[pb] = b_pu;
-    pin_v[pb] = b_pv;
+#pragma unroll
+  for (int q = 0; q < NR; q++) {
+    if (!rv[q]) continue;   // warp-uniform
+    const int rr = ty + 8 * q;
+    const int i = r0 + rr;
+    const int64_t e = p.lad.e[cd[q]];
+    const bool nl = colok && e != 0;
+    const bool eu = (colok && !nl) || (nl && syu[q] == 0);
+    const bool ev = (colok && !nl) || (nl && syv[q] == 0);
+    const unsigned b_eu = __ballot_sync(FULL, eu);
+    const unsigned b_ev = __ballot_sync(FULL, ev);
+    int64_t lidx = lrow[q] + pll[q] + __popc(b_eu & lt) + __popc(b_ev & lt);
+    const int64_t two_e = 2 * e;
+    const int64_t qu = syu[q] - p.radius, qv = syv[q] - p.radius;
+    // Pd = p - pU - pL + pUL of the previous frame (zero outside)
+    const uint32_t pd_u = (uint32_t)sp[0][rr + 1][lane + 1] - (uint32_t)sp[0][rr][lane + 1] -
+                          (uint32_t)sp[0][rr + 1][lane] + (uint32_t)sp[0][rr][lane];
+    const uint32_t pd_v = (uint32_t)sp[1][rr + 1][lane + 1] - (uint32_t)sp[1][rr][lane + 1] -
+                          (uint32_t)sp[1][rr + 1][lane] + (uint32_t)sp[1][rr][lane];
+    uint32_t val_u = pd_u + (uint32_t)(qu * two_e);
+    uint32_t val_v = pd_v + (uint32_t)(qv * two_e);
+    const bool sl = nl && sl_blk;
+    if (sl) {
+      int64_t pr_u, pr_v;
+      sl_predict2(TwoPlanes{rec_prev_u, rec_prev_v, Wp}, H, W, i, j, p.cfl_x,
+                  p.cfl_y, p.d_max, p.n_max, &pr_u, &pr_v);
+      val_u = (uint32_t)(pr_u + qu * two_e);
+      val_v = (uint32_t)(pr_v + qv * two_e);
+    }
+    if (eu) { val_u = (uint32_t)ll[lidx]; lidx++; }
+    if (ev) val_v = (uint32_t)ll[lidx];
+    const unsigned b_pu = __ballot_sync(FULL, colok && (eu || sl));
+    const unsigned b_pv = __ballot_sync(FULL, colok && (ev || sl));
+    const int64_t pr = (int64_t)i * Wp + j;
+    a0[pr] = colok ? (int32_t)val_u : 0;
+    a1[pr] = colok ? (int32_t)val_v : 0;
+    if (lane == 0) {
+      const int64_t pb = (int64_t)i * nchunks + bj;
+      pin_u[pb] = b_pu;
+      pin_v[pb] = b_pv;
+    }
   }
 }
 
@@ -667,15 +722,15 @@ emit_frame_kernel(const int32_t* __restrict__ ru, const int32_t* __restrict__ rv
                   int H, int W, int Wp, double inv_S, double* __restrict__ ou,
                   double* __restrict__ ov, int64_t* __restrict__ fu,
                   int64_t* __restrict__ fv) {
-  const int64_t n = (int64_t)H * W;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = k / W, j = k - i * W;
-    const int32_t a = __ldg(ru + i * Wp + j), b = __ldg(rv + i * Wp + j);
-    ou[k] = __dmul_rn((double)a, inv_S);
-    ov[k] = __dmul_rn((double)b, inv_S);
-    if (fu) { fu[k] = a; fv[k] = b; }
-  }
+  // grid (column groups of 256, rows): coalesced, no divisions
+  const int i = blockIdx.y;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= W) return;
+  const int32_t a = __ldg(ru + (int64_t)i * Wp + j), b = __ldg(rv + (int64_t)i * Wp + j);
+  const int64_t k = (int64_t)i * W + j;
+  ou[k] = __dmul_rn((double)a, inv_S);
+  ov[k] = __dmul_rn((double)b, inv_S);
+  if (fu) { fu[k] = a; fv[k] = b; }
 }
 
 // ------------------------------------------------------------ launchers
@@ -708,12 +763,7 @@ cudaError_t launch_enc_mop(const F* u, const F* v, const int32_t* a0,
                            const int32_t* a1, const int32_t* prevrec,
                            const PrepParams& p, const double* log2tab,
                            uint8_t* modes_t, cudaStream_t st) {
-  const int nblk = p.nbx * p.nby;
-  const size_t smem = MOP_WARPS * sizeof(MopSmem);
-  cudaError_t ce = cudaFuncSetAttribute(
-      enc_mop_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (ce != cudaSuccess) return ce;
-  enc_mop_kernel<F><<<(nblk + MOP_WARPS - 1) / MOP_WARPS, 32 * MOP_WARPS, smem, st>>>(
+  enc_mop_kernel<F><<<dim3(p.nbx, p.nby), 128, 0, st>>>(
       u, v, a0, a1, reinterpret_cast<const int2*>(prevrec), p, log2tab, modes_t);
   return cudaGetLastError();
 }
@@ -742,7 +792,7 @@ cudaError_t launch_dec_prep(const uint8_t* codes, const SYM* qd,
                             const int32_t* pre_ll, const PrepParams& p,
                             int32_t* a0, int32_t* a1, uint32_t* pin_u,
                             uint32_t* pin_v, cudaStream_t st) {
-  const dim3 grid((p.nchunks + 7) / 8, p.H);
+  const dim3 grid(p.nchunks, p.nby);
   dec_prep_kernel<SYM><<<grid, 256, 0, st>>>(
       codes, qd, ll, modes_t, ru, rv, qd_row_off, ll_row_off, pre_nl, pre_ll,
       p, a0, a1, pin_u, pin_v);
@@ -753,7 +803,8 @@ cudaError_t launch_emit_frame(const int32_t* ru, const int32_t* rv, int H,
                               int W, int Wp, double inv_S, double* ou,
                               double* ov, int64_t* fu, int64_t* fv,
                               cudaStream_t st) {
-  emit_frame_kernel<<<1184, 256, 0, st>>>(ru, rv, H, W, Wp, inv_S, ou, ov, fu, fv);
+  emit_frame_kernel<<<dim3((W + 255) / 256, H), 256, 0, st>>>(ru, rv, H, W, Wp,
+                                                              inv_S, ou, ov, fu, fv);
   return cudaGetLastError();
 }
 
