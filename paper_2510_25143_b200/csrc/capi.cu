@@ -10,9 +10,6 @@
 #include <cstring>
 #include <string>
 #include <vector>
-#include <chrono>
-#include <algorithm>
-#include <cmath>
 
 #include "../../include/vfcp_b200.h"
 #include "chain.cuh"
@@ -84,7 +81,7 @@ cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
                             const int32_t*, const PrepParams&, int32_t*,
                             int32_t*, uint32_t*, uint32_t*, cudaStream_t);
 template <bool ENC>
-cudaError_t launch_chain(const ChainIO&, int, cudaStream_t, int*);
+cudaError_t launch_chain(const ChainIO&, int, cudaStream_t);
 cudaError_t launch_emit_frame(const int32_t*, const int32_t*, int, int, int,
                               double, double*, double*, int64_t*, int64_t*,
                               cudaStream_t);
@@ -422,9 +419,6 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
   pp.mop = p->predictor == VFCP_PRED_MOP && t >= 1 && p->tau > 0;
   pp.force_sl = p->predictor == VFCP_PRED_SL && t >= 1 && p->tau > 0;
   pp.lad = lad;
-  pp.gate = nullptr;
-  pp.gate_target = 0;
-  pp.gate_reach = 0;
   return pp;
 }
 
@@ -451,74 +445,6 @@ void print_stamps(const char* tag, unsigned long long* d, int H, cudaStream_t st
   }
 }
 
-// ---- frame overlap ---------------------------------------
-// Frame t+1's prepare kernels run on a side stream while frame t's chain is
-// in flight; each prepare tile waits (prep_gate) for the chain strips its
-// inputs come from.  A prepare kernel is launched only once every CTA of the
-// chain it waits on is resident -- the chain counts its CTAs into
-// host-mapped memory -- so spinning tiles can never keep the chain from
-// being scheduled.  If that does not happen within a second the side stream
-// simply waits for the chain to finish (no overlap, same result).
-struct Overlap {
-  cudaStream_t side = nullptr;
-  std::vector<cudaEvent_t> ev;
-  int* h_res = nullptr;   // host-mapped resident counters (slots of a ring)
-  int* d_res = nullptr;
-  int base = 0;
-  static constexpr int RING = 1 << 16;
-
-  int init(int T) {
-    static cudaStream_t s_side = nullptr;
-    static int* s_h = nullptr;
-    static int* s_d = nullptr;
-    static int s_cursor = 0;
-    if (!s_side) {
-      CK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
-      CK(cudaHostAlloc((void**)&s_h, sizeof(int) * RING, cudaHostAllocMapped));
-      CK(cudaHostGetDevicePointer((void**)&s_d, s_h, 0));
-      memset(s_h, 0, sizeof(int) * RING);
-    }
-    side = s_side;
-    if (s_cursor + T > RING) s_cursor = 0;
-    base = s_cursor;
-    s_cursor += T;
-    h_res = s_h + base;
-    d_res = s_d + base;
-    for (int t = 0; t < T; t++) ((volatile int*)h_res)[t] = 0;
-    ev.resize(2 * T + 2);
-    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return VFCP_OK;
-  }
-  cudaEvent_t prep_done(int t) { return ev[2 * t]; }
-  cudaEvent_t chain_done(int t) { return ev[2 * t + 1]; }
-  cudaEvent_t start() { return ev[ev.size() - 2]; }
-  cudaEvent_t end() { return ev[ev.size() - 1]; }
-  // true once chain(t)'s CTAs are all resident
-  bool wait_resident(int t, int grid) {
-    const auto t0 = std::chrono::steady_clock::now();
-    while (((volatile int*)h_res)[t] < grid) {
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1))
-        return false;
-    }
-    return true;
-  }
-  ~Overlap() {
-    for (auto& e : ev) cudaEventDestroy(e);
-  }
-};
-
-// previous-frame rows a tile of 32 rows may read, in strips: Lorenzo needs
-// the row above; a semi-Lagrangian departure point moves at most
-// |v| * cfl <= (2^30 + tau') * cfl cells, plus the bilinear taps
-int gate_reach(const vfcp_params* p, int nby) {
-  if (p->predictor == VFCP_PRED_LORENZO || p->tau <= 0) return 1;
-  const double cfl = std::max((p->dt / p->dx) / p->scale, (p->dt / p->dy) / p->scale);
-  const double disp = ((double)(1 << 30) + (double)p->tau) * cfl;
-  if (!(disp < 1e9)) return nby;
-  const int rows = (int)std::ceil(disp) + 3;
-  return std::min(nby, (rows + 31) / 32 + 1);
-}
-
 int nsm_of() {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -541,7 +467,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   const int nsm = nsm_of();
   Scratch sc(st);
   uint8_t* codes_p;
-  CK(sc.get(&codes_p, (size_t)2 * plane));   // two frames in flight
+  CK(sc.get(&codes_p, (size_t)plane));
   int32_t *pre_nl, *a, *err;
   uint32_t* pins;
   uint64_t* bnd;
@@ -550,17 +476,14 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   CK(sc.get(&pre_nl, (size_t)T * cplane));
   int32_t *prevrec, *q0;
   uint16_t* syms;
-  int* strip_done;
-  CK(sc.get(&a, (size_t)4 * plane));
-  CK(sc.get(&q0, (size_t)4 * plane));
+  CK(sc.get(&a, (size_t)2 * plane));
+  CK(sc.get(&q0, (size_t)2 * plane));
   CK(sc.get(&err, (size_t)4 * plane));
   CK(sc.get(&prevrec, (size_t)2 * plane));
-  CK(sc.get(&syms, (size_t)4 * plane));
-  CK(sc.get(&pins, (size_t)8 * cplane));
+  CK(sc.get(&syms, (size_t)2 * plane));
+  CK(sc.get(&pins, (size_t)4 * cplane));
   CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
-  CK(sc.get(&strip_done, (size_t)nby));
-  CK(cudaMemsetAsync(strip_done, 0, sizeof(int) * nby, st));
   CK(sc.get(&ovf, 1));
   CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
@@ -597,86 +520,47 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
     CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
   }
+  io.a0 = a;
+  io.a1 = a + plane;
+  io.pin_u = pins;
+  io.pin_v = pins + cplane;
+  io.q0_0 = q0;
+  io.q0_1 = q0 + plane;
+  io.sym0 = syms;
+  io.sym1 = syms + plane;
   io.bnd = bnd;
-  io.strip_done = strip_done;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
-  Overlap ov;
-  if (int rc = ov.init(T)) return rc;
-  cudaStream_t side = ov.side;
-  const int reach = gate_reach(p, nby);
-  // per-frame buffers of the two frames in flight
-  auto A = [&](int t) { return a + 2 * plane * (t & 1); };
-  auto Q = [&](int t) { return q0 + 2 * plane * (t & 1); };
-  auto CP = [&](int t) { return codes_p + plane * (t & 1); };
-  auto PN = [&](int t) { return pins + 4 * cplane * (t & 1); };
-  auto SY = [&](int t) { return syms + 2 * plane * (t & 1); };
-  auto prep = [&](int t, bool gated) -> int {
-    PrepParams pp = prep_params(p, t, lad);
-    if (gated) {
-      pp.gate = strip_done;
-      pp.gate_target = 2 * t;   // chain(t-1) adds 2 per strip
-      pp.gate_reach = reach;
-    }
-    int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
-    uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
-    int32_t* at = A(t);
-    uint32_t* pt = PN(t);
-    LAUNCH(K_PREP, side,
-           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, at, at + plane,
-                            Q(t), Q(t) + plane, prevrec, CP(t), ovf, side));
-    pp.gate = nullptr;   // r0 passed the gate; mop / pix follow in order
-    if (pp.mop)
-      LAUNCH(K_MOP, side,
-             launch_enc_mop<F>(u, v, at, at + plane, prevrec, pp, log2tab,
-                               modes_t, side));
-    LAUNCH(K_PREP, side,
-           launch_enc_pix<F>(u, v, CP(t), prevrec, qd_row_off, pre_nl, pp,
-                             modes_t, at, at + plane, pt, pt + cplane,
-                             pt + 2 * cplane, pt + 3 * cplane, qd, row_ll,
-                             side));
-    return VFCP_OK;
-  };
-  CK(cudaEventRecord(ov.start(), st));
-  CK(cudaStreamWaitEvent(side, ov.start(), 0));
-  if (int rc = prep(0, false)) return rc;
-  CK(cudaEventRecord(ov.prep_done(0), side));
   for (int t = 0; t < T; t++) {
+    const PrepParams pp = prep_params(p, t, lad);
+    int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
     int32_t* ecur = err + 2 * plane * (t & 1);
-    io.a0 = A(t);
-    io.a1 = A(t) + plane;
-    io.q0_0 = Q(t);
-    io.q0_1 = Q(t) + plane;
-    io.codes = CP(t);
-    io.pin_u = PN(t);
-    io.pin_v = PN(t) + cplane;
-    io.sym0 = SY(t);
-    io.sym1 = SY(t) + plane;
+    uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
+    LAUNCH(K_PREP, st,
+           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, a, a + plane,
+                            q0, q0 + plane, prevrec, codes_p, ovf, st));
+    if (pp.mop)
+      LAUNCH(K_MOP, st,
+             launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
+                               modes_t, st));
+    LAUNCH(K_PREP, st,
+           launch_enc_pix<F>(u, v, codes_p, prevrec, qd_row_off, pre_nl, pp,
+                             modes_t, a, a + plane, pins, pins + cplane,
+                             pins + 2 * cplane, pins + 3 * cplane, qd, row_ll,
+                             st));
+    io.codes = codes_p;
     io.out_i0 = ecur;
     io.out_i1 = ecur + plane;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    io.resident = ov.d_res + t;
-    CK(cudaStreamWaitEvent(st, ov.prep_done(t), 0));
-    int grid = 0;
-    LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st, &grid));
-    CK(cudaEventRecord(ov.chain_done(t), st));
+    LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
     if (wprof && t == 1) print_stamps("enc", io.tstamp, H, st);
-    if (t + 1 < T) {
-      const bool overlap = ov.wait_resident(t, grid);
-      if (!overlap) CK(cudaStreamWaitEvent(side, ov.chain_done(t), 0));
-      if (int rc = prep(t + 1, overlap)) return rc;
-      CK(cudaEventRecord(ov.prep_done(t + 1), side));
-    }
-    CK(cudaStreamWaitEvent(side, ov.chain_done(t), 0));
-    LAUNCH(K_LLW, side,
-           launch_sym_scatter(SY(t), SY(t) + plane, PN(t) + 2 * cplane,
-                              PN(t) + 3 * cplane, qd_row_off + (size_t)t * H,
+    LAUNCH(K_LLW, st,
+           launch_sym_scatter(syms, syms + plane, pins + 2 * cplane,
+                              pins + 3 * cplane, qd_row_off + (size_t)t * H,
                               pre_nl + (size_t)t * cplane, H, W, Wp, nchunks,
-                              qd, row_ll + (size_t)t * H, side));
+                              qd, row_ll + (size_t)t * H, st));
   }
-  CK(cudaEventRecord(ov.end(), side));
-  CK(cudaStreamWaitEvent(st, ov.end(), 0));
   if (wprof) {
     unsigned long long h[WP_N];
     CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -714,18 +598,15 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   uint32_t* pins;
   uint64_t* bnd;
   int* ticket;
-  int* strip_done;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
   CK(sc.get(&pre_ll, (size_t)T * cplane));
-  CK(sc.get(&a, (size_t)4 * plane));       // two frames in flight
+  CK(sc.get(&a, (size_t)2 * plane));
   CK(sc.get(&rec, (size_t)4 * plane));
-  CK(sc.get(&pins, (size_t)4 * cplane));
+  CK(sc.get(&pins, (size_t)2 * cplane));
   CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
-  CK(sc.get(&strip_done, (size_t)nby));
   CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
-  CK(cudaMemsetAsync(strip_done, 0, sizeof(int) * nby, st));
   LAUNCH(K_SCAN, st,
          launch_chunk_prefix<uint16_t>(codes, qd, qd_row_off, (int64_t)T * H,
                                        W, nchunks, p->tau, pre_nl, pre_ll,
@@ -742,67 +623,35 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
     CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
   }
+  io.a0 = a;
+  io.a1 = a + plane;
+  io.pin_u = pins;
+  io.pin_v = pins + cplane;
   io.bnd = bnd;
-  io.strip_done = strip_done;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
-  Overlap ov;
-  if (int rc = ov.init(T)) return rc;
-  cudaStream_t side = ov.side;
-  const int reach = gate_reach(p, nby);
-  auto prep = [&](int t, bool gated) -> int {
-    PrepParams pp = prep_params(p, t, lad);
-    if (gated) {
-      pp.gate = strip_done;
-      pp.gate_target = 2 * t;   // chain(t-1) adds 2 per strip
-      pp.gate_reach = reach;
-    }
+  for (int t = 0; t < T; t++) {
+    const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
-    int32_t* ab = a + 2 * plane * (t & 1);
-    uint32_t* pb = pins + 2 * cplane * (t & 1);
-    LAUNCH(K_DROWS, side,
+    int32_t* rcur = rec + 2 * plane * (t & 1);
+    LAUNCH(K_DROWS, st,
            launch_dec_prep<uint16_t>(
                codes, qd, ll,
                t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr, rprev,
-               rprev + plane, qd_row_off, ll_row_off, pre_nl, pre_ll, pp, ab,
-               ab + plane, pb, pb + cplane, side));
-    return VFCP_OK;
-  };
-  CK(cudaEventRecord(ov.start(), st));
-  CK(cudaStreamWaitEvent(side, ov.start(), 0));
-  if (int rc = prep(0, false)) return rc;
-  CK(cudaEventRecord(ov.prep_done(0), side));
-  for (int t = 0; t < T; t++) {
-    int32_t* rcur = rec + 2 * plane * (t & 1);
-    io.a0 = a + 2 * plane * (t & 1);
-    io.a1 = io.a0 + plane;
-    io.pin_u = pins + 2 * cplane * (t & 1);
-    io.pin_v = io.pin_u + cplane;
+               rprev + plane, qd_row_off, ll_row_off, pre_nl, pre_ll, pp, a,
+               a + plane, pins, pins + cplane, st));
     io.out_i0 = rcur;
     io.out_i1 = rcur + plane;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    io.resident = ov.d_res + t;
-    CK(cudaStreamWaitEvent(st, ov.prep_done(t), 0));
-    int grid = 0;
-    LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st, &grid));
-    CK(cudaEventRecord(ov.chain_done(t), st));
+    LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
     if (wprof && t == 1) print_stamps("dec", io.tstamp, H, st);
-    if (t + 1 < T) {
-      const bool overlap = ov.wait_resident(t, grid);
-      if (!overlap) CK(cudaStreamWaitEvent(side, ov.chain_done(t), 0));
-      if (int rc = prep(t + 1, overlap)) return rc;
-      CK(cudaEventRecord(ov.prep_done(t + 1), side));
-    }
-    CK(cudaStreamWaitEvent(side, ov.chain_done(t), 0));
-    LAUNCH(K_AUX, side,
+    LAUNCH(K_AUX, st,
            launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
                              out_u + (size_t)t * HW, out_v + (size_t)t * HW,
                              fix_u ? fix_u + (size_t)t * HW : nullptr,
-                             fix_v ? fix_v + (size_t)t * HW : nullptr, side));
+                             fix_v ? fix_v + (size_t)t * HW : nullptr, st));
   }
-  CK(cudaEventRecord(ov.end(), side));
-  CK(cudaStreamWaitEvent(st, ov.end(), 0));
   if (wprof) {
     unsigned long long h[WP_N];
     CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));

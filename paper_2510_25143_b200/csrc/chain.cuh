@@ -57,8 +57,6 @@ struct ChainIO {
   uint16_t* sym0;            // encoder: symbol planes (pitch Wp)
   uint16_t* sym1;
   uint64_t* bnd;             // tagged last-row slots [ntask][W]
-  int* strip_done;           // per strip: +1 per component when written out
-  int* resident;             // host-mapped: CTAs that have started
   unsigned long long* stats; // optional phase timers (WavePhase)
   unsigned long long* tstamp; // optional per-task [start, first block, end] ns
   int* ticket;
@@ -76,23 +74,7 @@ struct PrepParams {
   int mop;          // run the MoP trial for this frame
   int force_sl;     // predictor 'sl' (and t >= 1, tau > 0)
   Ladder lad;
-  // frame overlap: the previous frame's chain counts finished strips in
-  // gate[]; a tile of block row bi needs strips bi +- gate_reach to reach
-  // gate_target (null: the previous frame is complete)
-  const int* gate;
-  int gate_target, gate_reach;
 };
-
-__device__ __forceinline__ void prep_gate(const PrepParams& p, int bi) {
-  if (!p.gate) return;
-  if (threadIdx.x == 0) {
-    const int lo = max(0, bi - p.gate_reach), hi = min(p.nby - 1, bi + p.gate_reach);
-    for (int k = lo; k <= hi; k++)
-      while (*(volatile const int*)(p.gate + k) < p.gate_target) __nanosleep(200);
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 // exact rha(x / 2e) for integer x, e > 0, |x| < 2^31
 __device__ __forceinline__ int32_t quant32(int32_t x, int32_t e, double inv2e) {
@@ -218,7 +200,6 @@ chain_kernel(ChainIO io) {
   const int nblocks = (W + 31 + 31) / 32;
   const int ntask = chain_ntask(ENC, H);
   if (threadIdx.x < 32) sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
-  if (io.resident && threadIdx.x == 0) atomicAdd_system(io.resident, 1);
 
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
@@ -317,11 +298,6 @@ chain_kernel(ChainIO io) {
         pc.lap(WP_PRE, lane);
       }
       retire_before(nchunks + CNS - 1);
-      if (io.strip_done) {   // this component of the strip is in memory
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(io.strip_done + NPAIR * g + pr, 1);
-      }
     } else if (wact) {
       // ===================================================== chain warp
       // Row i0-1 (the strip above's last row) arrives in hin[pr] (a ring of

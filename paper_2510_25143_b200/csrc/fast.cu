@@ -274,7 +274,6 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const int c0 = 32 * blockIdx.x, r0 = 32 * blockIdx.y;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int64_t HW = (int64_t)H * W;
-  prep_gate(p, blockIdx.y);
   const F* uo = u + (int64_t)p.t * HW;
   const F* vo = v + (int64_t)p.t * HW;
   const bool has_prev = p.t > 0;
@@ -595,7 +594,6 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   const bool sl_blk = has_prev && modes_t && modes_t[bi * p.nbx + bj] == 1;
-  prep_gate(p, bi);
   {
 #pragma unroll 5
     for (int k = tid; k < 33 * 33; k += 256) {
@@ -823,8 +821,7 @@ cudaError_t launch_sym_scatter(const uint16_t* s0, const uint16_t* s1,
 }
 
 template <bool ENC>
-cudaError_t launch_chain(const ChainIO& io, int nsm, cudaStream_t st,
-                         int* grid_out) {
+cudaError_t launch_chain(const ChainIO& io, int nsm, cudaStream_t st) {
   const size_t smem = sizeof(ChainSmem<ENC>);
   cudaError_t e = cudaFuncSetAttribute(
       chain_kernel<ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -836,9 +833,7 @@ cudaError_t launch_chain(const ChainIO& io, int nsm, cudaStream_t st,
                                                     threads, smem);
   if (e != cudaSuccess) return e;
   const int ntask = chain_ntask(ENC, io.H);
-  const int grid = min(max(occ, 1) * nsm, ntask);
-  if (grid_out) *grid_out = grid;
-  chain_kernel<ENC><<<grid, threads, smem, st>>>(io);
+  chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), threads, smem, st>>>(io);
   return cudaGetLastError();
 }
 
@@ -885,7 +880,7 @@ template cudaError_t launch_dec_prep<uint16_t>(
     const int32_t*, const int32_t*, const int64_t*, const int64_t*,
     const int32_t*, const int32_t*, const PrepParams&, int32_t*, int32_t*,
     uint32_t*, uint32_t*, cudaStream_t);
-template cudaError_t launch_chain<true>(const ChainIO&, int, cudaStream_t, int*);
-template cudaError_t launch_chain<false>(const ChainIO&, int, cudaStream_t, int*);
+template cudaError_t launch_chain<true>(const ChainIO&, int, cudaStream_t);
+template cudaError_t launch_chain<false>(const ChainIO&, int, cudaStream_t);
 
 }  // namespace vfcp
