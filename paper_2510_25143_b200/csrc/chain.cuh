@@ -167,19 +167,32 @@ struct ChainSmem {
 // tightly (they are on the critical path); the producers back off so their
 // polling does not take issue slots and shared-memory bandwidth from the
 // chain warp on the same sub-partition.
+// The counters use acquire loads / release stores at CTA scope instead of
+// full fences: a fence would also wait for the warp's outstanding global
+// loads (the prefetched boundary slots).
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
 template <int SLEEP_NS = 0>
 __device__ __forceinline__ void spin_ge(const int* p, int need) {
-  while (!__all_sync(0xffffffffu, ld_volatile(p) >= need)) {
+  while (!__all_sync(0xffffffffu, ld_acquire_cta(p) >= need)) {
     if (SLEEP_NS) __nanosleep(SLEEP_NS);
   }
-  __threadfence_block();
 }
 __device__ __forceinline__ void signal_set(int* p, int v, int lane) {
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence_block();
-    *(volatile int*)p = v;
-  }
+  __syncwarp();   // the warp's writes happen before lane 0's release
+  if (lane == 0) st_release_cta(p, v);
   __syncwarp();
 }
 
@@ -362,10 +375,7 @@ chain_kernel(ChainIO io) {
         };
         // after step jj, row 31 has finished column c0-31+jj
         auto publish = [&](int jj) {
-          if (lane31) {
-            __threadfence_block();
-            *(volatile int*)hprog_out = min(max(c0 - 31 + jj + 1, 0), W);
-          }
+          if (lane31) st_release_cta(hprog_out, min(max(c0 - 31 + jj + 1, 0), W));
         };
         // ---- this lane's 32 columns c = c0 - lane + jj (two chunks).
         // vm: bit jj = pixel (my_i, cbase+jj) exists; pm: pinned or not
