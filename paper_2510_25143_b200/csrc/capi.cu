@@ -516,6 +516,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   std::vector<unsigned long long> tsv;
   if (wprof) {
     CK(sc.get(&io.stats, WP_N));
+    io.stats_strip0 = strcmp(getenv("VFCP_WAVE_PROFILE"), "strip0") == 0;
     CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
     CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
     CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
@@ -619,6 +620,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   std::vector<unsigned long long> tsv;
   if (wprof) {
     CK(sc.get(&io.stats, WP_N));
+    io.stats_strip0 = strcmp(getenv("VFCP_WAVE_PROFILE"), "strip0") == 0;
     CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
     CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
     CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));

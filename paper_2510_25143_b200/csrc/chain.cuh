@@ -58,6 +58,7 @@ struct ChainIO {
   uint16_t* sym1;
   uint64_t* bnd;             // tagged last-row slots [ntask][W]
   unsigned long long* stats; // optional phase timers (WavePhase)
+  int stats_strip0;          // time only task 0, pair 0
   unsigned long long* tstamp; // optional per-task [start, first block, end] ns
   int* ticket;
   uint32_t tag_base;         // tags unique across frames sharing `bnd`
@@ -229,7 +230,8 @@ chain_kernel(ChainIO io) {
     const int nrows = wact ? min(32, H - i0) : 0;
     const int my_i = i0 + lane;
     const bool rowok = my_i < H;
-    PhaseClock pc(io.stats);
+    // VFCP_WAVE_PROFILE=strip0 times only the first strip (its own work, no waits on others)
+    PhaseClock pc((io.stats && (!io.stats_strip0 || (task == 0 && pr == 0))) ? io.stats : nullptr);
 
     if (producer && wact) {
       // ===================================================== producer
@@ -238,50 +240,48 @@ chain_kernel(ChainIO io) {
       const uint32_t* pinp = comp ? io.pin_v : io.pin_u;
       int32_t* out_i = comp ? io.out_i1 : io.out_i0;
       uint16_t* symp = comp ? io.sym1 : io.sym0;
+      // 16-byte moves: lane = (row 4k + lane/8, columns 4*(lane%8) .. +3),
+      // a 32x32 int32 tile in 8 instructions per plane (rows are 128-byte
+      // aligned: Wp is a multiple of 32)
+      const int vr = lane >> 3, vc = 4 * (lane & 7);
       auto stage = [&](int x) {
         const int s = x % CNS;
-        const int c = 32 * x + lane;
-#pragma unroll 8
-        for (int r = 0; r < 32; r++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int r = 4 * k + vr;
           const bool rv = r < nrows;
-          const int64_t k = (int64_t)(i0 + (rv ? r : 0)) * Wp + c;
-          cp_async<4>(&R.v[s][r][lane], a + k, rv);
-          if (ENC) cp_async<4>(&R.q0[s][r][lane], q0p + k, rv);
+          const int64_t kk = (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * x + vc;
+          cp_async<16>(&R.v[s][r][vc], a + kk, rv);
+          if (ENC) cp_async<16>(&R.q0[s][r][vc], q0p + kk, rv);
         }
         const int64_t pb = (int64_t)(rowok ? my_i : i0) * nchunks + x;
         cp_async<4>(&R.pin[s][lane], pinp + pb, rowok);
         if (ENC) {
+          // codes: 32 rows x 32 bytes, 16 bytes per lane, 2 instructions
 #pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const int r = (lane >> 3) + 4 * k, q = lane & 7;
+          for (int k = 0; k < 2; k++) {
+            const int r = 16 * k + (lane >> 1), h = 16 * (lane & 1);
             const bool rv = r < nrows;
-            cp_async<4>(&R.code[s][r][q],
-                        io.codes + (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * x + 4 * q,
-                        rv);
+            cp_async<16>(reinterpret_cast<unsigned char*>(&R.code[s][r][0]) + h,
+                         io.codes + (int64_t)(i0 + (rv ? r : 0)) * Wp + 32 * x + h, rv);
           }
         }
       };
-      // batched 16 rows at a time so the loads of a batch overlap
+      // finished chunk -> global (columns past W land in the pitch padding)
       auto write_out = [&](int x) {
         const int s = x % CNS;
-        const int c = 32 * x + lane;
-        const bool cv = c < W;
 #pragma unroll
-        for (int h = 0; h < 32; h += 16) {
-          int32_t val[16], sy[16];
-#pragma unroll
-          for (int k = 0; k < 16; k++) {
-            const int r = h + k;
-            val[k] = R.v[s][r][lane];
-            if (ENC) sy[k] = R.q0[s][r][lane];
-          }
-#pragma unroll
-          for (int k = 0; k < 16; k++) {
-            const int r = h + k;
-            if (cv && r < nrows) {
-              const int64_t kk = (int64_t)(i0 + r) * Wp + c;
-              out_i[kk] = val[k];
-              if (ENC) symp[kk] = (uint16_t)sy[k];
+        for (int k = 0; k < 8; k++) {
+          const int r = 4 * k + vr;
+          if (r < nrows) {
+            const int64_t kk = (int64_t)(i0 + r) * Wp + 32 * x + vc;
+            *reinterpret_cast<int4*>(out_i + kk) = *reinterpret_cast<const int4*>(&R.v[s][r][vc]);
+            if (ENC) {
+              const int4 q = *reinterpret_cast<const int4*>(&R.q0[s][r][vc]);
+              uint2 w;
+              w.x = ((uint32_t)q.x & 0xffffu) | ((uint32_t)q.y << 16);
+              w.y = ((uint32_t)q.z & 0xffffu) | ((uint32_t)q.w << 16);
+              *reinterpret_cast<uint2*>(symp + kk) = w;
             }
           }
         }

@@ -1,6 +1,6 @@
 """Per-phase cycle breakdown of the wavefront kernels (VFCP_WAVE_PROFILE)."""
 import os, sys, time
-if not os.environ.get("NOPROF"): os.environ["VFCP_WAVE_PROFILE"] = "1"
+if not os.environ.get("NOPROF"): os.environ.setdefault("VFCP_WAVE_PROFILE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2510_25143_b200 as vg
