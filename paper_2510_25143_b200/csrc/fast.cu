@@ -279,22 +279,38 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const bool has_prev = p.t > 0;
   const F* up_ = u + (int64_t)(p.t - 1) * HW;
   const F* vp_ = v + (int64_t)(p.t - 1) * HW;
-#pragma unroll 5
-  for (int k = tid; k < 33 * 33; k += 256) {
+  // all loads of the thread first (5 x 6 in flight), then the conversions
+  constexpr int NK = (33 * 33 + 255) / 256;
+  F xo_u[NK], xo_v[NK], xp_u[NK], xp_v[NK];
+  int32_t xe_u[NK], xe_v[NK];
+  bool okk[NK];
+#pragma unroll
+  for (int q = 0; q < NK; q++) {
+    const int k = tid + 256 * q;
     const int rr = k / 33, cc = k - rr * 33;
     const int i = r0 - 1 + rr, j = c0 - 1 + cc;
-    const bool ok = i >= 0 && j >= 0 && i < H && j < W;
-    const int64_t n = (int64_t)i * W + j;
-    so[0][rr][cc] = ok ? load_fixed(uo, n, p.S) : 0;
-    so[1][rr][cc] = ok ? load_fixed(vo, n, p.S) : 0;
-    int32_t pu = 0, pv = 0;
-    if (has_prev && ok) {
-      const int64_t m = (int64_t)i * Wp + j;
-      pu = load_fixed(up_, n, p.S) + __ldg(err_prev_u + m);
-      pv = load_fixed(vp_, n, p.S) + __ldg(err_prev_v + m);
-    }
-    sp[0][rr][cc] = pu;
-    sp[1][rr][cc] = pv;
+    const bool ok = k < 33 * 33 && i >= 0 && j >= 0 && i < H && j < W;
+    okk[q] = ok;
+    const int64_t n = ok ? (int64_t)i * W + j : 0;
+    const int64_t m = ok ? (int64_t)i * Wp + j : 0;
+    xo_u[q] = ok ? __ldg(uo + n) : F(0);
+    xo_v[q] = ok ? __ldg(vo + n) : F(0);
+    const bool okp = ok && has_prev;
+    xp_u[q] = okp ? __ldg(up_ + n) : F(0);
+    xp_v[q] = okp ? __ldg(vp_ + n) : F(0);
+    xe_u[q] = okp ? __ldg(err_prev_u + m) : 0;
+    xe_v[q] = okp ? __ldg(err_prev_v + m) : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < NK; q++) {
+    const int k = tid + 256 * q;
+    if (k >= 33 * 33) break;
+    const int rr = k / 33, cc = k - rr * 33;
+    const bool ok = okk[q];
+    so[0][rr][cc] = ok ? fixed_of((double)xo_u[q], p.S) : 0;
+    so[1][rr][cc] = ok ? fixed_of((double)xo_v[q], p.S) : 0;
+    sp[0][rr][cc] = (ok && has_prev) ? fixed_of((double)xp_u[q], p.S) + xe_u[q] : 0;
+    sp[1][rr][cc] = (ok && has_prev) ? fixed_of((double)xp_v[q], p.S) + xe_v[q] : 0;
   }
   __syncthreads();
   bool ovf = false;
