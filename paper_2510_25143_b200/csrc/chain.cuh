@@ -156,9 +156,10 @@ constexpr int HRING = 128;   // boundary-row ring (columns), power of two
 template <bool ENC>
 struct ChainSmem {
   PairRing<ENC> r[chain_pairs(ENC)];
-  int32_t hin[chain_pairs(ENC) + 1][HRING];   // row i0-1 of strip p
+  // row i0-1 of strip p: (column + 1) << 32 | value, so the consumer spins
+  // on the entry itself (no separate flag, no fence on the producer side)
+  uint64_t hin[chain_pairs(ENC) + 1][HRING];
   int32_t etab[32];
-  int hprog[chain_pairs(ENC) + 1];   // columns of hin[p] available
   int full[chain_pairs(ENC)];        // chunks P_p has staged
   int done[chain_pairs(ENC)];        // blocks C_p has swept
   int task;
@@ -218,9 +219,10 @@ chain_kernel(ChainIO io) {
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
     if (threadIdx.x < NPAIR) {
-      sm.hprog[threadIdx.x] = 0;
       sm.full[threadIdx.x] = 0; sm.done[threadIdx.x] = 0;
     }
+    for (int k = threadIdx.x; k < (NPAIR + 1) * HRING; k += blockDim.x)
+      (&sm.hin[0][0])[k] = 0;   // no stale tags from an earlier task
     __syncthreads();
     const int task = sm.task;
     if (task >= ntask) break;
@@ -326,9 +328,8 @@ chain_kernel(ChainIO io) {
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
       const bool top = i0 > 0;
       const bool lane0 = lane == 0, lane31 = lane == 31;
-      int32_t* hin = sm.hin[pr];
-      int32_t* hout = sm.hin[pr + (stream_out ? 1 : 0)];
-      int* hprog_out = &sm.hprog[pr + (stream_out ? 1 : 0)];
+      uint64_t* hin = sm.hin[pr];
+      uint64_t* hout = sm.hin[pr + (stream_out ? 1 : 0)];
       int32_t l = 0, ul = 0;
       uint64_t bpre = 0;   // prefetched tagged boundary slot (pr == 0)
       if (top && pr == 0 && lane < W) bpre = ld_relaxed_u64(up_gb + lane);
@@ -358,7 +359,7 @@ chain_kernel(ChainIO io) {
               ok = (uint32_t)(w >> 32) == tag - 2;
             }
           }
-          hin[c & (HRING - 1)] = (int32_t)(uint32_t)w;
+          hin[c & (HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)w;
           __syncwarp();
           const int cn = c + 32;
           if (cn < W) bpre = ld_relaxed_u64(up_gb + cn);
@@ -366,16 +367,25 @@ chain_kernel(ChainIO io) {
         // the consumer below must be done with the ring entries we reuse
         if (stream_out) spin_ge(&sm.done[pr + 1], m - (HRING / 32 - 1));
         pc.lap(WP_WAITBND, lane);
-        // wait for the boundary columns c0+jj .. c0+jj+7 (pr > 0)
-        auto need_bnd = [&](int jj) {
-          if (top && pr > 0) spin_ge(&sm.hprog[pr], min(c0 + jj + 8, W));
+        // boundary columns c0+jj .. c0+jj+7: lane k < 8 waits for column
+        // c0+jj+k's tag and holds its value (0 outside the frame / top strip)
+        auto bnd_group = [&](int jj) -> int32_t {
+          const int c = c0 + jj + lane;
+          const bool want = top && lane < 8 && c < W;
+          const volatile uint64_t* e = hin + (c & (HRING - 1));
+          uint64_t w = want ? *e : 0;
+          bool ok = !want || (uint32_t)(w >> 32) == (uint32_t)(c + 1);
+          while (!__all_sync(FULL, ok)) {
+            if (!ok) {
+              w = *e;
+              ok = (uint32_t)(w >> 32) == (uint32_t)(c + 1);
+            }
+          }
+          return want ? (int32_t)(uint32_t)w : 0;
         };
-        auto bnd_at = [&](int jj) -> int32_t {
-          return top ? hin[(c0 + jj) & (HRING - 1)] : 0;
-        };
-        // after step jj, row 31 has finished column c0-31+jj
-        auto publish = [&](int jj) {
-          if (lane31) st_release_cta(hprog_out, min(max(c0 - 31 + jj + 1, 0), W));
+        // row 31 of this strip finished column c: stream it to the strip below
+        auto put_bnd = [&](int c, int32_t r) {
+          if (c >= 0) hout[c & (HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)r;
         };
         // ---- this lane's 32 columns c = c0 - lane + jj (two chunks).
         // vm: bit jj = pixel (my_i, cbase+jj) exists; pm: pinned or not
@@ -392,7 +402,6 @@ chain_kernel(ChainIO io) {
                 : 0u;
         const uint32_t pm =
             __funnelshift_r(R.pin[s_lo][lane], R.pin[s_hi][lane], cbase & 31) | ~vm;
-        const int hcol = (c0 - 31) & (HRING - 1);   // lane 31's ring column at jj = 0
         if (!ENC) {
           int32_t av[32];
 #pragma unroll
@@ -402,18 +411,12 @@ chain_kernel(ChainIO io) {
             const int32_t x = R.v[sl][lane][c & 31];
             av[jj] = c < 0 ? 0 : x;
           }
-          int32_t bbv[8];
+          int32_t bg = 0;
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
-            if ((jj & 7) == 0) {
-              // the group's boundary values into registers up front: the
-              // ring stores below may alias, so loads inside the loop would
-              // wait for the previous step's result
-              need_bnd(jj);
-#pragma unroll
-              for (int k = 0; k < 8; k++) bbv[k] = bnd_at(jj + k);
-            }
-            const int32_t bb = bbv[jj & 7];
+            // the group's boundary values up front (lane k: column c0+jj+k)
+            if ((jj & 7) == 0) bg = bnd_group(jj);
+            const int32_t bb = __shfl_sync(FULL, bg, jj & 7);
             const int32_t up = __shfl_up_sync(FULL, l, 1);
             const int32_t nu = lane0 ? bb : up;
             const int32_t t = (int32_t)((uint32_t)av[jj] - (uint32_t)ul);
@@ -422,10 +425,7 @@ chain_kernel(ChainIO io) {
             av[jj] = r;
             l = r;
             ul = nu;
-            if (stream_out) {
-              if (lane31) hout[(hcol + jj) & (HRING - 1)] = r;
-              if ((jj & 7) == 7) publish(jj);
-            }
+            if (stream_out && lane31) put_bnd(c0 - 31 + jj, r);
           }
 #pragma unroll
           for (int jj = 0; jj < 32; jj++) {
@@ -464,17 +464,14 @@ chain_kernel(ChainIO io) {
 #pragma unroll
           for (int g8 = 0; g8 < 32; g8 += 8) {
             if (!redo) {
-              need_bnd(g8);
-              int32_t bbv[8];   // see the decoder sweep
-#pragma unroll
-              for (int k = 0; k < 8; k++) bbv[k] = bnd_at(g8 + k);
+              const int32_t bg = bnd_group(g8);
               bool slow = false;
 #pragma unroll
               for (int k = 0; k < 8; k++) {
                 const int jj = g8 + k;
                 const int32_t R0 = rr[jj], q0 = qq[jj], e = ee[jj];
                 const int32_t rho = R0 - q0 * (2 * e);
-                const int32_t bb = bbv[k];
+                const int32_t bb = __shfl_sync(FULL, bg, k);
                 const int32_t up = __shfl_up_sync(FULL, l, 1);
                 const int32_t nu = lane0 ? bb : up;
                 const int32_t d = nu + l - ul;
@@ -488,17 +485,24 @@ chain_kernel(ChainIO io) {
                 rr[jj] = r;
                 l = r;
                 ul = nu;
-                if (stream_out && lane31) hout[(hcol + jj) & (HRING - 1)] = r;
               }
-              if (__any_sync(FULL, slow)) redo = true;
-              else if (stream_out) publish(g8 + 7);
+              if (__any_sync(FULL, slow)) {
+                redo = true;
+              } else if (stream_out && lane31) {
+                // exact results (no step of the group needed the exact
+                // path): stream the group's row-31 values
+#pragma unroll
+                for (int k = 0; k < 8; k++) put_bnd(c0 - 31 + g8 + k, rr[g8 + k]);
+              }
             }
           }
           if (redo) {
             // mixed steps: redo the block with the exact step
             if (io.stats && lane == 0) atomicAdd(io.stats + WP_X2, 1ull);
             l = l_s; ul = ul_s;
-            if (top && pr > 0) spin_ge(&sm.hprog[pr], min(c0 + 32, W));
+            int32_t bgr[4];
+#pragma unroll
+            for (int g = 0; g < 4; g++) bgr[g] = bnd_group(8 * g);
 #pragma unroll 1
             for (int jj = 0; jj < 32; jj++) {
               const int c = cbase + jj;
@@ -509,7 +513,8 @@ chain_kernel(ChainIO io) {
               const int32_t R0 = c < 0 ? 0 : R.v[sl][lane][col];
               const int32_t q0 = R.q0[sl][lane][col];
               const int32_t e = pin ? 0 : sm.etab[(lo ? cb_lo : cb_hi)[c & 31] & 31];
-              const int32_t bb = bnd_at(jj);
+              const int32_t bgj = (jj < 8) ? bgr[0] : (jj < 16) ? bgr[1] : (jj < 24) ? bgr[2] : bgr[3];
+              const int32_t bb = __shfl_sync(FULL, bgj, jj & 7);
               const int32_t up = __shfl_up_sync(FULL, l, 1);
               const int32_t nu = lane0 ? bb : up;
               const int32_t d = nu + l - ul;
@@ -521,11 +526,10 @@ chain_kernel(ChainIO io) {
                 R.v[sl][lane][col] = r;
                 R.q0[sl][lane][col] = pin ? 0 : (int32_t)sy;
               }
-              if (stream_out && lane31) hout[(hcol + jj) & (HRING - 1)] = r;
+              if (stream_out && lane31) put_bnd(c0 - 31 + jj, r);
               l = r;
               ul = nu;
             }
-            if (stream_out) publish(31);
           } else {
 #pragma unroll
             for (int jj = 0; jj < 32; jj++) {
