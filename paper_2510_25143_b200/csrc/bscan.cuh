@@ -1,0 +1,565 @@
+// The raster-order Lorenzo recurrence of one frame as a 2D block scan.
+//
+// Same contract as chain_kernel (chain.cuh, ChainIO): the prepared planes
+// a (encoder: R0 or the pinned err; decoder: A or the pinned recon), the
+// per-(row, chunk) pin words and (encoder) the frame codes in; the err /
+// recon plane and (encoder) the symbol planes out, bit for bit what the
+// reference's raster loop (codec.py:118-164 _encode_frame, 167-206
+// _decode_frame) produces.
+//
+// Why a scan is exact.  Per component, with v the chain value (encoder: err
+// = recon - orig; decoder: recon) and zero padding outside the frame,
+//   decoder:  v = vU + vL - vUL + A                 (exact)
+//   encoder:  v = q*2e - x,  x = R0 - (vU + vL - vUL),  q = rha(x / 2e)
+// so in the encoder v == -R0 + vU + vL - vUL (mod 2e) whenever the pixel is
+// quantised with the same step e (v in [-e, e] is the representative of
+// that residue; a residue of exactly e is a tie whose sign follows x, which
+// rounds away from zero).  Over a 32x32 block whose pixels all share one
+// step, have no pins and cannot escape (|R0| < (2 radius - 4) e), every
+// value is therefore a 2D prefix sum of the block plus its boundary:
+//   v(i, j) = top(j) + left(i) - corner + sum_{a<=i, b<=j} X(a, b)
+// with X = A (decoder, wrapping uint32 arithmetic is exact because the
+// result fits int32) or X = -R0 mod 2e (encoder, then the representative).
+// Blocks whose values are known without the recurrence (all pixels pinned:
+// semi-Lagrangian blocks, lossless areas) pass their prepared values; any
+// other block (mixed pins, mixed steps, possible escapes, a tie on its
+// boundary) is swept exactly, pixel by pixel, given its exact boundary.
+//
+// Three kernels per frame:
+//   bs_local_kernel   fully parallel: block class and the bottom row / right
+//                     column of the block-local prefix sums (LB, LR);
+//   bs_chain_kernel   the only sequential part: block boundaries travel
+//                     down the block rows (one warp per block row and
+//                     component walks its row; 32 exact values per block
+//                     are handed to the warp below) -- the critical path is
+//                     ~nby + nbx cheap block steps instead of H + W pixel
+//                     steps of a per-pixel wavefront;
+//   bs_final_kernel   fully parallel: the interior of every block from its
+//                     exact boundary (prefix sums in shared memory, ties
+//                     resolved in raster order, symbols).
+#pragma once
+
+#include "chain.cuh"
+
+namespace vfcp {
+
+enum : uint8_t { BS_SLOW = 0, BS_KNOWN = 1, BS_REG = 2, BS_DONE = 3 };
+
+struct BScanIO {
+  const int32_t* a[2];
+  const uint8_t* codes;     // encoder: frame codes (pitch Wp)
+  const uint32_t* pin[2];   // per (row, chunk)
+  int32_t* out[2];          // encoder: err; decoder: recon (pitch Wp)
+  uint16_t* sym[2];         // encoder: symbol planes (pitch Wp)
+  int32_t* lb;              // [2][nblk][32] local prefix, block bottom row
+  int32_t* lr;              // [2][nblk][32] local prefix, block right column
+  uint8_t* cls;             // [2][nblk] class | code << 2
+  uint64_t* bnd;            // tagged boundary slots [ntask][W]
+  int* ticket;
+  uint32_t tag_base;
+  int H, W, Wp, nchunks, nbx, nby;
+  int radius;
+  int32_t e_tab[32];        // e per code (0: lossless)
+  uint32_t mag_tab[32];     // floor(2^32 / 2e) per code (0: lossless)
+};
+
+constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
+constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
+
+__host__ __device__ inline int bs_ntask(int nby) {
+  return 2 * ((nby + BS_NW - 1) / BS_NW);
+}
+
+// x mod m for any uint32 x, M = floor(2^32 / m), m >= 2: the estimate
+// umulhi(x, M) is floor(x/m) or one less.
+__device__ __forceinline__ uint32_t bs_umod(uint32_t x, uint32_t m, uint32_t M) {
+  const uint32_t r = x - __umulhi(x, M) * m;
+  return r >= m ? r - m : r;
+}
+__device__ __forceinline__ uint32_t bs_madd(uint32_t a, uint32_t b, uint32_t m) {
+  const uint32_t s = a + b;
+  return s >= m ? s - m : s;
+}
+__device__ __forceinline__ uint32_t bs_msub(uint32_t a, uint32_t b, uint32_t m) {
+  return a >= b ? a - b : a + m - b;
+}
+// residue in [0, m) of any int32 (neighbouring values may come from blocks
+// with other step sizes)
+__device__ __forceinline__ uint32_t bs_res(int32_t v, uint32_t m, uint32_t M) {
+  if (v >= 0) return bs_umod((uint32_t)v, m, M);
+  const uint32_t r = bs_umod((uint32_t)0 - (uint32_t)v, m, M);
+  return r ? m - r : 0u;
+}
+// residue of -R0 (|R0| < 2^31 - 1 on this path)
+__device__ __forceinline__ uint32_t bs_negres(int32_t r0, uint32_t m, uint32_t M) {
+  return bs_res(-r0, m, M);
+}
+// representative in [-e, e] of a residue that is not the tie e
+__device__ __forceinline__ int32_t bs_rep(uint32_t r, uint32_t e, uint32_t m) {
+  return r < e ? (int32_t)r : (int32_t)r - (int32_t)m;
+}
+
+// Exact encoder step (codec.py:140-155): x = R0 - d, q = rha(x / 2e);
+// escape -> err 0, symbol 0.
+__device__ __forceinline__ int32_t bs_enc_exact(int32_t R0, int32_t d,
+                                                int32_t e, int32_t radius,
+                                                uint32_t* sym) {
+  const int64_t m = 2 * (int64_t)e;
+  const int64_t x = (int64_t)R0 - d;
+  int64_t q = (int64_t)floor(__ddiv_rn((double)x, (double)m));
+  int64_t r = x - q * m;
+  if (r < 0) { q--; r += m; }
+  else if (r >= m) { q++; r -= m; }
+  if (2 * r > m || (2 * r == m && x > 0)) q++;
+  if (q <= -radius || q >= radius) { *sym = 0u; return 0; }
+  *sym = (uint32_t)(q + radius);
+  return (int32_t)(q * m - x);
+}
+
+// ------------------------------------------------------------ phase A
+// CTA = one block, warp = component (lane = column).
+template <bool ENC>
+__global__ void __launch_bounds__(64) bs_local_kernel(BScanIO io) {
+  __shared__ uint32_t sx[2][32][33];
+  __shared__ int32_t etab[32];
+  __shared__ uint32_t mtab[32];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
+  const int bj = blockIdx.x, bi = blockIdx.y;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int32_t* a = io.a[comp];
+  const uint32_t vm = ncl >= 32 ? FULL : ((1u << ncl) - 1u);
+  const uint32_t pw =
+      lane < nr ? (io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] & vm) : 0u;
+  const bool anypin = __any_sync(FULL, pw != 0u);
+  const bool allpin = __all_sync(FULL, lane >= nr || pw == vm);
+  __syncthreads();
+  uint8_t cls;
+  if (allpin) cls = BS_KNOWN;
+  else if (anypin) cls = BS_SLOW;
+  else {
+    const bool colok = lane < ncl;
+    int32_t xa[32];
+#pragma unroll
+    for (int r = 0; r < 32; r++)
+      xa[r] = (r < nr && colok) ? __ldg(a + (int64_t)(r0 + r) * io.Wp + c0 + lane) : 0;
+    bool ok = true;
+    uint32_t m = 0, M = 0;
+    int code = 0;
+    if (ENC) {
+      code = io.codes[(int64_t)r0 * io.Wp + c0];
+      const int32_t e = etab[code & 31];
+      m = 2u * (uint32_t)e;
+      M = mtab[code & 31];
+      const int64_t lim = (2 * (int64_t)io.radius - 4) * (int64_t)e;
+      ok = e > 0 && lim > 0;
+#pragma unroll
+      for (int r = 0; r < 32; r++) {
+        if (r < nr && colok) {
+          const int cd = io.codes[(int64_t)(r0 + r) * io.Wp + c0 + lane];
+          const int64_t ax = xa[r] < 0 ? -(int64_t)xa[r] : (int64_t)xa[r];
+          ok &= (cd == code) && ax < lim;
+        }
+      }
+      ok = __all_sync(FULL, ok);
+    }
+    if (!ok) {
+      cls = BS_SLOW;
+    } else {
+      cls = (uint8_t)(BS_REG | (code << 2));
+#pragma unroll
+      for (int r = 0; r < 32; r++)
+        sx[comp][r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
+      __syncwarp();
+      // column sum (lane = column) and row sum (lane = row)
+      uint64_t cs = 0, rs = 0;
+#pragma unroll
+      for (int k = 0; k < 32; k++) {
+        cs += sx[comp][k][lane];
+        rs += sx[comp][lane][k];
+      }
+      uint32_t c32, r32;
+      if (ENC) { c32 = (uint32_t)(cs % m); r32 = (uint32_t)(rs % m); }
+      else { c32 = (uint32_t)cs; r32 = (uint32_t)rs; }
+      // inclusive scans over lanes: LB(j) = sum_{b<=j} colsum(b),
+      // LR(i) = sum_{a<=i} rowsum(a)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t pc = __shfl_up_sync(FULL, c32, o);
+        const uint32_t pr = __shfl_up_sync(FULL, r32, o);
+        if (lane >= o) {
+          c32 = ENC ? bs_madd(c32, pc, m) : c32 + pc;
+          r32 = ENC ? bs_madd(r32, pr, m) : r32 + pr;
+        }
+      }
+      io.lb[(comp * nblk + blk) * 32 + lane] = (int32_t)c32;
+      io.lr[(comp * nblk + blk) * 32 + lane] = (int32_t)r32;
+    }
+  }
+  if (lane == 0) io.cls[comp * nblk + blk] = cls;
+}
+
+// ------------------------------------------------------------ phase B
+struct BSChainSmem {
+  uint64_t hin[BS_NW + 1][BS_HRING];   // tagged (column + 1) << 32 | value
+  int done[BS_NW];                     // blocks warp w has consumed
+  int32_t etab[32];
+  uint32_t mtab[32];
+  int task;
+  // slow path tiles, [row][col] unpadded: the skewed sweep reads column
+  // s - lane in row lane, distinct banks across lanes
+  int32_t tv[BS_NW][32][32];           // slow path: values
+  uint16_t ts[BS_NW][32][32];          // slow path: symbols (encoder)
+  uint8_t tc[BS_NW][32][32];           // slow path: codes (encoder)
+};
+
+template <bool ENC>
+__device__ __forceinline__ void bs_slow_block(
+    const BScanIO& io, BSChainSmem& sm, int w, int comp, int bi, int bj,
+    int nr, int ncl, int32_t top, int32_t left, int32_t corner, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const bool colok = lane < ncl;
+  const int32_t* a = io.a[comp];
+  int32_t(*tv)[32] = sm.tv[w];
+  for (int r = 0; r < nr; r++) {
+    const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
+    tv[r][lane] = colok ? __ldcg(a + k) : 0;
+    if (ENC) sm.tc[w][r][lane] = colok ? io.codes[k] : (uint8_t)CODE_LOSSLESS;
+  }
+  const uint32_t pw = lane < nr ? io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
+  __syncwarp();
+  int32_t l = left;
+  int32_t ul = __shfl_up_sync(FULL, left, 1);
+  if (lane == 0) ul = corner;
+  const int32_t radius = io.radius;
+  for (int s = 0; s < 63; s++) {
+    const int jj = s - lane;
+    const bool act = lane < nr && jj >= 0 && jj < ncl;
+    const int32_t bb = __shfl_sync(FULL, top, s & 31);
+    const int32_t up = __shfl_up_sync(FULL, l, 1);
+    const int32_t nu = lane == 0 ? bb : up;
+    if (act) {
+      const int32_t x = tv[lane][jj];
+      int32_t v;
+      uint32_t sy = 0;
+      if ((pw >> jj) & 1u) {
+        v = x;
+      } else if (ENC) {
+        const int32_t e = sm.etab[sm.tc[w][lane][jj] & 31];
+        v = e > 0 ? bs_enc_exact(x, nu + l - ul, e, radius, &sy) : 0;
+      } else {
+        v = (int32_t)((uint32_t)nu + (uint32_t)l - (uint32_t)ul + (uint32_t)x);
+      }
+      tv[lane][jj] = v;
+      if (ENC) sm.ts[w][lane][jj] = (uint16_t)sy;
+      ul = nu;
+      l = v;
+    }
+  }
+  __syncwarp();
+  int32_t* out = io.out[comp];
+  for (int r = 0; r < nr; r++) {
+    const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
+    if (colok) {
+      out[k] = tv[r][lane];
+      if (ENC) io.sym[comp][k] = sm.ts[w][r][lane];
+    }
+  }
+}
+
+template <bool ENC>
+__global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BSChainSmem& sm = *reinterpret_cast<BSChainSmem*>(smem_raw);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int H = io.H, W = io.W, Wp = io.Wp, nbx = io.nbx, nby = io.nby;
+  const int64_t nblk = (int64_t)nbx * nby;
+  const int ntask = bs_ntask(nby);
+  if (threadIdx.x < 32) {
+    sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
+    sm.mtab[threadIdx.x] = io.mag_tab[threadIdx.x];
+  }
+  for (;;) {
+    if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
+    if (threadIdx.x < BS_NW) sm.done[threadIdx.x] = 0;
+    for (int k = threadIdx.x; k < (BS_NW + 1) * BS_HRING; k += blockDim.x)
+      (&sm.hin[0][0])[k] = 0;
+    __syncthreads();
+    const int task = sm.task;
+    if (task >= ntask) break;
+    const int g = task >> 1, comp = task & 1;
+    const int bi = g * BS_NW + w;
+    if (bi < nby) {
+      const int r0 = 32 * bi;
+      const int nr = min(32, H - r0);
+      const bool has_next = bi + 1 < nby;
+      const bool out_smem = has_next && w + 1 < BS_NW;
+      const uint32_t tag_me = io.tag_base + (uint32_t)task + 1u;
+      const uint32_t tag_up = io.tag_base + (uint32_t)task - 1u;   // task - 2
+      uint64_t* my_gb = io.bnd + (int64_t)task * W;
+      const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
+      const int32_t* a = io.a[comp];
+      int32_t* out = io.out[comp];
+      const uint8_t* clsp = io.cls + comp * nblk + (int64_t)bi * nbx;
+      const int32_t* lbp = io.lb + (comp * nblk + (int64_t)bi * nbx) * 32;
+      const int32_t* lrp = io.lr + (comp * nblk + (int64_t)bi * nbx) * 32;
+      int32_t left = 0, corner = 0;
+      // prefetched per-block inputs (independent of the recurrence)
+      uint8_t cls_n = clsp[0];
+      int32_t lb_n = __ldg(lbp + lane), lr_n = __ldg(lrp + lane);
+      for (int bj = 0; bj < nbx; bj++) {
+        const int c0 = 32 * bj;
+        const int ncl = min(32, W - c0);
+        const int c = c0 + lane;
+        const bool colok = lane < ncl;
+        const uint8_t cls = cls_n;
+        const int32_t lbv = lb_n, lrv = lr_n;
+        if (bj + 1 < nbx) {
+          cls_n = clsp[bj + 1];
+          lb_n = __ldg(lbp + 32 * (bj + 1) + lane);
+          lr_n = __ldg(lrp + 32 * (bj + 1) + lane);
+        }
+        // ---- the exact row above the block
+        int32_t top = 0;
+        if (bi > 0) {
+          if (w == 0) {
+            top = TaggedSlot<int32_t>::get(up_gb + c, tag_up, colok);
+          } else {
+            const volatile uint64_t* e = &sm.hin[w][c & (BS_HRING - 1)];
+            uint64_t v = colok ? *e : 0;
+            bool ok = !colok || (uint32_t)(v >> 32) == (uint32_t)(c + 1);
+            while (!__all_sync(FULL, ok)) {
+              if (!ok) {
+                v = *e;
+                ok = (uint32_t)(v >> 32) == (uint32_t)(c + 1);
+              }
+            }
+            top = colok ? (int32_t)(uint32_t)v : 0;
+          }
+          if (!colok) top = 0;
+        }
+        int kind = cls & 3;
+        int32_t bot = 0, right = 0;
+        if (kind == BS_REG) {
+          const int32_t ll = __shfl_sync(FULL, left, nr - 1);
+          const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
+          if (ENC) {
+            const int code = cls >> 2;
+            const uint32_t e = (uint32_t)sm.etab[code];
+            const uint32_t m = 2u * e, M = sm.mtab[code];
+            const uint32_t rc = bs_res(corner, m, M);
+            const uint32_t rb = bs_madd(bs_madd(bs_res(top, m, M), bs_res(ll, m, M), m),
+                                        bs_msub((uint32_t)lbv, rc, m), m);
+            const uint32_t rr = bs_madd(bs_madd(bs_res(left, m, M), bs_res(tl, m, M), m),
+                                        bs_msub((uint32_t)lrv, rc, m), m);
+            const bool tie = (colok && rb == e) || (lane < nr && rr == e);
+            if (__any_sync(FULL, tie)) {
+              kind = BS_SLOW;
+            } else {
+              bot = bs_rep(rb, e, m);
+              right = bs_rep(rr, e, m);
+            }
+          } else {
+            bot = (int32_t)((uint32_t)top + (uint32_t)ll - (uint32_t)corner + (uint32_t)lbv);
+            right = (int32_t)((uint32_t)left + (uint32_t)tl - (uint32_t)corner + (uint32_t)lrv);
+          }
+        } else if (kind == BS_KNOWN) {
+          bot = colok ? __ldcg(a + (int64_t)(r0 + nr - 1) * Wp + c) : 0;
+          right = lane < nr ? __ldcg(a + (int64_t)(r0 + lane) * Wp + c0 + ncl - 1) : 0;
+        }
+        if (kind == BS_SLOW) {
+          bs_slow_block<ENC>(io, sm, w, comp, bi, bj, nr, ncl, top, left, corner, lane);
+          bot = sm.tv[w][nr - 1][lane];
+          right = sm.tv[w][lane][ncl - 1];
+          if (lane == 0) io.cls[comp * nblk + (int64_t)bi * nbx + bj] = BS_DONE;
+          __syncwarp();
+        }
+        if (!colok) bot = 0;
+        if (lane >= nr) right = 0;
+        // ---- hand the bottom row to the block row below
+        if (has_next) {
+          if (out_smem) {
+            spin_ge<0>(&sm.done[w + 1], bj - (BS_HRING / 32 - 1));
+            if (colok)
+              sm.hin[w + 1][c & (BS_HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)bot;
+          } else if (colok) {
+            TaggedSlot<int32_t>::put(my_gb + c, tag_me, bot);
+          }
+        }
+        // ---- the block's exact boundary for the interior pass
+        if (kind != BS_SLOW) {
+          if (colok) out[(int64_t)(r0 + nr - 1) * Wp + c] = bot;
+          if (lane < nr) out[(int64_t)(r0 + lane) * Wp + c0 + ncl - 1] = right;
+        }
+        signal_set(&sm.done[w], bj + 1, lane);
+        corner = __shfl_sync(FULL, top, 31);
+        left = right;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ phase C
+// CTA = one block, warp = component.
+template <bool ENC>
+__global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
+  __shared__ uint32_t sx[2][32][33];
+  __shared__ int32_t sv[2][33][33];
+  __shared__ int32_t etab[32];
+  __shared__ uint32_t mtab[32];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
+  __syncthreads();
+  const int bj = blockIdx.x, bi = blockIdx.y;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const uint8_t cls = io.cls[comp * nblk + blk];
+  const int kind = cls & 3;
+  if (kind == BS_DONE || kind == BS_SLOW) return;   // warp-uniform
+  const int Wp = io.Wp;
+  const int32_t* a = io.a[comp];
+  int32_t* out = io.out[comp];
+  const bool colok = lane < ncl;
+  int32_t xa[32];
+#pragma unroll
+  for (int r = 0; r < 32; r++)
+    xa[r] = (r < nr && colok) ? __ldg(a + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
+  if (kind == BS_KNOWN) {
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      if (r < nr && colok) {
+        const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
+        out[k] = xa[r];
+        if (ENC) io.sym[comp][k] = 0;
+      }
+    }
+    return;
+  }
+  // ---- exact boundary from phase B
+  const int32_t top = (r0 > 0 && colok) ? __ldcg(out + (int64_t)(r0 - 1) * Wp + c0 + lane) : 0;
+  const int32_t left = (c0 > 0 && lane < nr) ? __ldcg(out + (int64_t)(r0 + lane) * Wp + c0 - 1) : 0;
+  const int32_t corner = (r0 > 0 && c0 > 0) ? __ldcg(out + (int64_t)(r0 - 1) * Wp + c0 - 1) : 0;
+  uint32_t e = 0, m = 0, M = 0;
+  if (ENC) {
+    const int code = cls >> 2;
+    e = (uint32_t)etab[code];
+    m = 2u * e;
+    M = mtab[code];
+  }
+  uint32_t(*x)[33] = sx[comp];
+  int32_t(*v)[33] = sv[comp];
+#pragma unroll
+  for (int r = 0; r < 32; r++) x[r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
+  v[0][lane + 1] = top;
+  v[lane + 1][0] = left;
+  if (lane == 0) v[0][0] = corner;
+  __syncwarp();
+  {  // row prefix (lane = row), then column prefix (lane = column)
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      acc = ENC ? bs_madd(acc, x[lane][k], m) : acc + x[lane][k];
+      x[lane][k] = acc;
+    }
+    __syncwarp();
+    acc = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      acc = ENC ? bs_madd(acc, x[k][lane], m) : acc + x[k][lane];
+      x[k][lane] = acc;
+    }
+    __syncwarp();
+  }
+  if (!ENC) {
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      if (r < nr && colok) {
+        const uint32_t val = (uint32_t)top + (uint32_t)v[r + 1][0] - (uint32_t)corner + x[r][lane];
+        out[(int64_t)(r0 + r) * Wp + c0 + lane] = (int32_t)val;
+      }
+    }
+    return;
+  }
+  const uint32_t rt = bs_res(top, m, M), rc = bs_res(corner, m, M);
+  const uint32_t base = bs_msub(rt, rc, m);
+  uint32_t tiem[32];
+  bool anytie = false;
+#pragma unroll
+  for (int r = 0; r < 32; r++) {
+    const uint32_t s = bs_madd(bs_madd(base, bs_res(v[r + 1][0], m, M), m), x[r][lane], m);
+    const bool tie = s == e && r < nr && colok;
+    tiem[r] = __ballot_sync(FULL, tie);
+    anytie |= tiem[r] != 0u;
+    v[r + 1][lane + 1] = tie ? 0 : bs_rep(s, e, m);
+  }
+  __syncwarp();
+  if (anytie) {
+    // raster order: a tie's sign follows x = R0 - (vU + vL - vUL), whose
+    // neighbours may be earlier ties
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      uint32_t tm = tiem[r];
+      while (tm) {
+        const int j = __ffs(tm) - 1;
+        tm &= tm - 1u;
+        if (lane == j) {
+          const int64_t d = (int64_t)v[r][j + 1] + v[r + 1][j] - v[r][j];
+          const int64_t xx = (int64_t)xa[r] - d;
+          v[r + 1][j + 1] = xx > 0 ? (int32_t)e : -(int32_t)e;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  const int32_t radius = io.radius;
+#pragma unroll
+  for (int r = 0; r < 32; r++) {
+    if (r < nr && colok) {
+      const int32_t err = v[r + 1][lane + 1];
+      const int64_t d = (int64_t)v[r][lane + 1] + v[r + 1][lane] - v[r][lane];
+      // x + err = q * 2e exactly
+      const int64_t n = (int64_t)xa[r] - d + err;
+      const uint32_t an = (uint32_t)(n < 0 ? -n : n);
+      uint32_t qa = __umulhi(an, M);
+      if (qa * m != an) qa++;
+      const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
+      const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
+      out[k] = err;
+      io.sym[comp][k] = (uint16_t)(q + radius);
+    }
+  }
+}
+
+template <bool ENC>
+cudaError_t launch_bscan(const BScanIO& io, int nsm, cudaStream_t st) {
+  const dim3 grid(io.nbx, io.nby);
+  bs_local_kernel<ENC><<<grid, 64, 0, st>>>(io);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = sizeof(BSChainSmem);
+  e = cudaFuncSetAttribute(bs_chain_kernel<ENC>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC>,
+                                                    32 * BS_NW, smem);
+  if (e != cudaSuccess) return e;
+  const int ntask = bs_ntask(io.nby);
+  bs_chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  bs_final_kernel<ENC><<<grid, 64, 0, st>>>(io);
+  return cudaGetLastError();
+}
+
+}  // namespace vfcp

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/vfcp_b200.h"
+#include "bscan.cuh"
 #include "chain.cuh"
 #include "common.cuh"
 #include "wavefront.cuh"
@@ -422,6 +423,39 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
   return pp;
 }
 
+// The block-scan chain (bscan.cuh) over the same prepared planes as the
+// strip chain; VFCP_CHAIN=strip selects the strip wavefront instead.
+bool use_bscan() {
+  const char* c = getenv("VFCP_CHAIN");
+  return !(c && strcmp(c, "strip") == 0);
+}
+
+int bscan_setup(Scratch& sc, const ChainIO& io, int nby, cudaStream_t st,
+                BScanIO* b) {
+  memset(b, 0, sizeof(*b));
+  const int64_t nblk = (int64_t)io.nchunks * nby;
+  const int ntask = bs_ntask(nby);
+  b->a[0] = io.a0; b->a[1] = io.a1;
+  b->codes = io.codes;
+  b->pin[0] = io.pin_u; b->pin[1] = io.pin_v;
+  b->sym[0] = io.sym0; b->sym[1] = io.sym1;
+  CK(sc.get(&b->lb, (size_t)2 * nblk * 32));
+  CK(sc.get(&b->lr, (size_t)2 * nblk * 32));
+  CK(sc.get(&b->cls, (size_t)2 * nblk));
+  CK(sc.get(&b->bnd, (size_t)ntask * io.W));
+  CK(cudaMemsetAsync(b->bnd, 0, sizeof(uint64_t) * ntask * io.W, st));
+  b->H = io.H; b->W = io.W; b->Wp = io.Wp; b->nchunks = io.nchunks;
+  b->nbx = io.nchunks; b->nby = nby;
+  b->radius = io.radius;
+  for (int k = 0; k < 32; k++) {
+    b->e_tab[k] = io.e_tab[k];
+    b->mag_tab[k] = io.e_tab[k] > 0
+        ? (uint32_t)((((uint64_t)1) << 32) / (2 * (uint64_t)io.e_tab[k]))
+        : 0u;
+  }
+  return VFCP_OK;
+}
+
 void chain_tables(ChainIO& io, const Ladder& lad) {
   for (int k = 0; k < 32; k++) {
     io.e_tab[k] = (int32_t)lad.e[k];
@@ -532,6 +566,16 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   io.bnd = bnd;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
+  io.codes = codes_p;
+  const bool bscan = use_bscan();
+  BScanIO bio;
+  int* bticket = nullptr;
+  if (bscan) {
+    CK(sc.get(&bticket, (size_t)T));
+    CK(cudaMemsetAsync(bticket, 0, sizeof(int) * T, st));
+    int rcb = bscan_setup(sc, io, nby, st, &bio);
+    if (rcb) return rcb;
+  }
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
@@ -554,7 +598,14 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     io.out_i1 = ecur + plane;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
+    if (bscan) {
+      bio.out[0] = ecur; bio.out[1] = ecur + plane;
+      bio.ticket = bticket + t;
+      bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+      LAUNCH(K_ENCODE, st, launch_bscan<true>(bio, nsm, st));
+    } else {
+      LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
+    }
     if (wprof && t == 1) print_stamps("enc", io.tstamp, H, st);
     LAUNCH(K_LLW, st,
            launch_sym_scatter(syms, syms + plane, pins + 2 * cplane,
@@ -632,6 +683,15 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   io.bnd = bnd;
   io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
   io.radius = p->radius;
+  const bool bscan = use_bscan();
+  BScanIO bio;
+  int* bticket = nullptr;
+  if (bscan) {
+    CK(sc.get(&bticket, (size_t)T));
+    CK(cudaMemsetAsync(bticket, 0, sizeof(int) * T, st));
+    int rcb = bscan_setup(sc, io, nby, st, &bio);
+    if (rcb) return rcb;
+  }
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
@@ -646,7 +706,14 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     io.out_i1 = rcur + plane;
     io.ticket = ticket + t;
     io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
+    if (bscan) {
+      bio.out[0] = rcur; bio.out[1] = rcur + plane;
+      bio.ticket = bticket + t;
+      bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+      LAUNCH(K_DECODE, st, launch_bscan<false>(bio, nsm, st));
+    } else {
+      LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
+    }
     if (wprof && t == 1) print_stamps("dec", io.tstamp, H, st);
     LAUNCH(K_AUX, st,
            launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
