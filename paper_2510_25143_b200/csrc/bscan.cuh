@@ -39,7 +39,7 @@
 //                     resolved in raster order, symbols).
 #pragma once
 
-#include "chain.cuh"
+#include "frame.cuh"
 
 namespace vfcp {
 
@@ -50,10 +50,18 @@ struct BScanIO {
   const uint8_t* codes;     // encoder: frame codes (pitch Wp)
   const uint32_t* pin[2];   // per (row, chunk)
   int32_t* out[2];          // encoder: err; decoder: recon (pitch Wp)
-  uint16_t* sym[2];         // encoder: symbol planes (pitch Wp)
-  int32_t* lb;              // [2][nblk][32] local prefix, block bottom row
-  int32_t* lr;              // [2][nblk][32] local prefix, block right column
-  uint8_t* cls;             // [2][nblk] class | code << 2
+  // encoder, frame t: the interleaved symbol stream (u, v per non-lossless
+  // vertex in raster order; positions from the per-row offsets and the
+  // per-(row, chunk) prefix counts) and the per-row escape counts
+  uint16_t* qd;
+  const int64_t* qd_row_off;  // [H] (frame t)
+  const int32_t* pre_nl;      // [H][nchunks] (frame t)
+  const uint32_t* nlw;        // [H][nchunks] non-lossless bit words
+  int32_t* row_ll;            // [H] (frame t)
+  int32_t* lb;              // [2][nblk][32] block bottom row: local prefix
+                            // (REG) or the known values (KNOWN)
+  int32_t* lr;              // [2][nblk][32] block right column, likewise
+  int32_t* cls;             // [2][nblk] class | code << 2
   uint64_t* bnd;            // tagged boundary slots [ntask][W]
   int* ticket;
   uint32_t tag_base;
@@ -65,6 +73,7 @@ struct BScanIO {
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
+constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
 
 __host__ __device__ inline int bs_ntask(int nby) {
   return 2 * ((nby + BS_NW - 1) / BS_NW);
@@ -138,10 +147,17 @@ __global__ void __launch_bounds__(64) bs_local_kernel(BScanIO io) {
   const bool anypin = __any_sync(FULL, pw != 0u);
   const bool allpin = __all_sync(FULL, lane >= nr || pw == vm);
   __syncthreads();
-  uint8_t cls;
-  if (allpin) cls = BS_KNOWN;
-  else if (anypin) cls = BS_SLOW;
-  else {
+  int32_t cls;
+  if (allpin) {
+    // known values: the chain passes the edges on
+    cls = BS_KNOWN;
+    io.lb[(comp * nblk + blk) * 32 + lane] =
+        lane < ncl ? __ldg(a + (int64_t)(r0 + nr - 1) * io.Wp + c0 + lane) : 0;
+    io.lr[(comp * nblk + blk) * 32 + lane] =
+        lane < nr ? __ldg(a + (int64_t)(r0 + lane) * io.Wp + c0 + ncl - 1) : 0;
+  } else if (anypin) {
+    cls = BS_SLOW;
+  } else {
     const bool colok = lane < ncl;
     int32_t xa[32];
 #pragma unroll
@@ -170,7 +186,7 @@ __global__ void __launch_bounds__(64) bs_local_kernel(BScanIO io) {
     if (!ok) {
       cls = BS_SLOW;
     } else {
-      cls = (uint8_t)(BS_REG | (code << 2));
+      cls = BS_REG | (code << 2);
 #pragma unroll
       for (int r = 0; r < 32; r++)
         sx[comp][r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
@@ -210,10 +226,13 @@ struct BSChainSmem {
   int32_t etab[32];
   uint32_t mtab[32];
   int task;
+  alignas(16) int32_t pf[BS_NW][BS_PF][64];   // LB (0..31), LR (32..63)
+  int32_t pfc[BS_NW][BS_PF];           // class word per block
   // slow path tiles, [row][col] unpadded: the skewed sweep reads column
   // s - lane in row lane, distinct banks across lanes
   int32_t tv[BS_NW][32][32];           // slow path: values
   uint16_t ts[BS_NW][32][32];          // slow path: symbols (encoder)
+  int64_t tq[BS_NW][32];               // slow path: row stream offsets
   uint8_t tc[BS_NW][32][32];           // slow path: codes (encoder)
 };
 
@@ -265,9 +284,29 @@ __device__ __forceinline__ void bs_slow_block(
   int32_t* out = io.out[comp];
   for (int r = 0; r < nr; r++) {
     const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
-    if (colok) {
-      out[k] = tv[r][lane];
-      if (ENC) io.sym[comp][k] = sm.ts[w][r][lane];
+    if (colok) out[k] = tv[r][lane];
+  }
+  if (ENC) {
+    // symbols of the non-pinned (Lorenzo, non-lossless) pixels into the
+    // stream; escapes (symbol 0) counted per row for the ll stream
+    const int64_t pb = (int64_t)(r0 + (lane < nr ? lane : 0)) * io.nchunks + bj;
+    const uint32_t nlr = lane < nr ? io.nlw[pb] : 0u;
+    if (lane < nr)
+      sm.tq[w][lane] = io.qd_row_off[r0 + lane] + 2 * (int64_t)io.pre_nl[pb];
+    __syncwarp();
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int r = 0; r < nr; r++) {
+      const uint32_t pr_w = __shfl_sync(FULL, pw, r);
+      const uint32_t nl_w = __shfl_sync(FULL, nlr, r);
+      const bool put = colok && !((pr_w >> lane) & 1u);
+      int esc = 0;
+      if (put) {
+        const uint16_t sy = sm.ts[w][r][lane];
+        io.qd[sm.tq[w][r] + 2 * __popc(nl_w & lt) + comp] = sy;
+        esc = sy == 0;
+      }
+      const int ne = __reduce_add_sync(FULL, esc);
+      if (lane == 0 && ne) atomicAdd(io.row_ll + r0 + r, ne);
     }
   }
 }
@@ -304,27 +343,37 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
       const uint32_t tag_up = io.tag_base + (uint32_t)task - 1u;   // task - 2
       uint64_t* my_gb = io.bnd + (int64_t)task * W;
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
-      const int32_t* a = io.a[comp];
       int32_t* out = io.out[comp];
-      const uint8_t* clsp = io.cls + comp * nblk + (int64_t)bi * nbx;
+      const int32_t* clsp = io.cls + comp * nblk + (int64_t)bi * nbx;
       const int32_t* lbp = io.lb + (comp * nblk + (int64_t)bi * nbx) * 32;
       const int32_t* lrp = io.lr + (comp * nblk + (int64_t)bi * nbx) * 32;
       int32_t left = 0, corner = 0;
-      // prefetched per-block inputs (independent of the recurrence)
-      uint8_t cls_n = clsp[0];
-      int32_t lb_n = __ldg(lbp + lane), lr_n = __ldg(lrp + lane);
+      // (class, LB, LR) of the next BS_PF blocks in flight (cp.async ring):
+      // they do not depend on the recurrence, so the block step never waits
+      // on DRAM
+      auto stage = [&](int b) {
+        if (b < nbx) {
+          const int s = b % BS_PF;
+          if (lane < 8) cp_async<16>(&sm.pf[w][s][4 * lane], lbp + 32 * b + 4 * lane, true);
+          else if (lane < 16) cp_async<16>(&sm.pf[w][s][32 + 4 * (lane - 8)], lrp + 32 * b + 4 * (lane - 8), true);
+          else if (lane == 16) cp_async<4>(&sm.pfc[w][s], clsp + b, true);
+        }
+        cp_async_commit();
+      };
+#pragma unroll 1
+      for (int b = 0; b < BS_PF; b++) stage(b);
       for (int bj = 0; bj < nbx; bj++) {
         const int c0 = 32 * bj;
         const int ncl = min(32, W - c0);
         const int c = c0 + lane;
         const bool colok = lane < ncl;
-        const uint8_t cls = cls_n;
-        const int32_t lbv = lb_n, lrv = lr_n;
-        if (bj + 1 < nbx) {
-          cls_n = clsp[bj + 1];
-          lb_n = __ldg(lbp + 32 * (bj + 1) + lane);
-          lr_n = __ldg(lrp + 32 * (bj + 1) + lane);
-        }
+        cp_async_wait_group<BS_PF - 1>();
+        __syncwarp();
+        const int slot = bj % BS_PF;
+        const int32_t cls = sm.pfc[w][slot];
+        const int32_t lbv = sm.pf[w][slot][lane], lrv = sm.pf[w][slot][32 + lane];
+        __syncwarp();
+        stage(bj + BS_PF);
         // ---- the exact row above the block
         int32_t top = 0;
         if (bi > 0) {
@@ -370,8 +419,8 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
             right = (int32_t)((uint32_t)left + (uint32_t)tl - (uint32_t)corner + (uint32_t)lrv);
           }
         } else if (kind == BS_KNOWN) {
-          bot = colok ? __ldcg(a + (int64_t)(r0 + nr - 1) * Wp + c) : 0;
-          right = lane < nr ? __ldcg(a + (int64_t)(r0 + lane) * Wp + c0 + ncl - 1) : 0;
+          bot = lbv;
+          right = lrv;
         }
         if (kind == BS_SLOW) {
           bs_slow_block<ENC>(io, sm, w, comp, bi, bj, nr, ncl, top, left, corner, lane);
@@ -423,7 +472,7 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
   const int64_t nblk = (int64_t)io.nbx * io.nby;
   const int64_t blk = (int64_t)bi * io.nbx + bj;
-  const uint8_t cls = io.cls[comp * nblk + blk];
+  const int32_t cls = io.cls[comp * nblk + blk];
   const int kind = cls & 3;
   if (kind == BS_DONE || kind == BS_SLOW) return;   // warp-uniform
   const int Wp = io.Wp;
@@ -440,7 +489,6 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
       if (r < nr && colok) {
         const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
         out[k] = xa[r];
-        if (ENC) io.sym[comp][k] = 0;
       }
     }
     return;
@@ -522,8 +570,15 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
     }
   }
   const int32_t radius = io.radius;
+  // every pixel of a regular block is a non-lossless Lorenzo pixel: row r's
+  // symbols are contiguous in the stream
+  int64_t qb = 0;
+  if (lane < nr)
+    qb = io.qd_row_off[r0 + lane] +
+         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
 #pragma unroll
   for (int r = 0; r < 32; r++) {
+    const int64_t qr = __shfl_sync(FULL, qb, r);
     if (r < nr && colok) {
       const int32_t err = v[r + 1][lane + 1];
       const int64_t d = (int64_t)v[r][lane + 1] + v[r + 1][lane] - v[r][lane];
@@ -535,7 +590,7 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
       const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
       const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
       out[k] = err;
-      io.sym[comp][k] = (uint16_t)(q + radius);
+      io.qd[qr + 2 * lane] = (uint16_t)(q + radius);
     }
   }
 }

@@ -13,7 +13,6 @@
 
 #include "../../include/vfcp_b200.h"
 #include "bscan.cuh"
-#include "chain.cuh"
 #include "common.cuh"
 #include "wavefront.cuh"
 
@@ -62,9 +61,8 @@ cudaError_t launch_chunk_prefix(const uint8_t*, const SYM*, const int64_t*,
                                 int32_t*, cudaStream_t);
 template <typename F>
 cudaError_t launch_enc_r0(const F*, const F*, const uint8_t*, const int32_t*,
-                          const int32_t*, const PrepParams&, int32_t*,
-                          int32_t*, int32_t*, int32_t*, int32_t*, uint8_t*,
-                          int*, cudaStream_t);
+                          const int32_t*, const PrepParams&, int32_t*, int32_t*,
+                          int32_t*, uint8_t*, int*, cudaStream_t);
 template <typename F>
 cudaError_t launch_enc_mop(const F*, const F*, const int32_t*, const int32_t*,
                            const int32_t*, const PrepParams&, const double*,
@@ -81,15 +79,9 @@ cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
                             const int64_t*, const int64_t*, const int32_t*,
                             const int32_t*, const PrepParams&, int32_t*,
                             int32_t*, uint32_t*, uint32_t*, cudaStream_t);
-template <bool ENC>
-cudaError_t launch_chain(const ChainIO&, int, cudaStream_t);
 cudaError_t launch_emit_frame(const int32_t*, const int32_t*, int, int, int,
                               double, double*, double*, int64_t*, int64_t*,
                               cudaStream_t);
-cudaError_t launch_sym_scatter(const uint16_t*, const uint16_t*,
-                               const uint32_t*, const uint32_t*,
-                               const int64_t*, const int32_t*, int, int, int,
-                               int, uint16_t*, int32_t*, cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -423,60 +415,27 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
   return pp;
 }
 
-// The block-scan chain (bscan.cuh) over the same prepared planes as the
-// strip chain; VFCP_CHAIN=strip selects the strip wavefront instead.
-bool use_bscan() {
-  const char* c = getenv("VFCP_CHAIN");
-  return !(c && strcmp(c, "strip") == 0);
-}
-
-int bscan_setup(Scratch& sc, const ChainIO& io, int nby, cudaStream_t st,
-                BScanIO* b) {
+// Tables and scratch of the block-scan chain (bscan.cuh).
+int bscan_setup(Scratch& sc, const Ladder& lad, int H, int W, int radius,
+                cudaStream_t st, BScanIO* b) {
   memset(b, 0, sizeof(*b));
-  const int64_t nblk = (int64_t)io.nchunks * nby;
+  const int nchunks = (W + 31) / 32, nby = (H + 31) / 32;
+  const int64_t nblk = (int64_t)nchunks * nby;
   const int ntask = bs_ntask(nby);
-  b->a[0] = io.a0; b->a[1] = io.a1;
-  b->codes = io.codes;
-  b->pin[0] = io.pin_u; b->pin[1] = io.pin_v;
-  b->sym[0] = io.sym0; b->sym[1] = io.sym1;
   CK(sc.get(&b->lb, (size_t)2 * nblk * 32));
   CK(sc.get(&b->lr, (size_t)2 * nblk * 32));
   CK(sc.get(&b->cls, (size_t)2 * nblk));
-  CK(sc.get(&b->bnd, (size_t)ntask * io.W));
-  CK(cudaMemsetAsync(b->bnd, 0, sizeof(uint64_t) * ntask * io.W, st));
-  b->H = io.H; b->W = io.W; b->Wp = io.Wp; b->nchunks = io.nchunks;
-  b->nbx = io.nchunks; b->nby = nby;
-  b->radius = io.radius;
+  CK(sc.get(&b->bnd, (size_t)ntask * W));
+  CK(cudaMemsetAsync(b->bnd, 0, sizeof(uint64_t) * ntask * W, st));
+  b->H = H; b->W = W; b->Wp = 32 * nchunks; b->nchunks = nchunks;
+  b->nbx = nchunks; b->nby = nby;
+  b->radius = radius;
   for (int k = 0; k < 32; k++) {
-    b->e_tab[k] = io.e_tab[k];
-    b->mag_tab[k] = io.e_tab[k] > 0
-        ? (uint32_t)((((uint64_t)1) << 32) / (2 * (uint64_t)io.e_tab[k]))
-        : 0u;
+    const int64_t e = lad.e[k];
+    b->e_tab[k] = (int32_t)e;
+    b->mag_tab[k] = e > 0 ? (uint32_t)((((uint64_t)1) << 32) / (2 * (uint64_t)e)) : 0u;
   }
   return VFCP_OK;
-}
-
-void chain_tables(ChainIO& io, const Ladder& lad) {
-  for (int k = 0; k < 32; k++) {
-    io.e_tab[k] = (int32_t)lad.e[k];
-  }
-}
-
-// VFCP_WAVE_PROFILE: per-strip start / first-block / end times of one frame
-void print_stamps(const char* tag, unsigned long long* d, int H, cudaStream_t st) {
-  const int K = (H + 31) / 32;
-  std::vector<unsigned long long> h((size_t)3 * 2 * K);
-  if (cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
-                      cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess)
-    return;
-  unsigned long long t0 = ~0ull;
-  for (auto x : h) if (x && x < t0) t0 = x;
-  fprintf(stderr, "[stamps %s] strip: first-block-start end (us, comp u)\n", tag);
-  for (int k = 0; k < K; k += (K > 16 ? K / 16 : 1)) {
-    const unsigned long long* e = &h[(size_t)(2 * k) * 3];
-    fprintf(stderr, "  %4d %9.1f %9.1f\n", k, (e[1] - t0) * 1e-3, (e[2] - t0) * 1e-3);
-  }
 }
 
 int nsm_of() {
@@ -492,34 +451,25 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
                 uint8_t* modes, int32_t* row_ll, cudaStream_t st,
                 bool* overflowed) {
   const int H = p->H, W = p->W, T = p->T;
-  const int64_t HW = (int64_t)H * W;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
   const int64_t nblk = (int64_t)nchunks * nby;
-  const int ntask = chain_ntask(true, H);
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
   uint8_t* codes_p;
   CK(sc.get(&codes_p, (size_t)plane));
-  int32_t *pre_nl, *a, *err;
+  int32_t *pre_nl, *a, *err, *prevrec;
   uint32_t* pins;
-  uint64_t* bnd;
   int *ticket, *ovf;
   double* log2tab = nullptr;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
-  int32_t *prevrec, *q0;
-  uint16_t* syms;
   CK(sc.get(&a, (size_t)2 * plane));
-  CK(sc.get(&q0, (size_t)2 * plane));
   CK(sc.get(&err, (size_t)4 * plane));
   CK(sc.get(&prevrec, (size_t)2 * plane));
-  CK(sc.get(&syms, (size_t)2 * plane));
   CK(sc.get(&pins, (size_t)4 * cplane));
-  CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
   CK(sc.get(&ovf, 1));
-  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
   CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
   CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
@@ -543,39 +493,16 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
                                        (int64_t)T * H, W, nchunks, p->tau,
                                        pre_nl, nullptr, st));
   const Ladder lad = make_ladder(p->tau);
-  ChainIO io;
-  memset(&io, 0, sizeof(io));
-  chain_tables(io, lad);
-  const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
-  std::vector<unsigned long long> tsv;
-  if (wprof) {
-    CK(sc.get(&io.stats, WP_N));
-    io.stats_strip0 = strcmp(getenv("VFCP_WAVE_PROFILE"), "strip0") == 0;
-    CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
-    CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
-    CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
-  }
-  io.a0 = a;
-  io.a1 = a + plane;
-  io.pin_u = pins;
-  io.pin_v = pins + cplane;
-  io.q0_0 = q0;
-  io.q0_1 = q0 + plane;
-  io.sym0 = syms;
-  io.sym1 = syms + plane;
-  io.bnd = bnd;
-  io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
-  io.radius = p->radius;
-  io.codes = codes_p;
-  const bool bscan = use_bscan();
   BScanIO bio;
-  int* bticket = nullptr;
-  if (bscan) {
-    CK(sc.get(&bticket, (size_t)T));
-    CK(cudaMemsetAsync(bticket, 0, sizeof(int) * T, st));
-    int rcb = bscan_setup(sc, io, nby, st, &bio);
-    if (rcb) return rcb;
+  {
+    int rc = bscan_setup(sc, lad, H, W, p->radius, st, &bio);
+    if (rc) return rc;
   }
+  bio.a[0] = a; bio.a[1] = a + plane;
+  bio.codes = codes_p;
+  bio.pin[0] = pins; bio.pin[1] = pins + cplane;
+  bio.qd = qd;
+  bio.nlw = pins + 2 * cplane;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
@@ -583,7 +510,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
     LAUNCH(K_PREP, st,
            launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, a, a + plane,
-                            q0, q0 + plane, prevrec, codes_p, ovf, st));
+                            prevrec, codes_p, ovf, st));
     if (pp.mop)
       LAUNCH(K_MOP, st,
              launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
@@ -593,37 +520,13 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
                              modes_t, a, a + plane, pins, pins + cplane,
                              pins + 2 * cplane, pins + 3 * cplane, qd, row_ll,
                              st));
-    io.codes = codes_p;
-    io.out_i0 = ecur;
-    io.out_i1 = ecur + plane;
-    io.ticket = ticket + t;
-    io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    if (bscan) {
-      bio.out[0] = ecur; bio.out[1] = ecur + plane;
-      bio.ticket = bticket + t;
-      bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
-      LAUNCH(K_ENCODE, st, launch_bscan<true>(bio, nsm, st));
-    } else {
-      LAUNCH(K_ENCODE, st, launch_chain<true>(io, nsm, st));
-    }
-    if (wprof && t == 1) print_stamps("enc", io.tstamp, H, st);
-    LAUNCH(K_LLW, st,
-           launch_sym_scatter(syms, syms + plane, pins + 2 * cplane,
-                              pins + 3 * cplane, qd_row_off + (size_t)t * H,
-                              pre_nl + (size_t)t * cplane, H, W, Wp, nchunks,
-                              qd, row_ll + (size_t)t * H, st));
-  }
-  if (wprof) {
-    unsigned long long h[WP_N];
-    CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    fprintf(stderr,
-            "[chain %s] C: waitchunk=%.3g waitbnd=%.3g sweep=%.3g handoff=%.3g"
-            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)"
-            " redo-blocks=%llu preload=%.3g\n",
-            "enc", (double)h[WP_WAITPREV], (double)h[WP_WAITBND],
-            (double)h[WP_CHAIN], (double)h[WP_X3], (double)h[WP_X1],
-            (double)h[WP_WRITE], (double)h[WP_PRE], h[WP_X2], (double)h[WP_TASKS]);
+    bio.out[0] = ecur; bio.out[1] = ecur + plane;
+    bio.ticket = ticket + t;
+    bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+    bio.qd_row_off = qd_row_off + (size_t)t * H;
+    bio.pre_nl = pre_nl + (size_t)t * cplane;
+    bio.row_ll = row_ll + (size_t)t * H;
+    LAUNCH(K_ENCODE, st, launch_bscan<true>(bio, nsm, st));
   }
   int h_ovf = 0;
   CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -642,56 +545,31 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
   const int64_t nblk = (int64_t)nchunks * nby;
-  const int ntask = chain_ntask(false, H);
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
   int32_t *pre_nl, *pre_ll, *a, *rec;
   uint32_t* pins;
-  uint64_t* bnd;
   int* ticket;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
   CK(sc.get(&pre_ll, (size_t)T * cplane));
   CK(sc.get(&a, (size_t)2 * plane));
   CK(sc.get(&rec, (size_t)4 * plane));
   CK(sc.get(&pins, (size_t)2 * cplane));
-  CK(sc.get(&bnd, (size_t)ntask * W));
   CK(sc.get(&ticket, (size_t)T));
-  CK(cudaMemsetAsync(bnd, 0, sizeof(uint64_t) * ntask * W, st));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
   LAUNCH(K_SCAN, st,
          launch_chunk_prefix<uint16_t>(codes, qd, qd_row_off, (int64_t)T * H,
                                        W, nchunks, p->tau, pre_nl, pre_ll,
                                        st));
   const Ladder lad = make_ladder(p->tau);
-  ChainIO io;
-  memset(&io, 0, sizeof(io));
-  chain_tables(io, lad);
-  const bool wprof = getenv("VFCP_WAVE_PROFILE") != nullptr;
-  std::vector<unsigned long long> tsv;
-  if (wprof) {
-    CK(sc.get(&io.stats, WP_N));
-    io.stats_strip0 = strcmp(getenv("VFCP_WAVE_PROFILE"), "strip0") == 0;
-    CK(cudaMemsetAsync(io.stats, 0, sizeof(unsigned long long) * WP_N, st));
-    CK(sc.get(&io.tstamp, (size_t)3 * 4 * H));
-    CK(cudaMemsetAsync(io.tstamp, 0, sizeof(unsigned long long) * 3 * 4 * H, st));
-  }
-  io.a0 = a;
-  io.a1 = a + plane;
-  io.pin_u = pins;
-  io.pin_v = pins + cplane;
-  io.bnd = bnd;
-  io.H = H; io.W = W; io.Wp = Wp; io.nchunks = nchunks;
-  io.radius = p->radius;
-  const bool bscan = use_bscan();
   BScanIO bio;
-  int* bticket = nullptr;
-  if (bscan) {
-    CK(sc.get(&bticket, (size_t)T));
-    CK(cudaMemsetAsync(bticket, 0, sizeof(int) * T, st));
-    int rcb = bscan_setup(sc, io, nby, st, &bio);
-    if (rcb) return rcb;
+  {
+    int rc = bscan_setup(sc, lad, H, W, p->radius, st, &bio);
+    if (rc) return rc;
   }
+  bio.a[0] = a; bio.a[1] = a + plane;
+  bio.pin[0] = pins; bio.pin[1] = pins + cplane;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
@@ -702,35 +580,15 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr, rprev,
                rprev + plane, qd_row_off, ll_row_off, pre_nl, pre_ll, pp, a,
                a + plane, pins, pins + cplane, st));
-    io.out_i0 = rcur;
-    io.out_i1 = rcur + plane;
-    io.ticket = ticket + t;
-    io.tag_base = (uint32_t)t * (uint32_t)ntask;
-    if (bscan) {
-      bio.out[0] = rcur; bio.out[1] = rcur + plane;
-      bio.ticket = bticket + t;
-      bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
-      LAUNCH(K_DECODE, st, launch_bscan<false>(bio, nsm, st));
-    } else {
-      LAUNCH(K_DECODE, st, launch_chain<false>(io, nsm, st));
-    }
-    if (wprof && t == 1) print_stamps("dec", io.tstamp, H, st);
+    bio.out[0] = rcur; bio.out[1] = rcur + plane;
+    bio.ticket = ticket + t;
+    bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+    LAUNCH(K_DECODE, st, launch_bscan<false>(bio, nsm, st));
     LAUNCH(K_AUX, st,
            launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
                              out_u + (size_t)t * HW, out_v + (size_t)t * HW,
                              fix_u ? fix_u + (size_t)t * HW : nullptr,
                              fix_v ? fix_v + (size_t)t * HW : nullptr, st));
-  }
-  if (wprof) {
-    unsigned long long h[WP_N];
-    CK(cudaMemcpyAsync(h, io.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    fprintf(stderr,
-            "[chain %s] C: waitchunk=%.3g waitbnd=%.3g sweep=%.3g handoff=%.3g"
-            " | P: waitdone=%.3g writeout=%.3g stage+split=%.3g (warp-cycles)\n",
-            "dec", (double)h[WP_WAITPREV], (double)h[WP_WAITBND],
-            (double)h[WP_CHAIN], (double)h[WP_X3], (double)h[WP_X1],
-            (double)h[WP_WRITE], (double)h[WP_PRE]);
   }
   return VFCP_OK;
 }

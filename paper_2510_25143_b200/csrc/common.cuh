@@ -78,9 +78,25 @@ __device__ __forceinline__ int32_t fixed_of(double x, double S) {
   return y > 0.0 ? q : (y < 0.0 ? -q : 0);
 }
 
+// binary32 input: x*S is exact in binary32 (S = 2^k, |x*S| < 2^30), and so
+// are its integer and fractional parts, so rounding half away from zero in
+// binary32 gives the reference's binary64 result with a few FP32 ops.
+__device__ __forceinline__ int32_t fixed_of_f32(float x, float S) {
+  const float y = __fmul_rn(x, S);
+  const float t = truncf(y);
+  const float f = __fsub_rn(y, t);
+  return (int32_t)t + (f >= 0.5f ? 1 : 0) - (f <= -0.5f ? 1 : 0);
+}
+__device__ __forceinline__ int32_t fixed_t(float x, double S) {
+  return fixed_of_f32(x, (float)S);
+}
+__device__ __forceinline__ int32_t fixed_t(double x, double S) {
+  return fixed_of(x, S);
+}
+
 template <typename F>
 __device__ __forceinline__ int32_t load_fixed(const F* p, int64_t k, double S) {
-  return fixed_of((double)__ldg(p + k), S);
+  return fixed_t(__ldg(p + k), S);
 }
 
 // Exact rha(x / (2e)) for integer x, e > 0 (equal to the reference's

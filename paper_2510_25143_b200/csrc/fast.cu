@@ -1,23 +1,22 @@
-// Frame-parallel preparation kernels + the chain wavefront (chain.cuh).
+// Frame-parallel preparation kernels around the block-scan chain
+// (bscan.cuh).
 //
 // Per frame t the compress path runs
-//   enc_prep_kernel  one warp per 32x32 block: MoP mode selection
-//                    (mop.py:68-151: Lorenzo trial with block-local
-//                    write-back, semi-Lagrangian trial at the stride samples,
-//                    first-touch entropy, theta gate), then every pixel that
-//                    does not need its reconstructed neighbours: lossless
-//                    pins, semi-Lagrangian pixels (prediction, symbol, err)
-//                    and, for Lorenzo pixels, R0 = orig - Lorenzo(orig, prev)
-//                    for the error-form chain;
-//   chain_kernel<ENC>  the raster recurrence (chain.cuh);
+//   enc_r0_kernel    R0 = orig - Lorenzo(orig, prev), the frame t-1
+//                    reconstruction as (u, v) pairs, the padded codes copy;
+//   enc_mop_kernel   (t >= 1, MoP) the per-block mode decision;
+//   enc_pix_kernel   lossless pins, semi-Lagrangian pixels (prediction,
+//                    symbol, pinned err), per-chunk bit words;
+//   launch_bscan<ENC>  the raster recurrence, the Lorenzo symbols into the
+//                    stream;
 // and the decompress path
-//   dec_prep_kernel  one warp per 32x32 block: pins (lossless, escapes,
-//                    semi-Lagrangian pixels) and A = Pd + (sym-radius)*2e;
-//   chain_kernel<DEC>.
+//   dec_prep_kernel  pins (lossless, escapes, semi-Lagrangian pixels) and
+//                    A = Pd + (sym-radius)*2e;
+//   launch_bscan<DEC>, emit_frame_kernel.
 // The reconstruction of frame t-1 is read as orig + err (encoder) or the int
 // recon frame (decoder).  Stream positions come from per-(row, chunk) prefix
 // counts, so any block can place its symbols and ll values.
-#include "chain.cuh"
+#include "bscan.cuh"
 
 namespace vfcp {
 
@@ -263,7 +262,6 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
               const int32_t* __restrict__ err_prev_u,
               const int32_t* __restrict__ err_prev_v, PrepParams p,
               int32_t* __restrict__ a0, int32_t* __restrict__ a1,
-              int32_t* __restrict__ q0u, int32_t* __restrict__ q0v,
               int2* __restrict__ prevrec, uint8_t* __restrict__ codes_p,
               int* __restrict__ overflow) {
   // one 32x32 tile per CTA; every input value is converted to fixed point
@@ -307,10 +305,10 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
     if (k >= 33 * 33) break;
     const int rr = k / 33, cc = k - rr * 33;
     const bool ok = okk[q];
-    so[0][rr][cc] = ok ? fixed_of((double)xo_u[q], p.S) : 0;
-    so[1][rr][cc] = ok ? fixed_of((double)xo_v[q], p.S) : 0;
-    sp[0][rr][cc] = (ok && has_prev) ? fixed_of((double)xp_u[q], p.S) + xe_u[q] : 0;
-    sp[1][rr][cc] = (ok && has_prev) ? fixed_of((double)xp_v[q], p.S) + xe_v[q] : 0;
+    so[0][rr][cc] = ok ? fixed_t(xo_u[q], p.S) : 0;
+    so[1][rr][cc] = ok ? fixed_t(xo_v[q], p.S) : 0;
+    sp[0][rr][cc] = (ok && has_prev) ? fixed_t(xp_u[q], p.S) + xe_u[q] : 0;
+    sp[1][rr][cc] = (ok && has_prev) ? fixed_t(xp_v[q], p.S) + xe_v[q] : 0;
   }
   __syncthreads();
   bool ovf = false;
@@ -334,14 +332,8 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
     ovf |= o;
     const int64_t pr = (int64_t)i * Wp + j;
     const int cd = colok ? codes[(int64_t)p.t * HW + (int64_t)i * W + j] : CODE_LOSSLESS;
-    // the chain's split R0 = Q0*2e + rho (e < 2^28 on this path)
-    const int32_t e = (int32_t)p.lad.e[cd];
-    const double inv = p.lad.inv2e[cd];
-    const int32_t ru = colok ? (int32_t)R_u : 0, rv = colok ? (int32_t)R_v : 0;
-    a0[pr] = ru;
-    a1[pr] = rv;
-    q0u[pr] = (e != 0 && !o) ? quant32(ru, e, inv) : 0;
-    q0v[pr] = (e != 0 && !o) ? quant32(rv, e, inv) : 0;
+    a0[pr] = colok ? (int32_t)R_u : 0;
+    a1[pr] = colok ? (int32_t)R_v : 0;
     if (has_prev) prevrec[pr] = make_int2(sp[0][rr + 1][tx + 1], sp[1][rr + 1][tx + 1]);
     codes_p[pr] = (uint8_t)cd;
   }
@@ -698,39 +690,6 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
   }
 }
 
-// ------------------------------------------------ encoder symbol scatter
-// warp per (row, chunk): the chain's symbol planes into the interleaved
-// symbol stream (u then v per non-lossless pixel, raster order) and the
-// escapes into the per-row ll counts
-__global__ void __launch_bounds__(256)
-enc_sym_scatter_kernel(const uint16_t* __restrict__ s0,
-                       const uint16_t* __restrict__ s1,
-                       const uint32_t* __restrict__ nlw,
-                       const uint32_t* __restrict__ symw,
-                       const int64_t* __restrict__ qd_row_off,
-                       const int32_t* __restrict__ pre_nl, int H, int W,
-                       int Wp, int nchunks, uint16_t* __restrict__ qd,
-                       int32_t* __restrict__ row_ll) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (bj >= nchunks) return;
-  const int64_t pb = (int64_t)i * nchunks + bj;
-  const uint32_t sw = symw[pb];
-  if (sw == 0) return;   // warp-uniform
-  const uint32_t nl = nlw[pb];
-  const uint32_t bit = 1u << lane;
-  int ne = 0;
-  if (sw & bit) {
-    const int64_t k = (int64_t)i * Wp + 32 * bj + lane;
-    const uint32_t su = s0[k], sv = s1[k];
-    const int64_t pos = qd_row_off[i] + 2 * ((int64_t)pre_nl[pb] + __popc(nl & (bit - 1u)));
-    *reinterpret_cast<uint32_t*>(qd + pos) = su | (sv << 16);
-    ne = (su == 0) + (sv == 0);
-  }
-  const int tot = __reduce_add_sync(0xffffffffu, ne);
-  if (lane == 0 && tot) atomicAdd(row_ll + i, tot);
-}
-
 // ------------------------------------------------ decoder frame output
 // int32 recon frame (pitch Wp) -> float64 output (and optionally int64)
 __global__ void __launch_bounds__(256)
@@ -765,11 +724,11 @@ template <typename F>
 cudaError_t launch_enc_r0(const F* u, const F* v, const uint8_t* codes,
                           const int32_t* eu, const int32_t* ev,
                           const PrepParams& p, int32_t* a0, int32_t* a1,
-                          int32_t* q0u, int32_t* q0v, int32_t* prevrec,
-                          uint8_t* codes_p, int* overflow, cudaStream_t st) {
+                          int32_t* prevrec, uint8_t* codes_p, int* overflow,
+                          cudaStream_t st) {
   const dim3 grid(p.nchunks, p.nby);
   enc_r0_kernel<F><<<grid, 256, 0, st>>>(
-      u, v, codes, eu, ev, p, a0, a1, q0u, q0v,
+      u, v, codes, eu, ev, p, a0, a1,
       reinterpret_cast<int2*>(prevrec), codes_p, overflow);
   return cudaGetLastError();
 }
@@ -824,34 +783,6 @@ cudaError_t launch_emit_frame(const int32_t* ru, const int32_t* rv, int H,
   return cudaGetLastError();
 }
 
-cudaError_t launch_sym_scatter(const uint16_t* s0, const uint16_t* s1,
-                               const uint32_t* nlw, const uint32_t* symw,
-                               const int64_t* qd_row_off,
-                               const int32_t* pre_nl, int H, int W, int Wp,
-                               int nchunks, uint16_t* qd, int32_t* row_ll,
-                               cudaStream_t st) {
-  const dim3 grid((nchunks + 7) / 8, H);
-  enc_sym_scatter_kernel<<<grid, 256, 0, st>>>(
-      s0, s1, nlw, symw, qd_row_off, pre_nl, H, W, Wp, nchunks, qd, row_ll);
-  return cudaGetLastError();
-}
-
-template <bool ENC>
-cudaError_t launch_chain(const ChainIO& io, int nsm, cudaStream_t st) {
-  const size_t smem = sizeof(ChainSmem<ENC>);
-  cudaError_t e = cudaFuncSetAttribute(
-      chain_kernel<ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      (int)smem);
-  if (e != cudaSuccess) return e;
-  const int threads = 64 * chain_pairs(ENC);
-  int occ = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chain_kernel<ENC>,
-                                                    threads, smem);
-  if (e != cudaSuccess) return e;
-  const int ntask = chain_ntask(ENC, io.H);
-  chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), threads, smem, st>>>(io);
-  return cudaGetLastError();
-}
 
 template cudaError_t launch_chunk_prefix<uint16_t>(const uint8_t*,
                                                    const uint16_t*,
@@ -863,8 +794,7 @@ template cudaError_t launch_enc_r0<float>(const float*, const float*,
                                           const uint8_t*, const int32_t*,
                                           const int32_t*, const PrepParams&,
                                           int32_t*, int32_t*, int32_t*,
-                                          int32_t*, int32_t*, uint8_t*, int*,
-                                          cudaStream_t);
+                                          uint8_t*, int*, cudaStream_t);
 template cudaError_t launch_enc_mop<float>(const float*, const float*,
                                            const int32_t*, const int32_t*,
                                            const int32_t*, const PrepParams&,
@@ -879,8 +809,7 @@ template cudaError_t launch_enc_r0<double>(const double*, const double*,
                                           const uint8_t*, const int32_t*,
                                           const int32_t*, const PrepParams&,
                                           int32_t*, int32_t*, int32_t*,
-                                          int32_t*, int32_t*, uint8_t*, int*,
-                                          cudaStream_t);
+                                          uint8_t*, int*, cudaStream_t);
 template cudaError_t launch_enc_mop<double>(const double*, const double*,
                                            const int32_t*, const int32_t*,
                                            const int32_t*, const PrepParams&,
@@ -896,7 +825,5 @@ template cudaError_t launch_dec_prep<uint16_t>(
     const int32_t*, const int32_t*, const int64_t*, const int64_t*,
     const int32_t*, const int32_t*, const PrepParams&, int32_t*, int32_t*,
     uint32_t*, uint32_t*, cudaStream_t);
-template cudaError_t launch_chain<true>(const ChainIO&, int, cudaStream_t);
-template cudaError_t launch_chain<false>(const ChainIO&, int, cudaStream_t);
 
 }  // namespace vfcp
