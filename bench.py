@@ -40,6 +40,12 @@ ALGO_BYTES = {
     "encode": 8.0 + 1.0 + 4.0,         # fp32 u,v + code in; 2 x u16 out
     "mop": 8.0,                        # fp32 u,v of the frame
     "decode": 1.0 + 4.0 + 16.0,        # code + 2 x u16 in; 2 x f64 out
+    # block-scan chain (encoder): prepared R0 planes + codes in (local);
+    # R0 in, err planes + 2 x u16 symbols out (final); the chain itself
+    # moves two 32-value edges per 32x32 block and component
+    "bs_local": 8.0 + 1.0,
+    "bs_chain": 2 * 2 * 32 * 4 / 1024.0,
+    "bs_final": 8.0 + 8.0 + 4.0,
 }
 
 
@@ -315,6 +321,8 @@ def main():
     dom = max((k for k in prof if prof[k][1]), key=lambda k: prof[k][0])
     dom_ms_per_launch = prof[dom][0] / prof[dom][1]
     units_per_launch = {"analyze": N, "encode": H * W, "mop": H * W,
+                        "bs_local": H * W, "bs_chain": H * W,
+                        "bs_final": H * W,
                         "range": N, "scan": T * H, "ll_write": N,
                         "aux": H * W}.get(dom, N)
     algo = ALGO_BYTES.get(dom, 0.0) * units_per_launch

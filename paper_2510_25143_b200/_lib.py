@@ -68,7 +68,8 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
-                  "decode_rows", "decode_ll", "decode", "aux", "prep")
+                  "decode_rows", "decode_ll", "decode", "aux", "prep",
+                  "bs_local", "bs_chain", "bs_final")
 
 
 def prof_enable(on=True):

@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
         // ---- hand the bottom row to the block row below
         if (has_next) {
           if (out_smem) {
-            spin_ge<0>(&sm.done[w + 1], bj - (BS_HRING / 32 - 1));
+            // ring slots of block bj - 8 must have been read (the reads fed
+            // the consumer's computation before it bumped its counter)
+            while (!__all_sync(FULL, *(volatile int*)&sm.done[w + 1] >= bj - (BS_HRING / 32 - 1))) {
+            }
             if (colok)
               sm.hin[w + 1][c & (BS_HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)bot;
           } else if (colok) {
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
           if (colok) out[(int64_t)(r0 + nr - 1) * Wp + c] = bot;
           if (lane < nr) out[(int64_t)(r0 + lane) * Wp + c0 + ncl - 1] = right;
         }
-        signal_set(&sm.done[w], bj + 1, lane);
+        if (lane == 0) *(volatile int*)&sm.done[w] = bj + 1;
         corner = __shfl_sync(FULL, top, 31);
         left = right;
       }
@@ -596,24 +599,30 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
 }
 
 template <bool ENC>
-cudaError_t launch_bscan(const BScanIO& io, int nsm, cudaStream_t st) {
-  const dim3 grid(io.nbx, io.nby);
-  bs_local_kernel<ENC><<<grid, 64, 0, st>>>(io);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+cudaError_t launch_bs_local(const BScanIO& io, cudaStream_t st) {
+  bs_local_kernel<ENC><<<dim3(io.nbx, io.nby), 64, 0, st>>>(io);
+  return cudaGetLastError();
+}
+
+template <bool ENC>
+cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   const size_t smem = sizeof(BSChainSmem);
-  e = cudaFuncSetAttribute(bs_chain_kernel<ENC>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(
+      bs_chain_kernel<ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 1;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC>,
                                                     32 * BS_NW, smem);
   if (e != cudaSuccess) return e;
   const int ntask = bs_ntask(io.nby);
+  // persistent: every CTA is resident, tickets in block-row order
   bs_chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  bs_final_kernel<ENC><<<grid, 64, 0, st>>>(io);
+  return cudaGetLastError();
+}
+
+template <bool ENC>
+cudaError_t launch_bs_final(const BScanIO& io, cudaStream_t st) {
+  bs_final_kernel<ENC><<<dim3(io.nbx, io.nby), 64, 0, st>>>(io);
   return cudaGetLastError();
 }
 

@@ -106,7 +106,7 @@ int fail(int code, const std::string& msg) {
 // counts it and, when profiling is on, brackets it with CUDA events on the
 // launching stream (vfcp_prof_*).
 enum KClass { K_RANGE, K_ANALYZE, K_SCAN, K_MOP, K_ENCODE, K_LLW, K_DROWS,
-              K_DLL, K_DECODE, K_AUX, K_PREP, K_NCLS };
+              K_DLL, K_DECODE, K_AUX, K_PREP, K_BSL, K_BSC, K_BSF, K_NCLS };
 struct Prof {
   bool on = false;
   int64_t launches = 0;
@@ -526,7 +526,9 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.row_ll = row_ll + (size_t)t * H;
-    LAUNCH(K_ENCODE, st, launch_bscan<true>(bio, nsm, st));
+    LAUNCH(K_BSL, st, launch_bs_local<true>(bio, st));
+    LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
+    LAUNCH(K_BSF, st, launch_bs_final<true>(bio, st));
   }
   int h_ovf = 0;
   CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -583,7 +585,9 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     bio.out[0] = rcur; bio.out[1] = rcur + plane;
     bio.ticket = ticket + t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
-    LAUNCH(K_DECODE, st, launch_bscan<false>(bio, nsm, st));
+    LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
+    LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
+    LAUNCH(K_BSF, st, launch_bs_final<false>(bio, st));
     LAUNCH(K_AUX, st,
            launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
                              out_u + (size_t)t * HW, out_v + (size_t)t * HW,
