@@ -406,9 +406,93 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
     (&sm.cnt[0][0])[k] = 0;
   }
   __syncthreads();
+  bool swept = false;
   if (wid < 2) {
-    // split R0 = Q0*2e + rho for the whole tile first (independent per
-    // pixel, lane = column), so the sweep below is only the recurrence
+    // Lorenzo trial of component wid with block-local errors (mop.py:88-110).
+    // Every pixel uses the step tau', so unless a pixel can escape
+    // (|R0| >= (2 radius - 4) tau') the trial errors are the representatives
+    // of the block's 2D prefix sums of -R0 mod 2 tau' (see bscan.cuh), with
+    // a zero boundary (outside the block the candidate is the original).
+    const int comp = wid;
+    const int64_t lim = (2 * (int64_t)radius - 4) * tau;
+    bool safe = lim > 0;
+#pragma unroll 8
+    for (int r = 0; r < 32; r++) {
+      const int32_t x0 = sm.r0[comp][r][lane];
+      safe &= (x0 < 0 ? -(int64_t)x0 : (int64_t)x0) < lim;
+    }
+    swept = !__all_sync(FULL, safe);
+    if (!swept) {
+      const uint32_t m = 2u * (uint32_t)e, ue = (uint32_t)e;
+      const uint32_t M = (uint32_t)((((uint64_t)1) << 32) / m);
+      int32_t(*v)[33] = sm.q0[comp];
+      int32_t(*x)[33] = sm.r0[comp];
+#pragma unroll 8
+      for (int r = 0; r < 32; r++) v[r][lane] = (int32_t)bs_negres(x[r][lane], m, M);
+      __syncwarp();
+      uint32_t acc = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; k++) {   // row prefix, lane = row
+        acc = bs_madd(acc, (uint32_t)v[lane][k], m);
+        v[lane][k] = (int32_t)acc;
+      }
+      __syncwarp();
+      acc = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; k++) {   // column prefix, lane = column
+        acc = bs_madd(acc, (uint32_t)v[k][lane], m);
+        v[k][lane] = (int32_t)acc;
+      }
+      bool anytie = false;
+      uint32_t tiem[32];
+#pragma unroll
+      for (int r = 0; r < 32; r++) {
+        const uint32_t sres = (uint32_t)v[r][lane];
+        const bool tie = sres == ue && r < nr && lane < ncl;
+        tiem[r] = __ballot_sync(FULL, tie);
+        anytie |= tiem[r] != 0u;
+        v[r][lane] = tie ? 0 : bs_rep(sres, ue, m);
+      }
+      __syncwarp();
+      if (anytie && lane == 0) {
+        // raster order: the tie's sign follows x = R0 - D
+#pragma unroll 1
+        for (int r = 0; r < 32; r++) {
+          uint32_t tm = tiem[r];
+          while (tm) {
+            const int j = __ffs(tm) - 1;
+            tm &= tm - 1u;
+            const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
+                              (j > 0 ? (int64_t)v[r][j - 1] : 0) -
+                              ((r > 0 && j > 0) ? (int64_t)v[r - 1][j - 1] : 0);
+            v[r][j] = ((int64_t)x[r][j] - d) > 0 ? e : -e;
+          }
+        }
+      }
+      __syncwarp();
+      // |idx| at the stride samples: x + err = q * 2 tau' exactly
+      const bool scol = lane < ncl && (lane % p.stride) == 0;
+      const int sj = lane / p.stride;
+#pragma unroll 1
+      for (int r = 0; r < nr; r += p.stride) {
+        if (scol) {
+          const int j = lane;
+          const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
+                            (j > 0 ? (int64_t)v[r][j - 1] : 0) -
+                            ((r > 0 && j > 0) ? (int64_t)v[r - 1][j - 1] : 0);
+          const int64_t n = (int64_t)x[r][j] - d + v[r][j];
+          const uint32_t an = (uint32_t)(n < 0 ? -n : n);
+          uint32_t qa = __umulhi(an, M);
+          if (qa * m != an) qa++;
+          sm.samp[0][2 * ((r / p.stride) * nsx + sj) + comp] = (int32_t)qa;
+        }
+      }
+    }
+  }
+  if (wid < 2 && swept) {
+    // escapes possible: the exact sweep.  Split R0 = Q0*2e + rho for the
+    // whole tile first (independent per pixel, lane = column), so the
+    // sweep below is only the recurrence
     {
       const int comp = wid;
 #pragma unroll 8
@@ -448,7 +532,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
         if (++jm == p.stride) { jm = 0; jq++; }
       }
     }
-  } else {
+  } else if (wid >= 2) {
     // semi-Lagrangian trial at the stride samples, 64 threads; samples of
     // a thread in lockstep so their departure-point gathers overlap
     const int64_t HW = (int64_t)H * W;
