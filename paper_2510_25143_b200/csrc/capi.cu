@@ -61,8 +61,9 @@ cudaError_t launch_chunk_prefix(const uint8_t*, const SYM*, const int64_t*,
                                 int32_t*, cudaStream_t);
 template <typename F>
 cudaError_t launch_enc_r0(const F*, const F*, const uint8_t*, const int32_t*,
-                          const int32_t*, const PrepParams&, int32_t*, int32_t*,
-                          int32_t*, uint8_t*, int*, cudaStream_t);
+                          const int32_t*, const PrepParams&, const BScanIO&,
+                          int32_t*, int32_t*, int32_t*, uint8_t*, int*,
+                          cudaStream_t);
 template <typename F>
 cudaError_t launch_enc_mop(const F*, const F*, const int32_t*, const int32_t*,
                            const int32_t*, const PrepParams&, const double*,
@@ -70,7 +71,7 @@ cudaError_t launch_enc_mop(const F*, const F*, const int32_t*, const int32_t*,
 template <typename F>
 cudaError_t launch_enc_pix(const F*, const F*, const uint8_t*, const int32_t*,
                            const int64_t*, const int32_t*, const PrepParams&,
-                           const uint8_t*, int32_t*, int32_t*, uint32_t*,
+                           const uint8_t*, const BScanIO&, int32_t*, int32_t*,
                            uint32_t*, uint32_t*, uint32_t*, uint16_t*,
                            int32_t*, cudaStream_t);
 template <typename SYM>
@@ -467,7 +468,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   CK(sc.get(&a, (size_t)2 * plane));
   CK(sc.get(&err, (size_t)4 * plane));
   CK(sc.get(&prevrec, (size_t)2 * plane));
-  CK(sc.get(&pins, (size_t)4 * cplane));
+  CK(sc.get(&pins, (size_t)3 * cplane));
   CK(sc.get(&ticket, (size_t)T));
   CK(sc.get(&ovf, 1));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
@@ -509,24 +510,22 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     int32_t* ecur = err + 2 * plane * (t & 1);
     uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
     LAUNCH(K_PREP, st,
-           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, a, a + plane,
-                            prevrec, codes_p, ovf, st));
+           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, bio, a,
+                            a + plane, prevrec, codes_p, ovf, st));
     if (pp.mop)
       LAUNCH(K_MOP, st,
              launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
                                modes_t, st));
     LAUNCH(K_PREP, st,
            launch_enc_pix<F>(u, v, codes_p, prevrec, qd_row_off, pre_nl, pp,
-                             modes_t, a, a + plane, pins, pins + cplane,
-                             pins + 2 * cplane, pins + 3 * cplane, qd, row_ll,
-                             st));
+                             modes_t, bio, a, a + plane, pins, pins + cplane,
+                             pins + 2 * cplane, qd, row_ll, st));
     bio.out[0] = ecur; bio.out[1] = ecur + plane;
     bio.ticket = ticket + t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.row_ll = row_ll + (size_t)t * H;
-    LAUNCH(K_BSL, st, launch_bs_local<true>(bio, st));
     LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
     LAUNCH(K_BSF, st, launch_bs_final<true>(bio, st));
   }

@@ -245,22 +245,26 @@ __device__ double block_rate(const int32_t* samp, int ns, int32_t* first,
 
 // ---------------------------------------------------------- encoder prep
 // Three frame-parallel kernels per frame t:
-//   enc_r0_kernel   warp per (row, 32-column chunk): R0 = orig -
-//                   Lorenzo(orig, prev) (zero padding outside the frame), the
-//                   frame t-1 reconstruction as (u, v) pairs, the padded
-//                   codes copy, the int32 overflow flag;
-//   enc_mop_kernel  warp per 32x32 block (frames t >= 1 with MoP): the mode
+//   enc_r0_kernel   CTA per 32x32 block (tile + one-pixel halo in shared
+//                   memory): R0 = orig - Lorenzo(orig, prev) (zero padding
+//                   outside the frame), the frame t-1 reconstruction as
+//                   (u, v) pairs, the padded codes copy, the int32 overflow
+//                   flag, and phase A of the block scan (bscan.cuh): the
+//                   block class and the edge sums LB / LR of -R0 mod 2e;
+//   enc_mop_kernel  CTA per 32x32 block (frames t >= 1 with MoP): the mode
 //                   decision of mop.py:79-151;
 //   enc_pix_kernel  warp per (row, chunk): lossless pins, semi-Lagrangian
 //                   pixels (prediction, symbol, pinned err), the per-chunk
-//                   non-lossless / pinned / chain-written bit words and the
-//                   per-row ll counts.
+//                   non-lossless / pinned bit words, the per-row ll counts
+//                   and the known edges of semi-Lagrangian blocks.
+//
 template <typename F>
 __global__ void __launch_bounds__(256)
 enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
               const uint8_t* __restrict__ codes,
               const int32_t* __restrict__ err_prev_u,
               const int32_t* __restrict__ err_prev_v, PrepParams p,
+              BScanIO bio,
               int32_t* __restrict__ a0, int32_t* __restrict__ a1,
               int2* __restrict__ prevrec, uint8_t* __restrict__ codes_p,
               int* __restrict__ overflow) {
@@ -268,6 +272,8 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
   // once, into shared memory with a one-pixel halo above and to the left
   __shared__ int32_t so[2][33][33];   // orig(t)
   __shared__ int32_t sp[2][33][33];   // recon(t-1) = orig(t-1) + err(t-1)
+  __shared__ uint32_t sx[2][32][33];  // phase A: -R0 mod 2e
+  __shared__ int sflag[3];            // non-uniform / possible escape (u, v); lossy
   const int H = p.H, W = p.W, Wp = p.Wp;
   const int c0 = 32 * blockIdx.x, r0 = 32 * blockIdx.y;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -310,8 +316,16 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
     sp[0][rr][cc] = (ok && has_prev) ? fixed_t(xp_u[q], p.S) + xe_u[q] : 0;
     sp[1][rr][cc] = (ok && has_prev) ? fixed_t(xp_v[q], p.S) + xe_v[q] : 0;
   }
+  const uint8_t* cf = codes + (int64_t)p.t * HW;
+  const int code0 = cf[(int64_t)r0 * W + c0];
+  const int32_t e0 = (int32_t)p.lad.e[code0 & 31];
+  const uint32_t m = e0 > 0 ? 2u * (uint32_t)e0 : 2u;
+  const uint32_t M = (uint32_t)((((uint64_t)1) << 32) / m);
+  int64_t lim = (2 * (int64_t)p.radius - 4) * (int64_t)e0;
+  if (lim > (int64_t)1 << 30) lim = (int64_t)1 << 30;   // int32 symbols in phase C
+  if (tid < 3) sflag[tid] = 0;
   __syncthreads();
-  bool ovf = false;
+  bool ovf = false, bad_u = false, bad_v = false, lossy = false;
   const int j = c0 + tx;
   const bool colok = j < W;
 #pragma unroll
@@ -331,13 +345,57 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
                              R_v >= 2147483647LL || R_v <= -2147483647LL);
     ovf |= o;
     const int64_t pr = (int64_t)i * Wp + j;
-    const int cd = colok ? codes[(int64_t)p.t * HW + (int64_t)i * W + j] : CODE_LOSSLESS;
+    const int cd = colok ? cf[(int64_t)i * W + j] : CODE_LOSSLESS;
     a0[pr] = colok ? (int32_t)R_u : 0;
     a1[pr] = colok ? (int32_t)R_v : 0;
+    // phase A of the block scan (bscan.cuh)
+    if (colok) {
+      lossy |= p.lad.e[cd & 31] != 0;
+      bad_u |= cd != code0 || (R_u < 0 ? -R_u : R_u) >= lim;
+      bad_v |= cd != code0 || (R_v < 0 ? -R_v : R_v) >= lim;
+    }
+    sx[0][rr][tx] = colok ? bs_negres((int32_t)R_u, m, M) : 0u;
+    sx[1][rr][tx] = colok ? bs_negres((int32_t)R_v, m, M) : 0u;
     if (has_prev) prevrec[pr] = make_int2(sp[0][rr + 1][tx + 1], sp[1][rr + 1][tx + 1]);
     codes_p[pr] = (uint8_t)cd;
   }
-  if (__syncthreads_or(ovf) && tid == 0) atomicOr(overflow, 1);
+  for (int q = H - r0; q < 32; q++)   // rows past the frame
+    if (ty == 0) { sx[0][q][tx] = 0u; sx[1][q][tx] = 0u; }
+  if (ovf) atomicOr(overflow, 1);
+  if (bad_u) sflag[0] = 1;
+  if (bad_v) sflag[1] = 1;
+  if (lossy) sflag[2] = 1;
+  __syncthreads();
+  if (tid >= 64) return;
+  // warp = component: LB(j) = prefix over columns of the column sums,
+  // LR(i) = prefix over rows of the row sums (mod 2e)
+  const int comp = tid >> 5, lane = tid & 31;
+  const bool lossless = sflag[2] == 0;
+  const bool reg = e0 > 0 && lim > 0 && sflag[comp] == 0;
+  uint32_t cs = 0, rs = 0;
+#pragma unroll 8
+  for (int k = 0; k < 32; k++) {
+    cs = bs_madd(cs, sx[comp][k][lane], m);
+    rs = bs_madd(rs, sx[comp][lane][k], m);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t pc = __shfl_up_sync(0xffffffffu, cs, o);
+    const uint32_t pr = __shfl_up_sync(0xffffffffu, rs, o);
+    if (lane >= o) {
+      cs = bs_madd(cs, pc, m);
+      rs = bs_madd(rs, pr, m);
+    }
+  }
+  const int64_t nblk = (int64_t)p.nbx * p.nby;
+  const int64_t blk = (int64_t)blockIdx.y * p.nbx + blockIdx.x;
+  // all lossless: every value is known (0); otherwise regular or swept.
+  // Semi-Lagrangian blocks are reclassified as known by enc_pix.
+  bio.lb[(comp * nblk + blk) * 32 + lane] = lossless ? 0 : (int32_t)cs;
+  bio.lr[(comp * nblk + blk) * 32 + lane] = lossless ? 0 : (int32_t)rs;
+  if (lane == 0)
+    bio.cls[comp * nblk + blk] =
+        lossless ? BS_KNOWN : (reg ? (BS_REG | (code0 << 2)) : BS_SLOW);
 }
 
 // MoP trial step with one step size e for the whole block (mop.py:88-110):
@@ -592,11 +650,11 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
                const int2* __restrict__ prevrec,
                const int64_t* __restrict__ qd_row_off,
                const int32_t* __restrict__ pre_nl, PrepParams p,
-               const uint8_t* __restrict__ modes_t, int32_t* __restrict__ a0,
+               const uint8_t* __restrict__ modes_t, BScanIO bio,
+               int32_t* __restrict__ a0,
                int32_t* __restrict__ a1, uint32_t* __restrict__ pin_u,
                uint32_t* __restrict__ pin_v, uint32_t* __restrict__ nlw,
-               uint32_t* __restrict__ symw, uint16_t* __restrict__ qd,
-               int32_t* __restrict__ row_ll) {
+               uint16_t* __restrict__ qd, int32_t* __restrict__ row_ll) {
   const int lane = threadIdx.x & 31;
   // grid (chunk groups of 8, rows): warp = one (row, 32-column chunk)
   const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -645,15 +703,34 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
   }
   const unsigned b_pu = __ballot_sync(FULL, colok && pu);
   const unsigned b_pv = __ballot_sync(FULL, colok && pv);
-  const unsigned b_sw = __ballot_sync(FULL, nl && !sl);
   const int tot = __reduce_add_sync(FULL, nll);
   if (lane == 0) {
     const int64_t pb = (int64_t)i * nchunks + bj;
     pin_u[pb] = b_pu;
     pin_v[pb] = b_pv;
     nlw[pb] = bnl;
-    symw[pb] = b_sw;
     if (tot) atomicAdd(row_ll + row, tot);
+  }
+  if (mode == 1) {
+    // every pixel of a semi-Lagrangian block is pinned: its values are
+    // known, and its edges go to the block scan directly
+    const int r0 = i & ~31, ri = i - r0;
+    const int nr = min(32, H - r0), ncl = min(32, W - 32 * bj);
+    const int64_t nblk = (int64_t)p.nbx * p.nby;
+    const int64_t blk = (int64_t)(i >> 5) * p.nbx + bj;
+    const int32_t vu = colok ? a0[pr] : 0, vv = colok ? a1[pr] : 0;
+    if (ri == nr - 1) {
+      bio.lb[blk * 32 + lane] = vu;
+      bio.lb[(nblk + blk) * 32 + lane] = vv;
+    }
+    if (lane == ncl - 1) {
+      bio.lr[blk * 32 + ri] = vu;
+      bio.lr[(nblk + blk) * 32 + ri] = vv;
+    }
+    if (ri == 0 && lane == 0) {
+      bio.cls[blk] = BS_KNOWN;
+      bio.cls[nblk + blk] = BS_KNOWN;
+    }
   }
 }
 
@@ -807,12 +884,13 @@ cudaError_t launch_chunk_prefix(const uint8_t* codes, const SYM* qd,
 template <typename F>
 cudaError_t launch_enc_r0(const F* u, const F* v, const uint8_t* codes,
                           const int32_t* eu, const int32_t* ev,
-                          const PrepParams& p, int32_t* a0, int32_t* a1,
+                          const PrepParams& p, const BScanIO& bio,
+                          int32_t* a0, int32_t* a1,
                           int32_t* prevrec, uint8_t* codes_p, int* overflow,
                           cudaStream_t st) {
   const dim3 grid(p.nchunks, p.nby);
   enc_r0_kernel<F><<<grid, 256, 0, st>>>(
-      u, v, codes, eu, ev, p, a0, a1,
+      u, v, codes, eu, ev, p, bio, a0, a1,
       reinterpret_cast<int2*>(prevrec), codes_p, overflow);
   return cudaGetLastError();
 }
@@ -831,14 +909,14 @@ template <typename F>
 cudaError_t launch_enc_pix(const F* u, const F* v, const uint8_t* codes_p,
                            const int32_t* prevrec, const int64_t* qd_row_off,
                            const int32_t* pre_nl, const PrepParams& p,
-                           const uint8_t* modes_t, int32_t* a0, int32_t* a1,
+                           const uint8_t* modes_t, const BScanIO& bio,
+                           int32_t* a0, int32_t* a1,
                            uint32_t* pin_u, uint32_t* pin_v, uint32_t* nlw,
-                           uint32_t* symw, uint16_t* qd, int32_t* row_ll,
-                           cudaStream_t st) {
+                           uint16_t* qd, int32_t* row_ll, cudaStream_t st) {
   const dim3 grid((p.nchunks + 7) / 8, p.H);
   enc_pix_kernel<F><<<grid, 256, 0, st>>>(
       u, v, codes_p, reinterpret_cast<const int2*>(prevrec), qd_row_off,
-      pre_nl, p, modes_t, a0, a1, pin_u, pin_v, nlw, symw, qd, row_ll);
+      pre_nl, p, modes_t, bio, a0, a1, pin_u, pin_v, nlw, qd, row_ll);
   return cudaGetLastError();
 }
 
@@ -877,8 +955,9 @@ template cudaError_t launch_chunk_prefix<uint16_t>(const uint8_t*,
 template cudaError_t launch_enc_r0<float>(const float*, const float*,
                                           const uint8_t*, const int32_t*,
                                           const int32_t*, const PrepParams&,
-                                          int32_t*, int32_t*, int32_t*,
-                                          uint8_t*, int*, cudaStream_t);
+                                          const BScanIO&, int32_t*, int32_t*,
+                                          int32_t*, uint8_t*, int*,
+                                          cudaStream_t);
 template cudaError_t launch_enc_mop<float>(const float*, const float*,
                                            const int32_t*, const int32_t*,
                                            const int32_t*, const PrepParams&,
@@ -886,14 +965,15 @@ template cudaError_t launch_enc_mop<float>(const float*, const float*,
                                            cudaStream_t);
 template cudaError_t launch_enc_pix<float>(
     const float*, const float*, const uint8_t*, const int32_t*, const int64_t*,
-    const int32_t*, const PrepParams&, const uint8_t*, int32_t*, int32_t*,
-    uint32_t*, uint32_t*, uint32_t*, uint32_t*, uint16_t*, int32_t*,
+    const int32_t*, const PrepParams&, const uint8_t*, const BScanIO&,
+    int32_t*, int32_t*, uint32_t*, uint32_t*, uint32_t*, uint16_t*, int32_t*,
     cudaStream_t);
 template cudaError_t launch_enc_r0<double>(const double*, const double*,
                                           const uint8_t*, const int32_t*,
                                           const int32_t*, const PrepParams&,
-                                          int32_t*, int32_t*, int32_t*,
-                                          uint8_t*, int*, cudaStream_t);
+                                          const BScanIO&, int32_t*, int32_t*,
+                                          int32_t*, uint8_t*, int*,
+                                          cudaStream_t);
 template cudaError_t launch_enc_mop<double>(const double*, const double*,
                                            const int32_t*, const int32_t*,
                                            const int32_t*, const PrepParams&,
@@ -901,8 +981,8 @@ template cudaError_t launch_enc_mop<double>(const double*, const double*,
                                            cudaStream_t);
 template cudaError_t launch_enc_pix<double>(
     const double*, const double*, const uint8_t*, const int32_t*, const int64_t*,
-    const int32_t*, const PrepParams&, const uint8_t*, int32_t*, int32_t*,
-    uint32_t*, uint32_t*, uint32_t*, uint32_t*, uint16_t*, int32_t*,
+    const int32_t*, const PrepParams&, const uint8_t*, const BScanIO&,
+    int32_t*, int32_t*, uint32_t*, uint32_t*, uint32_t*, uint16_t*, int32_t*,
     cudaStream_t);
 template cudaError_t launch_dec_prep<uint16_t>(
     const uint8_t*, const uint16_t*, const int64_t*, const uint8_t*,

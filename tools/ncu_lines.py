@@ -1,5 +1,6 @@
-"""Per-CUDA-source-line warp-stall samples of one kernel from an ncu report:
-python tools/ncu_lines.py report.ncu-rep kernel_regex [top]"""
+"""Per-CUDA-source-line warp-stall samples (or executed instructions) of one
+kernel from an ncu report:
+python tools/ncu_lines.py report.ncu-rep kernel_regex [top] [inst]"""
 import csv
 import io
 import subprocess
@@ -7,6 +8,8 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+# column 4: warp-stall samples; 7: instructions executed ("inst")
+col = 7 if len(sys.argv) > 4 and sys.argv[4] == "inst" else 4
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",
                       "--print-source", "cuda,sass", "--kernel-name",
                       "regex:" + kern, "-c", "1"],
@@ -23,7 +26,7 @@ for r in csv.reader(io.StringIO(out)):
         continue
     if r[0] and r[0] != "":
         try:
-            s = float(r[4])
+            s = float(r[col])
         except (ValueError, IndexError):
             continue
         rows.append((s, f"{fname}:{r[0]}", r[1].strip()[:100]))
