@@ -184,54 +184,67 @@ __device__ __forceinline__ bool sl_predict_rk2(const Src& s, int H, int W,
 
 // ------------------------------------------------ first-touch block entropy
 // mop.py:118-138.  samp[sp] = |idx| of sample sp (sequence order: raster
-// (i, j), u then v) or -1 for an overflow sample.
+// (i, j), u then v) or -1 for an overflow sample.  The reference sums
+// h*log2(h) over the distinct values in first-touch order (float64, so the
+// order is part of the result).  One warp, 32 samples per step in sequence
+// order: __match_any_sync groups equal values, the group leader (its first
+// occurrence) adds the group's count, and a value's first touch appends it
+// to an ordered list; values >= ETB take the generic path.
 constexpr int ETB = 512;
-__device__ double block_rate(const int32_t* samp, int ns, int32_t* first,
-                             int32_t* cnt, const double* log2tab, double lam,
-                             double rmeta, int lane) {
-  int n_ok = 0, lp = 0;
-  for (int sp = lane; sp < ns; sp += 32) {
-    const int a = samp[sp];
-    if (a < 0) { lp++; continue; }
-    n_ok++;
-    if (a < ETB) { atomicMin(first + a, sp); atomicAdd(cnt + a, 1); }
+__device__ double block_rate(const int32_t* samp, int ns, int32_t* cnt,
+                             int32_t* order, const double* log2tab,
+                             double lam, double rmeta, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned below = (1u << lane) - 1u;
+  int n_ok = 0, lp = 0, nd = 0;
+  for (int c = 0; c < ns; c += 32) {
+    const int sp = c + lane;
+    const int a = sp < ns ? samp[sp] : -2;
+    n_ok += a >= 0;
+    lp += a == -1;
+    const bool small = a >= 0 && a < ETB;
+    const int key = small ? a : -1;
+    const unsigned grp = __match_any_sync(FULL, key);
+    const bool leader = small && (grp & below) == 0;
+    int prev = 0;
+    if (leader) prev = cnt[key];
+    bool fresh = leader && prev == 0;
+    if (a >= ETB) {   // rare: first touch by search
+      fresh = true;
+      for (int q = 0; q < sp; q++)
+        if (samp[q] == a) { fresh = false; break; }
+    }
+    const unsigned fm = __ballot_sync(FULL, fresh);
+    if (leader) cnt[key] = prev + __popc(grp);
+    if (fresh) order[nd + __popc(fm & below)] = small ? key : -(sp + 1);
+    nd += __popc(fm);
   }
   for (int o = 16; o; o >>= 1) {
-    n_ok += __shfl_xor_sync(0xffffffffu, n_ok, o);
-    lp += __shfl_xor_sync(0xffffffffu, lp, o);
+    n_ok += __shfl_xor_sync(FULL, n_ok, o);
+    lp += __shfl_xor_sync(FULL, lp, o);
   }
   __syncwarp();
   double acc = 0.0;
-  for (int c = 0; c < ns; c += 32) {
-    const int sp = c + lane;
-    bool ft = false;
-    int h = 0;
-    if (sp < ns) {
-      const int a = samp[sp];
-      if (a >= 0 && a < ETB) {
-        ft = first[a] == sp;
-        h = cnt[a];
-      } else if (a >= ETB) {
-        ft = true;
-        for (int q = 0; q < sp; q++)
-          if (samp[q] == a) { ft = false; break; }
-        if (ft)
-          for (int q = 0; q < ns; q++) h += samp[q] == a;
+  for (int k0 = 0; k0 < nd; k0 += 32) {
+    const int k = k0 + lane;
+    double term = 0.0;
+    if (k < nd) {
+      const int key = order[k];
+      int h = 0;
+      if (key >= 0) {
+        h = cnt[key];
+      } else {
+        const int a = samp[-key - 1];
+        for (int q = 0; q < ns; q++) h += samp[q] == a;
       }
+      term = __dmul_rn((double)h, log2tab[h]);
     }
-    const double term = ft ? __dmul_rn((double)h, log2tab[h]) : 0.0;
-    unsigned bal = __ballot_sync(0xffffffffu, ft);
-    while (bal) {
-      const int b = __ffs(bal) - 1;
-      bal &= bal - 1;
-      acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, term, b));
-    }
+    const int nk = min(32, nd - k0);
+    for (int b = 0; b < nk; b++) acc = __dadd_rn(acc, __shfl_sync(FULL, term, b));
   }
   __syncwarp();
-  for (int sp = lane; sp < ns; sp += 32) {
-    const int a = samp[sp];
-    if (a >= 0 && a < ETB) { first[a] = 0x7fffffff; cnt[a] = 0; }
-  }
+  for (int k = lane; k < nd; k += 32)
+    if (order[k] >= 0) cnt[order[k]] = 0;
   __syncwarp();
   double h0 = 0.0;
   if (n_ok > 0) h0 = __dsub_rn(log2tab[n_ok], __ddiv_rn(acc, (double)n_ok));
@@ -424,7 +437,7 @@ struct MopSmem {
   int32_t r0[2][32][33];   // [comp][row][col] R0 tile, then rho
   int32_t q0[2][32][33];   // [comp][row][col] Q0 = rha(R0 / 2 tau')
   int32_t samp[2][512];    // [trial] |idx| per sample (-1: escape)
-  int32_t first[2][ETB];
+  int32_t order[2][ETB];  // distinct |idx| in first-touch order
   int32_t cnt[2][ETB];
   double rate[2];
 };
@@ -459,10 +472,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
     sm.r0[0][r][lane] = rv ? __ldg(a0 + k) : 0;
     sm.r0[1][r][lane] = rv ? __ldg(a1 + k) : 0;
   }
-  for (int k = threadIdx.x; k < 2 * ETB; k += 128) {
-    (&sm.first[0][0])[k] = 0x7fffffff;
-    (&sm.cnt[0][0])[k] = 0;
-  }
+  for (int k = threadIdx.x; k < 2 * ETB; k += 128) (&sm.cnt[0][0])[k] = 0;
   __syncthreads();
   bool swept = false;
   if (wid < 2) {
@@ -531,8 +541,9 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
       // |idx| at the stride samples: x + err = q * 2 tau' exactly
       const bool scol = lane < ncl && (lane % p.stride) == 0;
       const int sj = lane / p.stride;
+      int srow = 0;
 #pragma unroll 1
-      for (int r = 0; r < nr; r += p.stride) {
+      for (int r = 0; r < nr; r += p.stride, srow += nsx) {
         if (scol) {
           const int j = lane;
           const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
@@ -542,7 +553,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
           const uint32_t an = (uint32_t)(n < 0 ? -n : n);
           uint32_t qa = __umulhi(an, M);
           if (qa * m != an) qa++;
-          sm.samp[0][2 * ((r / p.stride) * nsx + sj) + comp] = (int32_t)qa;
+          sm.samp[0][2 * (srow + sj) + comp] = (int32_t)qa;
         }
       }
     }
@@ -631,7 +642,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
   __syncthreads();
   if (wid == 0 || wid == 2) {
     const int tr = wid >> 1;
-    const double r = block_rate(sm.samp[tr], ns, sm.first[tr], sm.cnt[tr],
+    const double r = block_rate(sm.samp[tr], ns, sm.cnt[tr], sm.order[tr],
                                 log2tab, p.lam, p.rmeta, lane);
     if (lane == 0) sm.rate[tr] = r;
   }
