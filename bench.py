@@ -32,21 +32,43 @@ METRIC = ("compress/decompress GB/s (fp32 u,v input) on 1 B200; "
           "fraction of HBM roofline")
 UNIT = "GB/s"
 
-# algorithmic bytes per vertex
+# algorithmic bytes per vertex (SURVEY.md §8d for the pipelines; per
+# kernel: the bytes its contract has to move)
 ALGO_BYTES = {
     "pipeline_compress": 21.125,
     "pipeline_decompress": 21.125,
+    "range": 8.0,                      # fp32 u,v
     "analyze": 8.0 + 1.0 + 0.125,      # fp32 u,v in; code + l_d out
-    "encode": 8.0 + 1.0 + 4.0,         # fp32 u,v + code in; 2 x u16 out
-    "mop": 8.0,                        # fp32 u,v of the frame
-    "decode": 1.0 + 4.0 + 16.0,        # code + 2 x u16 in; 2 x f64 out
-    # block-scan chain (encoder): prepared R0 planes + codes in (local);
-    # R0 in, err planes + 2 x u16 symbols out (final); the chain itself
-    # moves two 32-value edges per 32x32 block and component
-    "bs_local": 8.0 + 1.0,
-    "bs_chain": 2 * 2 * 32 * 4 / 1024.0,
+    # enc_r0: fp32 u,v of frames t and t-1, err(t-1) in; R0 planes and the
+    # recon(t-1) pairs out; codes in and the padded copy out
+    "prep": 8.0 + 8.0 + 8.0 + 8.0 + 8.0 + 2.0,
+    # enc_mop: the R0 tile and one read of recon(t-1) pairs
+    "mop": 8.0 + 8.0,
+    # enc_pix: codes, pin / non-lossless words (semi-Lagrangian pixels are a
+    # data-dependent share on top)
+    "pix": 1.0 + 12.0 / 32.0,
+    # block scan: two 32-value edges per block and component (chain); R0
+    # planes in, err planes + 2 x u16 symbols out (final)
+    "bs_chain": 2 * 2 * 2 * 32 * 4 / 1024.0,
     "bs_final": 8.0 + 8.0 + 4.0,
+    "scan": 1.0,                       # codes
+    # decoder: dec_prep (codes, symbols, recon(t-1) in; A planes out)
+    "decode_rows": 1.0 + 4.0 + 8.0 + 8.0,
+    "aux": 8.0 + 16.0,                 # int32 recon in, 2 x f64 out
 }
+UNITS_FULL = ("analyze", "range")      # per launch: all T frames
+
+# ncu --set full DRAM bytes per launch of each class (profiles/), if captured
+TRAFFIC_FILE = ROOT / "profiles" / "traffic_per_launch.json"
+
+
+def kernel_traffic():
+    if TRAFFIC_FILE.exists():
+        try:
+            return json.loads(TRAFFIC_FILE.read_text())
+        except ValueError:
+            return {}
+    return {}
 
 
 def measured_peak():
@@ -320,13 +342,13 @@ def main():
     steps = args.steps
     dom = max((k for k in prof if prof[k][1]), key=lambda k: prof[k][0])
     dom_ms_per_launch = prof[dom][0] / prof[dom][1]
-    units_per_launch = {"analyze": N, "encode": H * W, "mop": H * W,
-                        "bs_local": H * W, "bs_chain": H * W,
-                        "bs_final": H * W,
-                        "range": N, "scan": T * H, "ll_write": N,
-                        "aux": H * W}.get(dom, N)
+    units_per_launch = N if dom in UNITS_FULL else H * W
     algo = ALGO_BYTES.get(dom, 0.0) * units_per_launch
     achieved = algo / (dom_ms_per_launch * 1e-3) / 1e9
+    tr = kernel_traffic().get(dom)
+    traffic = None
+    if tr:
+        traffic = round(tr["dram_bytes_per_unit"] * units_per_launch)
     value = 8.0 * N * world / (comp_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT,
@@ -342,7 +364,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dom,
                      "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None,
+                     "traffic": traffic,
                      "algo_bytes_per_vertex": ALGO_BYTES.get(dom),
                      "peak_source": peak_src,
                      "pipeline_frac": round(

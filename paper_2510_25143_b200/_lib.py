@@ -67,9 +67,12 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
+# launch classes of vfcp_prof_collect (capi.cu KClass): "prep" is
+# enc_r0_kernel, "pix" enc_pix_kernel, "decode_rows" dec_prep_kernel (and
+# decode_rows_kernel), "aux" emit_frame_kernel
 KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
                   "decode_rows", "decode_ll", "decode", "aux", "prep",
-                  "bs_local", "bs_chain", "bs_final")
+                  "bs_local", "bs_chain", "bs_final", "pix")
 
 
 def prof_enable(on=True):

@@ -61,6 +61,8 @@ struct BScanIO {
   int32_t* lb;              // [2][nblk][32] block bottom row: local prefix
                             // (REG) or the known values (KNOWN)
   int32_t* lr;              // [2][nblk][32] block right column, likewise
+  int32_t* ebot;            // [2][nblk][32] exact block bottom rows (chain)
+  int32_t* eright;          // [2][nblk][32] exact block right columns (chain)
   int32_t* cls;             // [2][nblk] class | code << 2
   uint64_t* bnd;            // tagged boundary slots [ntask][W]
   int* ticket;
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
   BSChainSmem& sm = *reinterpret_cast<BSChainSmem*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int H = io.H, W = io.W, Wp = io.Wp, nbx = io.nbx, nby = io.nby;
+  const int H = io.H, W = io.W, nbx = io.nbx, nby = io.nby;
   const int64_t nblk = (int64_t)nbx * nby;
   const int ntask = bs_ntask(nby);
   if (threadIdx.x < 32) {
@@ -343,7 +345,6 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
       const uint32_t tag_up = io.tag_base + (uint32_t)task - 1u;   // task - 2
       uint64_t* my_gb = io.bnd + (int64_t)task * W;
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
-      int32_t* out = io.out[comp];
       const int32_t* clsp = io.cls + comp * nblk + (int64_t)bi * nbx;
       const int32_t* lbp = io.lb + (comp * nblk + (int64_t)bi * nbx) * 32;
       const int32_t* lrp = io.lr + (comp * nblk + (int64_t)bi * nbx) * 32;
@@ -444,10 +445,11 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
             TaggedSlot<int32_t>::put(my_gb + c, tag_me, bot);
           }
         }
-        // ---- the block's exact boundary for the interior pass
-        if (kind != BS_SLOW) {
-          if (colok) out[(int64_t)(r0 + nr - 1) * Wp + c] = bot;
-          if (lane < nr) out[(int64_t)(r0 + lane) * Wp + c0 + ncl - 1] = right;
+        // ---- the block's exact edges for the interior pass (coalesced)
+        {
+          const int64_t eo = (comp * nblk + (int64_t)bi * nbx + bj) * 32 + lane;
+          io.ebot[eo] = bot;
+          io.eright[eo] = right;
         }
         if (lane == 0) *(volatile int*)&sm.done[w] = bj + 1;
         corner = __shfl_sync(FULL, top, 31);
@@ -497,9 +499,11 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
     return;
   }
   // ---- exact boundary from phase B
-  const int32_t top = (r0 > 0 && colok) ? __ldcg(out + (int64_t)(r0 - 1) * Wp + c0 + lane) : 0;
-  const int32_t left = (c0 > 0 && lane < nr) ? __ldcg(out + (int64_t)(r0 + lane) * Wp + c0 - 1) : 0;
-  const int32_t corner = (r0 > 0 && c0 > 0) ? __ldcg(out + (int64_t)(r0 - 1) * Wp + c0 - 1) : 0;
+  const int32_t* eb = io.ebot + comp * nblk * 32;
+  const int32_t* er = io.eright + comp * nblk * 32;
+  const int32_t top = (bi > 0 && colok) ? __ldcg(eb + (blk - io.nbx) * 32 + lane) : 0;
+  const int32_t left = (bj > 0 && lane < nr) ? __ldcg(er + (blk - 1) * 32 + lane) : 0;
+  const int32_t corner = (bi > 0 && bj > 0) ? __ldcg(eb + (blk - io.nbx - 1) * 32 + 31) : 0;
   uint32_t e = 0, m = 0, M = 0;
   if (ENC) {
     const int code = cls >> 2;

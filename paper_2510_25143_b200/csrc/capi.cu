@@ -107,7 +107,8 @@ int fail(int code, const std::string& msg) {
 // counts it and, when profiling is on, brackets it with CUDA events on the
 // launching stream (vfcp_prof_*).
 enum KClass { K_RANGE, K_ANALYZE, K_SCAN, K_MOP, K_ENCODE, K_LLW, K_DROWS,
-              K_DLL, K_DECODE, K_AUX, K_PREP, K_BSL, K_BSC, K_BSF, K_NCLS };
+              K_DLL, K_DECODE, K_AUX, K_PREP, K_BSL, K_BSC, K_BSF, K_PIX,
+              K_NCLS };
 struct Prof {
   bool on = false;
   int64_t launches = 0;
@@ -425,6 +426,8 @@ int bscan_setup(Scratch& sc, const Ladder& lad, int H, int W, int radius,
   const int ntask = bs_ntask(nby);
   CK(sc.get(&b->lb, (size_t)2 * nblk * 32));
   CK(sc.get(&b->lr, (size_t)2 * nblk * 32));
+  CK(sc.get(&b->ebot, (size_t)2 * nblk * 32));
+  CK(sc.get(&b->eright, (size_t)2 * nblk * 32));
   CK(sc.get(&b->cls, (size_t)2 * nblk));
   CK(sc.get(&b->bnd, (size_t)ntask * W));
   CK(cudaMemsetAsync(b->bnd, 0, sizeof(uint64_t) * ntask * W, st));
@@ -516,7 +519,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
       LAUNCH(K_MOP, st,
              launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
                                modes_t, st));
-    LAUNCH(K_PREP, st,
+    LAUNCH(K_PIX, st,
            launch_enc_pix<F>(u, v, codes_p, prevrec, qd_row_off, pre_nl, pp,
                              modes_t, bio, a, a + plane, pins, pins + cplane,
                              pins + 2 * cplane, qd, row_ll, st));
