@@ -547,30 +547,30 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   }
   const uint32_t rt = bs_res(top, m, M), rc = bs_res(corner, m, M);
   const uint32_t base = bs_msub(rt, rc, m);
-  uint32_t tiem[32];
-  bool anytie = false;
+  const uint32_t rl = bs_res(left, m, M);   // lane r: row r's left residue
+  // representatives; a tie (residue e) is marked and resolved below
+  uint32_t tierows = 0;
 #pragma unroll
   for (int r = 0; r < 32; r++) {
-    const uint32_t s = bs_madd(bs_madd(base, bs_res(v[r + 1][0], m, M), m), x[r][lane], m);
+    const uint32_t s = bs_madd(bs_madd(base, __shfl_sync(FULL, rl, r), m), x[r][lane], m);
     const bool tie = s == e && r < nr && colok;
-    tiem[r] = __ballot_sync(FULL, tie);
-    anytie |= tiem[r] != 0u;
-    v[r + 1][lane + 1] = tie ? 0 : bs_rep(s, e, m);
+    tierows |= (__any_sync(FULL, tie) ? 1u : 0u) << r;
+    v[r + 1][lane + 1] = tie ? INT32_MIN : bs_rep(s, e, m);
   }
   __syncwarp();
-  if (anytie) {
+  if (tierows) {
     // raster order: a tie's sign follows x = R0 - (vU + vL - vUL), whose
     // neighbours may be earlier ties
 #pragma unroll
     for (int r = 0; r < 32; r++) {
-      uint32_t tm = tiem[r];
+      if (!((tierows >> r) & 1u)) continue;   // warp-uniform
+      uint32_t tm = __ballot_sync(FULL, colok && v[r + 1][lane + 1] == INT32_MIN);
       while (tm) {
         const int j = __ffs(tm) - 1;
         tm &= tm - 1u;
         if (lane == j) {
           const int64_t d = (int64_t)v[r][j + 1] + v[r + 1][j] - v[r][j];
-          const int64_t xx = (int64_t)xa[r] - d;
-          v[r + 1][j + 1] = xx > 0 ? (int32_t)e : -(int32_t)e;
+          v[r + 1][j + 1] = ((int64_t)xa[r] - d) > 0 ? (int32_t)e : -(int32_t)e;
         }
         __syncwarp();
       }
@@ -583,20 +583,21 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   if (lane < nr)
     qb = io.qd_row_off[r0 + lane] +
          2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
+  int32_t* op = out + (int64_t)r0 * Wp + c0 + lane;
 #pragma unroll
-  for (int r = 0; r < 32; r++) {
+  for (int r = 0; r < 32; r++, op += Wp) {
     const int64_t qr = __shfl_sync(FULL, qb, r);
     if (r < nr && colok) {
+      // x + err = q * 2e exactly; int32 is exact here (|R0| < 2^30 in a
+      // regular block, |vU + vL - vUL - err| < 2^30)
       const int32_t err = v[r + 1][lane + 1];
-      const int64_t d = (int64_t)v[r][lane + 1] + v[r + 1][lane] - v[r][lane];
-      // x + err = q * 2e exactly
-      const int64_t n = (int64_t)xa[r] - d + err;
+      const int32_t d = v[r][lane + 1] + v[r + 1][lane] - v[r][lane];
+      const int32_t n = xa[r] - d + err;
       const uint32_t an = (uint32_t)(n < 0 ? -n : n);
       uint32_t qa = __umulhi(an, M);
       if (qa * m != an) qa++;
       const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
-      const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
-      out[k] = err;
+      *op = err;
       io.qd[qr + 2 * lane] = (uint16_t)(q + radius);
     }
   }
