@@ -430,9 +430,9 @@ __device__ __forceinline__ int32_t trial_step(int32_t rho, int32_t q0,
 }
 
 // One CTA of 4 warps per 32x32 block: warps 0 / 1 run the Lorenzo trial of
-// u / v (lane = row, skewed sweep), warps 2 / 3 the semi-Lagrangian trial at
-// the stride samples; then warp 0 rates the Lorenzo samples while warp 2
-// rates the SL samples (first-touch order, mop.py:118-138).
+// u / v, then all four warps the semi-Lagrangian trial at the stride samples
+// (warps 2 / 3 start on it at once); then warp 0 rates the Lorenzo samples
+// while warp 2 rates the SL samples (first-touch order, mop.py:118-138).
 struct MopSmem {
   int32_t r0[2][32][33];   // [comp][row][col] R0 tile, then rho
   int32_t q0[2][32][33];   // [comp][row][col] Q0 = rha(R0 / 2 tau')
@@ -465,24 +465,41 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const double inv = 1.0 / (double)(2 * p.tau);
   const int32_t radius = p.radius;
   const int64_t tau = p.tau;
-  // R0 tile (all 4 warps; lane = column)
-  for (int r = wid; r < 32; r += 4) {
-    const bool rv = r < nr;
-    const int64_t k = (int64_t)(r0 + (rv ? r : 0)) * Wp + c0 + lane;
-    sm.r0[0][r][lane] = rv ? __ldg(a0 + k) : 0;
-    sm.r0[1][r][lane] = rv ? __ldg(a1 + k) : 0;
-  }
   for (int k = threadIdx.x; k < 2 * ETB; k += 128) (&sm.cnt[0][0])[k] = 0;
-  __syncthreads();
+  const int64_t HW = (int64_t)H * W;
+  const F* uo = u + (int64_t)p.t * HW;
+  const F* vo = v + (int64_t)p.t * HW;
+  // semi-Lagrangian samples of this thread: sidx = tid and tid + 128; the
+  // originals are loaded first (warps 2 / 3 start on their gathers at once,
+  // warps 0 / 1 after the Lorenzo trial)
+  constexpr int NSB = 2;
+  F sou[NSB], sov[NSB];
+#pragma unroll
+  for (int b = 0; b < NSB; b++) {
+    const int sidx = min((int)threadIdx.x + 128 * b, nsamp - 1);
+    const int si = sidx / nsx, sj = sidx - si * nsx;
+    const int64_t k = (int64_t)(r0 + si * p.stride) * W + c0 + sj * p.stride;
+    sou[b] = __ldg(uo + k);
+    sov[b] = __ldg(vo + k);
+  }
   bool swept = false;
   if (wid < 2) {
+    // R0 tile of this warp's component (lane = column)
+    const int32_t* ap = wid ? a1 : a0;
+#pragma unroll 8
+    for (int r = 0; r < 32; r++)
+      sm.r0[wid][r][lane] = r < nr ? __ldg(ap + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
+    __syncwarp();
     // Lorenzo trial of component wid with block-local errors (mop.py:88-110).
     // Every pixel uses the step tau', so unless a pixel can escape
     // (|R0| >= (2 radius - 4) tau') the trial errors are the representatives
     // of the block's 2D prefix sums of -R0 mod 2 tau' (see bscan.cuh), with
     // a zero boundary (outside the block the candidate is the original).
     const int comp = wid;
-    const int64_t lim = (2 * (int64_t)radius - 4) * tau;
+    // (|R0| < 2^30 as well: the sample arithmetic below is then exact in
+    // int32)
+    int64_t lim = (2 * (int64_t)radius - 4) * tau;
+    if (lim > ((int64_t)1 << 30)) lim = (int64_t)1 << 30;
     bool safe = lim > 0;
 #pragma unroll 8
     for (int r = 0; r < 32; r++) {
@@ -511,29 +528,32 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
         acc = bs_madd(acc, (uint32_t)v[k][lane], m);
         v[k][lane] = (int32_t)acc;
       }
-      bool anytie = false;
-      uint32_t tiem[32];
+      uint32_t tierows = 0;
 #pragma unroll
       for (int r = 0; r < 32; r++) {
         const uint32_t sres = (uint32_t)v[r][lane];
         const bool tie = sres == ue && r < nr && lane < ncl;
-        tiem[r] = __ballot_sync(FULL, tie);
-        anytie |= tiem[r] != 0u;
-        v[r][lane] = tie ? 0 : bs_rep(sres, ue, m);
+        tierows |= (__any_sync(FULL, tie) ? 1u : 0u) << r;
+        v[r][lane] = tie ? INT32_MIN : bs_rep(sres, ue, m);
       }
       __syncwarp();
-      if (anytie && lane == 0) {
-        // raster order: the tie's sign follows x = R0 - D
+      if (tierows) {
+        // raster order: the tie's sign follows x = R0 - D, whose neighbours
+        // may be earlier ties
 #pragma unroll 1
         for (int r = 0; r < 32; r++) {
-          uint32_t tm = tiem[r];
+          if (!((tierows >> r) & 1u)) continue;   // warp-uniform
+          uint32_t tm = __ballot_sync(FULL, lane < ncl && v[r][lane] == INT32_MIN);
           while (tm) {
             const int j = __ffs(tm) - 1;
             tm &= tm - 1u;
-            const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
-                              (j > 0 ? (int64_t)v[r][j - 1] : 0) -
-                              ((r > 0 && j > 0) ? (int64_t)v[r - 1][j - 1] : 0);
-            v[r][j] = ((int64_t)x[r][j] - d) > 0 ? e : -e;
+            if (lane == j) {
+              const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
+                                (j > 0 ? (int64_t)v[r][j - 1] : 0) -
+                                ((r > 0 && j > 0) ? (int64_t)v[r - 1][j - 1] : 0);
+              v[r][j] = ((int64_t)x[r][j] - d) > 0 ? e : -e;
+            }
+            __syncwarp();
           }
         }
       }
@@ -546,10 +566,9 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
       for (int r = 0; r < nr; r += p.stride, srow += nsx) {
         if (scol) {
           const int j = lane;
-          const int64_t d = (r > 0 ? (int64_t)v[r - 1][j] : 0) +
-                            (j > 0 ? (int64_t)v[r][j - 1] : 0) -
-                            ((r > 0 && j > 0) ? (int64_t)v[r - 1][j - 1] : 0);
-          const int64_t n = (int64_t)x[r][j] - d + v[r][j];
+          const int32_t d = (r > 0 ? v[r - 1][j] : 0) + (j > 0 ? v[r][j - 1] : 0) -
+                            ((r > 0 && j > 0) ? v[r - 1][j - 1] : 0);
+          const int32_t n = x[r][j] - d + v[r][j];
           const uint32_t an = (uint32_t)(n < 0 ? -n : n);
           uint32_t qa = __umulhi(an, M);
           if (qa * m != an) qa++;
@@ -601,42 +620,35 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
         if (++jm == p.stride) { jm = 0; jq++; }
       }
     }
-  } else if (wid >= 2) {
-    // semi-Lagrangian trial at the stride samples, 64 threads; samples of
-    // a thread in lockstep so their departure-point gathers overlap
-    const int64_t HW = (int64_t)H * W;
-    const F* uo = u + (int64_t)p.t * HW;
-    const F* vo = v + (int64_t)p.t * HW;
+  }
+  {
+    // semi-Lagrangian trial at the stride samples, all 128 threads, NSB
+    // samples each in lockstep so their departure-point gathers overlap
     const PairPlane src{prevrec, Wp};
-    const int tt = threadIdx.x - 64;
-    constexpr int NB = 2;   // 64 threads x 2 x 2 rounds = 256 samples (stride 2)
-    for (int base = 0; base < nsamp; base += 64 * NB) {
-      int64_t pr_u[NB], pr_v[NB];
-      int si_i[NB], si_j[NB];
-      bool slow[NB];
+    int64_t pr_u[NSB], pr_v[NSB];
+    int si_i[NSB], si_j[NSB];
+    bool slow[NSB];
 #pragma unroll
-      for (int b = 0; b < NB; b++) {
-        const int sidx = min(base + tt + 64 * b, nsamp - 1);
-        const int si = sidx / nsx, sj = sidx - si * nsx;
-        si_i[b] = r0 + si * p.stride;
-        si_j[b] = c0 + sj * p.stride;
-        slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
-                                  p.d_max, &pr_u[b], &pr_v[b]);
-      }
+    for (int b = 0; b < NSB; b++) {
+      const int sidx = min((int)threadIdx.x + 128 * b, nsamp - 1);
+      const int si = sidx / nsx, sj = sidx - si * nsx;
+      si_i[b] = r0 + si * p.stride;
+      si_j[b] = c0 + sj * p.stride;
+      slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
+                                p.d_max, &pr_u[b], &pr_v[b]);
+    }
 #pragma unroll
-      for (int b = 0; b < NB; b++) {
-        const int sidx = base + tt + 64 * b;
-        if (sidx >= nsamp) continue;
-        const int i = si_i[b], jj = si_j[b];
-        if (slow[b])
-          sl_predict2(src, H, W, i, jj, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
-                      &pr_u[b], &pr_v[b]);
-        const int64_t ru = (int64_t)load_fixed(uo, (int64_t)i * W + jj, p.S) - pr_u[b];
-        const int64_t rv = (int64_t)load_fixed(vo, (int64_t)i * W + jj, p.S) - pr_v[b];
-        const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
-        sm.samp[1][2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
-        sm.samp[1][2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
-      }
+    for (int b = 0; b < NSB; b++) {
+      const int sidx = threadIdx.x + 128 * b;
+      if (sidx >= nsamp) continue;
+      if (slow[b])
+        sl_predict2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y, p.d_max,
+                    p.n_max, &pr_u[b], &pr_v[b]);
+      const int64_t ru = (int64_t)fixed_t(sou[b], p.S) - pr_u[b];
+      const int64_t rv = (int64_t)fixed_t(sov[b], p.S) - pr_v[b];
+      const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
+      sm.samp[1][2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
+      sm.samp[1][2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
     }
   }
   __syncthreads();
