@@ -125,18 +125,37 @@ analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
     (&sm.acc[0][0][0])[k] = 0;
   for (int k = tid; k < TI * TJ; k += K1_THREADS) (&sm.mask[0][0])[k] = 0;
 
-  auto load_frame = [&](int t) {
-    int s = t & 1;
+  // Frame loads are software-pipelined: the raw values of frame t+2 are in
+  // flight (registers) while slab (t, t+1) is processed, and converted into
+  // shared memory at the start of the next iteration.
+  constexpr int NL = (RH * RW + K1_THREADS - 1) / K1_THREADS;
+  F ru[NL], rv[NL];
+  auto issue = [&](int t) {
     const int64_t base = (int64_t)t * HW;
-    for (int k = tid; k < RH * RW; k += K1_THREADS) {
-      int lr = k / RW, lc = k - lr * RW;
-      int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
+#pragma unroll
+    for (int q = 0; q < NL; q++) {
+      const int k = tid + q * K1_THREADS;
+      const int lr = k / RW, lc = k - lr * RW;
+      const int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
+      const bool ok = k < RH * RW && gi >= 0 && gi < H && gj >= 0 && gj < W;
+      const int64_t n = ok ? base + (int64_t)gi * W + gj : 0;
+      ru[q] = ok ? __ldg(u + n) : F(0);
+      rv[q] = ok ? __ldg(v + n) : F(0);
+    }
+  };
+  auto commit = [&](int t) {
+    const int s = t & 1;
+#pragma unroll
+    for (int q = 0; q < NL; q++) {
+      const int k = tid + q * K1_THREADS;
+      if (k >= RH * RW) break;
+      const int lr = k / RW, lc = k - lr * RW;
+      const int gi = i0 - 1 + lr, gj = j0 - 1 + lc;
       int32_t x = 0, y = 0;
       uint8_t c = 0;
       if (gi >= 0 && gi < H && gj >= 0 && gj < W) {
-        int64_t q = base + (int64_t)gi * W + gj;
-        x = load_fixed(u, q, S);
-        y = load_fixed(v, q, S);
+        x = fixed_t(ru[q], S);
+        y = fixed_t(rv[q], S);
         c = vertex_class(x, y, thr);
       }
       sm.u[s][lr][lc] = x;
@@ -145,10 +164,13 @@ analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
     }
   };
 
-  load_frame(0);
+  issue(0);
+  commit(0);
+  if (T > 1) issue(1);
   for (int t = 0; t < T; t++) {
     const bool slab = t + 1 < T;
-    if (slab) load_frame(t + 1);
+    if (slab) commit(t + 1);
+    if (t + 2 < T) issue(t + 2);
     if (tid == 0) sm.nlist = 0;
     __syncthreads();
 
