@@ -96,6 +96,17 @@ int vfcp_encode(const vfcp_params* p, const void* u, const void* v,
                 void* qd, uint8_t* modes, double* scores, int32_t* row_ll,
                 int64_t* recon, void* stream);
 
+/* vfcp_encode that also streams the symbol stream to (pinned) host memory
+ * while it runs: frame t's symbols qd[frame_off[t] .. frame_off[t+1]) are
+ * copied to host_qd on a side stream as soon as frame t is encoded, so the
+ * D2H overlaps the later frames (the entropy stage of codec.py:378-387 reads
+ * them on the host).  frame_off: host i64[T+1] = qd_row_off[t*H]. */
+int vfcp_encode_host(const vfcp_params* p, const void* u, const void* v,
+                     int dtype, const uint8_t* codes,
+                     const int64_t* qd_row_off, void* qd, uint8_t* modes,
+                     int32_t* row_ll, void* host_qd,
+                     const int64_t* frame_off, void* stream);
+
 /* Exclusive scan of per-row counts: off[r] = sum_{q<r} cnt[q], off[nrows] =
  * total.  Synchronising: *total_host = total. */
 int vfcp_row_offsets(const int32_t* cnt, int64_t nrows, int64_t* off,

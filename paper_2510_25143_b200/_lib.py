@@ -53,6 +53,7 @@ _SIGS = {
     "vfcp_analyze": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P]),
     "vfcp_qd_offsets": (_I, [_PP, _P, _P, _P, _P]),
     "vfcp_encode": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vfcp_encode_host": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vfcp_row_offsets": (_I, [_P, _I64, _P, _P, _P]),
     "vfcp_encode_ll": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "vfcp_decode_prepare": (_I, [_PP, _P, _P, _P, _I64, _P, _P, _P, _P, _P,

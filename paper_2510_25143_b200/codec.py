@@ -247,13 +247,18 @@ class DeviceStreams:
     scores: object = None
     recon: object = None
     n_faces: int | None = None
+    host: dict | None = None   # host copies (compress_device(host_out=True))
 
 
 def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                     relative: bool = False, want_mask: bool = False,
                     want_scores: bool = False, want_recon: bool = False,
-                    ) -> DeviceStreams:
-    """codec.py:321-376 up to (not including) the entropy stage, on device."""
+                    host_out: bool = False) -> DeviceStreams:
+    """codec.py:321-376 up to (not including) the entropy stage, on device.
+
+    host_out: also bring the streams to pinned host memory (``.host``),
+    overlapping the copies with the encode: the codes and l_d right after
+    the analysis, each frame's symbols as soon as the frame is encoded."""
     import torch
     cfg = config or Config()
     if eps < 0:
@@ -296,10 +301,36 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
     recon = (torch.empty(2 * N, dtype=torch.int64, device=dev)
              if want_recon else None)
     row_ll = torch.empty(T * H, dtype=torch.int32, device=dev)
-    _lib.check(L.vfcp_encode(pp, du.data_ptr(), dv.data_ptr(), dt_code,
-                             codes.data_ptr(), qd_row_off.data_ptr(),
-                             qd.data_ptr(), modes.data_ptr(), _lib.ptr(scores),
-                             row_ll.data_ptr(), _lib.ptr(recon), st), "encode")
+    host = None
+    if host_out and qd.dtype == torch.uint16 and not (want_scores or want_recon):
+        # codes / l_d on a side stream while the encode runs
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(main)
+        h_codes = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+        h_ld = torch.empty((N + 7) // 8, dtype=torch.uint8, pin_memory=True)
+        with torch.cuda.stream(side):
+            h_codes.copy_(codes, non_blocking=True)
+            h_ld.copy_(ld_words.view(torch.uint8)[:(N + 7) // 8],
+                       non_blocking=True)
+        codes.record_stream(side)
+        ld_words.record_stream(side)
+        frame_off = qd_row_off[::H][:T + 1].cpu().numpy().astype(np.int64)
+        h_qd = torch.empty(max(nqd.value, 1), dtype=torch.uint16,
+                           pin_memory=True)
+        _lib.check(L.vfcp_encode_host(
+            pp, du.data_ptr(), dv.data_ptr(), dt_code, codes.data_ptr(),
+            qd_row_off.data_ptr(), qd.data_ptr(), modes.data_ptr(),
+            row_ll.data_ptr(), h_qd.data_ptr(), frame_off.ctypes.data, st),
+            "encode (host out)")
+        host = {"codes": h_codes, "ld": h_ld, "qd": h_qd[:nqd.value],
+                "side": side}
+    else:
+        _lib.check(L.vfcp_encode(pp, du.data_ptr(), dv.data_ptr(), dt_code,
+                                 codes.data_ptr(), qd_row_off.data_ptr(),
+                                 qd.data_ptr(), modes.data_ptr(),
+                                 _lib.ptr(scores), row_ll.data_ptr(),
+                                 _lib.ptr(recon), st), "encode")
     ll_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
     nll = ctypes.c_int64(0)
     _lib.check(L.vfcp_row_offsets(row_ll.data_ptr(), T * H,
@@ -313,12 +344,21 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                                     ll_row_off.data_ptr(), ll.data_ptr(), st),
                    "encode ll")
     ld = ld_words.view(torch.uint8)[:(N + 7) // 8]
+    if host is not None:
+        side = host.pop("side")
+        h_ll = _to_host(ll[:nll.value])
+        h_modes = _to_host(modes[:(T - 1) * nby * nbx])
+        torch.cuda.current_stream().synchronize()
+        side.synchronize()
+        host = {"codes": host["codes"].numpy(), "ld": host["ld"].numpy(),
+                "qd": host["qd"].numpy(), "ll": h_ll.numpy(),
+                "modes": h_modes.numpy()}
     return DeviceStreams(
         eps=eps, scale=S, tau=tau, codes=codes, ld=ld,
         qd=qd[:nqd.value], ll=ll[:nll.value],
         modes=modes[:(T - 1) * nby * nbx], mask=mask,
         scores=scores[:(T - 1) * nby * nbx * 2] if scores is not None else None,
-        recon=recon)
+        recon=recon, host=host)
 
 
 def archive_from_streams(f_dims, s: DeviceStreams, cfg: Config,
@@ -349,6 +389,8 @@ def _to_host(x):
 
 def streams_to_host(s: DeviceStreams) -> dict:
     import torch
+    if s.host is not None:
+        return s.host
     hs = {k: _to_host(getattr(s, k)) for k in ("codes", "ld", "qd", "ll", "modes")}
     torch.cuda.current_stream().synchronize()
     return {k: v.numpy() for k, v in hs.items()}
@@ -362,7 +404,8 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
     value range.  Every critical-point trajectory of the input is preserved
     exactly by construction."""
     cfg = config or Config()
-    s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats)
+    s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats,
+                        host_out=True)
     host = streams_to_host(s)
     a = archive_from_streams((f.H, f.W, f.T, f.dx, f.dy, f.dt), s, cfg, host)
     if cfg.stats:

@@ -449,11 +449,45 @@ int nsm_of() {
   return nsm;
 }
 
+// D2H of finished frames' symbols on a side stream (vfcp_encode_host)
+struct HostOut {
+  uint16_t* host_qd = nullptr;
+  const int64_t* frame_off = nullptr;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int init(int T) {
+    if (!host_qd) return VFCP_OK;
+    CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    ev.resize(T);
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return VFCP_OK;
+  }
+  int frame(int t, const uint16_t* qd, cudaStream_t st) {
+    if (!host_qd) return VFCP_OK;
+    const int64_t a = frame_off[t], n = frame_off[t + 1] - a;
+    if (n <= 0) return VFCP_OK;
+    CK(cudaEventRecord(ev[t], st));
+    CK(cudaStreamWaitEvent(side, ev[t], 0));
+    CK(cudaMemcpyAsync(host_qd + a, qd + a, sizeof(uint16_t) * n,
+                       cudaMemcpyDeviceToHost, side));
+    return VFCP_OK;
+  }
+  int finish() {
+    if (!side) return VFCP_OK;
+    CK(cudaStreamSynchronize(side));
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(side);
+    side = nullptr;
+    return VFCP_OK;
+  }
+  ~HostOut() { finish(); }
+};
+
 template <typename F>
 int encode_fast(const vfcp_params* p, const F* u, const F* v,
                 const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
                 uint8_t* modes, int32_t* row_ll, cudaStream_t st,
-                bool* overflowed) {
+                bool* overflowed, HostOut* ho) {
   const int H = p->H, W = p->W, T = p->T;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
@@ -531,6 +565,10 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.row_ll = row_ll + (size_t)t * H;
     LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
     LAUNCH(K_BSF, st, launch_bs_final<true>(bio, st));
+    {
+      int rch = ho->frame(t, qd, st);
+      if (rch) return rch;
+    }
   }
   int h_ovf = 0;
   CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -595,6 +633,51 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                              out_u + (size_t)t * HW, out_v + (size_t)t * HW,
                              fix_u ? fix_u + (size_t)t * HW : nullptr,
                              fix_v ? fix_v + (size_t)t * HW : nullptr, st));
+  }
+  return VFCP_OK;
+}
+
+int encode_common(const vfcp_params* p, const void* u, const void* v,
+                  int dtype, const uint8_t* codes, const int64_t* qd_row_off,
+                  void* qd, uint8_t* modes, double* scores, int32_t* row_ll,
+                  int64_t* recon, HostOut* ho, cudaStream_t st) {
+  if (fast_ok(p) && !scores && !recon && !getenv("VFCP_SLOW_PATH")) {
+    bool ovf = false;
+    int rc2 = ho->init(p->T);
+    if (rc2) return rc2;
+    rc2 = dtype == VFCP_F32
+              ? encode_fast<float>(p, (const float*)u, (const float*)v,
+                                   codes, qd_row_off, (uint16_t*)qd,
+                                   modes, row_ll, st, &ovf, ho)
+              : encode_fast<double>(p, (const double*)u, (const double*)v,
+                                    codes, qd_row_off, (uint16_t*)qd,
+                                    modes, row_ll, st, &ovf, ho);
+    if (rc2) return rc2;
+    rc2 = ho->finish();
+    if (rc2 || !ovf) return rc2;
+    // an R0 did not fit int32: redo the field with the generic kernels
+  }
+  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
+  int rc = VFCP_OK;
+#define ENC(F, I, SYM)                                                      \
+  rc = encode_impl<F, I, SYM>(p, (const F*)u, (const F*)v, codes,          \
+                              qd_row_off, (SYM*)qd, modes, scores, row_ll,  \
+                              recon, st)
+  if (dtype == VFCP_F32) {
+    if (nf) { if (ns) ENC(float, int32_t, uint16_t); else ENC(float, int32_t, uint32_t); }
+    else { if (ns) ENC(float, int64_t, uint16_t); else ENC(float, int64_t, uint32_t); }
+  } else {
+    if (nf) { if (ns) ENC(double, int32_t, uint16_t); else ENC(double, int32_t, uint32_t); }
+    else { if (ns) ENC(double, int64_t, uint16_t); else ENC(double, int64_t, uint32_t); }
+  }
+#undef ENC
+  if (rc || !ho->host_qd) return rc;
+  // generic path: the whole stream at the end
+  const int64_t n = ho->frame_off[p->T] - ho->frame_off[0];
+  if (n > 0) {
+    CK(cudaMemcpyAsync(ho->host_qd, qd, sizeof(uint16_t) * n,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
   return VFCP_OK;
 }
@@ -710,32 +793,25 @@ int vfcp_encode(const vfcp_params* p, const void* u, const void* v,
                 int64_t* recon, void* stream) {
   int rc = check_params(p);
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_ok(p) && !scores && !recon && !getenv("VFCP_SLOW_PATH")) {
-    bool ovf = false;
-    int rc2 = dtype == VFCP_F32
-                  ? encode_fast<float>(p, (const float*)u, (const float*)v,
-                                       codes, qd_row_off, (uint16_t*)qd,
-                                       modes, row_ll, st, &ovf)
-                  : encode_fast<double>(p, (const double*)u, (const double*)v,
-                                        codes, qd_row_off, (uint16_t*)qd,
-                                        modes, row_ll, st, &ovf);
-    if (rc2 || !ovf) return rc2;
-    // an R0 did not fit int32: redo the field with the generic kernels
-  }
-  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
-#define ENC(F, I, SYM)                                                      \
-  return encode_impl<F, I, SYM>(p, (const F*)u, (const F*)v, codes,         \
-                                qd_row_off, (SYM*)qd, modes, scores, row_ll, \
-                                recon, st)
-  if (dtype == VFCP_F32) {
-    if (nf) { if (ns) ENC(float, int32_t, uint16_t); else ENC(float, int32_t, uint32_t); }
-    else { if (ns) ENC(float, int64_t, uint16_t); else ENC(float, int64_t, uint32_t); }
-  } else {
-    if (nf) { if (ns) ENC(double, int32_t, uint16_t); else ENC(double, int32_t, uint32_t); }
-    else { if (ns) ENC(double, int64_t, uint16_t); else ENC(double, int64_t, uint32_t); }
-  }
-#undef ENC
+  HostOut ho;
+  return encode_common(p, u, v, dtype, codes, qd_row_off, qd, modes, scores,
+                       row_ll, recon, &ho, (cudaStream_t)stream);
+}
+
+int vfcp_encode_host(const vfcp_params* p, const void* u, const void* v,
+                     int dtype, const uint8_t* codes,
+                     const int64_t* qd_row_off, void* qd, uint8_t* modes,
+                     int32_t* row_ll, void* host_qd,
+                     const int64_t* frame_off, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (!narrow_symbols(p->radius))
+    return fail(VFCP_EINVAL, "vfcp_encode_host: radius > 32768");
+  HostOut ho;
+  ho.host_qd = (uint16_t*)host_qd;
+  ho.frame_off = frame_off;
+  return encode_common(p, u, v, dtype, codes, qd_row_off, qd, modes, nullptr,
+                       row_ll, nullptr, &ho, (cudaStream_t)stream);
 }
 
 int vfcp_encode_ll(const vfcp_params* p, const void* u, const void* v,

@@ -66,3 +66,21 @@ def test_bscan_paths_match_oracle(name):
     r = vg.reconstruct_fixed(a)
     np.testing.assert_array_equal(r.u_fp, ref["recon"][0].reshape(-1))
     np.testing.assert_array_equal(r.v_fp, ref["recon"][1].reshape(-1))
+
+
+@pytest.mark.parametrize("name", ["spectral_multicta_mop", "ints_radius16"])
+def test_host_streaming_matches_device_streams(name):
+    """compress_device(host_out=True): the symbol stream copied frame by frame
+    to pinned host memory while later frames encode equals the device
+    streams."""
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import codec
+    gen, eps, rel, pred, radius = CASES[name]
+    H, W, T, u, v = gen()
+    cfg = vg.Config(predictor=pred, radius=radius)
+    f = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v)
+    s = vg.compress_device(f, eps, cfg, relative=rel, host_out=True)
+    assert s.host is not None
+    d = codec.streams_to_host(vg.compress_device(f, eps, cfg, relative=rel))
+    for k in ("codes", "ld", "qd", "ll", "modes"):
+        np.testing.assert_array_equal(s.host[k], d[k])
