@@ -61,6 +61,7 @@ struct BScanIO {
   int32_t* lb;              // [2][nblk][32] block bottom row: local prefix
                             // (REG) or the known values (KNOWN)
   int32_t* lr;              // [2][nblk][32] block right column, likewise
+  unsigned long long* stamps;  // optional [2][nby][3] ns: start, first top, end
   int32_t* ebot;            // [2][nblk][32] exact block bottom rows (chain)
   int32_t* eright;          // [2][nblk][32] exact block right columns (chain)
   int32_t* cls;             // [2][nblk] class | code << 2
@@ -74,7 +75,7 @@ struct BScanIO {
 };
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
-constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
+constexpr int BS_HRING = 2048;  // shared boundary ring (columns), power of 2
 constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
 
 __host__ __device__ inline int bs_ntask(int nby) {
@@ -96,14 +97,22 @@ __device__ __forceinline__ uint32_t bs_msub(uint32_t a, uint32_t b, uint32_t m) 
 }
 // residue in [0, m) of any int32 (neighbouring values may come from blocks
 // with other step sizes)
+__device__ __forceinline__ uint32_t bs_res_any(int32_t v, uint32_t m, uint32_t M) {
+  // branch-free: lanes of a warp hold values of both signs
+  const uint32_t a = v < 0 ? (uint32_t)0 - (uint32_t)v : (uint32_t)v;
+  const uint32_t r = bs_umod(a, m, M);
+  return (v < 0 && r != 0u) ? m - r : r;
+}
+// residue of a neighbour's exact value: |v| < m unless the neighbour was
+// quantised with a larger step
 __device__ __forceinline__ uint32_t bs_res(int32_t v, uint32_t m, uint32_t M) {
-  if (v >= 0) return bs_umod((uint32_t)v, m, M);
-  const uint32_t r = bs_umod((uint32_t)0 - (uint32_t)v, m, M);
-  return r ? m - r : 0u;
+  const uint32_t r = (uint32_t)v + (v < 0 ? m : 0u);
+  if (r < m) return r;
+  return bs_res_any(v, m, M);
 }
 // residue of -R0 (|R0| < 2^31 - 1 on this path)
 __device__ __forceinline__ uint32_t bs_negres(int32_t r0, uint32_t m, uint32_t M) {
-  return bs_res(-r0, m, M);
+  return bs_res_any(-r0, m, M);
 }
 // representative in [-e, e] of a residue that is not the tie e
 __device__ __forceinline__ int32_t bs_rep(uint32_t r, uint32_t e, uint32_t m) {
@@ -229,6 +238,7 @@ struct BSChainSmem {
   uint32_t mtab[32];
   int task;
   alignas(16) int32_t pf[BS_NW][BS_PF][64];   // LB (0..31), LR (32..63)
+  alignas(16) int32_t pfd[BS_NW][32][4];      // per-lane sink of idle copies
   int32_t pfc[BS_NW][BS_PF];           // class word per block
   // slow path tiles, [row][col] unpadded: the skewed sweep reads column
   // s - lane in row lane, distinct banks across lanes
@@ -349,20 +359,41 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
       const int32_t* lbp = io.lb + (comp * nblk + (int64_t)bi * nbx) * 32;
       const int32_t* lrp = io.lr + (comp * nblk + (int64_t)bi * nbx) * 32;
       int32_t left = 0, corner = 0;
+      // first warp of a CTA (row above in another CTA): the tagged slots of
+      // the next two blocks are loaded ahead, so a block step does not pay
+      // an L2 round trip whenever the CTA above is ahead
+      const bool gtop = w == 0 && bi > 0;
+      uint64_t g0 = 0, g1 = 0;
+      if (gtop) {
+        if (lane < W) g0 = ld_relaxed_u64(up_gb + lane);
+        if (32 + lane < W) g1 = ld_relaxed_u64(up_gb + 32 + lane);
+      }
       // (class, LB, LR) of the next BS_PF blocks in flight (cp.async ring):
       // they do not depend on the recurrence, so the block step never waits
       // on DRAM
       auto stage = [&](int b) {
-        if (b < nbx) {
-          const int s = b % BS_PF;
-          if (lane < 8) cp_async<16>(&sm.pf[w][s][4 * lane], lbp + 32 * b + 4 * lane, true);
-          else if (lane < 16) cp_async<16>(&sm.pf[w][s][32 + 4 * (lane - 8)], lrp + 32 * b + 4 * (lane - 8), true);
-          else if (lane == 16) cp_async<4>(&sm.pfc[w][s], clsp + b, true);
-        }
+        // branch-free: lanes 0-15 copy LB / LR (16 bytes each), lane 16 the
+        // class word; the other lanes' copies are empty and land in a sink
+        const bool vb = b < nbx;
+        const int s = b % BS_PF, bb = vb ? b : 0;
+        int32_t* d16 = lane < 16 ? &sm.pf[w][s][4 * lane] : &sm.pfd[w][lane][0];
+        const int32_t* s16 = lane < 8 ? lbp + 32 * bb + 4 * lane
+                                      : lrp + 32 * bb + 4 * ((lane - 8) & 7);
+        cp_async<16>(d16, s16, vb && lane < 16);
+        int32_t* d4 = lane == 16 ? &sm.pfc[w][s] : &sm.pfd[w][lane][0];
+        cp_async<4>(d4, clsp + bb, vb && lane == 16);
         cp_async_commit();
       };
 #pragma unroll 1
       for (int b = 0; b < BS_PF; b++) stage(b);
+      auto stamp = [&](int k) {
+        if (io.stamps && lane == 0) {
+          unsigned long long tn;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+          io.stamps[((int64_t)comp * nby + bi) * 3 + k] = tn;
+        }
+      };
+      stamp(0);
       for (int bj = 0; bj < nbx; bj++) {
         const int c0 = 32 * bj;
         const int ncl = min(32, W - c0);
@@ -375,18 +406,63 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
         const int32_t lbv = sm.pf[w][slot][lane], lrv = sm.pf[w][slot][32 + lane];
         __syncwarp();
         stage(bj + BS_PF);
+        // ---- hand a bottom row to the block row below
+        auto publish = [&](int32_t b) {
+          if (!has_next) return;
+          if (out_smem) {
+            // ring slots of block bj - HRING/32 must have been read (the
+            // reads fed the consumer's computation before it bumped its
+            // counter)
+            if (bj >= BS_HRING / 32 - 1)
+              while (!__all_sync(FULL, *(volatile int*)&sm.done[w + 1] >=
+                                           bj - (BS_HRING / 32 - 1))) {
+              }
+            if (colok)
+              sm.hin[w + 1][c & (BS_HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)b;
+          } else if (colok) {
+            TaggedSlot<int32_t>::put(my_gb + c, tag_me, b);
+          }
+        };
+        // ---- everything that does not need the row above, before waiting
+        const int kind0 = cls & 3;
+        const int32_t ll = __shfl_sync(FULL, left, nr - 1);
+        uint32_t e = 0, m = 2, M = 0, pb = 0, pr = 0;
+        if (kind0 == BS_REG) {
+          if (ENC) {
+            const int code = cls >> 2;
+            e = (uint32_t)sm.etab[code];
+            m = 2u * e;
+            M = sm.mtab[code];
+            const uint32_t rc = bs_res(corner, m, M);
+            pb = bs_madd(bs_res(ll, m, M), bs_msub((uint32_t)lbv, rc, m), m);
+            pr = bs_madd(bs_res(left, m, M), bs_msub((uint32_t)lrv, rc, m), m);
+          } else {
+            pb = (uint32_t)ll - (uint32_t)corner + (uint32_t)lbv;
+            pr = (uint32_t)left - (uint32_t)corner + (uint32_t)lrv;
+          }
+        }
         // ---- the exact row above the block
         int32_t top = 0;
         if (bi > 0) {
-          if (w == 0) {
-            top = TaggedSlot<int32_t>::get(up_gb + c, tag_up, colok);
+          if (gtop) {
+            uint64_t wv = colok ? g0 : 0;
+            bool ok = !colok || (uint32_t)(wv >> 32) == tag_up;
+            while (!__all_sync(FULL, ok)) {
+              if (!ok) {
+                wv = ld_relaxed_u64(up_gb + c);
+                ok = (uint32_t)(wv >> 32) == tag_up;
+              }
+            }
+            top = (int32_t)(uint32_t)wv;
+            g0 = g1;
+            g1 = c + 64 < W ? ld_relaxed_u64(up_gb + c + 64) : 0;
           } else {
-            const volatile uint64_t* e = &sm.hin[w][c & (BS_HRING - 1)];
-            uint64_t v = colok ? *e : 0;
+            const volatile uint64_t* ep = &sm.hin[w][c & (BS_HRING - 1)];
+            uint64_t v = colok ? *ep : 0;
             bool ok = !colok || (uint32_t)(v >> 32) == (uint32_t)(c + 1);
             while (!__all_sync(FULL, ok)) {
               if (!ok) {
-                v = *e;
+                v = *ep;
                 ok = (uint32_t)(v >> 32) == (uint32_t)(c + 1);
               }
             }
@@ -394,30 +470,32 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
           }
           if (!colok) top = 0;
         }
-        int kind = cls & 3;
+        if (bj == 0) stamp(1);
+        int kind = kind0;
         int32_t bot = 0, right = 0;
+        bool published = false;
         if (kind == BS_REG) {
-          const int32_t ll = __shfl_sync(FULL, left, nr - 1);
-          const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
           if (ENC) {
-            const int code = cls >> 2;
-            const uint32_t e = (uint32_t)sm.etab[code];
-            const uint32_t m = 2u * e, M = sm.mtab[code];
-            const uint32_t rc = bs_res(corner, m, M);
-            const uint32_t rb = bs_madd(bs_madd(bs_res(top, m, M), bs_res(ll, m, M), m),
-                                        bs_msub((uint32_t)lbv, rc, m), m);
-            const uint32_t rr = bs_madd(bs_madd(bs_res(left, m, M), bs_res(tl, m, M), m),
-                                        bs_msub((uint32_t)lrv, rc, m), m);
-            const bool tie = (colok && rb == e) || (lane < nr && rr == e);
-            if (__any_sync(FULL, tie)) {
-              kind = BS_SLOW;
-            } else {
-              bot = bs_rep(rb, e, m);
-              right = bs_rep(rr, e, m);
+            // the bottom row is exact unless one of its own residues is a
+            // tie: hand it down first, the right column after
+            const uint32_t rb = bs_madd(bs_res(top, m, M), pb, m);
+            const bool btie = __any_sync(FULL, colok && rb == e);
+            if (!btie) {
+              bot = colok ? bs_rep(rb, e, m) : 0;
+              publish(bot);
+              published = true;
             }
+            const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
+            const uint32_t rr = bs_madd(pr, bs_res(tl, m, M), m);
+            const bool rtie = __any_sync(FULL, lane < nr && rr == e);
+            if (btie || rtie) kind = BS_SLOW;
+            else right = bs_rep(rr, e, m);
           } else {
-            bot = (int32_t)((uint32_t)top + (uint32_t)ll - (uint32_t)corner + (uint32_t)lbv);
-            right = (int32_t)((uint32_t)left + (uint32_t)tl - (uint32_t)corner + (uint32_t)lrv);
+            bot = colok ? (int32_t)((uint32_t)top + pb) : 0;
+            publish(bot);
+            published = true;
+            const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
+            right = (int32_t)(pr + (uint32_t)tl);
           }
         } else if (kind == BS_KNOWN) {
           bot = lbv;
@@ -432,19 +510,7 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
         }
         if (!colok) bot = 0;
         if (lane >= nr) right = 0;
-        // ---- hand the bottom row to the block row below
-        if (has_next) {
-          if (out_smem) {
-            // ring slots of block bj - 8 must have been read (the reads fed
-            // the consumer's computation before it bumped its counter)
-            while (!__all_sync(FULL, *(volatile int*)&sm.done[w + 1] >= bj - (BS_HRING / 32 - 1))) {
-            }
-            if (colok)
-              sm.hin[w + 1][c & (BS_HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)bot;
-          } else if (colok) {
-            TaggedSlot<int32_t>::put(my_gb + c, tag_me, bot);
-          }
-        }
+        if (!published) publish(bot);
         // ---- the block's exact edges for the interior pass (coalesced)
         {
           const int64_t eo = (comp * nblk + (int64_t)bi * nbx + bj) * 32 + lane;
@@ -455,6 +521,7 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
         corner = __shfl_sync(FULL, top, 31);
         left = right;
       }
+      stamp(2);
     }
     __syncthreads();
   }

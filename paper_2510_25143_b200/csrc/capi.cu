@@ -442,6 +442,22 @@ int bscan_setup(Scratch& sc, const Ladder& lad, int H, int W, int radius,
   return VFCP_OK;
 }
 
+// VFCP_CHAIN_STAMPS: per block row start / first block / end of frame 1's
+// chain (ns from the first start), to separate pipeline lag from step time
+void print_chain_stamps(const BScanIO& b, cudaStream_t st) {
+  std::vector<unsigned long long> h((size_t)2 * b.nby * 3);
+  if (cudaMemcpyAsync(h.data(), b.stamps, sizeof(unsigned long long) * h.size(),
+                      cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return;
+  unsigned long long t0 = ~0ull;
+  for (int k = 0; k < b.nby; k++) t0 = h[k * 3] < t0 ? h[k * 3] : t0;
+  fprintf(stderr, "[chain stamps] block row: start first-top end (us, comp u)\n");
+  for (int k = 0; k < b.nby; k += (b.nby > 32 ? b.nby / 32 : 1))
+    fprintf(stderr, "  %5d %9.1f %9.1f %9.1f\n", k, (h[k * 3] - t0) * 1e-3,
+            (h[k * 3 + 1] - t0) * 1e-3, (h[k * 3 + 2] - t0) * 1e-3);
+}
+
 int nsm_of() {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -541,6 +557,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   bio.pin[0] = pins; bio.pin[1] = pins + cplane;
   bio.qd = qd;
   bio.nlw = pins + 2 * cplane;
+  if (getenv("VFCP_CHAIN_STAMPS")) CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
@@ -564,6 +581,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.row_ll = row_ll + (size_t)t * H;
     LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
+    if (bio.stamps && t == 1) print_chain_stamps(bio, st);
     LAUNCH(K_BSF, st, launch_bs_final<true>(bio, st));
     {
       int rch = ho->frame(t, qd, st);
