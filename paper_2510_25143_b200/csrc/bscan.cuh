@@ -62,6 +62,11 @@ struct BScanIO {
                             // (REG) or the known values (KNOWN)
   int32_t* lr;              // [2][nblk][32] block right column, likewise
   unsigned long long* stamps;  // optional [2][nby][3] ns: start, first top, end
+  // decoder, frame t: the float64 output recon * inv_S (and optionally the
+  // int64 fixed-point recon), pitch W -- written by the interior pass
+  double* f64[2];
+  int64_t* fix[2];
+  double inv_S;
   int32_t* ebot;            // [2][nblk][32] exact block bottom rows (chain)
   int32_t* eright;          // [2][nblk][32] exact block right columns (chain)
   int32_t* cls;             // [2][nblk] class | code << 2
@@ -546,11 +551,28 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   const int64_t blk = (int64_t)bi * io.nbx + bj;
   const int32_t cls = io.cls[comp * nblk + blk];
   const int kind = cls & 3;
-  if (kind == BS_DONE || kind == BS_SLOW) return;   // warp-uniform
   const int Wp = io.Wp;
   const int32_t* a = io.a[comp];
   int32_t* out = io.out[comp];
   const bool colok = lane < ncl;
+  // decoder: every finished value also goes out as float64 (codec.py:425-426
+  // recon * (1/S), exact) and optionally as int64
+  auto emit = [&](int r, int32_t val) {
+    if (!ENC) {
+      const int64_t k = (int64_t)(r0 + r) * io.W + c0 + lane;
+      io.f64[comp][k] = __dmul_rn((double)val, io.inv_S);
+      if (io.fix[comp]) io.fix[comp][k] = val;
+    }
+  };
+  if (kind == BS_DONE || kind == BS_SLOW) {   // warp-uniform
+    // swept by the chain kernel
+    if (!ENC) {
+#pragma unroll 4
+      for (int r = 0; r < nr; r++)
+        if (colok) emit(r, __ldcg(out + (int64_t)(r0 + r) * Wp + c0 + lane));
+    }
+    return;
+  }
   int32_t xa[32];
 #pragma unroll
   for (int r = 0; r < 32; r++)
@@ -561,6 +583,7 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
       if (r < nr && colok) {
         const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
         out[k] = xa[r];
+        emit(r, xa[r]);
       }
     }
     return;
@@ -608,6 +631,7 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
       if (r < nr && colok) {
         const uint32_t val = (uint32_t)top + (uint32_t)v[r + 1][0] - (uint32_t)corner + x[r][lane];
         out[(int64_t)(r0 + r) * Wp + c0 + lane] = (int32_t)val;
+        emit(r, (int32_t)val);
       }
     }
     return;

@@ -80,9 +80,6 @@ cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
                             const int64_t*, const int64_t*, const int32_t*,
                             const int32_t*, const PrepParams&, int32_t*,
                             int32_t*, uint32_t*, uint32_t*, cudaStream_t);
-cudaError_t launch_emit_frame(const int32_t*, const int32_t*, int, int, int,
-                              double, double*, double*, int64_t*, int64_t*,
-                              cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -643,14 +640,15 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     bio.out[0] = rcur; bio.out[1] = rcur + plane;
     bio.ticket = ticket + t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+    bio.f64[0] = out_u + (size_t)t * HW;
+    bio.f64[1] = out_v + (size_t)t * HW;
+    bio.fix[0] = fix_u ? fix_u + (size_t)t * HW : nullptr;
+    bio.fix[1] = fix_v ? fix_v + (size_t)t * HW : nullptr;
+    bio.inv_S = 1.0 / p->scale;
     LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
     LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
     LAUNCH(K_BSF, st, launch_bs_final<false>(bio, st));
-    LAUNCH(K_AUX, st,
-           launch_emit_frame(rcur, rcur + plane, H, W, Wp, 1.0 / p->scale,
-                             out_u + (size_t)t * HW, out_v + (size_t)t * HW,
-                             fix_u ? fix_u + (size_t)t * HW : nullptr,
-                             fix_v ? fix_v + (size_t)t * HW : nullptr, st));
+
   }
   return VFCP_OK;
 }

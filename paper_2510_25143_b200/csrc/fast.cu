@@ -12,7 +12,8 @@
 // and the decompress path
 //   dec_prep_kernel  pins (lossless, escapes, semi-Lagrangian pixels) and
 //                    A = Pd + (sym-radius)*2e;
-//   launch_bscan<DEC>, emit_frame_kernel.
+//   the block scan (bscan.cuh), whose interior pass also writes the
+//   float64 output.
 // The reconstruction of frame t-1 is read as orig + err (encoder) or the int
 // recon frame (decoder).  Stream positions come from per-(row, chunk) prefix
 // counts, so any block can place its symbols and ll values.
@@ -874,24 +875,6 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
   }
 }
 
-// ------------------------------------------------ decoder frame output
-// int32 recon frame (pitch Wp) -> float64 output (and optionally int64)
-__global__ void __launch_bounds__(256)
-emit_frame_kernel(const int32_t* __restrict__ ru, const int32_t* __restrict__ rv,
-                  int H, int W, int Wp, double inv_S, double* __restrict__ ou,
-                  double* __restrict__ ov, int64_t* __restrict__ fu,
-                  int64_t* __restrict__ fv) {
-  // grid (column groups of 256, rows): coalesced, no divisions
-  const int i = blockIdx.y;
-  const int j = blockIdx.x * 256 + threadIdx.x;
-  if (j >= W) return;
-  const int32_t a = __ldg(ru + (int64_t)i * Wp + j), b = __ldg(rv + (int64_t)i * Wp + j);
-  const int64_t k = (int64_t)i * W + j;
-  ou[k] = __dmul_rn((double)a, inv_S);
-  ov[k] = __dmul_rn((double)b, inv_S);
-  if (fu) { fu[k] = a; fv[k] = b; }
-}
-
 // ------------------------------------------------------------ launchers
 template <typename SYM>
 cudaError_t launch_chunk_prefix(const uint8_t* codes, const SYM* qd,
@@ -959,14 +942,6 @@ cudaError_t launch_dec_prep(const uint8_t* codes, const SYM* qd,
   return cudaGetLastError();
 }
 
-cudaError_t launch_emit_frame(const int32_t* ru, const int32_t* rv, int H,
-                              int W, int Wp, double inv_S, double* ou,
-                              double* ov, int64_t* fu, int64_t* fv,
-                              cudaStream_t st) {
-  emit_frame_kernel<<<dim3((W + 255) / 256, H), 256, 0, st>>>(ru, rv, H, W, Wp,
-                                                              inv_S, ou, ov, fu, fv);
-  return cudaGetLastError();
-}
 
 
 template cudaError_t launch_chunk_prefix<uint16_t>(const uint8_t*,
