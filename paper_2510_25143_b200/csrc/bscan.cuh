@@ -67,6 +67,9 @@ struct BScanIO {
   double* f64[2];
   int64_t* fix[2];
   double inv_S;
+  // decoder: the chain runs on Z = recon - p (dec_prep_kernel); p is the
+  // previous frame's recon (pitch Wp), nullptr for frame 0
+  const int32_t* prev[2];
   int32_t* ebot;            // [2][nblk][32] exact block bottom rows (chain)
   int32_t* eright;          // [2][nblk][32] exact block right columns (chain)
   int32_t* cls;             // [2][nblk] class | code << 2
@@ -555,10 +558,22 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   const int32_t* a = io.a[comp];
   int32_t* out = io.out[comp];
   const bool colok = lane < ncl;
-  // decoder: every finished value also goes out as float64 (codec.py:425-426
-  // recon * (1/S), exact) and optionally as int64
-  auto emit = [&](int r, int32_t val) {
+  // decoder: the finished recon = Z + p goes to the recon plane (the next
+  // frame's p) and out as float64 (codec.py:425-426 recon * (1/S), exact),
+  // optionally as int64
+  const int32_t* pv = ENC ? nullptr : io.prev[comp];
+  // p of the block's rows, loaded up front (all loads in flight before the
+  // stores below, which the compiler cannot reorder them past)
+  int32_t pp[ENC ? 1 : 32];
+  if (!ENC) {
+#pragma unroll
+    for (int r = 0; r < 32; r++)
+      pp[ENC ? 0 : r] = (pv && r < nr && colok) ? __ldg(pv + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
+  }
+  auto emit = [&](int r, int32_t z) {
     if (!ENC) {
+      const int32_t val = (int32_t)((uint32_t)z + (uint32_t)pp[ENC ? 0 : r]);
+      out[(int64_t)(r0 + r) * Wp + c0 + lane] = val;
       const int64_t k = (int64_t)(r0 + r) * io.W + c0 + lane;
       io.f64[comp][k] = __dmul_rn((double)val, io.inv_S);
       if (io.fix[comp]) io.fix[comp][k] = val;
@@ -567,9 +582,13 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
   if (kind == BS_DONE || kind == BS_SLOW) {   // warp-uniform
     // swept by the chain kernel
     if (!ENC) {
-#pragma unroll 4
-      for (int r = 0; r < nr; r++)
-        if (colok) emit(r, __ldcg(out + (int64_t)(r0 + r) * Wp + c0 + lane));
+      int32_t zz[32];
+#pragma unroll
+      for (int r = 0; r < 32; r++)
+        zz[r] = (r < nr && colok) ? __ldcg(out + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
+#pragma unroll
+      for (int r = 0; r < 32; r++)
+        if (r < nr && colok) emit(r, zz[r]);
     }
     return;
   }
@@ -581,9 +600,8 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
 #pragma unroll
     for (int r = 0; r < 32; r++) {
       if (r < nr && colok) {
-        const int64_t k = (int64_t)(r0 + r) * Wp + c0 + lane;
-        out[k] = xa[r];
-        emit(r, xa[r]);
+        if (ENC) out[(int64_t)(r0 + r) * Wp + c0 + lane] = xa[r];
+        else emit(r, xa[r]);
       }
     }
     return;
@@ -630,7 +648,6 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
     for (int r = 0; r < 32; r++) {
       if (r < nr && colok) {
         const uint32_t val = (uint32_t)top + (uint32_t)v[r + 1][0] - (uint32_t)corner + x[r][lane];
-        out[(int64_t)(r0 + r) * Wp + c0 + lane] = (int32_t)val;
         emit(r, (int32_t)val);
       }
     }

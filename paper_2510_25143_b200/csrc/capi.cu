@@ -645,6 +645,8 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     bio.fix[0] = fix_u ? fix_u + (size_t)t * HW : nullptr;
     bio.fix[1] = fix_v ? fix_v + (size_t)t * HW : nullptr;
     bio.inv_S = 1.0 / p->scale;
+    bio.prev[0] = t > 0 ? rprev : nullptr;
+    bio.prev[1] = t > 0 ? rprev + plane : nullptr;
     LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
     LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
     LAUNCH(K_BSF, st, launch_bs_final<false>(bio, st));

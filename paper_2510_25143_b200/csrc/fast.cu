@@ -759,11 +759,15 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
 }
 
 // ---------------------------------------------------------- decoder prep
-// One 32x32 tile per CTA (8 warps x 4 rows, lane = column): the frame t-1
-// reconstruction of the tile and its halo is staged in shared memory once;
-// per row: pins (lossless, escapes, semi-Lagrangian pixels) and
-// A = Pd + (sym-radius)*2e for the others.  The four rows of a warp are
-// processed together so their stream loads overlap.
+// One 32x32 tile per CTA (8 warps x 4 rows, lane = column).  The decoder's
+// recurrence recon = reconU + reconL - reconUL + Pd + (sym-radius)*2e
+// (Pd = p - pU - pL + pUL of the previous frame p) is run on
+// Z = recon - p, for which the previous frame drops out:
+//   Z = ZU + ZL - ZUL + (sym-radius)*2e     (Lorenzo pixels)
+//   Z = recon - p                           (pins: lossless, escapes,
+//                                            semi-Lagrangian pixels)
+// so only pinned pixels read p; the interior pass adds p back.  The four
+// rows of a warp are processed together so their stream loads overlap.
 template <typename SYM>
 __global__ void __launch_bounds__(256)
 dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
@@ -777,7 +781,6 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
                 const int32_t* __restrict__ pre_ll, PrepParams p,
                 int32_t* __restrict__ a0, int32_t* __restrict__ a1,
                 uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v) {
-  __shared__ int32_t sp[2][33][33];   // recon(t-1), rows r0-1.., cols c0-1..
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
   const int bj = blockIdx.x, bi = blockIdx.y;
   const int c0 = 32 * bj, r0 = 32 * bi;
@@ -787,18 +790,6 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   const bool sl_blk = has_prev && modes_t && modes_t[bi * p.nbx + bj] == 1;
-  {
-#pragma unroll 5
-    for (int k = tid; k < 33 * 33; k += 256) {
-      const int rr = k / 33, cc = k - rr * 33;
-      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
-      const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
-      const int64_t m = (int64_t)i * Wp + j;
-      sp[0][rr][cc] = ok ? __ldg(rec_prev_u + m) : 0;
-      sp[1][rr][cc] = ok ? __ldg(rec_prev_v + m) : 0;
-    }
-  }
-  __syncthreads();
   const int j = c0 + lane;
   const bool colok = j < W;
   constexpr int NR = 4;
@@ -845,13 +836,8 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
     int64_t lidx = lrow[q] + pll[q] + __popc(b_eu & lt) + __popc(b_ev & lt);
     const int64_t two_e = 2 * e;
     const int64_t qu = syu[q] - p.radius, qv = syv[q] - p.radius;
-    // Pd = p - pU - pL + pUL of the previous frame (zero outside)
-    const uint32_t pd_u = (uint32_t)sp[0][rr + 1][lane + 1] - (uint32_t)sp[0][rr][lane + 1] -
-                          (uint32_t)sp[0][rr + 1][lane] + (uint32_t)sp[0][rr][lane];
-    const uint32_t pd_v = (uint32_t)sp[1][rr + 1][lane + 1] - (uint32_t)sp[1][rr][lane + 1] -
-                          (uint32_t)sp[1][rr + 1][lane] + (uint32_t)sp[1][rr][lane];
-    uint32_t val_u = pd_u + (uint32_t)(qu * two_e);
-    uint32_t val_v = pd_v + (uint32_t)(qv * two_e);
+    uint32_t val_u = (uint32_t)(qu * two_e);
+    uint32_t val_v = (uint32_t)(qv * two_e);
     const bool sl = nl && sl_blk;
     if (sl) {
       int64_t pr_u, pr_v;
@@ -862,9 +848,14 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
     }
     if (eu) { val_u = (uint32_t)ll[lidx]; lidx++; }
     if (ev) val_v = (uint32_t)ll[lidx];
-    const unsigned b_pu = __ballot_sync(FULL, colok && (eu || sl));
-    const unsigned b_pv = __ballot_sync(FULL, colok && (ev || sl));
+    const bool pu = colok && (eu || sl), pv = colok && (ev || sl);
+    const unsigned b_pu = __ballot_sync(FULL, pu);
+    const unsigned b_pv = __ballot_sync(FULL, pv);
     const int64_t pr = (int64_t)i * Wp + j;
+    if (has_prev) {   // pinned: Z = recon - p
+      if (pu) val_u -= (uint32_t)__ldg(rec_prev_u + pr);
+      if (pv) val_v -= (uint32_t)__ldg(rec_prev_v + pr);
+    }
     a0[pr] = colok ? (int32_t)val_u : 0;
     a1[pr] = colok ? (int32_t)val_v : 0;
     if (lane == 0) {
