@@ -23,8 +23,11 @@ namespace vfcp {
 
 // ----------------------------------------------------------- prefix counts
 // Per frame row: for each 32-column chunk, the number of non-lossless
-// pixels (and, for the decoder, ll entries) before it in the row.
-// One warp per row.
+// pixels (and, for the decoder, ll entries: 2 per lossless pixel plus the
+// escapes, symbol 0, among the chunk's symbols) before it in the row.
+// One warp per row, lane = chunk (32 chunks per step): every load of a step
+// is independent (a chunk's symbol range follows from the scan of the
+// non-lossless counts, not from the previous chunk's loads).
 template <typename SYM>
 __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
                                     const SYM* __restrict__ qd,
@@ -32,35 +35,101 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
                                     int64_t nrows, int W, int nchunks,
                                     int64_t tau, int32_t* __restrict__ pre_nl,
                                     int32_t* __restrict__ pre_ll) {
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= nrows) return;
-  const int64_t rb = row * W;
+  // bit c: code c quantises (e = tau >> c > 0); 31 is lossless
+  uint32_t lossy = 0;
+  for (int c = 0; c < CODE_LOSSLESS; c++)
+    if (tau > 0 && (tau >> c) != 0) lossy |= 1u << c;
+  const uint8_t* cr = codes + row * (int64_t)W;
+  const bool vec = ((row * (int64_t)W) & 15) == 0 &&
+                   ((uintptr_t)codes & 15) == 0;
+  const int64_t q0 = qd ? qd_row_off[row] : 0;
   int32_t nl_run = 0, ll_run = 0;
-  int64_t qp = qd ? qd_row_off[row] : 0;
-  for (int x = 0; x < nchunks; x++) {
-    const int j = 32 * x + lane;
-    bool nl = false, ll0 = false;
-    if (j < W) {
-      const int c = codes[rb + j];
-      nl = !(c >= CODE_LOSSLESS || tau <= 0 || (tau >> c) == 0);
+  for (int x0 = 0; x0 < nchunks; x0 += 32) {
+    const int x = x0 + lane;
+    int nl = 0, ncl = 0;
+    if (x < nchunks) {
+      const int jb = 32 * x;
+      ncl = min(32, W - jb);
+      if (vec && ncl == 32) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(cr + jb));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(cr + jb + 16));
+        const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+#pragma unroll
+          for (int y = 0; y < 4; y++) nl += (lossy >> ((wv[k] >> (8 * y)) & 31)) & 1;
+      } else {
+        for (int k = 0; k < ncl; k++) nl += (lossy >> (cr[jb + k] & 31)) & 1;
+      }
     }
-    const unsigned b = __ballot_sync(0xffffffffu, nl);
-    int esc = 0;
-    if (qd && nl) {
-      const int64_t q = qp + 2 * __popc(b & ((1u << lane) - 1u));
-      esc = (qd[q] == 0) + (qd[q + 1] == 0);
+    int incl = nl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
     }
-    if (j < W && !nl) ll0 = true;
-    int cnt = esc + (ll0 ? 2 : 0);
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) {
-      pre_nl[row * nchunks + x] = nl_run;
-      if (pre_ll) pre_ll[row * nchunks + x] = ll_run;
+    const int32_t my_nl = nl_run + incl - nl;
+    if (x < nchunks) pre_nl[row * nchunks + x] = my_nl;
+    if (pre_ll) {
+      // escapes (symbol 0) among the group's symbols: the 32 chunks'
+      // symbols are contiguous, so the warp reads them coalesced; a word
+      // with an escape is attributed to its chunk by a binary search over
+      // the chunks' starting offsets (escapes are rare)
+      int esc = 0;
+      if (qd) {
+        const int excl = incl - nl;                 // group-relative start
+        const int S = __shfl_sync(FULL, incl, 31);  // group's symbol pairs
+        const int64_t qs = q0 + 2 * (int64_t)nl_run;
+        for (int k0 = 0; k0 < S; k0 += 128) {
+          int zc[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int k = k0 + 32 * u + lane;
+            zc[u] = 0;
+            if (k < S) {
+              if (sizeof(SYM) == 2) {
+                const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qd + qs) + k);
+                zc[u] = ((w & 0xffffu) == 0u) + ((w >> 16) == 0u);
+              } else {
+                zc[u] = (__ldg(qd + qs + 2 * k) == 0) + (__ldg(qd + qs + 2 * k + 1) == 0);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (!__any_sync(FULL, zc[u] != 0)) continue;   // warp-uniform
+            const int k = k0 + 32 * u + lane;
+            int idx = 0;
+#pragma unroll
+            for (int st = 16; st; st >>= 1) {
+              const int b = __shfl_sync(FULL, excl, idx + st);
+              if (b <= k) idx += st;
+            }
+            // per-chunk escape counts: lane idx receives zc from the lanes
+            // whose words fall in its chunk
+            for (int src = 0; src < 32; src++) {
+              const int zs = __shfl_sync(FULL, zc[u], src);
+              const int is = __shfl_sync(FULL, idx, src);
+              if (zs && lane == is) esc += zs;
+            }
+          }
+        }
+      }
+      const int ll = 2 * (ncl - nl) + esc;
+      int lincl = ll;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, lincl, o);
+        if (lane >= o) lincl += y;
+      }
+      if (x < nchunks) pre_ll[row * nchunks + x] = ll_run + lincl - ll;
+      ll_run += __shfl_sync(FULL, lincl, 31);
     }
-    nl_run += __popc(b);
-    ll_run += cnt;
-    qp += 2 * __popc(b);
+    nl_run += __shfl_sync(FULL, incl, 31);
   }
 }
 
