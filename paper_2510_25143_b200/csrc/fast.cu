@@ -749,80 +749,112 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
                uint32_t* __restrict__ pin_v, uint32_t* __restrict__ nlw,
                uint16_t* __restrict__ qd, int32_t* __restrict__ row_ll) {
   const int lane = threadIdx.x & 31;
-  // grid (chunk groups of 8, rows): warp = one (row, 32-column chunk)
-  const int i = blockIdx.y, bj = blockIdx.x * 8 + (threadIdx.x >> 5);
+  // grid (chunk groups of 8, row pairs): warp = two rows of one 32-column
+  // chunk (both in the same block row), so the semi-Lagrangian departure
+  // gathers of the two rows overlap
+  constexpr int NRW = 2;
+  const int bj = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (bj >= p.nchunks) return;
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
+  const int ib = NRW * blockIdx.y;
   const int j = 32 * bj + lane;
   const bool colok = j < W;
   const int64_t HW = (int64_t)H * W;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  const int mode = p.mop ? modes_t[(i >> 5) * p.nbx + bj] : p.force_sl;
-  const int64_t row = (int64_t)p.t * H + i;
-  const int64_t pr = (int64_t)i * Wp + j;
-  const int cd = codes_p[pr];
-  const int64_t e = p.lad.e[cd];
-  const bool nl = colok && e != 0;
-  const unsigned bnl = __ballot_sync(FULL, nl);
-  const bool sl = nl && mode == 1;
-  int nll = (colok && !nl) ? 2 : 0;
-  bool pu = !nl, pv = !nl;   // lossless pixels are pinned (err 0)
-  if (sl) {
-    const F* uo = u + (int64_t)p.t * HW;
-    const F* vo = v + (int64_t)p.t * HW;
-    int64_t pr_u, pr_v;
-    sl_predict2(PairPlane{prevrec, Wp}, H, W, i, j, p.cfl_x, p.cfl_y, p.d_max,
-                p.n_max, &pr_u, &pr_v);
-    const int64_t two_e = 2 * e;
-    const double inv = p.lad.inv2e[cd];
-    const int64_t ou = load_fixed(uo, (int64_t)i * W + j, p.S);
-    const int64_t ov = load_fixed(vo, (int64_t)i * W + j, p.S);
-    const int64_t qu = quant_rha(ou - pr_u, e, inv), qv = quant_rha(ov - pr_v, e, inv);
-    const bool oku = qu > -p.radius && qu < p.radius;
-    const bool okv = qv > -p.radius && qv < p.radius;
-    a0[pr] = oku ? (int32_t)(pr_u + qu * two_e - ou) : 0;
-    a1[pr] = okv ? (int32_t)(pr_v + qv * two_e - ov) : 0;
-    const uint32_t syu = oku ? (uint32_t)(qu + p.radius) : 0u;
-    const uint32_t syv = okv ? (uint32_t)(qv + p.radius) : 0u;
-    const int64_t pos = qd_row_off[row] +
-                        2 * ((int64_t)pre_nl[row * nchunks + bj] + __popc(bnl & lt));
-    *reinterpret_cast<uint32_t*>(qd + pos) = syu | (syv << 16);
-    pu = pv = true;
-    nll = (oku ? 0 : 1) + (okv ? 0 : 1);
-  } else if (colok && !nl) {
-    a0[pr] = 0;
-    a1[pr] = 0;
-  }
-  const unsigned b_pu = __ballot_sync(FULL, colok && pu);
-  const unsigned b_pv = __ballot_sync(FULL, colok && pv);
-  const int tot = __reduce_add_sync(FULL, nll);
-  if (lane == 0) {
-    const int64_t pb = (int64_t)i * nchunks + bj;
-    pin_u[pb] = b_pu;
-    pin_v[pb] = b_pv;
-    nlw[pb] = bnl;
-    if (tot) atomicAdd(row_ll + row, tot);
+  const int mode = p.mop ? modes_t[(ib >> 5) * p.nbx + bj] : p.force_sl;
+  const F* uo = u + (int64_t)p.t * HW;
+  const F* vo = v + (int64_t)p.t * HW;
+  int cd[NRW];
+  F fu[NRW], fv[NRW];
+  int64_t spu[NRW], spv[NRW];
+#pragma unroll
+  for (int q = 0; q < NRW; q++) {
+    const int i = min(ib + q, H - 1);
+    cd[q] = codes_p[(int64_t)i * Wp + j];
+    if (mode == 1) {   // originals first: in flight during the gathers
+      fu[q] = colok ? __ldg(uo + (int64_t)i * W + j) : F(0);
+      fv[q] = colok ? __ldg(vo + (int64_t)i * W + j) : F(0);
+    }
   }
   if (mode == 1) {
-    // every pixel of a semi-Lagrangian block is pinned: its values are
-    // known, and its edges go to the block scan directly
-    const int r0 = i & ~31, ri = i - r0;
-    const int nr = min(32, H - r0), ncl = min(32, W - 32 * bj);
-    const int64_t nblk = (int64_t)p.nbx * p.nby;
-    const int64_t blk = (int64_t)(i >> 5) * p.nbx + bj;
-    const int32_t vu = colok ? a0[pr] : 0, vv = colok ? a1[pr] : 0;
-    if (ri == nr - 1) {
-      bio.lb[blk * 32 + lane] = vu;
-      bio.lb[(nblk + blk) * 32 + lane] = vv;
+    const PairPlane src{prevrec, Wp};
+    bool slow[NRW];
+    const int jc = min(j, W - 1);
+#pragma unroll
+    for (int q = 0; q < NRW; q++)
+      slow[q] = !sl_predict_rk2(src, H, W, min(ib + q, H - 1), jc, p.cfl_x,
+                                p.cfl_y, p.d_max, &spu[q], &spv[q]);
+#pragma unroll
+    for (int q = 0; q < NRW; q++)
+      if (slow[q] && colok && ib + q < H)
+        sl_predict2(src, H, W, ib + q, j, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
+                    &spu[q], &spv[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < NRW; q++) {
+    const int i = ib + q;
+    if (i >= H) break;   // warp-uniform
+    const int64_t row = (int64_t)p.t * H + i;
+    const int64_t pr = (int64_t)i * Wp + j;
+    const int64_t e = p.lad.e[cd[q]];
+    const bool nl = colok && e != 0;
+    const unsigned bnl = __ballot_sync(FULL, nl);
+    const bool sl = nl && mode == 1;
+    int nll = (colok && !nl) ? 2 : 0;
+    bool pu = !nl, pv = !nl;   // lossless pixels are pinned (err 0)
+    int32_t vu = 0, vv = 0;
+    if (sl) {
+      const int64_t two_e = 2 * e;
+      const double inv = p.lad.inv2e[cd[q]];
+      const int64_t ou = fixed_t(fu[q], p.S), ov = fixed_t(fv[q], p.S);
+      const int64_t qu = quant_rha(ou - spu[q], e, inv), qv = quant_rha(ov - spv[q], e, inv);
+      const bool oku = qu > -p.radius && qu < p.radius;
+      const bool okv = qv > -p.radius && qv < p.radius;
+      vu = oku ? (int32_t)(spu[q] + qu * two_e - ou) : 0;
+      vv = okv ? (int32_t)(spv[q] + qv * two_e - ov) : 0;
+      a0[pr] = vu;
+      a1[pr] = vv;
+      const uint32_t syu = oku ? (uint32_t)(qu + p.radius) : 0u;
+      const uint32_t syv = okv ? (uint32_t)(qv + p.radius) : 0u;
+      const int64_t pos = qd_row_off[row] +
+                          2 * ((int64_t)pre_nl[row * nchunks + bj] + __popc(bnl & lt));
+      *reinterpret_cast<uint32_t*>(qd + pos) = syu | (syv << 16);
+      pu = pv = true;
+      nll = (oku ? 0 : 1) + (okv ? 0 : 1);
+    } else if (colok && !nl) {
+      a0[pr] = 0;
+      a1[pr] = 0;
     }
-    if (lane == ncl - 1) {
-      bio.lr[blk * 32 + ri] = vu;
-      bio.lr[(nblk + blk) * 32 + ri] = vv;
+    const unsigned b_pu = __ballot_sync(FULL, colok && pu);
+    const unsigned b_pv = __ballot_sync(FULL, colok && pv);
+    const int tot = __reduce_add_sync(FULL, nll);
+    if (lane == 0) {
+      const int64_t pb = (int64_t)i * nchunks + bj;
+      pin_u[pb] = b_pu;
+      pin_v[pb] = b_pv;
+      nlw[pb] = bnl;
+      if (tot) atomicAdd(row_ll + row, tot);
     }
-    if (ri == 0 && lane == 0) {
-      bio.cls[blk] = BS_KNOWN;
-      bio.cls[nblk + blk] = BS_KNOWN;
+    if (mode == 1) {
+      // every pixel of a semi-Lagrangian block is pinned: its values are
+      // known, and its edges go to the block scan directly
+      const int r0 = i & ~31, ri = i - r0;
+      const int nr = min(32, H - r0), ncl = min(32, W - 32 * bj);
+      const int64_t nblk = (int64_t)p.nbx * p.nby;
+      const int64_t blk = (int64_t)(i >> 5) * p.nbx + bj;
+      if (ri == nr - 1) {
+        bio.lb[blk * 32 + lane] = vu;
+        bio.lb[(nblk + blk) * 32 + lane] = vv;
+      }
+      if (lane == ncl - 1) {
+        bio.lr[blk * 32 + ri] = vu;
+        bio.lr[(nblk + blk) * 32 + ri] = vv;
+      }
+      if (ri == 0 && lane == 0) {
+        bio.cls[blk] = BS_KNOWN;
+        bio.cls[nblk + blk] = BS_KNOWN;
+      }
     }
   }
 }
@@ -979,7 +1011,7 @@ cudaError_t launch_enc_pix(const F* u, const F* v, const uint8_t* codes_p,
                            int32_t* a0, int32_t* a1,
                            uint32_t* pin_u, uint32_t* pin_v, uint32_t* nlw,
                            uint16_t* qd, int32_t* row_ll, cudaStream_t st) {
-  const dim3 grid((p.nchunks + 7) / 8, p.H);
+  const dim3 grid((p.nchunks + 7) / 8, (p.H + 1) / 2);
   enc_pix_kernel<F><<<grid, 256, 0, st>>>(
       u, v, codes_p, reinterpret_cast<const int2*>(prevrec), qd_row_off,
       pre_nl, p, modes_t, bio, a0, a1, pin_u, pin_v, nlw, qd, row_ll);
