@@ -537,22 +537,21 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
 
 // ------------------------------------------------------------ phase C
 // CTA = one block, warp = component.
+// The interior of block (bi, bj), component comp, by one warp (lane =
+// column); x, v: the warp's shared tiles.
 template <bool ENC>
-__global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
-  __shared__ uint32_t sx[2][32][33];
-  __shared__ int32_t sv[2][33][33];
-  __shared__ int32_t etab[32];
-  __shared__ uint32_t mtab[32];
+__device__ __forceinline__ void bs_final_block(const BScanIO& io,
+                                               uint32_t (*x)[33],
+                                               int32_t (*v)[33],
+                                               const int32_t* etab,
+                                               const uint32_t* mtab, int bi,
+                                               int bj, int comp, int lane) {
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
-  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
-  __syncthreads();
-  const int bj = blockIdx.x, bi = blockIdx.y;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
   const int64_t nblk = (int64_t)io.nbx * io.nby;
   const int64_t blk = (int64_t)bi * io.nbx + bj;
-  const int32_t cls = io.cls[comp * nblk + blk];
+  const int32_t cls = __ldcg(io.cls + comp * nblk + blk);
   const int kind = cls & 3;
   const int Wp = io.Wp;
   const int32_t* a = io.a[comp];
@@ -619,8 +618,6 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
     m = 2u * e;
     M = mtab[code];
   }
-  uint32_t(*x)[33] = sx[comp];
-  int32_t(*v)[33] = sv[comp];
 #pragma unroll
   for (int r = 0; r < 32; r++) x[r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
   v[0][lane + 1] = top;
@@ -709,6 +706,19 @@ __global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
       io.qd[qr + 2 * lane] = (uint16_t)(q + radius);
     }
   }
+}
+
+template <bool ENC>
+__global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
+  __shared__ uint32_t sx[2][32][33];
+  __shared__ int32_t sv[2][33][33];
+  __shared__ int32_t etab[32];
+  __shared__ uint32_t mtab[32];
+  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
+  __syncthreads();
+  bs_final_block<ENC>(io, sx[comp], sv[comp], etab, mtab, blockIdx.y,
+                      blockIdx.x, comp, lane);
 }
 
 template <bool ENC>
