@@ -62,6 +62,8 @@ struct BScanIO {
                             // (REG) or the known values (KNOWN)
   int32_t* lr;              // [2][nblk][32] block right column, likewise
   unsigned long long* stamps;  // optional [2][nby][3] ns: start, first top, end
+  unsigned long long* prog;    // [2][nby]: frame tag << 32 | blocks finished
+  uint32_t frame_tag;          // unique per frame of a call (t + 1)
   // decoder, frame t: the float64 output recon * inv_S (and optionally the
   // int64 fixed-point recon), pitch W -- written by the interior pass
   double* f64[2];
@@ -83,8 +85,9 @@ struct BScanIO {
 };
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
-constexpr int BS_HRING = 2048;  // shared boundary ring (columns), power of 2
+constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
 constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
+constexpr int BS_SEG = 32;      // blocks per progress mark / interior task
 
 __host__ __device__ inline int bs_ntask(int nby) {
   return 2 * ((nby + BS_NW - 1) / BS_NW);
@@ -239,21 +242,32 @@ __global__ void __launch_bounds__(64) bs_local_kernel(BScanIO io) {
 }
 
 // ------------------------------------------------------------ phase B
+// Shared memory of the fused chain / interior kernel.  The interior tiles
+// (tasks after the chain tasks) overlay the chain-only region.
+struct BSFinTiles {
+  uint32_t x[BS_NW][32][33];
+  int32_t v[BS_NW][33][33];
+};
 struct BSChainSmem {
-  uint64_t hin[BS_NW + 1][BS_HRING];   // tagged (column + 1) << 32 | value
-  int done[BS_NW];                     // blocks warp w has consumed
   int32_t etab[32];
   uint32_t mtab[32];
   int task;
+  int done[BS_NW];                     // blocks warp w has consumed
   alignas(16) int32_t pf[BS_NW][BS_PF][64];   // LB (0..31), LR (32..63)
   alignas(16) int32_t pfd[BS_NW][32][4];      // per-lane sink of idle copies
   int32_t pfc[BS_NW][BS_PF];           // class word per block
-  // slow path tiles, [row][col] unpadded: the skewed sweep reads column
-  // s - lane in row lane, distinct banks across lanes
-  int32_t tv[BS_NW][32][32];           // slow path: values
-  uint16_t ts[BS_NW][32][32];          // slow path: symbols (encoder)
-  int64_t tq[BS_NW][32];               // slow path: row stream offsets
-  uint8_t tc[BS_NW][32][32];           // slow path: codes (encoder)
+  union {
+    struct {
+      uint64_t hin[BS_NW + 1][BS_HRING];   // tagged (column + 1) << 32 | value
+      // slow path tiles, [row][col] unpadded: the skewed sweep reads column
+      // s - lane in row lane, distinct banks across lanes
+      int32_t tv[BS_NW][32][32];           // slow path: values
+      uint16_t ts[BS_NW][32][32];          // slow path: symbols (encoder)
+      int64_t tq[BS_NW][32];               // slow path: row stream offsets
+      uint8_t tc[BS_NW][32][32];           // slow path: codes (encoder)
+    };
+    BSFinTiles fin;
+  };
 };
 
 template <bool ENC>
@@ -332,6 +346,14 @@ __device__ __forceinline__ void bs_slow_block(
 }
 
 template <bool ENC>
+__device__ __forceinline__ void bs_final_block(const BScanIO& io,
+                                               uint32_t (*x)[33],
+                                               int32_t (*v)[33],
+                                               const int32_t* etab,
+                                               const uint32_t* mtab, int bi,
+                                               int bj, int comp, int lane);
+
+template <bool ENC>
 __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSChainSmem& sm = *reinterpret_cast<BSChainSmem*>(smem_raw);
@@ -351,7 +373,35 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
       (&sm.hin[0][0])[k] = 0;
     __syncthreads();
     const int task = sm.task;
-    if (task >= ntask) break;
+    if (task >= ntask) {
+      // ---- interior tasks: (block row, segment of BS_SEG blocks, comp),
+      // in block-row order, each once the chain has finished the segment
+      // in its row and in the row above
+      const int nseg = (nbx + BS_SEG - 1) / BS_SEG;
+      const int ft = task - ntask;
+      if (ft >= 2 * nby * nseg) break;
+      const int comp = ft & 1, rs = ft >> 1;
+      const int bi = rs / nseg, sg = rs - bi * nseg;
+      const int b0 = sg * BS_SEG, b1 = min(nbx, b0 + BS_SEG);
+      if (threadIdx.x == 0) {
+        const unsigned long long need = ((unsigned long long)io.frame_tag << 32) | (unsigned)b1;
+        for (int r = bi; r >= bi - 1 && r >= 0; r--) {
+          const volatile unsigned long long* pg = io.prog + (int64_t)comp * nby + r;
+          long long spins = 0;
+          while (*pg < need) {
+            __nanosleep(128);
+            if (++spins > (1ll << 28)) __trap();   // never: a hang guard
+          }
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      for (int bj = b0 + w; bj < b1; bj += BS_NW)
+        bs_final_block<ENC>(io, sm.fin.x[w], sm.fin.v[w], sm.etab, sm.mtab, bi,
+                            bj, comp, lane);
+      __syncthreads();
+      continue;
+    }
     const int g = task >> 1, comp = task & 1;
     const int bi = g * BS_NW + w;
     if (bi < nby) {
@@ -526,6 +576,15 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
           io.eright[eo] = right;
         }
         if (lane == 0) *(volatile int*)&sm.done[w] = bj + 1;
+        // progress for the interior tasks: the block edges (and any swept
+        // block) are visible GPU-wide before the mark
+        if ((bj + 1) % BS_SEG == 0 || bj + 1 == nbx) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0)
+            *(volatile unsigned long long*)(io.prog + (int64_t)comp * nby + bi) =
+                ((unsigned long long)io.frame_tag << 32) | (unsigned)(bj + 1);
+        }
         corner = __shfl_sync(FULL, top, 31);
         left = right;
       }
@@ -737,8 +796,10 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC>,
                                                     32 * BS_NW, smem);
   if (e != cudaSuccess) return e;
-  const int ntask = bs_ntask(io.nby);
-  // persistent: every CTA is resident, tickets in block-row order
+  const int ntask = bs_ntask(io.nby) +
+                    2 * io.nby * ((io.nbx + BS_SEG - 1) / BS_SEG);
+  // persistent: every CTA is resident; tickets hand out the chain tasks
+  // (block-row order) first, then the interior tasks
   bs_chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
   return cudaGetLastError();
 }

@@ -424,6 +424,8 @@ int bscan_setup(Scratch& sc, const Ladder& lad, int H, int W, int radius,
   CK(sc.get(&b->lb, (size_t)2 * nblk * 32));
   CK(sc.get(&b->lr, (size_t)2 * nblk * 32));
   CK(sc.get(&b->ebot, (size_t)2 * nblk * 32));
+  CK(sc.get(&b->prog, (size_t)2 * nby));
+  CK(cudaMemsetAsync(b->prog, 0, sizeof(unsigned long long) * 2 * nby, st));
   CK(sc.get(&b->eright, (size_t)2 * nblk * 32));
   CK(sc.get(&b->cls, (size_t)2 * nblk));
   CK(sc.get(&b->bnd, (size_t)ntask * W));
@@ -577,9 +579,9 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.row_ll = row_ll + (size_t)t * H;
+    bio.frame_tag = (uint32_t)t + 1u;
     LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
     if (bio.stamps && t == 1) print_chain_stamps(bio, st);
-    LAUNCH(K_BSF, st, launch_bs_final<true>(bio, st));
     {
       int rch = ho->frame(t, qd, st);
       if (rch) return rch;
@@ -648,8 +650,8 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     bio.prev[0] = t > 0 ? rprev : nullptr;
     bio.prev[1] = t > 0 ? rprev + plane : nullptr;
     LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
+    bio.frame_tag = (uint32_t)t + 1u;
     LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
-    LAUNCH(K_BSF, st, launch_bs_final<false>(bio, st));
 
   }
   return VFCP_OK;
