@@ -47,10 +47,10 @@ ALGO_BYTES = {
     # enc_pix: codes, pin / non-lossless words (semi-Lagrangian pixels are a
     # data-dependent share on top)
     "pix": 1.0 + 12.0 / 32.0,
-    # block scan: two 32-value edges per block and component (chain); R0
-    # planes in, err planes + 2 x u16 symbols out (final)
-    "bs_chain": 2 * 2 * 2 * 32 * 4 / 1024.0,
-    "bs_final": 8.0 + 8.0 + 4.0,
+    # block scan (bs_chain_kernel: chain tasks + interior tasks): two
+    # 32-value edges per block and component, then R0 planes in, err planes
+    # + 2 x u16 symbols out
+    "bs_chain": 2 * 2 * 2 * 32 * 4 / 1024.0 + 8.0 + 8.0 + 4.0,
     "scan": 1.0,                       # codes
     # decoder: dec_prep (codes, symbols, recon(t-1) in; A planes out)
     "decode_rows": 1.0 + 4.0 + 8.0 + 8.0,

@@ -34,9 +34,12 @@
 //                     are handed to the warp below) -- the critical path is
 //                     ~nby + nbx cheap block steps instead of H + W pixel
 //                     steps of a per-pixel wavefront;
-//   bs_final_kernel   fully parallel: the interior of every block from its
+//   phase C           fully parallel: the interior of every block from its
 //                     exact boundary (prefix sums in shared memory, ties
-//                     resolved in raster order, symbols).
+//                     resolved in raster order, symbols) -- tasks of the
+//                     same persistent kernel, handed out after the chain
+//                     tasks and started per 32-block segment as soon as the
+//                     chain has published it, so they overlap the chain.
 #pragma once
 
 #include "frame.cuh"
@@ -768,19 +771,6 @@ __device__ __forceinline__ void bs_final_block(const BScanIO& io,
 }
 
 template <bool ENC>
-__global__ void __launch_bounds__(64) bs_final_kernel(BScanIO io) {
-  __shared__ uint32_t sx[2][32][33];
-  __shared__ int32_t sv[2][33][33];
-  __shared__ int32_t etab[32];
-  __shared__ uint32_t mtab[32];
-  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
-  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
-  __syncthreads();
-  bs_final_block<ENC>(io, sx[comp], sv[comp], etab, mtab, blockIdx.y,
-                      blockIdx.x, comp, lane);
-}
-
-template <bool ENC>
 cudaError_t launch_bs_local(const BScanIO& io, cudaStream_t st) {
   bs_local_kernel<ENC><<<dim3(io.nbx, io.nby), 64, 0, st>>>(io);
   return cudaGetLastError();
@@ -804,10 +794,5 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <bool ENC>
-cudaError_t launch_bs_final(const BScanIO& io, cudaStream_t st) {
-  bs_final_kernel<ENC><<<dim3(io.nbx, io.nby), 64, 0, st>>>(io);
-  return cudaGetLastError();
-}
 
 }  // namespace vfcp
