@@ -20,39 +20,78 @@
 namespace vfcp {
 
 // ---------------------------------------------------------------- K0
+// min / max / max |.| over u and v (field.py:69-73, 300-310).  Element
+// minima and maxima are exact in the input precision; binary32 input is
+// read as 16-byte vectors, four in flight per thread.
+__device__ __forceinline__ void range_acc(float x, float& lo, float& hi,
+                                          float& ma) {
+  lo = fminf(lo, x);
+  hi = fmaxf(hi, x);
+  ma = fmaxf(ma, fabsf(x));
+}
+__device__ __forceinline__ void range_acc(double x, double& lo, double& hi,
+                                          double& ma) {
+  lo = fmin(lo, x);
+  hi = fmax(hi, x);
+  ma = fmax(ma, fabs(x));
+}
+
 template <typename F>
 __global__ void __launch_bounds__(256) range_kernel(const F* __restrict__ u,
                                                     const F* __restrict__ v,
                                                     int64_t n,
                                                     double* __restrict__ part) {
-  double lo = INFINITY, hi = -INFINITY, ma = 0.0;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  F lo = F(INFINITY), hi = F(-INFINITY), ma = F(0);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int c = 0; c < 2; c++) {
     const F* p = c ? v : u;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += stride) {
-      double x = (double)__ldg(p + k);
-      lo = fmin(lo, x);
-      hi = fmax(hi, x);
-      ma = fmax(ma, fabs(x));
+    int64_t head = 0;
+    if (sizeof(F) == 4 && ((uintptr_t)p & 15) == 0) {
+      const float4* p4 = reinterpret_cast<const float4*>(p);
+      const int64_t n4 = n / 4;
+      constexpr int U = 4;
+      int64_t k = tid;
+      for (; k + (U - 1) * stride < n4; k += U * stride) {
+        float4 q[U];
+#pragma unroll
+        for (int e = 0; e < U; e++) q[e] = __ldg(p4 + k + e * stride);
+#pragma unroll
+        for (int e = 0; e < U; e++) {
+          range_acc((F)q[e].x, lo, hi, ma);
+          range_acc((F)q[e].y, lo, hi, ma);
+          range_acc((F)q[e].z, lo, hi, ma);
+          range_acc((F)q[e].w, lo, hi, ma);
+        }
+      }
+      for (; k < n4; k += stride) {
+        const float4 q = __ldg(p4 + k);
+        range_acc((F)q.x, lo, hi, ma);
+        range_acc((F)q.y, lo, hi, ma);
+        range_acc((F)q.z, lo, hi, ma);
+        range_acc((F)q.w, lo, hi, ma);
+      }
+      head = 4 * n4;
     }
+    for (int64_t k = head + tid; k < n; k += stride) range_acc(__ldg(p + k), lo, hi, ma);
   }
+  double dlo = (double)lo, dhi = (double)hi, dma = (double)ma;
   for (int o = 16; o; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+    dlo = fmin(dlo, __shfl_xor_sync(0xffffffffu, dlo, o));
+    dhi = fmax(dhi, __shfl_xor_sync(0xffffffffu, dhi, o));
+    dma = fmax(dma, __shfl_xor_sync(0xffffffffu, dma, o));
   }
   __shared__ double s[3][8];
   int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { s[0][w] = lo; s[1][w] = hi; s[2][w] = ma; }
+  if (l == 0) { s[0][w] = dlo; s[1][w] = dhi; s[2][w] = dma; }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
-      lo = fmin(lo, s[0][q]); hi = fmax(hi, s[1][q]); ma = fmax(ma, s[2][q]);
+      dlo = fmin(dlo, s[0][q]); dhi = fmax(dhi, s[1][q]); dma = fmax(dma, s[2][q]);
     }
-    part[3 * blockIdx.x + 0] = lo;
-    part[3 * blockIdx.x + 1] = hi;
-    part[3 * blockIdx.x + 2] = ma;
+    part[3 * blockIdx.x + 0] = dlo;
+    part[3 * blockIdx.x + 1] = dhi;
+    part[3 * blockIdx.x + 2] = dma;
   }
 }
 
