@@ -554,37 +554,34 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
   }
   bool swept = false;
   if (wid < 2) {
-    // R0 tile of this warp's component (lane = column)
-    const int32_t* ap = wid ? a1 : a0;
-#pragma unroll 8
-    for (int r = 0; r < 32; r++)
-      sm.r0[wid][r][lane] = r < nr ? __ldg(ap + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
-    __syncwarp();
     // Lorenzo trial of component wid with block-local errors (mop.py:88-110).
     // Every pixel uses the step tau', so unless a pixel can escape
     // (|R0| >= (2 radius - 4) tau') the trial errors are the representatives
     // of the block's 2D prefix sums of -R0 mod 2 tau' (see bscan.cuh), with
     // a zero boundary (outside the block the candidate is the original).
-    const int comp = wid;
     // (|R0| < 2^30 as well: the sample arithmetic below is then exact in
-    // int32)
-    int64_t lim = (2 * (int64_t)radius - 4) * tau;
-    if (lim > ((int64_t)1 << 30)) lim = (int64_t)1 << 30;
+    // int32.)  The R0 tile (lane = column) goes to shared memory together
+    // with its residues.
+    const int comp = wid;
+    const int32_t* ap = wid ? a1 : a0;
+    int64_t lim64 = (2 * (int64_t)radius - 4) * tau;
+    if (lim64 > ((int64_t)1 << 30)) lim64 = (int64_t)1 << 30;
+    const int32_t lim = (int32_t)(lim64 > 0 ? lim64 : 0);
+    const uint32_t m = 2u * (uint32_t)e, ue = (uint32_t)e;
+    const uint32_t M = (uint32_t)((((uint64_t)1) << 32) / m);
+    int32_t(*v)[33] = sm.q0[comp];
+    int32_t(*x)[33] = sm.r0[comp];
     bool safe = lim > 0;
 #pragma unroll 8
     for (int r = 0; r < 32; r++) {
-      const int32_t x0 = sm.r0[comp][r][lane];
-      safe &= (x0 < 0 ? -(int64_t)x0 : (int64_t)x0) < lim;
+      const int32_t x0 = r < nr ? __ldg(ap + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
+      x[r][lane] = x0;
+      v[r][lane] = (int32_t)bs_negres(x0, m, M);
+      safe &= (x0 < 0 ? -x0 : x0) < lim;   // |R0| < 2^31 - 1 (enc_r0)
     }
     swept = !__all_sync(FULL, safe);
+    __syncwarp();
     if (!swept) {
-      const uint32_t m = 2u * (uint32_t)e, ue = (uint32_t)e;
-      const uint32_t M = (uint32_t)((((uint64_t)1) << 32) / m);
-      int32_t(*v)[33] = sm.q0[comp];
-      int32_t(*x)[33] = sm.r0[comp];
-#pragma unroll 8
-      for (int r = 0; r < 32; r++) v[r][lane] = (int32_t)bs_negres(x[r][lane], m, M);
-      __syncwarp();
       uint32_t acc = 0;
 #pragma unroll 8
       for (int k = 0; k < 32; k++) {   // row prefix, lane = row
@@ -629,21 +626,28 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
       }
       __syncwarp();
       // |idx| at the stride samples: x + err = q * 2 tau' exactly
-      const bool scol = lane < ncl && (lane % p.stride) == 0;
-      const int sj = lane / p.stride;
-      int srow = 0;
+      auto sample = [&](int r, int j) {
+        const int32_t d = (r > 0 ? v[r - 1][j] : 0) + (j > 0 ? v[r][j - 1] : 0) -
+                          ((r > 0 && j > 0) ? v[r - 1][j - 1] : 0);
+        const int32_t n = x[r][j] - d + v[r][j];
+        const uint32_t an = (uint32_t)(n < 0 ? -n : n);
+        uint32_t qa = __umulhi(an, M);
+        if (qa * m != an) qa++;
+        return (int32_t)qa;
+      };
+      if (p.stride == 2) {
+        // lane = (sample column, row parity): two sample rows per step
+        const int sj = lane & 15, j = 2 * sj, rp = lane >> 4;
+#pragma unroll 2
+        for (int r = 2 * rp; r < nr; r += 4)
+          if (j < ncl) sm.samp[0][2 * ((r >> 1) * nsx + sj) + comp] = sample(r, j);
+      } else {
+        const bool scol = lane < ncl && (lane % p.stride) == 0;
+        const int sj = lane / p.stride;
+        int srow = 0;
 #pragma unroll 1
-      for (int r = 0; r < nr; r += p.stride, srow += nsx) {
-        if (scol) {
-          const int j = lane;
-          const int32_t d = (r > 0 ? v[r - 1][j] : 0) + (j > 0 ? v[r][j - 1] : 0) -
-                            ((r > 0 && j > 0) ? v[r - 1][j - 1] : 0);
-          const int32_t n = x[r][j] - d + v[r][j];
-          const uint32_t an = (uint32_t)(n < 0 ? -n : n);
-          uint32_t qa = __umulhi(an, M);
-          if (qa * m != an) qa++;
-          sm.samp[0][2 * (srow + sj) + comp] = (int32_t)qa;
-        }
+        for (int r = 0; r < nr; r += p.stride, srow += nsx)
+          if (scol) sm.samp[0][2 * (srow + sj) + comp] = sample(r, lane);
       }
     }
   }
