@@ -157,6 +157,22 @@ int vfcp_huff_unpack(const uint8_t* data, int64_t total_bits,
                      const uint8_t* lens, int32_t alphabet, int64_t n,
                      void* out, int sym_bytes);
 
+/* Device-side entropy stage (huffman.py:16-76 encode): counts of
+ * a device symbol array (sym_bytes 1 or 2) added into device u64
+ * counts[alphabet]; wbase: the first bin of the shared-memory window (the
+ * symbols' mode, e.g. radius - 4096 for the residual stream). */
+int vfcp_huff_hist_dev(const void* symbols, int sym_bytes, int64_t n,
+                       int32_t alphabet, int32_t wbase,
+                       unsigned long long* counts, void* stream);
+
+/* MSB-first canonical-Huffman bits of a device symbol array under the code
+ * lengths lens_host (host, from vfcp_huff_lengths) into device out_words
+ * (n_words >= ceil(total_bits / 32); zeroed here): the bytes are the
+ * reference's _pack_bits output. */
+int vfcp_huff_pack_dev(const void* symbols, int sym_bytes, int64_t n,
+                       const uint8_t* lens_host, int32_t alphabet,
+                       uint32_t* out_words, int64_t n_words, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -404,6 +404,21 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
     value range.  Every critical-point trajectory of the input is preserved
     exactly by construction."""
     cfg = config or Config()
+    if not cfg.stats and cfg.radius <= 32768:
+        # entropy stage on the device (csrc/huffman_gpu.cu): only the packed
+        # sections come back; zlib stays on the host
+        s = compress_device(f, eps, cfg, relative)
+        nby, nbx = _mode_grid_shape(f.H, f.W, cfg)
+        q_xi = huffman.encode_device(s.codes, EB_ALPHABET, 0)
+        q_d = huffman.encode_device(s.qd, 2 * cfg.radius,
+                                    max(0, cfg.radius - 4096))
+        return Archive(
+            H=f.H, W=f.W, T=f.T, dx=f.dx, dy=f.dy, dt=f.dt, scale=s.scale,
+            eps=s.eps, tau_prime=s.tau, config=cfg, q_xi=q_xi, q_d=q_d,
+            l_d=s.ld.cpu().numpy().tobytes(),
+            lossless_stream=s.ll.cpu().numpy().astype("<i8").tobytes(),
+            mode_bitmap=np.packbits(s.modes.cpu().numpy()).tobytes(),
+        )
     s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats,
                         host_out=True)
     host = streams_to_host(s)

@@ -707,6 +707,11 @@ int encode_common(const vfcp_params* p, const void* u, const void* v,
 extern "C" {
 
 const char* vfcp_last_error(void) { return g_err.c_str(); }
+}  // extern "C"
+
+int vfcp_record_error(int code, const char* msg) { return fail(code, msg); }
+
+extern "C" {
 int vfcp_version(void) { return 1; }
 
 int64_t vfcp_launch_count(void) { return g_prof.launches; }

@@ -1,10 +1,11 @@
-"""Canonical Huffman coding over a fixed integer alphabet (host backend).
+"""Canonical Huffman coding over a fixed integer alphabet.
 
 Same blob layout and bytes as the reference (huffman.py:16,101-149):
 ``<IQQ`` (alphabet, symbol count, bit count) + one length byte per symbol +
-MSB-first code bits.  The heavy loops run in the native library
-(csrc/huffman.cpp, multi-threaded packing); this stage stays on the host, as
-in the reference, and is timed separately from the device pipeline.
+MSB-first code bits.  ``encode`` runs on the host (csrc/huffman.cpp,
+multi-threaded packing); ``encode_device`` packs a device symbol array on
+the GPU (csrc/huffman_gpu.cu: histogram and bit packing on the device, the
+code lengths on the host) and copies only the packed bytes back.
 """
 
 from __future__ import annotations
@@ -64,6 +65,38 @@ def encode(symbols, alphabet_size: int) -> bytes:
                                     bits.ref(), _lib.host_threads()),
                    "huffman pack")
     return _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes() + out.tobytes()
+
+
+def encode_device(symbols, alphabet_size: int, window_base: int = 0) -> bytes:
+    """encode() of a CUDA uint8 / uint16 tensor: the same bytes.
+
+    window_base: first symbol of the shared-memory histogram window (the
+    symbols' mode; radius - 4096 for the residual stream)."""
+    import torch
+    n = int(symbols.numel())
+    sb = symbols.element_size()
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    counts = torch.zeros(alphabet_size, dtype=torch.int64, device=symbols.device)
+    if n:
+        _lib.check(L.vfcp_huff_hist_dev(symbols.data_ptr(), sb, n, alphabet_size,
+                                        window_base, counts.data_ptr(), st),
+                   "huffman histogram")
+    counts_h = counts.cpu().numpy()
+    lens = code_lengths(counts_h)
+    total_bits = int((counts_h * lens.astype(np.int64)).sum())
+    n_words = max(1, (total_bits + 31) // 32)
+    words = torch.empty(n_words, dtype=torch.int32, device=symbols.device)
+    if n:
+        _lib.check(L.vfcp_huff_pack_dev(symbols.data_ptr(), sb, n,
+                                        lens.ctypes.data, alphabet_size,
+                                        words.data_ptr(), n_words, st),
+                   "huffman pack (device)")
+    h = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
+    h.copy_(words, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    packed = h.numpy().view(np.uint8)[:(total_bits + 7) // 8]
+    return _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes() + packed.tobytes()
 
 
 def decode(blob, out_dtype=np.int64) -> np.ndarray:

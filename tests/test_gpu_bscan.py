@@ -84,3 +84,21 @@ def test_host_streaming_matches_device_streams(name):
     d = codec.streams_to_host(vg.compress_device(f, eps, cfg, relative=rel))
     for k in ("codes", "ld", "qd", "ll", "modes"):
         np.testing.assert_array_equal(s.host[k], d[k])
+
+
+@pytest.mark.parametrize("name", ["spectral_multicta_mop", "ints_radius16",
+                                  "tiny_tau_mop"])
+def test_device_huffman_matches_host(name):
+    """huffman.encode_device (histogram + canonical-code bit packing on the
+    GPU) gives the host encoder's bytes, for the eb codes and the residual
+    symbols."""
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import huffman
+    gen, eps, rel, pred, radius = CASES[name]
+    H, W, T, u, v = gen()
+    cfg = vg.Config(predictor=pred, radius=radius)
+    f = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v)
+    s = vg.compress_device(f, eps, cfg, relative=rel)
+    assert huffman.encode_device(s.codes, 32) == huffman.encode(s.codes.cpu().numpy(), 32)
+    assert (huffman.encode_device(s.qd, 2 * radius, max(0, radius - 4096))
+            == huffman.encode(s.qd.cpu().numpy(), 2 * radius))
