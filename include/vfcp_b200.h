@@ -173,6 +173,18 @@ int vfcp_huff_pack_dev(const void* symbols, int sym_bytes, int64_t n,
                        const uint8_t* lens_host, int32_t alphabet,
                        uint32_t* out_words, int64_t n_words, void* stream);
 
+/* huffman.py:79-98 decode on the device: the packed bytes as 32-bit words
+ * (device, n_words >= ceil(total_bits / 32) + 2, padding zero) -> n symbols
+ * (sym_bytes 1 or 2) in device `out`.  Chunks of the stream are decoded in
+ * parallel and resynchronised to the sequential decoder's codeword
+ * boundaries.  VFCP_ECORRUPT for a stream the sequential decoder would not
+ * consume exactly (the caller then decodes on the host for the reference's
+ * exact error). */
+int vfcp_huff_unpack_dev(const uint32_t* words, int64_t n_words,
+                         int64_t total_bits, const uint8_t* lens_host,
+                         int32_t alphabet, int64_t n, void* out,
+                         int sym_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ _SIGS = {
     "vfcp_huff_unpack": (_I, [_P, _I64, _P, _I32, _I64, _P, _I]),
     "vfcp_huff_hist_dev": (_I, [_P, _I, _I64, _I32, _I32, _P, _P]),
     "vfcp_huff_pack_dev": (_I, [_P, _I, _I64, _P, _I32, _P, _I64, _P]),
+    "vfcp_huff_unpack_dev": (_I, [_P, _I64, _I64, _P, _I32, _I64, _P, _I, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -451,16 +451,28 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
     cfg = a.config
     n = a.H * a.W * a.T
     if codes is None:
-        codes = huffman.decode(a.q_xi, np.uint8)
+        # entropy decode on the device (huffman.decode_device)
+        codes = huffman.decode_device(a.q_xi, np.uint8)
     if codes.shape[0] != n:
         raise ValueError("eb code stream length mismatch")
     if len(a.l_d) < (n + 7) // 8:
         # np.unpackbits(...)[:n] is shorter than n: never equal to eq == 0
         raise ValueError("lossless bitmap disagrees with eb codes")
     if qd is None:
-        qd = huffman.decode(
-            a.q_d, np.uint16 if cfg.radius <= 32768 else np.uint32)
-        if qd.size and int(qd.max()) >= 2 * cfg.radius:
+        if cfg.radius <= 32768:
+            qd = huffman.decode_device(a.q_d, np.uint16)
+            # any symbol >= 2 radius (uint16 seen as int16: no uint16 max)
+            q16, lim = qd.view(torch.int16), 2 * cfg.radius
+            if lim >= 65536:
+                bad = False
+            elif lim <= 32768:
+                bad = bool(((q16 < 0) | (q16 >= lim)).any().item())
+            else:
+                bad = bool(((q16 < 0) & (q16 >= lim - 65536)).any().item())
+        else:
+            qd = huffman.decode(a.q_d, np.uint32)
+            bad = qd.size and int(qd.max()) >= 2 * cfg.radius
+        if bad:
             raise ValueError("corrupt entropy stream")
     if ll is None:
         ll = np.frombuffer(a.lossless_stream, dtype="<i8").astype(np.int64)

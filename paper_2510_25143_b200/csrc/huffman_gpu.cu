@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -131,6 +132,116 @@ huff_pack_kernel(const S* __restrict__ sym, int64_t n,
   if (nb > 0) atomicOr(out + wi, bswap32((uint32_t)(buf >> 32)));
 }
 
+// ------------------------------------------------------------- decode
+// huffman.py:79-98 (_unpack_bits) in parallel: the bitstream is cut into
+// chunks of HD_CB bits; a thread decodes its chunk from a start position
+// until the first codeword boundary at or past the chunk end (its exit).
+// The true start of chunk k+1 is the exit of chunk k decoded from its true
+// start; starting from the chunk boundaries and re-decoding every chunk
+// whose start moved converges quickly (Huffman codes resynchronise within a
+// few codewords), and reproduces the sequential decoder's codeword
+// boundaries exactly.  Then the per-chunk counts are scanned and every chunk
+// writes its symbols.
+constexpr int HD_CB = 4096;      // bits per chunk
+constexpr int HD_LB = 12;        // lookup-table bits
+
+struct HuffDecTables {
+  const uint32_t* lut;           // [1 << lb]: (symbol << 8) | length, 0: long
+  const uint32_t* symtab;        // symbols by (length, symbol)
+  int64_t first_code[64];
+  int64_t count_at[64];
+  int64_t offset_at[64];
+  int lb, max_len;
+};
+
+// 64 bits of the big-endian stream from bit p (words: bswapped 32-bit)
+__device__ __forceinline__ unsigned long long hd_window(const uint32_t* w,
+                                                        int64_t p) {
+  const int64_t wi = p >> 5;
+  const int o = (int)(p & 31);
+  const unsigned long long a = ((unsigned long long)bswap32(__ldg(w + wi)) << 32) |
+                               bswap32(__ldg(w + wi + 1));
+  if (o == 0) return a;
+  return (a << o) | (bswap32(__ldg(w + wi + 2)) >> (32 - o));
+}
+
+// one codeword at p: returns its length (0: invalid) and the symbol
+__device__ __forceinline__ int hd_step(const HuffDecTables& t, const uint32_t* lut,
+                                       const uint32_t* w, int64_t p,
+                                       uint32_t* sym) {
+  const unsigned long long win = hd_window(w, p);
+  const uint32_t e = lut[win >> (64 - t.lb)];
+  if (e) {
+    *sym = e >> 8;
+    return (int)(e & 255u);
+  }
+  for (int L = t.lb + 1; L <= t.max_len; L++) {
+    if (t.count_at[L] == 0) continue;
+    const int64_t d = (int64_t)(win >> (64 - L)) - t.first_code[L];
+    if (d >= 0 && d < t.count_at[L]) {
+      *sym = __ldg(t.symtab + t.offset_at[L] + d);
+      return L;
+    }
+  }
+  return 0;
+}
+
+// sync pass: chunks whose start moved are decoded to their exit
+__global__ void __launch_bounds__(256)
+huff_sync_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
+                 int64_t total_bits, int64_t nchunk,
+                 int64_t* __restrict__ start, int64_t* __restrict__ exitp,
+                 int32_t* __restrict__ count, int* __restrict__ dirty,
+                 int* __restrict__ changed, int* __restrict__ bad) {
+  __shared__ uint32_t lut[1 << HD_LB];
+  for (int k = threadIdx.x; k < (1 << t.lb); k += blockDim.x) lut[k] = t.lut[k];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nchunk) return;
+  if (!dirty[k]) return;
+  dirty[k] = 0;
+  const int64_t end = min((k + 1) * (int64_t)HD_CB, total_bits);
+  int64_t p = start[k];
+  int32_t c = 0;
+  while (p < end) {
+    uint32_t sym;
+    const int L = hd_step(t, lut, w, p, &sym);
+    if (L == 0) { atomicOr(bad, 1); break; }
+    p += L;
+    c++;
+  }
+  exitp[k] = p;
+  count[k] = c;
+  if (k + 1 < nchunk && start[k + 1] != p) {
+    start[k + 1] = p;
+    dirty[k + 1] = 1;
+    atomicOr(changed, 1);
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256)
+huff_write_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
+                  int64_t total_bits, int64_t nchunk,
+                  const int64_t* __restrict__ start,
+                  const long long* __restrict__ off, S* __restrict__ out) {
+  __shared__ uint32_t lut[1 << HD_LB];
+  for (int k = threadIdx.x; k < (1 << t.lb); k += blockDim.x) lut[k] = t.lut[k];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nchunk) return;
+  const int64_t end = min((k + 1) * (int64_t)HD_CB, total_bits);
+  int64_t p = start[k];
+  int64_t o = off[k];
+  while (p < end) {
+    uint32_t sym;
+    const int L = hd_step(t, lut, w, p, &sym);
+    if (L == 0) break;
+    p += L;
+    out[o++] = (S)sym;
+  }
+}
+
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -237,6 +348,134 @@ int vfcp_huff_pack_dev(const void* symbols, int sym_bytes, int64_t n,
   cudaFreeAsync(d_bits, st);
   cudaFreeAsync(d_off, st);
   cudaFreeAsync(d_tmp, st);
+  return VFCP_OK;
+}
+
+int vfcp_huff_unpack_dev(const uint32_t* words, int64_t n_words,
+                         int64_t total_bits, const uint8_t* lens_host,
+                         int32_t alphabet, int64_t n, void* out,
+                         int sym_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return VFCP_OK;
+  if (sym_bytes != 1 && sym_bytes != 2) return hfail(VFCP_EINVAL, "symbol width");
+  // the window reads two words past any bit position inside the stream
+  if (n_words < (total_bits + 31) / 32 + 2)
+    return hfail(VFCP_ECAPACITY, "vfcp_huff_unpack_dev: words need 2 words of padding");
+  int max_len = 0;
+  for (int s = 0; s < alphabet; s++) max_len = std::max<int>(max_len, lens_host[s]);
+  if (max_len == 0 || max_len > 60) return hfail(VFCP_ECORRUPT, "corrupt entropy stream");
+  std::vector<int32_t> order;
+  for (int s = 0; s < alphabet; s++)
+    if (lens_host[s]) order.push_back(s);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return lens_host[a] < lens_host[b]; });
+  HuffDecTables t;
+  memset(&t, 0, sizeof(t));
+  {
+    unsigned long long code = 0;
+    int64_t idx = 0;
+    for (int s : order) t.count_at[lens_host[s]]++;
+    for (int L = 1; L <= max_len; L++) {
+      code <<= 1;
+      t.first_code[L] = (int64_t)code;
+      t.offset_at[L] = idx;
+      code += (unsigned long long)t.count_at[L];
+      idx += t.count_at[L];
+    }
+  }
+  t.lb = std::min(max_len, HD_LB);
+  t.max_len = max_len;
+  std::vector<uint32_t> lut((size_t)1 << t.lb, 0), symtab(order.size());
+  for (size_t q = 0; q < order.size(); q++) symtab[q] = (uint32_t)order[q];
+  for (int L = 1; L <= t.lb; L++)
+    for (int64_t q = 0; q < t.count_at[L]; q++) {
+      const uint64_t c = (uint64_t)t.first_code[L] + (uint64_t)q;
+      const uint32_t sym = (uint32_t)order[t.offset_at[L] + q];
+      const uint64_t lo = c << (t.lb - L), hi = (c + 1) << (t.lb - L);
+      for (uint64_t x = lo; x < hi; x++) lut[x] = (sym << 8) | (uint32_t)L;
+    }
+  const int64_t nchunk = (total_bits + HD_CB - 1) / HD_CB;
+  if (nchunk == 0) return hfail(VFCP_ECORRUPT, "corrupt entropy stream");
+  uint32_t *d_lut = nullptr, *d_sym = nullptr;
+  int64_t *d_start = nullptr, *d_exit = nullptr;
+  int32_t* d_count = nullptr;
+  long long* d_off = nullptr;
+  int *d_dirty = nullptr, *d_flags = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  HCK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_count, d_off, (int)nchunk, st));
+  HCK(cudaMallocAsync(&d_lut, sizeof(uint32_t) * lut.size(), st));
+  HCK(cudaMallocAsync(&d_sym, sizeof(uint32_t) * std::max<size_t>(1, symtab.size()), st));
+  HCK(cudaMallocAsync(&d_start, sizeof(int64_t) * nchunk, st));
+  HCK(cudaMallocAsync(&d_exit, sizeof(int64_t) * nchunk, st));
+  HCK(cudaMallocAsync(&d_count, sizeof(int32_t) * nchunk, st));
+  HCK(cudaMallocAsync(&d_off, sizeof(long long) * (nchunk + 1), st));
+  HCK(cudaMallocAsync(&d_dirty, sizeof(int) * nchunk, st));
+  HCK(cudaMallocAsync(&d_flags, sizeof(int) * 2, st));
+  HCK(cudaMallocAsync(&d_tmp, tmp_bytes + 16, st));
+  HCK(cudaMemcpyAsync(d_lut, lut.data(), sizeof(uint32_t) * lut.size(),
+                      cudaMemcpyHostToDevice, st));
+  HCK(cudaMemcpyAsync(d_sym, symtab.data(), sizeof(uint32_t) * symtab.size(),
+                      cudaMemcpyHostToDevice, st));
+  {
+    std::vector<int64_t> s0(nchunk);
+    for (int64_t k = 0; k < nchunk; k++) s0[k] = k * (int64_t)HD_CB;
+    HCK(cudaMemcpyAsync(d_start, s0.data(), sizeof(int64_t) * nchunk,
+                        cudaMemcpyHostToDevice, st));
+    std::vector<int> d1(nchunk, 1);
+    HCK(cudaMemcpyAsync(d_dirty, d1.data(), sizeof(int) * nchunk,
+                        cudaMemcpyHostToDevice, st));
+  }
+  t.lut = d_lut;
+  t.symtab = d_sym;
+  HCK(cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, st));
+  const unsigned grid = (unsigned)((nchunk + 255) / 256);
+  int rc = VFCP_OK;
+  int h[2] = {0, 0};
+  for (int it = 0; it < 64; it++) {
+    HCK(cudaMemsetAsync(d_flags, 0, sizeof(int), st));   // changed
+    huff_sync_kernel<<<grid, 256, 0, st>>>(t, words, total_bits, nchunk, d_start,
+                                           d_exit, d_count, d_dirty, d_flags,
+                                           d_flags + 1);
+    HCK(cudaGetLastError());
+    HCK(cudaMemcpyAsync(h, d_flags, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+    HCK(cudaStreamSynchronize(st));
+    if (h[1] || !h[0]) break;
+  }
+  long long total = 0;
+  int64_t last_exit = -1;
+  if (!h[1] && !h[0]) {
+    HCK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_count, d_off, (int)nchunk, st));
+    int32_t lc = 0;
+    long long lo = 0;
+    HCK(cudaMemcpyAsync(&lo, d_off + nchunk - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    HCK(cudaMemcpyAsync(&lc, d_count + nchunk - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HCK(cudaMemcpyAsync(&last_exit, d_exit + nchunk - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HCK(cudaStreamSynchronize(st));
+    total = lo + lc;
+  }
+  if (h[1] || h[0] || total != n || last_exit != total_bits) {
+    // invalid code, no convergence or a length mismatch: the caller decodes
+    // on the host (the reference's exact error behaviour)
+    rc = hfail(VFCP_ECORRUPT, "corrupt entropy stream");
+  } else if (sym_bytes == 2) {
+    huff_write_kernel<uint16_t><<<grid, 256, 0, st>>>(t, words, total_bits, nchunk,
+                                                      d_start, d_off, (uint16_t*)out);
+  } else {
+    huff_write_kernel<uint8_t><<<grid, 256, 0, st>>>(t, words, total_bits, nchunk,
+                                                     d_start, d_off, (uint8_t*)out);
+  }
+  cudaFreeAsync(d_lut, st);
+  cudaFreeAsync(d_sym, st);
+  cudaFreeAsync(d_start, st);
+  cudaFreeAsync(d_exit, st);
+  cudaFreeAsync(d_count, st);
+  cudaFreeAsync(d_off, st);
+  cudaFreeAsync(d_dirty, st);
+  cudaFreeAsync(d_flags, st);
+  cudaFreeAsync(d_tmp, st);
+  if (rc) return rc;
+  HCK(cudaGetLastError());
   return VFCP_OK;
 }
 

@@ -121,6 +121,38 @@ def decode(blob, out_dtype=np.int64) -> np.ndarray:
     return out
 
 
+def decode_device(blob, out_dtype=np.uint16):
+    """decode() into a CUDA tensor (uint8 / uint16): the packed bits go to
+    the device and are decoded there (csrc/huffman_gpu.cu); a stream the
+    sequential decoder would reject is decoded on the host, which raises
+    the reference's error."""
+    import torch
+    blob = memoryview(blob)
+    alphabet, n_symbols, total_bits = _HDR.unpack_from(blob, 0)
+    off = _HDR.size
+    tdt = {np.uint8: torch.uint8, np.uint16: torch.uint16}[np.dtype(out_dtype).type]
+    if n_symbols == 0:
+        return torch.empty(0, dtype=tdt, device="cuda")
+    lens = np.ascontiguousarray(
+        np.frombuffer(blob, dtype=np.uint8, count=alphabet, offset=off))
+    off += alphabet
+    nbytes = (total_bits + 7) // 8
+    n_words = (total_bits + 31) // 32 + 2
+    hw = torch.zeros(n_words, dtype=torch.int32, pin_memory=True)
+    hw.numpy().view(np.uint8)[:nbytes] = np.frombuffer(blob, dtype=np.uint8,
+                                                       count=nbytes, offset=off)
+    words = hw.cuda(non_blocking=True)
+    out = torch.empty(n_symbols, dtype=tdt, device="cuda")
+    L = _lib.lib()
+    rc = L.vfcp_huff_unpack_dev(words.data_ptr(), n_words, total_bits,
+                                lens.ctypes.data, alphabet, n_symbols,
+                                out.data_ptr(), out.element_size(),
+                                _lib.stream_ptr())
+    if rc != 0:
+        return torch.from_numpy(decode(blob, out_dtype)).cuda()
+    return out
+
+
 class ctypes_i64:
     def __init__(self):
         import ctypes

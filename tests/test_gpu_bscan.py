@@ -102,3 +102,25 @@ def test_device_huffman_matches_host(name):
     assert huffman.encode_device(s.codes, 32) == huffman.encode(s.codes.cpu().numpy(), 32)
     assert (huffman.encode_device(s.qd, 2 * radius, max(0, radius - 4096))
             == huffman.encode(s.qd.cpu().numpy(), 2 * radius))
+
+
+@pytest.mark.parametrize("name", ["spectral_multicta_mop", "ints_radius16",
+                                  "tiny_tau_mop"])
+def test_device_huffman_decode(name):
+    """huffman.decode_device (chunk-parallel, resynchronised decode on the
+    GPU) returns the symbols of the host decoder."""
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import huffman
+    gen, eps, rel, pred, radius = CASES[name]
+    H, W, T, u, v = gen()
+    cfg = vg.Config(predictor=pred, radius=radius)
+    f = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v)
+    s = vg.compress_device(f, eps, cfg, relative=rel)
+    for sym, alpha, dt in ((s.codes, 32, np.uint8), (s.qd, 2 * radius, np.uint16)):
+        blob = huffman.encode(sym.cpu().numpy(), alpha)
+        np.testing.assert_array_equal(huffman.decode_device(blob, dt).cpu().numpy(),
+                                      huffman.decode(blob, dt))
+    # a truncated stream: the host decoder's error
+    blob = huffman.encode(s.qd.cpu().numpy(), 2 * radius)
+    with pytest.raises(ValueError):
+        huffman.decode_device(blob[:-3], np.uint16)
