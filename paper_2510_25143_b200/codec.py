@@ -540,9 +540,15 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
 
 
 def decompress_with_stats(a: Archive) -> tuple[FieldSeries, DecodeStats]:
+    import torch
     out_u, out_v, _, _ = decompress_device(a)
-    fs = FieldSeries(a.H, a.W, a.T, a.dx, a.dy, a.dt,
-                     out_u.cpu().numpy(), out_v.cpu().numpy())
+    # FieldSeries re-validates the output (codec.py:451): on the device, then
+    # the arrays come back through pinned memory
+    fs = FieldSeries(a.H, a.W, a.T, a.dx, a.dy, a.dt, out_u, out_v)
+    hu, hv = _to_host(out_u), _to_host(out_v)
+    torch.cuda.current_stream().synchronize()
+    object.__setattr__(fs, "u", hu.numpy())
+    object.__setattr__(fs, "v", hv.numpy())
     return fs, DecodeStats(aux_component_buffers=4)
 
 
@@ -552,6 +558,8 @@ def decompress(a: Archive) -> FieldSeries:
 
 def reconstruct_fixed(a: Archive) -> FixedField:
     """Reconstruction as integers at the archive's scale (codec.py:460-463)."""
+    import torch
     _, _, fu, fv = decompress_device(a, want_fixed=True)
-    return FixedField(a.H, a.W, a.T, fu.cpu().numpy(), fv.cpu().numpy(),
-                      a.scale)
+    hu, hv = _to_host(fu), _to_host(fv)
+    torch.cuda.current_stream().synchronize()
+    return FixedField(a.H, a.W, a.T, hu.numpy(), hv.numpy(), a.scale)

@@ -18,7 +18,10 @@ vp = torch.from_numpy(v).pin_memory()
 f = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, up, vp)
 for backend in ("identity", "zlib"):
     cfg = vg.Config(backend=backend)
-    vg.compress(f, 1e-3, cfg, relative=True)   # warm-up
+    # warm-up (JIT, pinned host buffers of torch's caching allocator)
+    w = vg.compress(f, 1e-3, cfg, relative=True)
+    r = vg.decompress(vg.Archive.from_bytes(w.to_bytes()))
+    del w, r
     t0 = time.perf_counter()
     a = vg.compress(f, 1e-3, cfg, relative=True)
     t1 = time.perf_counter()
@@ -34,3 +37,4 @@ for backend in ("identity", "zlib"):
           f"({len(blob) / 1e6:.1f} MB, CR {8.0 * H * W * T / len(blob):.1f}), "
           f"from_bytes {t3 - t2:.3f} s, decompress() {t4 - t3:.3f} s; "
           f"compress+to_bytes {gb / (t2 - t0):.2f} GB/s")
+    del a, b, r, blob
