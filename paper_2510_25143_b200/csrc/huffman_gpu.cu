@@ -142,7 +142,7 @@ huff_pack_kernel(const S* __restrict__ sym, int64_t n,
 // few codewords), and reproduces the sequential decoder's codeword
 // boundaries exactly.  Then the per-chunk counts are scanned and every chunk
 // writes its symbols.
-constexpr int HD_CB = 4096;      // bits per chunk
+constexpr int HD_CB = 1024;      // bits per chunk
 constexpr int HD_LB = 12;        // lookup-table bits
 
 struct HuffDecTables {

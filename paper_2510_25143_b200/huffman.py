@@ -94,9 +94,14 @@ def encode_device(symbols, alphabet_size: int, window_base: int = 0) -> bytes:
                    "huffman pack (device)")
     h = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
     h.copy_(words, non_blocking=True)
+    nbytes = (total_bits + 7) // 8
+    # the blob is assembled with one host copy of the packed bytes
+    head = _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes()
+    blob = bytearray(len(head) + nbytes)
+    blob[:len(head)] = head
     torch.cuda.current_stream().synchronize()
-    packed = h.numpy().view(np.uint8)[:(total_bits + 7) // 8]
-    return _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes() + packed.tobytes()
+    np.frombuffer(blob, dtype=np.uint8)[len(head):] = h.numpy().view(np.uint8)[:nbytes]
+    return blob
 
 
 def decode(blob, out_dtype=np.int64) -> np.ndarray:
@@ -138,9 +143,10 @@ def decode_device(blob, out_dtype=np.uint16):
     off += alphabet
     nbytes = (total_bits + 7) // 8
     n_words = (total_bits + 31) // 32 + 2
-    hw = torch.zeros(n_words, dtype=torch.int32, pin_memory=True)
-    hw.numpy().view(np.uint8)[:nbytes] = np.frombuffer(blob, dtype=np.uint8,
-                                                       count=nbytes, offset=off)
+    hw = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
+    hb = hw.numpy().view(np.uint8)
+    hb[:nbytes] = np.frombuffer(blob, dtype=np.uint8, count=nbytes, offset=off)
+    hb[nbytes:] = 0
     words = hw.cuda(non_blocking=True)
     out = torch.empty(n_symbols, dtype=tdt, device="cuda")
     L = _lib.lib()
