@@ -360,6 +360,29 @@ def main():
     zlib.compress(b1, 6)
     zlib.compress(b2, 6)
     ent_s = time.perf_counter() - t0
+    # the device entropy stage (csrc/huffman_gpu.cu) on the whole field's
+    # streams, resident from the timed compress: encode and decode of the
+    # q_xi and q_d sections (byte-identical to the host encoder)
+    s3 = vg.compress_device(f_dev, args.eps, cfg, relative=True)
+    for _ in range(2):   # warm-up (pinned host buffers of the sections)
+        huffman.decode_device(huffman.encode_device(s3.codes, 32), np.uint8)
+        huffman.decode_device(huffman.encode_device(
+            s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096)), np.uint16)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bx = huffman.encode_device(s3.codes, 32)
+    bq = huffman.encode_device(s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096))
+    torch.cuda.synchronize()
+    dent_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    huffman.decode_device(bx, np.uint8)
+    huffman.decode_device(bq, np.uint16)
+    torch.cuda.synchronize()
+    dent_dec = time.perf_counter() - t0
+    dent = {"sections_MB": round((len(bx) + len(bq)) / 1e6, 1),
+            "encode_s": round(dent_enc, 4), "decode_s": round(dent_dec, 4),
+            "encode_GBps_fp32_input": round(8.0 * N / dent_enc / 1e9, 2)}
+    del s3, bx, bq
 
     peak, peak_src = measured_peak()
     # dominant kernel roofline
@@ -400,6 +423,7 @@ def main():
         "e2e": {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
                 "unit": UNIT, "h2d_bytes_per_step": 8 * N,
                 "d2h_bytes_per_step": d2h},
+        "device_entropy": dent,
         "host_entropy": {"sample": "frame 0 codes + qd: Huffman + zlib(6)",
                          "seconds": round(ent_s, 3),
                          "MBps_fp32_input": round(8.0 * H * W / ent_s / 1e6, 2)},
