@@ -79,7 +79,7 @@ def face_mask_fixed(H, W, T, u_fp, v_fp):
     return face_mask_float(H, W, T, u.double(), v.double(), 1.0)
 
 
-def face_mask_float(H, W, T, du, dv, scale):
+def face_mask_float(H, W, T, du, dv, scale, host=True):
     import torch
     from .codec import Config, make_params
     from .field import dtype_code
@@ -93,6 +93,8 @@ def face_mask_float(H, W, T, du, dv, scale):
         ctypes.byref(p), du.data_ptr(), dv.data_ptr(), dtype_code(du),
         codes.data_ptr(), ld.data_ptr(), mask.data_ptr(), row.data_ptr(),
         _lib.stream_ptr()), "analyze")
+    if not host:
+        return mask
     return mask.cpu().numpy().view(np.uint16)
 
 

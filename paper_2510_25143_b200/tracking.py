@@ -1,0 +1,177 @@
+"""Critical-point trajectory verification (the reference's
+tracking.py:145-195 ``verify``), with the face predicates on the device.
+
+The positive faces of the original and of the reconstruction, both at the
+original's fixed-point scale, come from the analysis kernel's 12-bit
+per-anchor face mask (csrc/analyze.cu, the same exact / SoS predicate as
+compression); the flipped-face counts fc_t / fc_s are popcounts of the two
+masks' XOR, on the device.  The trajectory graph is linked on the host over
+the (sparse) crossed faces: every tet of the space-time mesh crossed by a
+trajectory has exactly two crossed faces and contributes the edge joining
+them (tracking.py:75-141), so components are simple paths or cycles.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from itertools import combinations
+
+import numpy as np
+
+from .field import FieldSeries, device_range, scale_for, to_device
+from .predicates import face_mask_float, mask_to_faces
+
+
+class TopologyError(AssertionError):
+    """A tet with 1 or >= 3 crossed faces: impossible under exact predicates."""
+
+
+@dataclass(frozen=True)
+class VerifyReport:
+    cr: float
+    psnr: float
+    max_abs_err: float
+    fc_t: int            # slice faces whose predicate flipped
+    fc_s: int            # slab faces whose predicate flipped
+    n_traj_orig: int
+    n_traj_recon: int
+    isomorphic: bool     # identical node AND edge sets
+
+    @property
+    def ok(self) -> bool:
+        return self.fc_t == 0 and self.fc_s == 0 and self.isomorphic
+
+    def lines(self):
+        yield f"fc_t={self.fc_t}"
+        yield f"fc_s={self.fc_s}"
+        yield f"n_traj_orig={self.n_traj_orig}"
+        yield f"n_traj_recon={self.n_traj_recon}"
+        yield f"isomorphic={str(self.isomorphic).lower()}"
+        yield f"cr={self.cr:.6g}"
+        yield f"psnr={self.psnr:.6g}"
+        yield f"max_abs_err={self.max_abs_err:.6g}"
+
+
+# ------------------------------------------------------------ mesh (tets)
+# The space-time mesh of mesh.py:27-56: cell (i, j) of frame t splits into
+# the triangles (v00, v01, v11) and (v00, v10, v11); the prism over slab
+# [t, t+1] of a triangle (a, b, c) (ascending ids) splits into the tets
+# (a, b, c, c'), (a, b, b', c'), (a, a', b', c') (primes: one frame up).
+
+def _tets_around(face, H, W, T):
+    """Tets of the mesh that contain `face` (found around its first vertex)."""
+    hw = H * W
+    a = face[0]
+    t, r = divmod(a, hw)
+    i, j = divmod(r, W)
+    fs = set(face)
+    for slab in (t - 1, t):
+        if not 0 <= slab < T - 1:
+            continue
+        for ci in range(max(0, i - 1), min(H - 1, i + 1)):
+            for cj in range(max(0, j - 1), min(W - 1, j + 1)):
+                v00 = slab * hw + ci * W + cj
+                for tri in ((v00, v00 + W, v00 + W + 1),
+                            (v00, v00 + 1, v00 + W + 1)):
+                    p, q, s = tri
+                    for tet in ((p, q, s, s + hw), (p, q, q + hw, s + hw),
+                                (p, p + hw, q + hw, s + hw)):
+                        if fs <= set(tet):
+                            yield tet
+
+
+def trajectory_graph(faces, H, W, T):
+    """(edges, n_components) of the crossed-face graph (tracking.py:75-141)."""
+    positives = set(faces)
+    edges = set()
+    seen = set()
+    for f in positives:
+        for tet in _tets_around(f, H, W, T):
+            if tet in seen:
+                continue
+            seen.add(tet)
+            crossed = [g for g in (tuple(sorted(c)) for c in combinations(tet, 3))
+                       if g in positives]
+            if len(crossed) != 2:
+                raise TopologyError(
+                    f"tet {tet} has {len(crossed)} crossed faces (expected 2)")
+            edges.add(tuple(sorted(crossed)))
+    degree = {f: 0 for f in positives}
+    parent = {f: f for f in positives}
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for f, g in edges:
+        degree[f] += 1
+        degree[g] += 1
+        rf, rg = find(f), find(g)
+        if rf != rg:
+            parent[rg] = rf
+    for f, d in degree.items():
+        if d > 2:
+            raise TopologyError(f"face {f} has degree {d}")
+    n_comp = len({find(f) for f in positives})
+    return frozenset(edges), n_comp
+
+
+# ------------------------------------------------------------------ verify
+
+def _popcount12(x):
+    """Per-element popcount of the low 12 bits, summed (torch, on device)."""
+    return int(sum(int(((x >> b) & 1).sum().item()) for b in range(12)))
+
+
+def _positive_faces(mask, H, W, T):
+    import torch
+    nz = torch.nonzero(mask).flatten()
+    anchors = nz.cpu().numpy()
+    bits = mask[nz].cpu().numpy().view(np.uint16)
+    sparse = np.zeros(H * W * T, np.uint16)
+    sparse[anchors] = bits
+    sl, sb = mask_to_faces(sparse, H, W, T)
+    return sl | sb
+
+
+def verify(orig: FieldSeries, recon: FieldSeries,
+           archive_size: int | None = None,
+           scale: float | None = None) -> VerifyReport:
+    """Compare predicates and trajectory graphs at a common fixed-point scale
+    (tracking.py:170-195); `scale` defaults to the original's automatic
+    scale (the one compression used)."""
+    import torch
+    if (orig.H, orig.W, orig.T) != (recon.H, recon.W, recon.T):
+        raise ValueError("dimension mismatch between original and reconstruction")
+    H, W, T = orig.H, orig.W, orig.T
+    ou, ov = to_device(orig.u), to_device(orig.v)
+    ru, rv = to_device(recon.u), to_device(recon.v)
+    if scale is None:
+        _, _, ma = device_range(ou, ov)
+        scale = scale_for(ma)
+    m_o = face_mask_float(H, W, T, ou, ov, scale, host=False)
+    m_r = face_mask_float(H, W, T, ru, rv, scale, host=False)
+    x = (m_o.to(torch.int32) ^ m_r.to(torch.int32)) & 0xFFF
+    fc_t = _popcount12(x & 0x3)
+    fc_s = _popcount12(x & 0xFFC)
+    f_o = _positive_faces(m_o, H, W, T)
+    f_r = _positive_faces(m_r, H, W, T)
+    e_o, n_o = trajectory_graph(f_o, H, W, T)
+    e_r, n_r = trajectory_graph(f_r, H, W, T)
+    iso = f_o == f_r and e_o == e_r
+    # field.py:346-372 psnr on the device (float64; the mean's summation
+    # order differs from numpy's, so the last bits may)
+    lo, hi, _ = device_range(ou, ov)
+    rng = hi - lo
+    du, dv = ou.double() - ru.double(), ov.double() - rv.double()
+    mse = 0.5 * (float((du * du).mean().item()) + float((dv * dv).mean().item()))
+    p = math.inf if mse == 0.0 else (-math.inf if rng == 0.0 else
+                                     20.0 * math.log10(rng) - 10.0 * math.log10(mse))
+    max_err = max(float(du.abs().max().item()), float(dv.abs().max().item()))
+    cr = orig.nbytes / archive_size if archive_size else float("nan")
+    return VerifyReport(cr=cr, psnr=p, max_abs_err=max_err,
+                        fc_t=fc_t, fc_s=fc_s, n_traj_orig=n_o,
+                        n_traj_recon=n_r, isomorphic=iso)
