@@ -741,7 +741,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
 }
 
 template <typename F>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
 enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
                const uint8_t* __restrict__ codes_p,
                const int2* __restrict__ prevrec,
@@ -874,7 +874,7 @@ enc_pix_kernel(const F* __restrict__ u, const F* __restrict__ v,
 // so only pinned pixels read p; the interior pass adds p back.  The four
 // rows of a warp are processed together so their stream loads overlap.
 template <typename SYM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
                 const int64_t* __restrict__ ll,
                 const uint8_t* __restrict__ modes_t,
