@@ -261,8 +261,8 @@ __device__ __forceinline__ bool sl_predict_rk2(const Src& s, int H, int W,
 // occurrence) adds the group's count, and a value's first touch appends it
 // to an ordered list; values >= ETB take the generic path.
 constexpr int ETB = 512;
-__device__ double block_rate(const int32_t* samp, int ns, int32_t* cnt,
-                             int32_t* order, const double* log2tab,
+__device__ double block_rate(const int16_t* samp, int ns, int16_t* cnt,
+                             int16_t* order, const double* log2tab,
                              double lam, double rmeta, int lane) {
   const unsigned FULL = 0xffffffffu;
   const unsigned below = (1u << lane) - 1u;
@@ -285,8 +285,8 @@ __device__ double block_rate(const int32_t* samp, int ns, int32_t* cnt,
         if (samp[q] == a) { fresh = false; break; }
     }
     const unsigned fm = __ballot_sync(FULL, fresh);
-    if (leader) cnt[key] = prev + __popc(grp);
-    if (fresh) order[nd + __popc(fm & below)] = small ? key : -(sp + 1);
+    if (leader) cnt[key] = (int16_t)(prev + __popc(grp));
+    if (fresh) order[nd + __popc(fm & below)] = (int16_t)(small ? key : -(sp + 1));
     nd += __popc(fm);
   }
   for (int o = 16; o; o >>= 1) {
@@ -506,9 +506,10 @@ __device__ __forceinline__ int32_t trial_step(int32_t rho, int32_t q0,
 struct MopSmem {
   int32_t r0[2][32][33];   // [comp][row][col] R0 tile, then rho
   int32_t q0[2][32][33];   // [comp][row][col] Q0 = rha(R0 / 2 tau')
-  int32_t samp[2][512];    // [trial] |idx| per sample (-1: escape)
-  int32_t order[2][ETB];  // distinct |idx| in first-touch order
-  int32_t cnt[2][ETB];
+  // int16: |idx| < radius <= 2^15, counts and positions <= 512
+  int16_t samp[2][512];    // [trial] |idx| per sample (-1: escape)
+  int16_t order[2][ETB];   // distinct |idx| in first-touch order
+  int16_t cnt[2][ETB];
   double rate[2];
 };
 
@@ -640,14 +641,14 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
         const int sj = lane & 15, j = 2 * sj, rp = lane >> 4;
 #pragma unroll 2
         for (int r = 2 * rp; r < nr; r += 4)
-          if (j < ncl) sm.samp[0][2 * ((r >> 1) * nsx + sj) + comp] = sample(r, j);
+          if (j < ncl) sm.samp[0][2 * ((r >> 1) * nsx + sj) + comp] = (int16_t)sample(r, j);
       } else {
         const bool scol = lane < ncl && (lane % p.stride) == 0;
         const int sj = lane / p.stride;
         int srow = 0;
 #pragma unroll 1
         for (int r = 0; r < nr; r += p.stride, srow += nsx)
-          if (scol) sm.samp[0][2 * (srow + sj) + comp] = sample(r, lane);
+          if (scol) sm.samp[0][2 * (srow + sj) + comp] = (int16_t)sample(r, lane);
       }
     }
   }
@@ -689,7 +690,7 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const int32_t er = trial_step(rho, q0, e, d, radius, &qa);
       eUL = eU;
       if (act) eL = er;
-      if (act && srow && jm == 0) sm.samp[0][sbase + 2 * jq] = qa;
+      if (act && srow && jm == 0) sm.samp[0][sbase + 2 * jq] = (int16_t)qa;
       if (jj >= 0) {
         if (++jm == p.stride) { jm = 0; jq++; }
       }
@@ -721,8 +722,8 @@ enc_mop_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const int64_t ru = (int64_t)fixed_t(sou[b], p.S) - pr_u[b];
       const int64_t rv = (int64_t)fixed_t(sov[b], p.S) - pr_v[b];
       const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
-      sm.samp[1][2 * sidx] = (qu > -radius && qu < radius) ? (int32_t)(qu < 0 ? -qu : qu) : -1;
-      sm.samp[1][2 * sidx + 1] = (qv > -radius && qv < radius) ? (int32_t)(qv < 0 ? -qv : qv) : -1;
+      sm.samp[1][2 * sidx] = (int16_t)((qu > -radius && qu < radius) ? (qu < 0 ? -qu : qu) : -1);
+      sm.samp[1][2 * sidx + 1] = (int16_t)((qv > -radius && qv < radius) ? (qv < 0 ? -qv : qv) : -1);
     }
   }
   __syncthreads();
