@@ -411,6 +411,9 @@ PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {
   pp.mop = p->predictor == VFCP_PRED_MOP && t >= 1 && p->tau > 0;
   pp.force_sl = p->predictor == VFCP_PRED_SL && t >= 1 && p->tau > 0;
   pp.lad = lad;
+  pp.lossy_mask = 0;
+  for (int k = 0; k < 32; k++)
+    if (lad.e[k] > 0) pp.lossy_mask |= 1u << k;
   return pp;
 }
 

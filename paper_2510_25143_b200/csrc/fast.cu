@@ -433,7 +433,7 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
     a1[pr] = colok ? (int32_t)R_v : 0;
     // phase A of the block scan (bscan.cuh)
     if (colok) {
-      lossy |= p.lad.e[cd & 31] != 0;
+      lossy |= (p.lossy_mask >> (cd & 31)) & 1u;
       bad_u |= cd != code0 || (R_u < 0 ? -R_u : R_u) >= lim;
       bad_v |= cd != code0 || (R_v < 0 ? -R_v : R_v) >= lim;
     }

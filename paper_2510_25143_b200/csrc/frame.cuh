@@ -14,6 +14,7 @@ struct PrepParams {
   int64_t tau;
   int mop;          // run the MoP trial for this frame
   int force_sl;     // predictor 'sl' (and t >= 1, tau > 0)
+  uint32_t lossy_mask;   // bit c: code c quantises (e > 0)
   Ladder lad;
 };
 
