@@ -73,7 +73,7 @@ EXPORTED = tuple(_SIGS)
 
 # launch classes of vfcp_prof_collect (capi.cu KClass): "prep" is
 # enc_r0_kernel, "pix" enc_pix_kernel, "decode_rows" dec_prep_kernel (and
-# decode_rows_kernel), "aux" emit_frame_kernel
+# decode_rows_kernel), "bs_chain" the block-scan kernel (chain + interior)
 KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
                   "decode_rows", "decode_ll", "decode", "aux", "prep",
                   "bs_local", "bs_chain", "bs_final", "pix")

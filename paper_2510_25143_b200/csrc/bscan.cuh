@@ -1,14 +1,15 @@
 // The raster-order Lorenzo recurrence of one frame as a 2D block scan.
 //
-// Same contract as chain_kernel (chain.cuh, ChainIO): the prepared planes
-// a (encoder: R0 or the pinned err; decoder: A or the pinned recon), the
-// per-(row, chunk) pin words and (encoder) the frame codes in; the err /
-// recon plane and (encoder) the symbol planes out, bit for bit what the
-// reference's raster loop (codec.py:118-164 _encode_frame, 167-206
-// _decode_frame) produces.
+// In: the prepared planes a (encoder: R0 = orig - Lorenzo(orig, prev), or
+// the pinned err; decoder, run on Z = recon - prev: (sym - radius) * 2e, or
+// the pinned Z), the per-(row, chunk) pin words and (encoder) the frame
+// codes.  Out: the err / recon plane, (encoder) the Lorenzo symbols written
+// into the interleaved symbol stream, (decoder) the float64 output -- bit for
+// bit what the reference's raster loop (codec.py:118-164 _encode_frame,
+// 167-206 _decode_frame) produces.
 //
 // Why a scan is exact.  Per component, with v the chain value (encoder: err
-// = recon - orig; decoder: recon) and zero padding outside the frame,
+// = recon - orig; decoder: Z) and zero padding outside the frame,
 //   decoder:  v = vU + vL - vUL + A                 (exact)
 //   encoder:  v = q*2e - x,  x = R0 - (vU + vL - vUL),  q = rha(x / 2e)
 // so in the encoder v == -R0 + vU + vL - vUL (mod 2e) whenever the pixel is
@@ -25,21 +26,21 @@
 // other block (mixed pins, mixed steps, possible escapes, a tie on its
 // boundary) is swept exactly, pixel by pixel, given its exact boundary.
 //
-// Three kernels per frame:
-//   bs_local_kernel   fully parallel: block class and the bottom row / right
-//                     column of the block-local prefix sums (LB, LR);
-//   bs_chain_kernel   the only sequential part: block boundaries travel
-//                     down the block rows (one warp per block row and
-//                     component walks its row; 32 exact values per block
-//                     are handed to the warp below) -- the critical path is
-//                     ~nby + nbx cheap block steps instead of H + W pixel
-//                     steps of a per-pixel wavefront;
-//   phase C           fully parallel: the interior of every block from its
-//                     exact boundary (prefix sums in shared memory, ties
-//                     resolved in raster order, symbols) -- tasks of the
-//                     same persistent kernel, handed out after the chain
-//                     tasks and started per 32-block segment as soon as the
-//                     chain has published it, so they overlap the chain.
+// Three phases per frame:
+//   phase A  fully parallel, in the prepare kernels (enc_r0_kernel and
+//            enc_pix_kernel; bs_local_kernel for the decoder): block class
+//            and the bottom row / right column of the block-local prefix
+//            sums (LB, LR), or the known edge values;
+//   phase B  chain tasks of bs_chain_kernel, the only sequential part: block
+//            boundaries travel down the block rows (one warp per block row
+//            and component walks its row; 32 exact values per block are
+//            handed to the warp below) -- the critical path is ~nby + nbx
+//            cheap block steps instead of H + W pixel steps;
+//   phase C  interior tasks of the same persistent kernel, handed out after
+//            the chain tasks and started per 32-block segment once the chain
+//            has published it, so they overlap the chain: the interior of
+//            every block from its exact boundary (prefix sums in shared
+//            memory, ties resolved in raster order, symbols).
 #pragma once
 
 #include "frame.cuh"

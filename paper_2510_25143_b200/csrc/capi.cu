@@ -380,7 +380,7 @@ int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
 }
 
 // ------------------------------------------------------------ fast paths
-// Frame-parallel prepare + chain wavefront (fast.cu, chain.cuh).  Valid for
+// Frame-parallel prepare kernels + block scan (fast.cu, bscan.cuh).  Valid for
 // the default 32x32 block grid, 16-bit symbols and tau' < 2^28 (every error
 // term then fits int32); the caller falls back to the generic kernels
 // otherwise.

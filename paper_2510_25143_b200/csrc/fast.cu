@@ -483,7 +483,7 @@ enc_r0_kernel(const F* __restrict__ u, const F* __restrict__ v,
 
 // MoP trial step with one step size e for the whole block (mop.py:88-110):
 // the neighbours' trial errors lie in [-e, e], so y = rho - d is within
-// [-4e, 4e] and q = q0 + g follows from comparisons (see chain.cuh)
+// [-4e, 4e] and q = q0 + g follows from comparisons of y with +-e, +-3e
 __device__ __forceinline__ int32_t trial_step(int32_t rho, int32_t q0,
                                               int32_t e, int32_t d,
                                               int32_t radius, int32_t* qabs) {

@@ -13,9 +13,8 @@ from pathlib import Path
 CLASSES = {  # kernel name prefix -> bench launch class
     "vfcp::enc_r0_kernel": "prep", "vfcp::enc_pix_kernel": "pix",
     "vfcp::enc_mop_kernel": "mop", "vfcp::bs_chain_kernel<1>": "bs_chain",
-    "vfcp::bs_final_kernel<1>": "bs_final", "vfcp::analyze_kernel": "analyze",
+    "vfcp::analyze_kernel": "analyze",
     "vfcp::range_kernel": "range", "vfcp::dec_prep_kernel": "decode_rows",
-    "vfcp::emit_frame_kernel": "aux",
 }
 UNIT = {"bytes": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
 
