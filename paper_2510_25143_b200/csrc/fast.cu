@@ -924,8 +924,14 @@ dec_prep_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
     syu[q] = 0; syv[q] = 0;
     if (nl) {
       const int64_t k = qrow[q] + 2 * ((int64_t)pnl[q] + __popc(bnl[q] & lt));
-      syu[q] = qd[k];
-      syv[q] = qd[k + 1];
+      if (sizeof(SYM) == 2) {   // the (u, v) pair as one 4-byte load (k even)
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qd + k));
+        syu[q] = w & 0xffffu;
+        syv[q] = w >> 16;
+      } else {
+        syu[q] = qd[k];
+        syv[q] = qd[k + 1];
+      }
     }
   }
 #pragma unroll
