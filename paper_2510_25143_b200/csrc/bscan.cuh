@@ -378,14 +378,16 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
     __syncthreads();
     const int task = sm.task;
     if (task >= ntask) {
-      // ---- interior tasks: (block row, segment of BS_SEG blocks, comp),
-      // in block-row order, each once the chain has finished the segment
-      // in its row and in the row above
+      // ---- interior tasks: (segment of BS_SEG blocks, block row, comp) in
+      // the order the chain finishes them (segment-major: segment s of row
+      // bi is done at ~ bi * lag + (s + 1) * BS_SEG * step), each started
+      // once the chain has finished the segment in its row and in the row
+      // above
       const int nseg = (nbx + BS_SEG - 1) / BS_SEG;
       const int ft = task - ntask;
       if (ft >= 2 * nby * nseg) break;
       const int comp = ft & 1, rs = ft >> 1;
-      const int bi = rs / nseg, sg = rs - bi * nseg;
+      const int sg = rs / nby, bi = rs - sg * nby;
       const int b0 = sg * BS_SEG, b1 = min(nbx, b0 + BS_SEG);
       if (threadIdx.x == 0) {
         const unsigned long long need = ((unsigned long long)io.frame_tag << 32) | (unsigned)b1;
