@@ -15,6 +15,8 @@
 // atomicMax.  A vertex class byte (|u|,|v| >= tau'+1 with a sign, and strict
 // signs) lets whole space-time cubes skip the exact integer work:
 // such faces can neither be positive nor lower xi below tau'.
+#include <cub/cub.cuh>
+
 #include "predicates.cuh"
 
 namespace vfcp {
@@ -323,30 +325,41 @@ analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
 // ------------------------------------------------- row offsets (exclusive)
 // out[r] = base + sum_{q < r} mul * (W - cnt[q])   (qd symbol offsets), or
 // out[r] = sum_{q < r} cnt[q] when W == 0 (plain exclusive scan).
-__global__ void __launch_bounds__(1024)
+// CTA b scans rows [1024 b, 1024 b + 1024): its carry-in is a coalesced
+// block reduction over all earlier rows (at most T*H 4-byte loads per CTA,
+// L2-resident), so the CTAs need no inter-CTA handoff.
+constexpr int RS_T = 1024;
+__device__ __forceinline__ int64_t row_term(const int32_t* cnt, int64_t r,
+                                            int W, int mul) {
+  return W ? (int64_t)mul * (W - __ldg(cnt + r)) : (int64_t)__ldg(cnt + r);
+}
+__global__ void __launch_bounds__(RS_T)
 row_scan_kernel(const int32_t* __restrict__ cnt, int64_t nrows, int W,
                 int mul, int64_t* __restrict__ out) {
-  __shared__ int64_t part[1024];
+  typedef cub::BlockReduce<int64_t, RS_T> BR;
+  typedef cub::BlockScan<int64_t, RS_T> BS;
+  __shared__ union {
+    typename BR::TempStorage r;
+    typename BS::TempStorage s;
+  } tmp;
+  __shared__ int64_t carry;
   const int tid = threadIdx.x;
-  int64_t per = (nrows + 1023) / 1024;
-  int64_t a = tid * per, b = min(nrows, a + per);
-  int64_t s = 0;
-  for (int64_t r = a; r < b; r++)
-    s += W ? (int64_t)mul * (W - cnt[r]) : (int64_t)cnt[r];
-  part[tid] = s;
+  const int64_t r0 = (int64_t)blockIdx.x * RS_T;
+  int64_t acc = 0;
+  int64_t r = tid;
+  for (; r + 3 * RS_T < r0; r += 4 * RS_T)
+    acc += row_term(cnt, r, W, mul) + row_term(cnt, r + RS_T, W, mul) +
+           row_term(cnt, r + 2 * RS_T, W, mul) + row_term(cnt, r + 3 * RS_T, W, mul);
+  for (; r < r0; r += RS_T) acc += row_term(cnt, r, W, mul);
+  const int64_t pre = BR(tmp.r).Sum(acc);
+  if (tid == 0) carry = pre;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    int64_t x = tid >= o ? part[tid - o] : 0;
-    __syncthreads();
-    part[tid] += x;
-    __syncthreads();
-  }
-  int64_t run = tid ? part[tid - 1] : 0;
-  for (int64_t r = a; r < b; r++) {
-    out[r] = run;
-    run += W ? (int64_t)mul * (W - cnt[r]) : (int64_t)cnt[r];
-  }
-  if (tid == 1023) out[nrows] = part[1023];
+  const int64_t me = r0 + tid;
+  const int64_t x = me < nrows ? row_term(cnt, me, W, mul) : 0;
+  int64_t excl, tot;
+  BS(tmp.s).ExclusiveSum(x, excl, tot);
+  if (me < nrows) out[me] = carry + excl;
+  if (r0 + RS_T >= nrows && tid == 0) out[nrows] = carry + tot;
 }
 
 // ------------------------------------------------------------ launchers
@@ -375,7 +388,8 @@ cudaError_t launch_analyze(const F* u, const F* v, int H, int W, int T,
 
 cudaError_t launch_row_scan(const int32_t* cnt, int64_t nrows, int W, int mul,
                             int64_t* out, cudaStream_t st) {
-  row_scan_kernel<<<1, 1024, 0, st>>>(cnt, nrows, W, mul, out);
+  const unsigned nb = (unsigned)((nrows + RS_T - 1) / RS_T);
+  row_scan_kernel<<<nb ? nb : 1, RS_T, 0, st>>>(cnt, nrows, W, mul, out);
   return cudaGetLastError();
 }
 

@@ -84,38 +84,63 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
         const int excl = incl - nl;                 // group-relative start
         const int S = __shfl_sync(FULL, incl, 31);  // group's symbol pairs
         const int64_t qs = q0 + 2 * (int64_t)nl_run;
-        for (int k0 = 0; k0 < S; k0 += 128) {
-          int zc[4];
+        // per-chunk escape counts: lane idx (the chunk holding pair k,
+        // binary search over the chunks' starts) receives zc from the
+        // lanes whose pairs fall in its chunk
+        auto attribute = [&](int zc, int k) {
+          if (!__any_sync(FULL, zc != 0)) return;   // warp-uniform
+          int idx = 0;
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int k = k0 + 32 * u + lane;
-            zc[u] = 0;
-            if (k < S) {
-              if (sizeof(SYM) == 2) {
-                const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qd + qs) + k);
-                zc[u] = ((w & 0xffffu) == 0u) + ((w >> 16) == 0u);
-              } else {
-                zc[u] = (__ldg(qd + qs + 2 * k) == 0) + (__ldg(qd + qs + 2 * k + 1) == 0);
+          for (int st = 16; st; st >>= 1) {
+            const int b = __shfl_sync(FULL, excl, idx + st);
+            if (b <= k) idx += st;
+          }
+          for (int src = 0; src < 32; src++) {
+            const int zs = __shfl_sync(FULL, zc, src);
+            const int is = __shfl_sync(FULL, idx, src);
+            if (zs && lane == is) esc += zs;
+          }
+        };
+        if constexpr (sizeof(SYM) == 2) {
+          // 16-byte loads over the group's pairs: the aligned quads that
+          // hold them (a quad with one pair of the range is mapped memory)
+          const uintptr_t bp = (uintptr_t)(qd + qs);
+          const uint4* qa = reinterpret_cast<const uint4*>(bp & ~(uintptr_t)15);
+          const int off = (int)((bp & 15) >> 2);   // pairs before the range
+          const int nq = (S + off + 3) >> 2;
+          constexpr int QU = 5;
+          for (int g0 = 0; g0 < nq; g0 += 32 * QU) {
+            uint4 w[QU];
+#pragma unroll
+            for (int u = 0; u < QU; u++) {
+              const int g = g0 + 32 * u + lane;
+              w[u] = g < nq ? __ldg(qa + g) : make_uint4(1u, 1u, 1u, 1u);
+            }
+#pragma unroll
+            for (int u = 0; u < QU; u++) {
+              const int kb = 4 * (g0 + 32 * u + lane) - off;
+              const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const int k = kb + q;
+                const int zc = (k >= 0 && k < S)
+                                   ? ((ww[q] & 0xffffu) == 0u) + ((ww[q] >> 16) == 0u)
+                                   : 0;
+                attribute(zc, k);
               }
             }
           }
+        } else {
+          for (int k0 = 0; k0 < S; k0 += 128) {
+            int zc[4];
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            if (!__any_sync(FULL, zc[u] != 0)) continue;   // warp-uniform
-            const int k = k0 + 32 * u + lane;
-            int idx = 0;
+            for (int u = 0; u < 4; u++) {
+              const int k = k0 + 32 * u + lane;
+              zc[u] = k < S ? (__ldg(qd + qs + 2 * k) == 0) + (__ldg(qd + qs + 2 * k + 1) == 0)
+                            : 0;
+            }
 #pragma unroll
-            for (int st = 16; st; st >>= 1) {
-              const int b = __shfl_sync(FULL, excl, idx + st);
-              if (b <= k) idx += st;
-            }
-            // per-chunk escape counts: lane idx receives zc from the lanes
-            // whose words fall in its chunk
-            for (int src = 0; src < 32; src++) {
-              const int zs = __shfl_sync(FULL, zc[u], src);
-              const int is = __shfl_sync(FULL, idx, src);
-              if (zs && lane == is) esc += zs;
-            }
+            for (int u = 0; u < 4; u++) attribute(zc[u], k0 + 32 * u + lane);
           }
         }
       }
