@@ -39,10 +39,14 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= nrows) return;
-  // bit c: code c quantises (e = tau >> c > 0); 31 is lossless
+  // bit c: code c quantises (e = tau >> c > 0); 31 is lossless.  The
+  // lossy codes are c < cmax = min(31, bit length of tau): counted four
+  // bytes at a time with a SIMD compare
   uint32_t lossy = 0;
+  int cmax = 0;
   for (int c = 0; c < CODE_LOSSLESS; c++)
-    if (tau > 0 && (tau >> c) != 0) lossy |= 1u << c;
+    if (tau > 0 && (tau >> c) != 0) { lossy |= 1u << c; cmax = c + 1; }
+  const uint32_t cm4 = 0x01010101u * (uint32_t)cmax;
   const uint8_t* cr = codes + row * (int64_t)W;
   const bool vec = ((row * (int64_t)W) & 15) == 0 &&
                    ((uintptr_t)codes & 15) == 0;
@@ -59,9 +63,8 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
         const uint4 b = __ldg(reinterpret_cast<const uint4*>(cr + jb + 16));
         const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int k = 0; k < 8; k++)
-#pragma unroll
-          for (int y = 0; y < 4; y++) nl += (lossy >> ((wv[k] >> (8 * y)) & 31)) & 1;
+        for (int k = 0; k < 8; k++) nl += __popc(__vcmpltu4(wv[k], cm4));
+        nl >>= 3;
       } else {
         for (int k = 0; k < ncl; k++) nl += (lossy >> (cr[jb + k] & 31)) & 1;
       }
@@ -116,6 +119,15 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
               const int g = g0 + 32 * u + lane;
               w[u] = g < nq ? __ldg(qa + g) : make_uint4(1u, 1u, 1u, 1u);
             }
+            // escapes are rare: one vote for the whole batch (a zero
+            // half-word outside the range only sends it down the exact
+            // per-pair path, which masks by k)
+            uint32_t z = 0;
+#pragma unroll
+            for (int u = 0; u < QU; u++)
+              z |= __vcmpeq2(w[u].x, 0u) | __vcmpeq2(w[u].y, 0u) |
+                   __vcmpeq2(w[u].z, 0u) | __vcmpeq2(w[u].w, 0u);
+            if (!__any_sync(FULL, z != 0u)) continue;   // warp-uniform
 #pragma unroll
             for (int u = 0; u < QU; u++) {
               const int kb = 4 * (g0 + 32 * u + lane) - off;
