@@ -25,93 +25,105 @@ namespace vfcp {
 // Per frame row: for each 32-column chunk, the number of non-lossless
 // pixels (and, for the decoder, ll entries: 2 per lossless pixel plus the
 // escapes, symbol 0, among the chunk's symbols) before it in the row.
-// One warp per row, lane = chunk (32 chunks per step): every load of a step
-// is independent (a chunk's symbol range follows from the scan of the
-// non-lossless counts, not from the previous chunk's loads).
+// One warp per row, lane = chunk; the row is taken in segments of 256
+// chunks.  Within a segment every load is independent of the counts: the
+// codes of all 256 chunks are read first, and the segment's symbol range
+// (which follows from the row offset and the running count) is then
+// streamed in 16-byte quads; a quad batch holding an escape attributes it
+// to its chunk by a binary search over the chunk starts kept in shared
+// memory (escapes are rare).
+constexpr int CP_SEG = 256;
 template <typename SYM>
-__global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
-                                    const SYM* __restrict__ qd,
-                                    const int64_t* __restrict__ qd_row_off,
-                                    int64_t nrows, int W, int nchunks,
-                                    int64_t tau, int32_t* __restrict__ pre_nl,
-                                    int32_t* __restrict__ pre_ll) {
+__global__ void __launch_bounds__(256)
+chunk_prefix_kernel(const uint8_t* __restrict__ codes,
+                    const SYM* __restrict__ qd,
+                    const int64_t* __restrict__ qd_row_off, int64_t nrows,
+                    int W, int nchunks, int64_t tau,
+                    int32_t* __restrict__ pre_nl, int32_t* __restrict__ pre_ll) {
+  __shared__ int32_t s_start[8][CP_SEG + 1];   // segment-relative pair starts
+  __shared__ int32_t s_esc[8][CP_SEG];
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   if (row >= nrows) return;
-  // bit c: code c quantises (e = tau >> c > 0); 31 is lossless.  The
-  // lossy codes are c < cmax = min(31, bit length of tau): counted four
-  // bytes at a time with a SIMD compare
-  uint32_t lossy = 0;
+  // code c quantises iff e = tau >> c > 0 (31 is lossless): the lossy codes
+  // are c < cmax = min(31, bit length of tau), counted four bytes at a time
   int cmax = 0;
   for (int c = 0; c < CODE_LOSSLESS; c++)
-    if (tau > 0 && (tau >> c) != 0) { lossy |= 1u << c; cmax = c + 1; }
+    if (tau > 0 && (tau >> c) != 0) cmax = c + 1;
   const uint32_t cm4 = 0x01010101u * (uint32_t)cmax;
   const uint8_t* cr = codes + row * (int64_t)W;
   const bool vec = ((row * (int64_t)W) & 15) == 0 &&
                    ((uintptr_t)codes & 15) == 0;
   const int64_t q0 = qd ? qd_row_off[row] : 0;
+  int32_t* st = s_start[wid];
+  int32_t* es = s_esc[wid];
   int32_t nl_run = 0, ll_run = 0;
-  for (int x0 = 0; x0 < nchunks; x0 += 32) {
-    const int x = x0 + lane;
-    int nl = 0, ncl = 0;
-    if (x < nchunks) {
-      const int jb = 32 * x;
-      ncl = min(32, W - jb);
-      if (vec && ncl == 32) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(cr + jb));
-        const uint4 b = __ldg(reinterpret_cast<const uint4*>(cr + jb + 16));
-        const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  for (int s0 = 0; s0 < nchunks; s0 += CP_SEG) {
+    const int nseg = min(CP_SEG, nchunks - s0);
+    int nl[8], ncl[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) nl += __popc(__vcmpltu4(wv[k], cm4));
-        nl >>= 3;
-      } else {
-        for (int k = 0; k < ncl; k++) nl += (lossy >> (cr[jb + k] & 31)) & 1;
+    for (int g = 0; g < 8; g++) {
+      const int x = s0 + 32 * g + lane;
+      nl[g] = 0;
+      ncl[g] = 0;
+      if (32 * g < nseg && x < nchunks) {
+        const int jb = 32 * x;
+        ncl[g] = min(32, W - jb);
+        if (vec && ncl[g] == 32) {
+          const uint4 a = __ldg(reinterpret_cast<const uint4*>(cr + jb));
+          const uint4 b = __ldg(reinterpret_cast<const uint4*>(cr + jb + 16));
+          nl[g] = (__popc(__vcmpltu4(a.x, cm4)) + __popc(__vcmpltu4(a.y, cm4)) +
+                   __popc(__vcmpltu4(a.z, cm4)) + __popc(__vcmpltu4(a.w, cm4)) +
+                   __popc(__vcmpltu4(b.x, cm4)) + __popc(__vcmpltu4(b.y, cm4)) +
+                   __popc(__vcmpltu4(b.z, cm4)) + __popc(__vcmpltu4(b.w, cm4))) >> 3;
+        } else {
+          for (int k = 0; k < ncl[g]; k++) nl[g] += (int)cr[jb + k] < cmax;
+        }
       }
     }
-    int incl = nl;
+    int carry = 0;   // segment-relative
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
+    for (int g = 0; g < 8; g++) {
+      if (32 * g >= nseg) break;   // warp-uniform
+      int incl = nl[g];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int c = 32 * g + lane;
+      if (c < nseg) {
+        pre_nl[row * nchunks + s0 + c] = nl_run + carry + incl - nl[g];
+        st[c] = carry + incl - nl[g];
+        es[c] = 0;
+      }
+      carry += __shfl_sync(FULL, incl, 31);
     }
-    const int32_t my_nl = nl_run + incl - nl;
-    if (x < nchunks) pre_nl[row * nchunks + x] = my_nl;
+    if (lane == 0) st[nseg] = carry;
+    __syncwarp();
     if (pre_ll) {
-      // escapes (symbol 0) among the group's symbols: the 32 chunks'
-      // symbols are contiguous, so the warp reads them coalesced; a word
-      // with an escape is attributed to its chunk by a binary search over
-      // the chunks' starting offsets (escapes are rare)
-      int esc = 0;
       if (qd) {
-        const int excl = incl - nl;                 // group-relative start
-        const int S = __shfl_sync(FULL, incl, 31);  // group's symbol pairs
+        const int S = carry;   // the segment's symbol pairs
         const int64_t qs = q0 + 2 * (int64_t)nl_run;
-        // per-chunk escape counts: lane idx (the chunk holding pair k,
-        // binary search over the chunks' starts) receives zc from the
-        // lanes whose pairs fall in its chunk
+        // the chunk holding pair k: the last start <= k
         auto attribute = [&](int zc, int k) {
-          if (!__any_sync(FULL, zc != 0)) return;   // warp-uniform
-          int idx = 0;
-#pragma unroll
-          for (int st = 16; st; st >>= 1) {
-            const int b = __shfl_sync(FULL, excl, idx + st);
-            if (b <= k) idx += st;
+          if (!zc) return;
+          int lo = 0, hi = nseg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (st[mid] <= k) lo = mid; else hi = mid - 1;
           }
-          for (int src = 0; src < 32; src++) {
-            const int zs = __shfl_sync(FULL, zc, src);
-            const int is = __shfl_sync(FULL, idx, src);
-            if (zs && lane == is) esc += zs;
-          }
+          atomicAdd(es + lo, zc);
         };
         if constexpr (sizeof(SYM) == 2) {
-          // 16-byte loads over the group's pairs: the aligned quads that
-          // hold them (a quad with one pair of the range is mapped memory)
+          // aligned quads holding the range (a quad with one pair of the
+          // range is mapped memory); pairs outside it are masked by k
           const uintptr_t bp = (uintptr_t)(qd + qs);
           const uint4* qa = reinterpret_cast<const uint4*>(bp & ~(uintptr_t)15);
-          const int off = (int)((bp & 15) >> 2);   // pairs before the range
+          const int off = (int)((bp & 15) >> 2);
           const int nq = (S + off + 3) >> 2;
-          constexpr int QU = 5;
+          constexpr int QU = 8;
           for (int g0 = 0; g0 < nq; g0 += 32 * QU) {
             uint4 w[QU];
 #pragma unroll
@@ -119,15 +131,12 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
               const int g = g0 + 32 * u + lane;
               w[u] = g < nq ? __ldg(qa + g) : make_uint4(1u, 1u, 1u, 1u);
             }
-            // escapes are rare: one vote for the whole batch (a zero
-            // half-word outside the range only sends it down the exact
-            // per-pair path, which masks by k)
             uint32_t z = 0;
 #pragma unroll
             for (int u = 0; u < QU; u++)
               z |= __vcmpeq2(w[u].x, 0u) | __vcmpeq2(w[u].y, 0u) |
                    __vcmpeq2(w[u].z, 0u) | __vcmpeq2(w[u].w, 0u);
-            if (!__any_sync(FULL, z != 0u)) continue;   // warp-uniform
+            if (z == 0u) continue;
 #pragma unroll
             for (int u = 0; u < QU; u++) {
               const int kb = 4 * (g0 + 32 * u + lane) - off;
@@ -135,38 +144,36 @@ __global__ void chunk_prefix_kernel(const uint8_t* __restrict__ codes,
 #pragma unroll
               for (int q = 0; q < 4; q++) {
                 const int k = kb + q;
-                const int zc = (k >= 0 && k < S)
-                                   ? ((ww[q] & 0xffffu) == 0u) + ((ww[q] >> 16) == 0u)
-                                   : 0;
-                attribute(zc, k);
+                if (k >= 0 && k < S)
+                  attribute(((ww[q] & 0xffffu) == 0u) + ((ww[q] >> 16) == 0u), k);
               }
             }
           }
         } else {
-          for (int k0 = 0; k0 < S; k0 += 128) {
-            int zc[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const int k = k0 + 32 * u + lane;
-              zc[u] = k < S ? (__ldg(qd + qs + 2 * k) == 0) + (__ldg(qd + qs + 2 * k + 1) == 0)
-                            : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) attribute(zc[u], k0 + 32 * u + lane);
-          }
+          for (int k = lane; k < S; k += 32)
+            attribute((__ldg(qd + qs + 2 * k) == 0) + (__ldg(qd + qs + 2 * k + 1) == 0), k);
         }
+        __syncwarp();
       }
-      const int ll = 2 * (ncl - nl) + esc;
-      int lincl = ll;
+      int lcarry = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, lincl, o);
-        if (lane >= o) lincl += y;
+      for (int g = 0; g < 8; g++) {
+        if (32 * g >= nseg) break;   // warp-uniform
+        const int c = 32 * g + lane;
+        const int ll = c < nseg ? 2 * (ncl[g] - nl[g]) + es[c] : 0;
+        int lincl = ll;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, lincl, o);
+          if (lane >= o) lincl += y;
+        }
+        if (c < nseg) pre_ll[row * nchunks + s0 + c] = ll_run + lcarry + lincl - ll;
+        lcarry += __shfl_sync(FULL, lincl, 31);
       }
-      if (x < nchunks) pre_ll[row * nchunks + x] = ll_run + lincl - ll;
-      ll_run += __shfl_sync(FULL, lincl, 31);
+      ll_run += lcarry;
     }
-    nl_run += __shfl_sync(FULL, incl, 31);
+    nl_run += carry;
+    __syncwarp();   // st / es are rewritten by the next segment
   }
 }
 

@@ -38,6 +38,10 @@ CASES = {
     "tiny_tau_mop": (lambda: _synth(5, 260, 270, 3), 4e-9, True, "mop", 32768),
     # integers, small radius: escapes and swept blocks
     "ints_radius16": (lambda: _ints(270, 300, 3, 7, -40, 41), 0.02, True, "mop", 16),
+    # rows wider than one 256-chunk segment of the prefix-count kernel,
+    # with escapes (and a ragged last chunk)
+    "ints_wide_radius16": (lambda: _ints(40, 9000, 2, 9, -40, 41), 0.02, True, "mop", 16),
+    "spectral_wide_sl": (lambda: _synth(2, 48, 8230, 2), 1e-3, True, "sl", 32768),
     # integers on a step of one fixed-point unit: exact reconstruction
     "ints_unit_step": (lambda: _ints(300, 260, 2, 8, -3, 4), 2.0 / 2 ** 28, False, "lorenzo", 32768),
 }
