@@ -350,6 +350,18 @@ def main():
     e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
     e2e_s = max_over_ranks(e2e_s)
     d2h = sum(int(x.nbytes) for x in host.values())
+    # the public compress() to an Archive (device entropy stage: only the
+    # packed sections come back), same pinned host input
+    arc = vg.compress(f_host, args.eps, cfg, relative=True)   # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        arc = None
+        arc = vg.compress(f_host, args.eps, cfg, relative=True)
+    torch.cuda.synchronize()
+    arc_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
+    arc_bytes = sum(len(x) for x in arc.sections)
+    del arc
     # host entropy backend (Huffman + zlib), timed on frame 0's streams
     nq0 = 2 * (H * W) if s.qd.numel() >= 2 * H * W else s.qd.numel()
     t0 = time.perf_counter()
@@ -423,6 +435,11 @@ def main():
         "e2e": {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
                 "unit": UNIT, "h2d_bytes_per_step": 8 * N,
                 "d2h_bytes_per_step": d2h},
+        "e2e_archive": {"value": round(8.0 * N * world / arc_s / 1e9, 3),
+                        "unit": UNIT, "ms_per_step": round(arc_s * 1e3, 1),
+                        "api": "compress() -> Archive sections",
+                        "h2d_bytes_per_step": 8 * N,
+                        "d2h_bytes_per_step": arc_bytes},
         "device_entropy": dent,
         "host_entropy": {"sample": "frame 0 codes + qd: Huffman + zlib(6)",
                          "seconds": round(ent_s, 3),

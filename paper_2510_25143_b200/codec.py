@@ -407,17 +407,31 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
     if not cfg.stats and cfg.radius <= 32768:
         # entropy stage on the device (csrc/huffman_gpu.cu): only the packed
         # sections come back; zlib stays on the host
+        import torch
         s = compress_device(f, eps, cfg, relative)
-        nby, nbx = _mode_grid_shape(f.H, f.W, cfg)
-        q_xi = huffman.encode_device(s.codes, EB_ALPHABET, 0)
-        q_d = huffman.encode_device(s.qd, 2 * cfg.radius,
-                                    max(0, cfg.radius - 4096))
+        # the small sections go to pinned memory on a side stream while
+        # the two Huffman sections are histogrammed and packed
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            h_ld, h_ll, h_modes = _to_host(s.ld), _to_host(s.ll), _to_host(s.modes)
+        for x in (s.ld, s.ll, s.modes):
+            x.record_stream(side)
+        pending = huffman.encode_device_many([
+            (s.codes, EB_ALPHABET, 0),
+            (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096))])
+        q_xi = pending[0].result()
+        q_d = pending[1].result()
+        side.synchronize()
+        l_d = huffman.new_bytearray(h_ld.numel())
+        huffman.host_copy(np.frombuffer(l_d, dtype=np.uint8), h_ld.numpy())
         return Archive(
             H=f.H, W=f.W, T=f.T, dx=f.dx, dy=f.dy, dt=f.dt, scale=s.scale,
             eps=s.eps, tau_prime=s.tau, config=cfg, q_xi=q_xi, q_d=q_d,
-            l_d=s.ld.cpu().numpy().tobytes(),
-            lossless_stream=s.ll.cpu().numpy().astype("<i8").tobytes(),
-            mode_bitmap=np.packbits(s.modes.cpu().numpy()).tobytes(),
+            l_d=l_d,
+            lossless_stream=h_ll.numpy().astype("<i8", copy=False).tobytes(),
+            mode_bitmap=np.packbits(h_modes.numpy()).tobytes(),
         )
     s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats,
                         host_out=True)

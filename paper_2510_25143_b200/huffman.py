@@ -67,41 +67,109 @@ def encode(symbols, alphabet_size: int) -> bytes:
     return _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes() + out.tobytes()
 
 
+_POOL = None
+_BA_NEW = None
+
+
+def new_bytearray(n: int) -> bytearray:
+    """A bytearray of n bytes WITHOUT bytearray(n)'s zero fill (which
+    touches every page of a fresh mapping single-threaded): the caller
+    overwrites all of it, with host_copy."""
+    global _BA_NEW
+    if _BA_NEW is None:
+        import ctypes
+        f = ctypes.pythonapi.PyByteArray_FromStringAndSize
+        f.restype = ctypes.py_object
+        f.argtypes = (ctypes.c_void_p, ctypes.c_ssize_t)
+        _BA_NEW = f
+    return _BA_NEW(None, n)
+
+
+def host_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src for large byte arrays, split over host threads (numpy
+    releases the GIL for the copies; a fresh destination's first-touch page
+    faults are taken in parallel too)."""
+    global _POOL
+    n = src.size
+    step = 1 << 25
+    if n <= step:
+        dst[:] = src
+        return
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max(1, min(8, _lib.host_threads())))
+
+    def part(o):
+        dst[o:o + step] = src[o:o + step]
+    list(_POOL.map(part, range(0, n, step)))
+
+
+class PendingBlob:
+    """A device-packed section on its way to pinned host memory."""
+
+    def __init__(self, head, nbytes, host, words, event):
+        self._head, self._nbytes = head, nbytes
+        self._host, self._words, self._event = host, words, event
+
+    def result(self) -> bytearray:
+        head = self._head
+        blob = new_bytearray(len(head) + self._nbytes)
+        blob[:len(head)] = head
+        if self._nbytes:
+            self._event.synchronize()
+            host_copy(np.frombuffer(blob, dtype=np.uint8)[len(head):],
+                      self._host.numpy().view(np.uint8)[:self._nbytes])
+        self._host = self._words = None
+        return blob
+
+
+def encode_device_many(sections) -> list:
+    """encode() of several CUDA uint8 / uint16 tensors, given as
+    (symbols, alphabet_size, window_base) (window_base: first symbol of the
+    shared-memory histogram window, the symbols' mode).  All histograms run
+    before the one host synchronisation (code lengths are built on the
+    host), then every section is packed and copied to pinned memory
+    asynchronously: the returned PendingBlob.result()s give the bytes."""
+    import torch
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    counts = []
+    for sym, alpha, base in sections:
+        c = torch.zeros(alpha, dtype=torch.int64, device=sym.device)
+        if sym.numel():
+            _lib.check(L.vfcp_huff_hist_dev(sym.data_ptr(), sym.element_size(),
+                                            int(sym.numel()), alpha, base,
+                                            c.data_ptr(), st),
+                       "huffman histogram")
+        counts.append(c)
+    counts = [c.cpu().numpy() for c in counts]   # one synchronisation
+    out = []
+    for (sym, alpha, _), counts_h in zip(sections, counts):
+        n = int(sym.numel())
+        lens = code_lengths(counts_h)
+        total_bits = int((counts_h * lens.astype(np.int64)).sum())
+        n_words = max(1, (total_bits + 31) // 32)
+        words = torch.empty(n_words, dtype=torch.int32, device=sym.device)
+        if n:
+            _lib.check(L.vfcp_huff_pack_dev(sym.data_ptr(), sym.element_size(),
+                                            n, lens.ctypes.data, alpha,
+                                            words.data_ptr(), n_words, st),
+                       "huffman pack (device)")
+        h = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
+        h.copy_(words, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        head = _HDR.pack(alpha, n, total_bits) + lens.tobytes()
+        out.append(PendingBlob(head, (total_bits + 7) // 8, h, words, ev))
+    return out
+
+
 def encode_device(symbols, alphabet_size: int, window_base: int = 0) -> bytes:
     """encode() of a CUDA uint8 / uint16 tensor: the same bytes.
 
     window_base: first symbol of the shared-memory histogram window (the
     symbols' mode; radius - 4096 for the residual stream)."""
-    import torch
-    n = int(symbols.numel())
-    sb = symbols.element_size()
-    L = _lib.lib()
-    st = _lib.stream_ptr()
-    counts = torch.zeros(alphabet_size, dtype=torch.int64, device=symbols.device)
-    if n:
-        _lib.check(L.vfcp_huff_hist_dev(symbols.data_ptr(), sb, n, alphabet_size,
-                                        window_base, counts.data_ptr(), st),
-                   "huffman histogram")
-    counts_h = counts.cpu().numpy()
-    lens = code_lengths(counts_h)
-    total_bits = int((counts_h * lens.astype(np.int64)).sum())
-    n_words = max(1, (total_bits + 31) // 32)
-    words = torch.empty(n_words, dtype=torch.int32, device=symbols.device)
-    if n:
-        _lib.check(L.vfcp_huff_pack_dev(symbols.data_ptr(), sb, n,
-                                        lens.ctypes.data, alphabet_size,
-                                        words.data_ptr(), n_words, st),
-                   "huffman pack (device)")
-    h = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
-    h.copy_(words, non_blocking=True)
-    nbytes = (total_bits + 7) // 8
-    # the blob is assembled with one host copy of the packed bytes
-    head = _HDR.pack(alphabet_size, n, total_bits) + lens.tobytes()
-    blob = bytearray(len(head) + nbytes)
-    blob[:len(head)] = head
-    torch.cuda.current_stream().synchronize()
-    np.frombuffer(blob, dtype=np.uint8)[len(head):] = h.numpy().view(np.uint8)[:nbytes]
-    return blob
+    return encode_device_many([(symbols, alphabet_size, window_base)])[0].result()
 
 
 def decode(blob, out_dtype=np.int64) -> np.ndarray:
