@@ -186,6 +186,47 @@ __device__ __forceinline__ int hd_step(const HuffDecTables& t, const uint32_t* l
   return 0;
 }
 
+// A decoding cursor over one chunk: a 64-bit window of the stream held in
+// registers and refilled when fewer than 32 of its bits are left (the
+// table needs lb <= 12 valid bits), so a short codeword costs a shared-
+// memory lookup and two shifts, not three global loads.
+struct HdCursor {
+  unsigned long long buf;
+  int avail;
+  int64_t p;
+  // next codeword: its length (0: invalid) and symbol
+  __device__ __forceinline__ int next(const HuffDecTables& t, const uint32_t* lut,
+                                      const uint32_t* w, uint32_t* sym) {
+    if (avail < 32) {
+      buf = hd_window(w, p);
+      avail = 64;
+    }
+    const uint32_t e = lut[buf >> (64 - t.lb)];
+    int L;
+    if (e) {
+      *sym = e >> 8;
+      L = (int)(e & 255u);
+    } else {
+      L = hd_step(t, lut, w, p, sym);   // long codeword: table walk
+      if (L == 0) return 0;
+    }
+    p += L;
+    buf <<= L;   // L <= 60
+    avail -= L;  // < 32 (even negative) forces a refill
+    return L;
+  }
+};
+
+// chunk k starts at its boundary and is decoded in the first pass
+__global__ void huff_init_kernel(int64_t nchunk, int64_t* __restrict__ start,
+                                 int* __restrict__ dirty) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nchunk) {
+    start[k] = k * (int64_t)HD_CB;
+    dirty[k] = 1;
+  }
+}
+
 // sync pass: chunks whose start moved are decoded to their exit
 __global__ void __launch_bounds__(256)
 huff_sync_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
@@ -201,15 +242,14 @@ huff_sync_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
   if (!dirty[k]) return;
   dirty[k] = 0;
   const int64_t end = min((k + 1) * (int64_t)HD_CB, total_bits);
-  int64_t p = start[k];
+  HdCursor cur{0ull, 0, start[k]};
   int32_t c = 0;
-  while (p < end) {
+  while (cur.p < end) {
     uint32_t sym;
-    const int L = hd_step(t, lut, w, p, &sym);
-    if (L == 0) { atomicOr(bad, 1); break; }
-    p += L;
+    if (cur.next(t, lut, w, &sym) == 0) { atomicOr(bad, 1); break; }
     c++;
   }
+  const int64_t p = cur.p;
   exitp[k] = p;
   count[k] = c;
   if (k + 1 < nchunk && start[k + 1] != p) {
@@ -219,6 +259,9 @@ huff_sync_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
   }
 }
 
+// symbols of chunk k from its true start to out[off[k]...]; once the
+// output position is 8-byte aligned, symbols are gathered in a 64-bit
+// register and stored 8 bytes at a time
 template <typename S>
 __global__ void __launch_bounds__(256)
 huff_write_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
@@ -230,16 +273,28 @@ huff_write_kernel(HuffDecTables t, const uint32_t* __restrict__ w,
   __syncthreads();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nchunk) return;
+  constexpr int V = 8 / sizeof(S);
   const int64_t end = min((k + 1) * (int64_t)HD_CB, total_bits);
-  int64_t p = start[k];
+  HdCursor cur{0ull, 0, start[k]};
   int64_t o = off[k];
-  while (p < end) {
-    uint32_t sym;
-    const int L = hd_step(t, lut, w, p, &sym);
-    if (L == 0) break;
-    p += L;
+  uint32_t sym;
+  while (cur.p < end && ((uintptr_t)(out + o) & 7) != 0) {
+    if (cur.next(t, lut, w, &sym) == 0) return;
     out[o++] = (S)sym;
   }
+  unsigned long long acc = 0;
+  int nv = 0;
+  while (cur.p < end) {
+    if (cur.next(t, lut, w, &sym) == 0) break;
+    acc |= (unsigned long long)sym << (8 * sizeof(S) * nv);
+    if (++nv == V) {
+      *reinterpret_cast<unsigned long long*>(out + o) = acc;
+      o += V;
+      acc = 0;
+      nv = 0;
+    }
+  }
+  for (int i = 0; i < nv; i++) out[o + i] = (S)(acc >> (8 * sizeof(S) * i));
 }
 
 }  // namespace vfcp
@@ -417,15 +472,9 @@ int vfcp_huff_unpack_dev(const uint32_t* words, int64_t n_words,
                       cudaMemcpyHostToDevice, st));
   HCK(cudaMemcpyAsync(d_sym, symtab.data(), sizeof(uint32_t) * symtab.size(),
                       cudaMemcpyHostToDevice, st));
-  {
-    std::vector<int64_t> s0(nchunk);
-    for (int64_t k = 0; k < nchunk; k++) s0[k] = k * (int64_t)HD_CB;
-    HCK(cudaMemcpyAsync(d_start, s0.data(), sizeof(int64_t) * nchunk,
-                        cudaMemcpyHostToDevice, st));
-    std::vector<int> d1(nchunk, 1);
-    HCK(cudaMemcpyAsync(d_dirty, d1.data(), sizeof(int) * nchunk,
-                        cudaMemcpyHostToDevice, st));
-  }
+  huff_init_kernel<<<(unsigned)((nchunk + 255) / 256), 256, 0, st>>>(nchunk, d_start,
+                                                                   d_dirty);
+  HCK(cudaGetLastError());
   t.lut = d_lut;
   t.symtab = d_sym;
   HCK(cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, st));
