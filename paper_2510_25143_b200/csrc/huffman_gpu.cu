@@ -90,10 +90,39 @@ huff_pack_kernel(const S* __restrict__ sym, int64_t n,
                  uint32_t* __restrict__ out) {
   typedef cub::BlockScan<unsigned long long, HP_T> BS;
   __shared__ typename BS::TempStorage tmp;
-  const int64_t first = (int64_t)blockIdx.x * HP_CHUNK + (int64_t)threadIdx.x * HP_PER;
-  const int cnt = (int)max((int64_t)0, min((int64_t)HP_PER, n - first));
+  // the CTA's symbols staged in shared memory with coalesced 16-byte loads,
+  // one padded row per thread (its HP_PER consecutive symbols), read back
+  // 16 bytes at a time without bank conflicts
+  constexpr int ROWB = HP_PER * (int)sizeof(S);
+  constexpr int PADB = ROWB + 16;
+  constexpr int V = 16 / (int)sizeof(S);
+  __shared__ __align__(16) unsigned char ss[HP_T * PADB];
+  const int64_t cbase = (int64_t)blockIdx.x * HP_CHUNK;
+  const int count = (int)min((int64_t)HP_CHUNK, n - cbase);
+  if (count == HP_CHUNK && ((uintptr_t)(sym + cbase) & 15) == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(sym + cbase);
+    for (int q = threadIdx.x; q < HP_CHUNK * (int)sizeof(S) / 16; q += HP_T)
+      *reinterpret_cast<uint4*>(ss + (q / (ROWB / 16)) * PADB + (q % (ROWB / 16)) * 16) =
+          __ldg(src + q);
+  } else {
+    for (int e = threadIdx.x; e < count; e += HP_T)
+      reinterpret_cast<S*>(ss + (e / HP_PER) * PADB)[e % HP_PER] = sym[cbase + e];
+  }
+  __syncthreads();
+  const unsigned char* row = ss + threadIdx.x * PADB;
+  const int cnt = max(0, min(HP_PER, count - (int)threadIdx.x * HP_PER));
+  auto sym_at = [&](const uint4& q, int i) -> int {   // i-th symbol of a piece
+    const uint32_t wd = i < V / 4 ? q.x : i < V / 2 ? q.y : i < 3 * V / 4 ? q.z : q.w;
+    const int sh = (i % (V / 4)) * 8 * (int)sizeof(S);
+    return (int)((wd >> sh) & (sizeof(S) == 1 ? 0xffu : 0xffffu));
+  };
   unsigned long long mine = 0;
-  for (int k = 0; k < cnt; k++) mine += __ldg(lens + sym[first + k]);
+  for (int k0 = 0; k0 < cnt; k0 += V) {
+    const uint4 q = *reinterpret_cast<const uint4*>(row + k0 * (int)sizeof(S));
+#pragma unroll
+    for (int i = 0; i < V; i++)
+      if (k0 + i < cnt) mine += __ldg(lens + sym_at(q, i));
+  }
   unsigned long long off;
   BS(tmp).ExclusiveSum(mine, off);
   if (cnt == 0 || mine == 0) return;
@@ -118,15 +147,20 @@ huff_pack_kernel(const S* __restrict__ sym, int64_t n,
     nb += L;
     emit_full();
   };
-  for (int k = 0; k < cnt; k++) {
-    const int s = (int)sym[first + k];
-    const int L = __ldg(lens + s);
-    const unsigned long long c = __ldg(codes + s);
-    if (L > 32) {
-      append(c >> 32, L - 32);
-      append(c & 0xffffffffull, 32);
-    } else if (L > 0) {
-      append(c, L);
+  for (int k0 = 0; k0 < cnt; k0 += V) {
+    const uint4 q = *reinterpret_cast<const uint4*>(row + k0 * (int)sizeof(S));
+#pragma unroll
+    for (int i = 0; i < V; i++) {
+      if (k0 + i >= cnt) break;
+      const int s = sym_at(q, i);
+      const int L = __ldg(lens + s);
+      const unsigned long long c = __ldg(codes + s);
+      if (L > 32) {
+        append(c >> 32, L - 32);
+        append(c & 0xffffffffull, 32);
+      } else if (L > 0) {
+        append(c, L);
+      }
     }
   }
   if (nb > 0) atomicOr(out + wi, bswap32((uint32_t)(buf >> 32)));
