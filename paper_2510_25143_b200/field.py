@@ -236,3 +236,67 @@ def _host(a):
     if _is_torch(a):
         return a.detach().cpu().numpy()
     return a
+
+
+# ------------------------------------------------------------- raw I/O
+# field.py:103-138: headerless little-endian float32 components plus a JSON
+# sidecar with the dims and spacing.  Components are read straight into
+# page-locked host memory, so compress() moves them to the GPU at PCIe rate.
+
+def _pinned_f32(n: int) -> np.ndarray:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(n, dtype=torch.float32, pin_memory=True).numpy()
+    except Exception:   # pragma: no cover - no torch / no driver
+        pass
+    return np.empty(n, dtype=np.float32)
+
+
+def load_raw(u_path, v_path, H, W, T, dx=1.0, dy=1.0, dt=1.0) -> FieldSeries:
+    """Two headerless little-endian float32 binaries of H*W*T samples each
+    (field.py:103-116: the same size check and message)."""
+    from pathlib import Path
+    n = H * W * T
+    comps = {}
+    for name, path in (("u", u_path), ("v", v_path)):
+        path = Path(path)
+        actual = path.stat().st_size
+        expected = n * 4
+        if actual != expected:
+            raise FieldError(
+                f"{path}: expected {expected} bytes ({n} float32), got {actual}")
+        a = _pinned_f32(n)
+        with path.open("rb") as fh:
+            got = fh.readinto(memoryview(a).cast("B"))
+        if got != expected:   # pragma: no cover - file shrank under us
+            raise FieldError(f"{path}: short read ({got} of {expected} bytes)")
+        if np.little_endian is False:   # pragma: no cover
+            a.byteswap(inplace=True)
+        comps[name] = a
+    return FieldSeries(H, W, T, dx, dy, dt, comps["u"], comps["v"])
+
+
+def save_raw(f: FieldSeries, u_path, v_path, meta_path=None) -> None:
+    """field.py:119-124."""
+    import json
+    from pathlib import Path
+    np.asarray(_host(f.u)).astype("<f4").tofile(u_path)
+    np.asarray(_host(f.v)).astype("<f4").tofile(v_path)
+    if meta_path is not None:
+        meta = {"H": f.H, "W": f.W, "T": f.T, "dx": f.dx, "dy": f.dy, "dt": f.dt}
+        Path(meta_path).write_text(json.dumps(meta, indent=2) + "\n")
+
+
+def load_meta(meta_path) -> dict:
+    """field.py:127-136."""
+    import json
+    from pathlib import Path
+    meta = json.loads(Path(meta_path).read_text())
+    for key in ("H", "W", "T"):
+        if key not in meta:
+            raise FieldError(f"metadata sidecar missing '{key}'")
+    meta.setdefault("dx", 1.0)
+    meta.setdefault("dy", 1.0)
+    meta.setdefault("dt", 1.0)
+    return meta

@@ -13,8 +13,10 @@ them (tracking.py:75-141), so components are simple paths or cycles.
 
 from __future__ import annotations
 
+import csv
 import math
 from dataclasses import dataclass
+from pathlib import Path
 from itertools import combinations
 
 import numpy as np
@@ -175,3 +177,66 @@ def verify(orig: FieldSeries, recon: FieldSeries,
     return VerifyReport(cr=cr, psnr=p, max_abs_err=max_err,
                         fc_t=fc_t, fc_s=fc_s, n_traj_orig=n_o,
                         n_traj_recon=n_r, isomorphic=iso)
+
+
+# --------------------------------------------------------- residual stats
+# tracking.py:199-268: distribution summaries of a symbol stream (0 = escape)
+# for `vfcp stats`; the run detection is vectorised (boundaries of the
+# center-symbol mask) instead of a Python loop over the stream.
+
+@dataclass
+class ResidualStats:
+    folded_pmf: np.ndarray        # P(|idx| = m), m = 0.. (escapes excluded)
+    tail_ccdf: np.ndarray         # P(|idx| >= m)
+    overflow_rate: float
+    run_lengths: np.ndarray       # maximal runs of the center symbol
+    run_ccdf: np.ndarray          # P(run >= L), L = 1..max
+    run_mean: float
+    run_percentiles: dict         # {75: ..., 80: ..., 85: ..., 90: ...}
+
+    def write_pmf_csv(self, path) -> None:
+        with Path(path).open("w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["magnitude", "pmf", "ccdf"])
+            for m, (p, c) in enumerate(zip(self.folded_pmf, self.tail_ccdf)):
+                w.writerow([m, f"{p:.10g}", f"{c:.10g}"])
+
+    def write_runs_csv(self, path) -> None:
+        with Path(path).open("w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["run_length", "ccdf"])
+            for L, c in enumerate(self.run_ccdf, start=1):
+                w.writerow([L, f"{c:.10g}"])
+            w.writerow([])
+            w.writerow(["mean", f"{self.run_mean:.10g}"])
+            for q, val in sorted(self.run_percentiles.items()):
+                w.writerow([f"p{q}", f"{val:.10g}"])
+
+
+def residual_stats(symbols, radius: int) -> ResidualStats:
+    """tracking.py:228-268."""
+    symbols = np.asarray(symbols, dtype=np.int64)
+    overflow = symbols == 0
+    mags = np.abs(symbols[~overflow] - radius)
+    if mags.size:
+        pmf = np.bincount(mags) / mags.size
+        ccdf = pmf[::-1].cumsum()[::-1]
+    else:
+        pmf = np.array([0.0])
+        ccdf = np.array([0.0])
+    c = np.concatenate(([False], symbols == radius, [False])).astype(np.int8)
+    d = np.diff(c)
+    runs = (np.flatnonzero(d == -1) - np.flatnonzero(d == 1)).astype(np.int64)
+    if runs.size:
+        rc = np.bincount(runs, minlength=int(runs.max()) + 1)[1:]
+        run_ccdf = rc[::-1].cumsum()[::-1] / runs.size
+        mean = float(runs.mean())
+        pct = {q: float(np.percentile(runs, q)) for q in (75, 80, 85, 90)}
+    else:
+        run_ccdf = np.array([0.0])
+        mean = 0.0
+        pct = {q: 0.0 for q in (75, 80, 85, 90)}
+    ov_rate = float(overflow.mean()) if symbols.size else 0.0
+    return ResidualStats(folded_pmf=pmf, tail_ccdf=ccdf, overflow_rate=ov_rate,
+                         run_lengths=runs, run_ccdf=run_ccdf, run_mean=mean,
+                         run_percentiles=pct)
