@@ -503,6 +503,39 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
 # --------------------------------------------------------------------------
 # decompression
 
+class _SideDecode:
+    """huffman.decode_device on a host thread and a side stream."""
+
+    def __init__(self, blob, dtype):
+        import threading
+
+        import torch
+        self._out = self._err = None
+        dev = torch.cuda.current_device()
+
+        def work():
+            try:
+                with torch.cuda.device(dev):
+                    side = torch.cuda.Stream()
+                    with torch.cuda.stream(side):
+                        self._out = huffman.decode_device(blob, dtype)
+                    side.synchronize()
+            except BaseException as err:
+                self._err = err
+
+        self._t = threading.Thread(target=work, daemon=True)
+        self._t.start()
+
+    def result(self):
+        import torch
+        self._t.join()
+        if self._err is not None:
+            raise self._err
+        if self._out.numel():
+            self._out.record_stream(torch.cuda.current_stream())
+        return self._out
+
+
 def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
                       qd=None, ll=None, modes=None, ld=None):
     """codec.py:401-453 on device.  Returns (out_u, out_v, fix_u, fix_v)
@@ -511,9 +544,21 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
     import torch
     cfg = a.config
     n = a.H * a.W * a.T
+    qd_pre = qd_err = None
     if codes is None:
-        # entropy decode on the device (huffman.decode_device)
-        codes = huffman.decode_device(a.q_xi, np.uint8)
+        # entropy decode on the device (huffman.decode_device); with the
+        # symbol section also to decode, the codes go to a host thread on a
+        # side stream and both sections decode concurrently (errors are
+        # raised in the sequential order: codes first)
+        if qd is None and cfg.radius <= 32768:
+            th = _SideDecode(a.q_xi, np.uint8)
+            try:
+                qd_pre = huffman.decode_device(a.q_d, np.uint16)
+            except ValueError as err:
+                qd_err = err
+            codes = th.result()
+        else:
+            codes = huffman.decode_device(a.q_xi, np.uint8)
     if codes.shape[0] != n:
         raise ValueError("eb code stream length mismatch")
     if len(a.l_d) < (n + 7) // 8:
@@ -521,7 +566,10 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
         raise ValueError("lossless bitmap disagrees with eb codes")
     if qd is None:
         if cfg.radius <= 32768:
-            qd = huffman.decode_device(a.q_d, np.uint16)
+            if qd_err is not None:
+                raise qd_err
+            qd = (qd_pre if qd_pre is not None
+                  else huffman.decode_device(a.q_d, np.uint16))
             # any symbol >= 2 radius (uint16 seen as int16: no uint16 max)
             q16, lim = qd.view(torch.int16), 2 * cfg.radius
             if lim >= 65536:
