@@ -138,6 +138,15 @@ int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
                 void* stream);
+/* vfcp_decode, and each frame's f64 output copied to host_u / host_v
+ * (f64[N], page-locked for the copies to overlap the decode of later
+ * frames) as soon as the frame is decoded; returns after the copies. */
+int vfcp_decode_host(const vfcp_params* p, const uint8_t* codes,
+                     const void* qd, int64_t n_qd, const int64_t* ll,
+                     int64_t n_ll, const uint8_t* modes,
+                     const int64_t* qd_row_off, const int64_t* ll_row_off,
+                     double* out_u, double* out_v, double* host_u,
+                     double* host_v, void* stream);
 
 /* ---- host entropy backend (huffman.py), byte-identical to the reference */
 /* huffman.py:21-48 code_lengths (heapq order, serial tie-break). */

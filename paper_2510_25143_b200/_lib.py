@@ -60,6 +60,8 @@ _SIGS = {
                                  _P, _P]),
     "vfcp_decode": (_I, [_PP, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P,
                          _P, _P, _P]),
+    "vfcp_decode_host": (_I, [_PP, _P, _P, _I64, _P, _I64, _P, _P, _P, _P,
+                              _P, _P, _P, _P]),
     "vfcp_huff_lengths": (_I, [_P, _I32, _P]),
     "vfcp_huff_count": (_I, [_P, _I, _I64, _I32, _P]),
     "vfcp_huff_pack": (_I, [_P, _I, _I64, _P, _I32, _P, _I64, _P, _I]),

@@ -537,10 +537,12 @@ class _SideDecode:
 
 
 def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
-                      qd=None, ll=None, modes=None, ld=None):
+                      qd=None, ll=None, modes=None, ld=None, host_out=None):
     """codec.py:401-453 on device.  Returns (out_u, out_v, fix_u, fix_v)
     as CUDA tensors.  codes/qd/ll/modes may be passed pre-decoded (host
-    numpy or device tensors) to skip the host entropy stage."""
+    numpy or device tensors) to skip the host entropy stage.  host_out:
+    (u, v) page-locked float64 host tensors that receive each frame's output
+    while later frames decode (not with want_fixed)."""
     import torch
     cfg = a.config
     n = a.H * a.W * a.T
@@ -640,21 +642,35 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
     out_v = torch.empty(n, dtype=torch.float64, device="cuda")
     fix_u = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
     fix_v = torch.empty(n, dtype=torch.int64, device="cuda") if want_fixed else None
-    _lib.check(L.vfcp_decode(pp, d_codes.data_ptr(), d_qd.data_ptr(), n_qd,
-                             d_ll.data_ptr(), len(ll), d_modes.data_ptr(),
-                             qd_row_off.data_ptr(), ll_row_off.data_ptr(),
-                             out_u.data_ptr(), out_v.data_ptr(),
-                             _lib.ptr(fix_u), _lib.ptr(fix_v), st), "decode")
+    if host_out is not None and not want_fixed:
+        hu, hv = host_out
+        if hu.numel() != n or hv.numel() != n or hu.dtype != torch.float64:
+            raise ValueError("host_out: two float64 host tensors of H*W*T")
+        _lib.check(L.vfcp_decode_host(pp, d_codes.data_ptr(), d_qd.data_ptr(),
+                                      n_qd, d_ll.data_ptr(), len(ll),
+                                      d_modes.data_ptr(), qd_row_off.data_ptr(),
+                                      ll_row_off.data_ptr(), out_u.data_ptr(),
+                                      out_v.data_ptr(), hu.data_ptr(),
+                                      hv.data_ptr(), st), "decode")
+    else:
+        _lib.check(L.vfcp_decode(pp, d_codes.data_ptr(), d_qd.data_ptr(), n_qd,
+                                 d_ll.data_ptr(), len(ll), d_modes.data_ptr(),
+                                 qd_row_off.data_ptr(), ll_row_off.data_ptr(),
+                                 out_u.data_ptr(), out_v.data_ptr(),
+                                 _lib.ptr(fix_u), _lib.ptr(fix_v), st), "decode")
     return out_u, out_v, fix_u, fix_v
 
 
 def decompress_with_stats(a: Archive) -> tuple[FieldSeries, DecodeStats]:
     import torch
-    out_u, out_v, _, _ = decompress_device(a)
-    # FieldSeries re-validates the output (codec.py:451): on the device, then
-    # the arrays come back through pinned memory
+    n = a.H * a.W * a.T
+    # each frame's output comes back to pinned memory while later frames
+    # decode; FieldSeries re-validates the output (codec.py:451) on the
+    # device
+    hu = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hv = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    out_u, out_v, _, _ = decompress_device(a, host_out=(hu, hv))
     fs = FieldSeries(a.H, a.W, a.T, a.dx, a.dy, a.dt, out_u, out_v)
-    hu, hv = _to_host(out_u), _to_host(out_v)
     torch.cuda.current_stream().synchronize()
     object.__setattr__(fs, "u", hu.numpy())
     object.__setattr__(fs, "v", hv.numpy())

@@ -597,11 +597,47 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   return VFCP_OK;
 }
 
+// Per-frame copies of the float64 output to (pinned) host memory on a side
+// stream, each gated by an event after the frame's last kernel, so the
+// transfers of frame t overlap the decode of frames > t.
+struct DecHostOut {
+  double* hu = nullptr;
+  double* hv = nullptr;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int init(int T) {
+    if (!hu) return VFCP_OK;
+    CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    ev.resize(T);
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return VFCP_OK;
+  }
+  int frame(int t, int64_t HW, const double* du, const double* dv, cudaStream_t st) {
+    if (!hu) return VFCP_OK;
+    CK(cudaEventRecord(ev[t], st));
+    CK(cudaStreamWaitEvent(side, ev[t], 0));
+    CK(cudaMemcpyAsync(hu + t * HW, du + t * HW, sizeof(double) * HW,
+                       cudaMemcpyDeviceToHost, side));
+    CK(cudaMemcpyAsync(hv + t * HW, dv + t * HW, sizeof(double) * HW,
+                       cudaMemcpyDeviceToHost, side));
+    return VFCP_OK;
+  }
+  int finish() {
+    if (!side) return VFCP_OK;
+    CK(cudaStreamSynchronize(side));
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(side);
+    side = nullptr;
+    return VFCP_OK;
+  }
+  ~DecHostOut() { finish(); }
+};
+
 int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                 const int64_t* ll, const uint8_t* modes,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
-                cudaStream_t st) {
+                cudaStream_t st, DecHostOut* ho) {
   const int H = p->H, W = p->W, T = p->T;
   const int64_t HW = (int64_t)H * W;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
@@ -655,7 +691,10 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
     bio.frame_tag = (uint32_t)t + 1u;
     LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
-
+    {
+      const int rh = ho->frame(t, HW, out_u, out_v, st);
+      if (rh) return rh;
+    }
   }
   return VFCP_OK;
 }
@@ -900,6 +939,38 @@ int vfcp_decode_prepare(const vfcp_params* p, const uint8_t* codes,
   return VFCP_OK;
 }
 
+static int decode_common(const vfcp_params* p, const uint8_t* codes,
+                         const void* qd, int64_t n_qd, const int64_t* ll,
+                         int64_t n_ll, const uint8_t* modes,
+                         const int64_t* qd_row_off, const int64_t* ll_row_off,
+                         double* out_u, double* out_v, int64_t* fix_u,
+                         int64_t* fix_v, DecHostOut* ho, cudaStream_t st) {
+  if (fast_ok(p) && !getenv("VFCP_SLOW_PATH")) {
+    int rc = ho->init(p->T);
+    if (rc) return rc;
+    rc = decode_fast(p, codes, (const uint16_t*)qd, ll, modes, qd_row_off,
+                     ll_row_off, out_u, out_v, fix_u, fix_v, st, ho);
+    const int rf = ho->finish();
+    return rc ? rc : rf;
+  }
+  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
+  int rc;
+#define DEC(I, SYM)                                                          \
+  rc = decode_impl<I, SYM>(p, codes, (const SYM*)qd, n_qd, ll, n_ll, modes,   \
+                           qd_row_off, ll_row_off, out_u, out_v, fix_u,      \
+                           fix_v, st)
+  if (nf) { if (ns) DEC(int32_t, uint16_t); else DEC(int32_t, uint32_t); }
+  else { if (ns) DEC(int64_t, uint16_t); else DEC(int64_t, uint32_t); }
+#undef DEC
+  if (rc || !ho->hu) return rc;
+  // generic path: the whole output at the end
+  const int64_t n = (int64_t)p->H * p->W * p->T;
+  CK(cudaMemcpyAsync(ho->hu, out_u, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ho->hv, out_v, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return VFCP_OK;
+}
+
 int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
                 int64_t n_qd, const int64_t* ll, int64_t n_ll,
                 const uint8_t* modes,
@@ -908,18 +979,28 @@ int vfcp_decode(const vfcp_params* p, const uint8_t* codes, const void* qd,
                 void* stream) {
   int rc = check_params(p);
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (fast_ok(p) && !getenv("VFCP_SLOW_PATH"))
-    return decode_fast(p, codes, (const uint16_t*)qd, ll, modes, qd_row_off,
-                       ll_row_off, out_u, out_v, fix_u, fix_v, st);
-  const bool nf = narrow_frames(p->tau), ns = narrow_symbols(p->radius);
-#define DEC(I, SYM)                                                          \
-  return decode_impl<I, SYM>(p, codes, (const SYM*)qd, n_qd, ll, n_ll, modes, \
-                             qd_row_off, ll_row_off, out_u, out_v, fix_u,    \
-                             fix_v, st)
-  if (nf) { if (ns) DEC(int32_t, uint16_t); else DEC(int32_t, uint32_t); }
-  else { if (ns) DEC(int64_t, uint16_t); else DEC(int64_t, uint32_t); }
-#undef DEC
+  DecHostOut ho;
+  return decode_common(p, codes, qd, n_qd, ll, n_ll, modes, qd_row_off,
+                       ll_row_off, out_u, out_v, fix_u, fix_v, &ho,
+                       (cudaStream_t)stream);
+}
+
+int vfcp_decode_host(const vfcp_params* p, const uint8_t* codes,
+                     const void* qd, int64_t n_qd, const int64_t* ll,
+                     int64_t n_ll, const uint8_t* modes,
+                     const int64_t* qd_row_off, const int64_t* ll_row_off,
+                     double* out_u, double* out_v, double* host_u,
+                     double* host_v, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (!host_u || !host_v)
+    return fail(VFCP_EINVAL, "vfcp_decode_host: null host buffer");
+  DecHostOut ho;
+  ho.hu = host_u;
+  ho.hv = host_v;
+  return decode_common(p, codes, qd, n_qd, ll, n_ll, modes, qd_row_off,
+                       ll_row_off, out_u, out_v, nullptr, nullptr, &ho,
+                       (cudaStream_t)stream);
 }
 
 }  // extern "C"
