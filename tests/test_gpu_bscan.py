@@ -128,3 +128,24 @@ def test_device_huffman_decode(name):
     blob = huffman.encode(s.qd.cpu().numpy(), 2 * radius)
     with pytest.raises(ValueError):
         huffman.decode_device(blob[:-3], np.uint16)
+
+
+@pytest.mark.parametrize("name", ["spectral_multicta_mop", "ints_radius16"])
+def test_decompress_host_paths_agree(name, monkeypatch):
+    """decompress() streams each frame's output to pinned host memory
+    (vfcp_decode_host); the generic decoder (VFCP_SLOW_PATH) copies it at
+    the end: both give the device decoder's output."""
+    import torch
+    import paper_2510_25143_b200 as vg
+    gen, eps, rel, pred, radius = CASES[name]
+    H, W, T, u, v = gen()
+    cfg = vg.Config(predictor=pred, radius=radius)
+    a = vg.compress(vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v), eps, cfg,
+                    relative=rel)
+    du, dv, _, _ = vg.decompress_device(a)
+    fast = vg.decompress(a)
+    monkeypatch.setenv("VFCP_SLOW_PATH", "1")
+    slow = vg.decompress(a)
+    for f in (fast, slow):
+        np.testing.assert_array_equal(f.u, du.cpu().numpy())
+        np.testing.assert_array_equal(f.v, dv.cpu().numpy())
