@@ -17,6 +17,7 @@ import csv
 import math
 from dataclasses import dataclass
 from pathlib import Path
+from fractions import Fraction
 from itertools import combinations
 
 import numpy as np
@@ -83,8 +84,10 @@ def _tets_around(face, H, W, T):
                             yield tet
 
 
-def trajectory_graph(faces, H, W, T):
-    """(edges, n_components) of the crossed-face graph (tracking.py:75-141)."""
+def _link(faces, H, W, T):
+    """(positives, edges, adj, find) of the crossed-face graph: every tet
+    around a crossed face contributes the edge joining its two crossed
+    faces (tracking.py:75-106)."""
     positives = set(faces)
     edges = set()
     seen = set()
@@ -99,7 +102,7 @@ def trajectory_graph(faces, H, W, T):
                 raise TopologyError(
                     f"tet {tet} has {len(crossed)} crossed faces (expected 2)")
             edges.add(tuple(sorted(crossed)))
-    degree = {f: 0 for f in positives}
+    adj = {f: [] for f in positives}
     parent = {f: f for f in positives}
 
     def find(x):
@@ -108,17 +111,159 @@ def trajectory_graph(faces, H, W, T):
             x = parent[x]
         return x
 
-    for f, g in edges:
-        degree[f] += 1
-        degree[g] += 1
+    for f, g in sorted(edges):
+        adj[f].append(g)
+        adj[g].append(f)
         rf, rg = find(f), find(g)
         if rf != rg:
             parent[rg] = rf
-    for f, d in degree.items():
-        if d > 2:
-            raise TopologyError(f"face {f} has degree {d}")
-    n_comp = len({find(f) for f in positives})
-    return frozenset(edges), n_comp
+    for f, nb in adj.items():
+        if len(nb) > 2:
+            raise TopologyError(f"face {f} has degree {len(nb)}")
+    return positives, edges, adj, find
+
+
+def trajectory_graph(faces, H, W, T):
+    """(edges, n_components) of the crossed-face graph (tracking.py:75-141)."""
+    positives, edges, _, find = _link(faces, H, W, T)
+    return frozenset(edges), len({find(f) for f in positives})
+
+
+def ordered_components(faces, H, W, T):
+    """(edges, chains, loops): each component as an ordered face chain,
+    components sorted by their first face (tracking.py:108-139).
+
+    A path starts at its smaller endpoint, as in the reference.  A closed
+    loop starts at its smallest face; the reference then steps to whichever
+    neighbour its adjacency list (built by iterating a Python set) holds
+    first, so its loop direction is an artefact of set iteration order --
+    here a loop steps to the smaller neighbour, which makes the order a
+    function of the face set alone.  Node and edge sets, paths, and each
+    loop's start and cyclic order match the reference; a loop may come out
+    reversed.
+    """
+    positives, edges, adj, find = _link(faces, H, W, T)
+    groups = {}
+    for f in sorted(positives):
+        groups.setdefault(find(f), []).append(f)
+    chains, loops = [], []
+    for members in groups.values():
+        ends = [f for f in members if len(adj[f]) <= 1]   # members sorted
+        is_loop = not ends
+        start = ends[0] if ends else members[0]
+        chain, prev, cur = [start], None, start
+        while True:
+            nxt = None
+            for g in sorted(adj[cur]):
+                if g != prev and (g != start or len(chain) > 2):
+                    nxt = g
+                    break
+            if nxt is None or nxt == start:
+                break
+            chain.append(nxt)
+            prev, cur = cur, nxt
+        if len(chain) != len(members):
+            raise TopologyError("component is not a simple path or cycle")
+        chains.append(chain)
+        loops.append(is_loop)
+    order = sorted(range(len(chains)), key=lambda k: chains[k][0])
+    return (frozenset(edges), [chains[k] for k in order],
+            [loops[k] for k in order])
+
+
+def crossing_point(face, fixed, H, W, dx=1.0, dy=1.0, dt=1.0):
+    """(x, y, t) of the zero crossing on a positive face: the origin's exact
+    rational barycentric coordinates in (u, v) applied to the vertices'
+    (j, i, t) (predicates.py:125-135, 304-318).  `fixed` maps a vertex id
+    to its fixed-point (u, v)."""
+    a, b, c = face
+    (ua, va), (ub, vb), (uc, vc) = fixed[a], fixed[b], fixed[c]
+    d_ab = ua * vb - va * ub
+    d_bc = ub * vc - vb * uc
+    d_ca = uc * va - vc * ua
+    df = d_ab + d_bc + d_ca
+    if df == 0:
+        raise TopologyError(f"degenerate positive face {face}")
+    hw = H * W
+    sx = sy = st = 0
+    for w, num in ((a, d_bc), (b, d_ca), (c, d_ab)):
+        t, r = divmod(w, hw)
+        i, j = divmod(r, W)
+        sx += num * j
+        sy += num * i
+        st += num * t
+    return (float(Fraction(sx, df)) * dx, float(Fraction(sy, df)) * dy,
+            float(Fraction(st, df)) * dt)
+
+
+@dataclass
+class TrajectoryGraph:
+    """tracking.py:44-56."""
+    nodes: dict           # face -> (x, y, t) crossing position
+    edges: frozenset      # sorted face pairs
+    components: list      # ordered face chains
+    loops: list           # bool per component
+
+    @property
+    def n_components(self) -> int:
+        return len(self.components)
+
+    def component_points(self, k: int):
+        return [self.nodes[f] for f in self.components[k]]
+
+
+def trajectories_from_faces(faces, fixed, H, W, T, dx=1.0, dy=1.0,
+                            dt=1.0) -> TrajectoryGraph:
+    """Host half of extract_trajectories: link `faces` and place their
+    crossing points from the vertices' fixed-point values `fixed`."""
+    edges, chains, loops = ordered_components(faces, H, W, T)
+    nodes = {fc: crossing_point(fc, fixed, H, W, dx, dy, dt) for fc in faces}
+    return TrajectoryGraph(nodes=nodes, edges=edges, components=chains,
+                           loops=loops)
+
+
+def extract_trajectories(f: FieldSeries, dx=None, dy=None, dt=None,
+                         scale: float | None = None) -> TrajectoryGraph:
+    """Critical-point trajectories of `f` (tracking.py:75-141 over
+    to_fixed(f)): the positive faces come from the device analysis kernel
+    at the automatic fixed-point scale (or `scale`); the fixed-point values
+    of their vertices are gathered and rounded on the device; linking and
+    the exact crossing points run on the host over that sparse set."""
+    import torch
+    H, W, T = f.H, f.W, f.T
+    dx = f.dx if dx is None else dx
+    dy = f.dy if dy is None else dy
+    dt = f.dt if dt is None else dt
+    du, dv = to_device(f.u), to_device(f.v)
+    if scale is None:
+        _, _, ma = device_range(du, dv)
+        scale = scale_for(ma)
+    faces = _positive_faces(face_mask_float(H, W, T, du, dv, scale, host=False),
+                            H, W, T)
+    ids = sorted({w for fc in faces for w in fc})
+    fixed = {}
+    if ids:
+        idx = torch.as_tensor(ids, dtype=torch.int64, device=du.device)
+
+        def rha(x):   # field.py:295-297, in float64 on the device
+            x = x.double() * scale
+            return (torch.sign(x) * torch.floor(torch.abs(x) + 0.5)).to(torch.int64)
+
+        fixed = {w: (uu, vv) for w, uu, vv in
+                 zip(ids, rha(du[idx]).cpu().tolist(), rha(dv[idx]).cpu().tolist())}
+    return trajectories_from_faces(faces, fixed, H, W, T, dx, dy, dt)
+
+
+def write_trajectory_csv(graph: TrajectoryGraph, path) -> None:
+    """component id, ordered crossing points, loop flag (tracking.py:271-280)."""
+    with Path(path).open("w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["component", "x", "y", "t", "loop"])
+        for k, chain in enumerate(graph.components):
+            flag = int(graph.loops[k])
+            for fc in chain:
+                x, y, t = graph.nodes[fc]
+                w.writerow([k, f"{x:.9g}", f"{y:.9g}", f"{t:.9g}", flag])
 
 
 # ------------------------------------------------------------------ verify

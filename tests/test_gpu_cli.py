@@ -101,3 +101,15 @@ def test_stats_writes_distribution_csvs(workspace, runner):
     assert 0.0 <= float(kv["overflow_rate"]) <= 1.0
     assert pmf.read_text().startswith("magnitude,pmf,ccdf")
     assert runs.read_text().startswith("run_length,ccdf")
+
+
+def test_track_writes_trajectory_csv(workspace, runner):
+    tmp, prefix = workspace
+    out = tmp / "traj.csv"
+    res = runner.invoke(main, ["track", "--input", str(prefix),
+                               "--out", str(out)])
+    assert res.exit_code == 0, res.output
+    n = int(_kv(res.output)["components"])
+    rows = out.read_text().strip().splitlines()
+    assert rows[0] == "component,x,y,t,loop"
+    assert n > 0 and len({r.split(",")[0] for r in rows[1:]}) == n
