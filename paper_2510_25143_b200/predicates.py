@@ -57,13 +57,17 @@ def mask_to_faces(mask, H, W, T):
     hw = H * W
     sl, sb = set(), set()
     mask = np.asarray(mask).view(np.uint16)
-    for an in np.flatnonzero(mask).tolist():
-        m = int(mask[an])
-        for c in range(12):
-            if m >> c & 1:
-                tri = tuple(an + dt * hw + di * W + dj
-                            for dt, di, dj in FACE_CLASS_OFFSETS[c])
-                (sl if c < 2 else sb).add(tri)
+    nz = np.flatnonzero(mask)
+    bits = mask[nz]
+    # class-major, anchors ascending: the insertion order of the reference's
+    # build_critical_face_set (mesh.py:91-128 class order), so the sets'
+    # iteration order -- which the reference's trajectory linking inherits
+    # (tracking.py:80-101) -- is the same
+    for c in range(12):
+        offs = [dt * hw + di * W + dj for dt, di, dj in FACE_CLASS_OFFSETS[c]]
+        dst = sl if c < 2 else sb
+        for an in nz[(bits >> c) & 1 == 1].tolist():
+            dst.add((an + offs[0], an + offs[1], an + offs[2]))
     return frozenset(sl), frozenset(sb)
 
 

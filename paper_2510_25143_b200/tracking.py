@@ -88,7 +88,7 @@ def _link(faces, H, W, T):
     """(positives, edges, adj, find) of the crossed-face graph: every tet
     around a crossed face contributes the edge joining its two crossed
     faces (tracking.py:75-106)."""
-    positives = set(faces)
+    positives = faces if isinstance(faces, (set, frozenset)) else set(faces)
     edges = set()
     seen = set()
     for f in positives:
@@ -111,7 +111,7 @@ def _link(faces, H, W, T):
             x = parent[x]
         return x
 
-    for f, g in sorted(edges):
+    for f, g in edges:
         adj[f].append(g)
         adj[g].append(f)
         rf, rg = find(f), find(g)
@@ -133,14 +133,12 @@ def ordered_components(faces, H, W, T):
     """(edges, chains, loops): each component as an ordered face chain,
     components sorted by their first face (tracking.py:108-139).
 
-    A path starts at its smaller endpoint, as in the reference.  A closed
-    loop starts at its smallest face; the reference then steps to whichever
-    neighbour its adjacency list (built by iterating a Python set) holds
-    first, so its loop direction is an artefact of set iteration order --
-    here a loop steps to the smaller neighbour, which makes the order a
-    function of the face set alone.  Node and edge sets, paths, and each
-    loop's start and cyclic order match the reference; a loop may come out
-    reversed.
+    A path starts at its smaller endpoint, a closed loop at its smallest
+    face, as in the reference.  A loop's direction is the first neighbour in
+    its start face's adjacency list, which the reference fills by iterating
+    Python sets; `faces` built by predicates.mask_to_faces (the reference's
+    insertion order) and the same set operations here reproduce that order,
+    so the chains match the reference's exactly (tests/test_track_cpu.py).
     """
     positives, edges, adj, find = _link(faces, H, W, T)
     groups = {}
@@ -154,7 +152,7 @@ def ordered_components(faces, H, W, T):
         chain, prev, cur = [start], None, start
         while True:
             nxt = None
-            for g in sorted(adj[cur]):
+            for g in adj[cur]:
                 if g != prev and (g != start or len(chain) > 2):
                     nxt = g
                     break
