@@ -74,3 +74,65 @@ def test_replicas_gloo_world2():
     assert all(r[3] == float(sum(map(len, blobs))) for r in res)
     for rank, blob in enumerate(blobs):                 # replicas independent
         assert blob == _archive_bytes(rank)
+
+
+# ---------------------------------------------- row bands (bands.py, §8e)
+
+def _band_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    from paper_2510_25143_b200 import bands, synth
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        H, W, T, u, v = synth.generate(1, 37, 20, 3)
+        r0, r1 = bands.band_rows(H, rank, world)
+        h0, h1 = bands.halo_rows(H, r0, r1)
+        ub = u.reshape(T, H, W)[:, r0:r1].astype(np.float64)
+        vb = v.reshape(T, H, W)[:, r0:r1].astype(np.float64)
+        # the band's own (min, max, max|x|) -- on the device in the product
+        # path (vfcp_value_range); numpy stands in here
+        lo = float(min(ub.min(), vb.min()))
+        hi = float(max(ub.max(), vb.max()))
+        ma = float(max(np.abs(ub).max(), np.abs(vb).max()))
+        eps, S = bands.band_scale(lo, hi, ma, 1e-2, True, dist, device="cpu")
+        q.put((rank, (r0, r1, h0, h1), eps, S))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bands_gloo_world2():
+    import torch.multiprocessing as mp
+    from paper_2510_25143_b200 import bands, synth
+    from paper_2510_25143_b200.field import scale_for
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, 2, port, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    H, W, T, u, v = synth.generate(1, 37, 20, 3)
+    x = np.concatenate([u, v]).astype(np.float64)
+    eps = 1e-2 * (float(x.max()) - float(x.min()))
+    S = scale_for(float(np.abs(x).max()))
+    assert [r[1][:2] for r in res] == [(0, 19), (19, 37)]
+    assert [r[1][2:] for r in res] == [(0, 20), (18, 37)]
+    assert all(r[2] == eps and r[3] == S for r in res)
+
+
+def test_band_rows_partition():
+    from paper_2510_25143_b200 import bands
+    for H in (2, 7, 64, 8192):
+        for world in (1, 2, 3, 8):
+            rows = [bands.band_rows(H, r, world) for r in range(world)]
+            assert rows[0][0] == 0 and rows[-1][1] == H
+            assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+            sizes = [b - a for a, b in rows]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        bands.band_rows(8, 2, 2)
