@@ -86,3 +86,39 @@ def analyze_band(u_band, v_band, H: int, W: int, T: int, r0: int, r1: int,
         codes.data_ptr(), ld.data_ptr(), _lib.ptr(None), row.data_ptr(),
         _lib.stream_ptr()), "analyze (band)")
     return codes.view(T, Hb, W)[:, r0 - h0:r1 - h0]
+
+
+def face_mask_band(u_band, v_band, H: int, W: int, T: int, r0: int, r1: int,
+                   scale: float):
+    """12-bit positive-face mask i16[T, r1 - r0, W] of the faces anchored in
+    band rows [r0, r1) (the K7 mask of `verify`, tracking.py:170-195).  A
+    face spans its anchor row and the row below, so the band needs only
+    the halo row below: `u_band`/`v_band` hold rows [r0, min(H, r1 + 1)) of
+    every frame.  Per-band flipped-face counts then add up across ranks
+    (one SUM all-reduce of fc_t, fc_s)."""
+    from .predicates import face_mask_float
+    h1 = min(H, r1 + 1)
+    du, dv = to_device(u_band), to_device(v_band)
+    if du.numel() != (h1 - r0) * W * T or dv.numel() != du.numel():
+        raise ValueError("band arrays must hold rows [r0, r1 + 1) of every frame")
+    m = face_mask_float(h1 - r0, W, T, du, dv, scale, host=False)
+    return m.view(T, h1 - r0, W)[:, :r1 - r0]
+
+
+def flipped_faces(mask_a, mask_b):
+    """(fc_t, fc_s) between two masks of the same faces (slice classes are
+    bits 0-1, slab classes bits 2-11), counted on the device."""
+    import torch
+    x = (mask_a.to(torch.int32) ^ mask_b.to(torch.int32)) & 0xFFF
+    pc = [((x >> b) & 1).sum() for b in range(12)]
+    return int((pc[0] + pc[1]).item()), int(sum(pc[2:]).item())
+
+
+def sum_counts(counts, dist=None, device="cuda"):
+    """Whole-field (fc_t, fc_s) from per-band counts: one SUM all-reduce."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return tuple(int(c) for c in counts)
+    import torch
+    t = torch.tensor(list(counts), dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return tuple(int(c) for c in t.tolist())

@@ -57,3 +57,56 @@ def test_band_codes_match_whole_field_large(world):
             np.ascontiguousarray(v.reshape(T, H, W)[:, r0:r1]).reshape(-1)))
     assert (min(r[0] for r in rng), max(r[1] for r in rng),
             max(r[2] for r in rng)) == (lo, hi, ma)
+
+
+def _rows(a, T, H, W, r0, r1):
+    return np.ascontiguousarray(a.reshape(T, H, W)[:, r0:r1]).reshape(-1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 6])
+def test_band_face_masks_and_flip_counts(world):
+    """Band masks tile the whole-field mask (and the reference's face set on
+    a golden field); per-band flipped-face counts between an original and
+    a perturbed reconstruction sum to verify()'s fc_t / fc_s."""
+    import torch
+    from paper_2510_25143_b200 import FieldSeries, verify
+    from paper_2510_25143_b200.predicates import face_mask_float
+    g = load_golden("int3")
+    H, W, T = int(g["H"]), int(g["W"]), int(g["T"])
+    S = float(g["scale"])
+    whole = face_mask_float(H, W, T, torch.as_tensor(g["u"]).cuda().double(),
+                            torch.as_tensor(g["v"]).cuda().double(), S,
+                            host=False).view(T, H, W)
+    ref = np.zeros(H * W * T, np.uint16)
+    ref[g["mask_anchor"]] = g["mask_bits"]
+    assert np.array_equal(whole.cpu().numpy().view(np.uint16).reshape(-1), ref)
+    world = min(world, H)
+    parts = []
+    for rank in range(world):
+        r0, r1 = bands.band_rows(H, rank, world)
+        h1 = min(H, r1 + 1)
+        parts.append(bands.face_mask_band(_rows(g["u"], T, H, W, r0, h1),
+                                          _rows(g["v"], T, H, W, r0, h1),
+                                          H, W, T, r0, r1, S))
+    assert torch.equal(torch.cat(parts, dim=1), whole)
+
+    H, W, T, u, v = synth.generate(1, 200, 160, 4)
+    rng = np.random.default_rng(5)
+    ur = (u + rng.normal(0, 2e-3, u.shape)).astype(np.float32)
+    vr = (v + rng.normal(0, 2e-3, v.shape)).astype(np.float32)
+    S = scale_for(max(device_range(u, v)[2], device_range(ur, vr)[2]))
+    counts = [0, 0]
+    for rank in range(world):
+        r0, r1 = bands.band_rows(H, rank, world)
+        h1 = min(H, r1 + 1)
+        ma_ = bands.face_mask_band(_rows(u, T, H, W, r0, h1),
+                                   _rows(v, T, H, W, r0, h1), H, W, T, r0, r1, S)
+        mb_ = bands.face_mask_band(_rows(ur, T, H, W, r0, h1),
+                                   _rows(vr, T, H, W, r0, h1), H, W, T, r0, r1, S)
+        ct, cs = bands.flipped_faces(ma_, mb_)
+        counts[0] += ct
+        counts[1] += cs
+    rep = verify(FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v),
+                 FieldSeries(H, W, T, 1.0, 1.0, 1.0, ur, vr), scale=S)
+    assert tuple(counts) == (rep.fc_t, rep.fc_s)
+    assert rep.fc_t + rep.fc_s > 0

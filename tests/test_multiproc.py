@@ -96,7 +96,8 @@ def _band_worker(rank, world, port, q):
         hi = float(max(ub.max(), vb.max()))
         ma = float(max(np.abs(ub).max(), np.abs(vb).max()))
         eps, S = bands.band_scale(lo, hi, ma, 1e-2, True, dist, device="cpu")
-        q.put((rank, (r0, r1, h0, h1), eps, S))
+        fc = bands.sum_counts((3 + rank, 10 * rank), dist, device="cpu")
+        q.put((rank, (r0, r1, h0, h1), eps, S, fc))
     finally:
         dist.destroy_process_group()
 
@@ -123,6 +124,7 @@ def test_bands_gloo_world2():
     assert [r[1][:2] for r in res] == [(0, 19), (19, 37)]
     assert [r[1][2:] for r in res] == [(0, 20), (18, 37)]
     assert all(r[2] == eps and r[3] == S for r in res)
+    assert all(r[4] == (7, 10) for r in res)          # fc_t, fc_s summed
 
 
 def test_band_rows_partition():
