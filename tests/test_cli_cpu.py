@@ -117,3 +117,16 @@ def test_residual_stats_csv(tmp_path):
     s.write_runs_csv(runs)
     assert pmf.read_text().splitlines()[0] == "magnitude,pmf,ccdf"
     assert runs.read_text().startswith("run_length,ccdf")
+
+
+def test_track_missing_input_fails(runner, tmp_path):
+    res = runner.invoke(main, ["track", "--input", str(tmp_path / "nope"),
+                               "--out", str(tmp_path / "t.csv")])
+    assert res.exit_code == 1
+    assert "missing field file" in res.output
+    assert not (tmp_path / "t.csv").exists()
+
+
+def test_track_requires_out(runner, tmp_path):
+    res = runner.invoke(main, ["track", "--input", str(tmp_path / "f")])
+    assert res.exit_code == 2          # click usage error, as the reference
