@@ -234,8 +234,22 @@ static const int CLS_LIM[12][3] = {
  * anchor vertex (mask[anchor] bit c set <=> face of class c positive).
  * ebounds.py:190-206 derive_all -> xi, then codec.py:338 codes.
  * Outputs (any may be NULL): mask u16[N], xi i64[N]. */
+void or_analyze_window(int H, int W, int T, const int32_t *u,
+                       const int32_t *v, int64_t tau, int ta0, int ta1,
+                       uint16_t *mask, int64_t *xi);
 void or_analyze(int H, int W, int T, const int32_t *u, const int32_t *v,
                 int64_t tau, uint16_t *mask, int64_t *xi) {
+    or_analyze_window(H, W, T, u, v, tau, 0, T, mask, xi);
+}
+
+/* The same scan restricted to anchors in frames [ta0, ta1) of a window of
+ * T frames (window-local ids keep the reference's id order, which is all
+ * SoS uses: SURVEY V5).  The xi of a frame-t vertex needs the anchors of
+ * frames t-1 and t; the mask of frame t's anchors needs frames t, t+1.
+ * Used by the full-size parity driver (tests/parity_full.py). */
+void or_analyze_window(int H, int W, int T, const int32_t *u,
+                       const int32_t *v, int64_t tau, int ta0, int ta1,
+                       uint16_t *mask, int64_t *xi) {
     int64_t hw = (int64_t)H * W, n = hw * T;
     if (mask) memset(mask, 0, sizeof(uint16_t) * n);
     if (xi) for (int64_t k = 0; k < n; k++) xi[k] = tau;
@@ -249,7 +263,7 @@ void or_analyze(int H, int W, int T, const int32_t *u, const int32_t *v,
         int64_t oa = CLS_OFF[c][0][0] * hw + CLS_OFF[c][0][1] * W + CLS_OFF[c][0][2];
         int64_t ob = CLS_OFF[c][1][0] * hw + CLS_OFF[c][1][1] * W + CLS_OFF[c][1][2];
         int64_t oc = CLS_OFF[c][2][0] * hw + CLS_OFF[c][2][1] * W + CLS_OFF[c][2][2];
-        for (int t = 0; t < tl; t++)
+        for (int t = ta0; t < tl && t < ta1; t++)
             for (int i = 0; i < il; i++)
                 for (int j = 0; j < jl; j++) {
                     int64_t an = t * hw + (int64_t)i * W + j;

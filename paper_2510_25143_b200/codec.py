@@ -536,6 +536,21 @@ class _SideDecode:
         return self._out
 
 
+def _clamp_codes(blob):
+    """Codes of a q_xi section whose alphabet exceeds 32, mapped to the
+    code with the same ladder step (codec.py:427-431 eq = tau >> min(code,
+    K_MAX), 0 for code 31): 31 stays 31, anything else above K_MAX becomes
+    K_MAX.  Decoded wide (uint16 on the device, or int64 on the host for an
+    alphabet past 2^16), so no code aliases to 31 by truncation."""
+    import torch
+    if huffman.alphabet_of(blob) <= 65536:
+        c = huffman.decode_device(blob, np.uint16).to(torch.int32)
+    else:
+        c = torch.from_numpy(huffman.decode(blob, np.int64)).cuda()
+    c = torch.where(c == CODE_LOSSLESS, c, c.clamp(max=K_MAX))
+    return c.to(torch.uint8)
+
+
 def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
                       qd=None, ll=None, modes=None, ld=None, host_out=None):
     """codec.py:401-453 on device.  Returns (out_u, out_v, fix_u, fix_v)
@@ -552,7 +567,12 @@ def decompress_device(a: Archive, want_fixed: bool = False, codes=None,
         # symbol section also to decode, the codes go to a host thread on a
         # side stream and both sections decode concurrently (errors are
         # raised in the sequential order: codes first)
-        if qd is None and cfg.radius <= 32768:
+        if huffman.alphabet_of(a.q_xi) > EB_ALPHABET:
+            # a q_xi section with codes >= 32 (never written by compress):
+            # the reference reads them through tau >> min(code, K_MAX), so
+            # every code other than 31 above K_MAX acts as K_MAX
+            codes = _clamp_codes(a.q_xi)
+        elif qd is None and cfg.radius <= 32768:
             th = _SideDecode(a.q_xi, np.uint8)
             try:
                 qd_pre = huffman.decode_device(a.q_d, np.uint16)

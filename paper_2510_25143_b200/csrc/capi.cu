@@ -217,6 +217,24 @@ __global__ void widen_kernel(const I* a, const I* b, int64_t n, int64_t* oa,
   }
 }
 
+// Fast path, optional recon output: recon(t) = fixed(orig(t)) + err(t) as
+// int64 [2][T][H][W] (the layout of the generic path's widen_kernel).
+template <typename F>
+__global__ void recon_out_kernel(const F* __restrict__ u, const F* __restrict__ v,
+                                 const int32_t* __restrict__ eu,
+                                 const int32_t* __restrict__ ev, int H, int W,
+                                 int Wp, double S, int t, int64_t N,
+                                 int64_t* __restrict__ recon) {
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < HW;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / W, j = k - i * W, m = i * Wp + j;
+    const int64_t g = (int64_t)t * HW + k;
+    recon[g] = (int64_t)fixed_t(u[g], S) + eu[m];
+    recon[N + g] = (int64_t)fixed_t(v[g], S) + ev[m];
+  }
+}
+
 template <typename F, typename I, typename SYM>
 int encode_impl(const vfcp_params* p, const F* u, const F* v,
                 const uint8_t* codes, const int64_t* qd_row_off, SYM* qd,
@@ -504,8 +522,8 @@ struct HostOut {
 template <typename F>
 int encode_fast(const vfcp_params* p, const F* u, const F* v,
                 const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
-                uint8_t* modes, int32_t* row_ll, cudaStream_t st,
-                bool* overflowed, HostOut* ho) {
+                uint8_t* modes, int32_t* row_ll, int64_t* recon,
+                cudaStream_t st, bool* overflowed, HostOut* ho) {
   const int H = p->H, W = p->W, T = p->T;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
@@ -585,6 +603,12 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.frame_tag = (uint32_t)t + 1u;
     LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
     if (bio.stamps && t == 1) print_chain_stamps(bio, st);
+    if (recon)
+      LAUNCH(K_AUX, st,
+             (recon_out_kernel<F><<<1184, 256, 0, st>>>(
+                  u, v, ecur, ecur + plane, H, W, Wp, p->scale, t,
+                  (int64_t)H * W * T, recon),
+              cudaGetLastError()));
     {
       int rch = ho->frame(t, qd, st);
       if (rch) return rch;
@@ -703,17 +727,17 @@ int encode_common(const vfcp_params* p, const void* u, const void* v,
                   int dtype, const uint8_t* codes, const int64_t* qd_row_off,
                   void* qd, uint8_t* modes, double* scores, int32_t* row_ll,
                   int64_t* recon, HostOut* ho, cudaStream_t st) {
-  if (fast_ok(p) && !scores && !recon && !getenv("VFCP_SLOW_PATH")) {
+  if (fast_ok(p) && !scores && !getenv("VFCP_SLOW_PATH")) {
     bool ovf = false;
     int rc2 = ho->init(p->T);
     if (rc2) return rc2;
     rc2 = dtype == VFCP_F32
               ? encode_fast<float>(p, (const float*)u, (const float*)v,
                                    codes, qd_row_off, (uint16_t*)qd,
-                                   modes, row_ll, st, &ovf, ho)
+                                   modes, row_ll, recon, st, &ovf, ho)
               : encode_fast<double>(p, (const double*)u, (const double*)v,
                                     codes, qd_row_off, (uint16_t*)qd,
-                                    modes, row_ll, st, &ovf, ho);
+                                    modes, row_ll, recon, st, &ovf, ho);
     if (rc2) return rc2;
     rc2 = ho->finish();
     if (rc2 || !ovf) return rc2;

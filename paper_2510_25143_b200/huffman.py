@@ -172,6 +172,11 @@ def encode_device(symbols, alphabet_size: int, window_base: int = 0) -> bytes:
     return encode_device_many([(symbols, alphabet_size, window_base)])[0].result()
 
 
+def alphabet_of(blob) -> int:
+    """The alphabet size recorded in a section's header."""
+    return _HDR.unpack_from(memoryview(blob), 0)[0]
+
+
 def decode(blob, out_dtype=np.int64) -> np.ndarray:
     """Inverse of encode(); raises ValueError on a corrupt stream."""
     blob = memoryview(blob)

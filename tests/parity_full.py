@@ -1,0 +1,470 @@
+"""Full-size parity of the GPU path against the CPU oracle (test harness).
+
+North-star acceptance test (BASELINE.json): bit-exact codes / l_d / face
+set / modes / symbols / ll / reconstruction and identical trajectories
+versus the CPU oracle on the BASELINE configs at their full sizes.
+
+The stock oracle run of config 5 (8192 x 8192 x 16) is sequential over
+2^30 vertices; this driver checks the same thing frame-parallel, by
+induction over frames (the reference's orchestration, codec.py:345-376,
+makes frame t depend on the past only through recon(t-1)):
+
+* analysis (predicates.py:290-301, ebounds.py:190-206, codec.py:338):
+  frame t's codes / l_d / face mask need only frames t-1, t, t+1; the
+  oracle analyses that window with window-local ids (SoS compares ids
+  only by order: SURVEY V5) -- ``or_analyze_window``;
+* encode (mop.py:154-173, codec.py:118-164): with prev = R(t-1), the
+  GPU's reconstruction of frame t-1 (0 for t = 0), the oracle's
+  ``or_score_frame`` + ``or_encode_frame`` must give exactly the GPU's
+  modes, symbols, ll and R(t).  If that holds for every t, then by
+  induction on t the GPU streams equal the oracle's sequential run and R
+  is the oracle's reconstruction;
+* decode (codec.py:167-206): ``or_decode_frame`` from prev = R(t-1) and
+  the GPU's streams of frame t must give R(t) again;
+* verify (tracking.py:170-195): the oracle's face mask of R at the
+  original's scale equals the oracle's face mask of the original (so
+  fc_t = fc_s = 0 and the trajectory graphs are the same, since they are
+  a function of the crossed-face set), and the GPU's ``verify`` agrees.
+
+The GPU side goes through the public API: ``compress_device`` for the raw
+streams (+ face mask), ``compress()`` for the Archive (its entropy-coded
+sections are decoded back on the device and compared with the streams),
+``decompress_device`` for the fixed-point and float64 reconstruction,
+``tracking.verify`` for the report.
+
+The oracle (oracle/cpu_oracle.py, oracle/vfcp_oracle.c) is the checker
+only; its C calls release the GIL, so frames run on a thread pool over
+the box's host cores.
+
+    python tests/parity_full.py --config 5 --eps 1e-3 --out report.json
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import ctypes
+import hashlib
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+# BASELINE.json configs and their eps lists (relative to the value range)
+BASELINE_EPS = {1: [1e-2], 2: [1e-3], 3: [1e-2, 1e-3], 4: [1e-3],
+                5: [1e-2, 1e-3, 1e-4]}
+
+
+def _sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()
+
+
+def _first_diff(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape:
+        return f"length {a.size} vs {b.size}"
+    k = int(np.flatnonzero(a != b)[0])
+    return f"index {k}: oracle {a[k]} gpu {b[k]}"
+
+
+def oracle_scale(u, v, T, HW):
+    """choose_scale + to_fixed's retry loop (field.py:300-336), per frame
+    so no N-sized temporary is needed."""
+    from oracle import cpu_oracle as O
+    L = O.lib()
+    ma = max(float(np.abs(u.astype(np.float64, copy=False)).max())
+             if u.dtype == np.float64 else float(np.abs(u).max()),
+             float(np.abs(v).max()))
+    s = O.choose_scale(ma)
+    tmp = np.empty(HW, np.int32)
+    while True:
+        m = 0
+        for t in range(T):
+            for x in (u, v):
+                xs = np.ascontiguousarray(x[t * HW:(t + 1) * HW])
+                m = max(m, L.or_to_fixed(xs.ctypes.data, O._dtype_code(xs),
+                                         HW, s, tmp))
+        if m < O.FIXED_LIMIT:
+            return s
+        s /= 2.0
+
+
+class Ctx:
+    """Everything a frame job reads (shared by the threads, read-only)."""
+
+
+def frame_job(c: Ctx, t: int) -> dict:
+    from oracle import cpu_oracle as O
+    L = O.lib()
+    H, W, T, HW = c.H, c.W, c.T, c.HW
+    cfg = c.cfg
+    t_start = time.perf_counter()
+    res = {"t": t}
+    bad = []
+    # ---- analysis on the window [t-1, t+1]
+    w0, w1 = max(0, t - 1), min(T, t + 2)
+    Tw = w1 - w0
+    uf = np.empty(Tw * HW, np.int32)
+    vf = np.empty(Tw * HW, np.int32)
+    for x, out in ((c.u, uf), (c.v, vf)):
+        xs = np.ascontiguousarray(x[w0 * HW:w1 * HW])
+        L.or_to_fixed(xs.ctypes.data, O._dtype_code(xs), Tw * HW, c.S, out)
+    xi = np.empty(Tw * HW, np.int64)
+    mask = np.empty(Tw * HW, np.uint16)
+    L.or_analyze_window(H, W, Tw, uf, vf, int(c.tau), max(0, t - 1) - w0,
+                        t - w0 + 1, mask.ctypes.data, xi.ctypes.data)
+    lt = t - w0
+    sl = slice(lt * HW, (lt + 1) * HW)
+    xi_t = np.ascontiguousarray(xi[sl])
+    del xi
+    codes = np.empty(HW, np.uint8)
+    ld = np.empty(HW, np.uint8)
+    L.or_codes(xi_t, HW, int(c.tau), codes, ld)
+    del xi_t
+    g = slice(t * HW, (t + 1) * HW)
+    mask_o = mask[sl].copy()
+    del mask
+    if not np.array_equal(codes, c.g_codes[g]):
+        bad.append(("codes", _first_diff(codes, c.g_codes[g])))
+    g_ld = np.unpackbits(c.g_ld_bytes[(t * HW) // 8:((t + 1) * HW + 7) // 8])
+    off = (t * HW) % 8
+    if not np.array_equal(ld, g_ld[off:off + HW]):
+        bad.append(("l_d", _first_diff(ld, g_ld[off:off + HW])))
+    if not np.array_equal(mask_o, c.g_mask[g]):
+        bad.append(("mask", _first_diff(mask_o, c.g_mask[g])))
+    res["n_lossless"] = int(ld.sum())
+    # quirk V7 (codec.py:338-341): code 31 from the ladder at xi > 0
+    res["v7"] = int(((codes == O.CODE_LOSSLESS) & (ld == 0)).sum())
+    res["n_positive_faces"] = int(np.unpackbits(mask_o.view(np.uint8)).sum())
+    # ---- modes + encode of frame t from prev = R(t-1)
+    uo = uf[sl].astype(np.int64)
+    vo = vf[sl].astype(np.int64)
+    del uf, vf
+    eq = np.where(codes == O.CODE_LOSSLESS, 0,
+                  int(c.tau) >> np.minimum(codes, O.K_MAX).astype(np.int64)
+                  ).astype(np.int64)
+    if t == 0:
+        pu = np.zeros(HW, np.int64)
+        pv = np.zeros(HW, np.int64)
+    else:
+        pu = c.R[0, t - 1].astype(np.int64)
+        pv = c.R[1, t - 1].astype(np.int64)
+    nby, nbx = c.nby, c.nbx
+    if t == 0 or c.tau == 0 or cfg.predictor == "lorenzo":
+        modes_t = np.zeros(nby * nbx, np.uint8)
+    elif cfg.predictor == "sl":
+        modes_t = np.ones(nby * nbx, np.uint8)
+    else:
+        modes_t = np.zeros(nby * nbx, np.uint8)
+        scores = np.zeros(nby * nbx * 2, np.float64)
+        L.or_score_frame(H, W, uo, vo, pu, pv, int(c.tau), int(cfg.radius),
+                         int(cfg.stride), int(cfg.bx), int(cfg.by),
+                         float(cfg.lam), 1.0 / (cfg.bx * cfg.by * 2),
+                         float(cfg.theta), c.cfl_x, c.cfl_y,
+                         float(cfg.d_max), int(cfg.n_max), modes_t, scores)
+    if t >= 1:
+        gm = c.g_modes[(t - 1) * nby * nbx:t * nby * nbx]
+        if not np.array_equal(modes_t, gm):
+            bad.append(("modes", _first_diff(modes_t, gm)))
+        res["sl_blocks"] = int(modes_t.sum())
+    cu = np.empty(HW, np.int64)
+    cv = np.empty(HW, np.int64)
+    qd = np.empty(2 * HW, np.int32)
+    ll = np.empty(2 * HW, np.int64)
+    qp = ctypes.c_int64(0)
+    lp = ctypes.c_int64(0)
+    L.or_encode_frame(H, W, uo, vo, pu, pv, cu, cv, eq, modes_t, int(t >= 1),
+                      int(cfg.by), int(cfg.bx), c.cfl_x, c.cfl_y,
+                      float(cfg.d_max), int(cfg.n_max), int(cfg.radius), qd,
+                      ctypes.byref(qp), ll, ctypes.byref(lp))
+    del uo, vo
+    q0, q1 = c.qd_off[t], c.qd_off[t + 1]
+    l0, l1 = c.ll_off[t], c.ll_off[t + 1]
+    gq = c.g_qd[q0:q1]
+    gl = c.g_ll[l0:l1]
+    if qp.value != q1 - q0 or not np.array_equal(qd[:qp.value], gq):
+        bad.append(("qd", _first_diff(qd[:qp.value], gq)))
+    if lp.value != l1 - l0 or not np.array_equal(ll[:lp.value], gl):
+        bad.append(("ll", _first_diff(ll[:lp.value], gl)))
+    res["escapes"] = int((qd[:qp.value] == 0).sum())
+    del qd, ll
+    Ru = c.R[0, t]
+    Rv = c.R[1, t]
+    if not (np.array_equal(cu, Ru) and np.array_equal(cv, Rv)):
+        bad.append(("recon", _first_diff(np.concatenate([cu, cv]),
+                                         np.concatenate([Ru, Rv]))))
+    # ---- decode of frame t from prev = R(t-1) and the GPU's streams
+    gq32 = gq.astype(np.int32)
+    glc = np.ascontiguousarray(gl, np.int64) if gl.size else np.zeros(1, np.int64)
+    qp2 = ctypes.c_int64(0)
+    lp2 = ctypes.c_int64(0)
+    L.or_decode_frame(H, W, pu, pv, cu, cv, eq, modes_t, int(t >= 1),
+                      int(cfg.by), int(cfg.bx), c.cfl_x, c.cfl_y,
+                      float(cfg.d_max), int(cfg.n_max), int(cfg.radius),
+                      gq32 if gq32.size else np.zeros(1, np.int32),
+                      ctypes.byref(qp2), glc, ctypes.byref(lp2))
+    if (qp2.value != q1 - q0 or lp2.value != l1 - l0 or
+            not (np.array_equal(cu, Ru) and np.array_equal(cv, Rv))):
+        bad.append(("decode", "oracle decode of the GPU streams != R(t)"))
+    del pu, pv, cu, cv, eq, gq32
+    # ---- verify: the reconstruction's face mask at the original's scale
+    r1 = min(T, t + 2)
+    Rw_u = np.ascontiguousarray(c.R[0, t:r1]).reshape(-1)
+    Rw_v = np.ascontiguousarray(c.R[1, t:r1]).reshape(-1)
+    mask_r = np.empty((r1 - t) * HW, np.uint16)
+    L.or_analyze_window(H, W, r1 - t, Rw_u, Rw_v, 0, 0, 1,
+                        mask_r.ctypes.data, None)
+    x = (mask_o ^ mask_r[:HW]).astype(np.uint16)
+    res["fc_t"] = int(np.unpackbits((x & 0x3).view(np.uint8)).sum())
+    res["fc_s"] = int(np.unpackbits((x & 0xFFC).view(np.uint8)).sum())
+    res["max_err_fixed"] = int(max(
+        np.abs(c.R[0, t].astype(np.int64) - fixed_frame(c, c.u, t)).max(),
+        np.abs(c.R[1, t].astype(np.int64) - fixed_frame(c, c.v, t)).max()))
+    res["bad"] = bad
+    res["seconds"] = round(time.perf_counter() - t_start, 2)
+    return res
+
+
+def fixed_frame(c, x, t):
+    from oracle import cpu_oracle as O
+    xs = np.ascontiguousarray(x[t * c.HW:(t + 1) * c.HW])
+    out = np.empty(c.HW, np.int32)
+    O.lib().or_to_fixed(xs.ctypes.data, O._dtype_code(xs), c.HW, c.S, out)
+    return out.astype(np.int64)
+
+
+def run(config: int, eps: float, predictor: str = "mop", H=None, W=None,
+        T=None, threads: int | None = None, log=print) -> dict:
+    import torch
+
+    import paper_2510_25143_b200 as vg
+    from oracle import cpu_oracle as O
+    from paper_2510_25143_b200 import codec, huffman, synth, tracking
+
+    L = O.lib()
+    L.or_analyze_window.restype = None
+    L.or_analyze_window.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    O._i32p, O._i32p, ctypes.c_int64,
+                                    ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_void_p, ctypes.c_void_p]
+    rep = {"config": config, "eps_rel": eps, "predictor": predictor}
+    t0 = time.perf_counter()
+    H, W, T, u, v = synth.generate(config, H, W, T)
+    HW = H * W
+    rep.update(H=H, W=W, T=T, N=H * W * T)
+    rep["gen_s"] = round(time.perf_counter() - t0, 1)
+    cfg = vg.Config(predictor=predictor)
+    nby, nbx = -(-H // cfg.by), -(-W // cfg.bx)
+
+    # ------------------------------------------------------------ GPU side
+    t0 = time.perf_counter()
+    du = torch.from_numpy(u).cuda()
+    dv = torch.from_numpy(v).cuda()
+    fd = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, du, dv)
+    s = codec.compress_device(fd, eps, cfg, relative=True, want_mask=True,
+                              want_recon=True)
+    S, tau, eps_abs = s.scale, s.tau, s.eps
+    host = codec.streams_to_host(s)
+    # the encoder's fixed-point reconstruction (int32 is exact: |recon| <
+    # 2^31 - 1) drives the frame induction below
+    R = np.empty((2, T, HW), np.int32)
+    rec = s.recon.view(2, T, HW)
+    assert int(rec.abs().max()) < 2 ** 31
+    R[0] = rec[0].to(torch.int32).cpu().numpy()
+    R[1] = rec[1].to(torch.int32).cpu().numpy()
+    del rec
+    s.recon = None
+    g_mask = s.mask.cpu().numpy().view(np.uint16)
+    g_codes, g_ld, g_qd, g_ll, g_modes = (host[k] for k in
+                                          ("codes", "ld", "qd", "ll", "modes"))
+    # the public compress(): archive sections == these streams
+    a = vg.compress(fd, eps, cfg, relative=True)
+    arch_ok = {}
+    dq = huffman.decode_device(a.q_xi, np.uint8)
+    arch_ok["q_xi"] = bool(torch.equal(dq, s.codes))
+    del dq
+    if cfg.radius <= 32768:
+        dq = huffman.decode_device(a.q_d, np.uint16)
+        arch_ok["q_d"] = bool(torch.equal(dq.view(torch.int16),
+                                          s.qd.view(torch.int16)))
+        del dq
+    arch_ok["l_d"] = bytes(a.l_d) == g_ld.tobytes()
+    arch_ok["lossless_stream"] = a.lossless_stream == g_ll.astype("<i8").tobytes()
+    arch_ok["mode_bitmap"] = a.mode_bitmap == np.packbits(g_modes).tobytes()
+    del s
+    torch.cuda.empty_cache()
+    # decompress: the archive decodes to the encoder's reconstruction, or
+    # (quirk V7: a vertex with xi > 0 whose ladder code is 31) raises the
+    # reference's error, as the reference's own decompress does
+    decode_error = ""
+    f64_ok = dec_equal = None
+    try:
+        out_u, out_v, fix_u, fix_v = codec.decompress_device(a, want_fixed=True)
+    except ValueError as err:
+        decode_error = str(err)
+    inv = 1.0 / S
+    if not decode_error:
+        f64_ok = bool(torch.equal(out_u, fix_u.double() * inv) and
+                      torch.equal(out_v, fix_v.double() * inv))
+        dec_equal = bool(np.array_equal(
+            fix_u.to(torch.int32).cpu().numpy().reshape(T, HW), R[0]) and
+            np.array_equal(fix_v.to(torch.int32).cpu().numpy().reshape(T, HW),
+                           R[1]))
+        del fix_u, fix_v
+    else:
+        out_u = torch.from_numpy(R[0].reshape(-1)).cuda().double() * inv
+        out_v = torch.from_numpy(R[1].reshape(-1)).cuda().double() * inv
+    rf = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, out_u, out_v)
+    vr = tracking.verify(fd, rf, None, scale=S)
+    del out_u, out_v, rf, fd, du, dv
+    torch.cuda.empty_cache()
+    rep["gpu_s"] = round(time.perf_counter() - t0, 1)
+    rep["gpu"] = {"scale": S, "tau": tau, "eps_abs": eps_abs,
+                  "archive_sections_equal_streams": arch_ok,
+                  "decode_error": decode_error,
+                  "decoder_recon_equals_encoder": dec_equal,
+                  "f64_output_equals_fixed_over_S": f64_ok,
+                  "verify": {"fc_t": vr.fc_t, "fc_s": vr.fc_s,
+                             "n_traj_orig": vr.n_traj_orig,
+                             "n_traj_recon": vr.n_traj_recon,
+                             "isomorphic": vr.isomorphic,
+                             "max_abs_err": vr.max_abs_err,
+                             "psnr": vr.psnr, "ok": vr.ok,
+                             "of": "the decoded field" if not decode_error
+                             else "the encoder's reconstruction"}}
+    log(f"[parity] cfg{config} eps {eps}: GPU side {rep['gpu_s']} s")
+
+    # --------------------------------------------------------- oracle side
+    t0 = time.perf_counter()
+    eps_o = eps * O.value_range(u, v)
+    S_o = oracle_scale(u, v, T, HW)
+    tau_o = O.tau_from_eps(eps_o, S_o)
+    rep["oracle_scalars"] = {"scale": S_o, "tau": tau_o, "eps_abs": eps_o,
+                             "equal": (S_o == S and tau_o == tau and
+                                       eps_o == eps_abs)}
+    c = Ctx()
+    c.H, c.W, c.T, c.HW, c.cfg = H, W, T, HW, cfg
+    c.S, c.tau = S_o, tau_o
+    c.cfl_x, c.cfl_y = O._cfl(1.0, 1.0, 1.0, S_o)
+    c.nby, c.nbx = nby, nbx
+    c.u, c.v = u, v
+    c.g_codes, c.g_ld_bytes, c.g_mask = g_codes, g_ld, g_mask
+    c.g_modes, c.g_ll, c.R = g_modes, g_ll, R
+    c.g_qd = g_qd
+    # per-frame offsets of the GPU streams (2 symbols per non-lossless
+    # vertex; ll = 2 per lossless vertex + 1 per escape)
+    nl = np.array([int((g_codes[t * HW:(t + 1) * HW] != 31).sum())
+                   for t in range(T)], np.int64)
+    c.qd_off = np.concatenate([[0], np.cumsum(2 * nl)])
+    esc = np.array([int((c.g_qd[c.qd_off[t]:c.qd_off[t + 1]] == 0).sum())
+                    for t in range(T)], np.int64)
+    c.ll_off = np.concatenate([[0], np.cumsum(2 * (HW - nl) + esc)])
+    sizes_ok = (c.qd_off[-1] == g_qd.size and c.ll_off[-1] == g_ll.size)
+    nthr = threads or os.cpu_count() or 1
+    # bound host memory: a frame job peaks near 100 bytes per frame pixel
+    mem = _host_mem_bytes()
+    if mem:
+        nthr = max(1, min(nthr, int(0.6 * mem) // (120 * HW) or 1))
+    rep["oracle_threads"] = nthr
+    log(f"[parity] oracle: {T} frames on {nthr} threads")
+    with cf.ThreadPoolExecutor(nthr) as ex:
+        frames = list(ex.map(lambda t: frame_job(c, t), range(T)))
+    rep["oracle_s"] = round(time.perf_counter() - t0, 1)
+    sections = {}
+    gpu_arrays = {"codes": g_codes, "l_d": g_ld, "mask": g_mask,
+                  "modes": g_modes, "qd": g_qd, "ll": g_ll, "recon": R}
+    with cf.ThreadPoolExecutor(len(gpu_arrays)) as ex:
+        shas = dict(zip(gpu_arrays, ex.map(_sha, gpu_arrays.values())))
+    for k in gpu_arrays:
+        fails = [(f["t"], d) for f in frames for (n, d) in f["bad"]
+                 if n == k or (k == "recon" and n == "decode")]
+        sections[k] = {"sha256": shas[k], "equal": not fails and sizes_ok,
+                       "first_failures": fails[:3]}
+    fc_t = sum(f["fc_t"] for f in frames)
+    fc_s = sum(f["fc_s"] for f in frames)
+    gv = rep["gpu"]["verify"]
+    rep["sections"] = sections
+    rep["oracle_verify"] = {"fc_t": fc_t, "fc_s": fc_s,
+                            "face_sets_equal": fc_t == 0 and fc_s == 0}
+    rep["stream_sizes"] = {"qd": int(g_qd.size), "ll": int(g_ll.size),
+                           "consistent": bool(sizes_ok)}
+    rep["field_stats"] = {
+        "positive_faces": sum(f["n_positive_faces"] for f in frames),
+        "lossless_vertices": sum(f["n_lossless"] for f in frames),
+        "escapes": sum(f["escapes"] for f in frames),
+        "sl_blocks": sum(f.get("sl_blocks", 0) for f in frames),
+        "blocks": (T - 1) * nby * nbx,
+        "max_err_fixed": max(f["max_err_fixed"] for f in frames),
+        "quirk_v7_vertices": sum(f["v7"] for f in frames),
+    }
+    v7 = rep["field_stats"]["quirk_v7_vertices"]
+    # the reference's decompress raises exactly when quirk V7 occurs
+    decode_ok = (decode_error == "lossless bitmap disagrees with eb codes"
+                 if v7 else (not decode_error and dec_equal and f64_ok))
+    rep["frame_seconds_max"] = max(f["seconds"] for f in frames)
+    rep["all_equal"] = bool(
+        all(sec["equal"] for sec in sections.values()) and
+        rep["oracle_scalars"]["equal"] and all(arch_ok.values()) and decode_ok
+        and gv["fc_t"] == fc_t and gv["fc_s"] == fc_s and gv["ok"]
+        and rep["field_stats"]["max_err_fixed"] <= tau_o
+        and gv["max_abs_err"] <= eps_abs)
+    log(f"[parity] cfg{config} eps {eps}: all_equal={rep['all_equal']} "
+        f"(oracle {rep['oracle_s']} s)")
+    return rep
+
+
+def _jsonable(o):
+    return o.item() if hasattr(o, "item") else str(o)
+
+
+def _host_mem_bytes():
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, nargs="+", default=[1, 2, 3, 4, 5])
+    ap.add_argument("--eps", type=float, nargs="*", default=None,
+                    help="default: the config's BASELINE eps list")
+    ap.add_argument("--predictor", default="mop")
+    ap.add_argument("--H", type=int)
+    ap.add_argument("--W", type=int)
+    ap.add_argument("--T", type=int)
+    ap.add_argument("--threads", type=int)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args(argv)
+    reports = []
+    if args.out and Path(args.out).exists():
+        reports = json.loads(Path(args.out).read_text()).get("runs", [])
+    for cfg_id in args.config:
+        for e in (args.eps or BASELINE_EPS[cfg_id]):
+            r = run(cfg_id, e, args.predictor, args.H, args.W, args.T,
+                    args.threads, log=lambda m: print(m, flush=True))
+            reports.append(r)
+            if args.out:
+                Path(args.out).write_text(json.dumps(
+                    {"runs": reports,
+                     "all_equal": all(x["all_equal"] for x in reports)},
+                    indent=1, default=_jsonable))
+            print(json.dumps({k: r[k] for k in ("config", "eps_rel", "all_equal",
+                                                "gpu_s", "oracle_s")},
+                             default=_jsonable), flush=True)
+    return 0 if all(x["all_equal"] for x in reports) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -20,6 +20,8 @@ correct implementation of the reference's codec (codec.py:321-453):
 * serialisation round trip: Archive.to_bytes -> from_bytes -> decompress
   gives the same field.
 """
+import os
+
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -56,10 +58,16 @@ def test_fullsize_properties(key):
     cfg = vg.Config()
     H, W, T = f.H, f.W, f.T
     dims = (H, W, T, 1.0, 1.0, 1.0)
-    # the block-scan path vs the per-strip path (want_recon selects it;
-    # both are oracle-exact on the small fixtures): identical streams
-    s = codec.compress_device(f, eps, cfg, relative=rel)
-    s2 = codec.compress_device(f, eps, cfg, relative=rel, want_recon=True)
+    # the block-scan path vs the per-strip path (VFCP_SLOW_PATH selects it;
+    # both are oracle-exact on the small fixtures): identical streams and
+    # reconstructions
+    s = codec.compress_device(f, eps, cfg, relative=rel, want_recon=True)
+    os.environ["VFCP_SLOW_PATH"] = "1"
+    try:
+        s2 = codec.compress_device(f, eps, cfg, relative=rel, want_recon=True)
+    finally:
+        del os.environ["VFCP_SLOW_PATH"]
+    assert torch.equal(s.recon, s2.recon)
     assert (s.scale, s.eps, s.tau) == (s2.scale, s2.eps, s2.tau)
     for name in ("codes", "ld", "qd", "ll", "modes"):
         x, y = getattr(s, name), getattr(s2, name)
