@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decompress", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="device-resident timings only (no e2e / entropy legs)")
     ap.add_argument("--ref-sample", type=int, nargs=3, default=(1024, 1024, 4))
     ap.add_argument("--cpu-sample", type=int, nargs=3, default=(2048, 2048, 4))
     args = ap.parse_args()
@@ -330,75 +332,79 @@ def main():
                "kernels_ms": {k: round(v[0] / args.steps, 3)
                               for k, v in dprof.items() if v[1]}}
 
-    # ---- end to end through the public API from pinned host buffers
-    u_pin = torch.from_numpy(u_h).pin_memory()
-    v_pin = torch.from_numpy(v_h).pin_memory()
-    f_host = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u_pin, v_pin)
-    # warm-up: the pinned host buffers of the streams come from torch's
-    # caching host allocator and are reused by the timed steps
-    for _ in range(max(1, args.warmup)):
-        host = None
-        host = codec.streams_to_host(vg.compress_device(f_host, args.eps, cfg,
-                                                        relative=True,
-                                                        host_out=True))
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(max(1, args.steps)):
-        s2 = host = None
-        s2 = vg.compress_device(f_host, args.eps, cfg, relative=True,
-                                host_out=True)
-        host = codec.streams_to_host(s2)
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
-    e2e_s = max_over_ranks(e2e_s)
-    d2h = sum(int(x.nbytes) for x in host.values())
-    # the public compress() to an Archive (device entropy stage: only the
-    # packed sections come back), same pinned host input
-    for _ in range(max(1, args.warmup)):   # warm-up (pinned / host buffers)
-        arc = None
-        arc = vg.compress(f_host, args.eps, cfg, relative=True)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(max(1, args.steps)):
-        arc = None
-        arc = vg.compress(f_host, args.eps, cfg, relative=True)
-    torch.cuda.synchronize()
-    arc_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
-    arc_bytes = sum(len(x) for x in arc.sections)
-    del arc
-    # host entropy backend (Huffman + zlib), timed on frame 0's streams
-    nq0 = 2 * (H * W) if s.qd.numel() >= 2 * H * W else s.qd.numel()
-    t0 = time.perf_counter()
-    from paper_2510_25143_b200 import huffman
-    import zlib
-    b1 = huffman.encode(host["codes"][:H * W], 32)
-    b2 = huffman.encode(host["qd"][:nq0], 2 * cfg.radius)
-    zlib.compress(b1, 6)
-    zlib.compress(b2, 6)
-    ent_s = time.perf_counter() - t0
-    # the device entropy stage (csrc/huffman_gpu.cu) on the whole field's
-    # streams, resident from the timed compress: encode and decode of the
-    # q_xi and q_d sections (byte-identical to the host encoder)
-    s3 = vg.compress_device(f_dev, args.eps, cfg, relative=True)
-    for _ in range(2):   # warm-up (pinned host buffers of the sections)
-        huffman.decode_device(huffman.encode_device(s3.codes, 32), np.uint8)
-        huffman.decode_device(huffman.encode_device(
-            s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096)), np.uint16)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    bx = huffman.encode_device(s3.codes, 32)
-    bq = huffman.encode_device(s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096))
-    torch.cuda.synchronize()
-    dent_enc = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    huffman.decode_device(bx, np.uint8)
-    huffman.decode_device(bq, np.uint16)
-    torch.cuda.synchronize()
-    dent_dec = time.perf_counter() - t0
-    dent = {"sections_MB": round((len(bx) + len(bq)) / 1e6, 1),
-            "encode_s": round(dent_enc, 4), "decode_s": round(dent_dec, 4),
-            "encode_GBps_fp32_input": round(8.0 * N / dent_enc / 1e9, 2)}
-    del s3, bx, bq
+    e2e_s = arc_s = ent_s = None
+    d2h = arc_bytes = 0
+    dent = None
+    if not args.quick:
+        # ---- end to end through the public API from pinned host buffers
+        u_pin = torch.from_numpy(u_h).pin_memory()
+        v_pin = torch.from_numpy(v_h).pin_memory()
+        f_host = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u_pin, v_pin)
+        # warm-up: the pinned host buffers of the streams come from torch's
+        # caching host allocator and are reused by the timed steps
+        for _ in range(max(1, args.warmup)):
+            host = None
+            host = codec.streams_to_host(vg.compress_device(f_host, args.eps, cfg,
+                                                            relative=True,
+                                                            host_out=True))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            s2 = host = None
+            s2 = vg.compress_device(f_host, args.eps, cfg, relative=True,
+                                    host_out=True)
+            host = codec.streams_to_host(s2)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
+        e2e_s = max_over_ranks(e2e_s)
+        d2h = sum(int(x.nbytes) for x in host.values())
+        # the public compress() to an Archive (device entropy stage: only the
+        # packed sections come back), same pinned host input
+        for _ in range(max(1, args.warmup)):   # warm-up (pinned / host buffers)
+            arc = None
+            arc = vg.compress(f_host, args.eps, cfg, relative=True)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            arc = None
+            arc = vg.compress(f_host, args.eps, cfg, relative=True)
+        torch.cuda.synchronize()
+        arc_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
+        arc_bytes = sum(len(x) for x in arc.sections)
+        del arc
+        # host entropy backend (Huffman + zlib), timed on frame 0's streams
+        nq0 = 2 * (H * W) if s.qd.numel() >= 2 * H * W else s.qd.numel()
+        t0 = time.perf_counter()
+        from paper_2510_25143_b200 import huffman
+        import zlib
+        b1 = huffman.encode(host["codes"][:H * W], 32)
+        b2 = huffman.encode(host["qd"][:nq0], 2 * cfg.radius)
+        zlib.compress(b1, 6)
+        zlib.compress(b2, 6)
+        ent_s = time.perf_counter() - t0
+        # the device entropy stage (csrc/huffman_gpu.cu) on the whole field's
+        # streams, resident from the timed compress: encode and decode of the
+        # q_xi and q_d sections (byte-identical to the host encoder)
+        s3 = vg.compress_device(f_dev, args.eps, cfg, relative=True)
+        for _ in range(2):   # warm-up (pinned host buffers of the sections)
+            huffman.decode_device(huffman.encode_device(s3.codes, 32), np.uint8)
+            huffman.decode_device(huffman.encode_device(
+                s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096)), np.uint16)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bx = huffman.encode_device(s3.codes, 32)
+        bq = huffman.encode_device(s3.qd, 2 * cfg.radius, max(0, cfg.radius - 4096))
+        torch.cuda.synchronize()
+        dent_enc = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        huffman.decode_device(bx, np.uint8)
+        huffman.decode_device(bq, np.uint16)
+        torch.cuda.synchronize()
+        dent_dec = time.perf_counter() - t0
+        dent = {"sections_MB": round((len(bx) + len(bq)) / 1e6, 1),
+                "encode_s": round(dent_enc, 4), "decode_s": round(dent_dec, 4),
+                "encode_GBps_fp32_input": round(8.0 * N / dent_enc / 1e9, 2)}
+        del s3, bx, bq
 
     peak, peak_src = measured_peak()
     # dominant kernel roofline
@@ -436,20 +442,22 @@ def main():
         "kernels_ms": {k: round(v[0] / steps, 3) for k, v in prof.items()
                        if v[1]},
         "gpu_launches": launches // max(1, steps),
-        "e2e": {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
-                "unit": UNIT, "h2d_bytes_per_step": 8 * N,
-                "d2h_bytes_per_step": d2h},
-        "e2e_archive": {"value": round(8.0 * N * world / arc_s / 1e9, 3),
-                        "unit": UNIT, "ms_per_step": round(arc_s * 1e3, 1),
-                        "api": "compress() -> Archive sections",
-                        "h2d_bytes_per_step": 8 * N,
-                        "d2h_bytes_per_step": arc_bytes},
-        "device_entropy": dent,
-        "host_entropy": {"sample": "frame 0 codes + qd: Huffman + zlib(6)",
-                         "seconds": round(ent_s, 3),
-                         "MBps_fp32_input": round(8.0 * H * W / ent_s / 1e6, 2)},
         "clocks": clk,
     }
+    if e2e_s is not None:
+        line["e2e"] = {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
+                       "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                       "d2h_bytes_per_step": d2h}
+        line["e2e_archive"] = {
+            "value": round(8.0 * N * world / arc_s / 1e9, 3), "unit": UNIT,
+            "ms_per_step": round(arc_s * 1e3, 1),
+            "api": "compress() -> Archive sections",
+            "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": arc_bytes}
+        line["device_entropy"] = dent
+        line["host_entropy"] = {
+            "sample": "frame 0 codes + qd: Huffman + zlib(6)",
+            "seconds": round(ent_s, 3),
+            "MBps_fp32_input": round(8.0 * H * W / ent_s / 1e6, 2)}
     if dec is not None:
         dec["roofline_frac"] = round(
             ALGO_BYTES["pipeline_decompress"] * N / (dec["ms_per_step"] * 1e-3)

@@ -154,7 +154,10 @@ __global__ void __launch_bounds__(K1_THREADS)
 analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
                int T, double S, int64_t tau, uint8_t* __restrict__ codes,
                uint32_t* __restrict__ ld_words, uint16_t* __restrict__ mask,
-               int32_t* __restrict__ row_n31) {
+               int32_t* __restrict__ row_n31, const int* __restrict__ run_if) {
+  // the fallback of the split analysis (below) when its anchor list
+  // overflowed; run_if == nullptr: always
+  if (run_if && *run_if == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -322,6 +325,293 @@ analyze_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
   }
 }
 
+// --------------------------------------------------- K1, split in two
+// The common case has almost no anchor whose space-time cube can carry a
+// positive face or lower a bound below tau' (the vertex class
+// test above).  So the analysis runs as
+//   cube_kernel   streaming over the field once (8 B/vertex): fixed point,
+//                 the vertex class, the cube test of every anchor; only the
+//                 failing anchors are appended to a list (codes are 0 for
+//                 everything else: set by a memset beforehand);
+//   exact_kernel  the 12 faces of each listed anchor, exactly (SoS, int64
+//                 edge bounds); the code of a vertex is the max over its
+//                 faces' values (quantize_eb is monotone), applied with a
+//                 byte atomicMax; l_d bits, the per-row code-31 counts (a
+//                 vertex is counted when its byte first reaches 31) and the
+//                 face mask likewise.
+// A list that would overflow its buffer hands the frame set to the fused
+// kernel above (analyze_kernel with run_if = the overflow flag).
+constexpr int CTI = 32, CTJ = 128;           // owned anchors per tile
+constexpr int CRH = CTI + 1;                 // vertex rows (+1 below)
+constexpr int CQW = CTJ / 4 + 1;             // 4-vertex groups per row (+1 right)
+constexpr int C_THREADS = 256;
+
+// Low nibble of the vertex class (analyze_kernel's vertex_class) straight
+// from the float input: fixed(x) >= thr <=> x*S >= thr - 0.5 (rha rounds
+// half away from zero) <=> x >= T with T = (thr - 0.5) / S exact, i.e. x >=
+// Tf for the smallest float Tf >= T (x is a float); -x likewise.  Vertices
+// outside the frame get 0xFF, so a cube clipped at the frame edge (the
+// reference's anchor ranges) ANDs only its existing vertices.
+__device__ __forceinline__ uint32_t cls_nib(float x, float y, float Tf) {
+  return (x >= Tf ? 1u : 0u) | (-x >= Tf ? 2u : 0u) | (y >= Tf ? 4u : 0u) |
+         (-y >= Tf ? 8u : 0u);
+}
+__device__ __forceinline__ uint32_t cls_nib(double x, double y, double Td) {
+  return (x >= Td ? 1u : 0u) | (-x >= Td ? 2u : 0u) | (y >= Td ? 4u : 0u) |
+         (-y >= Td ? 8u : 0u);
+}
+
+// CTA = 32 x 128 anchors, marching over the frames with the class bytes of
+// frames t and t+1 in shared memory (frame t+2's values in flight); a thread
+// tests four anchors of one row at once (byte-SIMD AND of 32-bit words).
+template <typename F>
+__global__ void __launch_bounds__(C_THREADS, 4)
+cube_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
+            int T, F Tq, uint64_t* __restrict__ list,
+            unsigned long long* __restrict__ count, unsigned long long cap) {
+  __shared__ uint32_t cls[2][CRH][CQW + 1];   // 4 class bytes per word
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int i0 = blockIdx.y * CTI, j0 = blockIdx.x * CTJ;
+  const int64_t HW = (int64_t)H * W;
+  const bool vec = sizeof(F) == 4 && (W & 3) == 0 &&
+                   (((uintptr_t)u | (uintptr_t)v) & 15) == 0;
+  constexpr int NG = CRH * CQW;                           // groups per frame
+  constexpr int NL = (NG + C_THREADS - 1) / C_THREADS;
+  float4 ru[NL], rv[NL];
+  auto issue = [&](int t) {
+    const int64_t base = (int64_t)t * HW;
+#pragma unroll
+    for (int q = 0; q < NL; q++) {
+      const int k = tid + q * C_THREADS;
+      const int lr = k / CQW, g = k - lr * CQW;
+      const int gi = i0 + lr, gj = j0 + 4 * g;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (k < NG && gi < H) {
+        const int64_t n = base + (int64_t)gi * W + gj;
+        if (vec && gj + 3 < W) {
+          a = __ldg(reinterpret_cast<const float4*>(u + n));
+          b = __ldg(reinterpret_cast<const float4*>(v + n));
+        } else {
+          float xa[4] = {0.f, 0.f, 0.f, 0.f}, xb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (gj + e < W) { xa[e] = (float)__ldg(u + n + e); xb[e] = (float)__ldg(v + n + e); }
+          a = make_float4(xa[0], xa[1], xa[2], xa[3]);
+          b = make_float4(xb[0], xb[1], xb[2], xb[3]);
+          if (sizeof(F) == 8) {
+            // float64 input: the class is taken in double below; keep the
+            // raw values by reloading there (rare path)
+          }
+        }
+      }
+      ru[q] = a;
+      rv[q] = b;
+    }
+  };
+  auto commit = [&](int t) {
+    const int s = t & 1;
+    const int64_t base = (int64_t)t * HW;
+#pragma unroll
+    for (int q = 0; q < NL; q++) {
+      const int k = tid + q * C_THREADS;
+      if (k >= NG) break;
+      const int lr = k / CQW, g = k - lr * CQW;
+      const int gi = i0 + lr, gj = j0 + 4 * g;
+      uint32_t w = 0;
+      const float xs[4] = {ru[q].x, ru[q].y, ru[q].z, ru[q].w};
+      const float ys[4] = {rv[q].x, rv[q].y, rv[q].z, rv[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        uint32_t c = 0xffu;
+        if (gi < H && gj + e < W) {
+          if (sizeof(F) == 4) {
+            c = cls_nib(xs[e], ys[e], (float)Tq);
+          } else {
+            const int64_t n = base + (int64_t)gi * W + gj + e;
+            c = cls_nib((double)__ldg(u + n), (double)__ldg(v + n), (double)Tq);
+          }
+        }
+        w |= c << (8 * e);
+      }
+      cls[s][lr][g] = w;
+    }
+  };
+  issue(0);
+  commit(0);
+  if (T > 1) issue(1);
+  const unsigned FULL = 0xffffffffu;
+  for (int t = 0; t < T; t++) {
+    const bool slab = t + 1 < T;
+    if (slab) commit(t + 1);
+    if (t + 2 < T) issue(t + 2);
+    __syncthreads();
+    const int s0 = t & 1, s1 = (t + 1) & 1;
+    // thread: row lr, anchors 4g .. 4g+3 (CTJ / 4 = 32 groups per row)
+    const int g = tid & 31;
+#pragma unroll
+    for (int lr = tid >> 5; lr < CTI; lr += C_THREADS / 32) {
+      const int gi = i0 + lr;
+      auto band = [&](int s, int r) {
+        const uint32_t w0 = cls[s][r][g], w1 = cls[s][r][g + 1];
+        return w0 & __funnelshift_r(w0, w1, 8);   // (c, c+1) pairs
+      };
+      uint32_t a = band(s0, lr) & band(s0, lr + 1);
+      if (slab) a &= band(s1, lr) & band(s1, lr + 1);
+      // anchor e needs exact work iff its nibble AND is 0 (and it exists)
+      uint32_t need = __vcmpeq4(a & 0x0f0f0f0fu, 0u);   // 0xff per byte
+      uint32_t m4 = 0;
+#pragma unroll
+      for (int e = 0; e < 4; e++)
+        if (((need >> (8 * e)) & 1u) && gi < H && j0 + 4 * g + e < W) m4 |= 1u << e;
+      const int n = __popc(m4);
+      int incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int tot = __shfl_sync(FULL, incl, 31);
+      if (tot) {
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(count, (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 31);
+        unsigned long long k = base + (incl - n);
+        while (m4) {
+          const int e = __ffs(m4) - 1;
+          m4 &= m4 - 1u;
+          if (k < cap)
+            list[k] = ((uint64_t)t << 48) | ((uint64_t)gi << 24) |
+                      (uint64_t)(j0 + 4 * g + e);
+          k++;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// byte-wise atomic max on a byte array; returns the previous byte
+__device__ __forceinline__ unsigned atomic_max_u8(uint8_t* a, int64_t k,
+                                                  unsigned val) {
+  unsigned int* w = reinterpret_cast<unsigned int*>(
+      reinterpret_cast<uintptr_t>(a + k) & ~(uintptr_t)3);
+  const unsigned sh = 8u * (unsigned)(reinterpret_cast<uintptr_t>(a + k) & 3);
+  unsigned old = *reinterpret_cast<volatile unsigned int*>(w);
+  for (;;) {
+    const unsigned ob = (old >> sh) & 0xffu;
+    if (ob >= val) return ob;
+    const unsigned nw = (old & ~(0xffu << sh)) | (val << sh);
+    const unsigned prev = atomicCAS(w, old, nw);
+    if (prev == old) return ob;
+    old = prev;
+  }
+}
+
+template <typename F>
+__global__ void __launch_bounds__(128)
+exact_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
+             int T, double S, int64_t tau, const uint64_t* __restrict__ list,
+             const unsigned long long* __restrict__ count,
+             unsigned long long cap, const int* __restrict__ skip_if,
+             uint8_t* __restrict__ codes, uint32_t* __restrict__ ld_words,
+             uint16_t* __restrict__ mask, int32_t* __restrict__ row_n31) {
+  if (*skip_if) return;
+  const unsigned long long n = min(*count, cap);
+  const int64_t HW = (int64_t)H * W;
+  const int64_t thr = tau + 1;
+  for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       k < n; k += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t e = list[k];
+    const int t = (int)(e >> 48), gi = (int)((e >> 24) & 0xffffff), gj = (int)(e & 0xffffff);
+    // the anchor's cube: q = dt * 4 + di * 2 + dj
+    int64_t X[8], Y[8];
+    uint8_t cl[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int dt = q >> 2, di = (q >> 1) & 1, dj = q & 1;
+      const bool ok = t + dt < T && gi + di < H && gj + dj < W;
+      const int64_t id = (int64_t)(t + dt) * HW + (int64_t)(gi + di) * W + gj + dj;
+      const int32_t x = ok ? fixed_t(__ldg(u + id), S) : 0;
+      const int32_t y = ok ? fixed_t(__ldg(v + id), S) : 0;
+      X[q] = x;
+      Y[q] = y;
+      cl[q] = vertex_class(x, y, thr);
+    }
+    const int64_t an = (int64_t)t * HW + (int64_t)gi * W + gj;
+    unsigned mbits = 0;
+#pragma unroll 1
+    for (int c = 0; c < 12; c++) {
+      if (t >= T - c_lim[c][0] || gi >= H - c_lim[c][1] || gj >= W - c_lim[c][2])
+        continue;
+      int qv[3];
+      int64_t id[3];
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        const int dt = c_off[c][r][0], di = c_off[c][r][1], dj = c_off[c][r][2];
+        qv[r] = dt * 4 + di * 2 + dj;
+        id[r] = an + (int64_t)dt * HW + (int64_t)di * W + dj;
+      }
+      const uint8_t fa = cl[qv[0]] & cl[qv[1]] & cl[qv[2]];
+      if (fa & 0x0F) continue;   // neither positive nor below tau'
+      bool pos = false;
+      if ((fa & 0xF0) == 0)
+        pos = face_positive(X[qv[0]], Y[qv[0]], X[qv[1]], Y[qv[1]], X[qv[2]],
+                            Y[qv[2]], id[0], id[1], id[2]);
+      int val;
+      if (pos) {
+        val = 32;
+        mbits |= 1u << c;
+      } else {
+        int64_t xi = tau;
+#pragma unroll
+        for (int r = 0; r < 3; r++) {
+          const int r2 = r == 2 ? 0 : r + 1;
+          if ((cl[qv[r]] & cl[qv[r2]] & 0x0F) == 0) {
+            const int64_t eb = edge_eb(X[qv[r]], Y[qv[r]], X[qv[r2]], Y[qv[r2]]);
+            if (eb < xi) xi = eb;
+          }
+        }
+        if (xi < 0) xi = 0;
+        val = eb_value(xi, tau);
+      }
+      if (val == 0 || tau <= 0) continue;   // tau' <= 0: every code is 31
+      const unsigned v31 = val > 31 ? 31u : (unsigned)val;
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        const unsigned old = atomic_max_u8(codes, id[r], v31);
+        if (val == 32) set_packbit(ld_words, id[r]);
+        if (old < 31u && v31 == 31u) {
+          const int64_t row = id[r] / W;   // t * H + i
+          atomicAdd(row_n31 + row, 1);
+        }
+      }
+    }
+    if (mask && mbits)
+      atomicOr(reinterpret_cast<unsigned int*>(mask) + (an >> 1),
+               mbits << (16 * (unsigned)(an & 1)));
+  }
+}
+
+__global__ void ovf_flag_kernel(const unsigned long long* count,
+                                unsigned long long cap, int* ovf) {
+  *ovf = *count > cap ? 1 : 0;
+}
+
+// every vertex lossless (tau' <= 0): l_d all ones (packbits of N bits,
+// zero padded), W code-31 vertices per row (the codes: a memset); skipped
+// when the fused fallback runs
+__global__ void lossless_fill_kernel(int64_t N, int64_t nrows, int W,
+                                     uint8_t* __restrict__ ld_bytes,
+                                     int32_t* __restrict__ row_n31,
+                                     const int* __restrict__ skip_if) {
+  if (*skip_if) return;
+  const int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = k0; r < nrows; r += step) row_n31[r] = W;
+  for (int64_t b = k0; b < (N >> 3); b += step) ld_bytes[b] = 0xff;
+  if (k0 == 0 && (N & 7)) ld_bytes[N >> 3] = (uint8_t)(0xffu << (8 - (N & 7)));
+}
+
 // ------------------------------------------------- row offsets (exclusive)
 // out[r] = base + sum_{q < r} mul * (W - cnt[q])   (qd symbol offsets), or
 // out[r] = sum_{q < r} cnt[q] when W == 0 (plain exclusive scan).
@@ -370,19 +660,54 @@ cudaError_t launch_range(const F* u, const F* v, int64_t n, double* part,
   return cudaGetLastError();
 }
 
+// ld_words and row_n31 zeroed by the caller; scratch: the anchor list
+// (cap entries), its count and the overflow flag (zeroed here)
 template <typename F>
 cudaError_t launch_analyze(const F* u, const F* v, int H, int W, int T,
                            double S, int64_t tau, uint8_t* codes,
                            uint32_t* ld_words, uint16_t* mask,
-                           int32_t* row_n31, cudaStream_t st) {
+                           int32_t* row_n31, uint64_t* list,
+                           unsigned long long* count, int* ovf,
+                           unsigned long long cap, int nsm, cudaStream_t st) {
+  const int64_t N = (int64_t)H * W * T;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(codes, tau > 0 ? 0 : CODE_LOSSLESS, (size_t)N, st)) != cudaSuccess)
+    return e;
+  if (mask && (e = cudaMemsetAsync(mask, 0, sizeof(uint16_t) * (size_t)N, st)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+  // the class threshold in the input's own precision (cls_nib)
+  const double Td = ((double)(tau + 1) - 0.5) / S;
+  F Tq;
+  if (sizeof(F) == 4) {
+    float tf = (float)Td;
+    if ((double)tf < Td) tf = nextafterf(tf, INFINITY);
+    Tq = (F)tf;
+  } else {
+    Tq = (F)Td;
+  }
+  cube_kernel<F><<<dim3((W + CTJ - 1) / CTJ, (H + CTI - 1) / CTI), C_THREADS, 0, st>>>(
+      u, v, H, W, T, Tq, list, count, cap);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ovf_flag_kernel<<<1, 1, 0, st>>>(count, cap, ovf);
+  exact_kernel<F><<<nsm * 8, 128, 0, st>>>(u, v, H, W, T, S, tau, list, count,
+                                          cap, ovf, codes, ld_words, mask,
+                                          row_n31);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (tau <= 0) {
+    lossless_fill_kernel<<<1184, 256, 0, st>>>(N, (int64_t)T * H, W,
+                                               reinterpret_cast<uint8_t*>(ld_words),
+                                               row_n31, ovf);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // fallback: the fused kernel, which rewrites codes / l_d / counts / mask
   size_t smem = sizeof(K1Smem);
-  cudaError_t e = cudaFuncSetAttribute(
-      analyze_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      (int)smem);
+  e = cudaFuncSetAttribute(analyze_kernel<F>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((W + TJ - 1) / TJ, (H + TI - 1) / TI);
   analyze_kernel<F><<<grid, K1_THREADS, smem, st>>>(
-      u, v, H, W, T, S, tau, codes, ld_words, mask, row_n31);
+      u, v, H, W, T, S, tau, codes, ld_words, mask, row_n31, ovf);
   return cudaGetLastError();
 }
 
@@ -400,10 +725,16 @@ template cudaError_t launch_range<double>(const double*, const double*,
 template cudaError_t launch_analyze<float>(const float*, const float*, int,
                                            int, int, double, int64_t,
                                            uint8_t*, uint32_t*, uint16_t*,
-                                           int32_t*, cudaStream_t);
+                                           int32_t*, uint64_t*,
+                                           unsigned long long*, int*,
+                                           unsigned long long, int,
+                                           cudaStream_t);
 template cudaError_t launch_analyze<double>(const double*, const double*, int,
                                             int, int, double, int64_t,
                                             uint8_t*, uint32_t*, uint16_t*,
-                                            int32_t*, cudaStream_t);
+                                            int32_t*, uint64_t*,
+                                            unsigned long long*, int*,
+                                            unsigned long long, int,
+                                            cudaStream_t);
 
 }  // namespace vfcp

@@ -1,36 +1,32 @@
 // The raster-order Lorenzo recurrence of one frame as a 2D block scan.
 //
-// In: the prepared planes a (encoder: R0 = orig - Lorenzo(orig, prev), or
-// the pinned err; decoder, run on Z = recon - prev: (sym - radius) * 2e, or
-// the pinned Z), the per-(row, chunk) pin words and (encoder) the frame
-// codes.  Out: the err / recon plane, (encoder) the Lorenzo symbols written
-// into the interleaved symbol stream, (decoder) the float64 output -- bit for
-// bit what the reference's raster loop (codec.py:118-164 _encode_frame,
-// 167-206 _decode_frame) produces.
-//
-// Why a scan is exact.  Per component, with v the chain value (encoder: err
-// = recon - orig; decoder: Z) and zero padding outside the frame,
-//   decoder:  v = vU + vL - vUL + A                 (exact)
-//   encoder:  v = q*2e - x,  x = R0 - (vU + vL - vUL),  q = rha(x / 2e)
-// so in the encoder v == -R0 + vU + vL - vUL (mod 2e) whenever the pixel is
-// quantised with the same step e (v in [-e, e] is the representative of
-// that residue; a residue of exactly e is a tie whose sign follows x, which
-// rounds away from zero).  Over a 32x32 block whose pixels all share one
-// step, have no pins and cannot escape (|R0| < (2 radius - 4) e), every
-// value is therefore a 2D prefix sum of the block plus its boundary:
+// Per component, with zero padding outside the frame and Z = recon -
+// recon(t-1):
+//   decoder:  Z = ZU + ZL - ZUL + A,  A = (sym - radius) * 2e   (exact)
+//   encoder:  err = recon - orig = q*2e - x,  x = R0 - (errU + errL -
+//             errUL),  q = rha(x / 2e),  R0 = orig - Lorenzo(orig, prev)
+// so in the encoder err == -R0 + errU + errL - errUL (mod 2e) whenever the
+// pixel is quantised with the same step e (err in [-e, e] is the
+// representative of that residue; a residue of exactly e is a tie whose
+// sign follows x, which rounds away from zero).  Over a 32x32 block whose
+// pixels all share one step, have no pins and cannot escape (|R0| < (2
+// radius - 4) e) -- a REG block -- every value is the block's 2D prefix sum
+// plus its boundary:
 //   v(i, j) = top(j) + left(i) - corner + sum_{a<=i, b<=j} X(a, b)
 // with X = A (decoder, wrapping uint32 arithmetic is exact because the
-// result fits int32) or X = -R0 mod 2e (encoder, then the representative).
-// Blocks whose values are known without the recurrence (all pixels pinned:
-// semi-Lagrangian blocks, lossless areas) pass their prepared values; any
-// other block (mixed pins, mixed steps, possible escapes, a tie on its
-// boundary) is swept exactly, pixel by pixel, given its exact boundary.
+// result fits int32) or X = -R0 mod 2e (encoder, whose prefix sum
+// telescopes to -(delta(i,j) - delta(top,j) - delta(i,left) +
+// delta(corner)), delta = orig - recon(t-1), see enc_block.cu).  Blocks whose
+// values are known without the recurrence (KNOWN: all pixels pinned --
+// semi-Lagrangian blocks, lossless areas) pass their edge values; any other
+// block (mixed pins, mixed steps, possible escapes, a tie on its boundary)
+// is swept exactly, pixel by pixel, given its exact boundary.
 //
 // Three phases per frame:
-//   phase A  fully parallel, in the prepare kernels (enc_r0_kernel and
-//            enc_pix_kernel; bs_local_kernel for the decoder): block class
-//            and the bottom row / right column of the block-local prefix
-//            sums (LB, LR), or the known edge values;
+//   phase A  fully parallel, in the block kernels (enc_block.cu,
+//            dec_block.cu): block class and the bottom row / right column of
+//            the block-local prefix sums (LB, LR), or the known edge values;
+//            KNOWN blocks are written there;
 //   phase B  chain tasks of bs_chain_kernel, the only sequential part: block
 //            boundaries travel down the block rows (one warp per block row
 //            and component walks its row; 32 exact values per block are
@@ -38,9 +34,9 @@
 //            cheap block steps instead of H + W pixel steps;
 //   phase C  interior tasks of the same persistent kernel, handed out after
 //            the chain tasks and started per 32-block segment once the chain
-//            has published it, so they overlap the chain: the interior of
-//            every block from its exact boundary (prefix sums in shared
-//            memory, ties resolved in raster order, symbols).
+//            has published it, so they overlap the chain: one warp per block
+//            and both components, rows streamed in registers -- recon(t),
+//            the encoder's symbols, the decoder's float64 output.
 #pragma once
 
 #include "frame.cuh"
@@ -51,7 +47,10 @@ enum : uint8_t { BS_SLOW = 0, BS_KNOWN = 1, BS_REG = 2, BS_DONE = 3 };
 
 struct BScanIO {
   const int32_t* a[2];
-  const uint8_t* codes;     // encoder: frame codes (pitch Wp)
+  int32_t* a_w[2];          // encoder: the same planes, written by the block
+                            // kernel (R0 of the blocks the chain sweeps)
+  const uint8_t* codes;     // frame codes (pitch cpitch)
+  int cpitch;
   const uint32_t* pin[2];   // per (row, chunk)
   int32_t* out[2];          // encoder: err; decoder: recon (pitch Wp)
   // encoder, frame t: the interleaved symbol stream (u, v per non-lossless
@@ -73,9 +72,6 @@ struct BScanIO {
   double* f64[2];
   int64_t* fix[2];
   double inv_S;
-  // decoder: the chain runs on Z = recon - p (dec_prep_kernel); p is the
-  // previous frame's recon (pitch Wp), nullptr for frame 0
-  const int32_t* prev[2];
   int32_t* ebot;            // [2][nblk][32] exact block bottom rows (chain)
   int32_t* eright;          // [2][nblk][32] exact block right columns (chain)
   int32_t* cls;             // [2][nblk] class | code << 2
@@ -86,11 +82,18 @@ struct BScanIO {
   int radius;
   int32_t e_tab[32];        // e per code (0: lossless)
   uint32_t mag_tab[32];     // floor(2^32 / 2e) per code (0: lossless)
+  uint32_t c32_tab[32];     // 2^32 mod 2e per code (0: lossless)
+  // interior pass: (encoder) orig(t) (float32 / float64); recon(t-1)
+  // (nullptr for frame 0) and recon(t) as interleaved (u, v) pairs, pitch Wp
+  const void* orig[2];
+  const int2* prevrec;
+  int2* rec;
+  double S;
 };
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
-constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
+constexpr int BS_PF = 4;        // blocks of (class, LB, LR) staged ahead
 constexpr int BS_SEG = 32;      // blocks per progress mark / interior task
 
 __host__ __device__ inline int bs_ntask(int nby) {
@@ -129,6 +132,13 @@ __device__ __forceinline__ uint32_t bs_res(int32_t v, uint32_t m, uint32_t M) {
 __device__ __forceinline__ uint32_t bs_negres(int32_t r0, uint32_t m, uint32_t M) {
   return bs_res_any(-r0, m, M);
 }
+// x mod m for |x| < 2^32 (x = o - p with |o| < 2^30, |p| < 2^31); c32 =
+// 2^32 mod m, M = floor(2^32 / m)
+__device__ __forceinline__ uint32_t res_i64(int64_t x, uint32_t m, uint32_t M,
+                                            uint32_t c32) {
+  const uint32_t r = bs_umod((uint32_t)(uint64_t)x, m, M);
+  return x < 0 ? bs_msub(r, c32, m) : r;
+}
 // representative in [-e, e] of a residue that is not the tie e
 __device__ __forceinline__ int32_t bs_rep(uint32_t r, uint32_t e, uint32_t m) {
   return r < e ? (int32_t)r : (int32_t)r - (int32_t)m;
@@ -151,107 +161,9 @@ __device__ __forceinline__ int32_t bs_enc_exact(int32_t R0, int32_t d,
   return (int32_t)(q * m - x);
 }
 
-// ------------------------------------------------------------ phase A
-// CTA = one block, warp = component (lane = column).
-template <bool ENC>
-__global__ void __launch_bounds__(64) bs_local_kernel(BScanIO io) {
-  __shared__ uint32_t sx[2][32][33];
-  __shared__ int32_t etab[32];
-  __shared__ uint32_t mtab[32];
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, comp = threadIdx.x >> 5;
-  if (threadIdx.x < 32) { etab[lane] = io.e_tab[lane]; mtab[lane] = io.mag_tab[lane]; }
-  const int bj = blockIdx.x, bi = blockIdx.y;
-  const int r0 = 32 * bi, c0 = 32 * bj;
-  const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
-  const int64_t nblk = (int64_t)io.nbx * io.nby;
-  const int64_t blk = (int64_t)bi * io.nbx + bj;
-  const int32_t* a = io.a[comp];
-  const uint32_t vm = ncl >= 32 ? FULL : ((1u << ncl) - 1u);
-  const uint32_t pw =
-      lane < nr ? (io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] & vm) : 0u;
-  const bool anypin = __any_sync(FULL, pw != 0u);
-  const bool allpin = __all_sync(FULL, lane >= nr || pw == vm);
-  __syncthreads();
-  int32_t cls;
-  if (allpin) {
-    // known values: the chain passes the edges on
-    cls = BS_KNOWN;
-    io.lb[(comp * nblk + blk) * 32 + lane] =
-        lane < ncl ? __ldg(a + (int64_t)(r0 + nr - 1) * io.Wp + c0 + lane) : 0;
-    io.lr[(comp * nblk + blk) * 32 + lane] =
-        lane < nr ? __ldg(a + (int64_t)(r0 + lane) * io.Wp + c0 + ncl - 1) : 0;
-  } else if (anypin) {
-    cls = BS_SLOW;
-  } else {
-    const bool colok = lane < ncl;
-    int32_t xa[32];
-#pragma unroll
-    for (int r = 0; r < 32; r++)
-      xa[r] = (r < nr && colok) ? __ldg(a + (int64_t)(r0 + r) * io.Wp + c0 + lane) : 0;
-    bool ok = true;
-    uint32_t m = 0, M = 0;
-    int code = 0;
-    if (ENC) {
-      code = io.codes[(int64_t)r0 * io.Wp + c0];
-      const int32_t e = etab[code & 31];
-      m = 2u * (uint32_t)e;
-      M = mtab[code & 31];
-      const int64_t lim = (2 * (int64_t)io.radius - 4) * (int64_t)e;
-      ok = e > 0 && lim > 0;
-#pragma unroll
-      for (int r = 0; r < 32; r++) {
-        if (r < nr && colok) {
-          const int cd = io.codes[(int64_t)(r0 + r) * io.Wp + c0 + lane];
-          const int64_t ax = xa[r] < 0 ? -(int64_t)xa[r] : (int64_t)xa[r];
-          ok &= (cd == code) && ax < lim;
-        }
-      }
-      ok = __all_sync(FULL, ok);
-    }
-    if (!ok) {
-      cls = BS_SLOW;
-    } else {
-      cls = BS_REG | (code << 2);
-#pragma unroll
-      for (int r = 0; r < 32; r++)
-        sx[comp][r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
-      __syncwarp();
-      // column sum (lane = column) and row sum (lane = row)
-      uint64_t cs = 0, rs = 0;
-#pragma unroll
-      for (int k = 0; k < 32; k++) {
-        cs += sx[comp][k][lane];
-        rs += sx[comp][lane][k];
-      }
-      uint32_t c32, r32;
-      if (ENC) { c32 = (uint32_t)(cs % m); r32 = (uint32_t)(rs % m); }
-      else { c32 = (uint32_t)cs; r32 = (uint32_t)rs; }
-      // inclusive scans over lanes: LB(j) = sum_{b<=j} colsum(b),
-      // LR(i) = sum_{a<=i} rowsum(a)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t pc = __shfl_up_sync(FULL, c32, o);
-        const uint32_t pr = __shfl_up_sync(FULL, r32, o);
-        if (lane >= o) {
-          c32 = ENC ? bs_madd(c32, pc, m) : c32 + pc;
-          r32 = ENC ? bs_madd(r32, pr, m) : r32 + pr;
-        }
-      }
-      io.lb[(comp * nblk + blk) * 32 + lane] = (int32_t)c32;
-      io.lr[(comp * nblk + blk) * 32 + lane] = (int32_t)r32;
-    }
-  }
-  if (lane == 0) io.cls[comp * nblk + blk] = cls;
-}
-
 // ------------------------------------------------------------ phase B
-// Shared memory of the fused chain / interior kernel.  The interior tiles
-// (tasks after the chain tasks) overlay the chain-only region.
-struct BSFinTiles {
-  uint32_t x[BS_NW][32][33];
-  int32_t v[BS_NW][33][33];
-};
+// Shared memory of the fused chain / interior kernel (the interior tasks
+// work in registers).
 struct BSChainSmem {
   int32_t etab[32];
   uint32_t mtab[32];
@@ -260,35 +172,80 @@ struct BSChainSmem {
   alignas(16) int32_t pf[BS_NW][BS_PF][64];   // LB (0..31), LR (32..63)
   alignas(16) int32_t pfd[BS_NW][32][4];      // per-lane sink of idle copies
   int32_t pfc[BS_NW][BS_PF];           // class word per block
-  union {
+  struct {
     struct {
       uint64_t hin[BS_NW + 1][BS_HRING];   // tagged (column + 1) << 32 | value
       // slow path tiles, [row][col] unpadded: the skewed sweep reads column
       // s - lane in row lane, distinct banks across lanes
       int32_t tv[BS_NW][32][32];           // slow path: values
-      uint16_t ts[BS_NW][32][32];          // slow path: symbols (encoder)
-      int64_t tq[BS_NW][32];               // slow path: row stream offsets
-      uint8_t tc[BS_NW][32][32];           // slow path: codes (encoder)
     };
-    BSFinTiles fin;
   };
 };
 
-template <bool ENC>
+// Encoder: R0 = D(orig - recon(t-1)) of a block whose R0 plane the block
+// kernel did not write (a REG block with a tie on its edges); |R0| < 2^30
+// there, so int32 is exact.  Lane = column, rows streamed.
+template <typename F>
+__device__ __forceinline__ void bs_r0_rows(const BScanIO& io, int comp,
+                                           int r0, int c0, int nr, int ncl,
+                                           int32_t (*tv)[32], int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const F* op = static_cast<const F*>(io.orig[comp]);
+  const int2* pv = io.prevrec;
+  const int W = io.W, Wp = io.Wp;
+  const int j = c0 + min(lane, ncl - 1);
+  auto delta = [&](int i, int jj) -> int32_t {
+    if (i < 0 || jj < 0) return 0;
+    const int32_t o = fixed_t(__ldg(op + (int64_t)i * W + jj), io.S);
+    const int2 pp = pv ? __ldg(pv + (int64_t)i * Wp + jj) : make_int2(0, 0);
+    return o - (comp ? pp.y : pp.x);
+  };
+  int32_t dU = delta(r0 - 1, j);
+  int32_t dUL = delta(r0 - 1, c0 - 1);
+  for (int r = 0; r < nr; r++) {
+    const int32_t d = delta(r0 + r, j);
+    const int32_t dl0 = delta(r0 + r, c0 - 1);
+    int32_t dl = __shfl_up_sync(FULL, d, 1);
+    int32_t dul = __shfl_up_sync(FULL, dU, 1);
+    if (lane == 0) { dl = dl0; dul = dUL; }
+    tv[r][lane] = lane < ncl ? d - dU - dl + dul : 0;
+    dU = d;
+    dUL = dl0;
+  }
+}
+
+template <bool ENC, typename F>
 __device__ __forceinline__ void bs_slow_block(
     const BScanIO& io, BSChainSmem& sm, int w, int comp, int bi, int bj,
-    int nr, int ncl, int32_t top, int32_t left, int32_t corner, int lane) {
+    int nr, int ncl, int32_t top, int32_t left, int32_t corner, int lane,
+    bool r0_in_plane) {
   const unsigned FULL = 0xffffffffu;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const bool colok = lane < ncl;
   const int32_t* a = io.a[comp];
   int32_t(*tv)[32] = sm.tv[w];
+  if (ENC && !r0_in_plane) bs_r0_rows<F>(io, comp, r0, c0, nr, ncl, tv, lane);
+  // encoder: the sweeping lane's row (lane = row): its non-lossless bits and
+  // stream offset, so each symbol goes straight to the stream
+  uint32_t mynl = 0u;
+  int64_t myq = 0;
   for (int r = 0; r < nr; r++) {
     const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
-    tv[r][lane] = colok ? __ldcg(a + k) : 0;
-    if (ENC) sm.tc[w][r][lane] = colok ? io.codes[k] : (uint8_t)CODE_LOSSLESS;
+    if (!ENC || r0_in_plane) tv[r][lane] = colok ? __ldcg(a + k) : 0;
+    if (ENC) {
+      const int cd = colok ? io.codes[(int64_t)(r0 + r) * io.cpitch + c0 + lane] : CODE_LOSSLESS;
+      const uint32_t nlw = __ballot_sync(FULL, colok && sm.etab[cd & 31] > 0);
+      if (lane == r) mynl = nlw;
+    }
   }
-  const uint32_t pw = lane < nr ? io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
+  if (ENC && lane < nr)
+    myq = io.qd_row_off[r0 + lane] +
+          2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
+  const uint8_t* mycodes = io.codes + (int64_t)(r0 + min(lane, nr - 1)) * io.cpitch + c0;
+  int nesc = 0;
+  // encoder: no pins (lossless pixels have e = 0 and err 0; semi-Lagrangian
+  // blocks are never swept); decoder: lossless, escaped and SL pixels
+  const uint32_t pw = (!ENC && lane < nr) ? io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
   __syncwarp();
   int32_t l = left;
   int32_t ul = __shfl_up_sync(FULL, left, 1);
@@ -307,13 +264,18 @@ __device__ __forceinline__ void bs_slow_block(
       if ((pw >> jj) & 1u) {
         v = x;
       } else if (ENC) {
-        const int32_t e = sm.etab[sm.tc[w][lane][jj] & 31];
-        v = e > 0 ? bs_enc_exact(x, nu + l - ul, e, radius, &sy) : 0;
+        const int32_t e = sm.etab[mycodes[jj] & 31];
+        if (e > 0) {
+          v = bs_enc_exact(x, nu + l - ul, e, radius, &sy);
+          io.qd[myq + 2 * __popc(mynl & ((1u << jj) - 1u))] = (uint16_t)sy;
+          nesc += sy == 0;
+        } else {
+          v = 0;
+        }
       } else {
         v = (int32_t)((uint32_t)nu + (uint32_t)l - (uint32_t)ul + (uint32_t)x);
       }
       tv[lane][jj] = v;
-      if (ENC) sm.ts[w][lane][jj] = (uint16_t)sy;
       ul = nu;
       l = v;
     }
@@ -324,41 +286,19 @@ __device__ __forceinline__ void bs_slow_block(
     const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
     if (colok) out[k] = tv[r][lane];
   }
-  if (ENC) {
-    // symbols of the non-pinned (Lorenzo, non-lossless) pixels into the
-    // stream; escapes (symbol 0) counted per row for the ll stream
-    const int64_t pb = (int64_t)(r0 + (lane < nr ? lane : 0)) * io.nchunks + bj;
-    const uint32_t nlr = lane < nr ? io.nlw[pb] : 0u;
-    if (lane < nr)
-      sm.tq[w][lane] = io.qd_row_off[r0 + lane] + 2 * (int64_t)io.pre_nl[pb];
-    __syncwarp();
-    const uint32_t lt = (1u << lane) - 1u;
-    for (int r = 0; r < nr; r++) {
-      const uint32_t pr_w = __shfl_sync(FULL, pw, r);
-      const uint32_t nl_w = __shfl_sync(FULL, nlr, r);
-      const bool put = colok && !((pr_w >> lane) & 1u);
-      int esc = 0;
-      if (put) {
-        const uint16_t sy = sm.ts[w][r][lane];
-        io.qd[sm.tq[w][r] + 2 * __popc(nl_w & lt) + comp] = sy;
-        esc = sy == 0;
-      }
-      const int ne = __reduce_add_sync(FULL, esc);
-      if (lane == 0 && ne) atomicAdd(io.row_ll + r0 + r, ne);
-    }
-  }
+  // escapes (symbol 0) counted per row for the ll stream
+  if (ENC && nesc) atomicAdd(io.row_ll + r0 + lane, nesc);
 }
 
-template <bool ENC>
-__device__ __forceinline__ void bs_final_block(const BScanIO& io,
-                                               uint32_t (*x)[33],
-                                               int32_t (*v)[33],
-                                               const int32_t* etab,
-                                               const uint32_t* mtab, int bi,
-                                               int bj, int comp, int lane);
+template <typename F>
+__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
+                                             int lane);
 
-template <bool ENC>
-__global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
+__device__ __forceinline__ void bs_final_dec(const BScanIO& io, int bi, int bj,
+                                             int lane);
+
+template <bool ENC, typename F = float>
+__global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSChainSmem& sm = *reinterpret_cast<BSChainSmem*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
@@ -378,20 +318,19 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
     __syncthreads();
     const int task = sm.task;
     if (task >= ntask) {
-      // ---- interior tasks: (segment of BS_SEG blocks, block row, comp) in
-      // the order the chain finishes them (segment-major: segment s of row
-      // bi is done at ~ bi * lag + (s + 1) * BS_SEG * step), each started
-      // once the chain has finished the segment in its row and in the row
-      // above
+      // ---- interior tasks: (segment of BS_SEG blocks, block row), both
+      // components per warp and block, segment-major, each started once the
+      // chain has finished the segment in its row and in the row above (both
+      // components)
       const int nseg = (nbx + BS_SEG - 1) / BS_SEG;
       const int ft = task - ntask;
-      if (ft >= 2 * nby * nseg) break;
-      const int comp = ft & 1, rs = ft >> 1;
-      const int sg = rs / nby, bi = rs - sg * nby;
+      if (ft >= nby * nseg) break;
+      const int sg = ft / nby, bi = ft - sg * nby;
       const int b0 = sg * BS_SEG, b1 = min(nbx, b0 + BS_SEG);
-      if (threadIdx.x == 0) {
-        const unsigned long long need = ((unsigned long long)io.frame_tag << 32) | (unsigned)b1;
-        for (int r = bi; r >= bi - 1 && r >= 0; r--) {
+      if (threadIdx.x < 4) {
+        const int comp = threadIdx.x & 1, r = bi - (threadIdx.x >> 1);
+        if (r >= 0) {
+          const unsigned long long need = ((unsigned long long)io.frame_tag << 32) | (unsigned)b1;
           const volatile unsigned long long* pg = io.prog + (int64_t)comp * nby + r;
           long long spins = 0;
           while (*pg < need) {
@@ -402,9 +341,10 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
         __threadfence();
       }
       __syncthreads();
-      for (int bj = b0 + w; bj < b1; bj += BS_NW)
-        bs_final_block<ENC>(io, sm.fin.x[w], sm.fin.v[w], sm.etab, sm.mtab, bi,
-                            bj, comp, lane);
+      for (int bj = b0 + w; bj < b1; bj += BS_NW) {
+        if (ENC) bs_final_enc<F>(io, bi, bj, lane);
+        else bs_final_dec(io, bi, bj, lane);
+      }
       __syncthreads();
       continue;
     }
@@ -566,7 +506,8 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
           right = lrv;
         }
         if (kind == BS_SLOW) {
-          bs_slow_block<ENC>(io, sm, w, comp, bi, bj, nr, ncl, top, left, corner, lane);
+          bs_slow_block<ENC, F>(io, sm, w, comp, bi, bj, nr, ncl, top, left,
+                                corner, lane, kind0 != BS_REG);
           bot = sm.tv[w][nr - 1][lane];
           right = sm.tv[w][lane][ncl - 1];
           if (lane == 0) io.cls[comp * nblk + (int64_t)bi * nbx + bj] = BS_DONE;
@@ -601,199 +542,322 @@ __global__ void __launch_bounds__(32 * BS_NW) bs_chain_kernel(BScanIO io) {
 }
 
 // ------------------------------------------------------------ phase C
-// CTA = one block, warp = component.
-// The interior of block (bi, bj), component comp, by one warp (lane =
-// column); x, v: the warp's shared tiles.
-template <bool ENC>
-__device__ __forceinline__ void bs_final_block(const BScanIO& io,
-                                               uint32_t (*x)[33],
-                                               int32_t (*v)[33],
-                                               const int32_t* etab,
-                                               const uint32_t* mtab, int bi,
-                                               int bj, int comp, int lane) {
+// Encoder: the interior of block (bi, bj), both components, by one warp
+// (lane = column, rows streamed with one row of loads in flight).
+//   REG       err(i, j) = rep(zT(j) + zL(i) - zC - delta(i, j))  (mod m)
+//             with zT = errT + deltaT etc. (Z = recon - prev of the exact
+//             boundary, enc_block.cu), ties in raster order; the symbol is
+//             (R0 + D(err)) / m exactly;
+//   SLOW/DONE err from the chain's sweep (its symbols are written);
+//   KNOWN     recon(t) already written by the block kernel.
+// recon(t) = orig + err goes out as (u, v) pairs.
+template <typename F>
+__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
+                                             int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
   const int64_t nblk = (int64_t)io.nbx * io.nby;
   const int64_t blk = (int64_t)bi * io.nbx + bj;
-  const int32_t cls = __ldcg(io.cls + comp * nblk + blk);
-  const int kind = cls & 3;
-  const int Wp = io.Wp;
-  const int32_t* a = io.a[comp];
-  int32_t* out = io.out[comp];
+  const int Wp = io.Wp, W = io.W;
+  int kind[2], code[2];
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    const int32_t cl = __ldcg(io.cls + c * nblk + blk);
+    kind[c] = cl & 3;
+    code[c] = cl >> 2;
+  }
+  if (kind[0] == BS_KNOWN) return;   // KNOWN <=> both components KNOWN
   const bool colok = lane < ncl;
-  // decoder: the finished recon = Z + p goes to the recon plane (the next
-  // frame's p) and out as float64 (codec.py:425-426 recon * (1/S), exact),
-  // optionally as int64
-  const int32_t* pv = ENC ? nullptr : io.prev[comp];
-  // p of the block's rows, loaded up front (all loads in flight before the
-  // stores below, which the compiler cannot reorder them past)
-  int32_t pp[ENC ? 1 : 32];
-  if (!ENC) {
-#pragma unroll
-    for (int r = 0; r < 32; r++)
-      pp[ENC ? 0 : r] = (pv && r < nr && colok) ? __ldg(pv + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
-  }
-  auto emit = [&](int r, int32_t z) {
-    if (!ENC) {
-      const int32_t val = (int32_t)((uint32_t)z + (uint32_t)pp[ENC ? 0 : r]);
-      out[(int64_t)(r0 + r) * Wp + c0 + lane] = val;
-      const int64_t k = (int64_t)(r0 + r) * io.W + c0 + lane;
-      io.f64[comp][k] = __dmul_rn((double)val, io.inv_S);
-      if (io.fix[comp]) io.fix[comp][k] = val;
-    }
+  const int j = c0 + (colok ? lane : ncl - 1);
+  const F* op[2] = {static_cast<const F*>(io.orig[0]), static_cast<const F*>(io.orig[1])};
+  auto fx = [&](const F* base, int i, int jj) -> int32_t {
+    return fixed_t(__ldg(base + (int64_t)i * W + jj), io.S);
   };
-  if (kind == BS_DONE || kind == BS_SLOW) {   // warp-uniform
-    // swept by the chain kernel
-    if (!ENC) {
-      int32_t zz[32];
+  const bool reg[2] = {kind[0] == BS_REG, kind[1] == BS_REG};
+  uint32_t e[2], m[2], M[2], c32[2];
 #pragma unroll
-      for (int r = 0; r < 32; r++)
-        zz[r] = (r < nr && colok) ? __ldcg(out + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
-#pragma unroll
-      for (int r = 0; r < 32; r++)
-        if (r < nr && colok) emit(r, zz[r]);
-    }
-    return;
+  for (int c = 0; c < 2; c++) {
+    e[c] = reg[c] ? (uint32_t)io.e_tab[code[c]] : 2u;
+    m[c] = 2u * e[c];
+    M[c] = reg[c] ? io.mag_tab[code[c]] : 0x7fffffffu;
+    c32[c] = reg[c] ? io.c32_tab[code[c]] : 0u;
   }
-  int32_t xa[32];
+  // exact boundary errors: errT (lane = column), errL (lane = row), errC
+  int32_t errT[2], errL[2], errC[2];
+  const int32_t* eb = io.ebot;
+  const int32_t* er = io.eright;
 #pragma unroll
-  for (int r = 0; r < 32; r++)
-    xa[r] = (r < nr && colok) ? __ldg(a + (int64_t)(r0 + r) * Wp + c0 + lane) : 0;
-  if (kind == BS_KNOWN) {
-#pragma unroll
-    for (int r = 0; r < 32; r++) {
-      if (r < nr && colok) {
-        if (ENC) out[(int64_t)(r0 + r) * Wp + c0 + lane] = xa[r];
-        else emit(r, xa[r]);
-      }
-    }
-    return;
+  for (int c = 0; c < 2; c++) {
+    errT[c] = (bi > 0 && colok) ? __ldcg(eb + (c * nblk + blk - io.nbx) * 32 + lane) : 0;
+    errL[c] = (bj > 0 && lane < nr) ? __ldcg(er + (c * nblk + blk - 1) * 32 + lane) : 0;
+    errC[c] = (bi > 0 && bj > 0) ? __ldcg(eb + (c * nblk + blk - io.nbx - 1) * 32 + 31) : 0;
   }
-  // ---- exact boundary from phase B
-  const int32_t* eb = io.ebot + comp * nblk * 32;
-  const int32_t* er = io.eright + comp * nblk * 32;
-  const int32_t top = (bi > 0 && colok) ? __ldcg(eb + (blk - io.nbx) * 32 + lane) : 0;
-  const int32_t left = (bj > 0 && lane < nr) ? __ldcg(er + (blk - 1) * 32 + lane) : 0;
-  const int32_t corner = (bi > 0 && bj > 0) ? __ldcg(eb + (blk - io.nbx - 1) * 32 + 31) : 0;
-  uint32_t e = 0, m = 0, M = 0;
-  if (ENC) {
-    const int code = cls >> 2;
-    e = (uint32_t)etab[code];
-    m = 2u * e;
-    M = mtab[code];
-  }
-#pragma unroll
-  for (int r = 0; r < 32; r++) x[r][lane] = ENC ? bs_negres(xa[r], m, M) : (uint32_t)xa[r];
-  v[0][lane + 1] = top;
-  v[lane + 1][0] = left;
-  if (lane == 0) v[0][0] = corner;
-  __syncwarp();
-  {  // row prefix (lane = row), then column prefix (lane = column)
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < 32; k++) {
-      acc = ENC ? bs_madd(acc, x[lane][k], m) : acc + x[lane][k];
-      x[lane][k] = acc;
-    }
-    __syncwarp();
-    acc = 0;
-#pragma unroll
-    for (int k = 0; k < 32; k++) {
-      acc = ENC ? bs_madd(acc, x[k][lane], m) : acc + x[k][lane];
-      x[k][lane] = acc;
-    }
-    __syncwarp();
-  }
-  if (!ENC) {
-#pragma unroll
-    for (int r = 0; r < 32; r++) {
-      if (r < nr && colok) {
-        const uint32_t val = (uint32_t)top + (uint32_t)v[r + 1][0] - (uint32_t)corner + x[r][lane];
-        emit(r, (int32_t)val);
-      }
-    }
-    return;
-  }
-  const uint32_t rt = bs_res(top, m, M), rc = bs_res(corner, m, M);
-  const uint32_t base = bs_msub(rt, rc, m);
-  const uint32_t rl = bs_res(left, m, M);   // lane r: row r's left residue
-  // representatives; a tie (residue e) is marked and resolved below
-  uint32_t tierows = 0;
-#pragma unroll
-  for (int r = 0; r < 32; r++) {
-    const uint32_t s = bs_madd(bs_madd(base, __shfl_sync(FULL, rl, r), m), x[r][lane], m);
-    const bool tie = s == e && r < nr && colok;
-    tierows |= (__any_sync(FULL, tie) ? 1u : 0u) << r;
-    v[r + 1][lane + 1] = tie ? INT32_MIN : bs_rep(s, e, m);
-  }
-  __syncwarp();
-  if (tierows) {
-    // raster order: a tie's sign follows x = R0 - (vU + vL - vUL), whose
-    // neighbours may be earlier ties
-#pragma unroll
-    for (int r = 0; r < 32; r++) {
-      if (!((tierows >> r) & 1u)) continue;   // warp-uniform
-      uint32_t tm = __ballot_sync(FULL, colok && v[r + 1][lane + 1] == INT32_MIN);
-      while (tm) {
-        const int j = __ffs(tm) - 1;
-        tm &= tm - 1u;
-        if (lane == j) {
-          const int64_t d = (int64_t)v[r][j + 1] + v[r + 1][j] - v[r][j];
-          v[r + 1][j + 1] = ((int64_t)xa[r] - d) > 0 ? (int32_t)e : -(int32_t)e;
-        }
-        __syncwarp();
-      }
+  // delta of the halo: row r0-1 (lane = column), column c0-1 (lane = row),
+  // the corner
+  int64_t dT[2] = {0, 0}, dL[2] = {0, 0}, dC[2] = {0, 0};
+  const int2* pv = io.prevrec;
+  if (bi > 0) {
+    const int2 pp = pv ? __ldg(pv + (int64_t)(r0 - 1) * Wp + j) : make_int2(0, 0);
+    dT[0] = colok ? (int64_t)fx(op[0], r0 - 1, j) - pp.x : 0;
+    dT[1] = colok ? (int64_t)fx(op[1], r0 - 1, j) - pp.y : 0;
+    if (bj > 0) {
+      const int2 pc = pv ? __ldg(pv + (int64_t)(r0 - 1) * Wp + c0 - 1) : make_int2(0, 0);
+      dC[0] = (int64_t)fx(op[0], r0 - 1, c0 - 1) - pc.x;
+      dC[1] = (int64_t)fx(op[1], r0 - 1, c0 - 1) - pc.y;
     }
   }
-  const int32_t radius = io.radius;
-  // every pixel of a regular block is a non-lossless Lorenzo pixel: row r's
-  // symbols are contiguous in the stream
+  if (bj > 0 && lane < nr) {
+    const int2 pl = pv ? __ldg(pv + (int64_t)(r0 + lane) * Wp + c0 - 1) : make_int2(0, 0);
+    dL[0] = (int64_t)fx(op[0], r0 + lane, c0 - 1) - pl.x;
+    dL[1] = (int64_t)fx(op[1], r0 + lane, c0 - 1) - pl.y;
+  }
+  // Z residues of the boundary (REG components)
+  uint32_t base[2] = {0u, 0u}, zL[2] = {0u, 0u};
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    if (!reg[c]) continue;
+    const uint32_t zT = bs_madd(bs_res(errT[c], m[c], M[c]), res_i64(dT[c], m[c], M[c], c32[c]), m[c]);
+    const uint32_t zC = bs_madd(bs_res(errC[c], m[c], M[c]), res_i64(dC[c], m[c], M[c], c32[c]), m[c]);
+    zL[c] = bs_madd(bs_res(errL[c], m[c], M[c]), res_i64(dL[c], m[c], M[c], c32[c]), m[c]);
+    base[c] = bs_msub(zT, zC, m[c]);
+  }
+  // the row above the current row: delta (low 32 bits suffice for R0, whose
+  // value fits int32 in a REG block) and err; the halo column of that row
+  int32_t dU[2] = {(int32_t)dT[0], (int32_t)dT[1]};
+  int32_t eU[2] = {errT[0], errT[1]};
+  int32_t dLU[2] = {(int32_t)dC[0], (int32_t)dC[1]};   // lane 0: halo of row i-1
+  int32_t eLU[2] = {errC[0], errC[1]};
   int64_t qb = 0;
   if (lane < nr)
     qb = io.qd_row_off[r0 + lane] +
-         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
-  int32_t* op = out + (int64_t)r0 * Wp + c0 + lane;
+         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj];
+  // row loads, three rows ahead (a four-slot register ring)
+  F bu[4], bv[4];
+  int2 bp[4];
+  auto issue = [&](int i, int sl) {
+    if (i < nr) {
+      bu[sl] = __ldg(op[0] + (int64_t)(r0 + i) * W + j);
+      bv[sl] = __ldg(op[1] + (int64_t)(r0 + i) * W + j);
+      bp[sl] = pv ? __ldg(pv + (int64_t)(r0 + i) * Wp + j) : make_int2(0, 0);
+    }
+  };
+  issue(0, 0);
+  issue(1, 1);
+  issue(2, 2);
+  for (int i0 = 0; i0 < nr; i0 += 4)
 #pragma unroll
-  for (int r = 0; r < 32; r++, op += Wp) {
-    const int64_t qr = __shfl_sync(FULL, qb, r);
-    if (r < nr && colok) {
-      // x + err = q * 2e exactly; int32 is exact here (|R0| < 2^30 in a
-      // regular block, |vU + vL - vUL - err| < 2^30)
-      const int32_t err = v[r + 1][lane + 1];
-      const int32_t d = v[r][lane + 1] + v[r + 1][lane] - v[r][lane];
-      const int32_t n = xa[r] - d + err;
+  for (int kk = 0; kk < 4; kk++) {
+    const int i = i0 + kk;
+    if (i >= nr) break;
+    issue(i + 3, (kk + 3) & 3);
+    const int32_t ou = fixed_t(bu[kk], io.S), ov = fixed_t(bv[kk], io.S);
+    const int2 pp = bp[kk];
+    const int32_t o[2] = {ou, ov};
+    const int32_t pr[2] = {pp.x, pp.y};
+    int32_t err[2], R0[2], errLi[2], dLi[2];
+    uint32_t sym[2] = {0u, 0u};
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int64_t d64 = (int64_t)o[c] - pr[c];
+      const int32_t d32 = (int32_t)d64;
+      dLi[c] = __shfl_sync(FULL, (int32_t)dL[c], i);
+      errLi[c] = __shfl_sync(FULL, errL[c], i);
+      int32_t dl = __shfl_up_sync(FULL, d32, 1);
+      int32_t dul = __shfl_up_sync(FULL, dU[c], 1);
+      if (lane == 0) { dl = dLi[c]; dul = dLU[c]; }
+      R0[c] = d32 - dU[c] - dl + dul;
+      if (reg[c]) {
+        const uint32_t zl = __shfl_sync(FULL, zL[c], i);
+        const uint32_t sres = bs_msub(bs_madd(base[c], zl, m[c]),
+                                      res_i64(d64, m[c], M[c], c32[c]), m[c]);
+        const bool tie = colok && sres == e[c];
+        err[c] = bs_rep(sres, e[c], m[c]);
+        uint32_t tm = __ballot_sync(FULL, tie);
+        if (tm) {
+          // raster order within the row: a tie's sign follows
+          // x = R0 - (errU + errL - errUL)
+          int32_t cur = tie ? 0 : err[c];
+          while (tm) {
+            const int jj = __ffs(tm) - 1;
+            tm &= tm - 1u;
+            int32_t el = __shfl_up_sync(FULL, cur, 1);
+            int32_t eul = __shfl_up_sync(FULL, eU[c], 1);
+            if (lane == 0) { el = errLi[c]; eul = eLU[c]; }
+            if (lane == jj) {
+              const int64_t x = (int64_t)R0[c] - ((int64_t)eU[c] + el - eul);
+              cur = x > 0 ? (int32_t)e[c] : -(int32_t)e[c];
+            }
+          }
+          err[c] = cur;
+        }
+      } else {
+        err[c] = colok ? __ldcg(io.out[c] + (int64_t)(r0 + i) * Wp + j) : 0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      if (!reg[c]) continue;
+      int32_t el = __shfl_up_sync(FULL, err[c], 1);
+      int32_t eul = __shfl_up_sync(FULL, eU[c], 1);
+      if (lane == 0) { el = errLi[c]; eul = eLU[c]; }
+      // x + err = q * m exactly (|R0| < 2^30 in a REG block)
+      const int32_t n = R0[c] + err[c] - eU[c] - el + eul;
       const uint32_t an = (uint32_t)(n < 0 ? -n : n);
-      uint32_t qa = __umulhi(an, M);
-      if (qa * m != an) qa++;
+      uint32_t qa = __umulhi(an, M[c]);
+      if (qa * m[c] != an) qa++;
       const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
-      *op = err;
-      io.qd[qr + 2 * lane] = (uint16_t)(q + radius);
+      sym[c] = (uint32_t)(q + io.radius);
+    }
+    const int64_t qr = __shfl_sync(FULL, qb, i);
+    if (colok) {
+      io.rec[(int64_t)(r0 + i) * Wp + j] = make_int2(o[0] + err[0], o[1] + err[1]);
+      if (reg[0] && reg[1])
+        *reinterpret_cast<uint32_t*>(io.qd + qr + 2 * lane) = sym[0] | (sym[1] << 16);
+      else if (reg[0])
+        io.qd[qr + 2 * lane] = (uint16_t)sym[0];
+      else if (reg[1])
+        io.qd[qr + 2 * lane + 1] = (uint16_t)sym[1];
+    }
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      dU[c] = (int32_t)((int64_t)o[c] - pr[c]);
+      eU[c] = colok ? err[c] : 0;
+      dLU[c] = dLi[c];
+      eLU[c] = errLi[c];
     }
   }
 }
 
-template <bool ENC>
-cudaError_t launch_bs_local(const BScanIO& io, cudaStream_t st) {
-  bs_local_kernel<ENC><<<dim3(io.nbx, io.nby), 64, 0, st>>>(io);
-  return cudaGetLastError();
+// Decoder: the interior of block (bi, bj), both components, by one warp
+// (lane = column, rows streamed).  REG: Z = ZU + ZL - ZUL + A, i.e. per row
+// Z(i, j) = Z(i-1, j) + (ZL(i) - ZL(i-1)) + sum_{b<=j} A(i, b) (warp scan;
+// wrapping uint32 arithmetic is exact, the result fits int32) with A =
+// (sym - radius) * 2e; SLOW: Z from the chain's sweep; KNOWN: written by the
+// block kernel (dec_block.cu).  recon = recon(t-1) + Z goes out as (u, v)
+// pairs, float64 (codec.py:425-426 recon * (1/S), exact) and optionally
+// int64.
+__device__ __forceinline__ void bs_final_dec(const BScanIO& io, int bi, int bj,
+                                             int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int Wp = io.Wp, W = io.W;
+  int kind[2];
+#pragma unroll
+  for (int c = 0; c < 2; c++) kind[c] = __ldcg(io.cls + c * nblk + blk) & 3;
+  const bool known[2] = {kind[0] == BS_KNOWN, kind[1] == BS_KNOWN};
+  if (known[0] && known[1]) return;
+  const bool reg[2] = {kind[0] == BS_REG, kind[1] == BS_REG};
+  const bool colok = lane < ncl;
+  const int j = c0 + (colok ? lane : ncl - 1);
+  int32_t zU[2], zL[2], zLp[2];
+  const int32_t* eb = io.ebot;
+  const int32_t* er = io.eright;
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    zU[c] = (bi > 0 && colok) ? __ldcg(eb + (c * nblk + blk - io.nbx) * 32 + lane) : 0;
+    zL[c] = (bj > 0 && lane < nr) ? __ldcg(er + (c * nblk + blk - 1) * 32 + lane) : 0;
+    zLp[c] = (bi > 0 && bj > 0) ? __ldcg(eb + (c * nblk + blk - io.nbx - 1) * 32 + 31) : 0;
+  }
+  int64_t qb = 0;
+  if (lane < nr)
+    qb = io.qd_row_off[r0 + lane] +
+         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj];
+  const bool any_reg = reg[0] || reg[1];
+  const int2* pv = io.prevrec;
+  int32_t* recw = reinterpret_cast<int32_t*>(io.rec);
+  // row loads, three rows ahead (a four-slot register ring)
+  uint32_t bsy[4] = {0u, 0u, 0u, 0u};
+  int bcd[4] = {0, 0, 0, 0};
+  int2 bpp[4];
+  auto issue = [&](int i, int sl) {
+    const int ic = min(i, nr - 1);
+    const int64_t qr = __shfl_sync(FULL, qb, ic);
+    if (i < nr) {
+      if (any_reg) {
+        bsy[sl] = colok ? __ldg(reinterpret_cast<const uint32_t*>(io.qd + qr) + lane) : 0u;
+        bcd[sl] = __ldg(io.codes + (int64_t)(r0 + i) * io.cpitch + j);
+      }
+      bpp[sl] = pv ? __ldg(pv + (int64_t)(r0 + i) * Wp + j) : make_int2(0, 0);
+    }
+  };
+  issue(0, 0);
+  issue(1, 1);
+  issue(2, 2);
+  for (int i0 = 0; i0 < nr; i0 += 4)
+#pragma unroll
+  for (int kk = 0; kk < 4; kk++) {
+    const int i = i0 + kk;
+    if (i >= nr) break;
+    issue(i + 3, (kk + 3) & 3);
+    const uint32_t sy = bsy[kk];
+    const int cd = bcd[kk];
+    const int2 pp = bpp[kk];
+    const int32_t pr[2] = {pp.x, pp.y};
+    int32_t z[2];
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int32_t zl = __shfl_sync(FULL, zL[c], i);
+      if (reg[c]) {
+        const uint32_t e2 = 2u * (uint32_t)io.e_tab[cd & 31];
+        const uint32_t s16 = c ? (sy >> 16) : (sy & 0xffffu);
+        uint32_t acc = colok ? (uint32_t)((int32_t)s16 - io.radius) * e2 : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, acc, o);
+          if (lane >= o) acc += y;
+        }
+        z[c] = (int32_t)((uint32_t)zU[c] + (uint32_t)zl - (uint32_t)zLp[c] + acc);
+      } else if (!known[c]) {
+        z[c] = colok ? __ldcg(io.out[c] + (int64_t)(r0 + i) * Wp + j) : 0;
+      } else {
+        z[c] = 0;
+      }
+      zU[c] = z[c];
+      zLp[c] = zl;
+    }
+    if (colok) {
+      const int64_t pk = (int64_t)(r0 + i) * Wp + j;
+      const int32_t ru = (int32_t)((uint32_t)z[0] + (uint32_t)pr[0]);
+      const int32_t rv = (int32_t)((uint32_t)z[1] + (uint32_t)pr[1]);
+      const int64_t ko = (int64_t)(r0 + i) * W + j;
+      if (!known[0] && !known[1]) {
+        io.rec[pk] = make_int2(ru, rv);
+      } else if (!known[0]) {
+        recw[2 * pk] = ru;
+      } else {
+        recw[2 * pk + 1] = rv;
+      }
+      if (!known[0]) {
+        io.f64[0][ko] = __dmul_rn((double)ru, io.inv_S);
+        if (io.fix[0]) io.fix[0][ko] = ru;
+      }
+      if (!known[1]) {
+        io.f64[1][ko] = __dmul_rn((double)rv, io.inv_S);
+        if (io.fix[1]) io.fix[1][ko] = rv;
+      }
+    }
+  }
 }
 
-template <bool ENC>
+template <bool ENC, typename F = float>
 cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   const size_t smem = sizeof(BSChainSmem);
   cudaError_t e = cudaFuncSetAttribute(
-      bs_chain_kernel<ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      bs_chain_kernel<ENC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC>,
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC, F>,
                                                     32 * BS_NW, smem);
   if (e != cudaSuccess) return e;
-  const int ntask = bs_ntask(io.nby) +
-                    2 * io.nby * ((io.nbx + BS_SEG - 1) / BS_SEG);
+  const int nseg = (io.nbx + BS_SEG - 1) / BS_SEG;
+  const int ntask = bs_ntask(io.nby) + io.nby * nseg;
   // persistent: every CTA is resident; tickets hand out the chain tasks
   // (block-row order) first, then the interior tasks
-  bs_chain_kernel<ENC><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
+  bs_chain_kernel<ENC, F><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,8 @@ cudaError_t launch_range(const F*, const F*, int64_t, double*, int,
 template <typename F>
 cudaError_t launch_analyze(const F*, const F*, int, int, int, double, int64_t,
                            uint8_t*, uint32_t*, uint16_t*, int32_t*,
-                           cudaStream_t);
+                           uint64_t*, unsigned long long*, int*,
+                           unsigned long long, int, cudaStream_t);
 cudaError_t launch_row_scan(const int32_t*, int64_t, int, int, int64_t*,
                             cudaStream_t);
 // encode.cu
@@ -59,27 +60,21 @@ template <typename SYM>
 cudaError_t launch_chunk_prefix(const uint8_t*, const SYM*, const int64_t*,
                                 int64_t, int, int, int64_t, int32_t*,
                                 int32_t*, cudaStream_t);
+// enc_block.cu
 template <typename F>
-cudaError_t launch_enc_r0(const F*, const F*, const uint8_t*, const int32_t*,
-                          const int32_t*, const PrepParams&, const BScanIO&,
-                          int32_t*, int32_t*, int32_t*, uint8_t*, int*,
-                          cudaStream_t);
-template <typename F>
-cudaError_t launch_enc_mop(const F*, const F*, const int32_t*, const int32_t*,
-                           const int32_t*, const PrepParams&, const double*,
-                           uint8_t*, cudaStream_t);
-template <typename F>
-cudaError_t launch_enc_pix(const F*, const F*, const uint8_t*, const int32_t*,
-                           const int64_t*, const int32_t*, const PrepParams&,
-                           const uint8_t*, const BScanIO&, int32_t*, int32_t*,
-                           uint32_t*, uint32_t*, uint32_t*, uint16_t*,
-                           int32_t*, cudaStream_t);
+cudaError_t launch_enc_block(const F*, const F*, const uint8_t*,
+                             const int32_t*, int32_t*, const PrepParams&,
+                             const BScanIO&, const double*, uint8_t*,
+                             const int64_t*, const int32_t*, uint16_t*,
+                             int32_t*, int*, cudaStream_t);
+// dec_block.cu
 template <typename SYM>
-cudaError_t launch_dec_prep(const uint8_t*, const SYM*, const int64_t*,
-                            const uint8_t*, const int32_t*, const int32_t*,
-                            const int64_t*, const int64_t*, const int32_t*,
-                            const int32_t*, const PrepParams&, int32_t*,
-                            int32_t*, uint32_t*, uint32_t*, cudaStream_t);
+cudaError_t launch_dec_block(const uint8_t*, const SYM*, const int64_t*,
+                             const uint8_t*, const int32_t*, int32_t*,
+                             const int64_t*, const int64_t*, const int32_t*,
+                             const int32_t*, const PrepParams&, const BScanIO&,
+                             uint32_t*, uint32_t*, double*, double*, int64_t*,
+                             int64_t*, double, cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -217,21 +212,20 @@ __global__ void widen_kernel(const I* a, const I* b, int64_t n, int64_t* oa,
   }
 }
 
-// Fast path, optional recon output: recon(t) = fixed(orig(t)) + err(t) as
-// int64 [2][T][H][W] (the layout of the generic path's widen_kernel).
-template <typename F>
-__global__ void recon_out_kernel(const F* __restrict__ u, const F* __restrict__ v,
-                                 const int32_t* __restrict__ eu,
-                                 const int32_t* __restrict__ ev, int H, int W,
-                                 int Wp, double S, int t, int64_t N,
-                                 int64_t* __restrict__ recon) {
+// Fast path, optional recon output: recon(t) from the (u, v) pair plane
+// (pitch Wp) as int64 [2][T][H][W] (the layout of the generic path's
+// widen_kernel).
+__global__ void recon_pairs_kernel(const int2* __restrict__ rec, int H, int W,
+                                   int Wp, int t, int64_t N,
+                                   int64_t* __restrict__ recon) {
   const int64_t HW = (int64_t)H * W;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < HW;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = k / W, j = k - i * W, m = i * Wp + j;
+    const int64_t i = k / W, j = k - i * W;
+    const int2 r = rec[i * Wp + j];
     const int64_t g = (int64_t)t * HW + k;
-    recon[g] = (int64_t)fixed_t(u[g], S) + eu[m];
-    recon[N + g] = (int64_t)fixed_t(v[g], S) + ev[m];
+    recon[g] = r.x;
+    recon[N + g] = r.y;
   }
 }
 
@@ -458,6 +452,7 @@ int bscan_setup(Scratch& sc, const Ladder& lad, int H, int W, int radius,
     const int64_t e = lad.e[k];
     b->e_tab[k] = (int32_t)e;
     b->mag_tab[k] = e > 0 ? (uint32_t)((((uint64_t)1) << 32) / (2 * (uint64_t)e)) : 0u;
+    b->c32_tab[k] = e > 0 ? (uint32_t)((((uint64_t)1) << 32) % (2 * (uint64_t)e)) : 0u;
   }
   return VFCP_OK;
 }
@@ -524,24 +519,24 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
                 const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
                 uint8_t* modes, int32_t* row_ll, int64_t* recon,
                 cudaStream_t st, bool* overflowed, HostOut* ho) {
+  // per frame: enc_block_kernel (enc_block.cu: tiles, MoP, SL blocks,
+  // block classes and edges) then the block-scan chain with the interior
+  // pass (bscan.cuh), which writes recon(t) and the Lorenzo symbols
   const int H = p->H, W = p->W, T = p->T;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
   const int nby = (H + 31) / 32;
   const int64_t nblk = (int64_t)nchunks * nby;
+  const int64_t HW = (int64_t)H * W;
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
-  uint8_t* codes_p;
-  CK(sc.get(&codes_p, (size_t)plane));
-  int32_t *pre_nl, *a, *err, *prevrec;
-  uint32_t* pins;
+  int32_t *pre_nl, *a, *out, *rec;
   int *ticket, *ovf;
   double* log2tab = nullptr;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
-  CK(sc.get(&a, (size_t)2 * plane));
-  CK(sc.get(&err, (size_t)4 * plane));
-  CK(sc.get(&prevrec, (size_t)2 * plane));
-  CK(sc.get(&pins, (size_t)3 * cplane));
+  CK(sc.get(&a, (size_t)2 * plane));      // R0 of swept blocks
+  CK(sc.get(&out, (size_t)2 * plane));    // err of swept blocks
+  CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
   CK(sc.get(&ticket, (size_t)T));
   CK(sc.get(&ovf, 1));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
@@ -573,40 +568,38 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     if (rc) return rc;
   }
   bio.a[0] = a; bio.a[1] = a + plane;
-  bio.codes = codes_p;
-  bio.pin[0] = pins; bio.pin[1] = pins + cplane;
+  bio.a_w[0] = a; bio.a_w[1] = a + plane;
+  bio.out[0] = out; bio.out[1] = out + plane;
   bio.qd = qd;
-  bio.nlw = pins + 2 * cplane;
+  bio.cpitch = W;
+  bio.S = p->scale;
   if (getenv("VFCP_CHAIN_STAMPS")) CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
-    int32_t* eprev = err + 2 * plane * ((t + 1) & 1);
-    int32_t* ecur = err + 2 * plane * (t & 1);
+    int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
+    int32_t* rcur = rec + 2 * plane * (t & 1);
     uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
     LAUNCH(K_PREP, st,
-           launch_enc_r0<F>(u, v, codes, eprev, eprev + plane, pp, bio, a,
-                            a + plane, prevrec, codes_p, ovf, st));
-    if (pp.mop)
-      LAUNCH(K_MOP, st,
-             launch_enc_mop<F>(u, v, a, a + plane, prevrec, pp, log2tab,
-                               modes_t, st));
-    LAUNCH(K_PIX, st,
-           launch_enc_pix<F>(u, v, codes_p, prevrec, qd_row_off, pre_nl, pp,
-                             modes_t, bio, a, a + plane, pins, pins + cplane,
-                             pins + 2 * cplane, qd, row_ll, st));
-    bio.out[0] = ecur; bio.out[1] = ecur + plane;
+           launch_enc_block<F>(u, v, codes + (size_t)t * HW,
+                               t > 0 ? rprev : nullptr, rcur, pp, bio, log2tab,
+                               modes_t, qd_row_off, pre_nl, qd, row_ll, ovf, st));
+    bio.codes = codes + (size_t)t * HW;
+    bio.orig[0] = u + (size_t)t * HW;
+    bio.orig[1] = v + (size_t)t * HW;
+    bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
+    bio.rec = reinterpret_cast<int2*>(rcur);
     bio.ticket = ticket + t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.row_ll = row_ll + (size_t)t * H;
     bio.frame_tag = (uint32_t)t + 1u;
-    LAUNCH(K_BSC, st, launch_bs_chain<true>(bio, nsm, st));
+    LAUNCH(K_BSC, st, (launch_bs_chain<true, F>(bio, nsm, st)));
     if (bio.stamps && t == 1) print_chain_stamps(bio, st);
     if (recon)
       LAUNCH(K_AUX, st,
-             (recon_out_kernel<F><<<1184, 256, 0, st>>>(
-                  u, v, ecur, ecur + plane, H, W, Wp, p->scale, t,
+             (recon_pairs_kernel<<<1184, 256, 0, st>>>(
+                  reinterpret_cast<const int2*>(rcur), H, W, Wp, t,
                   (int64_t)H * W * T, recon),
               cudaGetLastError()));
     {
@@ -662,6 +655,9 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                 const int64_t* qd_row_off, const int64_t* ll_row_off,
                 double* out_u, double* out_v, int64_t* fix_u, int64_t* fix_v,
                 cudaStream_t st, DecHostOut* ho) {
+  // per frame: dec_block_kernel (dec_block.cu: symbols, ll values, SL and
+  // KNOWN blocks, block classes and edges) then the block-scan chain with
+  // the interior pass (bscan.cuh), which writes recon(t) and the output
   const int H = p->H, W = p->W, T = p->T;
   const int64_t HW = (int64_t)H * W;
   const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
@@ -670,13 +666,14 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
   const int nsm = nsm_of();
   Scratch sc(st);
-  int32_t *pre_nl, *pre_ll, *a, *rec;
+  int32_t *pre_nl, *pre_ll, *a, *out, *rec;
   uint32_t* pins;
   int* ticket;
   CK(sc.get(&pre_nl, (size_t)T * cplane));
   CK(sc.get(&pre_ll, (size_t)T * cplane));
-  CK(sc.get(&a, (size_t)2 * plane));
-  CK(sc.get(&rec, (size_t)4 * plane));
+  CK(sc.get(&a, (size_t)2 * plane));      // A / Z of swept blocks
+  CK(sc.get(&out, (size_t)2 * plane));    // Z of swept blocks
+  CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
   CK(sc.get(&pins, (size_t)2 * cplane));
   CK(sc.get(&ticket, (size_t)T));
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
@@ -691,29 +688,36 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     if (rc) return rc;
   }
   bio.a[0] = a; bio.a[1] = a + plane;
+  bio.a_w[0] = a; bio.a_w[1] = a + plane;
+  bio.out[0] = out; bio.out[1] = out + plane;
   bio.pin[0] = pins; bio.pin[1] = pins + cplane;
+  bio.qd = const_cast<uint16_t*>(qd);
+  bio.cpitch = W;
+  bio.inv_S = 1.0 / p->scale;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
     int32_t* rcur = rec + 2 * plane * (t & 1);
     LAUNCH(K_DROWS, st,
-           launch_dec_prep<uint16_t>(
-               codes, qd, ll,
-               t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr, rprev,
-               rprev + plane, qd_row_off, ll_row_off, pre_nl, pre_ll, pp, a,
-               a + plane, pins, pins + cplane, st));
-    bio.out[0] = rcur; bio.out[1] = rcur + plane;
+           launch_dec_block<uint16_t>(
+               codes + (size_t)t * HW, qd, ll,
+               t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,
+               t > 0 ? rprev : nullptr, rcur, qd_row_off, ll_row_off, pre_nl,
+               pre_ll, pp, bio, pins, pins + cplane, out_u, out_v, fix_u,
+               fix_v, bio.inv_S, st));
+    bio.codes = codes + (size_t)t * HW;
+    bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
+    bio.rec = reinterpret_cast<int2*>(rcur);
     bio.ticket = ticket + t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
+    bio.qd_row_off = qd_row_off + (size_t)t * H;
+    bio.pre_nl = pre_nl + (size_t)t * cplane;
     bio.f64[0] = out_u + (size_t)t * HW;
     bio.f64[1] = out_v + (size_t)t * HW;
     bio.fix[0] = fix_u ? fix_u + (size_t)t * HW : nullptr;
     bio.fix[1] = fix_v ? fix_v + (size_t)t * HW : nullptr;
-    bio.inv_S = 1.0 / p->scale;
-    bio.prev[0] = t > 0 ? rprev : nullptr;
-    bio.prev[1] = t > 0 ? rprev + plane : nullptr;
-    LAUNCH(K_BSL, st, launch_bs_local<false>(bio, st));
     bio.frame_tag = (uint32_t)t + 1u;
+    bio.pin[0] = pins; bio.pin[1] = pins + cplane;
     LAUNCH(K_BSC, st, launch_bs_chain<false>(bio, nsm, st));
     {
       const int rh = ho->frame(t, HW, out_u, out_v, st);
@@ -844,16 +848,28 @@ int vfcp_analyze(const vfcp_params* p, const void* u, const void* v,
   const int64_t N = (int64_t)p->H * p->W * p->T;
   CK(cudaMemsetAsync(ld_words, 0, sizeof(uint32_t) * ((N + 31) / 32), st));
   CK(cudaMemsetAsync(row_n31, 0, sizeof(int32_t) * (size_t)p->T * p->H, st));
+  // the anchors that need exact work (analyze.cu cube_kernel); a fuller
+  // list falls back to the fused kernel
+  const unsigned long long cap =
+      (unsigned long long)std::min<int64_t>(N, (int64_t)1 << 25);
+  Scratch sc(st);
+  uint64_t* list;
+  unsigned long long* count;
+  int* ovf;
+  CK(sc.get(&list, (size_t)cap));
+  CK(sc.get(&count, 1));
+  CK(sc.get(&ovf, 1));
+  const int nsm = nsm_of();
   if (dtype == VFCP_F32)
     LAUNCH(K_ANALYZE, st,
            launch_analyze((const float*)u, (const float*)v, p->H, p->W, p->T,
                           p->scale, p->tau, codes, ld_words, mask, row_n31,
-                          st));
+                          list, count, ovf, cap, nsm, st));
   else
     LAUNCH(K_ANALYZE, st,
            launch_analyze((const double*)u, (const double*)v, p->H, p->W,
                           p->T, p->scale, p->tau, codes, ld_words, mask,
-                          row_n31, st));
+                          row_n31, list, count, ovf, cap, nsm, st));
   return VFCP_OK;
 }
 
