@@ -238,6 +238,9 @@ def main():
     ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decompress", action="store_true")
+    ap.add_argument("--eps-sweep", type=float, nargs="*", default=[1e-2, 1e-4],
+                    help="extra eps of the same field (BASELINE config 5: "
+                         "1e-2, 1e-3, 1e-4), device-resident timings")
     ap.add_argument("--quick", action="store_true",
                     help="device-resident timings only (no e2e / entropy legs)")
     ap.add_argument("--ref-sample", type=int, nargs=3, default=(1024, 1024, 4))
@@ -331,6 +334,48 @@ def main():
                "gpu_launches": dlaunch,
                "kernels_ms": {k: round(v[0] / args.steps, 3)
                               for k, v in dprof.items() if v[1]}}
+
+    # ---- the BASELINE eps sweep of this config on the same field (device-
+    # resident timings, W warm-up + K timed steps each): extra keys
+    sweep = {}
+    for e_x in args.eps_sweep:
+        if e_x == args.eps:
+            continue
+        for _ in range(args.warmup):
+            sx = vg.compress_device(f_dev, e_x, cfg, relative=True)
+        barrier()
+        e0.record(st)
+        for _ in range(args.steps):
+            sx = None
+            sx = vg.compress_device(f_dev, e_x, cfg, relative=True)
+        e1.record(st)
+        barrier()
+        cx = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        nbm = max(1, int(sx.modes.numel()))
+        ent = {"compress_GBps": round(8.0 * N * world / (cx * 1e-3) / 1e9, 3),
+               "compress_ms": round(cx, 3),
+               "sl_block_frac": round(float(sx.modes.sum().item()) / nbm, 4)}
+        if not args.no_decompress:
+            am = codec.Archive(H, W, T, 1.0, 1.0, 1.0, sx.scale, sx.eps, sx.tau,
+                               cfg, b"", b"", sx.ld.cpu().numpy().tobytes(),
+                               b"", b"")
+            kx = dict(codes=sx.codes, qd=sx.qd, ll=sx.ll, modes=sx.modes, ld=sx.ld)
+            for _ in range(args.warmup):
+                vg.decompress_device(am, **kx)
+            barrier()
+            out = None
+            e0.record(st)
+            for _ in range(args.steps):
+                out = None
+                out = vg.decompress_device(am, **kx)
+            e1.record(st)
+            barrier()
+            dx = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+            del out
+            ent.update(decompress_GBps=round(8.0 * N * world / (dx * 1e-3) / 1e9, 3),
+                       decompress_ms=round(dx, 3))
+        sweep[str(e_x)] = ent
+        del sx
 
     e2e_s = arc_s = ent_s = None
     d2h = arc_bytes = 0
@@ -444,6 +489,8 @@ def main():
         "gpu_launches": launches // max(1, steps),
         "clocks": clk,
     }
+    if sweep:
+        line["eps_sweep"] = sweep
     if e2e_s is not None:
         line["e2e"] = {"value": round(8.0 * N * world / e2e_s / 1e9, 3),
                        "unit": UNIT, "h2d_bytes_per_step": 8 * N,

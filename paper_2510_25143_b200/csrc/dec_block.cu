@@ -25,6 +25,8 @@ struct DecBlockSmem {
   uint32_t colsum[2][DB_NW][32];   // per warp: column sums of A (REG edges)
   uint32_t rowsum[2][32];      // row sums of A
   int anypin[2], notall[2];
+  int32_t etab[32];            // e per code
+  alignas(16) int2 pv[SLT][SLT];   // recon(t-1) tile (semi-Lagrangian blocks)
 };
 
 template <typename SYM>
@@ -60,29 +62,38 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
   const int64_t fbase = (int64_t)p.t * H * W;
   int32_t* recw = reinterpret_cast<int32_t*>(rec);
   if (tid < 2) { sm.anypin[tid] = 0; sm.notall[tid] = 0; }
+  if (tid < 32) sm.etab[tid] = bio.e_tab[tid];
+  if (sl_blk) load_prev_tile(sm.pv, prev, H, W, Wp, r0, c0, tid, 32 * DB_NW);
+  __syncthreads();
 
   // ---- warp w: rows w, w+8, ... (lane = column); the loads of all four
-  // rows are issued together, in three dependent rounds: codes and stream
-  // offsets; symbols; ll values and recon(t-1) where needed
+  // rows are issued together, in dependent rounds: codes and the rows'
+  // stream offsets (lane q loads row q's, then shuffled); symbols; ll values
+  // and recon(t-1) only for rows with a pinned pixel (and SL blocks)
   constexpr int NR = 32 / DB_NW;
+  const int32_t* etab = sm.etab;
   int cd[NR];
-  int64_t qoff[NR], loff[NR];
+  int64_t qo = 0, lo = 0;   // lane q < NR: offsets of row wid + DB_NW * q
+  if (lane < NR) {
+    const int i = min(wid + DB_NW * lane, nr - 1);
+    const int64_t row = rowbase + r0 + i;
+    qo = qd_row_off[row] + 2 * (int64_t)pre_nl[row * nchunks + bj];
+  }
 #pragma unroll
   for (int q = 0; q < NR; q++) {
     const int i = min(wid + DB_NW * q, nr - 1);
-    const int64_t row = rowbase + r0 + i;
-    cd[q] = (wid + DB_NW * q < nr && colok) ? codes_t[(int64_t)(r0 + i) * W + j] : CODE_LOSSLESS;
-    qoff[q] = qd_row_off[row] + 2 * (int64_t)pre_nl[row * nchunks + bj];
-    loff[q] = ll_row_off[row] + pre_ll[row * nchunks + bj];
+    cd[q] = (wid + DB_NW * q < nr && colok) ? __ldg(codes_t + (int64_t)(r0 + i) * W + j) : CODE_LOSSLESS;
   }
   uint32_t sy[NR];
+  bool nlq[NR];
 #pragma unroll
   for (int q = 0; q < NR; q++) {
-    const bool nl = p.lad.e[cd[q]] != 0;
-    const unsigned bnl = __ballot_sync(FULL, nl);
+    nlq[q] = colok && etab[cd[q] & 31] != 0;
+    const unsigned bnl = __ballot_sync(FULL, nlq[q]);
+    const int64_t qoff = __shfl_sync(FULL, qo, q);
     sy[q] = 0u;
-    if (nl) {
-      const int64_t k = qoff[q] + 2 * __popc(bnl & lt);
+    if (nlq[q]) {
+      const int64_t k = qoff + 2 * __popc(bnl & lt);
       if (sizeof(SYM) == 2)
         sy[q] = __ldg(reinterpret_cast<const uint32_t*>(qd + k));
       else
@@ -92,22 +103,35 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
   int32_t lu[NR], lv[NR];
   int2 pp[NR];
   unsigned peu[NR], pev[NR];
+  unsigned pinrows = 0;
 #pragma unroll
   for (int q = 0; q < NR; q++) {
     const int i = wid + DB_NW * q;
     const bool rv = i < nr;
-    const bool nl = colok && p.lad.e[cd[q]] != 0;
     const uint32_t syu = sy[q] & 0xffffu, syv = sy[q] >> 16;
-    const bool eu = rv && ((colok && !nl) || (nl && syu == 0));
-    const bool ev = rv && ((colok && !nl) || (nl && syv == 0));
+    const bool eu = rv && ((colok && !nlq[q]) || (nlq[q] && syu == 0));
+    const bool ev = rv && ((colok && !nlq[q]) || (nlq[q] && syv == 0));
     peu[q] = __ballot_sync(FULL, eu);
     pev[q] = __ballot_sync(FULL, ev);
-    int64_t lidx = loff[q] + __popc(peu[q] & lt) + __popc(pev[q] & lt);
+    if (peu[q] | pev[q]) pinrows |= 1u << q;
+  }
+  if (pinrows && lane < NR) {
+    const int i = min(wid + DB_NW * lane, nr - 1);
+    const int64_t row = rowbase + r0 + i;
+    lo = ll_row_off[row] + pre_ll[row * nchunks + bj];
+  }
+#pragma unroll
+  for (int q = 0; q < NR; q++) {
+    const int i = wid + DB_NW * q;
     lu[q] = 0;
     lv[q] = 0;
-    if (eu) { lu[q] = (int32_t)ll[lidx]; lidx++; }
-    if (ev) lv[q] = (int32_t)ll[lidx];
-    pp[q] = (rv && has_prev && (sl_blk || eu || ev))
+    const bool eu = (peu[q] >> lane) & 1u, ev = (pev[q] >> lane) & 1u;
+    if ((pinrows >> q) & 1u) {
+      int64_t lidx = __shfl_sync(FULL, lo, q) + __popc(peu[q] & lt) + __popc(pev[q] & lt);
+      if (eu) { lu[q] = (int32_t)ll[lidx]; lidx++; }
+      if (ev) lv[q] = (int32_t)ll[lidx];
+    }
+    pp[q] = (i < nr && has_prev && (sl_blk || eu || ev))
                 ? __ldg(prev + (int64_t)(r0 + min(i, nr - 1)) * Wp + j)
                 : make_int2(0, 0);
   }
@@ -118,7 +142,7 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
   if (sl_blk) {
     // every pixel known: the SL predictions (two rows at a time so their
     // gathers overlap), recon, the float64 output, Z edges
-    const PairPlane src{prev, Wp};
+    const TileSrc src{sm.pv, r0 - SLH, c0 - SLH, prev, Wp};
 #pragma unroll
     for (int q0 = 0; q0 < NR; q0 += 2) {
       int64_t pu[2] = {0, 0}, pv[2] = {0, 0};
@@ -127,7 +151,7 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
       for (int h = 0; h < 2; h++) {
         const int q = q0 + h;
         const int i = min(wid + DB_NW * q, nr - 1);
-        need[h] = wid + DB_NW * q < nr && colok && p.lad.e[cd[q]] != 0 &&
+        need[h] = wid + DB_NW * q < nr && nlq[q] &&
                   !(((peu[q] & pev[q]) >> lane) & 1u);
         if (__any_sync(FULL, need[h]))
           slow[h] = !sl_predict_rk2(src, H, W, r0 + i, j, p.cfl_x, p.cfl_y,
@@ -139,9 +163,9 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
         const int i = wid + DB_NW * q;
         if (i >= nr) break;   // warp-uniform
         if (slow[h] && need[h])
-          sl_predict2(src, H, W, r0 + i, j, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
-                      &pu[h], &pv[h]);
-        const int64_t two_e = 2 * p.lad.e[cd[q]];
+          sl_general(prev, Wp, H, W, r0 + i, j, p.cfl_x, p.cfl_y, p.d_max,
+                     p.n_max, &pu[h], &pv[h]);
+        const int64_t two_e = 2 * (int64_t)etab[cd[q] & 31];
         const bool eu = (peu[q] >> lane) & 1u, ev = (pev[q] >> lane) & 1u;
         const int64_t qu = (int64_t)(sy[q] & 0xffffu) - p.radius;
         const int64_t qv = (int64_t)(sy[q] >> 16) - p.radius;
@@ -173,7 +197,7 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
       a[0][q] = a[1][q] = 0u;
       if (i >= nr) continue;   // warp-uniform
       const bool eu = (peu[q] >> lane) & 1u, ev = (pev[q] >> lane) & 1u;
-      const int64_t two_e = 2 * p.lad.e[cd[q]];
+      const int64_t two_e = 2 * (int64_t)etab[cd[q] & 31];
       const int64_t qu = (int64_t)(sy[q] & 0xffffu) - p.radius;
       const int64_t qv = (int64_t)(sy[q] >> 16) - p.radius;
       a[0][q] = colok ? (eu ? (uint32_t)(lu[q] - pp[q].x) : (uint32_t)(qu * two_e)) : 0u;
@@ -198,7 +222,6 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
     }
     return;
   }
-  __syncthreads();   // the flags' initialisation
 #pragma unroll
   for (int c = 0; c < 2; c++) {
     sm.colsum[c][wid][lane] = csum[c];

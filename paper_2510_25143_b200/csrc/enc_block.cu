@@ -44,7 +44,7 @@ namespace vfcp {
 
 struct EncBlockSmem {
   int32_t o[2][33][33];     // fixed orig(t), [comp][1+i][1+j], halo row/col 0
-  int32_t p[2][33][33];     // recon(t-1)
+  int32_t p[2][33][33];     // recon(t-1) at the delta tile
   uint8_t cd[32][36];       // codes of the block (31 outside)
   int32_t spu[256], spv[256];   // SL trial predictions at the samples
   int16_t samp[2][512];     // |idx| per trial sample (-1: escape)
@@ -52,6 +52,7 @@ struct EncBlockSmem {
   int16_t cnt[2][ETB];
   double rate[2];
   int flag[8];              // see F_* below
+  int32_t etab[32];         // e per code (tau' < 2^28 on this path)
 };
 enum {
   F_NONUNI = 0,   // a valid code differs from code0
@@ -61,6 +62,15 @@ enum {
   F_UNSAFE_T = 4, // bit c: comp c has |R0| >= lim(tau') (trial sweep)
   F_UNSAFE_0 = 5, // bit c: comp c has |R0| >= lim(e0)
   F_OVF = 6,      // some |R0| >= 2^31 - 1
+};
+
+// recon(t-1) of component c at delta-tile coordinates (rr, cc) (row 0 =
+// r0 - 1, column 0 = c0 - 1)
+struct PvTile {
+  const int32_t (*t)[33][33];
+  __device__ __forceinline__ int32_t at(int c, int rr, int cc) const {
+    return t[c][rr][cc];
+  }
 };
 
 // residue in [0, m) of delta = o - p: int32 when the tile is narrow
@@ -82,7 +92,7 @@ __device__ __forceinline__ uint32_t res_delta(int64_t d, uint32_t m, uint32_t M,
 // the stride samples (STRIDE: 2, or 0 for the runtime stride).
 template <typename I, int STRIDE>
 __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
-                                           const int32_t (*pp)[33], int nr,
+                                           PvTile pp, int nr,
                                            int ncl, int stride, int nsx,
                                            int32_t e, uint32_t m, uint32_t M,
                                            uint32_t c32, int16_t* samp,
@@ -90,7 +100,7 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
   const unsigned FULL = 0xffffffffu;
   const uint32_t ue = (uint32_t)e;
   const bool colok = lane < ncl;
-  auto dlt = [&](int rr, int cc) -> I { return (I)o[rr][cc] - (I)pp[rr][cc]; };
+  auto dlt = [&](int rr, int cc) -> I { return (I)o[rr][cc] - (I)pp.at(comp, rr, cc); };
   const I dT = dlt(0, lane + 1), dC = dlt(0, 0);
   const I hL = dlt(lane + 1, 0);   // lane = row: the left halo of row lane
   const uint32_t rL = res_delta(hL, m, M, c32);
@@ -144,6 +154,14 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
   }
 }
 
+// the runtime-stride / wide-tile trial (rare) out of line
+static __device__ __noinline__ void trial_rows_generic(
+    const int32_t (*o)[33], PvTile pp, int nr, int ncl,
+    int stride, int nsx, int32_t e, uint32_t m, uint32_t M, uint32_t c32,
+    int16_t* samp, int comp, int lane) {
+  trial_rows<int64_t, 0>(o, pp, nr, ncl, stride, nsx, e, m, M, c32, samp, comp, lane);
+}
+
 template <typename F>
 __global__ void __launch_bounds__(128, 6)
 enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
@@ -170,27 +188,31 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const F* vo = v + (int64_t)p.t * HW;
   const bool has_prev = prev != nullptr;
 
-  // ---- tiles: rows r0-1 .. r0+31, columns c0-1 .. c0+31 (zero outside the
-  // frame, as the reference's Lorenzo terms vanish there)
+  // ---- tiles: orig(t) rows r0-1 .. r0+31, columns c0-1 .. c0+31, and
+  // recon(t-1) with an SLH-cell margin (zero outside the frame, as the
+  // reference's Lorenzo terms vanish there)
   if (tid < 8) sm.flag[tid] = 0;
+  if (tid < 32) sm.etab[tid] = bio.e_tab[tid];
   for (int k = tid; k < 2 * ETB; k += 128) (&sm.cnt[0][0])[k] = 0;
-  int64_t maxd = 0;
-  auto put = [&](int rr, int cc, F xu, F xv, int2 pr, bool ok) {
-    const int32_t ou = ok ? fixed_t(xu, p.S) : 0;
-    const int32_t ov = ok ? fixed_t(xv, p.S) : 0;
-    if (!ok) pr = make_int2(0, 0);
-    sm.o[0][rr][cc] = ou;
-    sm.o[1][rr][cc] = ov;
+  auto put = [&](int rr, int cc, F xu, F xv, bool ok) {
+    sm.o[0][rr][cc] = ok ? fixed_t(xu, p.S) : 0;
+    sm.o[1][rr][cc] = ok ? fixed_t(xv, p.S) : 0;
+  };
+  // recon(t-1) at the delta tile
+#pragma unroll 3
+  for (int k = tid; k < 33 * 33; k += 128) {
+    const int rr = k / 33, cc = k - 33 * rr;
+    const int i = r0 - 1 + rr, j = c0 - 1 + cc;
+    const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
+    const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
     sm.p[0][rr][cc] = pr.x;
     sm.p[1][rr][cc] = pr.y;
-    const int64_t du = (int64_t)ou - pr.x, dv = (int64_t)ov - pr.y;
-    maxd = max(maxd, max(du < 0 ? -du : du, dv < 0 ? -dv : dv));
-  };
+  }
   const bool full = nr == 32 && ncl == 32;
   const bool vec = full && sizeof(F) == 4 && (W & 3) == 0 &&
                    (((uintptr_t)uo | (uintptr_t)vo | (uintptr_t)codes_t) & 15) == 0;
   if (vec) {
-    // interior: 16-byte loads (4 pixels of one component, 2 recon pairs)
+    // interior: 16-byte loads (4 pixels of one component)
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const int idx = tid + 128 * q;     // 256 = 32 rows x 8 quads
@@ -198,16 +220,10 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const int64_t n = (int64_t)(r0 + i) * W + c0 + c4;
       const float4 a = __ldg(reinterpret_cast<const float4*>(uo + n));
       const float4 b = __ldg(reinterpret_cast<const float4*>(vo + n));
-      int4 p01 = make_int4(0, 0, 0, 0), p23 = make_int4(0, 0, 0, 0);
-      if (has_prev) {
-        const int4* pp = reinterpret_cast<const int4*>(prev + (int64_t)(r0 + i) * Wp + c0 + c4);
-        p01 = __ldg(pp);
-        p23 = __ldg(pp + 1);
-      }
-      put(i + 1, c4 + 1, (F)a.x, (F)b.x, make_int2(p01.x, p01.y), true);
-      put(i + 1, c4 + 2, (F)a.y, (F)b.y, make_int2(p01.z, p01.w), true);
-      put(i + 1, c4 + 3, (F)a.z, (F)b.z, make_int2(p23.x, p23.y), true);
-      put(i + 1, c4 + 4, (F)a.w, (F)b.w, make_int2(p23.z, p23.w), true);
+      put(i + 1, c4 + 1, (F)a.x, (F)b.x, true);
+      put(i + 1, c4 + 2, (F)a.y, (F)b.y, true);
+      put(i + 1, c4 + 3, (F)a.z, (F)b.z, true);
+      put(i + 1, c4 + 4, (F)a.w, (F)b.w, true);
     }
     // halo: row r0-1 (33 values incl. the corner), column c0-1
     if (tid < 65) {
@@ -217,13 +233,11 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const bool ok = i >= 0 && j >= 0;
       const int64_t n = ok ? (int64_t)i * W + j : 0;
       F xu = 0, xv = 0;
-      int2 pr = make_int2(0, 0);
       if (ok) {
         xu = __ldg(uo + n);
         xv = __ldg(vo + n);
-        if (has_prev) pr = __ldg(prev + (int64_t)i * Wp + j);
       }
-      put(rr, cc, xu, xv, pr, ok);
+      put(rr, cc, xu, xv, ok);
     }
     // codes: 4-byte loads
 #pragma unroll
@@ -242,13 +256,11 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const bool ok = i >= 0 && j >= 0 && i < H && j < W;
       const int64_t n = ok ? (int64_t)i * W + j : 0;
       F xu = 0, xv = 0;
-      int2 pr = make_int2(0, 0);
       if (ok) {
         xu = __ldg(uo + n);
         xv = __ldg(vo + n);
-        if (has_prev) pr = __ldg(prev + (int64_t)i * Wp + j);
       }
-      put(rr, cc, xu, xv, pr, ok);
+      put(rr, cc, xu, xv, ok);
     }
 #pragma unroll 2
     for (int k = tid; k < 1024; k += 128) {
@@ -257,7 +269,18 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
                                         : (uint8_t)CODE_LOSSLESS;
     }
   }
+  __syncthreads();
+  const PvTile pvt{sm.p};
   {
+    // max |delta| over the delta tile
+    int64_t maxd = 0;
+#pragma unroll 3
+    for (int k = tid; k < 33 * 33; k += 128) {
+      const int rr = k / 33, cc = k - 33 * rr;
+      const int64_t du = (int64_t)sm.o[0][rr][cc] - pvt.at(0, rr, cc);
+      const int64_t dv = (int64_t)sm.o[1][rr][cc] - pvt.at(1, rr, cc);
+      maxd = max(maxd, max(du < 0 ? -du : du, dv < 0 ? -dv : dv));
+    }
     int md = (int)min(maxd, (int64_t)INT32_MAX);
     md = __reduce_max_sync(FULL, md);
     if (lane == 0) atomicMax(&sm.flag[F_MAXD], md);
@@ -280,25 +303,24 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
   // R0 of pixel (i, j) from the tiles (exact)
   auto R0_at = [&](int c, int i, int j) -> int64_t {
     const int32_t(*o)[33] = sm.o[c];
-    const int32_t(*pp)[33] = sm.p[c];
     if (narrow) {
-      const int32_t d = o[i + 1][j + 1] - pp[i + 1][j + 1];
-      const int32_t dU = o[i][j + 1] - pp[i][j + 1];
-      const int32_t dL = o[i + 1][j] - pp[i + 1][j];
-      const int32_t dUL = o[i][j] - pp[i][j];
+      const int32_t d = o[i + 1][j + 1] - pvt.at(c, i + 1, j + 1);
+      const int32_t dU = o[i][j + 1] - pvt.at(c, i, j + 1);
+      const int32_t dL = o[i + 1][j] - pvt.at(c, i + 1, j);
+      const int32_t dUL = o[i][j] - pvt.at(c, i, j);
       return (int64_t)(d - dU - dL + dUL);
     }
-    return ((int64_t)o[i + 1][j + 1] - pp[i + 1][j + 1]) -
-           ((int64_t)o[i][j + 1] - pp[i][j + 1]) -
-           ((int64_t)o[i + 1][j] - pp[i + 1][j]) +
-           ((int64_t)o[i][j] - pp[i][j]);
+    return ((int64_t)o[i + 1][j + 1] - pvt.at(c, i + 1, j + 1)) -
+           ((int64_t)o[i][j + 1] - pvt.at(c, i, j + 1)) -
+           ((int64_t)o[i + 1][j] - pvt.at(c, i + 1, j)) +
+           ((int64_t)o[i][j] - pvt.at(c, i, j));
   };
   {
     bool nonuni = false, lossy = false, lossless = false;
     for (int i = wid; i < nr; i += 4) {
       if (!colok) continue;
       const int cd = sm.cd[i][lane];
-      const bool ls = p.lad.e[cd] > 0;
+      const bool ls = sm.etab[cd & 31] > 0;
       nonuni |= cd != code0;
       lossy |= ls;
       lossless |= !ls;
@@ -346,17 +368,13 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const uint32_t m = 2u * (uint32_t)e, ue = (uint32_t)e;
       const uint32_t M = bio.mag_tab[0], c32 = bio.c32_tab[0];
       const int32_t(*o)[33] = sm.o[comp];
-      const int32_t(*pp)[33] = sm.p[comp];
+      const PvTile pp = pvt;
       if (!((sm.flag[F_UNSAFE_T] >> comp) & 1)) {
         int16_t* samp = &sm.samp[0][0];
-        if (narrow) {
-          if (p.stride == 2)
-            trial_rows<int32_t, 2>(o, pp, nr, ncl, 2, nsx, e, m, M, c32, samp, comp, lane);
-          else
-            trial_rows<int32_t, 0>(o, pp, nr, ncl, p.stride, nsx, e, m, M, c32, samp, comp, lane);
-        } else {
-          trial_rows<int64_t, 0>(o, pp, nr, ncl, p.stride, nsx, e, m, M, c32, samp, comp, lane);
-        }
+        if (narrow && p.stride == 2)
+          trial_rows<int32_t, 2>(o, pp, nr, ncl, 2, nsx, e, m, M, c32, samp, comp, lane);
+        else
+          trial_rows_generic(o, pp, nr, ncl, p.stride, nsx, e, m, M, c32, samp, comp, lane);
       } else {
         // escapes possible: the exact raster sweep of the trial (skewed:
         // lane = row, step s visits column s - lane)
@@ -386,32 +404,32 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
           }
         }
       }
-    } else {
-      // semi-Lagrangian trial at the stride samples (warps 2 and 3, four
-      // samples per thread in lockstep so the departure-point gathers
-      // overlap); the predictions are kept for the block's encode
-      const PairPlane src{prev, Wp};
-      constexpr int NSB = 4;
-      const int t2 = tid - 64;
-      int64_t pr_u[NSB], pr_v[NSB];
-      int si_i[NSB], si_j[NSB];
-      bool slow[NSB];
+    }
+    {
+      // semi-Lagrangian trial at the stride samples, two per lane in lockstep
+      // so the departure-point gathers overlap: warps 2 and 3 take samples
+      // [0, 128) at once, warps 0 and 1 [128, 256) after their Lorenzo trial;
+      // the predictions are kept for the block's encode
+      const int t2 = wid >= 2 ? tid - 64 : tid + 128;
+      int64_t pr_u[2], pr_v[2];
+      int si_i[2], si_j[2];
+      bool slow[2];
 #pragma unroll
-      for (int b = 0; b < NSB; b++) {
+      for (int b = 0; b < 2; b++) {
         const int sidx = min(t2 + 64 * b, nsamp - 1);
         const int si = sidx / nsx, sj = sidx - si * nsx;
         si_i[b] = r0 + si * p.stride;
         si_j[b] = c0 + sj * p.stride;
-        slow[b] = !sl_predict_rk2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y,
-                                  p.d_max, &pr_u[b], &pr_v[b]);
+        slow[b] = !sl_predict_rk2(PairPlane{prev, Wp}, H, W, si_i[b], si_j[b],
+                                  p.cfl_x, p.cfl_y, p.d_max, &pr_u[b], &pr_v[b]);
       }
-#pragma unroll
-      for (int b = 0; b < NSB; b++) {
+#pragma unroll 1
+      for (int b = 0; b < 2; b++) {
         const int sidx = t2 + 64 * b;
         if (sidx >= nsamp) continue;
         if (slow[b])
-          sl_predict2(src, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y, p.d_max,
-                      p.n_max, &pr_u[b], &pr_v[b]);
+          sl_general(prev, Wp, H, W, si_i[b], si_j[b], p.cfl_x, p.cfl_y, p.d_max,
+                     p.n_max, &pr_u[b], &pr_v[b]);
         const int li = si_i[b] - r0 + 1, lj = si_j[b] - c0 + 1;
         const int64_t ru = (int64_t)sm.o[0][li][lj] - pr_u[b];
         const int64_t rv = (int64_t)sm.o[1][li][lj] - pr_v[b];
@@ -453,7 +471,7 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
         const int i = i0 + 4 * q;
         const bool rv_ = i < nr;
         const int cd = rv_ && colok ? sm.cd[i][lane] : CODE_LOSSLESS;
-        need[q] = rv_ && colok && p.lad.e[cd] > 0;
+        need[q] = rv_ && colok && sm.etab[cd & 31] > 0;
         have[q] = p.mop && sc && (i % p.stride) == 0;
         pu[q] = pv[q] = 0;
         slow[q] = false;
@@ -475,10 +493,10 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
         const int i = i0 + 4 * q;
         if (i >= nr) break;   // warp-uniform
         if (slow[q] && need[q])
-          sl_predict2(src, H, W, r0 + i, j, p.cfl_x, p.cfl_y, p.d_max, p.n_max,
-                      &pu[q], &pv[q]);
+          sl_general(prev, Wp, H, W, r0 + i, j, p.cfl_x, p.cfl_y, p.d_max,
+                     p.n_max, &pu[q], &pv[q]);
         const int cd = colok ? sm.cd[i][lane] : CODE_LOSSLESS;
-        const int64_t e = p.lad.e[cd];
+        const int64_t e = sm.etab[cd & 31];
         const bool nl = colok && e > 0;
         const int32_t ou = colok ? sm.o[0][i + 1][lane + 1] : 0;
         const int32_t ov = colok ? sm.o[1][i + 1][lane + 1] : 0;
@@ -546,7 +564,7 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
   if (any_lossless) {
     // two ll values per lossless pixel (the chain sweeps such a block)
     for (int i = wid; i < nr; i += 4) {
-      const bool ll = colok && p.lad.e[sm.cd[i][lane]] == 0;
+      const bool ll = colok && sm.etab[sm.cd[i][lane] & 31] == 0;
       const int nll = 2 * __popc(__ballot_sync(FULL, ll));
       if (lane == 0 && nll) atomicAdd(row_ll + rowbase + r0 + i, nll);
     }
@@ -561,9 +579,8 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
       const uint32_t m = 2u * (uint32_t)e0;
       const uint32_t M = bio.mag_tab[code0], c32 = bio.c32_tab[code0];
       const int32_t(*o)[33] = sm.o[c];
-      const int32_t(*pp)[33] = sm.p[c];
       auto rd = [&](int rr, int cc) -> uint32_t {
-        return res_i64((int64_t)o[rr][cc] - pp[rr][cc], m, M, c32);
+        return res_i64((int64_t)o[rr][cc] - pvt.at(c, rr, cc), m, M, c32);
       };
       const uint32_t rc = rd(0, 0);
       int32_t lbv = 0, lrv = 0;

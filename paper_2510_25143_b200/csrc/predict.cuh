@@ -32,6 +32,58 @@ struct TwoPlanes {
   }
 };
 
+// recon(t-1) tile: the block plus SLH cells on every side, so the
+// semi-Lagrangian departure points of the trial and of SL blocks mostly
+// gather from shared memory (TileSrc falls back to global memory outside)
+constexpr int SLH = 8;
+constexpr int SLT = 32 + 2 * SLH;
+
+// Value source of the semi-Lagrangian sampler (below): recon(t-1)
+// from the block's shared tile, or global memory outside it.
+struct TileSrc {
+  const int2 (*t)[SLT];
+  int ti0, tj0;           // frame coordinates of t[0][0]
+  const int2* g;          // recon(t-1), pitch Wp
+  int Wp;
+  __device__ __forceinline__ void get(int i, int j, double& u, double& v) const {
+    const int a = i - ti0, b = j - tj0;
+    const int2 x = ((unsigned)a < (unsigned)SLT && (unsigned)b < (unsigned)SLT)
+                       ? t[a][b]
+                       : __ldg(g + (int64_t)i * Wp + j);
+    u = (double)x.x;
+    v = (double)x.y;
+  }
+};
+
+
+// Load the recon(t-1) tile of the block at (r0, c0) with its SLH margin
+// (zero outside the frame; all of the CTA's threads, 16-byte loads:
+// c0 - SLH is even).
+__device__ __forceinline__ void load_prev_tile(int2 (*tile)[SLT],
+                                               const int2* prev, int H, int W,
+                                               int Wp, int r0, int c0,
+                                               int tid, int nthreads) {
+  const int ti0 = r0 - SLH, tj0 = c0 - SLH;
+  int4* dst = reinterpret_cast<int4*>(&tile[0][0]);
+  constexpr int NQ = SLT * SLT / 2;
+#pragma unroll 3
+  for (int k = tid; k < NQ; k += nthreads) {
+    const int a = k / (SLT / 2), b2 = (k - a * (SLT / 2)) * 2;
+    const int i = ti0 + a, j = tj0 + b2;
+    int4 x = make_int4(0, 0, 0, 0);
+    if (prev && i >= 0 && i < H && j >= 0) {
+      const int2* src = prev + (int64_t)i * Wp + j;
+      if (j + 1 < W) {
+        x = __ldg(reinterpret_cast<const int4*>(src));
+      } else if (j < W) {
+        const int2 y = __ldg(src);
+        x = make_int4(y.x, y.y, 0, 0);
+      }
+    }
+    dst[k] = x;
+  }
+}
+
 // predictors.py:33-59 (shared weights for u and v)
 template <typename Src>
 __device__ __forceinline__ void bilinear2(const Src& s, int H, int W,
@@ -125,6 +177,17 @@ __device__ __forceinline__ bool sl_predict_rk2(const Src& s, int H, int W,
   const double fj = __dsub_rn((double)j, __dmul_rn((double)um, cfl_x));
   bilinear2(s, H, W, fi, fj, pu, pv);
   return d_inf <= d_max;
+}
+
+// The general predictor (Euler substeps when d_inf > d_max) out of line:
+// one copy of its code per kernel, taken by the rare samples whose RK2 fast
+// path does not apply.
+static __device__ __noinline__ void sl_general(const int2* prev, int Wp, int H,
+                                               int W, int i, int j,
+                                               double cfl_x, double cfl_y,
+                                               double d_max, int n_max,
+                                               int64_t* pu, int64_t* pv) {
+  sl_predict2(PairPlane{prev, Wp}, H, W, i, j, cfl_x, cfl_y, d_max, n_max, pu, pv);
 }
 
 // ------------------------------------------------ first-touch block entropy
