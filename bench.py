@@ -216,6 +216,155 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+MATRIX_DOC = """The BASELINE measurement matrix (BASELINE.md "What to report per config
+and eps"): every config at its full size and every eps of its list.
+
+Per (config, eps), on one B200, device-resident inputs (CUDA events, W
+warm-up + K timed steps): compress and decompress GB/s of fp32 input, the
+kernel split, the algorithmic-bytes fraction of the HBM roofline (21.125
+B/vertex each way, SURVEY 8d); end to end through compress_device(...,
+host_out=True) from pinned host buffers; the share of semi-Lagrangian
+blocks.  CPU baselines, labelled: the C port of the reference path (this
+repo's oracle, single thread) timed on this host on a bounded sample, and
+the real reference (numba, single thread) timed in the build container
+(profiles/ref_cpu_numba_r02.json, tools/ref_cpu_time.py).  Parity status
+from profiles/parity_full_r02.json.
+
+    python bench.py --matrix profiles/bench_matrix_r02.json
+"""
+
+BASELINE_EPS = {1: [1e-2], 2: [1e-3], 3: [1e-2, 1e-3], 4: [1e-3],
+                5: [1e-2, 1e-3, 1e-4]}
+# oracle-port CPU sample per config (H, W, T): ~2-10 s of single-core work
+CPU_SAMPLE = {1: (None, None, None), 2: (None, None, 12), 3: (None, None, 24),
+              4: (600, 900, 6), 5: (1024, 1024, 4)}
+
+
+def run_matrix(args):
+    """--matrix: every BASELINE config at full size x its eps list (see
+    MATRIX_DOC)."""
+    import torch
+
+    import paper_2510_25143_b200 as vg
+    from oracle import cpu_oracle as O
+    from paper_2510_25143_b200 import _lib, codec, synth
+
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    numba = {}
+    nf = ROOT / "profiles" / "ref_cpu_numba_r02.json"
+    if nf.exists():
+        for r in json.loads(nf.read_text())["runs"]:
+            numba[(r["config"], r["eps_rel"])] = r
+    parity = {}
+    pf = ROOT / "profiles" / "parity_full_r02.json"
+    if pf.exists():
+        for r in json.loads(pf.read_text())["runs"]:
+            parity[(r["config"], r["eps_rel"])] = r["all_equal"]
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    rows = []
+    cfg = vg.Config()
+    for c in args.matrix_configs:
+        H, W, T, u, v = synth.generate(c)
+        N = H * W * T
+        du, dv = torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda()
+        fd = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, du, dv)
+        up, vp = torch.from_numpy(u).pin_memory(), torch.from_numpy(v).pin_memory()
+        fh = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, up, vp)
+        for eps in BASELINE_EPS[c]:
+            for _ in range(args.warmup):
+                s = codec.compress_device(fd, eps, cfg, relative=True)
+            _lib.prof_enable(True)
+            e0.record(st)
+            for _ in range(args.steps):
+                s = None
+                s = codec.compress_device(fd, eps, cfg, relative=True)
+            e1.record(st)
+            torch.cuda.synchronize()
+            cms = e0.elapsed_time(e1) / args.steps
+            prof = _lib.prof_collect()
+            _lib.prof_enable(False)
+            am = codec.Archive(H, W, T, 1.0, 1.0, 1.0, s.scale, s.eps, s.tau, cfg,
+                               b"", b"", s.ld.cpu().numpy().tobytes(), b"", b"")
+            kw = dict(codes=s.codes, qd=s.qd, ll=s.ll, modes=s.modes, ld=s.ld)
+            for _ in range(args.warmup):
+                vg.decompress_device(am, **kw)
+            _lib.prof_enable(True)
+            e0.record(st)
+            for _ in range(args.steps):
+                out = None
+                out = vg.decompress_device(am, **kw)
+            e1.record(st)
+            torch.cuda.synchronize()
+            dms = e0.elapsed_time(e1) / args.steps
+            dprof = _lib.prof_collect()
+            _lib.prof_enable(False)
+            del out
+            sl = float(s.modes.sum().item()) / max(1, int(s.modes.numel()))
+            del s, kw, am
+            # end to end: pinned host input -> streams in pinned host memory
+            for _ in range(max(1, args.warmup)):
+                h = codec.streams_to_host(codec.compress_device(
+                    fh, eps, cfg, relative=True, host_out=True))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                h = None
+                h = codec.streams_to_host(codec.compress_device(
+                    fh, eps, cfg, relative=True, host_out=True))
+            torch.cuda.synchronize()
+            e2e_s = (time.perf_counter() - t0) / args.steps
+            d2h = sum(int(x.nbytes) for x in h.values())
+            del h
+            # CPU: the oracle port on a bounded sample of the same generator
+            sh, sw, stt = CPU_SAMPLE[c]
+            Hs, Ws, Ts, us, vs = synth.generate(c, sh, sw, stt)
+            t0 = time.perf_counter()
+            O.compress_streams(us, vs, Hs, Ws, Ts, 1.0, 1.0, 1.0, eps, cfg,
+                               relative=True)
+            cpu_s = time.perf_counter() - t0
+            nb = numba.get((c, eps))
+            row = {
+                "config": c, "eps_rel": eps, "H": H, "W": W, "T": T, "N": N,
+                "compress": {"GBps": round(8.0 * N / cms / 1e6, 3),
+                             "ms": round(cms, 3),
+                             "algo_frac": round(21.125 * N / (cms * 1e-3) / 1e9 / peak, 4),
+                             "kernels_ms": {k: round(v[0] / args.steps, 3)
+                                            for k, v in prof.items() if v[1]}},
+                "decompress": {"GBps": round(8.0 * N / dms / 1e6, 3),
+                               "ms": round(dms, 3),
+                               "algo_frac": round(21.125 * N / (dms * 1e-3) / 1e9 / peak, 4),
+                               "kernels_ms": {k: round(v[0] / args.steps, 3)
+                                              for k, v in dprof.items() if v[1]}},
+                "e2e": {"GBps": round(8.0 * N / e2e_s / 1e9, 3),
+                        "ms": round(e2e_s * 1e3, 2),
+                        "h2d_bytes": 8 * N, "d2h_bytes": d2h},
+                "sl_block_frac": round(sl, 4),
+                "cpu_port": {"kind": "port (C oracle, 1 thread, this host)",
+                             "MBps": round(8.0 * Hs * Ws * Ts / cpu_s / 1e6, 2),
+                             "sample": f"{Hs}x{Ws}x{Ts}"},
+                "cpu_numba": ({"kind": "reference (vfcp numba, 1 thread, build container)",
+                               "compress_MBps": nb["compress_MBps"],
+                               "decompress_MBps": nb["decompress_MBps"],
+                               "sample": f"{nb['H']}x{nb['W']}x{nb['T']}"}
+                              if nb else None),
+                "parity_full_size": parity.get((c, eps)),
+            }
+            rows.append(row)
+            print(json.dumps({k: row[k] for k in ("config", "eps_rel")} |
+                             {"c": row["compress"]["GBps"], "d": row["decompress"]["GBps"],
+                              "e2e": row["e2e"]["GBps"]}), flush=True)
+        del du, dv, fd, up, vp, fh
+        torch.cuda.empty_cache()
+    res = {"what": MATRIX_DOC, "peak_hbm_GBps": peak,
+           "rows": rows}
+    Path(args.matrix).write_text(json.dumps(res, indent=1))
+    return 0
+
+
+
 def workload_name(args):
     from paper_2510_25143_b200 import synth
     c = synth.CONFIGS[args.config]
@@ -245,7 +394,12 @@ def main():
                     help="device-resident timings only (no e2e / entropy legs)")
     ap.add_argument("--ref-sample", type=int, nargs=3, default=(1024, 1024, 4))
     ap.add_argument("--cpu-sample", type=int, nargs=3, default=(2048, 2048, 4))
+    ap.add_argument("--matrix", default=None, metavar="OUT.json",
+                    help="run the BASELINE config x eps matrix (1 GPU) instead")
+    ap.add_argument("--matrix-configs", type=int, nargs="*", default=[1, 2, 3, 4, 5])
     args = ap.parse_args()
+    if args.matrix:
+        return run_matrix(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -93,7 +93,7 @@ struct BScanIO {
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
-constexpr int BS_PF = 4;        // blocks of (class, LB, LR) staged ahead
+constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
 constexpr int BS_SEG = 32;      // blocks per progress mark / interior task
 
 __host__ __device__ inline int bs_ntask(int nby) {
@@ -290,12 +290,12 @@ __device__ __forceinline__ void bs_slow_block(
   if (ENC && nesc) atomicAdd(io.row_ll + r0 + lane, nesc);
 }
 
-template <typename F>
-__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
-                                             int lane);
-
-__device__ __forceinline__ void bs_final_dec(const BScanIO& io, int bi, int bj,
-                                             int lane);
+template <typename F, int C>
+__device__ __forceinline__ void bs_final_enc1(const BScanIO& io, int bi, int bj,
+                                              int lane);
+template <int C>
+__device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
+                                              int lane);
 
 template <bool ENC, typename F = float>
 __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
@@ -341,9 +341,16 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
         __threadfence();
       }
       __syncthreads();
-      for (int bj = b0 + w; bj < b1; bj += BS_NW) {
-        if (ENC) bs_final_enc<F>(io, bi, bj, lane);
-        else bs_final_dec(io, bi, bj, lane);
+      // one warp per (block, component)
+      for (int x = w; x < 2 * (b1 - b0); x += BS_NW) {
+        const int bj = b0 + (x >> 1);
+        if (ENC) {
+          if (x & 1) bs_final_enc1<F, 1>(io, bi, bj, lane);
+          else bs_final_enc1<F, 0>(io, bi, bj, lane);
+        } else {
+          if (x & 1) bs_final_dec1<1>(io, bi, bj, lane);
+          else bs_final_dec1<0>(io, bi, bj, lane);
+        }
       }
       __syncthreads();
       continue;
@@ -542,104 +549,86 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
 }
 
 // ------------------------------------------------------------ phase C
-// Encoder: the interior of block (bi, bj), both components, by one warp
-// (lane = column, rows streamed with one row of loads in flight).
+// The interior of block (bi, bj), component C, by one warp (lane = column,
+// rows streamed with three rows of loads in flight).
+// Encoder (bs_final_enc1):
 //   REG       err(i, j) = rep(zT(j) + zL(i) - zC - delta(i, j))  (mod m)
 //             with zT = errT + deltaT etc. (Z = recon - prev of the exact
 //             boundary, enc_block.cu), ties in raster order; the symbol is
 //             (R0 + D(err)) / m exactly;
 //   SLOW/DONE err from the chain's sweep (its symbols are written);
-//   KNOWN     recon(t) already written by the block kernel.
-// recon(t) = orig + err goes out as (u, v) pairs.
-template <typename F>
-__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
-                                             int lane) {
+//   KNOWN     recon(t) already written by the block kernel;
+// recon(t) = orig + err goes into component C of the (u, v) pair plane.
+// Decoder (bs_final_dec1): REG: Z = ZU + ZL - ZUL + A, i.e. per row
+// Z(i, j) = Z(i-1, j) + (ZL(i) - ZL(i-1)) + sum_{b<=j} A(i, b) (warp scan;
+// wrapping uint32 arithmetic is exact: recon fits int32) with A =
+// (sym - radius) * 2e; SLOW: Z from the chain's sweep; KNOWN: written by
+// the block kernel (dec_block.cu).  recon = recon(t-1) + Z goes out to the
+// pair plane, as float64 (codec.py:425-426 recon * (1/S), exact) and
+// optionally as int64.
+template <typename F, int C>
+__device__ __forceinline__ void bs_final_enc1(const BScanIO& io, int bi, int bj,
+                                              int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
   const int64_t nblk = (int64_t)io.nbx * io.nby;
   const int64_t blk = (int64_t)bi * io.nbx + bj;
   const int Wp = io.Wp, W = io.W;
-  int kind[2], code[2];
-#pragma unroll
-  for (int c = 0; c < 2; c++) {
-    const int32_t cl = __ldcg(io.cls + c * nblk + blk);
-    kind[c] = cl & 3;
-    code[c] = cl >> 2;
-  }
-  if (kind[0] == BS_KNOWN) return;   // KNOWN <=> both components KNOWN
+  const int32_t cl = __ldcg(io.cls + C * nblk + blk);
+  const int kind = cl & 3, code = cl >> 2;
+  if (kind == BS_KNOWN) return;
+  const bool reg = kind == BS_REG;
   const bool colok = lane < ncl;
   const int j = c0 + (colok ? lane : ncl - 1);
-  const F* op[2] = {static_cast<const F*>(io.orig[0]), static_cast<const F*>(io.orig[1])};
-  auto fx = [&](const F* base, int i, int jj) -> int32_t {
-    return fixed_t(__ldg(base + (int64_t)i * W + jj), io.S);
+  const F* op = static_cast<const F*>(io.orig[C]);
+  const int32_t* pvc = io.prevrec ? reinterpret_cast<const int32_t*>(io.prevrec) + C : nullptr;
+  auto pvat = [&](int i, int jj) -> int32_t {
+    return pvc ? __ldg(pvc + 2 * ((int64_t)i * Wp + jj)) : 0;
   };
-  const bool reg[2] = {kind[0] == BS_REG, kind[1] == BS_REG};
-  uint32_t e[2], m[2], M[2], c32[2];
-#pragma unroll
-  for (int c = 0; c < 2; c++) {
-    e[c] = reg[c] ? (uint32_t)io.e_tab[code[c]] : 2u;
-    m[c] = 2u * e[c];
-    M[c] = reg[c] ? io.mag_tab[code[c]] : 0x7fffffffu;
-    c32[c] = reg[c] ? io.c32_tab[code[c]] : 0u;
-  }
-  // exact boundary errors: errT (lane = column), errL (lane = row), errC
-  int32_t errT[2], errL[2], errC[2];
-  const int32_t* eb = io.ebot;
-  const int32_t* er = io.eright;
-#pragma unroll
-  for (int c = 0; c < 2; c++) {
-    errT[c] = (bi > 0 && colok) ? __ldcg(eb + (c * nblk + blk - io.nbx) * 32 + lane) : 0;
-    errL[c] = (bj > 0 && lane < nr) ? __ldcg(er + (c * nblk + blk - 1) * 32 + lane) : 0;
-    errC[c] = (bi > 0 && bj > 0) ? __ldcg(eb + (c * nblk + blk - io.nbx - 1) * 32 + 31) : 0;
-  }
-  // delta of the halo: row r0-1 (lane = column), column c0-1 (lane = row),
-  // the corner
-  int64_t dT[2] = {0, 0}, dL[2] = {0, 0}, dC[2] = {0, 0};
-  const int2* pv = io.prevrec;
-  if (bi > 0) {
-    const int2 pp = pv ? __ldg(pv + (int64_t)(r0 - 1) * Wp + j) : make_int2(0, 0);
-    dT[0] = colok ? (int64_t)fx(op[0], r0 - 1, j) - pp.x : 0;
-    dT[1] = colok ? (int64_t)fx(op[1], r0 - 1, j) - pp.y : 0;
-    if (bj > 0) {
-      const int2 pc = pv ? __ldg(pv + (int64_t)(r0 - 1) * Wp + c0 - 1) : make_int2(0, 0);
-      dC[0] = (int64_t)fx(op[0], r0 - 1, c0 - 1) - pc.x;
-      dC[1] = (int64_t)fx(op[1], r0 - 1, c0 - 1) - pc.y;
+  auto fx = [&](int i, int jj) -> int32_t {
+    return fixed_t(__ldg(op + (int64_t)i * W + jj), io.S);
+  };
+  int32_t* recw = reinterpret_cast<int32_t*>(io.rec) + C;
+  if (!reg) {
+    // SLOW / DONE: err from the chain's sweep
+#pragma unroll 4
+    for (int i = 0; i < nr; i++) {
+      if (colok) {
+        const int32_t err = __ldcg(io.out[C] + (int64_t)(r0 + i) * Wp + j);
+        recw[2 * ((int64_t)(r0 + i) * Wp + j)] = fx(r0 + i, j) + err;
+      }
     }
+    return;
   }
-  if (bj > 0 && lane < nr) {
-    const int2 pl = pv ? __ldg(pv + (int64_t)(r0 + lane) * Wp + c0 - 1) : make_int2(0, 0);
-    dL[0] = (int64_t)fx(op[0], r0 + lane, c0 - 1) - pl.x;
-    dL[1] = (int64_t)fx(op[1], r0 + lane, c0 - 1) - pl.y;
+  const uint32_t e = (uint32_t)io.e_tab[code], m = 2u * e;
+  const uint32_t M = io.mag_tab[code], c32 = io.c32_tab[code];
+  const int32_t* eb = io.ebot + C * nblk * 32;
+  const int32_t* er = io.eright + C * nblk * 32;
+  const int32_t errT = (bi > 0 && colok) ? __ldcg(eb + (blk - io.nbx) * 32 + lane) : 0;
+  const int32_t errL = (bj > 0 && lane < nr) ? __ldcg(er + (blk - 1) * 32 + lane) : 0;
+  const int32_t errC = (bi > 0 && bj > 0) ? __ldcg(eb + (blk - io.nbx - 1) * 32 + 31) : 0;
+  int64_t dT = 0, dL = 0, dC = 0;
+  if (bi > 0) {
+    dT = colok ? (int64_t)fx(r0 - 1, j) - pvat(r0 - 1, j) : 0;
+    if (bj > 0) dC = (int64_t)fx(r0 - 1, c0 - 1) - pvat(r0 - 1, c0 - 1);
   }
-  // Z residues of the boundary (REG components)
-  uint32_t base[2] = {0u, 0u}, zL[2] = {0u, 0u};
-#pragma unroll
-  for (int c = 0; c < 2; c++) {
-    if (!reg[c]) continue;
-    const uint32_t zT = bs_madd(bs_res(errT[c], m[c], M[c]), res_i64(dT[c], m[c], M[c], c32[c]), m[c]);
-    const uint32_t zC = bs_madd(bs_res(errC[c], m[c], M[c]), res_i64(dC[c], m[c], M[c], c32[c]), m[c]);
-    zL[c] = bs_madd(bs_res(errL[c], m[c], M[c]), res_i64(dL[c], m[c], M[c], c32[c]), m[c]);
-    base[c] = bs_msub(zT, zC, m[c]);
-  }
-  // the row above the current row: delta (low 32 bits suffice for R0, whose
-  // value fits int32 in a REG block) and err; the halo column of that row
-  int32_t dU[2] = {(int32_t)dT[0], (int32_t)dT[1]};
-  int32_t eU[2] = {errT[0], errT[1]};
-  int32_t dLU[2] = {(int32_t)dC[0], (int32_t)dC[1]};   // lane 0: halo of row i-1
-  int32_t eLU[2] = {errC[0], errC[1]};
+  if (bj > 0 && lane < nr) dL = (int64_t)fx(r0 + lane, c0 - 1) - pvat(r0 + lane, c0 - 1);
+  const uint32_t zT = bs_madd(bs_res(errT, m, M), res_i64(dT, m, M, c32), m);
+  const uint32_t zC = bs_madd(bs_res(errC, m, M), res_i64(dC, m, M, c32), m);
+  const uint32_t zL = bs_madd(bs_res(errL, m, M), res_i64(dL, m, M, c32), m);
+  const uint32_t base = bs_msub(zT, zC, m);
+  int32_t dU = (int32_t)dT, eU = errT, dLU = (int32_t)dC, eLU = errC;
   int64_t qb = 0;
   if (lane < nr)
     qb = io.qd_row_off[r0 + lane] +
-         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj];
-  // row loads, three rows ahead (a four-slot register ring)
-  F bu[4], bv[4];
-  int2 bp[4];
+         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + C;
+  F bo[4];
+  int32_t bp[4];
   auto issue = [&](int i, int sl) {
     if (i < nr) {
-      bu[sl] = __ldg(op[0] + (int64_t)(r0 + i) * W + j);
-      bv[sl] = __ldg(op[1] + (int64_t)(r0 + i) * W + j);
-      bp[sl] = pv ? __ldg(pv + (int64_t)(r0 + i) * Wp + j) : make_int2(0, 0);
+      bo[sl] = __ldg(op + (int64_t)(r0 + i) * W + j);
+      bp[sl] = pvat(r0 + i, j);
     }
   };
   issue(0, 0);
@@ -651,137 +640,100 @@ __device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
     const int i = i0 + kk;
     if (i >= nr) break;
     issue(i + 3, (kk + 3) & 3);
-    const int32_t ou = fixed_t(bu[kk], io.S), ov = fixed_t(bv[kk], io.S);
-    const int2 pp = bp[kk];
-    const int32_t o[2] = {ou, ov};
-    const int32_t pr[2] = {pp.x, pp.y};
-    int32_t err[2], R0[2], errLi[2], dLi[2];
-    uint32_t sym[2] = {0u, 0u};
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      const int64_t d64 = (int64_t)o[c] - pr[c];
-      const int32_t d32 = (int32_t)d64;
-      dLi[c] = __shfl_sync(FULL, (int32_t)dL[c], i);
-      errLi[c] = __shfl_sync(FULL, errL[c], i);
-      int32_t dl = __shfl_up_sync(FULL, d32, 1);
-      int32_t dul = __shfl_up_sync(FULL, dU[c], 1);
-      if (lane == 0) { dl = dLi[c]; dul = dLU[c]; }
-      R0[c] = d32 - dU[c] - dl + dul;
-      if (reg[c]) {
-        const uint32_t zl = __shfl_sync(FULL, zL[c], i);
-        const uint32_t sres = bs_msub(bs_madd(base[c], zl, m[c]),
-                                      res_i64(d64, m[c], M[c], c32[c]), m[c]);
-        const bool tie = colok && sres == e[c];
-        err[c] = bs_rep(sres, e[c], m[c]);
-        uint32_t tm = __ballot_sync(FULL, tie);
-        if (tm) {
-          // raster order within the row: a tie's sign follows
-          // x = R0 - (errU + errL - errUL)
-          int32_t cur = tie ? 0 : err[c];
-          while (tm) {
-            const int jj = __ffs(tm) - 1;
-            tm &= tm - 1u;
-            int32_t el = __shfl_up_sync(FULL, cur, 1);
-            int32_t eul = __shfl_up_sync(FULL, eU[c], 1);
-            if (lane == 0) { el = errLi[c]; eul = eLU[c]; }
-            if (lane == jj) {
-              const int64_t x = (int64_t)R0[c] - ((int64_t)eU[c] + el - eul);
-              cur = x > 0 ? (int32_t)e[c] : -(int32_t)e[c];
-            }
-          }
-          err[c] = cur;
+    const int32_t o = fixed_t(bo[kk], io.S);
+    const int32_t pr = bp[kk];
+    const int64_t d64 = (int64_t)o - pr;
+    const int32_t d32 = (int32_t)d64;
+    const int32_t dLi = __shfl_sync(FULL, (int32_t)dL, i);
+    const int32_t errLi = __shfl_sync(FULL, errL, i);
+    int32_t dl = __shfl_up_sync(FULL, d32, 1);
+    int32_t dul = __shfl_up_sync(FULL, dU, 1);
+    if (lane == 0) { dl = dLi; dul = dLU; }
+    const int32_t R0 = d32 - dU - dl + dul;
+    const uint32_t zl = __shfl_sync(FULL, zL, i);
+    const uint32_t sres = bs_msub(bs_madd(base, zl, m), res_i64(d64, m, M, c32), m);
+    const bool tie = colok && sres == e;
+    int32_t err = bs_rep(sres, e, m);
+    uint32_t tm = __ballot_sync(FULL, tie);
+    if (tm) {
+      // raster order within the row: x = R0 - (errU + errL - errUL)
+      int32_t cur = tie ? 0 : err;
+      while (tm) {
+        const int jj = __ffs(tm) - 1;
+        tm &= tm - 1u;
+        int32_t el = __shfl_up_sync(FULL, cur, 1);
+        int32_t eul = __shfl_up_sync(FULL, eU, 1);
+        if (lane == 0) { el = errLi; eul = eLU; }
+        if (lane == jj) {
+          const int64_t x = (int64_t)R0 - ((int64_t)eU + el - eul);
+          cur = x > 0 ? (int32_t)e : -(int32_t)e;
         }
-      } else {
-        err[c] = colok ? __ldcg(io.out[c] + (int64_t)(r0 + i) * Wp + j) : 0;
       }
+      err = cur;
     }
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      if (!reg[c]) continue;
-      int32_t el = __shfl_up_sync(FULL, err[c], 1);
-      int32_t eul = __shfl_up_sync(FULL, eU[c], 1);
-      if (lane == 0) { el = errLi[c]; eul = eLU[c]; }
-      // x + err = q * m exactly (|R0| < 2^30 in a REG block)
-      const int32_t n = R0[c] + err[c] - eU[c] - el + eul;
-      const uint32_t an = (uint32_t)(n < 0 ? -n : n);
-      uint32_t qa = __umulhi(an, M[c]);
-      if (qa * m[c] != an) qa++;
-      const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
-      sym[c] = (uint32_t)(q + io.radius);
-    }
+    int32_t el = __shfl_up_sync(FULL, err, 1);
+    int32_t eul = __shfl_up_sync(FULL, eU, 1);
+    if (lane == 0) { el = errLi; eul = eLU; }
+    // x + err = q * m exactly (|R0| < 2^30 in a REG block)
+    const int64_t n = (int64_t)R0 + err - eU - el + eul;
+    const uint32_t an = (uint32_t)(n < 0 ? -n : n);
+    uint32_t qa = __umulhi(an, M);
+    if (qa * m != an) qa++;
+    const int32_t q = n < 0 ? -(int32_t)qa : (int32_t)qa;
     const int64_t qr = __shfl_sync(FULL, qb, i);
     if (colok) {
-      io.rec[(int64_t)(r0 + i) * Wp + j] = make_int2(o[0] + err[0], o[1] + err[1]);
-      if (reg[0] && reg[1])
-        *reinterpret_cast<uint32_t*>(io.qd + qr + 2 * lane) = sym[0] | (sym[1] << 16);
-      else if (reg[0])
-        io.qd[qr + 2 * lane] = (uint16_t)sym[0];
-      else if (reg[1])
-        io.qd[qr + 2 * lane + 1] = (uint16_t)sym[1];
+      recw[2 * ((int64_t)(r0 + i) * Wp + j)] = o + err;
+      io.qd[qr + 2 * lane] = (uint16_t)(q + io.radius);
     }
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      dU[c] = (int32_t)((int64_t)o[c] - pr[c]);
-      eU[c] = colok ? err[c] : 0;
-      dLU[c] = dLi[c];
-      eLU[c] = errLi[c];
-    }
+    dU = d32;
+    eU = colok ? err : 0;
+    dLU = dLi;
+    eLU = errLi;
   }
 }
 
-// Decoder: the interior of block (bi, bj), both components, by one warp
-// (lane = column, rows streamed).  REG: Z = ZU + ZL - ZUL + A, i.e. per row
-// Z(i, j) = Z(i-1, j) + (ZL(i) - ZL(i-1)) + sum_{b<=j} A(i, b) (warp scan;
-// wrapping uint32 arithmetic is exact, the result fits int32) with A =
-// (sym - radius) * 2e; SLOW: Z from the chain's sweep; KNOWN: written by the
-// block kernel (dec_block.cu).  recon = recon(t-1) + Z goes out as (u, v)
-// pairs, float64 (codec.py:425-426 recon * (1/S), exact) and optionally
-// int64.
-__device__ __forceinline__ void bs_final_dec(const BScanIO& io, int bi, int bj,
-                                             int lane) {
+template <int C>
+__device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
+                                              int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
   const int64_t nblk = (int64_t)io.nbx * io.nby;
   const int64_t blk = (int64_t)bi * io.nbx + bj;
   const int Wp = io.Wp, W = io.W;
-  int kind[2];
-#pragma unroll
-  for (int c = 0; c < 2; c++) kind[c] = __ldcg(io.cls + c * nblk + blk) & 3;
-  const bool known[2] = {kind[0] == BS_KNOWN, kind[1] == BS_KNOWN};
-  if (known[0] && known[1]) return;
-  const bool reg[2] = {kind[0] == BS_REG, kind[1] == BS_REG};
+  const int kind = __ldcg(io.cls + C * nblk + blk) & 3;
+  if (kind == BS_KNOWN) return;
+  const bool reg = kind == BS_REG;
   const bool colok = lane < ncl;
   const int j = c0 + (colok ? lane : ncl - 1);
-  int32_t zU[2], zL[2], zLp[2];
-  const int32_t* eb = io.ebot;
-  const int32_t* er = io.eright;
-#pragma unroll
-  for (int c = 0; c < 2; c++) {
-    zU[c] = (bi > 0 && colok) ? __ldcg(eb + (c * nblk + blk - io.nbx) * 32 + lane) : 0;
-    zL[c] = (bj > 0 && lane < nr) ? __ldcg(er + (c * nblk + blk - 1) * 32 + lane) : 0;
-    zLp[c] = (bi > 0 && bj > 0) ? __ldcg(eb + (c * nblk + blk - io.nbx - 1) * 32 + 31) : 0;
-  }
+  const int32_t* eb = io.ebot + C * nblk * 32;
+  const int32_t* er = io.eright + C * nblk * 32;
+  int32_t zU = (bi > 0 && colok) ? __ldcg(eb + (blk - io.nbx) * 32 + lane) : 0;
+  const int32_t zL = (bj > 0 && lane < nr) ? __ldcg(er + (blk - 1) * 32 + lane) : 0;
+  int32_t zLp = (bi > 0 && bj > 0) ? __ldcg(eb + (blk - io.nbx - 1) * 32 + 31) : 0;
   int64_t qb = 0;
-  if (lane < nr)
+  if (reg && lane < nr)
     qb = io.qd_row_off[r0 + lane] +
-         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj];
-  const bool any_reg = reg[0] || reg[1];
-  const int2* pv = io.prevrec;
-  int32_t* recw = reinterpret_cast<int32_t*>(io.rec);
-  // row loads, three rows ahead (a four-slot register ring)
-  uint32_t bsy[4] = {0u, 0u, 0u, 0u};
+         2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + C;
+  const int32_t* pvc = io.prevrec ? reinterpret_cast<const int32_t*>(io.prevrec) + C : nullptr;
+  int32_t* recw = reinterpret_cast<int32_t*>(io.rec) + C;
+  double* f64 = io.f64[C];
+  int64_t* fix = io.fix[C];
+  uint32_t bz[4];
   int bcd[4] = {0, 0, 0, 0};
-  int2 bpp[4];
+  int32_t bpp[4];
   auto issue = [&](int i, int sl) {
     const int ic = min(i, nr - 1);
     const int64_t qr = __shfl_sync(FULL, qb, ic);
     if (i < nr) {
-      if (any_reg) {
-        bsy[sl] = colok ? __ldg(reinterpret_cast<const uint32_t*>(io.qd + qr) + lane) : 0u;
+      const int64_t pk = (int64_t)(r0 + i) * Wp + j;
+      if (reg) {
+        bz[sl] = colok ? (uint32_t)__ldg(io.qd + qr + 2 * lane) : 0u;
         bcd[sl] = __ldg(io.codes + (int64_t)(r0 + i) * io.cpitch + j);
+      } else {
+        bz[sl] = colok ? (uint32_t)__ldcg(io.out[C] + pk) : 0u;
       }
-      bpp[sl] = pv ? __ldg(pv + (int64_t)(r0 + i) * Wp + j) : make_int2(0, 0);
+      bpp[sl] = pvc ? __ldg(pvc + 2 * pk) : 0;
     }
   };
   issue(0, 0);
@@ -793,52 +745,29 @@ __device__ __forceinline__ void bs_final_dec(const BScanIO& io, int bi, int bj,
     const int i = i0 + kk;
     if (i >= nr) break;
     issue(i + 3, (kk + 3) & 3);
-    const uint32_t sy = bsy[kk];
-    const int cd = bcd[kk];
-    const int2 pp = bpp[kk];
-    const int32_t pr[2] = {pp.x, pp.y};
-    int32_t z[2];
+    int32_t z;
+    const int32_t zl = __shfl_sync(FULL, zL, i);
+    if (reg) {
+      const uint32_t e2 = 2u * (uint32_t)io.e_tab[bcd[kk] & 31];
+      uint32_t acc = colok ? (uint32_t)((int32_t)bz[kk] - io.radius) * e2 : 0u;
 #pragma unroll
-    for (int c = 0; c < 2; c++) {
-      const int32_t zl = __shfl_sync(FULL, zL[c], i);
-      if (reg[c]) {
-        const uint32_t e2 = 2u * (uint32_t)io.e_tab[cd & 31];
-        const uint32_t s16 = c ? (sy >> 16) : (sy & 0xffffu);
-        uint32_t acc = colok ? (uint32_t)((int32_t)s16 - io.radius) * e2 : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, acc, o);
-          if (lane >= o) acc += y;
-        }
-        z[c] = (int32_t)((uint32_t)zU[c] + (uint32_t)zl - (uint32_t)zLp[c] + acc);
-      } else if (!known[c]) {
-        z[c] = colok ? __ldcg(io.out[c] + (int64_t)(r0 + i) * Wp + j) : 0;
-      } else {
-        z[c] = 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, acc, o);
+        if (lane >= o) acc += y;
       }
-      zU[c] = z[c];
-      zLp[c] = zl;
+      z = (int32_t)((uint32_t)zU + (uint32_t)zl - (uint32_t)zLp + acc);
+    } else {
+      z = (int32_t)bz[kk];
     }
+    zU = z;
+    zLp = zl;
     if (colok) {
       const int64_t pk = (int64_t)(r0 + i) * Wp + j;
-      const int32_t ru = (int32_t)((uint32_t)z[0] + (uint32_t)pr[0]);
-      const int32_t rv = (int32_t)((uint32_t)z[1] + (uint32_t)pr[1]);
+      const int32_t r = (int32_t)((uint32_t)z + (uint32_t)bpp[kk]);
       const int64_t ko = (int64_t)(r0 + i) * W + j;
-      if (!known[0] && !known[1]) {
-        io.rec[pk] = make_int2(ru, rv);
-      } else if (!known[0]) {
-        recw[2 * pk] = ru;
-      } else {
-        recw[2 * pk + 1] = rv;
-      }
-      if (!known[0]) {
-        io.f64[0][ko] = __dmul_rn((double)ru, io.inv_S);
-        if (io.fix[0]) io.fix[0][ko] = ru;
-      }
-      if (!known[1]) {
-        io.f64[1][ko] = __dmul_rn((double)rv, io.inv_S);
-        if (io.fix[1]) io.fix[1][ko] = rv;
-      }
+      recw[2 * pk] = r;
+      f64[ko] = __dmul_rn((double)r, io.inv_S);
+      if (fix) fix[ko] = r;
     }
   }
 }

@@ -392,13 +392,14 @@ int decode_impl(const vfcp_params* p, const uint8_t* codes, const SYM* qd,
 }
 
 // ------------------------------------------------------------ fast paths
-// Frame-parallel prepare kernels + block scan (fast.cu, bscan.cuh).  Valid for
-// the default 32x32 block grid, 16-bit symbols and tau' < 2^28 (every error
-// term then fits int32); the caller falls back to the generic kernels
-// otherwise.
+// Block kernels + block scan (enc_block.cu, dec_block.cu, bscan.cuh).  Valid
+// for the default 32x32 block grid, 16-bit symbols and tau' < 2^29 (errors,
+// recon values and the residue moduli 2e then fit 32 bits; the few sums that
+// can exceed them are taken in int64); the caller falls back to the generic
+// kernels otherwise.
 bool fast_ok(const vfcp_params* p) {
   return p->bx == 32 && p->by == 32 && p->radius <= 32768 &&
-         p->tau < ((int64_t)1 << 28) && p->stride >= 2 && p->H <= 65535;
+         p->tau < ((int64_t)1 << 29) && p->stride >= 2 && p->H <= 65535;
 }
 
 PrepParams prep_params(const vfcp_params* p, int t, const Ladder& lad) {

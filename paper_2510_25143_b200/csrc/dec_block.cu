@@ -30,6 +30,19 @@ struct DecBlockSmem {
 };
 
 template <typename SYM>
+__device__ __forceinline__ void dec_block_body(
+    const uint8_t* __restrict__ codes_t, const SYM* __restrict__ qd,
+    const int64_t* __restrict__ ll, const uint8_t* __restrict__ modes_t,
+    const int2* __restrict__ prev, int2* __restrict__ rec,
+    const int64_t* __restrict__ qd_row_off,
+    const int64_t* __restrict__ ll_row_off, const int32_t* __restrict__ pre_nl,
+    const int32_t* __restrict__ pre_ll, const PrepParams& p, const BScanIO& bio,
+    uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v,
+    double* __restrict__ f64u, double* __restrict__ f64v,
+    int64_t* __restrict__ fixu, int64_t* __restrict__ fixv, double inv_S,
+    DecBlockSmem& sm);
+
+template <typename SYM>
 __global__ void __launch_bounds__(32 * DB_NW, 3)
 dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
                  const SYM* __restrict__ qd, const int64_t* __restrict__ ll,
@@ -45,6 +58,23 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
                  int64_t* __restrict__ fixu, int64_t* __restrict__ fixv,
                  double inv_S) {
   __shared__ DecBlockSmem sm;
+  dec_block_body<SYM>(codes_t, qd, ll, modes_t, prev, rec, qd_row_off,
+                      ll_row_off, pre_nl, pre_ll, p, bio, pin_u, pin_v, f64u,
+                      f64v, fixu, fixv, inv_S, sm);
+}
+
+template <typename SYM>
+__device__ __forceinline__ void dec_block_body(
+    const uint8_t* __restrict__ codes_t, const SYM* __restrict__ qd,
+    const int64_t* __restrict__ ll, const uint8_t* __restrict__ modes_t,
+    const int2* __restrict__ prev, int2* __restrict__ rec,
+    const int64_t* __restrict__ qd_row_off,
+    const int64_t* __restrict__ ll_row_off, const int32_t* __restrict__ pre_nl,
+    const int32_t* __restrict__ pre_ll, const PrepParams& p, const BScanIO& bio,
+    uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v,
+    double* __restrict__ f64u, double* __restrict__ f64v,
+    int64_t* __restrict__ fixu, int64_t* __restrict__ fixv, double inv_S,
+    DecBlockSmem& sm) {
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;

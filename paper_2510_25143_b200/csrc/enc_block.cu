@@ -52,7 +52,7 @@ struct EncBlockSmem {
   int16_t cnt[2][ETB];
   double rate[2];
   int flag[8];              // see F_* below
-  int32_t etab[32];         // e per code (tau' < 2^28 on this path)
+  int32_t etab[32];         // e per code (tau' < 2^29 on this path)
 };
 enum {
   F_NONUNI = 0,   // a valid code differs from code0
@@ -138,7 +138,7 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
     const bool srw = STRIDE == 2 ? (i & 1) == 0 : rph == 0;
     if (scol && srw) {
       // |idx| = |R0 + D(err')| / m, an exact multiple
-      const int32_t n = R0 + er - eU - el + eul;
+      const int64_t n = (int64_t)R0 + er - eU - el + eul;
       const uint32_t an = (uint32_t)(n < 0 ? -n : n);
       uint32_t qa = __umulhi(an, M);
       if (qa * m != an) qa++;
@@ -163,7 +163,17 @@ static __device__ __noinline__ void trial_rows_generic(
 }
 
 template <typename F>
-__global__ void __launch_bounds__(128, 6)
+__device__ __forceinline__ void enc_block_body(
+    const F* __restrict__ u, const F* __restrict__ v,
+    const uint8_t* __restrict__ codes_t, const int2* __restrict__ prev,
+    int2* __restrict__ rec, const PrepParams& p, const BScanIO& bio,
+    const double* __restrict__ log2tab, uint8_t* __restrict__ modes_t,
+    const int64_t* __restrict__ qd_row_off, const int32_t* __restrict__ pre_nl,
+    uint16_t* __restrict__ qd, int32_t* __restrict__ row_ll,
+    int* __restrict__ overflow, EncBlockSmem& sm);
+
+template <typename F>
+__global__ void __launch_bounds__(128, 8)
 enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
                  const uint8_t* __restrict__ codes_t,   // frame t, pitch W
                  const int2* __restrict__ prev,         // recon(t-1), pitch Wp
@@ -174,6 +184,19 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
                  int32_t* __restrict__ row_ll, int* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EncBlockSmem& sm = *reinterpret_cast<EncBlockSmem*>(smem_raw);
+  enc_block_body<F>(u, v, codes_t, prev, rec, p, bio, log2tab, modes_t,
+                    qd_row_off, pre_nl, qd, row_ll, overflow, sm);
+}
+
+template <typename F>
+__device__ __forceinline__ void enc_block_body(
+    const F* __restrict__ u, const F* __restrict__ v,
+    const uint8_t* __restrict__ codes_t, const int2* __restrict__ prev,
+    int2* __restrict__ rec, const PrepParams& p, const BScanIO& bio,
+    const double* __restrict__ log2tab, uint8_t* __restrict__ modes_t,
+    const int64_t* __restrict__ qd_row_off, const int32_t* __restrict__ pre_nl,
+    uint16_t* __restrict__ qd, int32_t* __restrict__ row_ll,
+    int* __restrict__ overflow, EncBlockSmem& sm) {
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -198,19 +221,44 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
     sm.o[0][rr][cc] = ok ? fixed_t(xu, p.S) : 0;
     sm.o[1][rr][cc] = ok ? fixed_t(xv, p.S) : 0;
   };
-  // recon(t-1) at the delta tile
-#pragma unroll 3
-  for (int k = tid; k < 33 * 33; k += 128) {
-    const int rr = k / 33, cc = k - 33 * rr;
-    const int i = r0 - 1 + rr, j = c0 - 1 + cc;
-    const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
-    const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
-    sm.p[0][rr][cc] = pr.x;
-    sm.p[1][rr][cc] = pr.y;
-  }
   const bool full = nr == 32 && ncl == 32;
   const bool vec = full && sizeof(F) == 4 && (W & 3) == 0 &&
                    (((uintptr_t)uo | (uintptr_t)vo | (uintptr_t)codes_t) & 15) == 0;
+  // recon(t-1) at the delta tile: 16-byte loads (two pairs) inside a full
+  // block, the halo row / column and ragged blocks element-wise
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int idx = tid + 128 * q;     // 512 = 32 rows x 16 pair-pairs
+      const int i = idx >> 4, c2 = (idx & 15) * 2;
+      int4 x = make_int4(0, 0, 0, 0);
+      if (has_prev)
+        x = __ldg(reinterpret_cast<const int4*>(prev + (int64_t)(r0 + i) * Wp + c0 + c2));
+      sm.p[0][i + 1][c2 + 1] = x.x;
+      sm.p[1][i + 1][c2 + 1] = x.y;
+      sm.p[0][i + 1][c2 + 2] = x.z;
+      sm.p[1][i + 1][c2 + 2] = x.w;
+    }
+    if (tid < 65) {
+      const bool rowh = tid < 33;
+      const int rr = rowh ? 0 : tid - 32, cc = rowh ? tid : 0;
+      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
+      const bool ok = has_prev && i >= 0 && j >= 0;
+      const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
+      sm.p[0][rr][cc] = pr.x;
+      sm.p[1][rr][cc] = pr.y;
+    }
+  } else {
+#pragma unroll 3
+    for (int k = tid; k < 33 * 33; k += 128) {
+      const int rr = k / 33, cc = k - 33 * rr;
+      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
+      const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
+      const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
+      sm.p[0][rr][cc] = pr.x;
+      sm.p[1][rr][cc] = pr.y;
+    }
+  }
   if (vec) {
     // interior: 16-byte loads (4 pixels of one component)
 #pragma unroll
@@ -358,7 +406,7 @@ enc_block_kernel(const F* __restrict__ u, const F* __restrict__ v,
   const int nsamp = nsx * nsy;
   int mode = p.force_sl;
   if (p.mop) {
-    const int32_t e = (int32_t)tau;   // fast path: tau' < 2^28
+    const int32_t e = (int32_t)tau;   // fast path: tau' < 2^29
     const double inv = p.lad.inv2e[0];
     const int32_t radius = p.radius;
     if (wid < 2) {

@@ -279,7 +279,7 @@ __device__ __forceinline__ int32_t trial_step(int32_t rho, int32_t q0,
   const int32_t q = qf - ((tie && qf <= 0) ? 1 : 0);
   const bool esc = (uint32_t)(q + radius - 1) >= (uint32_t)(2 * radius - 1);
   *qabs = esc ? -1 : (q < 0 ? -q : q);
-  return esc ? 0 : (q - q0) * 2 * e - y;
+  return esc ? 0 : (int32_t)((int64_t)(q - q0) * 2 * e - y);
 }
 
 }  // namespace vfcp

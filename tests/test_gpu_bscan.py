@@ -42,6 +42,11 @@ CASES = {
     # with escapes (and a ragged last chunk)
     "ints_wide_radius16": (lambda: _ints(40, 9000, 2, 9, -40, 41), 0.02, True, "mop", 16),
     "spectral_wide_sl": (lambda: _synth(2, 48, 8230, 2), 1e-3, True, "sl", 32768),
+    # large steps: tau' in [2^28, 2^29) (the widest the block kernels take,
+    # sums in int64) and just past it (the generic kernels)
+    "large_tau_mop": (lambda: _synth(5, 200, 230, 3), 0.2, True, "mop", 32768),
+    "large_tau_lorenzo": (lambda: _synth(2, 230, 190, 3), 0.35, True, "lorenzo", 32768),
+    "huge_tau_generic": (lambda: _synth(5, 130, 150, 3), 0.6, True, "mop", 32768),
     # integers on a step of one fixed-point unit: exact reconstruction
     "ints_unit_step": (lambda: _ints(300, 260, 2, 8, -3, 4), 2.0 / 2 ** 28, False, "lorenzo", 32768),
 }
@@ -59,6 +64,8 @@ def test_bscan_paths_match_oracle(name):
     ref = O.compress_streams(u, v, H, W, T, 1.0, 1.0, 1.0, eps, cfg,
                              relative=rel)
     assert s.scale == ref["scale"] and s.tau == ref["tau"]
+    if name.startswith("large_tau"):
+        assert 2 ** 28 <= s.tau < 2 ** 29, s.tau
     np.testing.assert_array_equal(s.codes.cpu().numpy(), ref["codes"])
     np.testing.assert_array_equal(s.modes.cpu().numpy(),
                                   ref["modes"].reshape(-1))
