@@ -38,22 +38,19 @@ ALGO_BYTES = {
     "pipeline_compress": 21.125,
     "pipeline_decompress": 21.125,
     "range": 8.0,                      # fp32 u,v
-    "analyze": 8.0 + 1.0 + 0.125,      # fp32 u,v in; code + l_d out
-    # enc_r0: fp32 u,v of frames t and t-1, err(t-1) in; R0 planes and the
-    # recon(t-1) pairs out; codes in and the padded copy out
-    "prep": 8.0 + 8.0 + 8.0 + 8.0 + 8.0 + 2.0,
-    # enc_mop: the R0 tile and one read of recon(t-1) pairs
-    "mop": 8.0 + 8.0,
-    # enc_pix: codes, pin / non-lossless words (semi-Lagrangian pixels are a
-    # data-dependent share on top)
-    "pix": 1.0 + 12.0 / 32.0,
-    # block scan (bs_chain_kernel: chain tasks + interior tasks): two
-    # 32-value edges per block and component, then R0 planes in, err planes
-    # + 2 x u16 symbols out
-    "bs_chain": 2 * 2 * 2 * 32 * 4 / 1024.0 + 8.0 + 8.0 + 4.0,
+    # split analysis: fp32 u,v in (the cube test), the code memset and l_d
+    # out (the exact pass over listed anchors is data-dependent and small)
+    "analyze": 8.0 + 1.0 + 0.125,
+    # enc_block: orig(t) fp32 u,v + recon(t-1) (u, v) int32 pairs + codes in,
+    # the block edges out (2 comps x 2 edges x 32 x 4 B per 1024 px);
+    # semi-Lagrangian blocks add their recon and symbols (data-dependent)
+    "enc_block": 8.0 + 8.0 + 1.0 + 0.5,
+    # bs_chain (encoder): edges in, then per pixel orig(t) + recon(t-1) in,
+    # recon(t) + 2 x u16 symbols out
+    "bs_chain": 0.5 + 8.0 + 8.0 + 8.0 + 4.0,
     "scan": 1.0,                       # codes
-    # decoder: dec_prep (codes, symbols, recon(t-1) in; A planes out)
-    "decode_rows": 1.0 + 4.0 + 8.0 + 8.0,
+    # dec_block: codes + symbols in, edges out
+    "dec_block": 1.0 + 4.0 + 0.5,
     "aux": 8.0 + 16.0,                 # int32 recon in, 2 x f64 out
 }
 UNITS_FULL = ("analyze", "range")      # per launch: all T frames
@@ -289,19 +286,24 @@ def run_matrix(args):
             am = codec.Archive(H, W, T, 1.0, 1.0, 1.0, s.scale, s.eps, s.tau, cfg,
                                b"", b"", s.ld.cpu().numpy().tobytes(), b"", b"")
             kw = dict(codes=s.codes, qd=s.qd, ll=s.ll, modes=s.modes, ld=s.ld)
-            for _ in range(args.warmup):
-                vg.decompress_device(am, **kw)
-            _lib.prof_enable(True)
-            e0.record(st)
-            for _ in range(args.steps):
-                out = None
-                out = vg.decompress_device(am, **kw)
-            e1.record(st)
-            torch.cuda.synchronize()
-            dms = e0.elapsed_time(e1) / args.steps
-            dprof = _lib.prof_collect()
+            dms, dprof, derr = None, {}, None
+            try:
+                for _ in range(args.warmup):
+                    vg.decompress_device(am, **kw)
+                _lib.prof_enable(True)
+                e0.record(st)
+                for _ in range(args.steps):
+                    out = None
+                    out = vg.decompress_device(am, **kw)
+                e1.record(st)
+                torch.cuda.synchronize()
+                dms = e0.elapsed_time(e1) / args.steps
+                dprof = _lib.prof_collect()
+                del out
+            except ValueError as err:
+                # quirk V7: the reference's decompress raises too
+                derr = str(err)
             _lib.prof_enable(False)
-            del out
             sl = float(s.modes.sum().item()) / max(1, int(s.modes.numel()))
             del s, kw, am
             # end to end: pinned host input -> streams in pinned host memory
@@ -333,11 +335,14 @@ def run_matrix(args):
                              "algo_frac": round(21.125 * N / (cms * 1e-3) / 1e9 / peak, 4),
                              "kernels_ms": {k: round(v[0] / args.steps, 3)
                                             for k, v in prof.items() if v[1]}},
-                "decompress": {"GBps": round(8.0 * N / dms / 1e6, 3),
-                               "ms": round(dms, 3),
-                               "algo_frac": round(21.125 * N / (dms * 1e-3) / 1e9 / peak, 4),
-                               "kernels_ms": {k: round(v[0] / args.steps, 3)
-                                              for k, v in dprof.items() if v[1]}},
+                "decompress": ({"GBps": round(8.0 * N / dms / 1e6, 3),
+                                "ms": round(dms, 3),
+                                "algo_frac": round(21.125 * N / (dms * 1e-3) / 1e9 / peak, 4),
+                                "kernels_ms": {k: round(v[0] / args.steps, 3)
+                                               for k, v in dprof.items() if v[1]}}
+                               if dms is not None else
+                               {"error": derr, "note": "quirk V7: the archive "
+                                "does not decode, as the reference's does not"}),
                 "e2e": {"GBps": round(8.0 * N / e2e_s / 1e9, 3),
                         "ms": round(e2e_s * 1e3, 2),
                         "h2d_bytes": 8 * N, "d2h_bytes": d2h},
@@ -354,7 +359,7 @@ def run_matrix(args):
             }
             rows.append(row)
             print(json.dumps({k: row[k] for k in ("config", "eps_rel")} |
-                             {"c": row["compress"]["GBps"], "d": row["decompress"]["GBps"],
+                             {"c": row["compress"]["GBps"], "d": row["decompress"].get("GBps"),
                               "e2e": row["e2e"]["GBps"]}), flush=True)
         del du, dv, fd, up, vp, fh
         torch.cuda.empty_cache()

@@ -73,12 +73,13 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
-# launch classes of vfcp_prof_collect (capi.cu KClass): "prep" is
-# enc_r0_kernel, "pix" enc_pix_kernel, "decode_rows" dec_prep_kernel (and
-# decode_rows_kernel), "bs_chain" the block-scan kernel (chain + interior)
+# launch classes of vfcp_prof_collect (capi.cu KClass): "analyze" the split
+# analysis (cube test + exact pass), "enc_block" / "dec_block" the per-block
+# frame kernels, "bs_chain" the block-scan kernel (chain + interior passes),
+# "scan" the prefix counts; "mop" / "encode" / "decode" the generic path
 KERNEL_CLASSES = ("range", "analyze", "scan", "mop", "encode", "ll_write",
-                  "decode_rows", "decode_ll", "decode", "aux", "prep",
-                  "bs_local", "bs_chain", "bs_final", "pix")
+                  "decode_rows", "decode_ll", "decode", "aux", "enc_block",
+                  "dec_block", "bs_chain")
 
 
 def prof_enable(on=True):

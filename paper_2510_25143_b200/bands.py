@@ -91,27 +91,36 @@ def analyze_band(u_band, v_band, H: int, W: int, T: int, r0: int, r1: int,
 def face_mask_band(u_band, v_band, H: int, W: int, T: int, r0: int, r1: int,
                    scale: float):
     """12-bit positive-face mask i16[T, r1 - r0, W] of the faces anchored in
-    band rows [r0, r1) (the K7 mask of `verify`, tracking.py:170-195).  A
-    face spans its anchor row and the row below, so the band needs only
-    the halo row below: `u_band`/`v_band` hold rows [r0, min(H, r1 + 1)) of
-    every frame.  Per-band flipped-face counts then add up across ranks
-    (one SUM all-reduce of fc_t, fc_s)."""
+    band rows [r0, r1) (the K7 mask of `verify`, tracking.py:170-195).
+    `u_band`/`v_band` hold the band with its halo rows, rows [h0, h1) of
+    every frame (halo_rows, as analyze_band): a face spans its anchor row and
+    the row below, and the row above keeps the sub-field at least two rows
+    tall for one-row bands (its anchors are dropped; SoS compares vertex ids
+    only by order, which the sub-field keeps).  An empty band (more ranks
+    than rows) gives an empty mask.  Per-band flipped-face counts add up
+    across ranks (one SUM all-reduce of fc_t, fc_s)."""
+    import torch
+
     from .predicates import face_mask_float
-    h1 = min(H, r1 + 1)
+    h0, h1 = halo_rows(H, r0, r1)
+    Hb = max(0, h1 - h0)
     du, dv = to_device(u_band), to_device(v_band)
-    if du.numel() != (h1 - r0) * W * T or dv.numel() != du.numel():
-        raise ValueError("band arrays must hold rows [r0, r1 + 1) of every frame")
-    m = face_mask_float(h1 - r0, W, T, du, dv, scale, host=False)
-    return m.view(T, h1 - r0, W)[:, :r1 - r0]
+    if du.numel() != Hb * W * T or dv.numel() != du.numel():
+        raise ValueError("band arrays must hold rows [h0, h1) of every frame")
+    if r1 <= r0:
+        return torch.zeros((T, 0, W), dtype=torch.int16, device=du.device)
+    m = face_mask_float(Hb, W, T, du, dv, scale, host=False)
+    return m.view(T, Hb, W)[:, r0 - h0:r1 - h0]
 
 
 def flipped_faces(mask_a, mask_b):
     """(fc_t, fc_s) between two masks of the same faces (slice classes are
     bits 0-1, slab classes bits 2-11), counted on the device."""
     import torch
+
+    from .tracking import _popcount12
     x = (mask_a.to(torch.int32) ^ mask_b.to(torch.int32)) & 0xFFF
-    pc = [((x >> b) & 1).sum() for b in range(12)]
-    return int((pc[0] + pc[1]).item()), int(sum(pc[2:]).item())
+    return _popcount12(x & 0x3), _popcount12(x & 0xFFC)
 
 
 def sum_counts(counts, dist=None, device="cuda"):

@@ -775,12 +775,18 @@ __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
 template <bool ENC, typename F = float>
 cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   const size_t smem = sizeof(BSChainSmem);
-  cudaError_t e = cudaFuncSetAttribute(
-      bs_chain_kernel<ENC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static OncePerDevice occ_once;
   int occ = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs_chain_kernel<ENC, F>,
-                                                    32 * BS_NW, smem);
+  cudaError_t e = occ_once.get(
+      [&](int* o) {
+        cudaError_t r = cudaFuncSetAttribute(
+            bs_chain_kernel<ENC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)smem);
+        if (r != cudaSuccess) return r;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            o, bs_chain_kernel<ENC, F>, 32 * BS_NW, smem);
+      },
+      &occ);
   if (e != cudaSuccess) return e;
   const int nseg = (io.nbx + BS_SEG - 1) / BS_SEG;
   const int ntask = bs_ntask(io.nby) + io.nby * nseg;

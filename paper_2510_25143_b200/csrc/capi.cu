@@ -99,8 +99,7 @@ int fail(int code, const std::string& msg) {
 // counts it and, when profiling is on, brackets it with CUDA events on the
 // launching stream (vfcp_prof_*).
 enum KClass { K_RANGE, K_ANALYZE, K_SCAN, K_MOP, K_ENCODE, K_LLW, K_DROWS,
-              K_DLL, K_DECODE, K_AUX, K_PREP, K_BSL, K_BSC, K_BSF, K_PIX,
-              K_NCLS };
+              K_DLL, K_DECODE, K_AUX, K_EBLK, K_DBLK, K_BSC, K_NCLS };
 struct Prof {
   bool on = false;
   int64_t launches = 0;
@@ -580,7 +579,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
     int32_t* rcur = rec + 2 * plane * (t & 1);
     uint8_t* modes_t = t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr;
-    LAUNCH(K_PREP, st,
+    LAUNCH(K_EBLK, st,
            launch_enc_block<F>(u, v, codes + (size_t)t * HW,
                                t > 0 ? rprev : nullptr, rcur, pp, bio, log2tab,
                                modes_t, qd_row_off, pre_nl, qd, row_ll, ovf, st));
@@ -699,7 +698,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
     int32_t* rcur = rec + 2 * plane * (t & 1);
-    LAUNCH(K_DROWS, st,
+    LAUNCH(K_DBLK, st,
            launch_dec_block<uint16_t>(
                codes + (size_t)t * HW, qd, ll,
                t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,

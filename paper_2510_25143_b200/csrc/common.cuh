@@ -64,6 +64,28 @@ struct DecodeParams {
   } while (0)
 #endif
 
+// Host: a per-device "done" flag for one-time launch setup (kernel
+// attributes, occupancy queries), so the per-frame launch loop of a small
+// field does not pay for them at every frame.
+struct OncePerDevice {
+  int val[64];
+  bool done[64] = {};
+  template <typename Fn>
+  cudaError_t get(Fn&& init, int* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return init(out);
+    if (!done[dev]) {
+      e = init(&val[dev]);
+      if (e != cudaSuccess) return e;
+      done[dev] = true;
+    }
+    *out = val[dev];
+    return cudaSuccess;
+  }
+};
+
 // predictors.py:25-30 _rha: round half away from zero (float64 -> int64).
 __device__ __forceinline__ int64_t rha_d(double x) {
   if (x >= 0.0) return (int64_t)floor(__dadd_rn(x, 0.5));

@@ -671,8 +671,15 @@ cudaError_t launch_enc_block(const F* u, const F* v, const uint8_t* codes_t,
                              uint16_t* qd, int32_t* row_ll, int* overflow,
                              cudaStream_t st) {
   const size_t smem = sizeof(EncBlockSmem);
-  cudaError_t e = cudaFuncSetAttribute(
-      enc_block_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static OncePerDevice once;
+  int dummy = 0;
+  const cudaError_t e = once.get(
+      [&](int*) {
+        return cudaFuncSetAttribute(enc_block_kernel<F>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
+      },
+      &dummy);
   if (e != cudaSuccess) return e;
   enc_block_kernel<F><<<dim3(p.nbx, p.nby), 128, smem, st>>>(
       u, v, codes_t, reinterpret_cast<const int2*>(prev),

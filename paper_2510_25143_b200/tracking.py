@@ -267,8 +267,15 @@ def write_trajectory_csv(graph: TrajectoryGraph, path) -> None:
 # ------------------------------------------------------------------ verify
 
 def _popcount12(x):
-    """Per-element popcount of the low 12 bits, summed (torch, on device)."""
-    return int(sum(int(((x >> b) & 1).sum().item()) for b in range(12)))
+    """Per-element popcount of the low 12 bits, summed (torch, on device):
+    SWAR bit counting in int32, one reduction, one host read."""
+    import torch
+    v = x & 0xFFF
+    v = v - ((v >> 1) & 0x555)
+    v = (v & 0x333) + ((v >> 2) & 0x333)
+    v = (v + (v >> 4)) & 0x0F0F
+    v = (v + (v >> 8)) & 0x1F
+    return int(v.sum(dtype=torch.int64).item())
 
 
 def _positive_faces(mask, H, W, T):

@@ -84,9 +84,9 @@ def test_band_face_masks_and_flip_counts(world):
     parts = []
     for rank in range(world):
         r0, r1 = bands.band_rows(H, rank, world)
-        h1 = min(H, r1 + 1)
-        parts.append(bands.face_mask_band(_rows(g["u"], T, H, W, r0, h1),
-                                          _rows(g["v"], T, H, W, r0, h1),
+        h0, h1 = bands.halo_rows(H, r0, r1)
+        parts.append(bands.face_mask_band(_rows(g["u"], T, H, W, h0, h1),
+                                          _rows(g["v"], T, H, W, h0, h1),
                                           H, W, T, r0, r1, S))
     assert torch.equal(torch.cat(parts, dim=1), whole)
 
@@ -98,11 +98,11 @@ def test_band_face_masks_and_flip_counts(world):
     counts = [0, 0]
     for rank in range(world):
         r0, r1 = bands.band_rows(H, rank, world)
-        h1 = min(H, r1 + 1)
-        ma_ = bands.face_mask_band(_rows(u, T, H, W, r0, h1),
-                                   _rows(v, T, H, W, r0, h1), H, W, T, r0, r1, S)
-        mb_ = bands.face_mask_band(_rows(ur, T, H, W, r0, h1),
-                                   _rows(vr, T, H, W, r0, h1), H, W, T, r0, r1, S)
+        h0, h1 = bands.halo_rows(H, r0, r1)
+        ma_ = bands.face_mask_band(_rows(u, T, H, W, h0, h1),
+                                   _rows(v, T, H, W, h0, h1), H, W, T, r0, r1, S)
+        mb_ = bands.face_mask_band(_rows(ur, T, H, W, h0, h1),
+                                   _rows(vr, T, H, W, h0, h1), H, W, T, r0, r1, S)
         ct, cs = bands.flipped_faces(ma_, mb_)
         counts[0] += ct
         counts[1] += cs
@@ -110,3 +110,26 @@ def test_band_face_masks_and_flip_counts(world):
                  FieldSeries(H, W, T, 1.0, 1.0, 1.0, ur, vr), scale=S)
     assert tuple(counts) == (rep.fc_t, rep.fc_s)
     assert rep.fc_t + rep.fc_s > 0
+
+
+def test_face_mask_one_row_and_empty_bands():
+    """bands of one row (world == H) and empty bands (world > H)
+    analyse with the halo row above and give the whole-field mask."""
+    import torch
+    from paper_2510_25143_b200 import bands, synth
+    from paper_2510_25143_b200.field import device_range, scale_for
+    from paper_2510_25143_b200.predicates import face_mask_float
+    H, W, T, u, v = synth.generate(1, 6, 40, 3)
+    S = scale_for(device_range(u, v)[2])
+    whole = face_mask_float(H, W, T, torch.as_tensor(u).cuda(),
+                            torch.as_tensor(v).cuda(), S, host=False).view(T, H, W)
+    for world in (H, H + 3):
+        parts = []
+        for rank in range(world):
+            r0, r1 = bands.band_rows(H, rank, world)
+            h0, h1 = bands.halo_rows(H, r0, r1)
+            m = bands.face_mask_band(_rows(u, T, H, W, h0, h1),
+                                     _rows(v, T, H, W, h0, h1), H, W, T, r0, r1, S)
+            assert m.shape == (T, max(0, r1 - r0), W)
+            parts.append(m)
+        assert torch.equal(torch.cat(parts, dim=1), whole)

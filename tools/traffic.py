@@ -11,10 +11,10 @@ import sys
 from pathlib import Path
 
 CLASSES = {  # kernel name prefix -> bench launch class
-    "vfcp::enc_r0_kernel": "prep", "vfcp::enc_pix_kernel": "pix",
-    "vfcp::enc_mop_kernel": "mop", "vfcp::bs_chain_kernel<1>": "bs_chain",
-    "vfcp::analyze_kernel": "analyze",
-    "vfcp::range_kernel": "range", "vfcp::dec_prep_kernel": "decode_rows",
+    "vfcp::enc_block_kernel": "enc_block", "vfcp::bs_chain_kernel<1": "bs_chain",
+    "vfcp::cube_kernel": "analyze", "vfcp::exact_kernel": "analyze",
+    "vfcp::analyze_kernel": "analyze", "vfcp::range_kernel": "range",
+    "vfcp::dec_block_kernel": "dec_block", "vfcp::bs_chain_kernel<0": "dec_chain",
 }
 UNIT = {"bytes": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
 
@@ -41,6 +41,9 @@ def main(path, H, W, T):
     out = {}
     for cls, a in acc.items():
         n = len(launches[cls])
+        if cls == "analyze":
+            # one analysis = cube + exact + the (empty) fused fallback launch
+            n = max(1, n // 3)
         units = H * W * T if cls in ("analyze", "range") else H * W
         out[cls] = {"dram_bytes_per_unit": round(a["bytes"] / n / units, 4),
                     "launches": n}
