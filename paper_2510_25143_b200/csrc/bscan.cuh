@@ -94,7 +94,9 @@ struct BScanIO {
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
 constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
-constexpr int BS_SEG = 32;      // blocks per progress mark / interior task
+constexpr int BS_SEG = 32;      // blocks per chain progress mark
+constexpr int BS_TW = BS_NW / 2;   // blocks per interior task (a warp per
+                                   // block and component)
 
 __host__ __device__ inline int bs_ntask(int nby) {
   return 2 * ((nby + BS_NW - 1) / BS_NW);
@@ -312,21 +314,25 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
   }
   for (;;) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
-    if (threadIdx.x < BS_NW) sm.done[threadIdx.x] = 0;
-    for (int k = threadIdx.x; k < (BS_NW + 1) * BS_HRING; k += blockDim.x)
-      (&sm.hin[0][0])[k] = 0;
     __syncthreads();
     const int task = sm.task;
+    if (task < ntask) {
+      // a chain task: fresh handoff ring and consumption counters
+      if (threadIdx.x < BS_NW) sm.done[threadIdx.x] = 0;
+      for (int k = threadIdx.x; k < (BS_NW + 1) * BS_HRING; k += blockDim.x)
+        (&sm.hin[0][0])[k] = 0;
+      __syncthreads();
+    }
     if (task >= ntask) {
-      // ---- interior tasks: (segment of BS_SEG blocks, block row), both
+      // ---- interior tasks: (group of BS_TW blocks, block row), both
       // components per warp and block, segment-major, each started once the
       // chain has finished the segment in its row and in the row above (both
       // components)
-      const int nseg = (nbx + BS_SEG - 1) / BS_SEG;
+      const int nseg = (nbx + BS_TW - 1) / BS_TW;
       const int ft = task - ntask;
       if (ft >= nby * nseg) break;
       const int sg = ft / nby, bi = ft - sg * nby;
-      const int b0 = sg * BS_SEG, b1 = min(nbx, b0 + BS_SEG);
+      const int b0 = sg * BS_TW, b1 = min(nbx, b0 + BS_TW);
       if (threadIdx.x < 4) {
         const int comp = threadIdx.x & 1, r = bi - (threadIdx.x >> 1);
         if (r >= 0) {
@@ -788,7 +794,7 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
       },
       &occ);
   if (e != cudaSuccess) return e;
-  const int nseg = (io.nbx + BS_SEG - 1) / BS_SEG;
+  const int nseg = (io.nbx + BS_TW - 1) / BS_TW;
   const int ntask = bs_ntask(io.nby) + io.nby * nseg;
   // persistent: every CTA is resident; tickets hand out the chain tasks
   // (block-row order) first, then the interior tasks
