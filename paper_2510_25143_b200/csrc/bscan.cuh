@@ -44,6 +44,10 @@
 namespace vfcp {
 
 enum : uint8_t { BS_SLOW = 0, BS_KNOWN = 1, BS_REG = 2, BS_DONE = 3 };
+// class word: kind | code << 2 | BS_NARROW (encoder: every |delta| of the
+// block's tile with its halo is below 2^27, so the interior pass works in
+// int32 on the integers themselves instead of residues)
+constexpr int32_t BS_NARROW = 0x100;
 
 struct BScanIO {
   const int32_t* a[2];
@@ -95,8 +99,7 @@ constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
 constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
 constexpr int BS_SEG = 32;      // blocks per chain progress mark
-constexpr int BS_TW = BS_NW / 2;   // blocks per interior task (a warp per
-                                   // block and component)
+constexpr int BS_TW = BS_NW;    // blocks per interior task (a warp per block)
 
 __host__ __device__ inline int bs_ntask(int nby) {
   return 2 * ((nby + BS_NW - 1) / BS_NW);
@@ -140,6 +143,28 @@ __device__ __forceinline__ uint32_t res_i64(int64_t x, uint32_t m, uint32_t M,
                                             uint32_t c32) {
   const uint32_t r = bs_umod((uint32_t)(uint64_t)x, m, M);
   return x < 0 ? bs_msub(r, c32, m) : r;
+}
+// |rha(x / m)| for a = |x| < 2^32 (m = 2e, M = floor(2^32 / m)): the
+// estimate umulhi(a, M) is floor(a / m) or one less; ties (remainder e) round
+// away from zero, as _rha does (predictors.py:25-30)
+__device__ __forceinline__ uint32_t bs_qabs(uint32_t a, uint32_t e, uint32_t m,
+                                            uint32_t M) {
+  uint32_t q = __umulhi(a, M);
+  uint32_t r = a - q * m;
+  if (r >= m) { q++; r -= m; }
+  return q + (r >= e ? 1u : 0u);
+}
+// k = the integer nearest to s / m (|s| < 2^31) and whether s - k m is the
+// tie +-e (whose sign the caller settles in raster order)
+__device__ __forceinline__ int32_t bs_knear(int32_t s, uint32_t e, uint32_t m,
+                                            uint32_t M, bool* tie) {
+  const uint32_t a = s < 0 ? (uint32_t)0 - (uint32_t)s : (uint32_t)s;
+  uint32_t q = __umulhi(a, M);
+  uint32_t r = a - q * m;
+  if (r >= m) { q++; r -= m; }
+  *tie = r == e;
+  q += r > e ? 1u : 0u;
+  return s < 0 ? -(int32_t)q : (int32_t)q;
 }
 // representative in [-e, e] of a residue that is not the tie e
 __device__ __forceinline__ int32_t bs_rep(uint32_t r, uint32_t e, uint32_t m) {
@@ -298,6 +323,9 @@ __device__ __forceinline__ void bs_final_enc1(const BScanIO& io, int bi, int bj,
 template <int C>
 __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
                                               int lane);
+template <typename F>
+__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
+                                             int lane);
 
 template <bool ENC, typename F = float>
 __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
@@ -347,15 +375,14 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
         __threadfence();
       }
       __syncthreads();
-      // one warp per (block, component)
-      for (int x = w; x < 2 * (b1 - b0); x += BS_NW) {
-        const int bj = b0 + (x >> 1);
+      // one warp per block
+      for (int x = w; x < b1 - b0; x += BS_NW) {
+        const int bj = b0 + x;
         if (ENC) {
-          if (x & 1) bs_final_enc1<F, 1>(io, bi, bj, lane);
-          else bs_final_enc1<F, 0>(io, bi, bj, lane);
+          bs_final_enc<F>(io, bi, bj, lane);
         } else {
-          if (x & 1) bs_final_dec1<1>(io, bi, bj, lane);
-          else bs_final_dec1<0>(io, bi, bj, lane);
+          bs_final_dec1<0>(io, bi, bj, lane);
+          bs_final_dec1<1>(io, bi, bj, lane);
         }
       }
       __syncthreads();
@@ -446,7 +473,7 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
         uint32_t e = 0, m = 2, M = 0, pb = 0, pr = 0;
         if (kind0 == BS_REG) {
           if (ENC) {
-            const int code = cls >> 2;
+            const int code = (cls >> 2) & 31;
             e = (uint32_t)sm.etab[code];
             m = 2u * e;
             M = sm.mtab[code];
@@ -582,7 +609,7 @@ __device__ __forceinline__ void bs_final_enc1(const BScanIO& io, int bi, int bj,
   const int64_t blk = (int64_t)bi * io.nbx + bj;
   const int Wp = io.Wp, W = io.W;
   const int32_t cl = __ldcg(io.cls + C * nblk + blk);
-  const int kind = cl & 3, code = cl >> 2;
+  const int kind = cl & 3, code = (cl >> 2) & 31;
   if (kind == BS_KNOWN) return;
   const bool reg = kind == BS_REG;
   const bool colok = lane < ncl;
@@ -695,6 +722,164 @@ __device__ __forceinline__ void bs_final_enc1(const BScanIO& io, int bi, int bj,
     eU = colok ? err : 0;
     dLU = dLi;
     eLU = errLi;
+  }
+}
+
+// Both components of a block that is REG and narrow in both (the usual
+// case): with s(i, j) = ZT(j) + ZL(i) - ZC - delta(i, j) as integers (ZT =
+// errT + deltaT etc. of the exact boundary; |s| < 2^31) the error is err = s
+// - k m with k the integer nearest to s / m, and since D(s) = -R0 the symbol
+// is (R0 + D(err)) / m = -D(k) with k = 0 on the boundary: one rounding per
+// pixel and two shuffles, no residues.  A tie (s - k m = +-e) takes the sign
+// of x = R0 - (errU + errL - errUL) in raster order (rare).
+template <typename F>
+__device__ __forceinline__ void bs_final_enc2(const BScanIO& io, int bi, int bj,
+                                              int lane, int code) {
+  const unsigned FULL = 0xffffffffu;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int nr = min(32, io.H - r0), ncl = min(32, io.W - c0);
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int Wp = io.Wp, W = io.W;
+  const bool colok = lane < ncl;
+  const int j = c0 + (colok ? lane : ncl - 1);
+  const F* opu = static_cast<const F*>(io.orig[0]);
+  const F* opv = static_cast<const F*>(io.orig[1]);
+  const int2* pv = io.prevrec;
+  const float Sf = (float)io.S;
+  auto delta_at = [&](int i, int jj) -> int2 {
+    const int2 p = pv ? __ldg(pv + (int64_t)i * Wp + jj) : make_int2(0, 0);
+    return make_int2(fixed_t(__ldg(opu + (int64_t)i * W + jj), io.S) - p.x,
+                     fixed_t(__ldg(opv + (int64_t)i * W + jj), io.S) - p.y);
+  };
+  (void)Sf;
+  const uint32_t e = (uint32_t)io.e_tab[code], m = 2u * e, M = io.mag_tab[code];
+  const int32_t* ebu = io.ebot;
+  const int32_t* ebv = io.ebot + nblk * 32;
+  const int32_t* eru = io.eright;
+  const int32_t* erv = io.eright + nblk * 32;
+  // exact boundary: Z = err + delta of the row above, the column to the left
+  // and the corner (zero outside the frame)
+  int32_t eTu = 0, eTv = 0, eLu = 0, eLv = 0, eCu = 0, eCv = 0;
+  int2 dT = make_int2(0, 0), dL = make_int2(0, 0), dC = make_int2(0, 0);
+  if (bi > 0) {
+    eTu = colok ? __ldcg(ebu + (blk - io.nbx) * 32 + lane) : 0;
+    eTv = colok ? __ldcg(ebv + (blk - io.nbx) * 32 + lane) : 0;
+    if (colok) dT = delta_at(r0 - 1, j);
+    if (bj > 0) {
+      eCu = __ldcg(ebu + (blk - io.nbx - 1) * 32 + 31);
+      eCv = __ldcg(ebv + (blk - io.nbx - 1) * 32 + 31);
+      dC = delta_at(r0 - 1, c0 - 1);
+    }
+  }
+  if (bj > 0 && lane < nr) {
+    eLu = __ldcg(eru + (blk - 1) * 32 + lane);
+    eLv = __ldcg(erv + (blk - 1) * 32 + lane);
+    dL = delta_at(r0 + lane, c0 - 1);
+  }
+  const int32_t baseu = (eTu + dT.x) - (eCu + dC.x);
+  const int32_t basev = (eTv + dT.y) - (eCv + dC.y);
+  const int32_t ZLu = eLu + dL.x, ZLv = eLv + dL.y;   // lane = row
+  // symbol positions relative to the block's first row (32 rows x 2 W
+  // symbols fit 32 bits)
+  const int64_t q0 = io.qd_row_off[r0] + 2 * (int64_t)io.pre_nl[(int64_t)r0 * io.nchunks + bj];
+  uint32_t qrel = 0;
+  if (lane < nr)
+    qrel = (uint32_t)(io.qd_row_off[r0 + lane] +
+                      2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] - q0);
+  uint16_t* qdb = io.qd + q0 + 2 * lane;
+  int2* recp = io.rec + (int64_t)r0 * Wp + j;
+  int32_t dUu = dT.x, dUv = dT.y, eUu = eTu, eUv = eTv, kUu = 0, kUv = 0;
+  F bu[4], bv[4];
+  int2 bp[4];
+  auto issue = [&](int i, int sl) {
+    if (i < nr) {
+      bu[sl] = __ldg(opu + (int64_t)(r0 + i) * W + j);
+      bv[sl] = __ldg(opv + (int64_t)(r0 + i) * W + j);
+      bp[sl] = pv ? __ldg(pv + (int64_t)(r0 + i) * Wp + j) : make_int2(0, 0);
+    }
+  };
+  issue(0, 0);
+  issue(1, 1);
+  issue(2, 2);
+  for (int i0 = 0; i0 < nr; i0 += 4)
+#pragma unroll
+  for (int kk = 0; kk < 4; kk++) {
+    const int i = i0 + kk;
+    if (i >= nr) break;
+    issue(i + 3, (kk + 3) & 3);
+    const int32_t ou = fixed_t(bu[kk], io.S), ov = fixed_t(bv[kk], io.S);
+    const int32_t du = ou - bp[kk].x, dv = ov - bp[kk].y;
+    const int32_t su = baseu + __shfl_sync(FULL, ZLu, i) - du;
+    const int32_t sv = basev + __shfl_sync(FULL, ZLv, i) - dv;
+    bool tu, tv;
+    int32_t ku = bs_knear(su, e, m, M, &tu);
+    int32_t kv = bs_knear(sv, e, m, M, &tv);
+    int32_t eu = su - ku * (int32_t)m, ev = sv - kv * (int32_t)m;
+    if (__any_sync(FULL, colok && (tu | tv))) {
+      // ties in raster order within the row, per component
+      const int iu = max(i - 1, 0);
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        unsigned tm = __ballot_sync(FULL, colok && (c ? tv : tu));
+        if (!tm) continue;
+        const int32_t d = c ? dv : du, dU = c ? dUv : dUu, eU = c ? eUv : eUu;
+        const int32_t eL = c ? eLv : eLu, ZL = c ? ZLv : ZLu;
+        // left boundary of this row and of the row above (lane 0 only)
+        const int32_t eLi = __shfl_sync(FULL, eL, i), dLi = __shfl_sync(FULL, ZL - eL, i);
+        int32_t eLp = __shfl_sync(FULL, eL, iu), dLp = __shfl_sync(FULL, ZL - eL, iu);
+        if (i == 0) { eLp = c ? eCv : eCu; dLp = c ? dC.y : dC.x; }
+        const int32_t err0 = c ? ev : eu;
+        int32_t cur = (c ? tv : tu) ? 0 : err0;
+        while (tm) {
+          const int jj = __ffs(tm) - 1;
+          tm &= tm - 1u;
+          int32_t el = __shfl_up_sync(FULL, cur, 1);
+          int32_t eul = __shfl_up_sync(FULL, eU, 1);
+          int32_t dl = __shfl_up_sync(FULL, d, 1);
+          int32_t dul = __shfl_up_sync(FULL, dU, 1);
+          if (lane == 0) { el = eLi; eul = eLp; dl = dLi; dul = dLp; }
+          if (lane == jj) {
+            const int64_t R0 = (int64_t)d - dU - dl + dul;
+            const int64_t x = R0 - ((int64_t)eU + el - eul);
+            cur = x > 0 ? (int32_t)e : -(int32_t)e;
+          }
+        }
+        // err = s - k m: the other sign of a tie moves k by one
+        if ((c ? tv : tu) && cur != err0) {
+          if (c) { kv += err0 > cur ? 1 : -1; ev = cur; }
+          else { ku += err0 > cur ? 1 : -1; eu = cur; }
+        }
+      }
+    }
+    int32_t kLu = __shfl_up_sync(FULL, ku, 1), kLv = __shfl_up_sync(FULL, kv, 1);
+    int32_t kULu = __shfl_up_sync(FULL, kUu, 1), kULv = __shfl_up_sync(FULL, kUv, 1);
+    if (lane == 0) { kLu = kLv = kULu = kULv = 0; }
+    const int32_t qu = kUu + kLu - kULu - ku, qv = kUv + kLv - kULv - kv;
+    const uint32_t qo = __shfl_sync(FULL, qrel, i);
+    if (colok) {
+      recp[(int64_t)i * Wp] = make_int2(ou + eu, ov + ev);
+      *reinterpret_cast<uint32_t*>(qdb + qo) =
+          (uint32_t)(qu + io.radius) | ((uint32_t)(qv + io.radius) << 16);
+    }
+    kUu = ku; kUv = kv;
+    dUu = du; dUv = dv;
+    eUu = colok ? eu : 0; eUv = colok ? ev : 0;
+  }
+}
+
+template <typename F>
+__device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
+                                             int lane) {
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int32_t cu = __ldcg(io.cls + blk), cv = __ldcg(io.cls + nblk + blk);
+  const int32_t want = BS_REG | BS_NARROW;
+  if ((cu & (3 | BS_NARROW)) == want && (cv & (3 | BS_NARROW)) == want) {
+    bs_final_enc2<F>(io, bi, bj, lane, (cu >> 2) & 31);
+  } else {
+    bs_final_enc1<F, 0>(io, bi, bj, lane);
+    bs_final_enc1<F, 1>(io, bi, bj, lane);
   }
 }
 

@@ -92,6 +92,12 @@ __device__ __forceinline__ int64_t rha_d(double x) {
   return -(int64_t)floor(__dadd_rn(-x, 0.5));
 }
 
+// the same for |x| < 2^31 - 1 (one 32-bit conversion)
+__device__ __forceinline__ int32_t rha_d32(double x) {
+  const int32_t r = __double2int_rd(__dadd_rn(fabs(x), 0.5));
+  return x < 0.0 ? -r : r;
+}
+
 // field.py:295-297 / 313-336: sign(x*S) * floor(|x*S| + 0.5).
 __device__ __forceinline__ int32_t fixed_of(double x, double S) {
   double y = __dmul_rn(x, S);

@@ -62,6 +62,7 @@ enum {
   F_UNSAFE_T = 4, // bit c: comp c has |R0| >= lim(tau') (trial sweep)
   F_UNSAFE_0 = 5, // bit c: comp c has |R0| >= lim(e0)
   F_OVF = 6,      // some |R0| >= 2^31 - 1
+  F_TIE = 7,      // the sample-parallel Lorenzo trial met a tie
 };
 
 // recon(t-1) of component c at delta-tile coordinates (rr, cc) (row 0 =
@@ -152,6 +153,33 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
     dU = d;
     hU = hl;
   }
+}
+
+// The same trial without the row recurrence (stride 2, narrow tile, no
+// escapes).  With s(i, j) = dT(j) + dL(i) - dC - d(i, j) (integers, |s| <
+// 2^31) the trial error is err' = s - k m, k the integer nearest to s / m,
+// and since D(s) = -D(d) = -R0 the symbol R0 + D(err') = -m D(k): one
+// rounding per pixel, no shuffles, k = 0 on the halo row / column.  A task is
+// one (sample, component): the 2x2 pixels ending at the sample.  A tie
+// (s - k m = +-e, decided in raster order by the sign of x) sends the block
+// to trial_rows.
+__device__ __forceinline__ bool trial_sample(const int32_t (*o)[33],
+                                             const int32_t (*pv)[33], int i,
+                                             int j, uint32_t e, uint32_t m,
+                                             uint32_t M, int* qabs) {
+  // tile coordinates: pixel (a, b) of the block is [a + 1][b + 1]
+  auto dl = [&](int rr, int cc) -> int32_t { return o[rr][cc] - pv[rr][cc]; };
+  const int32_t dC = dl(0, 0);
+  const int32_t bT0 = dl(0, j) - dC, bT1 = dl(0, j + 1) - dC;
+  const int32_t dL0 = dl(i, 0), dL1 = dl(i + 1, 0);
+  bool t00, t01, t10, t11;
+  const int32_t k00 = bs_knear(bT0 + dL0 - dl(i, j), e, m, M, &t00);
+  const int32_t k01 = bs_knear(bT1 + dL0 - dl(i, j + 1), e, m, M, &t01);
+  const int32_t k10 = bs_knear(bT0 + dL1 - dl(i + 1, j), e, m, M, &t10);
+  const int32_t k11 = bs_knear(bT1 + dL1 - dl(i + 1, j + 1), e, m, M, &t11);
+  const int32_t q = k11 - k01 - k10 + k00;
+  *qabs = q < 0 ? -q : q;
+  return t00 | t01 | t10 | t11;
 }
 
 // the runtime-stride / wide-tile trial (rare) out of line
@@ -320,16 +348,18 @@ __device__ __forceinline__ void enc_block_body(
   __syncthreads();
   const PvTile pvt{sm.p};
   {
-    // max |delta| over the delta tile
-    int64_t maxd = 0;
+    // max |delta| over the delta tile (|o - p| < 2^32: exact in uint32)
+    uint32_t maxd = 0;
+    auto absdiff = [](int32_t a, int32_t b) -> uint32_t {
+      return a > b ? (uint32_t)a - (uint32_t)b : (uint32_t)b - (uint32_t)a;
+    };
 #pragma unroll 3
     for (int k = tid; k < 33 * 33; k += 128) {
-      const int rr = k / 33, cc = k - 33 * rr;
-      const int64_t du = (int64_t)sm.o[0][rr][cc] - pvt.at(0, rr, cc);
-      const int64_t dv = (int64_t)sm.o[1][rr][cc] - pvt.at(1, rr, cc);
-      maxd = max(maxd, max(du < 0 ? -du : du, dv < 0 ? -dv : dv));
+      const uint32_t du = absdiff((&sm.o[0][0][0])[k], (&sm.p[0][0][0])[k]);
+      const uint32_t dv = absdiff((&sm.o[1][0][0])[k], (&sm.p[1][0][0])[k]);
+      maxd = max(maxd, max(du, dv));
     }
-    int md = (int)min(maxd, (int64_t)INT32_MAX);
+    int md = (int)min(maxd, (uint32_t)INT32_MAX);
     md = __reduce_max_sync(FULL, md);
     if (lane == 0) atomicMax(&sm.flag[F_MAXD], md);
   }
@@ -409,6 +439,25 @@ __device__ __forceinline__ void enc_block_body(
     const int32_t e = (int32_t)tau;   // fast path: tau' < 2^29
     const double inv = p.lad.inv2e[0];
     const int32_t radius = p.radius;
+    // sample-parallel trial when the tile is narrow and cannot escape
+    const bool kform = narrow && p.stride == 2 && (sm.flag[F_UNSAFE_T] & 3) == 0;
+    if (kform) {
+      const uint32_t ue = (uint32_t)e, m = 2u * ue, M = bio.mag_tab[0];
+      const int comp = lane >> 4, sj = lane & 15;
+      const int32_t(*o)[33] = sm.o[comp];
+      const int32_t(*pv)[33] = sm.p[comp];
+      bool tie = false;
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int si = wid + 4 * r;
+        if (2 * si < nr && 2 * sj < ncl) {
+          int qa;
+          tie |= trial_sample(o, pv, 2 * si, 2 * sj, ue, m, M, &qa);
+          sm.samp[0][2 * (si * nsx + sj) + comp] = (int16_t)qa;
+        }
+      }
+      if (__any_sync(FULL, tie) && lane == 0) sm.flag[F_TIE] = 1;
+    } else
     if (wid < 2) {
       // Lorenzo trial of component wid with the step tau' everywhere and a
       // zero error boundary (candidate = orig outside the block)
@@ -481,14 +530,25 @@ __device__ __forceinline__ void enc_block_body(
         const int li = si_i[b] - r0 + 1, lj = si_j[b] - c0 + 1;
         const int64_t ru = (int64_t)sm.o[0][li][lj] - pr_u[b];
         const int64_t rv = (int64_t)sm.o[1][li][lj] - pr_v[b];
-        const int64_t qu = quant_rha(ru, tau, inv), qv = quant_rha(rv, tau, inv);
-        sm.samp[1][2 * sidx] = (int16_t)((qu > -radius && qu < radius) ? (qu < 0 ? -qu : qu) : -1);
-        sm.samp[1][2 * sidx + 1] = (int16_t)((qv > -radius && qv < radius) ? (qv < 0 ? -qv : qv) : -1);
+        // |idx| = |rha(r / 2 tau')|, |r| < 2^32
+        const uint32_t mt = 2u * (uint32_t)e, Mt = bio.mag_tab[0];
+        const uint32_t qu = bs_qabs((uint32_t)(ru < 0 ? -ru : ru), (uint32_t)e, mt, Mt);
+        const uint32_t qv = bs_qabs((uint32_t)(rv < 0 ? -rv : rv), (uint32_t)e, mt, Mt);
+        sm.samp[1][2 * sidx] = (int16_t)(qu < (uint32_t)radius ? (int)qu : -1);
+        sm.samp[1][2 * sidx + 1] = (int16_t)(qv < (uint32_t)radius ? (int)qv : -1);
         sm.spu[sidx] = (int32_t)pr_u[b];
         sm.spv[sidx] = (int32_t)pr_v[b];
       }
     }
     __syncthreads();
+    if (kform && sm.flag[F_TIE]) {
+      // rare: a tie somewhere in the block, the trial in raster order
+      if (wid < 2)
+        trial_rows<int32_t, 2>(sm.o[wid], pvt, nr, ncl, 2, nsx, e,
+                               2u * (uint32_t)e, bio.mag_tab[0], bio.c32_tab[0],
+                               &sm.samp[0][0], wid, lane);
+      __syncthreads();
+    }
     if (wid == 0 || wid == 2) {
       const int tr = wid >> 1;
       const double r = block_rate(sm.samp[tr], 2 * nsamp, sm.cnt[tr], sm.order[tr],
@@ -552,13 +612,17 @@ __device__ __forceinline__ void enc_block_body(
         int nll = (colok && !nl) ? 2 : 0;
         const unsigned bnl = __ballot_sync(FULL, nl);
         if (nl) {
-          const int64_t two_e = 2 * e;
-          const int64_t qu = quant_rha((int64_t)ou - pu[q], e, inv2e[cd]);
-          const int64_t qv = quant_rha((int64_t)ov - pv[q], e, inv2e[cd]);
-          const bool oku = qu > -p.radius && qu < p.radius;
-          const bool okv = qv > -p.radius && qv < p.radius;
-          if (oku) ru = (int32_t)(pu[q] + qu * two_e);
-          if (okv) rv = (int32_t)(pv[q] + qv * two_e);
+          // idx = rha(r / 2e) from its magnitude (|r| < 2^32); recon fits
+          // int32, so pred + idx * 2e may wrap on the way
+          const uint32_t ue = (uint32_t)e, m = 2u * ue, M = bio.mag_tab[cd & 31];
+          const int64_t du = (int64_t)ou - pu[q], dv = (int64_t)ov - pv[q];
+          const uint32_t au = bs_qabs((uint32_t)(du < 0 ? -du : du), ue, m, M);
+          const uint32_t av = bs_qabs((uint32_t)(dv < 0 ? -dv : dv), ue, m, M);
+          const bool oku = au < (uint32_t)p.radius, okv = av < (uint32_t)p.radius;
+          const int32_t qu = du < 0 ? -(int32_t)au : (int32_t)au;
+          const int32_t qv = dv < 0 ? -(int32_t)av : (int32_t)av;
+          if (oku) ru = (int32_t)((uint32_t)pu[q] + (uint32_t)qu * m);
+          if (okv) rv = (int32_t)((uint32_t)pv[q] + (uint32_t)qv * m);
           const uint32_t syu = oku ? (uint32_t)(qu + p.radius) : 0u;
           const uint32_t syv = okv ? (uint32_t)(qv + p.radius) : 0u;
           const int64_t row = rowbase + r0 + i;
@@ -645,7 +709,9 @@ __device__ __forceinline__ void enc_block_body(
       }
       bio.lb[(c * nblk + blk) * 32 + lane] = lbv;
       bio.lr[(c * nblk + blk) * 32 + lane] = lrv;
-      if (lane == 0) bio.cls[c * nblk + blk] = BS_REG | (code0 << 2);
+      if (lane == 0)
+        bio.cls[c * nblk + blk] = BS_REG | (code0 << 2) |
+                                  (sm.flag[F_MAXD] < (1 << 27) ? BS_NARROW : 0);
     } else if (lane == 0) {
       bio.cls[c * nblk + blk] = BS_SLOW;
     }

@@ -115,8 +115,9 @@ __device__ __forceinline__ void bilinear2(const Src& s, int H, int W,
   vv = __dadd_rn(vv, __dmul_rn(w01, v01));
   vv = __dadd_rn(vv, __dmul_rn(w10, v10));
   vv = __dadd_rn(vv, __dmul_rn(w11, v11));
-  *pu = rha_d(vu);
-  *pv = rha_d(vv);
+  // |recon| < 2^30 + 2^29 on the block path, so is every interpolated value
+  *pu = rha_d32(vu);
+  *pv = rha_d32(vv);
 }
 
 // predictors.py:76-108 + the prediction sample at the departure point
