@@ -69,6 +69,8 @@ struct BScanIO {
                             // (REG) or the known values (KNOWN)
   int32_t* lr;              // [2][nblk][32] block right column, likewise
   unsigned long long* stamps;  // optional [2][nby][3] ns: start, first top, end
+  int dbg_skip_interior;       // VFCP_CHAIN_ONLY (timing experiments only)
+  unsigned long long* phase;   // optional [nby][8] clock cycles per chain phase (comp u)
   unsigned long long* prog;    // [2][nby]: frame tag << 32 | blocks finished
   uint32_t frame_tag;          // unique per frame of a call (t + 1)
   // decoder, frame t: the float64 output recon * inv_S (and optionally the
@@ -96,9 +98,10 @@ struct BScanIO {
 };
 
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
-constexpr int BS_HRING = 256;   // shared boundary ring (columns), power of 2
-constexpr int BS_PF = 8;        // blocks of (class, LB, LR) staged ahead
+constexpr int BS_HRING = 1024;   // shared boundary ring (columns), power of 2
 constexpr int BS_SEG = 32;      // blocks per chain progress mark
+constexpr int BS_CH = 4;        // blocks per chain step (a chunk)
+constexpr int BS_SPIN_NS = 64;  // back-off of a waiting chain warp (its polls share the MIO pipe)
 constexpr int BS_TW = BS_NW;    // blocks per interior task (a warp per block)
 
 __host__ __device__ inline int bs_ntask(int nby) {
@@ -195,29 +198,55 @@ struct BSChainSmem {
   int32_t etab[32];
   uint32_t mtab[32];
   int task;
-  int done[BS_NW];                     // blocks warp w has consumed
-  alignas(16) int32_t pf[BS_NW][BS_PF][64];   // LB (0..31), LR (32..63)
-  alignas(16) int32_t pfd[BS_NW][32][4];      // per-lane sink of idle copies
-  int32_t pfc[BS_NW][BS_PF];           // class word per block
-  struct {
-    struct {
-      uint64_t hin[BS_NW + 1][BS_HRING];   // tagged (column + 1) << 32 | value
-      // slow path tiles, [row][col] unpadded: the skewed sweep reads column
-      // s - lane in row lane, distinct banks across lanes
-      int32_t tv[BS_NW][32][32];           // slow path: values
-    };
-  };
+  int done[BS_NW];   // blocks of the row above that warp w has read
+  int pub[BS_NW];    // blocks warp w has handed to warp w + 1
+  // (LB, LR, class) of two chunks per warp (cp.async ring)
+  alignas(16) int32_t pfb[BS_NW][2][32 * BS_CH];
+  alignas(16) int32_t pfr[BS_NW][2][32 * BS_CH];
+  alignas(16) int32_t pfc[BS_NW][2][BS_CH];
+  // bottom rows handed from warp w - 1 to warp w (a ring of columns)
+  int32_t hin[BS_NW + 1][BS_HRING];
+  // slow path tiles, [row][col] unpadded: the skewed sweep reads column
+  // s - lane in row lane, distinct banks across lanes
+  int32_t tv[BS_NW][32][32];
 };
+
+// What the exact sweep of one block needs (passed by value to the
+// out-of-line sweep, so the kernel's parameter struct stays in the constant
+// bank)
+struct BSSlowIO {
+  const int32_t* a;
+  const uint8_t* codes;
+  const uint32_t* pin;
+  int32_t* out;
+  uint16_t* qd;
+  const int64_t* qd_row_off;
+  const int32_t* pre_nl;
+  int32_t* row_ll;
+  const void* orig;
+  const int2* prevrec;
+  double S;
+  int cpitch, W, Wp, nchunks, radius;
+};
+__device__ __forceinline__ BSSlowIO bs_slow_io(const BScanIO& io, int comp) {
+  BSSlowIO s;
+  s.a = io.a[comp]; s.codes = io.codes; s.pin = io.pin[comp]; s.out = io.out[comp];
+  s.qd = io.qd; s.qd_row_off = io.qd_row_off; s.pre_nl = io.pre_nl;
+  s.row_ll = io.row_ll; s.orig = io.orig[comp]; s.prevrec = io.prevrec;
+  s.S = io.S; s.cpitch = io.cpitch; s.W = io.W; s.Wp = io.Wp;
+  s.nchunks = io.nchunks; s.radius = io.radius;
+  return s;
+}
 
 // Encoder: R0 = D(orig - recon(t-1)) of a block whose R0 plane the block
 // kernel did not write (a REG block with a tie on its edges); |R0| < 2^30
 // there, so int32 is exact.  Lane = column, rows streamed.
 template <typename F>
-__device__ __forceinline__ void bs_r0_rows(const BScanIO& io, int comp,
+__device__ __forceinline__ void bs_r0_rows(const BSSlowIO& io, int comp,
                                            int r0, int c0, int nr, int ncl,
                                            int32_t (*tv)[32], int lane) {
   const unsigned FULL = 0xffffffffu;
-  const F* op = static_cast<const F*>(io.orig[comp]);
+  const F* op = static_cast<const F*>(io.orig);
   const int2* pv = io.prevrec;
   const int W = io.W, Wp = io.Wp;
   const int j = c0 + min(lane, ncl - 1);
@@ -242,14 +271,14 @@ __device__ __forceinline__ void bs_r0_rows(const BScanIO& io, int comp,
 }
 
 template <bool ENC, typename F>
-__device__ __forceinline__ void bs_slow_block(
-    const BScanIO& io, BSChainSmem& sm, int w, int comp, int bi, int bj,
+static __device__ __noinline__ void bs_slow_block(
+    const BSSlowIO io, BSChainSmem& sm, int w, int comp, int bi, int bj,
     int nr, int ncl, int32_t top, int32_t left, int32_t corner, int lane,
     bool r0_in_plane) {
   const unsigned FULL = 0xffffffffu;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const bool colok = lane < ncl;
-  const int32_t* a = io.a[comp];
+  const int32_t* a = io.a;
   int32_t(*tv)[32] = sm.tv[w];
   if (ENC && !r0_in_plane) bs_r0_rows<F>(io, comp, r0, c0, nr, ncl, tv, lane);
   // encoder: the sweeping lane's row (lane = row): its non-lossless bits and
@@ -272,7 +301,7 @@ __device__ __forceinline__ void bs_slow_block(
   int nesc = 0;
   // encoder: no pins (lossless pixels have e = 0 and err 0; semi-Lagrangian
   // blocks are never swept); decoder: lossless, escaped and SL pixels
-  const uint32_t pw = (!ENC && lane < nr) ? io.pin[comp][(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
+  const uint32_t pw = (!ENC && lane < nr) ? io.pin[(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
   __syncwarp();
   int32_t l = left;
   int32_t ul = __shfl_up_sync(FULL, left, 1);
@@ -308,7 +337,7 @@ __device__ __forceinline__ void bs_slow_block(
     }
   }
   __syncwarp();
-  int32_t* out = io.out[comp];
+  int32_t* out = io.out;
   for (int r = 0; r < nr; r++) {
     const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
     if (colok) out[k] = tv[r][lane];
@@ -327,8 +356,76 @@ template <typename F>
 __device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
                                              int lane);
 
+// One block step of the chain, the general form: any block kind, given the
+// exact row above (top), the exact column to the left (left, lane = row) and
+// the corner.  Returns the block's exact bottom row in *bot_out and its right
+// column in *right_out; publish() hands a bottom row to the block row below
+// (a REG bottom row goes down before the right column is known).
+template <bool ENC, typename F, typename Publish>
+__device__ __forceinline__ void bs_block_step(
+    const BScanIO& io, BSChainSmem& sm, int w, int comp, int bi, int bj,
+    int nr, int ncl, int32_t cls, int32_t lbv, int32_t lrv, int32_t top,
+    int32_t left, int32_t corner, int lane, Publish&& publish,
+    int32_t* bot_out, int32_t* right_out) {
+  const unsigned FULL = 0xffffffffu;
+  const bool colok = lane < ncl;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int kind0 = cls & 3;
+  int kind = kind0;
+  int32_t bot = 0, right = 0;
+  bool published = false;
+  if (kind == BS_REG) {
+    const int32_t ll = __shfl_sync(FULL, left, nr - 1);
+    const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
+    if (ENC) {
+      const int code = (cls >> 2) & 31;
+      const uint32_t e = (uint32_t)sm.etab[code], m = 2u * e, M = sm.mtab[code];
+      const uint32_t rc = bs_res(corner, m, M);
+      const uint32_t pb = bs_madd(bs_res(ll, m, M), bs_msub((uint32_t)lbv, rc, m), m);
+      const uint32_t pr = bs_madd(bs_res(left, m, M), bs_msub((uint32_t)lrv, rc, m), m);
+      // the bottom row is exact unless one of its own residues is a tie:
+      // hand it down first, the right column after
+      const uint32_t rb = bs_madd(bs_res(top, m, M), pb, m);
+      const bool btie = __any_sync(FULL, colok && rb == e);
+      if (!btie) {
+        bot = colok ? bs_rep(rb, e, m) : 0;
+        publish(bot);
+        published = true;
+      }
+      const uint32_t rr = bs_madd(pr, bs_res(tl, m, M), m);
+      const bool rtie = __any_sync(FULL, lane < nr && rr == e);
+      if (btie || rtie) kind = BS_SLOW;
+      else right = bs_rep(rr, e, m);
+    } else {
+      const uint32_t pb = (uint32_t)ll - (uint32_t)corner + (uint32_t)lbv;
+      const uint32_t pr = (uint32_t)left - (uint32_t)corner + (uint32_t)lrv;
+      bot = colok ? (int32_t)((uint32_t)top + pb) : 0;
+      publish(bot);
+      published = true;
+      right = (int32_t)(pr + (uint32_t)tl);
+    }
+  } else if (kind == BS_KNOWN) {
+    bot = lbv;
+    right = lrv;
+  }
+  if (kind == BS_SLOW) {
+    bs_slow_block<ENC, F>(bs_slow_io(io, comp), sm, w, comp, bi, bj, nr, ncl, top, left, corner,
+                          lane, kind0 != BS_REG);
+    bot = sm.tv[w][nr - 1][lane];
+    right = sm.tv[w][lane][ncl - 1];
+    if (lane == 0) io.cls[comp * nblk + (int64_t)bi * io.nbx + bj] = BS_DONE;
+    __syncwarp();
+  }
+  if (!colok) bot = 0;
+  if (lane >= nr) right = 0;
+  if (!published) publish(bot);
+  *bot_out = bot;
+  *right_out = right;
+}
+
 template <bool ENC, typename F = float>
-__global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
+__global__ void __launch_bounds__(32 * BS_NW, 1)
+bs_chain_kernel(const __grid_constant__ BScanIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSChainSmem& sm = *reinterpret_cast<BSChainSmem*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
@@ -344,50 +441,13 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
     if (threadIdx.x == 0) sm.task = atomicAdd(io.ticket, 1);
     __syncthreads();
     const int task = sm.task;
-    if (task < ntask) {
-      // a chain task: fresh handoff ring and consumption counters
-      if (threadIdx.x < BS_NW) sm.done[threadIdx.x] = 0;
-      for (int k = threadIdx.x; k < (BS_NW + 1) * BS_HRING; k += blockDim.x)
-        (&sm.hin[0][0])[k] = 0;
-      __syncthreads();
+    if (task >= ntask) break;
+    // a chain task: fresh handoff counters
+    if (threadIdx.x < BS_NW) {
+      sm.done[threadIdx.x] = 0;
+      sm.pub[threadIdx.x] = 0;
     }
-    if (task >= ntask) {
-      // ---- interior tasks: (group of BS_TW blocks, block row), both
-      // components per warp and block, segment-major, each started once the
-      // chain has finished the segment in its row and in the row above (both
-      // components)
-      const int nseg = (nbx + BS_TW - 1) / BS_TW;
-      const int ft = task - ntask;
-      if (ft >= nby * nseg) break;
-      const int sg = ft / nby, bi = ft - sg * nby;
-      const int b0 = sg * BS_TW, b1 = min(nbx, b0 + BS_TW);
-      if (threadIdx.x < 4) {
-        const int comp = threadIdx.x & 1, r = bi - (threadIdx.x >> 1);
-        if (r >= 0) {
-          const unsigned long long need = ((unsigned long long)io.frame_tag << 32) | (unsigned)b1;
-          const volatile unsigned long long* pg = io.prog + (int64_t)comp * nby + r;
-          long long spins = 0;
-          while (*pg < need) {
-            __nanosleep(128);
-            if (++spins > (1ll << 28)) __trap();   // never: a hang guard
-          }
-        }
-        __threadfence();
-      }
-      __syncthreads();
-      // one warp per block
-      for (int x = w; x < b1 - b0; x += BS_NW) {
-        const int bj = b0 + x;
-        if (ENC) {
-          bs_final_enc<F>(io, bi, bj, lane);
-        } else {
-          bs_final_dec1<0>(io, bi, bj, lane);
-          bs_final_dec1<1>(io, bi, bj, lane);
-        }
-      }
-      __syncthreads();
-      continue;
-    }
+    __syncthreads();
     const int g = task >> 1, comp = task & 1;
     const int bi = g * BS_NW + w;
     if (bi < nby) {
@@ -399,37 +459,44 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
       const uint32_t tag_up = io.tag_base + (uint32_t)task - 1u;   // task - 2
       uint64_t* my_gb = io.bnd + (int64_t)task * W;
       const uint64_t* up_gb = io.bnd + (int64_t)(task - 2) * W;
-      const int32_t* clsp = io.cls + comp * nblk + (int64_t)bi * nbx;
-      const int32_t* lbp = io.lb + (comp * nblk + (int64_t)bi * nbx) * 32;
-      const int32_t* lrp = io.lr + (comp * nblk + (int64_t)bi * nbx) * 32;
+      const int64_t rowblk = comp * nblk + (int64_t)bi * nbx;
+      const int32_t* clsp = io.cls + rowblk;
+      const int32_t* lbp = io.lb + rowblk * 32;
+      const int32_t* lrp = io.lr + rowblk * 32;
+      int32_t* ebp = io.ebot + rowblk * 32 + lane;
+      int32_t* erp = io.eright + rowblk * 32 + lane;
       int32_t left = 0, corner = 0;
       // first warp of a CTA (row above in another CTA): the tagged slots of
-      // the next two blocks are loaded ahead, so a block step does not pay
-      // an L2 round trip whenever the CTA above is ahead
+      // the next chunk are loaded ahead, so a chunk does not pay an L2 round
+      // trip whenever the CTA above is ahead
       const bool gtop = w == 0 && bi > 0;
-      uint64_t g0 = 0, g1 = 0;
-      if (gtop) {
-        if (lane < W) g0 = ld_relaxed_u64(up_gb + lane);
-        if (32 + lane < W) g1 = ld_relaxed_u64(up_gb + 32 + lane);
-      }
-      // (class, LB, LR) of the next BS_PF blocks in flight (cp.async ring):
-      // they do not depend on the recurrence, so the block step never waits
-      // on DRAM
-      auto stage = [&](int b) {
-        // branch-free: lanes 0-15 copy LB / LR (16 bytes each), lane 16 the
-        // class word; the other lanes' copies are empty and land in a sink
-        const bool vb = b < nbx;
-        const int s = b % BS_PF, bb = vb ? b : 0;
-        int32_t* d16 = lane < 16 ? &sm.pf[w][s][4 * lane] : &sm.pfd[w][lane][0];
-        const int32_t* s16 = lane < 8 ? lbp + 32 * bb + 4 * lane
-                                      : lrp + 32 * bb + 4 * ((lane - 8) & 7);
-        cp_async<16>(d16, s16, vb && lane < 16);
-        int32_t* d4 = lane == 16 ? &sm.pfc[w][s] : &sm.pfd[w][lane][0];
-        cp_async<4>(d4, clsp + bb, vb && lane == 16);
+      uint64_t gq[BS_CH];
+      auto gload = [&](int bk0) {
+#pragma unroll
+        for (int b = 0; b < BS_CH; b++) {
+          const int c = 32 * (bk0 + b) + lane;
+          gq[b] = c < W ? ld_relaxed_u64(up_gb + c) : 0;
+        }
+      };
+      if (gtop) gload(0);
+      // (LB, LR, class) of the next two chunks in flight (cp.async): they do
+      // not depend on the recurrence, so the chain never waits on DRAM.  The
+      // LB / LR rows of a chunk's blocks are contiguous: lane l copies 16
+      // bytes of each (block l / 8); copies past the row's end fill zeros
+      auto stage = [&](int ck) {
+        const int bk0 = ck * BS_CH, slot = ck & 1;
+        const bool vb = bk0 + (lane >> 3) < nbx;
+        const int off = vb ? 32 * bk0 + 4 * lane : 0;
+        cp_async<16>(&sm.pfb[w][slot][4 * lane], lbp + off, vb);
+        cp_async<16>(&sm.pfr[w][slot][4 * lane], lrp + off, vb);
+        if (lane < BS_CH) {
+          const bool vc = bk0 + lane < nbx;
+          cp_async<4>(&sm.pfc[w][slot][lane], clsp + (vc ? bk0 + lane : 0), vc);
+        }
         cp_async_commit();
       };
-#pragma unroll 1
-      for (int b = 0; b < BS_PF; b++) stage(b);
+      stage(0);
+      stage(1);
       auto stamp = [&](int k) {
         if (io.stamps && lane == 0) {
           unsigned long long tn;
@@ -438,143 +505,273 @@ __global__ void __launch_bounds__(32 * BS_NW, 3) bs_chain_kernel(BScanIO io) {
         }
       };
       stamp(0);
-      for (int bj = 0; bj < nbx; bj++) {
-        const int c0 = 32 * bj;
-        const int ncl = min(32, W - c0);
-        const int c = c0 + lane;
-        const bool colok = lane < ncl;
-        cp_async_wait_group<BS_PF - 1>();
+      // the ring slots of block b - HRING/32 must have been read before
+      // block b is handed down
+      auto ring_wait = [&](int blast) {
+        if (out_smem && blast >= BS_HRING / 32)
+          spin_ge<BS_SPIN_NS>(&sm.done[w + 1], blast - (BS_HRING / 32 - 1));
+      };
+      auto put_bot = [&](int bj, int32_t b) {
+        const int c = 32 * bj + lane;
+        if (!has_next || c >= W) return;
+        if (out_smem) sm.hin[w + 1][c & (BS_HRING - 1)] = b;
+        else TaggedSlot<int32_t>::put(my_gb + c, tag_me, b);
+      };
+      // blocks [0, n) of this row are in the ring of the warp below
+      auto put_done = [&](int n) {
+        if (out_smem) signal_set(&sm.pub[w], n, lane);
+      };
+      const int32_t e0 = ENC ? sm.etab[0] : 0, m0 = 2 * e0;
+#ifdef VFCP_CHAIN_PHASES
+      long long pc_t = clock64();
+      unsigned long long pc_acc[6] = {0, 0, 0, 0, 0, 0};
+#define BS_PHASE(k)                                   \
+  if (io.phase) {                                     \
+    const long long n_ = clock64();                   \
+    pc_acc[k] += (unsigned long long)(n_ - pc_t);     \
+    pc_t = n_;                                        \
+  }
+#else
+#define BS_PHASE(k)
+#endif
+      const int nchunk = (nbx + BS_CH - 1) / BS_CH;
+      const int32_t e = e0, m = m0;
+      auto add32 = [](int32_t a, int32_t b) -> int32_t {
+        return (int32_t)((uint32_t)a + (uint32_t)b);
+      };
+      auto sub32 = [](int32_t a, int32_t b) -> int32_t {
+        return (int32_t)((uint32_t)a - (uint32_t)b);
+      };
+      // x in [-m, 2m) -> [0, m)
+      auto norm = [&](int32_t x) -> int32_t {
+        if (!ENC) return x;
+        if (x < 0) x += m;
+        if (x >= m) x -= m;
+        return x;
+      };
+      // x in [-e - m, e + m] -> [-e, e]
+      auto center = [&](int32_t x) -> int32_t {
+        if (!ENC) return x;
+        if (x > e) x -= m;
+        else if (x < -e) x += m;
+        return x;
+      };
+#pragma unroll 1
+      for (int ck = 0; ck < nchunk; ck++) {
+        const int bk = ck * BS_CH;
+        const int nb = min(BS_CH, nbx - bk);
+        // ---- the chunk's (class, LB, LR), then the chunk after the next
+        // staged into its slot
+        cp_async_wait_group<1>();
         __syncwarp();
-        const int slot = bj % BS_PF;
-        const int32_t cls = sm.pfc[w][slot];
-        const int32_t lbv = sm.pf[w][slot][lane], lrv = sm.pf[w][slot][32 + lane];
+        const int slot = ck & 1;
+        const int32_t cls_l = lane < nb ? sm.pfc[w][slot][lane] : (int32_t)BS_KNOWN;
+        int32_t lbv[BS_CH], lrv[BS_CH];
+#pragma unroll
+        for (int b = 0; b < BS_CH; b++) {
+          lbv[b] = sm.pfb[w][slot][32 * b + lane];
+          lrv[b] = sm.pfr[w][slot][32 * b + lane];
+        }
+        // LB at the block's last column (the block's own G term)
+        const int ncl_l = max(1, min(32, W - 32 * (bk + lane)));
+        const int32_t lk_l = lane < nb ? sm.pfb[w][slot][32 * lane + ncl_l - 1] : 0;
         __syncwarp();
-        stage(bj + BS_PF);
-        // ---- hand a bottom row to the block row below
-        auto publish = [&](int32_t b) {
-          if (!has_next) return;
-          if (out_smem) {
-            // ring slots of block bj - HRING/32 must have been read (the
-            // reads fed the consumer's computation before it bumped its
-            // counter)
-            if (bj >= BS_HRING / 32 - 1)
-              while (!__all_sync(FULL, *(volatile int*)&sm.done[w + 1] >=
-                                           bj - (BS_HRING / 32 - 1))) {
-              }
-            if (colok)
-              sm.hin[w + 1][c & (BS_HRING - 1)] = ((uint64_t)(c + 1) << 32) | (uint32_t)b;
-          } else if (colok) {
-            TaggedSlot<int32_t>::put(my_gb + c, tag_me, b);
+        stage(ck + 2);
+        BS_PHASE(0)
+        const int kind_l = cls_l & 3;
+        // the chunk's fast form: every block KNOWN or REG with the largest
+        // step (code 0: e = tau' bounds every error of the frame, so the
+        // sums below stay within two moduli); anything else block by block
+        bool general = __any_sync(
+            FULL, kind_l == BS_SLOW || (ENC && kind_l == BS_REG && ((cls_l >> 2) & 31) != 0));
+        // ---- The blocks of a row are coupled only through scalars: with C
+        // the block's bottom-right value and T the value above its last
+        // column, bottom(j) = top(j) + (C - T)(previous block) + LB(j) and
+        // right(i) = left(i) + (T - T(previous block)) + LR(i); for a REG
+        // block G = C - T = G(previous) + LB(last column), whatever the row
+        // above holds (mod 2e in the encoder; wrapping integers in the
+        // decoder).  Lane b holds the scalars of block bk + b.  A chunk of
+        // REG blocks has its G chain and q = G(previous) + LB before the row
+        // above arrives, so a bottom row is one addition away from its top.
+        const bool early = !general && !__any_sync(FULL, lane < nb && kind_l != BS_REG);
+        int32_t t31_l = 0;
+        int kb[BS_CH];
+        int32_t q[BS_CH];
+        auto prep = [&]() {
+          const int32_t ll = __shfl_sync(FULL, left, nr - 1);
+          const int32_t Gin = norm(center(sub32(ll, corner)));
+          int32_t G_l = 0, ps_l = 0;
+#pragma unroll
+          for (int b = 0; b < BS_CH; b++) {
+            int32_t gp = __shfl_up_sync(FULL, G_l, 1);
+            if (b == 0) gp = Gin;
+            if (lane == b) {
+              ps_l = gp;
+              G_l = kind_l == BS_REG ? norm(add32(gp, lk_l))
+                                     : norm(center(sub32(lk_l, t31_l)));
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < BS_CH; b++) {
+            kb[b] = __shfl_sync(FULL, kind_l, b);
+            q[b] = add32(__shfl_sync(FULL, ps_l, b), lbv[b]);   // [0, 2m)
+            if (ENC && q[b] >= m) q[b] -= m;
           }
         };
-        // ---- everything that does not need the row above, before waiting
-        const int kind0 = cls & 3;
-        const int32_t ll = __shfl_sync(FULL, left, nr - 1);
-        uint32_t e = 0, m = 2, M = 0, pb = 0, pr = 0;
-        if (kind0 == BS_REG) {
-          if (ENC) {
-            const int code = (cls >> 2) & 31;
-            e = (uint32_t)sm.etab[code];
-            m = 2u * e;
-            M = sm.mtab[code];
-            const uint32_t rc = bs_res(corner, m, M);
-            pb = bs_madd(bs_res(ll, m, M), bs_msub((uint32_t)lbv, rc, m), m);
-            pr = bs_madd(bs_res(left, m, M), bs_msub((uint32_t)lrv, rc, m), m);
-          } else {
-            pb = (uint32_t)ll - (uint32_t)corner + (uint32_t)lbv;
-            pr = (uint32_t)left - (uint32_t)corner + (uint32_t)lrv;
+        // T of block bk + lane (only a row's last block can be ragged)
+        int32_t top[BS_CH];
+        auto gather_t31 = [&]() {
+#pragma unroll
+          for (int b = 0; b < BS_CH; b++) {
+            const int nclb = max(1, min(32, W - 32 * (bk + b)));
+            const int32_t x = __shfl_sync(FULL, top[b], nclb - 1);
+            if (lane == b) t31_l = x;
           }
+        };
+        if (early) {
+          prep();
+          ring_wait(bk + nb - 1);
         }
-        // ---- the exact row above the block
-        int32_t top = 0;
+        BS_PHASE(1)
+        // ---- the exact rows above the chunk's blocks
+#pragma unroll
+        for (int b = 0; b < BS_CH; b++) top[b] = 0;
         if (bi > 0) {
           if (gtop) {
-            uint64_t wv = colok ? g0 : 0;
-            bool ok = !colok || (uint32_t)(wv >> 32) == tag_up;
-            while (!__all_sync(FULL, ok)) {
-              if (!ok) {
-                wv = ld_relaxed_u64(up_gb + c);
-                ok = (uint32_t)(wv >> 32) == tag_up;
+#pragma unroll
+            for (int b = 0; b < BS_CH; b++) {
+              const int c = 32 * (bk + b) + lane;
+              const bool cv = b < nb && c < W;
+              uint64_t wv = cv ? gq[b] : 0;
+              bool ok = !cv || (uint32_t)(wv >> 32) == tag_up;
+              while (!__all_sync(FULL, ok)) {
+                if (!ok) {
+                  wv = ld_relaxed_u64(up_gb + c);
+                  ok = (uint32_t)(wv >> 32) == tag_up;
+                }
               }
+              top[b] = cv ? (int32_t)(uint32_t)wv : 0;
             }
-            top = (int32_t)(uint32_t)wv;
-            g0 = g1;
-            g1 = c + 64 < W ? ld_relaxed_u64(up_gb + c + 64) : 0;
           } else {
-            const volatile uint64_t* ep = &sm.hin[w][c & (BS_HRING - 1)];
-            uint64_t v = colok ? *ep : 0;
-            bool ok = !colok || (uint32_t)(v >> 32) == (uint32_t)(c + 1);
-            while (!__all_sync(FULL, ok)) {
-              if (!ok) {
-                v = *ep;
-                ok = (uint32_t)(v >> 32) == (uint32_t)(c + 1);
-              }
+            spin_ge<BS_SPIN_NS>(&sm.pub[w - 1], bk + nb);
+#pragma unroll
+            for (int b = 0; b < BS_CH; b++) {
+              const int c = 32 * (bk + b) + lane;
+              if (b < nb && c < W) top[b] = sm.hin[w][c & (BS_HRING - 1)];
             }
-            top = colok ? (int32_t)(uint32_t)v : 0;
           }
-          if (!colok) top = 0;
         }
-        if (bj == 0) stamp(1);
-        int kind = kind0;
-        int32_t bot = 0, right = 0;
-        bool published = false;
-        if (kind == BS_REG) {
-          if (ENC) {
-            // the bottom row is exact unless one of its own residues is a
-            // tie: hand it down first, the right column after
-            const uint32_t rb = bs_madd(bs_res(top, m, M), pb, m);
-            const bool btie = __any_sync(FULL, colok && rb == e);
-            if (!btie) {
-              bot = colok ? bs_rep(rb, e, m) : 0;
-              publish(bot);
-              published = true;
-            }
-            const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
-            const uint32_t rr = bs_madd(pr, bs_res(tl, m, M), m);
-            const bool rtie = __any_sync(FULL, lane < nr && rr == e);
-            if (btie || rtie) kind = BS_SLOW;
-            else right = bs_rep(rr, e, m);
+        if (ck == 0) stamp(1);
+        BS_PHASE(2)
+        int32_t bot[BS_CH], right[BS_CH];
+        if (!general) {
+          if (!early) {
+            gather_t31();
+            prep();
+            ring_wait(bk + nb - 1);
+          }
+          // ---- bottom rows
+          bool tie = false;
+#pragma unroll
+          for (int b = 0; b < BS_CH; b++) {
+            const bool cv = b < nb && 32 * (bk + b) + lane < W;
+            int32_t x = add32(top[b], q[b]);    // [-e, m + e)
+            if (ENC && x > e) x -= m;
+            tie |= ENC && kb[b] == BS_REG && cv && (x == e || x == -e);
+            bot[b] = cv ? (kb[b] == BS_REG ? x : lbv[b]) : 0;
+          }
+          if (ENC && __any_sync(FULL, tie)) {
+            general = true;   // a tie on a bottom row: block by block
           } else {
-            bot = colok ? (int32_t)((uint32_t)top + pb) : 0;
-            publish(bot);
-            published = true;
-            const int32_t tl = __shfl_sync(FULL, top, ncl - 1);
-            right = (int32_t)(pr + (uint32_t)tl);
+#pragma unroll
+            for (int b = 0; b < BS_CH; b++)
+              if (b < nb) put_bot(bk + b, bot[b]);
+            put_done(bk + nb);
           }
-        } else if (kind == BS_KNOWN) {
-          bot = lbv;
-          right = lrv;
         }
-        if (kind == BS_SLOW) {
-          bs_slow_block<ENC, F>(io, sm, w, comp, bi, bj, nr, ncl, top, left,
-                                corner, lane, kind0 != BS_REG);
-          bot = sm.tv[w][nr - 1][lane];
-          right = sm.tv[w][lane][ncl - 1];
-          if (lane == 0) io.cls[comp * nblk + (int64_t)bi * nbx + bj] = BS_DONE;
-          __syncwarp();
+        // the ring reads are complete (the tops are in registers); the next
+        // chunk's slots of the CTA above
+        if (bi > 0) {
+          if (gtop) gload(bk + BS_CH);
+          else signal_set(&sm.done[w], bk + nb, lane);
         }
-        if (!colok) bot = 0;
-        if (lane >= nr) right = 0;
-        if (!published) publish(bot);
-        // ---- the block's exact edges for the interior pass (coalesced)
-        {
-          const int64_t eo = (comp * nblk + (int64_t)bi * nbx + bj) * 32 + lane;
-          io.ebot[eo] = bot;
-          io.eright[eo] = right;
+        BS_PHASE(3)
+        if (!general) {
+          // ---- right columns (lane = row): left -> right, block by block
+          if (early) gather_t31();
+          int32_t cor_l = __shfl_up_sync(FULL, t31_l, 1);
+          if (lane == 0) cor_l = corner;
+          const int32_t prs_l = sub32(t31_l, cor_l);
+#pragma unroll
+          for (int b = 0; b < BS_CH; b++) {
+            if (b >= nb) break;
+            const int32_t ps = __shfl_sync(FULL, prs_l, b);
+            int32_t x = center(add32(left, ps));   // [-e, e]
+            x = add32(x, lrv[b]);                  // [-e, e + m)
+            if (ENC && x > e) x -= m;
+            const bool rtie = ENC && kb[b] == BS_REG && lane < nr && (x == e || x == -e);
+            int32_t rg = kb[b] == BS_REG ? x : lrv[b];
+            if (ENC && __any_sync(FULL, rtie)) {
+              // a tie on the right column: the block is swept exactly (its
+              // bottom row went down already and is unchanged)
+              const int bj = bk + b, ncl = min(32, W - 32 * bj);
+              const int32_t cb = __shfl_sync(FULL, cor_l, b);
+              bs_slow_block<ENC, F>(bs_slow_io(io, comp), sm, w, comp, bi, bj,
+                                    nr, ncl, top[b], left, cb, lane, false);
+              rg = sm.tv[w][lane][ncl - 1];
+              if (lane == 0) io.cls[rowblk + bj] = BS_DONE;
+              __syncwarp();
+            }
+            if (lane >= nr) rg = 0;
+            right[b] = rg;
+            left = rg;
+          }
+          // (only a row's last block can be ragged: t31 is column 31 here)
+          corner = __shfl_sync(FULL, t31_l, nb - 1);
         }
-        if (lane == 0) *(volatile int*)&sm.done[w] = bj + 1;
-        // progress for the interior tasks: the block edges (and any swept
-        // block) are visible GPU-wide before the mark
-        if ((bj + 1) % BS_SEG == 0 || bj + 1 == nbx) {
-          __threadfence();
-          __syncwarp();
-          if (lane == 0)
-            *(volatile unsigned long long*)(io.prog + (int64_t)comp * nby + bi) =
-                ((unsigned long long)io.frame_tag << 32) | (unsigned)(bj + 1);
+        if (general) {
+          // ---- block by block, any block kind (not unrolled: the chunk's
+          // registers are picked by selects so the loop body stays small)
+#pragma unroll 1
+          for (int b = 0; b < nb; b++) {
+            const int bj = bk + b, ncl = min(32, W - 32 * bj);
+            const int32_t cls = __shfl_sync(FULL, cls_l, b);
+            int32_t tb = top[0], lb = lbv[0], lr = lrv[0];
+#pragma unroll
+            for (int k = 1; k < BS_CH; k++)
+              if (b == k) { tb = top[k]; lb = lbv[k]; lr = lrv[k]; }
+            ring_wait(bj);
+            int32_t bo, ri;
+            bs_block_step<ENC, F>(io, sm, w, comp, bi, bj, nr, ncl, cls, lb, lr,
+                                  tb, left, corner, lane,
+                                  [&](int32_t v) {
+                                    put_bot(bj, v);
+                                    put_done(bj + 1);
+                                  },
+                                  &bo, &ri);
+#pragma unroll
+            for (int k = 0; k < BS_CH; k++)
+              if (b == k) { bot[k] = bo; right[k] = ri; }
+            corner = __shfl_sync(FULL, tb, 31);
+            left = ri;
+          }
         }
-        corner = __shfl_sync(FULL, top, 31);
-        left = right;
+        BS_PHASE(4)
+        // ---- the blocks' exact edges for the interior pass (coalesced)
+#pragma unroll
+        for (int b = 0; b < BS_CH; b++) {
+          if (b >= nb) break;
+          ebp[(int64_t)(bk + b) * 32] = bot[b];
+          erp[(int64_t)(bk + b) * 32] = right[b];
+        }
+        BS_PHASE(5)
       }
+#ifdef VFCP_CHAIN_PHASES
+      if (io.phase && comp == 0 && lane == 0)
+        for (int k = 0; k < 6; k++) io.phase[bi * 8 + k] = pc_acc[k];
+#endif
+#undef BS_PHASE
+      cp_async_wait_all();   // the staged chunks past the row's end
       stamp(2);
     }
     __syncthreads();
@@ -963,6 +1160,27 @@ __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
   }
 }
 
+// Phase C as its own kernel, after the chain of the frame has finished: a
+// warp per block, blocks in raster order (neighbouring warps share the cache
+// lines of their halo loads).
+template <bool ENC, typename F = float>
+__global__ void __launch_bounds__(256, 3)
+bs_interior_kernel(const __grid_constant__ BScanIO io) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       blk < nblk; blk += nwarp) {
+    const int bi = (int)(blk / io.nbx), bj = (int)(blk - (int64_t)bi * io.nbx);
+    if (ENC) {
+      bs_final_enc<F>(io, bi, bj, lane);
+    } else {
+      bs_final_dec1<0>(io, bi, bj, lane);
+      bs_final_dec1<1>(io, bi, bj, lane);
+    }
+  }
+}
+
 template <bool ENC, typename F = float>
 cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
   const size_t smem = sizeof(BSChainSmem);
@@ -979,13 +1197,24 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
       },
       &occ);
   if (e != cudaSuccess) return e;
-  const int nseg = (io.nbx + BS_TW - 1) / BS_TW;
-  const int ntask = bs_ntask(io.nby) + io.nby * nseg;
-  // persistent: every CTA is resident; tickets hand out the chain tasks
-  // (block-row order) first, then the interior tasks
-  bs_chain_kernel<ENC, F><<<min(max(occ, 1) * nsm, ntask), 32 * BS_NW, smem, st>>>(io);
+  // persistent: every CTA is resident; tickets hand out the chain tasks in
+  // block-row order (a task waits only for tasks with smaller tickets)
+  bs_chain_kernel<ENC, F><<<min(max(occ, 1) * nsm, bs_ntask(io.nby)), 32 * BS_NW, smem, st>>>(io);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || io.dbg_skip_interior) return e;
+  static OncePerDevice occ2_once;
+  int occ2 = 1;
+  e = occ2_once.get(
+      [&](int* o) {
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            o, bs_interior_kernel<ENC, F>, 256, 0);
+      },
+      &occ2);
+  if (e != cudaSuccess) return e;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t want = (nblk + 7) / 8, cap = (int64_t)max(occ2, 1) * nsm * 4;
+  bs_interior_kernel<ENC, F><<<(int)(want < cap ? want : cap), 256, 0, st>>>(io);
   return cudaGetLastError();
 }
-
 
 }  // namespace vfcp

@@ -467,10 +467,41 @@ void print_chain_stamps(const BScanIO& b, cudaStream_t st) {
     return;
   unsigned long long t0 = ~0ull;
   for (int k = 0; k < b.nby; k++) t0 = h[k * 3] < t0 ? h[k * 3] : t0;
+  if (b.phase) {
+    std::vector<unsigned long long> ph((size_t)b.nby * 8);
+    if (cudaMemcpy(ph.data(), b.phase, sizeof(unsigned long long) * ph.size(),
+                   cudaMemcpyDeviceToHost) == cudaSuccess) {
+      fprintf(stderr, "[chain phases] row: topwait meta chain+bots ringwait rights writes (kcycles)\n");
+      for (int k = 0; k < b.nby; k += (b.nby > 16 ? b.nby / 16 : 1))
+        fprintf(stderr, "  %5d %8.1f %8.1f %8.1f %8.1f %8.1f %8.1f\n", k,
+                ph[k * 8] * 1e-3, ph[k * 8 + 1] * 1e-3, ph[k * 8 + 2] * 1e-3,
+                ph[k * 8 + 3] * 1e-3, ph[k * 8 + 4] * 1e-3, ph[k * 8 + 5] * 1e-3);
+    }
+  }
   fprintf(stderr, "[chain stamps] block row: start first-top end (us, comp u)\n");
   for (int k = 0; k < b.nby; k += (b.nby > 32 ? b.nby / 32 : 1))
     fprintf(stderr, "  %5d %9.1f %9.1f %9.1f\n", k, (h[k * 3] - t0) * 1e-3,
             (h[k * 3 + 1] - t0) * 1e-3, (h[k * 3 + 2] - t0) * 1e-3);
+}
+
+// VFCP_CLS_STATS: block classes of a frame after its chain (DONE = swept)
+void print_cls_stats(const BScanIO& b, int t, cudaStream_t st) {
+  const int64_t nblk = (int64_t)b.nbx * b.nby;
+  std::vector<int32_t> h((size_t)2 * nblk);
+  if (cudaMemcpyAsync(h.data(), b.cls, sizeof(int32_t) * h.size(),
+                      cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return;
+  long cnt[2][4] = {{0}}, codes[32] = {0};
+  for (int c = 0; c < 2; c++)
+    for (int64_t k = 0; k < nblk; k++) {
+      cnt[c][h[c * nblk + k] & 3]++;
+      if ((h[c * nblk + k] & 3) == BS_REG) codes[(h[c * nblk + k] >> 2) & 31]++;
+    }
+  fprintf(stderr, "[cls] t=%d u: slow %ld known %ld reg %ld swept %ld | v: slow %ld known %ld reg %ld swept %ld | reg codes:",
+          t, cnt[0][0], cnt[0][1], cnt[0][2], cnt[0][3], cnt[1][0], cnt[1][1], cnt[1][2], cnt[1][3]);
+  for (int k = 0; k < 32; k++) if (codes[k]) fprintf(stderr, " %d:%ld", k, codes[k]);
+  fprintf(stderr, "\n");
 }
 
 int nsm_of() {
@@ -537,9 +568,9 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   CK(sc.get(&a, (size_t)2 * plane));      // R0 of swept blocks
   CK(sc.get(&out, (size_t)2 * plane));    // err of swept blocks
   CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
-  CK(sc.get(&ticket, (size_t)T));
+  CK(sc.get(&ticket, (size_t)2 * T));   // per frame: chain / interior
   CK(sc.get(&ovf, 1));
-  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
+  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * 2 * T, st));
   CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
   CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
   const bool mop = p->predictor == VFCP_PRED_MOP && p->tau > 0;
@@ -573,7 +604,12 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   bio.qd = qd;
   bio.cpitch = W;
   bio.S = p->scale;
-  if (getenv("VFCP_CHAIN_STAMPS")) CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
+  if (getenv("VFCP_CHAIN_STAMPS")) {
+    CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
+    CK(sc.get(&bio.phase, (size_t)nby * 8));
+  }
+  const bool cls_stats = getenv("VFCP_CLS_STATS") != nullptr;
+  bio.dbg_skip_interior = getenv("VFCP_CHAIN_ONLY") != nullptr;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
@@ -588,7 +624,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.orig[1] = v + (size_t)t * HW;
     bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
     bio.rec = reinterpret_cast<int2*>(rcur);
-    bio.ticket = ticket + t;
+    bio.ticket = ticket + 2 * t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
@@ -596,6 +632,7 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
     bio.frame_tag = (uint32_t)t + 1u;
     LAUNCH(K_BSC, st, (launch_bs_chain<true, F>(bio, nsm, st)));
     if (bio.stamps && t == 1) print_chain_stamps(bio, st);
+    if (cls_stats) print_cls_stats(bio, t, st);
     if (recon)
       LAUNCH(K_AUX, st,
              (recon_pairs_kernel<<<1184, 256, 0, st>>>(
@@ -675,8 +712,8 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   CK(sc.get(&out, (size_t)2 * plane));    // Z of swept blocks
   CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
   CK(sc.get(&pins, (size_t)2 * cplane));
-  CK(sc.get(&ticket, (size_t)T));
-  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * T, st));
+  CK(sc.get(&ticket, (size_t)2 * T));   // per frame: chain / interior
+  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * 2 * T, st));
   LAUNCH(K_SCAN, st,
          launch_chunk_prefix<uint16_t>(codes, qd, qd_row_off, (int64_t)T * H,
                                        W, nchunks, p->tau, pre_nl, pre_ll,
@@ -708,7 +745,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     bio.codes = codes + (size_t)t * HW;
     bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
     bio.rec = reinterpret_cast<int2*>(rcur);
-    bio.ticket = ticket + t;
+    bio.ticket = ticket + 2 * t;
     bio.tag_base = (uint32_t)t * (uint32_t)bs_ntask(nby);
     bio.qd_row_off = qd_row_off + (size_t)t * H;
     bio.pre_nl = pre_nl + (size_t)t * cplane;
