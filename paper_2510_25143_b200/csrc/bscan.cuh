@@ -70,6 +70,7 @@ struct BScanIO {
   int32_t* lr;              // [2][nblk][32] block right column, likewise
   unsigned long long* stamps;  // optional [2][nby][3] ns: start, first top, end
   int dbg_skip_interior;       // VFCP_CHAIN_ONLY (timing experiments only)
+  int vec4;                    // float32 rows 16-byte aligned (W % 4 == 0)
   unsigned long long* phase;   // optional [nby][8] clock cycles per chain phase (comp u)
   unsigned long long* prog;    // [2][nby]: frame tag << 32 | blocks finished
   uint32_t frame_tag;          // unique per frame of a call (t + 1)
@@ -1065,6 +1066,152 @@ __device__ __forceinline__ void bs_final_enc2(const BScanIO& io, int bi, int bj,
   }
 }
 
+// The same block four pixels per lane (float32 input, full 32x32 block, rows
+// 16-byte aligned): lane = (row in a group of four, column quad), eight
+// groups per block, 16-byte loads with three groups in flight.  Every k is
+// independent of the others (see above); the symbol needs the k of the
+// left / upper / upper-left pixels, which come from the lane's own quad, the
+// lane to the left and the group of rows above (one rotation by 8 lanes
+// carries the previous group's last row into lanes 0-7).  A tie anywhere
+// sends the block to the row-streamed form.  Returns false on a tie.
+__device__ __forceinline__ bool bs_final_enc4(const BScanIO& io, int bi, int bj,
+                                              int lane, int code) {
+  const unsigned FULL = 0xffffffffu;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int Wp = io.Wp, W = io.W;
+  const int rq = lane >> 3, cq = lane & 7;
+  const float* opu = static_cast<const float*>(io.orig[0]);
+  const float* opv = static_cast<const float*>(io.orig[1]);
+  const int2* pv = io.prevrec;
+  const float Sf = (float)io.S;
+  const uint32_t e = (uint32_t)io.e_tab[code], m = 2u * e, M = io.mag_tab[code];
+  const int32_t* ebu = io.ebot;
+  const int32_t* ebv = io.ebot + nblk * 32;
+  const int32_t* eru = io.eright;
+  const int32_t* erv = io.eright + nblk * 32;
+  // delta = orig - recon(t-1) of four pixels (u0 v0 u1 v1 ...)
+  struct Quad { float4 u, v; int4 p01, p23; };
+  auto load_quad = [&](int i) -> Quad {
+    Quad q;
+    const int64_t n = (int64_t)i * W + c0 + 4 * cq;
+    q.u = __ldg(reinterpret_cast<const float4*>(opu + n));
+    q.v = __ldg(reinterpret_cast<const float4*>(opv + n));
+    if (pv) {
+      const int4* pp = reinterpret_cast<const int4*>(pv + (int64_t)i * Wp + c0 + 4 * cq);
+      q.p01 = __ldg(pp);
+      q.p23 = __ldg(pp + 1);
+    } else {
+      q.p01 = q.p23 = make_int4(0, 0, 0, 0);
+    }
+    return q;
+  };
+  // exact boundary: Z = err + delta of the row above (the lane's four
+  // columns), the column to the left (lane = row) and the corner
+  int32_t bu[4] = {0, 0, 0, 0}, bv[4] = {0, 0, 0, 0};
+  int32_t ZLu = 0, ZLv = 0, eLu = 0, eLv = 0;
+  auto delta1 = [&](int i, int jj) -> int2 {
+    const int2 p = pv ? __ldg(pv + (int64_t)i * Wp + jj) : make_int2(0, 0);
+    return make_int2(fixed_of_f32(__ldg(opu + (int64_t)i * W + jj), Sf) - p.x,
+                     fixed_of_f32(__ldg(opv + (int64_t)i * W + jj), Sf) - p.y);
+  };
+  if (bi > 0) {
+    const int4 tu = __ldcg(reinterpret_cast<const int4*>(ebu + (blk - io.nbx) * 32) + cq);
+    const int4 tv = __ldcg(reinterpret_cast<const int4*>(ebv + (blk - io.nbx) * 32) + cq);
+    const Quad q = load_quad(r0 - 1);
+    int32_t zcu = 0, zcv = 0;
+    if (bj > 0) {
+      const int2 dC = delta1(r0 - 1, c0 - 1);
+      zcu = __ldcg(ebu + (blk - io.nbx - 1) * 32 + 31) + dC.x;
+      zcv = __ldcg(ebv + (blk - io.nbx - 1) * 32 + 31) + dC.y;
+    }
+    bu[0] = tu.x + (fixed_of_f32(q.u.x, Sf) - q.p01.x) - zcu;
+    bu[1] = tu.y + (fixed_of_f32(q.u.y, Sf) - q.p01.z) - zcu;
+    bu[2] = tu.z + (fixed_of_f32(q.u.z, Sf) - q.p23.x) - zcu;
+    bu[3] = tu.w + (fixed_of_f32(q.u.w, Sf) - q.p23.z) - zcu;
+    bv[0] = tv.x + (fixed_of_f32(q.v.x, Sf) - q.p01.y) - zcv;
+    bv[1] = tv.y + (fixed_of_f32(q.v.y, Sf) - q.p01.w) - zcv;
+    bv[2] = tv.z + (fixed_of_f32(q.v.z, Sf) - q.p23.y) - zcv;
+    bv[3] = tv.w + (fixed_of_f32(q.v.w, Sf) - q.p23.w) - zcv;
+  }
+  if (bj > 0) {
+    eLu = __ldcg(eru + (blk - 1) * 32 + lane);
+    eLv = __ldcg(erv + (blk - 1) * 32 + lane);
+    const int2 dL = delta1(r0 + lane, c0 - 1);
+    ZLu = eLu + dL.x;
+    ZLv = eLv + dL.y;
+  }
+  // symbol positions relative to the block's first row (lane = row)
+  const int64_t q0 = io.qd_row_off[r0] + 2 * (int64_t)io.pre_nl[(int64_t)r0 * io.nchunks + bj];
+  const uint32_t qrel =
+      (uint32_t)(io.qd_row_off[r0 + lane] +
+                 2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] - q0);
+  uint32_t* qdb = reinterpret_cast<uint32_t*>(io.qd + q0) + 4 * cq;
+  int4* recp = reinterpret_cast<int4*>(io.rec + (int64_t)(r0 + rq) * Wp + c0 + 4 * cq);
+  const int32_t rad = io.radius;
+  int32_t kqu[4] = {0, 0, 0, 0}, kqv[4] = {0, 0, 0, 0};   // k of the group above
+  Quad st[3];
+  st[0] = load_quad(r0 + rq);
+  st[1] = load_quad(r0 + 4 + rq);
+#pragma unroll
+  for (int it = 0; it < 8; it++) {
+    if (it + 2 < 8) st[(it + 2) % 3] = load_quad(r0 + 4 * (it + 2) + rq);
+    const Quad& q = st[it % 3];
+    const int i = 4 * it + rq;
+    const int32_t zlu = __shfl_sync(FULL, ZLu, i), zlv = __shfl_sync(FULL, ZLv, i);
+    int32_t ou[4], ov[4], ku[4], kv[4];
+    ou[0] = fixed_of_f32(q.u.x, Sf); ou[1] = fixed_of_f32(q.u.y, Sf);
+    ou[2] = fixed_of_f32(q.u.z, Sf); ou[3] = fixed_of_f32(q.u.w, Sf);
+    ov[0] = fixed_of_f32(q.v.x, Sf); ov[1] = fixed_of_f32(q.v.y, Sf);
+    ov[2] = fixed_of_f32(q.v.z, Sf); ov[3] = fixed_of_f32(q.v.w, Sf);
+    const int32_t pu[4] = {q.p01.x, q.p01.z, q.p23.x, q.p23.z};
+    const int32_t pw[4] = {q.p01.y, q.p01.w, q.p23.y, q.p23.w};
+    bool tie = false;
+    int32_t ru[4], rv[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      bool tu, tv;
+      const int32_t su = bu[c] + zlu - (ou[c] - pu[c]);
+      const int32_t sv = bv[c] + zlv - (ov[c] - pw[c]);
+      ku[c] = bs_knear(su, e, m, M, &tu);
+      kv[c] = bs_knear(sv, e, m, M, &tv);
+      tie |= tu | tv;
+      ru[c] = ou[c] + (su - ku[c] * (int32_t)m);
+      rv[c] = ov[c] + (sv - kv[c] * (int32_t)m);
+    }
+    if (__any_sync(FULL, tie)) return false;
+    // k of the row above: a rotation by one group (lanes 0-7 get the last
+    // row of the group before), then of the pixel to the left
+    int32_t kUu[4], kUv[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      kUu[c] = __shfl_sync(FULL, rq == 3 ? kqu[c] : ku[c], (lane + 24) & 31);
+      kUv[c] = __shfl_sync(FULL, rq == 3 ? kqv[c] : kv[c], (lane + 24) & 31);
+    }
+    int32_t kLu = __shfl_up_sync(FULL, ku[3], 1), kLv = __shfl_up_sync(FULL, kv[3], 1);
+    int32_t kULu = __shfl_up_sync(FULL, kUu[3], 1), kULv = __shfl_up_sync(FULL, kUv[3], 1);
+    if (cq == 0) { kLu = kLv = kULu = kULv = 0; }
+    uint32_t sy[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const int32_t lu = c ? ku[c - 1] : kLu, lv = c ? kv[c - 1] : kLv;
+      const int32_t ulu = c ? kUu[c - 1] : kULu, ulv = c ? kUv[c - 1] : kULv;
+      const int32_t qu = kUu[c] + lu - ulu - ku[c], qv = kUv[c] + lv - ulv - kv[c];
+      sy[c] = (uint32_t)(qu + rad) | ((uint32_t)(qv + rad) << 16);
+      kqu[c] = ku[c];
+      kqv[c] = kv[c];
+    }
+    const uint32_t qo = __shfl_sync(FULL, qrel, i);
+    int4* rp = recp + (int64_t)it * 2 * Wp;   // four rows of Wp pairs down
+    rp[0] = make_int4(ru[0], rv[0], ru[1], rv[1]);
+    rp[1] = make_int4(ru[2], rv[2], ru[3], rv[3]);
+    uint32_t* qp = qdb + (qo >> 1);
+    qp[0] = sy[0]; qp[1] = sy[1]; qp[2] = sy[2]; qp[3] = sy[3];
+  }
+  return true;
+}
+
 template <typename F>
 __device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
                                              int lane) {
@@ -1073,6 +1220,9 @@ __device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
   const int32_t cu = __ldcg(io.cls + blk), cv = __ldcg(io.cls + nblk + blk);
   const int32_t want = BS_REG | BS_NARROW;
   if ((cu & (3 | BS_NARROW)) == want && (cv & (3 | BS_NARROW)) == want) {
+    if (sizeof(F) == 4 && io.vec4 && 32 * bi + 32 <= io.H && 32 * bj + 32 <= io.W &&
+        bs_final_enc4(io, bi, bj, lane, (cu >> 2) & 31))
+      return;
     bs_final_enc2<F>(io, bi, bj, lane, (cu >> 2) & 31);
   } else {
     bs_final_enc1<F, 0>(io, bi, bj, lane);
@@ -1164,7 +1314,7 @@ __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
 // warp per block, blocks in raster order (neighbouring warps share the cache
 // lines of their halo loads).
 template <bool ENC, typename F = float>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, ENC ? 2 : 3)
 bs_interior_kernel(const __grid_constant__ BScanIO io) {
   const int lane = threadIdx.x & 31;
   const int64_t nblk = (int64_t)io.nbx * io.nby;

@@ -610,6 +610,8 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
   }
   const bool cls_stats = getenv("VFCP_CLS_STATS") != nullptr;
   bio.dbg_skip_interior = getenv("VFCP_CHAIN_ONLY") != nullptr;
+  bio.vec4 = sizeof(F) == 4 && (W & 3) == 0 &&
+             (((uintptr_t)u | (uintptr_t)v | (uintptr_t)qd) & 15) == 0;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);

@@ -110,10 +110,11 @@ __device__ __forceinline__ int32_t fixed_of(double x, double S) {
 // are its integer and fractional parts, so rounding half away from zero in
 // binary32 gives the reference's binary64 result with a few FP32 ops.
 __device__ __forceinline__ int32_t fixed_of_f32(float x, float S) {
+  // below 2^23 the sum y +- 0.5 is exact (ulp(y) <= 0.5) and truncation
+  // rounds half away from zero; from 2^23 on y is an integer
   const float y = __fmul_rn(x, S);
-  const float t = truncf(y);
-  const float f = __fsub_rn(y, t);
-  return (int32_t)t + (f >= 0.5f ? 1 : 0) - (f <= -0.5f ? 1 : 0);
+  const float h = fabsf(y) < 8388608.0f ? 0.5f : 0.0f;
+  return __float2int_rz(__fadd_rn(y, copysignf(h, y)));
 }
 __device__ __forceinline__ int32_t fixed_t(float x, double S) {
   return fixed_of_f32(x, (float)S);

@@ -44,12 +44,12 @@ namespace vfcp {
 
 struct EncBlockSmem {
   int32_t o[2][33][33];     // fixed orig(t), [comp][1+i][1+j], halo row/col 0
-  int32_t p[2][33][33];     // recon(t-1) at the delta tile
+  int32_t d[2][33][33];     // delta = orig - recon(t-1) (wrapping int32)
   uint8_t cd[32][36];       // codes of the block (31 outside)
   int32_t spu[256], spv[256];   // SL trial predictions at the samples
   int16_t samp[2][512];     // |idx| per trial sample (-1: escape)
   int16_t order[2][ETB];
-  int16_t cnt[2][ETB];
+  alignas(16) int16_t cnt[2][ETB];
   double rate[2];
   int flag[8];              // see F_* below
   int32_t etab[32];         // e per code (tau' < 2^29 on this path)
@@ -68,9 +68,10 @@ enum {
 // recon(t-1) of component c at delta-tile coordinates (rr, cc) (row 0 =
 // r0 - 1, column 0 = c0 - 1)
 struct PvTile {
-  const int32_t (*t)[33][33];
+  const int32_t (*o)[33][33];
+  const int32_t (*d)[33][33];
   __device__ __forceinline__ int32_t at(int c, int rr, int cc) const {
-    return t[c][rr][cc];
+    return (int32_t)((uint32_t)o[c][rr][cc] - (uint32_t)d[c][rr][cc]);
   }
 };
 
@@ -101,7 +102,10 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
   const unsigned FULL = 0xffffffffu;
   const uint32_t ue = (uint32_t)e;
   const bool colok = lane < ncl;
-  auto dlt = [&](int rr, int cc) -> I { return (I)o[rr][cc] - (I)pp.at(comp, rr, cc); };
+  auto dlt = [&](int rr, int cc) -> I {
+    if (sizeof(I) == 4) return (I)pp.d[comp][rr][cc];
+    return (I)o[rr][cc] - (I)pp.at(comp, rr, cc);
+  };
   const I dT = dlt(0, lane + 1), dC = dlt(0, 0);
   const I hL = dlt(lane + 1, 0);   // lane = row: the left halo of row lane
   const uint32_t rL = res_delta(hL, m, M, c32);
@@ -163,12 +167,11 @@ __device__ __forceinline__ void trial_rows(const int32_t (*o)[33],
 // one (sample, component): the 2x2 pixels ending at the sample.  A tie
 // (s - k m = +-e, decided in raster order by the sign of x) sends the block
 // to trial_rows.
-__device__ __forceinline__ bool trial_sample(const int32_t (*o)[33],
-                                             const int32_t (*pv)[33], int i,
+__device__ __forceinline__ bool trial_sample(const int32_t (*dt)[33], int i,
                                              int j, uint32_t e, uint32_t m,
                                              uint32_t M, int* qabs) {
   // tile coordinates: pixel (a, b) of the block is [a + 1][b + 1]
-  auto dl = [&](int rr, int cc) -> int32_t { return o[rr][cc] - pv[rr][cc]; };
+  auto dl = [&](int rr, int cc) -> int32_t { return dt[rr][cc]; };
   const int32_t dC = dl(0, 0);
   const int32_t bT0 = dl(0, j) - dC, bT1 = dl(0, j + 1) - dC;
   const int32_t dL0 = dl(i, 0), dL1 = dl(i + 1, 0);
@@ -239,56 +242,30 @@ __device__ __forceinline__ void enc_block_body(
   const F* vo = v + (int64_t)p.t * HW;
   const bool has_prev = prev != nullptr;
 
-  // ---- tiles: orig(t) rows r0-1 .. r0+31, columns c0-1 .. c0+31, and
-  // recon(t-1) with an SLH-cell margin (zero outside the frame, as the
-  // reference's Lorenzo terms vanish there)
+  // ---- tiles: orig(t) (fixed point) and delta = orig - recon(t-1) at rows
+  // r0-1 .. r0+31, columns c0-1 .. c0+31 (recon(t-1) is zero outside the
+  // frame, as the reference's Lorenzo terms vanish there); max |delta| on
+  // the way (|o - p| < 2^32: exact in uint32)
   if (tid < 8) sm.flag[tid] = 0;
   if (tid < 32) sm.etab[tid] = bio.e_tab[tid];
-  for (int k = tid; k < 2 * ETB; k += 128) (&sm.cnt[0][0])[k] = 0;
-  auto put = [&](int rr, int cc, F xu, F xv, bool ok) {
-    sm.o[0][rr][cc] = ok ? fixed_t(xu, p.S) : 0;
-    sm.o[1][rr][cc] = ok ? fixed_t(xv, p.S) : 0;
+  reinterpret_cast<uint4*>(&sm.cnt[0][0])[tid] = make_uint4(0, 0, 0, 0);
+  static_assert(2 * ETB * sizeof(int16_t) == 128 * sizeof(uint4), "cnt zeroing");
+  uint32_t maxd = 0;
+  auto put = [&](int rr, int cc, F xu, F xv, int2 pr, bool ok) {
+    const int32_t ou = ok ? fixed_t(xu, p.S) : 0, ov = ok ? fixed_t(xv, p.S) : 0;
+    sm.o[0][rr][cc] = ou;
+    sm.o[1][rr][cc] = ov;
+    sm.d[0][rr][cc] = (int32_t)((uint32_t)ou - (uint32_t)pr.x);
+    sm.d[1][rr][cc] = (int32_t)((uint32_t)ov - (uint32_t)pr.y);
+    const uint32_t du = ou > pr.x ? (uint32_t)ou - (uint32_t)pr.x : (uint32_t)pr.x - (uint32_t)ou;
+    const uint32_t dv = ov > pr.y ? (uint32_t)ov - (uint32_t)pr.y : (uint32_t)pr.y - (uint32_t)ov;
+    maxd = max(maxd, max(du, dv));
   };
   const bool full = nr == 32 && ncl == 32;
   const bool vec = full && sizeof(F) == 4 && (W & 3) == 0 &&
                    (((uintptr_t)uo | (uintptr_t)vo | (uintptr_t)codes_t) & 15) == 0;
-  // recon(t-1) at the delta tile: 16-byte loads (two pairs) inside a full
-  // block, the halo row / column and ragged blocks element-wise
-  if (full) {
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int idx = tid + 128 * q;     // 512 = 32 rows x 16 pair-pairs
-      const int i = idx >> 4, c2 = (idx & 15) * 2;
-      int4 x = make_int4(0, 0, 0, 0);
-      if (has_prev)
-        x = __ldg(reinterpret_cast<const int4*>(prev + (int64_t)(r0 + i) * Wp + c0 + c2));
-      sm.p[0][i + 1][c2 + 1] = x.x;
-      sm.p[1][i + 1][c2 + 1] = x.y;
-      sm.p[0][i + 1][c2 + 2] = x.z;
-      sm.p[1][i + 1][c2 + 2] = x.w;
-    }
-    if (tid < 65) {
-      const bool rowh = tid < 33;
-      const int rr = rowh ? 0 : tid - 32, cc = rowh ? tid : 0;
-      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
-      const bool ok = has_prev && i >= 0 && j >= 0;
-      const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
-      sm.p[0][rr][cc] = pr.x;
-      sm.p[1][rr][cc] = pr.y;
-    }
-  } else {
-#pragma unroll 3
-    for (int k = tid; k < 33 * 33; k += 128) {
-      const int rr = k / 33, cc = k - 33 * rr;
-      const int i = r0 - 1 + rr, j = c0 - 1 + cc;
-      const bool ok = has_prev && i >= 0 && j >= 0 && i < H && j < W;
-      const int2 pr = ok ? __ldg(prev + (int64_t)i * Wp + j) : make_int2(0, 0);
-      sm.p[0][rr][cc] = pr.x;
-      sm.p[1][rr][cc] = pr.y;
-    }
-  }
   if (vec) {
-    // interior: 16-byte loads (4 pixels of one component)
+    // interior: 16-byte loads, four pixels per thread and step
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const int idx = tid + 128 * q;     // 256 = 32 rows x 8 quads
@@ -296,10 +273,16 @@ __device__ __forceinline__ void enc_block_body(
       const int64_t n = (int64_t)(r0 + i) * W + c0 + c4;
       const float4 a = __ldg(reinterpret_cast<const float4*>(uo + n));
       const float4 b = __ldg(reinterpret_cast<const float4*>(vo + n));
-      put(i + 1, c4 + 1, (F)a.x, (F)b.x, true);
-      put(i + 1, c4 + 2, (F)a.y, (F)b.y, true);
-      put(i + 1, c4 + 3, (F)a.z, (F)b.z, true);
-      put(i + 1, c4 + 4, (F)a.w, (F)b.w, true);
+      int4 p01 = make_int4(0, 0, 0, 0), p23 = make_int4(0, 0, 0, 0);
+      if (has_prev) {
+        const int4* pp = reinterpret_cast<const int4*>(prev + (int64_t)(r0 + i) * Wp + c0 + c4);
+        p01 = __ldg(pp);
+        p23 = __ldg(pp + 1);
+      }
+      put(i + 1, c4 + 1, (F)a.x, (F)b.x, make_int2(p01.x, p01.y), true);
+      put(i + 1, c4 + 2, (F)a.y, (F)b.y, make_int2(p01.z, p01.w), true);
+      put(i + 1, c4 + 3, (F)a.z, (F)b.z, make_int2(p23.x, p23.y), true);
+      put(i + 1, c4 + 4, (F)a.w, (F)b.w, make_int2(p23.z, p23.w), true);
     }
     // halo: row r0-1 (33 values incl. the corner), column c0-1
     if (tid < 65) {
@@ -307,13 +290,14 @@ __device__ __forceinline__ void enc_block_body(
       const int rr = rowh ? 0 : tid - 32, cc = rowh ? tid : 0;
       const int i = r0 - 1 + rr, j = c0 - 1 + cc;
       const bool ok = i >= 0 && j >= 0;
-      const int64_t n = ok ? (int64_t)i * W + j : 0;
       F xu = 0, xv = 0;
+      int2 pr = make_int2(0, 0);
       if (ok) {
-        xu = __ldg(uo + n);
-        xv = __ldg(vo + n);
+        xu = __ldg(uo + (int64_t)i * W + j);
+        xv = __ldg(vo + (int64_t)i * W + j);
+        if (has_prev) pr = __ldg(prev + (int64_t)i * Wp + j);
       }
-      put(rr, cc, xu, xv, ok);
+      put(rr, cc, xu, xv, pr, ok);
     }
     // codes: 4-byte loads
 #pragma unroll
@@ -330,13 +314,14 @@ __device__ __forceinline__ void enc_block_body(
       const int rr = k / 33, cc = k - 33 * rr;
       const int i = r0 - 1 + rr, j = c0 - 1 + cc;
       const bool ok = i >= 0 && j >= 0 && i < H && j < W;
-      const int64_t n = ok ? (int64_t)i * W + j : 0;
       F xu = 0, xv = 0;
+      int2 pr = make_int2(0, 0);
       if (ok) {
-        xu = __ldg(uo + n);
-        xv = __ldg(vo + n);
+        xu = __ldg(uo + (int64_t)i * W + j);
+        xv = __ldg(vo + (int64_t)i * W + j);
+        if (has_prev) pr = __ldg(prev + (int64_t)i * Wp + j);
       }
-      put(rr, cc, xu, xv, ok);
+      put(rr, cc, xu, xv, pr, ok);
     }
 #pragma unroll 2
     for (int k = tid; k < 1024; k += 128) {
@@ -345,29 +330,47 @@ __device__ __forceinline__ void enc_block_body(
                                         : (uint8_t)CODE_LOSSLESS;
     }
   }
-  __syncthreads();
-  const PvTile pvt{sm.p};
+  __syncthreads();   // flag[] zeroed before the atomics below
   {
-    // max |delta| over the delta tile (|o - p| < 2^32: exact in uint32)
-    uint32_t maxd = 0;
-    auto absdiff = [](int32_t a, int32_t b) -> uint32_t {
-      return a > b ? (uint32_t)a - (uint32_t)b : (uint32_t)b - (uint32_t)a;
-    };
-#pragma unroll 3
-    for (int k = tid; k < 33 * 33; k += 128) {
-      const uint32_t du = absdiff((&sm.o[0][0][0])[k], (&sm.p[0][0][0])[k]);
-      const uint32_t dv = absdiff((&sm.o[1][0][0])[k], (&sm.p[1][0][0])[k]);
-      maxd = max(maxd, max(du, dv));
-    }
     int md = (int)min(maxd, (uint32_t)INT32_MAX);
     md = __reduce_max_sync(FULL, md);
     if (lane == 0) atomicMax(&sm.flag[F_MAXD], md);
   }
+  const PvTile pvt{sm.o, sm.d};
+  // ---- code checks (whole words in a full block)
+  const int code0 = sm.cd[0][0];
+  {
+    bool nonuni = false, lossy = false, lossless = false;
+    if (full) {
+      const uint32_t cm4 = 0x01010101u * (uint32_t)__popc(p.lossy_mask);
+      const uint32_t c04 = 0x01010101u * (uint32_t)code0;
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int idx = tid + 128 * q;
+        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(&sm.cd[idx >> 3][(idx & 7) * 4]);
+        const uint32_t lt = __vcmpltu4(w4, cm4);   // 0xff where the code quantises
+        nonuni |= w4 != c04;
+        lossy |= lt != 0u;
+        lossless |= lt != 0xffffffffu;
+      }
+    } else {
+      for (int i = wid; i < nr; i += 4) {
+        if (lane >= ncl) continue;
+        const int cd = sm.cd[i][lane];
+        const bool ls = sm.etab[cd & 31] > 0;
+        nonuni |= cd != code0;
+        lossy |= ls;
+        lossless |= !ls;
+      }
+    }
+    if (__any_sync(FULL, nonuni) && lane == 0) sm.flag[F_NONUNI] = 1;
+    if (__any_sync(FULL, lossy) && lane == 0) sm.flag[F_LOSSY] = 1;
+    if (__any_sync(FULL, lossless) && lane == 0) sm.flag[F_LOSSLESS] = 1;
+  }
   __syncthreads();
 
-  // ---- code checks and, unless 4 max|delta| bounds them, the exact R0
-  // escape checks (warp w: rows w, w+4, ...; lane = column)
-  const int code0 = sm.cd[0][0];
+  // ---- unless 4 max|delta| bounds them, the exact R0 escape checks (warp
+  // w: rows w, w+4, ...; lane = column)
   const int64_t e0 = p.lad.e[code0];
   const int64_t tau = p.tau;
   auto lim_of = [&](int64_t e) -> int64_t {
@@ -380,33 +383,18 @@ __device__ __forceinline__ void enc_block_body(
   const bool colok = lane < ncl;
   // R0 of pixel (i, j) from the tiles (exact)
   auto R0_at = [&](int c, int i, int j) -> int64_t {
-    const int32_t(*o)[33] = sm.o[c];
     if (narrow) {
-      const int32_t d = o[i + 1][j + 1] - pvt.at(c, i + 1, j + 1);
-      const int32_t dU = o[i][j + 1] - pvt.at(c, i, j + 1);
-      const int32_t dL = o[i + 1][j] - pvt.at(c, i + 1, j);
-      const int32_t dUL = o[i][j] - pvt.at(c, i, j);
-      return (int64_t)(d - dU - dL + dUL);
+      const int32_t(*dt)[33] = sm.d[c];
+      return (int64_t)(dt[i + 1][j + 1] - dt[i][j + 1] - dt[i + 1][j] + dt[i][j]);
     }
+    const int32_t(*o)[33] = sm.o[c];
     return ((int64_t)o[i + 1][j + 1] - pvt.at(c, i + 1, j + 1)) -
            ((int64_t)o[i][j + 1] - pvt.at(c, i, j + 1)) -
            ((int64_t)o[i + 1][j] - pvt.at(c, i + 1, j)) +
            ((int64_t)o[i][j] - pvt.at(c, i, j));
   };
-  {
-    bool nonuni = false, lossy = false, lossless = false;
-    for (int i = wid; i < nr; i += 4) {
-      if (!colok) continue;
-      const int cd = sm.cd[i][lane];
-      const bool ls = sm.etab[cd & 31] > 0;
-      nonuni |= cd != code0;
-      lossy |= ls;
-      lossless |= !ls;
-    }
-    if (__any_sync(FULL, nonuni) && lane == 0) sm.flag[F_NONUNI] = 1;
-    if (__any_sync(FULL, lossy) && lane == 0) sm.flag[F_LOSSY] = 1;
-    if (__any_sync(FULL, lossless) && lane == 0) sm.flag[F_LOSSLESS] = 1;
-    if (maxd4 >= lim0) {
+  if (maxd4 >= lim0) {   // (uniform over the CTA)
+    {
       bool ovf = false;
       bool unT[2] = {false, false}, un0[2] = {false, false};
       for (int i = wid; i < nr; i += 4) {
@@ -426,9 +414,9 @@ __device__ __forceinline__ void enc_block_body(
       if (lane == 0 && ut) atomicOr(&sm.flag[F_UNSAFE_T], (int)ut);
       if (lane == 0 && u0) atomicOr(&sm.flag[F_UNSAFE_0], (int)u0);
     }
+    __syncthreads();
+    if (tid == 0 && sm.flag[F_OVF]) atomicOr(overflow, 1);
   }
-  __syncthreads();
-  if (tid == 0 && sm.flag[F_OVF]) atomicOr(overflow, 1);
 
   // ---- MoP mode decision (mop.py:68-151)
   const int nsx = (ncl + p.stride - 1) / p.stride;
@@ -444,15 +432,14 @@ __device__ __forceinline__ void enc_block_body(
     if (kform) {
       const uint32_t ue = (uint32_t)e, m = 2u * ue, M = bio.mag_tab[0];
       const int comp = lane >> 4, sj = lane & 15;
-      const int32_t(*o)[33] = sm.o[comp];
-      const int32_t(*pv)[33] = sm.p[comp];
+      const int32_t(*dt)[33] = sm.d[comp];
       bool tie = false;
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const int si = wid + 4 * r;
         if (2 * si < nr && 2 * sj < ncl) {
           int qa;
-          tie |= trial_sample(o, pv, 2 * si, 2 * sj, ue, m, M, &qa);
+          tie |= trial_sample(dt, 2 * si, 2 * sj, ue, m, M, &qa);
           sm.samp[0][2 * (si * nsx + sj) + comp] = (int16_t)qa;
         }
       }
@@ -692,6 +679,7 @@ __device__ __forceinline__ void enc_block_body(
       const uint32_t M = bio.mag_tab[code0], c32 = bio.c32_tab[code0];
       const int32_t(*o)[33] = sm.o[c];
       auto rd = [&](int rr, int cc) -> uint32_t {
+        if (narrow) return bs_res_any(sm.d[c][rr][cc], m, M);
         return res_i64((int64_t)o[rr][cc] - pvt.at(c, rr, cc), m, M, c32);
       };
       const uint32_t rc = rd(0, 0);
