@@ -74,7 +74,8 @@ cudaError_t launch_dec_block(const uint8_t*, const SYM*, const int64_t*,
                              const int64_t*, const int64_t*, const int32_t*,
                              const int32_t*, const PrepParams&, const BScanIO&,
                              uint32_t*, uint32_t*, double*, double*, int64_t*,
-                             int64_t*, double, cudaStream_t);
+                             int64_t*, double, const int32_t*, int*, int*, int,
+                             cudaStream_t);
 }  // namespace vfcp
 
 using namespace vfcp;
@@ -714,6 +715,13 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   CK(sc.get(&out, (size_t)2 * plane));    // Z of swept blocks
   CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
   CK(sc.get(&pins, (size_t)2 * cplane));
+  // blocks the fast block kernel hands to the general one, per frame
+  int *blist, *bcount;
+  int32_t* etab_dev;
+  CK(sc.get(&blist, (size_t)nblk));
+  CK(sc.get(&bcount, (size_t)T));
+  CK(sc.get(&etab_dev, 32));
+  CK(cudaMemsetAsync(bcount, 0, sizeof(int) * T, st));
   CK(sc.get(&ticket, (size_t)2 * T));   // per frame: chain / interior
   CK(cudaMemsetAsync(ticket, 0, sizeof(int) * 2 * T, st));
   LAUNCH(K_SCAN, st,
@@ -726,6 +734,8 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
     int rc = bscan_setup(sc, lad, H, W, p->radius, st, &bio);
     if (rc) return rc;
   }
+  CK(cudaMemcpyAsync(etab_dev, bio.e_tab, sizeof(int32_t) * 32,
+                     cudaMemcpyHostToDevice, st));
   bio.a[0] = a; bio.a[1] = a + plane;
   bio.a_w[0] = a; bio.a_w[1] = a + plane;
   bio.out[0] = out; bio.out[1] = out + plane;
@@ -743,7 +753,7 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
                t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,
                t > 0 ? rprev : nullptr, rcur, qd_row_off, ll_row_off, pre_nl,
                pre_ll, pp, bio, pins, pins + cplane, out_u, out_v, fix_u,
-               fix_v, bio.inv_S, st));
+               fix_v, bio.inv_S, etab_dev, blist, bcount + t, nsm, st));
     bio.codes = codes + (size_t)t * HW;
     bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
     bio.rec = reinterpret_cast<int2*>(rcur);

@@ -22,7 +22,7 @@ namespace vfcp {
 constexpr int DB_NW = 8;           // warps per block (rows w, w + 8, ...)
 
 struct DecBlockSmem {
-  uint32_t colsum[2][DB_NW][32];   // per warp: column sums of A (REG edges)
+  alignas(16) uint32_t colsum[2][DB_NW][32];   // per warp: column sums of A (REG edges)
   uint32_t rowsum[2][32];      // row sums of A
   int anypin[2], notall[2];
   int32_t etab[32];            // e per code
@@ -40,7 +40,7 @@ __device__ __forceinline__ void dec_block_body(
     uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v,
     double* __restrict__ f64u, double* __restrict__ f64v,
     int64_t* __restrict__ fixu, int64_t* __restrict__ fixv, double inv_S,
-    DecBlockSmem& sm);
+    DecBlockSmem& sm, int bi, int bj);
 
 template <typename SYM>
 __global__ void __launch_bounds__(32 * DB_NW, 3)
@@ -56,11 +56,137 @@ dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
                  uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v,
                  double* __restrict__ f64u, double* __restrict__ f64v,
                  int64_t* __restrict__ fixu, int64_t* __restrict__ fixv,
-                 double inv_S) {
+                 double inv_S, const int* __restrict__ list,
+                 const int* __restrict__ count) {
   __shared__ DecBlockSmem sm;
-  dec_block_body<SYM>(codes_t, qd, ll, modes_t, prev, rec, qd_row_off,
-                      ll_row_off, pre_nl, pre_ll, p, bio, pin_u, pin_v, f64u,
-                      f64v, fixu, fixv, inv_S, sm);
+  if (!list) {
+    // every block of the frame (grid nbx x nby)
+    dec_block_body<SYM>(codes_t, qd, ll, modes_t, prev, rec, qd_row_off,
+                        ll_row_off, pre_nl, pre_ll, p, bio, pin_u, pin_v, f64u,
+                        f64v, fixu, fixv, inv_S, sm, blockIdx.y, blockIdx.x);
+    return;
+  }
+  // the blocks the fast kernel listed
+  const int n = *count;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int blk = list[k];
+    const int bi = blk / p.nbx, bj = blk - bi * p.nbx;
+    dec_block_body<SYM>(codes_t, qd, ll, modes_t, prev, rec, qd_row_off,
+                        ll_row_off, pre_nl, pre_ll, p, bio, pin_u, pin_v, f64u,
+                        f64v, fixu, fixv, inv_S, sm, bi, bj);
+    __syncthreads();
+  }
+}
+
+// The usual block on its own: a full block whose pixels share one quantising
+// code and hold no escape is REG in both components, its symbols are dense
+// (64 per row) and A = (sym - radius) * 2e needs no per-pixel table: four
+// pixels per thread (row tid / 8, column quad tid % 8), row sums over the 8
+// lanes of a row, column sums over the warp's four rows and then the CTA's
+// warps.  Any other block (semi-Lagrangian, ragged, mixed codes, lossless
+// pixels, an escape) goes to the list for dec_block_kernel.
+template <typename SYM>
+__global__ void __launch_bounds__(32 * DB_NW, 8)
+dec_block_fast_kernel(const uint8_t* __restrict__ codes_t,
+                      const SYM* __restrict__ qd,
+                      const uint8_t* __restrict__ modes_t,
+                      const int64_t* __restrict__ qd_row_off,
+                      const int32_t* __restrict__ pre_nl, PrepParams p,
+                      int32_t* __restrict__ lb, int32_t* __restrict__ lr,
+                      int32_t* __restrict__ cls, int32_t e_of_code0_unused,
+                      const int32_t* __restrict__ e_tab_g,
+                      int* __restrict__ list, int* __restrict__ count) {
+  __shared__ alignas(16) uint32_t s_colsum[2][DB_NW][32];
+  __shared__ uint32_t s_rowsum[2][32];
+  __shared__ int s_esc;
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int bj = blockIdx.x, bi = blockIdx.y;
+  const int H = p.H, W = p.W, nchunks = p.nchunks;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int nr = min(32, H - r0), ncl = min(32, W - c0);
+  const int64_t nblk = (int64_t)p.nbx * p.nby;
+  const int64_t blk = (int64_t)bi * p.nbx + bj;
+  const int64_t rowbase = (int64_t)p.t * H;
+  auto defer = [&]() {
+    if (tid == 0) list[atomicAdd(count, 1)] = (int)blk;
+  };
+  const bool sl_blk = modes_t && modes_t[blk] == 1;
+  if (sl_blk || nr != 32 || ncl != 32) {
+    defer();
+    return;
+  }
+  if (tid == 0) s_esc = 0;
+  const int i = tid >> 3, cq = tid & 7;
+  const int code0 = __ldg(codes_t + (int64_t)r0 * W + c0);
+  const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t*>(
+      codes_t + (int64_t)(r0 + i) * W + c0 + 4 * cq));
+  const int32_t e = __ldg(e_tab_g + (code0 & 31));
+  const int64_t row = rowbase + r0 + i;
+  const int64_t qoff = qd_row_off[row] + 2 * (int64_t)pre_nl[row * nchunks + bj];
+  // (uniform over the CTA; also orders s_esc = 0 before the votes below)
+  if (__syncthreads_or(w4 != 0x01010101u * (uint32_t)code0 || e == 0)) {
+    defer();
+    return;
+  }
+  const uint32_t* sp = reinterpret_cast<const uint32_t*>(qd + qoff) + 4 * cq;
+  uint32_t sq[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) sq[k] = __ldg(sp + k);
+  const uint32_t e2 = 2u * (uint32_t)e, rad = (uint32_t)p.radius;
+  uint32_t au[4], av[4];
+  bool esc = false;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint32_t su = sq[k] & 0xffffu, sv = sq[k] >> 16;
+    esc |= su == 0u || sv == 0u;
+    au[k] = (su - rad) * e2;
+    av[k] = (sv - rad) * e2;
+  }
+  // row sums (8 lanes of the row)
+  uint32_t ru = au[0] + au[1] + au[2] + au[3], rv = av[0] + av[1] + av[2] + av[3];
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    ru += __shfl_xor_sync(FULL, ru, o);
+    rv += __shfl_xor_sync(FULL, rv, o);
+  }
+  if (cq == 0) {
+    s_rowsum[0][i] = ru;
+    s_rowsum[1][i] = rv;
+  }
+  // column sums (the warp's four rows; lanes 0-7 hold columns 4 cq + k)
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    au[k] += __shfl_xor_sync(FULL, au[k], 8);
+    av[k] += __shfl_xor_sync(FULL, av[k], 8);
+    au[k] += __shfl_xor_sync(FULL, au[k], 16);
+    av[k] += __shfl_xor_sync(FULL, av[k], 16);
+  }
+  if (lane < 8) {
+    *reinterpret_cast<uint4*>(&s_colsum[0][wid][4 * cq]) = make_uint4(au[0], au[1], au[2], au[3]);
+    *reinterpret_cast<uint4*>(&s_colsum[1][wid][4 * cq]) = make_uint4(av[0], av[1], av[2], av[3]);
+  }
+  if (__any_sync(FULL, esc) && lane == 0) s_esc = 1;
+  __syncthreads();
+  if (s_esc) {
+    defer();
+    return;
+  }
+  if (tid >= 64) return;
+  const int c = tid >> 5;
+  uint32_t cs = 0u;
+#pragma unroll
+  for (int w = 0; w < DB_NW; w++) cs += s_colsum[c][w][lane];
+  uint32_t rs = s_rowsum[c][lane];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t pc = __shfl_up_sync(FULL, cs, o);
+    const uint32_t pr = __shfl_up_sync(FULL, rs, o);
+    if (lane >= o) { cs += pc; rs += pr; }
+  }
+  lb[(c * nblk + blk) * 32 + lane] = (int32_t)cs;
+  lr[(c * nblk + blk) * 32 + lane] = (int32_t)rs;
+  if (lane == 0) cls[c * nblk + blk] = BS_REG;
 }
 
 template <typename SYM>
@@ -74,11 +200,10 @@ __device__ __forceinline__ void dec_block_body(
     uint32_t* __restrict__ pin_u, uint32_t* __restrict__ pin_v,
     double* __restrict__ f64u, double* __restrict__ f64v,
     int64_t* __restrict__ fixu, int64_t* __restrict__ fixv, double inv_S,
-    DecBlockSmem& sm) {
+    DecBlockSmem& sm, int bi, int bj) {
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const int bj = blockIdx.x, bi = blockIdx.y;
   const int H = p.H, W = p.W, Wp = p.Wp, nchunks = p.nchunks;
   const int r0 = 32 * bi, c0 = 32 * bj;
   const int nr = min(32, H - r0), ncl = min(32, W - c0);
@@ -329,11 +454,30 @@ cudaError_t launch_dec_block(const uint8_t* codes_t, const SYM* qd,
                              const BScanIO& bio, uint32_t* pin_u,
                              uint32_t* pin_v, double* f64u, double* f64v,
                              int64_t* fixu, int64_t* fixv, double inv_S,
-                             cudaStream_t st) {
+                             const int32_t* e_tab_dev, int* list, int* count,
+                             int nsm, cudaStream_t st) {
+  const int64_t nblk = (int64_t)p.nbx * p.nby;
+  // a large frame of 16-bit symbols: the usual blocks by the fast kernel, the
+  // rest (listed) by the general one
+  const bool split = list && sizeof(SYM) == 2 && nblk >= 1024 && (p.W & 3) == 0 &&
+                     ((uintptr_t)codes_t & 3) == 0;
+  if (split) {
+    dec_block_fast_kernel<SYM><<<dim3(p.nbx, p.nby), 32 * DB_NW, 0, st>>>(
+        codes_t, qd, prev ? modes_t : nullptr, qd_row_off, pre_nl, p, bio.lb,
+        bio.lr, bio.cls, 0, e_tab_dev, list, count);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t cap = (int64_t)nsm * 4;
+    dec_block_kernel<SYM><<<(int)(nblk < cap ? nblk : cap), 32 * DB_NW, 0, st>>>(
+        codes_t, qd, ll, modes_t, reinterpret_cast<const int2*>(prev),
+        reinterpret_cast<int2*>(rec), qd_row_off, ll_row_off, pre_nl, pre_ll, p,
+        bio, pin_u, pin_v, f64u, f64v, fixu, fixv, inv_S, list, count);
+    return cudaGetLastError();
+  }
   dec_block_kernel<SYM><<<dim3(p.nbx, p.nby), 32 * DB_NW, 0, st>>>(
       codes_t, qd, ll, modes_t, reinterpret_cast<const int2*>(prev),
       reinterpret_cast<int2*>(rec), qd_row_off, ll_row_off, pre_nl, pre_ll, p,
-      bio, pin_u, pin_v, f64u, f64v, fixu, fixv, inv_S);
+      bio, pin_u, pin_v, f64u, f64v, fixu, fixv, inv_S, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -341,6 +485,7 @@ template cudaError_t launch_dec_block<uint16_t>(
     const uint8_t*, const uint16_t*, const int64_t*, const uint8_t*,
     const int32_t*, int32_t*, const int64_t*, const int64_t*, const int32_t*,
     const int32_t*, const PrepParams&, const BScanIO&, uint32_t*, uint32_t*,
-    double*, double*, int64_t*, int64_t*, double, cudaStream_t);
+    double*, double*, int64_t*, int64_t*, double, const int32_t*, int*, int*,
+    int, cudaStream_t);
 
 }  // namespace vfcp
