@@ -1230,6 +1230,167 @@ __device__ __forceinline__ void bs_final_enc(const BScanIO& io, int bi, int bj,
   }
 }
 
+// Decoder, both components of a full block whose pixels share one code (the
+// decoder's fast block kernel marks it BS_NARROW): four pixels per lane, lane
+// = (band of eight rows, column quad).  Z = ZT(j) + ZL(i) - ZC + P(i, j), P
+// the block's 2D prefix sum of A = (sym - radius) * 2e (wrapping uint32).
+// Pass 1 sums the band's columns (lane-local) and scans them along the row,
+// which gives P at the band's last row, hence the offsets of the bands
+// below; pass 2 walks the band's rows: one row scan each, the column sums
+// running in registers.  The symbols stay in registers between the passes.
+__device__ __forceinline__ void bs_final_dec4(const BScanIO& io, int bi, int bj,
+                                              int lane, int code) {
+  const unsigned FULL = 0xffffffffu;
+  const int r0 = 32 * bi, c0 = 32 * bj;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t blk = (int64_t)bi * io.nbx + bj;
+  const int Wp = io.Wp, W = io.W;
+  const int rq = lane >> 3, cq = lane & 7;
+  const uint32_t e2 = 2u * (uint32_t)io.e_tab[code], rad = (uint32_t)io.radius;
+  const int32_t* ebu = io.ebot;
+  const int32_t* ebv = io.ebot + nblk * 32;
+  const int32_t* eru = io.eright;
+  const int32_t* erv = io.eright + nblk * 32;
+  // symbols of the band's eight rows (lane = row holds the row offsets)
+  const int64_t q0 = io.qd_row_off[r0] + 2 * (int64_t)io.pre_nl[(int64_t)r0 * io.nchunks + bj];
+  const uint32_t qrel =
+      (uint32_t)(io.qd_row_off[r0 + lane] +
+                 2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] - q0);
+  const uint32_t* qdb = reinterpret_cast<const uint32_t*>(io.qd + q0) + 4 * cq;
+  // pass 1 reads the band's symbols, pass 2 reads them again (L2 hits)
+  auto load_sym = [&](int it, uint32_t (&x)[4]) {
+    const uint32_t qo = __shfl_sync(FULL, qrel, 8 * rq + it);
+    const uint32_t* sp = qdb + (qo >> 1);
+#pragma unroll
+    for (int k = 0; k < 4; k++) x[k] = __ldg(sp + k);
+  };
+  // recon(t-1) of the band's first rows in flight
+  const int2* pv = io.prevrec;
+  auto load_prev = [&](int it, int4& a, int4& b) {
+    if (pv) {
+      const int4* pp = reinterpret_cast<const int4*>(
+          pv + (int64_t)(r0 + 8 * rq + it) * Wp + c0 + 4 * cq);
+      a = __ldg(pp);
+      b = __ldg(pp + 1);
+    } else {
+      a = b = make_int4(0, 0, 0, 0);
+    }
+  };
+  // exact boundary (Z of the row above, the column to the left, the corner)
+  uint32_t ou[4] = {0, 0, 0, 0}, ov[4] = {0, 0, 0, 0};   // ZT(j) - ZC + band offset
+  uint32_t zLu = 0, zLv = 0;
+  if (bi > 0) {
+    const int4 tu = __ldcg(reinterpret_cast<const int4*>(ebu + (blk - io.nbx) * 32) + cq);
+    const int4 tv = __ldcg(reinterpret_cast<const int4*>(ebv + (blk - io.nbx) * 32) + cq);
+    uint32_t zcu = 0, zcv = 0;
+    if (bj > 0) {
+      zcu = (uint32_t)__ldcg(ebu + (blk - io.nbx - 1) * 32 + 31);
+      zcv = (uint32_t)__ldcg(ebv + (blk - io.nbx - 1) * 32 + 31);
+    }
+    ou[0] = (uint32_t)tu.x - zcu; ou[1] = (uint32_t)tu.y - zcu;
+    ou[2] = (uint32_t)tu.z - zcu; ou[3] = (uint32_t)tu.w - zcu;
+    ov[0] = (uint32_t)tv.x - zcv; ov[1] = (uint32_t)tv.y - zcv;
+    ov[2] = (uint32_t)tv.z - zcv; ov[3] = (uint32_t)tv.w - zcv;
+  }
+  if (bj > 0) {
+    zLu = (uint32_t)__ldcg(eru + (blk - 1) * 32 + lane);
+    zLv = (uint32_t)__ldcg(erv + (blk - 1) * 32 + lane);
+  }
+  auto amp = [&](uint32_t s2, uint32_t& au, uint32_t& av) {
+    au = ((s2 & 0xffffu) - rad) * e2;
+    av = ((s2 >> 16) - rad) * e2;
+  };
+  // inclusive scan of the lane's quad along the row (8 lanes per row)
+  auto row_scan = [&](uint32_t (&x)[4]) {
+    x[1] += x[0]; x[2] += x[1]; x[3] += x[2];
+    uint32_t t = x[3];
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, t, o, 8);
+      if (cq >= o) t += y;
+    }
+    const uint32_t ex = t - x[3];
+    x[0] += ex; x[1] += ex; x[2] += ex; x[3] += ex;
+  };
+  // ---- pass 1: P at the band's last row, offsets of the bands below
+  {
+    uint32_t cu[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      uint32_t sy[4][4];
+#pragma unroll
+      for (int it = 0; it < 4; it++) load_sym(4 * h + it, sy[it]);
+#pragma unroll
+      for (int it = 0; it < 4; it++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          uint32_t au, av;
+          amp(sy[it][k], au, av);
+          cu[k] += au;
+          cv[k] += av;
+        }
+    }
+    row_scan(cu);
+    row_scan(cv);
+    // exclusive scan over the four bands (lanes l, l + 8, l + 16, l + 24)
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint32_t tu = cu[k], tv = cv[k];
+      uint32_t y = __shfl_up_sync(FULL, tu, 8), z = __shfl_up_sync(FULL, tv, 8);
+      if (rq >= 1) { tu += y; tv += z; }
+      y = __shfl_up_sync(FULL, tu, 16); z = __shfl_up_sync(FULL, tv, 16);
+      if (rq >= 2) { tu += y; tv += z; }
+      ou[k] += tu - cu[k];
+      ov[k] += tv - cv[k];
+    }
+  }
+  // ---- pass 2: the band's rows
+  int4* recp = reinterpret_cast<int4*>(io.rec + (int64_t)(r0 + 8 * rq) * Wp + c0 + 4 * cq);
+  double2* fu = reinterpret_cast<double2*>(io.f64[0] + (int64_t)(r0 + 8 * rq) * W + c0 + 4 * cq);
+  double2* fv = reinterpret_cast<double2*>(io.f64[1] + (int64_t)(r0 + 8 * rq) * W + c0 + 4 * cq);
+  const double inv_S = io.inv_S;
+  int4 pa[3], pb[3];
+  uint32_t sq[3][4];
+  load_prev(0, pa[0], pb[0]);
+  load_sym(0, sq[0]);
+  load_prev(1, pa[1], pb[1]);
+  load_sym(1, sq[1]);
+#pragma unroll
+  for (int it = 0; it < 8; it++) {
+    if (it + 2 < 8) {
+      load_prev(it + 2, pa[(it + 2) % 3], pb[(it + 2) % 3]);
+      load_sym(it + 2, sq[(it + 2) % 3]);
+    }
+    const int i = 8 * rq + it;
+    const uint32_t zlu = __shfl_sync(FULL, zLu, i), zlv = __shfl_sync(FULL, zLv, i);
+    uint32_t au[4], av[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) amp(sq[it % 3][k], au[k], av[k]);
+    row_scan(au);
+    row_scan(av);
+    const int4 p01 = pa[it % 3], p23 = pb[it % 3];
+    const uint32_t pu[4] = {(uint32_t)p01.x, (uint32_t)p01.z, (uint32_t)p23.x, (uint32_t)p23.z};
+    const uint32_t pw[4] = {(uint32_t)p01.y, (uint32_t)p01.w, (uint32_t)p23.y, (uint32_t)p23.w};
+    int32_t ru[4], rv[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      ou[k] += au[k];   // column sums run down the band
+      ov[k] += av[k];
+      ru[k] = (int32_t)(ou[k] + zlu + pu[k]);
+      rv[k] = (int32_t)(ov[k] + zlv + pw[k]);
+    }
+    int4* rp = recp + (int64_t)it * (Wp / 2);
+    rp[0] = make_int4(ru[0], rv[0], ru[1], rv[1]);
+    rp[1] = make_int4(ru[2], rv[2], ru[3], rv[3]);
+    double2* du = fu + (int64_t)it * (W / 2);
+    double2* dv = fv + (int64_t)it * (W / 2);
+    du[0] = make_double2(__dmul_rn((double)ru[0], inv_S), __dmul_rn((double)ru[1], inv_S));
+    du[1] = make_double2(__dmul_rn((double)ru[2], inv_S), __dmul_rn((double)ru[3], inv_S));
+    dv[0] = make_double2(__dmul_rn((double)rv[0], inv_S), __dmul_rn((double)rv[1], inv_S));
+    dv[1] = make_double2(__dmul_rn((double)rv[2], inv_S), __dmul_rn((double)rv[3], inv_S));
+  }
+}
+
 template <int C>
 __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
                                               int lane) {
@@ -1314,7 +1475,7 @@ __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
 // warp per block, blocks in raster order (neighbouring warps share the cache
 // lines of their halo loads).
 template <bool ENC, typename F = float>
-__global__ void __launch_bounds__(256, ENC ? 2 : 3)
+__global__ void __launch_bounds__(256, 2)
 bs_interior_kernel(const __grid_constant__ BScanIO io) {
   const int lane = threadIdx.x & 31;
   const int64_t nblk = (int64_t)io.nbx * io.nby;
@@ -1325,8 +1486,14 @@ bs_interior_kernel(const __grid_constant__ BScanIO io) {
     if (ENC) {
       bs_final_enc<F>(io, bi, bj, lane);
     } else {
-      bs_final_dec1<0>(io, bi, bj, lane);
-      bs_final_dec1<1>(io, bi, bj, lane);
+      const int32_t cu = __ldcg(io.cls + blk), cv = __ldcg(io.cls + nblk + blk);
+      const int32_t want = BS_REG | BS_NARROW;
+      if (io.vec4 && (cu & (3 | BS_NARROW)) == want && (cv & (3 | BS_NARROW)) == want) {
+        bs_final_dec4(io, bi, bj, lane, (cu >> 2) & 31);
+      } else {
+        bs_final_dec1<0>(io, bi, bj, lane);
+        bs_final_dec1<1>(io, bi, bj, lane);
+      }
     }
   }
 }

@@ -743,6 +743,9 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   bio.qd = const_cast<uint16_t*>(qd);
   bio.cpitch = W;
   bio.inv_S = 1.0 / p->scale;
+  // the interior pass's vector form: 16-byte rows, float64 output only
+  bio.vec4 = (W & 3) == 0 && !fix_u && !fix_v &&
+             (((uintptr_t)out_u | (uintptr_t)out_v) & 15) == 0;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);

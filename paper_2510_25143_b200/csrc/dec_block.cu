@@ -186,7 +186,8 @@ dec_block_fast_kernel(const uint8_t* __restrict__ codes_t,
   }
   lb[(c * nblk + blk) * 32 + lane] = (int32_t)cs;
   lr[(c * nblk + blk) * 32 + lane] = (int32_t)rs;
-  if (lane == 0) cls[c * nblk + blk] = BS_REG;
+  // (BS_NARROW: one code, dense symbols -- the interior pass's vector form)
+  if (lane == 0) cls[c * nblk + blk] = BS_REG | (code0 << 2) | BS_NARROW;
 }
 
 template <typename SYM>
