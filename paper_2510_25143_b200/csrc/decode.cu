@@ -43,6 +43,48 @@ __global__ void decode_rows_kernel(const uint8_t* __restrict__ codes,
   if (lane == 0) row_n31[row] = n31;
 }
 
+// The same with 16 codes per lane and step (rows of a multiple of 16
+// columns, 16-byte aligned): a code is lossless iff it is >= cmax (the bit
+// length of tau; 0 when tau <= 0), compared four bytes at a time; the l_d bits
+// of 16 pixels are two bytes, most significant bit first.
+__global__ void decode_rows16_kernel(const uint8_t* __restrict__ codes,
+                                     const uint8_t* __restrict__ ld,
+                                     int64_t nrows, int W, int cmax,
+                                     int32_t* __restrict__ row_n31,
+                                     int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= nrows) return;
+  const int64_t rb = row * W;
+  const uint4* cr = reinterpret_cast<const uint4*>(codes + rb);
+  const uint16_t* lr = ld ? reinterpret_cast<const uint16_t*>(ld + (rb >> 3)) : nullptr;
+  const uint32_t cm4 = 0x01010101u * (uint32_t)cmax;
+  int n31 = 0;
+  bool mismatch = false;
+  const int nq = W >> 4;
+  for (int q = lane; q < nq; q += 32) {
+    const uint4 c = __ldg(cr + q);
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+    uint32_t bits = 0;   // pixel 0 in bit 15
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t ge = __vcmpgeu4(w[k], cm4) & 0x01010101u;
+      n31 += __popc(ge);
+      bits = (bits << 4) | ((ge * 0x08040201u) >> 24);
+    }
+    if (lr) {
+      const uint32_t l2 = __ldg(lr + q);   // bytes k/8, k/8 + 1 (little endian)
+      const uint32_t want = ((l2 & 0xffu) << 8) | (l2 >> 8);
+      mismatch |= want != bits;
+    }
+  }
+  for (int o = 16; o; o >>= 1) n31 += __shfl_xor_sync(0xffffffffu, n31, o);
+  if (__any_sync(0xffffffffu, mismatch) && lane == 0) atomicOr(bad, 1);
+  if (lane == 0) row_n31[row] = n31;
+}
+
+// Escapes (symbol 0) of a row's symbols, eight 16-bit symbols per lane and
+// step where the row's range allows 16-byte loads.
 template <typename SYM>
 __global__ void decode_ll_kernel(const SYM* __restrict__ qd,
                                  const int64_t* __restrict__ qd_row_off,
@@ -53,7 +95,23 @@ __global__ void decode_ll_kernel(const SYM* __restrict__ qd,
   if (row >= nrows) return;
   int64_t a = qd_row_off[row], b = qd_row_off[row + 1];
   int z = 0;
-  for (int64_t q = a + lane; q < b; q += 32) z += qd[q] == 0;
+  if (sizeof(SYM) == 2) {
+    // head up to the first 16-byte boundary, 16-byte body, tail
+    int64_t a8 = (a + 7) & ~(int64_t)7;
+    if (a8 > b) a8 = b;
+    const int64_t b8 = a8 + ((b - a8) & ~(int64_t)7);
+    for (int64_t q = a + lane; q < a8; q += 32) z += qd[q] == 0;
+    const uint4* body = reinterpret_cast<const uint4*>(qd + a8);
+    const int64_t nv = (b8 - a8) >> 3;
+    for (int64_t q = lane; q < nv; q += 32) {
+      const uint4 x = __ldg(body + q);
+      z += __popc(__vcmpeq2(x.x, 0u) & 0x00010001u) + __popc(__vcmpeq2(x.y, 0u) & 0x00010001u) +
+           __popc(__vcmpeq2(x.z, 0u) & 0x00010001u) + __popc(__vcmpeq2(x.w, 0u) & 0x00010001u);
+    }
+    for (int64_t q = b8 + lane; q < b; q += 32) z += qd[q] == 0;
+  } else {
+    for (int64_t q = a + lane; q < b; q += 32) z += qd[q] == 0;
+  }
   for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
   if (lane == 0) row_ll[row] = z + 2 * row_n31[row];
 }
@@ -515,6 +573,14 @@ wf_decode_kernel(const uint8_t* __restrict__ codes, const SYM* __restrict__ qd,
 cudaError_t launch_decode_rows(const uint8_t* codes, const uint8_t* ld,
                                int64_t nrows, int W, int64_t tau,
                                int32_t* row_n31, int* bad, cudaStream_t st) {
+  if ((W & 15) == 0 && ((uintptr_t)codes & 15) == 0 && ((uintptr_t)ld & 1) == 0) {
+    int cmax = 0;   // codes below cmax quantise (e = tau >> code > 0)
+    for (int c = 0; c < CODE_LOSSLESS; c++)
+      if (tau > 0 && (tau >> c) != 0) cmax = c + 1;
+    decode_rows16_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, st>>>(
+        codes, ld, nrows, W, cmax, row_n31, bad);
+    return cudaGetLastError();
+  }
   decode_rows_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, st>>>(
       codes, ld, nrows, W, tau, row_n31, bad);
   return cudaGetLastError();
