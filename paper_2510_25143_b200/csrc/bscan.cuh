@@ -434,6 +434,9 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
   const int H = io.H, W = io.W, nbx = io.nbx, nby = io.nby;
   const int64_t nblk = (int64_t)nbx * nby;
   const int ntask = bs_ntask(nby);
+  // the interior kernel (a programmatic dependent launch) may start once
+  // every chain CTA is resident; it follows the progress marks below
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x < 32) {
     sm.etab[threadIdx.x] = io.e_tab[threadIdx.x];
     sm.mtab[threadIdx.x] = io.mag_tab[threadIdx.x];
@@ -654,7 +657,7 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
               top[b] = cv ? (int32_t)(uint32_t)wv : 0;
             }
           } else {
-            spin_ge<BS_SPIN_NS>(&sm.pub[w - 1], bk + nb);
+            spin_ge<0>(&sm.pub[w - 1], bk + nb);   // on the critical path: no back-off
 #pragma unroll
             for (int b = 0; b < BS_CH; b++) {
               const int c = 32 * (bk + b) + lane;
@@ -764,6 +767,15 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
           if (b >= nb) break;
           ebp[(int64_t)(bk + b) * 32] = bot[b];
           erp[(int64_t)(bk + b) * 32] = right[b];
+        }
+        // progress for the interior kernel: the block edges (and any swept
+        // block) are visible GPU-wide before the mark
+        if ((bk + nb) % BS_SEG == 0 || bk + nb == nbx) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            st_release_gpu_u64(io.prog + (int64_t)comp * nby + bi,
+                               ((unsigned long long)io.frame_tag << 32) | (unsigned)(bk + nb));
         }
         BS_PHASE(5)
       }
@@ -1471,28 +1483,66 @@ __device__ __forceinline__ void bs_final_dec1(const BScanIO& io, int bi, int bj,
   }
 }
 
-// Phase C as its own kernel, after the chain of the frame has finished: a
-// warp per block, blocks in raster order (neighbouring warps share the cache
-// lines of their halo loads).
+// Phase C as its own kernel, launched as a programmatic dependent of the
+// chain kernel so that it runs beside it: a warp takes a ticket of four
+// blocks of one block row and waits until the chain has marked the segment
+// (32 blocks) in that row and in the row above, both components.  Tickets
+// follow the chain's front: the frame in cells of 32 block rows x one
+// segment, cells by anti-diagonals (a band of rows starts about one segment
+// time after the band above).
 template <bool ENC, typename F = float>
 __global__ void __launch_bounds__(256, 2)
 bs_interior_kernel(const __grid_constant__ BScanIO io) {
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int64_t nblk = (int64_t)io.nbx * io.nby;
-  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       blk < nblk; blk += nwarp) {
-    const int bi = (int)(blk / io.nbx), bj = (int)(blk - (int64_t)bi * io.nbx);
-    if (ENC) {
-      bs_final_enc<F>(io, bi, bj, lane);
-    } else {
-      const int32_t cu = __ldcg(io.cls + blk), cv = __ldcg(io.cls + nblk + blk);
-      const int32_t want = BS_REG | BS_NARROW;
-      if (io.vec4 && (cu & (3 | BS_NARROW)) == want && (cv & (3 | BS_NARROW)) == want) {
-        bs_final_dec4(io, bi, bj, lane, (cu >> 2) & 31);
+  const int nbx = io.nbx, nby = io.nby;
+  const int64_t nblk = (int64_t)nbx * nby;
+  const int nseg = (nbx + BS_SEG - 1) / BS_SEG, nband = (nby + 31) / 32;
+  const int ntick = nseg * nband * 256;
+  for (;;) {
+    int tk = 0;
+    if (lane == 0) tk = atomicAdd(io.ticket + 1, 1);
+    tk = __shfl_sync(FULL, tk, 0);
+    if (tk >= ntick) break;
+    int rem = tk >> 8, d = 0, kmin = 0;
+    for (;;) {
+      kmin = max(0, d - (nseg - 1));
+      const int cnt = min(d, nband - 1) - kmin + 1;
+      if (rem < cnt) break;
+      rem -= cnt;
+      d++;
+    }
+    const int band = kmin + rem, seg = d - band;
+    const int bi = 32 * band + ((tk & 255) >> 3);
+    const int bj0 = BS_SEG * seg + 4 * (tk & 7);
+    if (bi >= nby || bj0 >= nbx) continue;
+    if (lane < 4) {
+      const int comp = lane & 1, r = bi - (lane >> 1);
+      if (r >= 0) {
+        const unsigned long long need =
+            ((unsigned long long)io.frame_tag << 32) | (unsigned)min(nbx, BS_SEG * (seg + 1));
+        const unsigned long long* pg = io.prog + (int64_t)comp * nby + r;
+        long long spins = 0;
+        while (ld_acquire_gpu_u64(pg) < need) {
+          __nanosleep(256);
+          if (++spins > (1ll << 26)) __trap();   // never: a hang guard
+        }
+      }
+    }
+    __syncwarp();
+    for (int bj = bj0; bj < min(nbx, bj0 + 4); bj++) {
+      const int64_t blk = (int64_t)bi * nbx + bj;
+      if (ENC) {
+        bs_final_enc<F>(io, bi, bj, lane);
       } else {
-        bs_final_dec1<0>(io, bi, bj, lane);
-        bs_final_dec1<1>(io, bi, bj, lane);
+        const int32_t cu = __ldcg(io.cls + blk), cv = __ldcg(io.cls + nblk + blk);
+        const int32_t want = BS_REG | BS_NARROW;
+        if (io.vec4 && (cu & (3 | BS_NARROW)) == want && (cv & (3 | BS_NARROW)) == want) {
+          bs_final_dec4(io, bi, bj, lane, (cu >> 2) & 31);
+        } else {
+          bs_final_dec1<0>(io, bi, bj, lane);
+          bs_final_dec1<1>(io, bi, bj, lane);
+        }
       }
     }
   }
@@ -1528,10 +1578,19 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
       },
       &occ2);
   if (e != cudaSuccess) return e;
-  const int64_t nblk = (int64_t)io.nbx * io.nby;
-  const int64_t want = (nblk + 7) / 8, cap = (int64_t)max(occ2, 1) * nsm * 4;
-  bs_interior_kernel<ENC, F><<<(int)(want < cap ? want : cap), 256, 0, st>>>(io);
-  return cudaGetLastError();
+  const int nseg = (io.nbx + BS_SEG - 1) / BS_SEG, nband = (io.nby + 31) / 32;
+  const int64_t want = (int64_t)nseg * nband * 32, cap = (int64_t)max(occ2, 1) * nsm;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(want < cap ? want : cap));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, bs_interior_kernel<ENC, F>, io);
 }
 
 }  // namespace vfcp
