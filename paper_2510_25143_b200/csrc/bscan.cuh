@@ -27,16 +27,16 @@
 //            dec_block.cu): block class and the bottom row / right column of
 //            the block-local prefix sums (LB, LR), or the known edge values;
 //            KNOWN blocks are written there;
-//   phase B  chain tasks of bs_chain_kernel, the only sequential part: block
-//            boundaries travel down the block rows (one warp per block row
-//            and component walks its row; 32 exact values per block are
-//            handed to the warp below) -- the critical path is ~nby + nbx
-//            cheap block steps instead of H + W pixel steps;
-//   phase C  interior tasks of the same persistent kernel, handed out after
-//            the chain tasks and started per 32-block segment once the chain
-//            has published it, so they overlap the chain: one warp per block
-//            and both components, rows streamed in registers -- recon(t),
-//            the encoder's symbols, the decoder's float64 output.
+//   phase B  bs_chain_kernel, the only sequential part: block boundaries
+//            travel down the block rows (one warp per block row and
+//            component walks its row in chunks of BS_CH blocks; the exact
+//            bottom rows are handed to the warp below) -- the critical path is
+//            ~nby hand-offs + nbx / BS_CH chunk steps instead of H + W pixel
+//            steps;
+//   phase C  bs_interior_kernel, a programmatic dependent launch of phase B
+//            that runs beside it and follows its per-segment progress marks:
+//            one warp per block and both components, four pixels per lane --
+//            recon(t), the encoder's symbols, the decoder's float64 output.
 #pragma once
 
 #include "frame.cuh"
@@ -101,7 +101,8 @@ struct BScanIO {
 constexpr int BS_NW = 8;        // block rows (warps) per chain CTA
 constexpr int BS_HRING = 1024;   // shared boundary ring (columns), power of 2
 constexpr int BS_SEG = 32;      // blocks per chain progress mark
-constexpr int BS_CH = 4;        // blocks per chain step (a chunk)
+constexpr int BS_CH = 4;        // blocks per chain step (a chunk; 8 lengthens
+                                // the hand-off to the row below: slower)
 constexpr int BS_SPIN_NS = 64;  // back-off of a waiting chain warp (its polls share the MIO pipe)
 constexpr int BS_TW = BS_NW;    // blocks per interior task (a warp per block)
 
@@ -193,8 +194,7 @@ __device__ __forceinline__ int32_t bs_enc_exact(int32_t R0, int32_t d,
 }
 
 // ------------------------------------------------------------ phase B
-// Shared memory of the fused chain / interior kernel (the interior tasks
-// work in registers).
+// Shared memory of the chain kernel.
 struct BSChainSmem {
   int32_t etab[32];
   uint32_t mtab[32];
@@ -489,10 +489,14 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
       // bytes of each (block l / 8); copies past the row's end fill zeros
       auto stage = [&](int ck) {
         const int bk0 = ck * BS_CH, slot = ck & 1;
-        const bool vb = bk0 + (lane >> 3) < nbx;
-        const int off = vb ? 32 * bk0 + 4 * lane : 0;
-        cp_async<16>(&sm.pfb[w][slot][4 * lane], lbp + off, vb);
-        cp_async<16>(&sm.pfr[w][slot][4 * lane], lrp + off, vb);
+#pragma unroll
+        for (int h = 0; h < BS_CH / 4; h++) {
+          const int l = lane + 32 * h;
+          const bool vb = bk0 + (l >> 3) < nbx;
+          const int off = vb ? 32 * bk0 + 4 * l : 0;
+          cp_async<16>(&sm.pfb[w][slot][4 * l], lbp + off, vb);
+          cp_async<16>(&sm.pfr[w][slot][4 * l], lrp + off, vb);
+        }
         if (lane < BS_CH) {
           const bool vc = bk0 + lane < nbx;
           cp_async<4>(&sm.pfc[w][slot][lane], clsp + (vc ? bk0 + lane : 0), vc);
@@ -706,6 +710,8 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
           int32_t cor_l = __shfl_up_sync(FULL, t31_l, 1);
           if (lane == 0) cor_l = corner;
           const int32_t prs_l = sub32(t31_l, cor_l);
+          const int32_t left0 = left;
+          bool rtie = false;
 #pragma unroll
           for (int b = 0; b < BS_CH; b++) {
             if (b >= nb) break;
@@ -713,22 +719,39 @@ bs_chain_kernel(const __grid_constant__ BScanIO io) {
             int32_t x = center(add32(left, ps));   // [-e, e]
             x = add32(x, lrv[b]);                  // [-e, e + m)
             if (ENC && x > e) x -= m;
-            const bool rtie = ENC && kb[b] == BS_REG && lane < nr && (x == e || x == -e);
+            rtie |= ENC && kb[b] == BS_REG && lane < nr && (x == e || x == -e);
             int32_t rg = kb[b] == BS_REG ? x : lrv[b];
-            if (ENC && __any_sync(FULL, rtie)) {
-              // a tie on the right column: the block is swept exactly (its
-              // bottom row went down already and is unchanged)
-              const int bj = bk + b, ncl = min(32, W - 32 * bj);
-              const int32_t cb = __shfl_sync(FULL, cor_l, b);
-              bs_slow_block<ENC, F>(bs_slow_io(io, comp), sm, w, comp, bi, bj,
-                                    nr, ncl, top[b], left, cb, lane, false);
-              rg = sm.tv[w][lane][ncl - 1];
-              if (lane == 0) io.cls[rowblk + bj] = BS_DONE;
-              __syncwarp();
-            }
             if (lane >= nr) rg = 0;
             right[b] = rg;
             left = rg;
+          }
+          if (ENC && __any_sync(FULL, rtie)) {
+            // a tie on a right column (rare): again block by block, the
+            // block with the tie swept exactly (its bottom row went down
+            // already and is unchanged)
+            left = left0;
+#pragma unroll
+            for (int b = 0; b < BS_CH; b++) {
+              if (b >= nb) break;
+              const int32_t ps = __shfl_sync(FULL, prs_l, b);
+              int32_t x = center(add32(left, ps));
+              x = add32(x, lrv[b]);
+              if (x > e) x -= m;
+              const bool tb = kb[b] == BS_REG && lane < nr && (x == e || x == -e);
+              int32_t rg = kb[b] == BS_REG ? x : lrv[b];
+              if (__any_sync(FULL, tb)) {
+                const int bj = bk + b, ncl = min(32, W - 32 * bj);
+                const int32_t cb = __shfl_sync(FULL, cor_l, b);
+                bs_slow_block<ENC, F>(bs_slow_io(io, comp), sm, w, comp, bi, bj,
+                                      nr, ncl, top[b], left, cb, lane, false);
+                rg = sm.tv[w][lane][ncl - 1];
+                if (lane == 0) io.cls[rowblk + bj] = BS_DONE;
+                __syncwarp();
+              }
+              if (lane >= nr) rg = 0;
+              right[b] = rg;
+              left = rg;
+            }
           }
           // (only a row's last block can be ragged: t31 is column 31 here)
           corner = __shfl_sync(FULL, t31_l, nb - 1);

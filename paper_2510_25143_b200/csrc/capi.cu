@@ -69,12 +69,19 @@ cudaError_t launch_enc_block(const F*, const F*, const uint8_t*,
                              int32_t*, int*, cudaStream_t);
 // dec_block.cu
 template <typename SYM>
+bool dec_block_split(const uint8_t*, const PrepParams&);
+template <typename SYM>
+cudaError_t launch_dec_block_fast(const uint8_t*, const SYM*, const uint8_t*,
+                                  bool, const int64_t*, const int32_t*,
+                                  const PrepParams&, const BScanIO&,
+                                  const int32_t*, int*, int*, cudaStream_t);
+template <typename SYM>
 cudaError_t launch_dec_block(const uint8_t*, const SYM*, const int64_t*,
                              const uint8_t*, const int32_t*, int32_t*,
                              const int64_t*, const int64_t*, const int32_t*,
                              const int32_t*, const PrepParams&, const BScanIO&,
                              uint32_t*, uint32_t*, double*, double*, int64_t*,
-                             int64_t*, double, const int32_t*, int*, int*, int,
+                             int64_t*, double, const int*, const int*, int,
                              cudaStream_t);
 }  // namespace vfcp
 
@@ -715,7 +722,9 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   CK(sc.get(&out, (size_t)2 * plane));    // Z of swept blocks
   CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
   CK(sc.get(&pins, (size_t)2 * cplane));
-  // blocks the fast block kernel hands to the general one, per frame
+  // blocks the fast block kernel (dec_block.cu) hands to the general one
+  // (the fast kernel stays on this stream: run beside the previous frame's
+  // chain it takes the chain warps' issue slots and the whole call slows down)
   int *blist, *bcount;
   int32_t* etab_dev;
   CK(sc.get(&blist, (size_t)nblk));
@@ -746,17 +755,25 @@ int decode_fast(const vfcp_params* p, const uint8_t* codes, const uint16_t* qd,
   // the interior pass's vector form: 16-byte rows, float64 output only
   bio.vec4 = (W & 3) == 0 && !fix_u && !fix_v &&
              (((uintptr_t)out_u | (uintptr_t)out_v) & 15) == 0;
+  const bool split = dec_block_split<uint16_t>(codes, prep_params(p, 0, lad)) &&
+                     ((W * (int64_t)H) & 3) == 0;
   for (int t = 0; t < T; t++) {
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
     int32_t* rcur = rec + 2 * plane * (t & 1);
+    if (split)
+      LAUNCH(K_DBLK, st,
+             launch_dec_block_fast<uint16_t>(
+                 codes + (size_t)t * HW, qd,
+                 t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr, t > 0,
+                 qd_row_off, pre_nl, pp, bio, etab_dev, blist, bcount + t, st));
     LAUNCH(K_DBLK, st,
            launch_dec_block<uint16_t>(
                codes + (size_t)t * HW, qd, ll,
                t >= 1 ? modes + (size_t)(t - 1) * nblk : nullptr,
                t > 0 ? rprev : nullptr, rcur, qd_row_off, ll_row_off, pre_nl,
                pre_ll, pp, bio, pins, pins + cplane, out_u, out_v, fix_u,
-               fix_v, bio.inv_S, etab_dev, blist, bcount + t, nsm, st));
+               fix_v, bio.inv_S, split ? blist : nullptr, bcount + t, nsm, st));
     bio.codes = codes + (size_t)t * HW;
     bio.prevrec = t > 0 ? reinterpret_cast<const int2*>(rprev) : nullptr;
     bio.rec = reinterpret_cast<int2*>(rcur);

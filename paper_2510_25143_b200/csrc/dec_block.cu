@@ -445,6 +445,32 @@ __device__ __forceinline__ void dec_block_body(
   if (lane == 0) bio.cls[c * nblk + blk] = BS_REG;
 }
 
+// true when the frame's usual blocks go through the fast kernel (a large
+// frame of 16-bit symbols with 4-byte-aligned code rows)
+template <typename SYM>
+bool dec_block_split(const uint8_t* codes_t, const PrepParams& p) {
+  const int64_t nblk = (int64_t)p.nbx * p.nby;
+  return sizeof(SYM) == 2 && nblk >= 1024 && (p.W & 3) == 0 &&
+         ((uintptr_t)codes_t & 3) == 0;
+}
+
+// The usual blocks of a frame; needs nothing of frame t - 1, so the caller
+// may run it ahead on a side stream.
+template <typename SYM>
+cudaError_t launch_dec_block_fast(const uint8_t* codes_t, const SYM* qd,
+                                  const uint8_t* modes_t, bool has_prev,
+                                  const int64_t* qd_row_off,
+                                  const int32_t* pre_nl, const PrepParams& p,
+                                  const BScanIO& bio, const int32_t* e_tab_dev,
+                                  int* list, int* count, cudaStream_t st) {
+  dec_block_fast_kernel<SYM><<<dim3(p.nbx, p.nby), 32 * DB_NW, 0, st>>>(
+      codes_t, qd, has_prev ? modes_t : nullptr, qd_row_off, pre_nl, p, bio.lb,
+      bio.lr, bio.cls, 0, e_tab_dev, list, count);
+  return cudaGetLastError();
+}
+
+// The general kernel: the listed blocks (list != nullptr, after the fast
+// kernel) or every block of the frame.
 template <typename SYM>
 cudaError_t launch_dec_block(const uint8_t* codes_t, const SYM* qd,
                              const int64_t* ll, const uint8_t* modes_t,
@@ -455,19 +481,10 @@ cudaError_t launch_dec_block(const uint8_t* codes_t, const SYM* qd,
                              const BScanIO& bio, uint32_t* pin_u,
                              uint32_t* pin_v, double* f64u, double* f64v,
                              int64_t* fixu, int64_t* fixv, double inv_S,
-                             const int32_t* e_tab_dev, int* list, int* count,
-                             int nsm, cudaStream_t st) {
+                             const int* list, const int* count, int nsm,
+                             cudaStream_t st) {
   const int64_t nblk = (int64_t)p.nbx * p.nby;
-  // a large frame of 16-bit symbols: the usual blocks by the fast kernel, the
-  // rest (listed) by the general one
-  const bool split = list && sizeof(SYM) == 2 && nblk >= 1024 && (p.W & 3) == 0 &&
-                     ((uintptr_t)codes_t & 3) == 0;
-  if (split) {
-    dec_block_fast_kernel<SYM><<<dim3(p.nbx, p.nby), 32 * DB_NW, 0, st>>>(
-        codes_t, qd, prev ? modes_t : nullptr, qd_row_off, pre_nl, p, bio.lb,
-        bio.lr, bio.cls, 0, e_tab_dev, list, count);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+  if (list) {
     const int64_t cap = (int64_t)nsm * 4;
     dec_block_kernel<SYM><<<(int)(nblk < cap ? nblk : cap), 32 * DB_NW, 0, st>>>(
         codes_t, qd, ll, modes_t, reinterpret_cast<const int2*>(prev),
@@ -482,11 +499,16 @@ cudaError_t launch_dec_block(const uint8_t* codes_t, const SYM* qd,
   return cudaGetLastError();
 }
 
+template bool dec_block_split<uint16_t>(const uint8_t*, const PrepParams&);
+template cudaError_t launch_dec_block_fast<uint16_t>(
+    const uint8_t*, const uint16_t*, const uint8_t*, bool, const int64_t*,
+    const int32_t*, const PrepParams&, const BScanIO&, const int32_t*, int*,
+    int*, cudaStream_t);
 template cudaError_t launch_dec_block<uint16_t>(
     const uint8_t*, const uint16_t*, const int64_t*, const uint8_t*,
     const int32_t*, int32_t*, const int64_t*, const int64_t*, const int32_t*,
     const int32_t*, const PrepParams&, const BScanIO&, uint32_t*, uint32_t*,
-    double*, double*, int64_t*, int64_t*, double, const int32_t*, int*, int*,
-    int, cudaStream_t);
+    double*, double*, int64_t*, int64_t*, double, const int*, const int*, int,
+    cudaStream_t);
 
 }  // namespace vfcp

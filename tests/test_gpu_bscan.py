@@ -156,3 +156,48 @@ def test_decompress_host_paths_agree(name, monkeypatch):
     for f in (fast, slow):
         np.testing.assert_array_equal(f.u, du.cpu().numpy())
         np.testing.assert_array_equal(f.v, dv.cpu().numpy())
+
+
+VECTOR_CASES = {
+    # frames of at least 1024 blocks with 16-byte rows: the four-pixel forms of
+    # the interior passes (bscan.cuh bs_final_enc4 / bs_final_dec4), the
+    # decoder's fast block kernel and its worklist (dec_block.cu), the vector
+    # pre-passes of the decoder (decode.cu)
+    "spectral_1024_mop": (lambda: _synth(5, 1024, 1040, 3), 1e-3, "mop"),
+    "vortex_1056_mop": (lambda: _synth(1, 1056, 1024, 3), 1e-2, "mop"),
+    "wake_1024_sl": (lambda: _synth(3, 1024, 1024, 2), 1e-3, "sl"),
+    # rows that are not a multiple of 4: every vector form falls back
+    "spectral_1030_lorenzo": (lambda: _synth(2, 1024, 1030, 2), 1e-3, "lorenzo"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(VECTOR_CASES))
+def test_vector_forms_match_oracle(name):
+    """Streams, float64 output (the float64-only decode takes the vector
+    interior) and fixed-point reconstruction vs the oracle, bit-exact."""
+    import paper_2510_25143_b200 as vg
+    from oracle import cpu_oracle as O
+    gen, eps, pred = VECTOR_CASES[name]
+    H, W, T, u, v = gen()
+    cfg = vg.Config(predictor=pred)
+    f = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0, u, v)
+    s = vg.compress_device(f, eps, cfg, relative=True)
+    ref = O.compress_streams(u, v, H, W, T, 1.0, 1.0, 1.0, eps, cfg,
+                             relative=True)
+    assert s.scale == ref["scale"] and s.tau == ref["tau"]
+    np.testing.assert_array_equal(s.codes.cpu().numpy(), ref["codes"])
+    np.testing.assert_array_equal(s.modes.cpu().numpy(),
+                                  ref["modes"].reshape(-1))
+    np.testing.assert_array_equal(s.qd.cpu().numpy().astype(np.int32),
+                                  ref["qd"])
+    np.testing.assert_array_equal(s.ll.cpu().numpy(), ref["ll"])
+    a = vg.compress(f, eps, cfg, relative=True)
+    du, dv, _, _ = vg.decompress_device(a)
+    inv = 1.0 / ref["scale"]
+    np.testing.assert_array_equal(du.cpu().numpy(),
+                                  ref["recon"][0].reshape(-1).astype(np.float64) * inv)
+    np.testing.assert_array_equal(dv.cpu().numpy(),
+                                  ref["recon"][1].reshape(-1).astype(np.float64) * inv)
+    r = vg.reconstruct_fixed(a)
+    np.testing.assert_array_equal(r.u_fp, ref["recon"][0].reshape(-1))
+    np.testing.assert_array_equal(r.v_fp, ref["recon"][1].reshape(-1))

@@ -10,11 +10,18 @@ import json
 import sys
 from pathlib import Path
 
-CLASSES = {  # kernel name prefix -> bench launch class
-    "vfcp::enc_block_kernel": "enc_block", "vfcp::bs_chain_kernel<1": "bs_chain",
-    "vfcp::cube_kernel": "analyze", "vfcp::exact_kernel": "analyze",
-    "vfcp::analyze_kernel": "analyze", "vfcp::range_kernel": "range",
-    "vfcp::dec_block_kernel": "dec_block", "vfcp::bs_chain_kernel<0": "dec_chain",
+CLASSES = {  # kernel name prefix -> (bench launch class, counts as a launch)
+    "vfcp::enc_block_kernel": ("enc_block", True),
+    # the block scan of a frame: chain kernel + its dependent interior kernel
+    "vfcp::bs_chain_kernel<1": ("bs_chain", True),
+    "vfcp::bs_interior_kernel<1": ("bs_chain", False),
+    "vfcp::cube_kernel": ("analyze", True), "vfcp::exact_kernel": ("analyze", True),
+    "vfcp::analyze_kernel": ("analyze", True), "vfcp::range_kernel": ("range", True),
+    # the decoder's block kernels of a frame: fast + general (listed blocks)
+    "vfcp::dec_block_fast_kernel": ("dec_block", True),
+    "vfcp::dec_block_kernel": ("dec_block", False),
+    "vfcp::bs_chain_kernel<0": ("dec_chain", True),
+    "vfcp::bs_interior_kernel<0": ("dec_chain", False),
 }
 UNIT = {"bytes": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
 
@@ -31,13 +38,15 @@ def main(path, H, W, T):
             continue
         d = dict(zip(hdr, r))
         name = d["Kernel Name"].replace("void ", "").split("(")[0]
-        cls = next((c for k, c in CLASSES.items() if name.startswith(k)), None)
+        cls, counts = next((c for k, c in CLASSES.items() if name.startswith(k)),
+                           (None, False))
         if cls is None:
             continue
         m = d["Metric Name"]
         if m.startswith("dram__bytes"):
             acc[cls]["bytes"] += float(d["Metric Value"].replace(",", "")) * UNIT.get(d["Metric Unit"], 1)
-            launches[cls].add(d["ID"])
+            if counts:
+                launches[cls].add(d["ID"])
     out = {}
     for cls, a in acc.items():
         n = len(launches[cls])
