@@ -179,18 +179,19 @@ __device__ __forceinline__ int32_t bs_rep(uint32_t r, uint32_t e, uint32_t m) {
 // Exact encoder step (codec.py:140-155): x = R0 - d, q = rha(x / 2e);
 // escape -> err 0, symbol 0.
 __device__ __forceinline__ int32_t bs_enc_exact(int32_t R0, int32_t d,
-                                                int32_t e, int32_t radius,
+                                                int32_t e, uint32_t M,
+                                                int32_t radius,
                                                 uint32_t* sym) {
-  const int64_t m = 2 * (int64_t)e;
+  // |x| < 2^31 + 3 e < 2^32 (the neighbours' errors are bounded by tau' <
+  // 2^29): the quotient from the magnitude, ties away from zero
   const int64_t x = (int64_t)R0 - d;
-  int64_t q = (int64_t)floor(__ddiv_rn((double)x, (double)m));
-  int64_t r = x - q * m;
-  if (r < 0) { q--; r += m; }
-  else if (r >= m) { q++; r -= m; }
-  if (2 * r > m || (2 * r == m && x > 0)) q++;
-  if (q <= -radius || q >= radius) { *sym = 0u; return 0; }
+  const uint32_t m = 2u * (uint32_t)e;
+  const uint32_t a = (uint32_t)(x < 0 ? -x : x);
+  const uint32_t qa = bs_qabs(a, (uint32_t)e, m, M);
+  if (qa >= (uint32_t)radius) { *sym = 0u; return 0; }
+  const int32_t q = x < 0 ? -(int32_t)qa : (int32_t)qa;
   *sym = (uint32_t)(q + radius);
-  return (int32_t)(q * m - x);
+  return (int32_t)((int64_t)q * (int64_t)m - x);
 }
 
 // ------------------------------------------------------------ phase B
@@ -210,6 +211,9 @@ struct BSChainSmem {
   // slow path tiles, [row][col] unpadded: the skewed sweep reads column
   // s - lane in row lane, distinct banks across lanes
   int32_t tv[BS_NW][32][32];
+  // slow path (encoder): the block's codes, [row][col] (rows 36 bytes apart:
+  // the sweep's lanes read different banks)
+  uint8_t tc[BS_NW][32][36];
 };
 
 // What the exact sweep of one block needs (passed by value to the
@@ -286,19 +290,39 @@ static __device__ __noinline__ void bs_slow_block(
   // stream offset, so each symbol goes straight to the stream
   uint32_t mynl = 0u;
   int64_t myq = 0;
-  for (int r = 0; r < nr; r++) {
-    const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
-    if (!ENC || r0_in_plane) tv[r][lane] = colok ? __ldcg(a + k) : 0;
-    if (ENC) {
-      const int cd = colok ? io.codes[(int64_t)(r0 + r) * io.cpitch + c0 + lane] : CODE_LOSSLESS;
-      const uint32_t nlw = __ballot_sync(FULL, colok && sm.etab[cd & 31] > 0);
+  // the tile's loads first, all rows in flight (into registers: the
+  // compiler does not move a global load above a shared-memory store), the
+  // ballots of the codes after
+  uint8_t(*tc)[36] = sm.tc[w];
+  {
+    int32_t xv[32];
+    uint8_t cv[32];
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      const bool ok = r < nr && colok;
+      const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
+      xv[r] = (ok && (!ENC || r0_in_plane)) ? __ldcg(a + k) : 0;
+      cv[r] = (ok && ENC) ? __ldg(io.codes + (int64_t)(r0 + r) * io.cpitch + c0 + lane)
+                          : (uint8_t)CODE_LOSSLESS;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      if (!ENC || r0_in_plane) tv[r][lane] = xv[r];
+      if (ENC) tc[r][lane] = cv[r];
+    }
+  }
+  if (ENC) {
+    __syncwarp();
+    for (int r = 0; r < nr; r++) {
+      const uint32_t nlw = __ballot_sync(FULL, colok && sm.etab[tc[r][lane] & 31] > 0);
       if (lane == r) mynl = nlw;
     }
   }
   if (ENC && lane < nr)
     myq = io.qd_row_off[r0 + lane] +
           2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
-  const uint8_t* mycodes = io.codes + (int64_t)(r0 + min(lane, nr - 1)) * io.cpitch + c0;
+  const uint8_t* mycodes = tc[min(lane, nr - 1)];
+  const int32_t* myrow = tv[min(lane, nr - 1)];
   int nesc = 0;
   // encoder: no pins (lossless pixels have e = 0 and err 0; semi-Lagrangian
   // blocks are never swept); decoder: lossless, escaped and SL pixels
@@ -307,31 +331,63 @@ static __device__ __noinline__ void bs_slow_block(
   int32_t l = left;
   int32_t ul = __shfl_up_sync(FULL, left, 1);
   if (lane == 0) ul = corner;
-  const int32_t radius = io.radius;
-  for (int s = 0; s < 63; s++) {
+  const uint32_t radius = (uint32_t)io.radius;
+  uint16_t* qdp = io.qd;
+  // The skewed sweep: lane = row, step s visits column s - lane.  A lone warp
+  // pays every dependent instruction's latency, so the step is kept to the
+  // recurrence itself: the operands of step s + 1 (the pixel's R0 / A, its
+  // step and reciprocal) are fetched during step s, the quantiser is
+  // branch-free on magnitudes (|x| < 2^32), the error in wrapping 32 bits.
+  int32_t xn = 0, en = 0;
+  uint32_t Mn = 0;
+  auto operands = [&](int s) {
     const int jj = s - lane;
-    const bool act = lane < nr && jj >= 0 && jj < ncl;
+    const bool act = lane < nr && (unsigned)jj < (unsigned)ncl;
+    const int jc = act ? jj : 0;
+    xn = myrow[jc];
+    if (ENC) {
+      const int cd = mycodes[jc] & 31;
+      en = act ? sm.etab[cd] : 0;
+      Mn = sm.mtab[cd];
+    }
+  };
+  operands(0);
+#pragma unroll 1
+  for (int s = 0; s < 63; s++) {
+    const int32_t x = xn, e = en;
+    const uint32_t M = Mn;
+    if (s + 1 < 63) operands(s + 1);
+    const int jj = s - lane;
+    const bool act = lane < nr && (unsigned)jj < (unsigned)ncl;
     const int32_t bb = __shfl_sync(FULL, top, s & 31);
     const int32_t up = __shfl_up_sync(FULL, l, 1);
     const int32_t nu = lane == 0 ? bb : up;
-    if (act) {
-      const int32_t x = tv[lane][jj];
-      int32_t v;
-      uint32_t sy = 0;
-      if ((pw >> jj) & 1u) {
-        v = x;
-      } else if (ENC) {
-        const int32_t e = sm.etab[mycodes[jj] & 31];
-        if (e > 0) {
-          v = bs_enc_exact(x, nu + l - ul, e, radius, &sy);
-          io.qd[myq + 2 * __popc(mynl & ((1u << jj) - 1u))] = (uint16_t)sy;
-          nesc += sy == 0;
-        } else {
-          v = 0;
-        }
-      } else {
-        v = (int32_t)((uint32_t)nu + (uint32_t)l - (uint32_t)ul + (uint32_t)x);
+    int32_t v;
+    if (ENC) {
+      // codec.py:140-155: x = R0 - d, q = rha(x / 2e); escape -> err 0, sym 0
+      const bool lossy = e > 0;
+      const int64_t x64 = (int64_t)x - ((int64_t)nu + l - ul);
+      const bool neg = x64 < 0;
+      const uint32_t a = (uint32_t)(neg ? -x64 : x64);
+      const uint32_t m = lossy ? 2u * (uint32_t)e : 2u;
+      uint32_t q = __umulhi(a, M);
+      uint32_t r = a - q * m;
+      if (r >= m) { q++; r -= m; }
+      q += r >= (uint32_t)e ? 1u : 0u;
+      const bool esc = q >= radius;
+      const uint32_t qs = neg ? 0u - q : q;
+      v = (lossy && !esc) ? (int32_t)(qs * m - (uint32_t)x64) : 0;
+      if (act && lossy) {
+        qdp[myq + 2 * __popc(mynl & ((1u << jj) - 1u))] =
+            (uint16_t)(esc ? 0u : qs + radius);
+        nesc += esc;
       }
+    } else {
+      v = ((pw >> (jj & 31)) & 1u)
+              ? x
+              : (int32_t)((uint32_t)nu + (uint32_t)l - (uint32_t)ul + (uint32_t)x);
+    }
+    if (act) {
       tv[lane][jj] = v;
       ul = nu;
       l = v;
@@ -1521,13 +1577,17 @@ bs_interior_kernel(const __grid_constant__ BScanIO io) {
   const int nbx = io.nbx, nby = io.nby;
   const int64_t nblk = (int64_t)nbx * nby;
   const int nseg = (nbx + BS_SEG - 1) / BS_SEG, nband = (nby + 31) / 32;
-  const int ntick = nseg * nband * 256;
+  // blocks per ticket: four on a large frame, one where the frame has few
+  // blocks per warp (a warp walks its ticket's blocks one after another)
+  const int tb = nblk >= 16384 ? 4 : 1, ngrp = BS_SEG / tb, percell = 32 * ngrp;
+  const int ntick = nseg * nband * percell;
   for (;;) {
     int tk = 0;
     if (lane == 0) tk = atomicAdd(io.ticket + 1, 1);
     tk = __shfl_sync(FULL, tk, 0);
     if (tk >= ntick) break;
-    int rem = tk >> 8, d = 0, kmin = 0;
+    const int cell = tk / percell, incell = tk - cell * percell;
+    int rem = cell, d = 0, kmin = 0;
     for (;;) {
       kmin = max(0, d - (nseg - 1));
       const int cnt = min(d, nband - 1) - kmin + 1;
@@ -1536,8 +1596,8 @@ bs_interior_kernel(const __grid_constant__ BScanIO io) {
       d++;
     }
     const int band = kmin + rem, seg = d - band;
-    const int bi = 32 * band + ((tk & 255) >> 3);
-    const int bj0 = BS_SEG * seg + 4 * (tk & 7);
+    const int bi = 32 * band + incell / ngrp;
+    const int bj0 = BS_SEG * seg + tb * (incell % ngrp);
     if (bi >= nby || bj0 >= nbx) continue;
     if (lane < 4) {
       const int comp = lane & 1, r = bi - (lane >> 1);
@@ -1553,7 +1613,7 @@ bs_interior_kernel(const __grid_constant__ BScanIO io) {
       }
     }
     __syncwarp();
-    for (int bj = bj0; bj < min(nbx, bj0 + 4); bj++) {
+    for (int bj = bj0; bj < min(nbx, bj0 + tb); bj++) {
       const int64_t blk = (int64_t)bi * nbx + bj;
       if (ENC) {
         bs_final_enc<F>(io, bi, bj, lane);
@@ -1602,7 +1662,9 @@ cudaError_t launch_bs_chain(const BScanIO& io, int nsm, cudaStream_t st) {
       &occ2);
   if (e != cudaSuccess) return e;
   const int nseg = (io.nbx + BS_SEG - 1) / BS_SEG, nband = (io.nby + 31) / 32;
-  const int64_t want = (int64_t)nseg * nband * 32, cap = (int64_t)max(occ2, 1) * nsm;
+  const int64_t nblk = (int64_t)io.nbx * io.nby;
+  const int64_t want = (int64_t)nseg * nband * (nblk >= 16384 ? 32 : 128),
+                cap = (int64_t)max(occ2, 1) * nsm;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(want < cap ? want : cap));
   cfg.blockDim = dim3(256);
