@@ -211,9 +211,10 @@ struct BSChainSmem {
   // slow path tiles, [row][col] unpadded: the skewed sweep reads column
   // s - lane in row lane, distinct banks across lanes
   int32_t tv[BS_NW][32][32];
-  // slow path (encoder): the block's codes, [row][col] (rows 36 bytes apart:
-  // the sweep's lanes read different banks)
-  uint8_t tc[BS_NW][32][36];
+  // slow path (encoder): per pixel (e, floor(2^32 / 2e)) and the sweep's
+  // symbols (rows 68 bytes apart)
+  uint2 te[BS_NW][32][32];
+  uint16_t ts[BS_NW][32][34];
 };
 
 // What the exact sweep of one block needs (passed by value to the
@@ -285,15 +286,14 @@ static __device__ __noinline__ void bs_slow_block(
   const bool colok = lane < ncl;
   const int32_t* a = io.a;
   int32_t(*tv)[32] = sm.tv[w];
+  uint2(*te)[32] = sm.te[w];        // encoder: (e, floor(2^32 / 2e)) per pixel
+  uint16_t(*ts)[34] = sm.ts[w];     // encoder: the symbols of the sweep
   if (ENC && !r0_in_plane) bs_r0_rows<F>(io, comp, r0, c0, nr, ncl, tv, lane);
-  // encoder: the sweeping lane's row (lane = row): its non-lossless bits and
-  // stream offset, so each symbol goes straight to the stream
+  // The tile's loads first, all rows in flight (into registers: the compiler
+  // does not move a global load above a shared-memory store).  Encoder: the
+  // pixel's step and reciprocal go into the (e, M) tile, and lane r keeps row
+  // r's non-lossless bits (a code quantises iff it is below cmax).
   uint32_t mynl = 0u;
-  int64_t myq = 0;
-  // the tile's loads first, all rows in flight (into registers: the
-  // compiler does not move a global load above a shared-memory store), the
-  // ballots of the codes after
-  uint8_t(*tc)[36] = sm.tc[w];
   {
     int32_t xv[32];
     uint8_t cv[32];
@@ -308,22 +308,17 @@ static __device__ __noinline__ void bs_slow_block(
 #pragma unroll
     for (int r = 0; r < 32; r++) {
       if (!ENC || r0_in_plane) tv[r][lane] = xv[r];
-      if (ENC) tc[r][lane] = cv[r];
+      if (ENC) {
+        const int cd = cv[r] & 31;
+        const uint32_t e = (uint32_t)sm.etab[cd];
+        te[r][lane] = make_uint2(e, sm.mtab[cd]);
+        const uint32_t nlw = __ballot_sync(FULL, e != 0u);
+        if (lane == r) mynl = nlw;
+      }
     }
   }
-  if (ENC) {
-    __syncwarp();
-    for (int r = 0; r < nr; r++) {
-      const uint32_t nlw = __ballot_sync(FULL, colok && sm.etab[tc[r][lane] & 31] > 0);
-      if (lane == r) mynl = nlw;
-    }
-  }
-  if (ENC && lane < nr)
-    myq = io.qd_row_off[r0 + lane] +
-          2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
-  const uint8_t* mycodes = tc[min(lane, nr - 1)];
   const int32_t* myrow = tv[min(lane, nr - 1)];
-  int nesc = 0;
+  const uint2* myem = te[min(lane, nr - 1)];
   // encoder: no pins (lossless pixels have e = 0 and err 0; semi-Lagrangian
   // blocks are never swept); decoder: lossless, escaped and SL pixels
   const uint32_t pw = (!ENC && lane < nr) ? io.pin[(int64_t)(r0 + lane) * io.nchunks + bj] : 0u;
@@ -332,30 +327,28 @@ static __device__ __noinline__ void bs_slow_block(
   int32_t ul = __shfl_up_sync(FULL, left, 1);
   if (lane == 0) ul = corner;
   const uint32_t radius = (uint32_t)io.radius;
-  uint16_t* qdp = io.qd;
   // The skewed sweep: lane = row, step s visits column s - lane.  A lone warp
   // pays every dependent instruction's latency, so the step is kept to the
-  // recurrence itself: the operands of step s + 1 (the pixel's R0 / A, its
-  // step and reciprocal) are fetched during step s, the quantiser is
-  // branch-free on magnitudes (|x| < 2^32), the error in wrapping 32 bits.
-  int32_t xn = 0, en = 0;
-  uint32_t Mn = 0;
+  // recurrence itself: the operands of step s + 1 are fetched during step s,
+  // the quantiser is branch-free on magnitudes (|x| < 2^32), the error in
+  // wrapping 32 bits, the symbols go to a tile and out to the stream after.
+  int32_t xn = 0;
+  uint2 emn = make_uint2(0u, 0u);
   auto operands = [&](int s) {
     const int jj = s - lane;
     const bool act = lane < nr && (unsigned)jj < (unsigned)ncl;
     const int jc = act ? jj : 0;
     xn = myrow[jc];
     if (ENC) {
-      const int cd = mycodes[jc] & 31;
-      en = act ? sm.etab[cd] : 0;
-      Mn = sm.mtab[cd];
+      emn = myem[jc];
+      if (!act) emn.x = 0u;
     }
   };
   operands(0);
 #pragma unroll 1
   for (int s = 0; s < 63; s++) {
-    const int32_t x = xn, e = en;
-    const uint32_t M = Mn;
+    const int32_t x = xn;
+    const uint32_t e = emn.x, M = emn.y;
     if (s + 1 < 63) operands(s + 1);
     const int jj = s - lane;
     const bool act = lane < nr && (unsigned)jj < (unsigned)ncl;
@@ -363,25 +356,22 @@ static __device__ __noinline__ void bs_slow_block(
     const int32_t up = __shfl_up_sync(FULL, l, 1);
     const int32_t nu = lane == 0 ? bb : up;
     int32_t v;
+    uint32_t sy = 0u;
     if (ENC) {
       // codec.py:140-155: x = R0 - d, q = rha(x / 2e); escape -> err 0, sym 0
-      const bool lossy = e > 0;
+      const bool lossy = e != 0u;
       const int64_t x64 = (int64_t)x - ((int64_t)nu + l - ul);
       const bool neg = x64 < 0;
-      const uint32_t a = (uint32_t)(neg ? -x64 : x64);
-      const uint32_t m = lossy ? 2u * (uint32_t)e : 2u;
-      uint32_t q = __umulhi(a, M);
-      uint32_t r = a - q * m;
+      const uint32_t ax = (uint32_t)(neg ? -x64 : x64);
+      const uint32_t m = lossy ? 2u * e : 2u;
+      uint32_t q = __umulhi(ax, M);
+      uint32_t r = ax - q * m;
       if (r >= m) { q++; r -= m; }
-      q += r >= (uint32_t)e ? 1u : 0u;
-      const bool esc = q >= radius;
+      q += r >= e ? 1u : 0u;
+      const bool ok = lossy && q < radius;
       const uint32_t qs = neg ? 0u - q : q;
-      v = (lossy && !esc) ? (int32_t)(qs * m - (uint32_t)x64) : 0;
-      if (act && lossy) {
-        qdp[myq + 2 * __popc(mynl & ((1u << jj) - 1u))] =
-            (uint16_t)(esc ? 0u : qs + radius);
-        nesc += esc;
-      }
+      v = ok ? (int32_t)(qs * m - (uint32_t)x64) : 0;
+      sy = ok ? qs + radius : 0u;
     } else {
       v = ((pw >> (jj & 31)) & 1u)
               ? x
@@ -389,17 +379,35 @@ static __device__ __noinline__ void bs_slow_block(
     }
     if (act) {
       tv[lane][jj] = v;
+      if (ENC) ts[lane][jj] = (uint16_t)sy;
       ul = nu;
       l = v;
     }
   }
   __syncwarp();
   int32_t* out = io.out;
+  // err / Z of the block for the interior pass; encoder: the symbols of the
+  // non-lossless pixels to their places in the stream (lane = column), the
+  // escapes (symbol 0) counted per row for the ll stream
+  int64_t myq = 0;
+  if (ENC && lane < nr)
+    myq = io.qd_row_off[r0 + lane] +
+          2 * (int64_t)io.pre_nl[(int64_t)(r0 + lane) * io.nchunks + bj] + comp;
+  const unsigned lt = (1u << lane) - 1u;
+  int nesc = 0;
   for (int r = 0; r < nr; r++) {
     const int64_t k = (int64_t)(r0 + r) * io.Wp + c0 + lane;
     if (colok) out[k] = tv[r][lane];
+    if (ENC) {
+      const uint32_t nlw = __shfl_sync(FULL, mynl, r);
+      const int64_t qr = __shfl_sync(FULL, myq, r);
+      const bool nl = (nlw >> lane) & 1u;
+      const uint16_t sv = ts[r][lane];
+      if (nl) io.qd[qr + 2 * __popc(nlw & lt)] = sv;
+      const int ne = __popc(__ballot_sync(FULL, nl && sv == 0));
+      if (lane == r) nesc = ne;
+    }
   }
-  // escapes (symbol 0) counted per row for the ll stream
   if (ENC && nesc) atomicAdd(io.row_ll + r0 + lane, nesc);
 }
 

@@ -193,6 +193,14 @@ static __device__ __noinline__ void trial_rows_generic(
   trial_rows<int64_t, 0>(o, pp, nr, ncl, stride, nsx, e, m, M, c32, samp, comp, lane);
 }
 
+// the row-streamed narrow trial (a tie in the sample-parallel trial, or a
+// component that may escape next to one that cannot) out of line
+static __device__ __noinline__ void trial_rows_n2(
+    const int32_t (*o)[33], PvTile pp, int nr, int ncl, int nsx, int32_t e,
+    uint32_t m, uint32_t M, uint32_t c32, int16_t* samp, int comp, int lane) {
+  trial_rows<int32_t, 2>(o, pp, nr, ncl, 2, nsx, e, m, M, c32, samp, comp, lane);
+}
+
 template <typename F>
 __device__ __forceinline__ void enc_block_body(
     const F* __restrict__ u, const F* __restrict__ v,
@@ -456,7 +464,7 @@ __device__ __forceinline__ void enc_block_body(
       if (!((sm.flag[F_UNSAFE_T] >> comp) & 1)) {
         int16_t* samp = &sm.samp[0][0];
         if (narrow && p.stride == 2)
-          trial_rows<int32_t, 2>(o, pp, nr, ncl, 2, nsx, e, m, M, c32, samp, comp, lane);
+          trial_rows_n2(o, pp, nr, ncl, nsx, e, m, M, c32, samp, comp, lane);
         else
           trial_rows_generic(o, pp, nr, ncl, p.stride, nsx, e, m, M, c32, samp, comp, lane);
       } else {
@@ -531,9 +539,8 @@ __device__ __forceinline__ void enc_block_body(
     if (kform && sm.flag[F_TIE]) {
       // rare: a tie somewhere in the block, the trial in raster order
       if (wid < 2)
-        trial_rows<int32_t, 2>(sm.o[wid], pvt, nr, ncl, 2, nsx, e,
-                               2u * (uint32_t)e, bio.mag_tab[0], bio.c32_tab[0],
-                               &sm.samp[0][0], wid, lane);
+        trial_rows_n2(sm.o[wid], pvt, nr, ncl, nsx, e, 2u * (uint32_t)e,
+                      bio.mag_tab[0], bio.c32_tab[0], &sm.samp[0][0], wid, lane);
       __syncthreads();
     }
     if (wid == 0 || wid == 2) {
