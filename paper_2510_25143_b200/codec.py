@@ -253,15 +253,12 @@ class DeviceStreams:
 def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                     relative: bool = False, want_mask: bool = False,
                     want_scores: bool = False, want_recon: bool = False,
-                    host_out: bool = False, hooks=None) -> DeviceStreams:
+                    host_out: bool = False) -> DeviceStreams:
     """codec.py:321-376 up to (not including) the entropy stage, on device.
 
     host_out: also bring the streams to pinned host memory (``.host``),
     overlapping the copies with the encode: the codes and l_d right after
-    the analysis, each frame's symbols as soon as the frame is encoded.
-
-    hooks (internal, used by compress()): hooks.after_analyze(codes) is
-    called once the analysis is enqueued."""
+    the analysis, each frame's symbols as soon as the frame is encoded."""
     import torch
     cfg = config or Config()
     if eps < 0:
@@ -290,8 +287,6 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                               codes.data_ptr(), ld_words.data_ptr(),
                               _lib.ptr(mask), row_n31.data_ptr(), st),
                "analyze")
-    if hooks is not None:
-        hooks.after_analyze(codes)
     qd_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
     nqd = ctypes.c_int64(0)
     _lib.check(L.vfcp_qd_offsets(pp, row_n31.data_ptr(), qd_row_off.data_ptr(),
@@ -401,48 +396,6 @@ def streams_to_host(s: DeviceStreams) -> dict:
     return {k: v.numpy() for k, v in hs.items()}
 
 
-class _CodesEntropy:
-    """compress() hooks: the codes are final once the analysis has run, so
-    their Huffman section is built by a host thread on a side stream while
-    the frames encode on the main stream (the main thread waits inside the
-    library call, which releases the GIL)."""
-
-    def __init__(self):
-        self.q_xi = None
-        self._err = None
-        self._thread = None
-
-    def after_analyze(self, codes):
-        import threading
-
-        import torch
-        ev = torch.cuda.Event()
-        ev.record()
-
-        def work():
-            try:
-                with torch.cuda.device(codes.device):
-                    side = torch.cuda.Stream()
-                    side.wait_event(ev)
-                    with torch.cuda.stream(side):
-                        pend = huffman.encode_device_many([(codes, EB_ALPHABET, 0)])
-                        self.q_xi = pend[0].result()
-            except BaseException as err:   # re-raised by result()
-                self._err = err
-
-        self._thread = threading.Thread(target=work, daemon=True)
-        self._thread.start()
-
-    def result(self, codes):
-        if self._thread is not None:
-            self._thread.join()
-        if self._err is not None:
-            raise self._err
-        if self.q_xi is None:   # the hook did not run
-            self.q_xi = huffman.encode_device(codes, EB_ALPHABET, 0)
-        return self.q_xi
-
-
 def compress(f: FieldSeries, eps: float, config: Config | None = None,
              relative: bool = False) -> Archive:
     """Compress a field series under a uniform pointwise error bound eps.
@@ -455,8 +408,10 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         # entropy stage on the device (csrc/huffman_gpu.cu): only the packed
         # sections come back; zlib stays on the host
         import torch
-        hooks = _CodesEntropy()
-        s = compress_device(f, eps, cfg, relative, hooks=hooks)
+        # (the codes' section is built after the frames: its kernels, run
+        # beside the frame loop on a side stream, take issue slots from the
+        # block-scan chain and the call ends later)
+        s = compress_device(f, eps, cfg, relative)
         # the small sections go to pinned memory on a side stream while
         # the symbol section is histogrammed and packed
         main = torch.cuda.current_stream()
@@ -467,9 +422,10 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         for x in (s.ld, s.ll, s.modes):
             x.record_stream(side)
         pending = huffman.encode_device_many([
-            (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096))])
+            (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096)),
+            (s.codes, EB_ALPHABET, 0)])
         q_d = pending[0].result()
-        q_xi = hooks.result(s.codes)
+        q_xi = pending[1].result()
         side.synchronize()
         l_d = huffman.new_bytearray(h_ld.numel())
         huffman.host_copy(np.frombuffer(l_d, dtype=np.uint8), h_ld.numpy())
