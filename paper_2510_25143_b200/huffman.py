@@ -85,41 +85,66 @@ def new_bytearray(n: int) -> bytearray:
     return _BA_NEW(None, n)
 
 
+def _pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max(1, min(8, _lib.host_threads())))
+    return _POOL
+
+
+_STEP = 1 << 25
+
+
 def host_copy(dst: np.ndarray, src: np.ndarray) -> None:
     """dst[:] = src for large byte arrays, split over host threads (numpy
     releases the GIL for the copies; a fresh destination's first-touch page
     faults are taken in parallel too)."""
-    global _POOL
     n = src.size
-    step = 1 << 25
-    if n <= step:
+    if n <= _STEP:
         dst[:] = src
         return
-    if _POOL is None:
-        from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max(1, min(8, _lib.host_threads())))
 
     def part(o):
-        dst[o:o + step] = src[o:o + step]
-    list(_POOL.map(part, range(0, n, step)))
+        dst[o:o + _STEP] = src[o:o + _STEP]
+    list(_pool().map(part, range(0, n, _STEP)))
+
+
+def host_touch(dst: np.ndarray) -> list:
+    """First-touch the pages of a fresh destination on the host threads (one
+    write per page); returns the futures.  Started while the device still
+    packs, it takes the page faults out of the copy that follows."""
+    n = dst.size
+    if n <= _STEP:
+        return []
+
+    def part(o):
+        dst[o:o + _STEP:4096] = 0
+    return [_pool().submit(part, o) for o in range(0, n, _STEP)]
 
 
 class PendingBlob:
-    """A device-packed section on its way to pinned host memory."""
+    """A device-packed section on its way to pinned host memory: the
+    destination bytes are allocated (and their pages touched, on host
+    threads) while the device packs and copies."""
 
     def __init__(self, head, nbytes, host, words, event):
         self._head, self._nbytes = head, nbytes
         self._host, self._words, self._event = host, words, event
+        self._blob = new_bytearray(len(head) + nbytes)
+        self._blob[:len(head)] = head
+        self._touch = host_touch(np.frombuffer(self._blob, dtype=np.uint8)[len(head):])
 
     def result(self) -> bytearray:
-        head = self._head
-        blob = new_bytearray(len(head) + self._nbytes)
-        blob[:len(head)] = head
+        blob, head = self._blob, self._head
         if self._nbytes:
+            for t in self._touch:
+                t.result()
             self._event.synchronize()
             host_copy(np.frombuffer(blob, dtype=np.uint8)[len(head):],
                       self._host.numpy().view(np.uint8)[:self._nbytes])
-        self._host = self._words = None
+        self._host = self._words = self._blob = None
+        self._touch = []
         return blob
 
 
