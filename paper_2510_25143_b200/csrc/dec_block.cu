@@ -20,6 +20,7 @@
 namespace vfcp {
 
 constexpr int DB_NW = 8;           // warps per block (rows w, w + 8, ...)
+constexpr int DB_OCC = 4;          // CTAs per SM of the general kernel (register cap)
 
 struct DecBlockSmem {
   alignas(16) uint32_t colsum[2][DB_NW][32];   // per warp: column sums of A (REG edges)
@@ -43,7 +44,7 @@ __device__ __forceinline__ void dec_block_body(
     DecBlockSmem& sm, int bi, int bj);
 
 template <typename SYM>
-__global__ void __launch_bounds__(32 * DB_NW, 3)
+__global__ void __launch_bounds__(32 * DB_NW, DB_OCC)
 dec_block_kernel(const uint8_t* __restrict__ codes_t,   // frame t, pitch W
                  const SYM* __restrict__ qd, const int64_t* __restrict__ ll,
                  const uint8_t* __restrict__ modes_t,
@@ -485,7 +486,7 @@ cudaError_t launch_dec_block(const uint8_t* codes_t, const SYM* qd,
                              cudaStream_t st) {
   const int64_t nblk = (int64_t)p.nbx * p.nby;
   if (list) {
-    const int64_t cap = (int64_t)nsm * 4;
+    const int64_t cap = (int64_t)nsm * DB_OCC;
     dec_block_kernel<SYM><<<(int)(nblk < cap ? nblk : cap), 32 * DB_NW, 0, st>>>(
         codes_t, qd, ll, modes_t, reinterpret_cast<const int2*>(prev),
         reinterpret_cast<int2*>(rec), qd_row_off, ll_row_off, pre_nl, pre_ll, p,
