@@ -40,17 +40,35 @@ huff_hist_kernel(const S* __restrict__ sym, int64_t n, int wbase,
   for (int k = threadIdx.x; k < HW_BINS; k += blockDim.x) h[k] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-    const int64_t i = i0 + threadIdx.x;   // warp-uniform loop bound
-    const bool ok = i < n;
-    const int s = ok ? (int)sym[i] : -1;
-    const unsigned grp = __match_any_sync(0xffffffffu, s);
-    const bool leader = ok && (grp & ((1u << lane) - 1u)) == 0;
-    if (leader) {
-      const int w = s - wbase;
-      if ((unsigned)w < (unsigned)HW_BINS) atomicAdd(&h[w], (unsigned)__popc(grp));
-      else atomicAdd(&counts[s], (unsigned long long)__popc(grp));
+  // 16 bytes of symbols per thread and step (the eight / sixteen match
+  // operations of a step are independent, so their latencies overlap)
+  constexpr int VPT = 16 / (int)sizeof(S);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * VPT;
+  const bool aligned = ((uintptr_t)sym & 15) == 0;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * VPT; i0 < n; i0 += stride) {
+    const int64_t i = i0 + (int64_t)threadIdx.x * VPT;   // warp-uniform loop bound
+    int sv[VPT];
+    if (aligned && i + VPT <= n) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(sym + i));
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < VPT; k++)
+        sv[k] = sizeof(S) == 2 ? (int)((w[k >> 1] >> (16 * (k & 1))) & 0xffffu)
+                               : (int)((w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; k++) sv[k] = i + k < n ? (int)sym[i + k] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; k++) {
+      const int s = sv[k];
+      const unsigned grp = __match_any_sync(0xffffffffu, s);
+      const bool leader = s >= 0 && (grp & ((1u << lane) - 1u)) == 0;
+      if (leader) {
+        const int w = s - wbase;
+        if ((unsigned)w < (unsigned)HW_BINS) atomicAdd(&h[w], (unsigned)__popc(grp));
+        else atomicAdd(&counts[s], (unsigned long long)__popc(grp));
+      }
     }
   }
   __syncthreads();
@@ -365,7 +383,7 @@ int vfcp_huff_hist_dev(const void* symbols, int sym_bytes, int64_t n,
   int dev = 0, nsm = 148;
   HCK(cudaGetDevice(&dev));
   HCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)nsm * 8);
+  const int64_t blocks = std::min<int64_t>((n + 2047) / 2048, (int64_t)nsm * 8);
   if (sym_bytes == 2)
     huff_hist_kernel<uint16_t><<<(unsigned)blocks, 256, 0, st>>>(
         (const uint16_t*)symbols, n, wbase, counts);
