@@ -107,6 +107,62 @@ int vfcp_encode_host(const vfcp_params* p, const void* u, const void* v,
                      int32_t* row_ll, void* host_qd,
                      const int64_t* frame_off, void* stream);
 
+/* ---- frame streaming: compress() of a field that is still crossing PCIe.
+ * The reference's compress (codec.py:321-376) is value_range -> to_fixed ->
+ * derive_all -> the frame loop; on a host-resident field the steps below let
+ * frame t be analysed and encoded as soon as frames <= t + 1 are on the
+ * device, while the later frames' H2D copies are in flight.             */
+
+/* field.py:69-73 value_range + choose_scale's max|x| on HOST memory (u, v:
+ * host arrays of n values), reduced by nthreads host threads: the scale and a
+ * relative eps must be known before the first frame can be converted, i.e.
+ * before the data has crossed PCIe.  out3 = {min, max, max|x|}.  A hint the
+ * device range (vfcp_value_range_part over every frame) is checked against. */
+int vfcp_host_range(const void* u, const void* v, int dtype, int64_t n,
+                    int nthreads, double* out3);
+
+/* The launch of vfcp_value_range without its host reduction: nb partial
+ * {min, max, max|x|} triples of n values into device part[3 * nb]. */
+int vfcp_value_range_part(const void* u, const void* v, int dtype, int64_t n,
+                          double* part, int nb, void* stream);
+
+/* vfcp_analyze restricted to the anchors of frames [t0, t1) (predicates.py:
+ * 290-301 / ebounds.py:190-206 enumerate faces per anchor vertex; an anchor
+ * of frame t touches frames t and t + 1 only).  Reads frames t0 ..
+ * min(t1, T-1).  codes / ld_words / mask / row_n31 / *ovf must be zeroed
+ * before the first slab; all updates are atomic max / or / first-touch
+ * counts, so any partition of [0, T) into slabs leaves vfcp_analyze's
+ * arrays.  Frame t's codes are final once the anchors of frames t - 1 and t
+ * have run.  list: device u64[cap] scratch, count: device u64, ovf: device
+ * int set when a slab's list overflowed (redo the field with vfcp_analyze).
+ * Needs tau' > 0. */
+int vfcp_analyze_slab(const vfcp_params* p, const void* u, const void* v,
+                      int dtype, int t0, int t1, uint8_t* codes,
+                      uint32_t* ld_words, uint16_t* mask, int32_t* row_n31,
+                      uint64_t* list, int64_t cap, unsigned long long* count,
+                      int* ovf, void* stream);
+
+/* vfcp_qd_offsets over the rows of the first nframes frames (their counts
+ * final); qd_row_off[nframes * H] also goes to *total (page-locked host
+ * memory) asynchronously on `stream`. */
+int vfcp_qd_offsets_upto(const vfcp_params* p, int nframes,
+                         const int32_t* row_n31, int64_t* qd_row_off,
+                         int64_t* total, void* stream);
+
+/* vfcp_encode's frame loop (codec.py:359-376) one frame at a time: begin
+ * allocates the scratch (block path only: VFCP_EINVAL otherwise, use
+ * vfcp_encode), frame(t) enqueues frame t on the stream given to begin --
+ * t = 0, 1, ... in order, each once orig(t), codes(t) and qd_row_off of its
+ * rows are final in stream order -- and end synchronises, frees the handle
+ * and reports whether an int32 overflow asks for vfcp_encode instead. */
+int vfcp_encode_stream_begin(const vfcp_params* p, const void* u,
+                             const void* v, int dtype, const uint8_t* codes,
+                             const int64_t* qd_row_off, void* qd,
+                             uint8_t* modes, int32_t* row_ll, void* stream,
+                             void** handle);
+int vfcp_encode_stream_frame(void* handle, int t);
+int vfcp_encode_stream_end(void* handle, int* overflowed);
+
 /* Exclusive scan of per-row counts: off[r] = sum_{q<r} cnt[q], off[nrows] =
  * total.  Synchronising: *total_host = total. */
 int vfcp_row_offsets(const int32_t* cnt, int64_t nrows, int64_t* off,

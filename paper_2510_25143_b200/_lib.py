@@ -54,6 +54,15 @@ _SIGS = {
     "vfcp_qd_offsets": (_I, [_PP, _P, _P, _P, _P]),
     "vfcp_encode": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vfcp_encode_host": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vfcp_host_range": (_I, [_P, _P, _I, _I64, _I, _P]),
+    "vfcp_value_range_part": (_I, [_P, _P, _I, _I64, _P, _I, _P]),
+    "vfcp_analyze_slab": (_I, [_PP, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P,
+                               _I64, _P, _P, _P]),
+    "vfcp_qd_offsets_upto": (_I, [_PP, _I, _P, _P, _P, _P]),
+    "vfcp_encode_stream_begin": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P,
+                                      _P, _P]),
+    "vfcp_encode_stream_frame": (_I, [_P, _I]),
+    "vfcp_encode_stream_end": (_I, [_P, _P]),
     "vfcp_row_offsets": (_I, [_P, _I64, _P, _P, _P]),
     "vfcp_encode_ll": (_I, [_PP, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "vfcp_decode_prepare": (_I, [_PP, _P, _P, _P, _I64, _P, _P, _P, _P, _P,

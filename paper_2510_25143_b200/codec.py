@@ -10,6 +10,7 @@ the reference and is timed separately.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import struct
 import time
@@ -248,22 +249,38 @@ class DeviceStreams:
     recon: object = None
     n_faces: int | None = None
     host: dict | None = None   # host copies (compress_device(host_out=True))
+    hist: dict | None = None   # device symbol counts of qd / codes (want_hist)
 
 
 def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                     relative: bool = False, want_mask: bool = False,
                     want_scores: bool = False, want_recon: bool = False,
-                    host_out: bool = False) -> DeviceStreams:
+                    host_out: bool = False,
+                    want_hist: bool = False) -> DeviceStreams:
     """codec.py:321-376 up to (not including) the entropy stage, on device.
 
     host_out: also bring the streams to pinned host memory (``.host``),
     overlapping the copies with the encode: the codes and l_d right after
-    the analysis, each frame's symbols as soon as the frame is encoded."""
+    the analysis, each frame's symbols as soon as the frame is encoded.
+    want_hist: the frame-streamed path also counts the symbols of qd and the
+    codes frame by frame (``.hist``, for the device entropy stage); the
+    whole-field path leaves ``.hist`` None."""
     import torch
     cfg = config or Config()
     if eps < 0:
         raise ValueError("eps must be non-negative")
-    du, dv = to_device(f.u), to_device(f.v)
+    H, W, T = f.H, f.W, f.T
+    N = H * W * T
+    L = _lib.lib()
+    resident = None
+    if _stream_ok(f, cfg, want_mask or want_scores or want_recon):
+        # page-locked host input: frames are analysed and encoded while the
+        # later ones are still crossing PCIe
+        r = _compress_streamed(f, eps, cfg, relative, host_out, want_hist)
+        if isinstance(r, DeviceStreams):
+            return r
+        resident = r    # left to the whole-field path below (already copied)
+    du, dv = resident or (to_device(f.u), to_device(f.v))
     if du.dtype != dv.dtype:
         du, dv = du.double(), dv.double()
     lo, hi, ma = device_range(du, dv)
@@ -271,11 +288,8 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
         eps = eps * (hi - lo)
     S = scale_for(ma)
     tau = tau_from_eps(eps, S)
-    H, W, T = f.H, f.W, f.T
-    N = H * W * T
     p = make_params(H, W, T, f.dx, f.dy, f.dt, S, tau, cfg)
     pp = ctypes.byref(p)
-    L = _lib.lib()
     st = _lib.stream_ptr()
     dev = du.device
     dt_code = dtype_code(du)
@@ -331,6 +345,24 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                                  qd.data_ptr(), modes.data_ptr(),
                                  _lib.ptr(scores), row_ll.data_ptr(),
                                  _lib.ptr(recon), st), "encode")
+    return _finish_streams(f, cfg, p, du, dv, dt_code, eps, S, tau, codes,
+                           ld_words, qd_row_off, nqd.value, qd, modes, row_ll,
+                           mask, scores, recon, host)
+
+
+def _finish_streams(f, cfg, p, du, dv, dt_code, eps, S, tau, codes, ld_words,
+                    qd_row_off, nqd, qd, modes, row_ll, mask, scores, recon,
+                    host):
+    """The lossless side stream (codec.py:129-131,155-158), the host copies
+    of the small streams, and the DeviceStreams record."""
+    import torch
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    pp = ctypes.byref(p)
+    H, W, T = f.H, f.W, f.T
+    N = H * W * T
+    dev = du.device
+    nby, nbx = _mode_grid_shape(H, W, cfg)
     ll_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
     nll = ctypes.c_int64(0)
     _lib.check(L.vfcp_row_offsets(row_ll.data_ptr(), T * H,
@@ -355,10 +387,241 @@ def compress_device(f: FieldSeries, eps: float, config: Config | None = None,
                 "modes": h_modes.numpy()}
     return DeviceStreams(
         eps=eps, scale=S, tau=tau, codes=codes, ld=ld,
-        qd=qd[:nqd.value], ll=ll[:nll.value],
+        qd=qd[:nqd], ll=ll[:nll.value],
         modes=modes[:(T - 1) * nby * nbx], mask=mask,
         scores=scores[:(T - 1) * nby * nbx * 2] if scores is not None else None,
         recon=recon, host=host)
+
+
+def _stream_ok(f, cfg: Config, extras: bool) -> bool:
+    """Whether compress_device may take the frame-streamed path: page-locked
+    host tensors of one float dtype and a configuration of the block path
+    (csrc/capi.cu fast_ok; tau' is checked once the range is known)."""
+    if extras or os.environ.get("VFCP_NO_STREAM") or os.environ.get("VFCP_SLOW_PATH"):
+        return False
+    u, v = f.u, f.v
+    if not (type(u).__module__.startswith("torch") and
+            type(v).__module__.startswith("torch")):
+        return False
+    import torch
+    if u.is_cuda or v.is_cuda or u.dtype != v.dtype:
+        return False
+    if u.dtype not in (torch.float32, torch.float64):
+        return False
+    if not (u.is_pinned() and v.is_pinned() and u.is_contiguous()
+            and v.is_contiguous()):
+        return False
+    return (cfg.bx == 32 and cfg.by == 32 and cfg.radius <= 32768
+            and cfg.stride >= 2 and f.H <= 65535 and f.T >= 2)
+
+
+def _compress_streamed(f: FieldSeries, eps: float, cfg: Config,
+                       relative: bool, host_out: bool, want_hist: bool = False):
+    """compress_device for a field in page-locked host memory, overlapped
+    with its own H2D copy (codec.py:321-376; the result is the whole-field
+    path's, stream for stream).
+
+    The frames are copied one by one on a copy stream.  The scale S and a
+    relative eps need the value range of the whole field before any vertex
+    can be converted, so host threads reduce it at memory bandwidth while the
+    first frames cross (vfcp_host_range); the device still reduces every
+    frame as it arrives and the two must agree.  Frame t's codes are final
+    once the anchors of frames t - 1 and t have been analysed
+    (vfcp_analyze_slab), which needs frame t + 1 on the device; its symbol
+    offsets follow from the counts of the frames before it; then the frame is
+    encoded (vfcp_encode_stream_frame) and, with host_out, its codes / l_d /
+    symbols go back on a side stream.  Returns the device copies (du, dv)
+    instead when the configuration turns out to be outside the block path
+    (tau', a list or int32 overflow): the caller then runs the whole-field
+    path on them."""
+    import torch
+    L = _lib.lib()
+    H, W, T = f.H, f.W, f.T
+    HW = H * W
+    N = HW * T
+    hu, hv = f.u.reshape(-1), f.v.reshape(-1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    du = torch.empty(N, dtype=hu.dtype, device=dev)
+    dv = torch.empty(N, dtype=hv.dtype, device=dev)
+    dt_code = dtype_code(du)
+    copy.wait_stream(main)
+    arrived = []
+    timing = bool(os.environ.get("VFCP_STREAM_TIMES"))
+    if timing:
+        import time
+        w0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(copy)
+    with torch.cuda.stream(copy):
+        for t in range(T):
+            a, b = t * HW, (t + 1) * HW
+            du[a:b].copy_(hu[a:b], non_blocking=True)
+            dv[a:b].copy_(hv[a:b], non_blocking=True)
+            ev = torch.cuda.Event(enable_timing=timing)
+            ev.record(copy)
+            arrived.append(ev)
+    du.record_stream(copy)
+    dv.record_stream(copy)
+
+    def whole_field():
+        main.wait_stream(copy)
+        return du, dv
+
+    out3 = np.zeros(3, np.float64)
+    # (more threads finish sooner but take memory bandwidth from the DMA:
+    # the streams' D2H of host_out can only start once the range is known)
+    nthr = int(os.environ.get("VFCP_RANGE_THREADS", "0")) or \
+        min(_lib.host_threads(), 16 if host_out else 8)
+    _lib.check(L.vfcp_host_range(hu.data_ptr(), hv.data_ptr(), dt_code, N,
+                                 nthr, out3.ctypes.data), "host range")
+    if timing:
+        w1 = time.perf_counter()
+    lo, hi, ma = float(out3[0]), float(out3[1]), float(out3[2])
+    if relative:
+        eps = eps * (hi - lo)
+    S = scale_for(ma)
+    tau = tau_from_eps(eps, S)
+    if not 0 < tau < (1 << 29):
+        return whole_field()
+    p = make_params(H, W, T, f.dx, f.dy, f.dt, S, tau, cfg)
+    pp = ctypes.byref(p)
+    st = main.cuda_stream
+    codes = torch.zeros(N, dtype=torch.uint8, device=dev)
+    ld_words = torch.zeros((N + 31) // 32, dtype=torch.int32, device=dev)
+    row_n31 = torch.zeros(T * H, dtype=torch.int32, device=dev)
+    cap = min(HW, 1 << 25)
+    lst = torch.empty(cap, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    nb = 8 * torch.cuda.get_device_properties(dev).multi_processor_count
+    parts = torch.empty((T, nb, 3), dtype=torch.float64, device=dev)
+    qd_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
+    qd = torch.empty(2 * N, dtype=torch.uint16, device=dev)
+    nby, nbx = _mode_grid_shape(H, W, cfg)
+    modes = torch.empty(max((T - 1) * nby * nbx, 1), dtype=torch.uint8,
+                        device=dev)
+    row_ll = torch.empty(T * H, dtype=torch.int32, device=dev)
+    frame_off = torch.zeros(T + 1, dtype=torch.int64, pin_memory=True)
+    fo = frame_off.numpy()
+    side = h_codes = h_ld = h_qd = None
+    ld_frames = HW % 32 == 0
+    if host_out:
+        side = torch.cuda.Stream()
+        h_codes = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+        h_ld = torch.empty((N + 7) // 8, dtype=torch.uint8, pin_memory=True)
+        h_qd = torch.empty(2 * N, dtype=torch.uint16, pin_memory=True)
+    ld_bytes = ld_words.view(torch.uint8)
+    hist = None
+    if want_hist:
+        hist = {"qd": torch.zeros(2 * cfg.radius, dtype=torch.int64, device=dev),
+                "codes": torch.zeros(EB_ALPHABET, dtype=torch.int64, device=dev)}
+        qd_base = max(0, cfg.radius - 4096)
+    handle = ctypes.c_void_p()
+    _lib.check(L.vfcp_encode_stream_begin(
+        pp, du.data_ptr(), dv.data_ptr(), dt_code, codes.data_ptr(),
+        qd_row_off.data_ptr(), qd.data_ptr(), modes.data_ptr(),
+        row_ll.data_ptr(), st, ctypes.byref(handle)), "encode stream begin")
+    esz = du.element_size()
+
+    def range_part(t):
+        _lib.check(L.vfcp_value_range_part(
+            du.data_ptr() + t * HW * esz, dv.data_ptr() + t * HW * esz,
+            dt_code, HW, parts[t].data_ptr(), nb, st), "value_range part")
+
+    try:
+        main.wait_event(arrived[0])
+        range_part(0)
+        for t in range(T):
+            if t + 1 < T:
+                main.wait_event(arrived[t + 1])
+                range_part(t + 1)
+            # the anchors of frame t (frames t, t + 1): frame t's codes final
+            _lib.check(L.vfcp_analyze_slab(
+                pp, du.data_ptr(), dv.data_ptr(), dt_code, t, t + 1,
+                codes.data_ptr(), ld_words.data_ptr(), None,
+                row_n31.data_ptr(), lst.data_ptr(), cap, count.data_ptr(),
+                ovf.data_ptr(), st), "analyze slab")
+            _lib.check(L.vfcp_qd_offsets_upto(
+                pp, t + 1, row_n31.data_ptr(), qd_row_off.data_ptr(),
+                frame_off.data_ptr() + 8 * (t + 1), st), "qd offsets")
+            ready = torch.cuda.Event()
+            ready.record(main)
+            if host_out:
+                side.wait_event(ready)
+                with torch.cuda.stream(side):
+                    a, b = t * HW, (t + 1) * HW
+                    h_codes[a:b].copy_(codes[a:b], non_blocking=True)
+                    if ld_frames:
+                        h_ld[a // 8:b // 8].copy_(ld_bytes[a // 8:b // 8],
+                                                  non_blocking=True)
+            _lib.check(L.vfcp_encode_stream_frame(handle, t), "encode frame")
+            if host_out:
+                done = torch.cuda.Event()
+                done.record(main)
+            if host_out or want_hist:
+                ready.synchronize()     # frame_off[t + 1] is on the host
+                a, b = int(fo[t]), int(fo[t + 1])
+            if host_out and b > a:
+                side.wait_event(done)
+                with torch.cuda.stream(side):
+                    h_qd[a:b].copy_(qd[a:b], non_blocking=True)
+            if want_hist:
+                # symbol counts while the GPU waits for the next frame; the
+                # spans are cut at multiples of 8 symbols (16-byte loads)
+                a8 = a & ~7
+                b8 = b if t == T - 1 else b & ~7
+                _lib.check(L.vfcp_huff_hist_dev(
+                    qd.data_ptr() + 2 * a8, 2, b8 - a8, 2 * cfg.radius, qd_base,
+                    hist["qd"].data_ptr(), st), "huffman histogram")
+                _lib.check(L.vfcp_huff_hist_dev(
+                    codes.data_ptr() + t * HW, 1, HW, EB_ALPHABET, 0,
+                    hist["codes"].data_ptr(), st), "huffman histogram")
+    except BaseException:
+        L.vfcp_encode_stream_end(handle, None)
+        raise
+    # the device's own range of every frame against the host's
+    pr = parts.view(-1, 3)
+    chk = torch.stack([pr[:, 0].min(), pr[:, 1].max(), pr[:, 2].max(),
+                       ovf[0].to(torch.float64)])
+    h_chk = torch.empty(4, dtype=torch.float64, pin_memory=True)
+    h_chk.copy_(chk, non_blocking=True)
+    enc_ovf = ctypes.c_int(0)
+    _lib.check(L.vfcp_encode_stream_end(handle, ctypes.byref(enc_ovf)),
+               "encode stream end")      # synchronises the main stream
+    if timing:
+        w2 = time.perf_counter()
+        import sys
+        print(f"[stream] host range {1e3 * (w1 - w0):.1f} ms ({nthr} threads); "
+              f"frames on device at "
+              + " ".join(f"{e0.elapsed_time(a):.0f}" for a in arrived)
+              + f" ms; main stream done {1e3 * (w2 - w0):.1f} ms",
+              file=sys.stderr)
+    c = h_chk.numpy()
+    if (float(c[0]), float(c[1]), float(c[2])) != (lo, hi, ma):
+        raise _lib.VfcpError(
+            "host and device value ranges disagree: "
+            f"{(lo, hi, ma)} vs {tuple(float(x) for x in c[:3])}")
+    if enc_ovf.value or c[3] != 0.0:
+        if side is not None:
+            side.synchronize()
+        return whole_field()
+    nqd = int(fo[T])
+    host = None
+    if host_out:
+        if not ld_frames:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                h_ld.copy_(ld_bytes[:(N + 7) // 8], non_blocking=True)
+        for x in (codes, ld_words, qd):
+            x.record_stream(side)
+        host = {"codes": h_codes, "ld": h_ld, "qd": h_qd[:nqd], "side": side}
+    s = _finish_streams(f, cfg, p, du, dv, dt_code, eps, S, tau, codes,
+                        ld_words, qd_row_off, nqd, qd, modes, row_ll,
+                        None, None, None, host)
+    s.hist = hist
+    return s
 
 
 def archive_from_streams(f_dims, s: DeviceStreams, cfg: Config,
@@ -411,7 +674,8 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         # (the codes' section is built after the frames: its kernels, run
         # beside the frame loop on a side stream, take issue slots from the
         # block-scan chain and the call ends later)
-        s = compress_device(f, eps, cfg, relative)
+        s = compress_device(f, eps, cfg, relative, want_hist=True)
+        hq, hc = (s.hist["qd"], s.hist["codes"]) if s.hist else (None, None)
         # the small sections go to pinned memory on a side stream while
         # the symbol section is histogrammed and packed
         main = torch.cuda.current_stream()
@@ -422,8 +686,8 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         for x in (s.ld, s.ll, s.modes):
             x.record_stream(side)
         pending = huffman.encode_device_many([
-            (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096)),
-            (s.codes, EB_ALPHABET, 0)])
+            (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096), hq),
+            (s.codes, EB_ALPHABET, 0, hc)])
         q_d = pending[0].result()
         q_xi = pending[1].result()
         side.synchronize()

@@ -367,7 +367,7 @@ __device__ __forceinline__ uint32_t cls_nib(double x, double y, double Td) {
 template <typename F>
 __global__ void __launch_bounds__(C_THREADS, 4)
 cube_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
-            int T, F Tq, uint64_t* __restrict__ list,
+            int T, int t0, int t1, F Tq, uint64_t* __restrict__ list,
             unsigned long long* __restrict__ count, unsigned long long cap) {
   __shared__ uint32_t cls[2][CRH][CQW + 1];   // 4 class bytes per word
   const int tid = threadIdx.x, lane = tid & 31;
@@ -436,14 +436,15 @@ cube_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
       cls[s][lr][g] = w;
     }
   };
-  issue(0);
-  commit(0);
-  if (T > 1) issue(1);
+  // anchors of frames [t0, t1): reads frames t0 .. min(t1, T - 1)
+  issue(t0);
+  commit(t0);
+  if (t0 + 1 < T) issue(t0 + 1);
   const unsigned FULL = 0xffffffffu;
-  for (int t = 0; t < T; t++) {
+  for (int t = t0; t < t1; t++) {
     const bool slab = t + 1 < T;
     if (slab) commit(t + 1);
-    if (t + 2 < T) issue(t + 2);
+    if (t + 2 < T && t + 1 < t1) issue(t + 2);
     __syncthreads();
     const int s0 = t & 1, s1 = (t + 1) & 1;
     // thread: row lr, anchors 4g .. 4g+3 (CTJ / 4 = 32 groups per row)
@@ -597,6 +598,12 @@ __global__ void ovf_flag_kernel(const unsigned long long* count,
   *ovf = *count > cap ? 1 : 0;
 }
 
+// the same for a slab of anchors: the flag of earlier slabs stays set
+__global__ void ovf_or_kernel(const unsigned long long* count,
+                              unsigned long long cap, int* ovf) {
+  if (*count > cap) *ovf = 1;
+}
+
 // every vertex lossless (tau' <= 0): l_d all ones (packbits of N bits,
 // zero padded), W code-31 vertices per row (the codes: a memset); skipped
 // when the fused fallback runs
@@ -687,7 +694,7 @@ cudaError_t launch_analyze(const F* u, const F* v, int H, int W, int T,
     Tq = (F)Td;
   }
   cube_kernel<F><<<dim3((W + CTJ - 1) / CTJ, (H + CTI - 1) / CTI), C_THREADS, 0, st>>>(
-      u, v, H, W, T, Tq, list, count, cap);
+      u, v, H, W, T, 0, T, Tq, list, count, cap);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ovf_flag_kernel<<<1, 1, 0, st>>>(count, cap, ovf);
   exact_kernel<F><<<nsm * 8, 128, 0, st>>>(u, v, H, W, T, S, tau, list, count,
@@ -708,6 +715,41 @@ cudaError_t launch_analyze(const F* u, const F* v, int H, int W, int T,
   dim3 grid((W + TJ - 1) / TJ, (H + TI - 1) / TI);
   analyze_kernel<F><<<grid, K1_THREADS, smem, st>>>(
       u, v, H, W, T, S, tau, codes, ld_words, mask, row_n31, ovf);
+  return cudaGetLastError();
+}
+
+// The anchors of frames [t0, t1) only (they read frames t0 .. min(t1, T-1)):
+// every update of codes / l_d / row counts / mask is an atomic max / or /
+// first-touch count, so the slabs of a field may run in any partition and
+// leave the same arrays as launch_analyze.  codes, ld_words, mask, row_n31
+// and *ovf are zeroed by the caller before the first slab; a list overflow
+// sets *ovf (the caller then redoes the field with launch_analyze).  tau > 0.
+template <typename F>
+cudaError_t launch_analyze_slab(const F* u, const F* v, int H, int W, int T,
+                                int t0, int t1, double S, int64_t tau,
+                                uint8_t* codes, uint32_t* ld_words,
+                                uint16_t* mask, int32_t* row_n31,
+                                uint64_t* list, unsigned long long* count,
+                                int* ovf, unsigned long long cap, int nsm,
+                                cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+  const double Td = ((double)(tau + 1) - 0.5) / S;
+  F Tq;
+  if (sizeof(F) == 4) {
+    float tf = (float)Td;
+    if ((double)tf < Td) tf = nextafterf(tf, INFINITY);
+    Tq = (F)tf;
+  } else {
+    Tq = (F)Td;
+  }
+  cube_kernel<F><<<dim3((W + CTJ - 1) / CTJ, (H + CTI - 1) / CTI), C_THREADS, 0, st>>>(
+      u, v, H, W, T, t0, t1, Tq, list, count, cap);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ovf_or_kernel<<<1, 1, 0, st>>>(count, cap, ovf);
+  exact_kernel<F><<<nsm * 8, 128, 0, st>>>(u, v, H, W, T, S, tau, list, count,
+                                          cap, ovf, codes, ld_words, mask,
+                                          row_n31);
   return cudaGetLastError();
 }
 
@@ -736,5 +778,14 @@ template cudaError_t launch_analyze<double>(const double*, const double*, int,
                                             unsigned long long*, int*,
                                             unsigned long long, int,
                                             cudaStream_t);
+
+template cudaError_t launch_analyze_slab<float>(
+    const float*, const float*, int, int, int, int, int, double, int64_t,
+    uint8_t*, uint32_t*, uint16_t*, int32_t*, uint64_t*, unsigned long long*,
+    int*, unsigned long long, int, cudaStream_t);
+template cudaError_t launch_analyze_slab<double>(
+    const double*, const double*, int, int, int, int, int, double, int64_t,
+    uint8_t*, uint32_t*, uint16_t*, int32_t*, uint64_t*, unsigned long long*,
+    int*, unsigned long long, int, cudaStream_t);
 
 }  // namespace vfcp

@@ -26,6 +26,12 @@ cudaError_t launch_analyze(const F*, const F*, int, int, int, double, int64_t,
                            uint8_t*, uint32_t*, uint16_t*, int32_t*,
                            uint64_t*, unsigned long long*, int*,
                            unsigned long long, int, cudaStream_t);
+template <typename F>
+cudaError_t launch_analyze_slab(const F*, const F*, int, int, int, int, int,
+                                double, int64_t, uint8_t*, uint32_t*,
+                                uint16_t*, int32_t*, uint64_t*,
+                                unsigned long long*, int*, unsigned long long,
+                                int, cudaStream_t);
 cudaError_t launch_row_scan(const int32_t*, int64_t, int, int, int64_t*,
                             cudaStream_t);
 // encode.cu
@@ -553,74 +559,120 @@ struct HostOut {
   ~HostOut() { finish(); }
 };
 
+// The frame loop of the block path as a stepping context: begin() sets up
+// the scratch and tables, frame(t) enqueues frame t (enc_block_kernel:
+// tiles, MoP, SL blocks, block classes and edges; then the block-scan chain
+// with the interior pass, bscan.cuh, which writes recon(t) and the Lorenzo
+// symbols), end() reads the int32-overflow flag.  vfcp_encode runs the
+// frames back to back; vfcp_encode_stream_* lets the caller enqueue frame t
+// as soon as its inputs (orig(t), codes(t), qd_row_off of its rows) exist,
+// e.g. while later frames are still crossing PCIe.
+struct EncFramesBase {
+  virtual ~EncFramesBase() {}
+  virtual int begin(bool prefix_all) = 0;
+  virtual int frame(int t) = 0;
+  virtual int end(bool* overflowed) = 0;
+};
+
 template <typename F>
-int encode_fast(const vfcp_params* p, const F* u, const F* v,
-                const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
-                uint8_t* modes, int32_t* row_ll, int64_t* recon,
-                cudaStream_t st, bool* overflowed, HostOut* ho) {
-  // per frame: enc_block_kernel (enc_block.cu: tiles, MoP, SL blocks,
-  // block classes and edges) then the block-scan chain with the interior
-  // pass (bscan.cuh), which writes recon(t) and the Lorenzo symbols
-  const int H = p->H, W = p->W, T = p->T;
-  const int nchunks = (W + 31) / 32, Wp = 32 * nchunks;
-  const int nby = (H + 31) / 32;
-  const int64_t nblk = (int64_t)nchunks * nby;
-  const int64_t HW = (int64_t)H * W;
-  const int64_t plane = (int64_t)H * Wp, cplane = (int64_t)H * nchunks;
-  const int nsm = nsm_of();
-  Scratch sc(st);
-  int32_t *pre_nl, *a, *out, *rec;
-  int *ticket, *ovf;
+struct EncFrames : EncFramesBase {
+  vfcp_params P;
+  const F *u, *v;
+  const uint8_t* codes;
+  const int64_t* qd_row_off;
+  uint16_t* qd;
+  uint8_t* modes;
+  int32_t* row_ll;
+  int64_t* recon;
+  cudaStream_t st;
+  Scratch sc;
+  int H, W, T, nchunks, Wp, nby, nsm;
+  int64_t nblk, HW, plane, cplane;
+  int32_t *pre_nl = nullptr, *a = nullptr, *out = nullptr, *rec = nullptr;
+  int *ticket = nullptr, *ovf = nullptr;
   double* log2tab = nullptr;
-  CK(sc.get(&pre_nl, (size_t)T * cplane));
-  CK(sc.get(&a, (size_t)2 * plane));      // R0 of swept blocks
-  CK(sc.get(&out, (size_t)2 * plane));    // err of swept blocks
-  CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
-  CK(sc.get(&ticket, (size_t)2 * T));   // per frame: chain / interior
-  CK(sc.get(&ovf, 1));
-  CK(cudaMemsetAsync(ticket, 0, sizeof(int) * 2 * T, st));
-  CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-  CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
-  const bool mop = p->predictor == VFCP_PRED_MOP && p->tau > 0;
   std::vector<double> tab;
-  if (mop) {
-    const int nlog = 2 * p->bx * p->by + 1;
-    tab.resize(nlog);
-    tab[0] = 0.0;
-    for (int h = 1; h < nlog; h++) tab[h] = std::log2((double)h);
-    CK(sc.get(&log2tab, (size_t)nlog));
-    CK(cudaMemcpyAsync(log2tab, tab.data(), sizeof(double) * nlog,
-                       cudaMemcpyHostToDevice, st));
-  }
-  if (T > 1)
-    CK(cudaMemsetAsync(modes,
-                       (p->predictor == VFCP_PRED_SL && p->tau > 0) ? 1 : 0,
-                       (size_t)(T - 1) * nblk, st));
-  LAUNCH(K_SCAN, st,
-         launch_chunk_prefix<uint16_t>(codes, nullptr, nullptr,
-                                       (int64_t)T * H, W, nchunks, p->tau,
-                                       pre_nl, nullptr, st));
-  const Ladder lad = make_ladder(p->tau);
+  Ladder lad;
   BScanIO bio;
-  {
-    int rc = bscan_setup(sc, lad, H, W, p->radius, st, &bio);
-    if (rc) return rc;
+  bool cls_stats = false, prefix_all = true;
+
+  EncFrames(const vfcp_params* p, const F* u_, const F* v_,
+            const uint8_t* codes_, const int64_t* qd_row_off_, uint16_t* qd_,
+            uint8_t* modes_, int32_t* row_ll_, int64_t* recon_,
+            cudaStream_t st_)
+      : P(*p), u(u_), v(v_), codes(codes_), qd_row_off(qd_row_off_), qd(qd_),
+        modes(modes_), row_ll(row_ll_), recon(recon_), st(st_), sc(st_) {
+    H = P.H; W = P.W; T = P.T;
+    nchunks = (W + 31) / 32; Wp = 32 * nchunks;
+    nby = (H + 31) / 32;
+    nblk = (int64_t)nchunks * nby;
+    HW = (int64_t)H * W;
+    plane = (int64_t)H * Wp; cplane = (int64_t)H * nchunks;
+    nsm = nsm_of();
   }
-  bio.a[0] = a; bio.a[1] = a + plane;
-  bio.a_w[0] = a; bio.a_w[1] = a + plane;
-  bio.out[0] = out; bio.out[1] = out + plane;
-  bio.qd = qd;
-  bio.cpitch = W;
-  bio.S = p->scale;
-  if (getenv("VFCP_CHAIN_STAMPS")) {
-    CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
-    CK(sc.get(&bio.phase, (size_t)nby * 8));
+
+  int begin(bool prefix_all_) override {
+    prefix_all = prefix_all_;
+    const vfcp_params* p = &P;
+    CK(sc.get(&pre_nl, (size_t)T * cplane));
+    CK(sc.get(&a, (size_t)2 * plane));      // R0 of swept blocks
+    CK(sc.get(&out, (size_t)2 * plane));    // err of swept blocks
+    CK(sc.get(&rec, (size_t)4 * plane));    // recon ping-pong, (u, v) pairs
+    CK(sc.get(&ticket, (size_t)2 * T));   // per frame: chain / interior
+    CK(sc.get(&ovf, 1));
+    CK(cudaMemsetAsync(ticket, 0, sizeof(int) * 2 * T, st));
+    CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(row_ll, 0, sizeof(int32_t) * (size_t)T * H, st));
+    const bool mop = p->predictor == VFCP_PRED_MOP && p->tau > 0;
+    if (mop) {
+      const int nlog = 2 * p->bx * p->by + 1;
+      tab.resize(nlog);
+      tab[0] = 0.0;
+      for (int h = 1; h < nlog; h++) tab[h] = std::log2((double)h);
+      CK(sc.get(&log2tab, (size_t)nlog));
+      CK(cudaMemcpyAsync(log2tab, tab.data(), sizeof(double) * nlog,
+                         cudaMemcpyHostToDevice, st));
+    }
+    if (T > 1)
+      CK(cudaMemsetAsync(modes,
+                         (p->predictor == VFCP_PRED_SL && p->tau > 0) ? 1 : 0,
+                         (size_t)(T - 1) * nblk, st));
+    if (prefix_all)
+      LAUNCH(K_SCAN, st,
+             launch_chunk_prefix<uint16_t>(codes, nullptr, nullptr,
+                                           (int64_t)T * H, W, nchunks, p->tau,
+                                           pre_nl, nullptr, st));
+    lad = make_ladder(p->tau);
+    {
+      int rc = bscan_setup(sc, lad, H, W, p->radius, st, &bio);
+      if (rc) return rc;
+    }
+    bio.a[0] = a; bio.a[1] = a + plane;
+    bio.a_w[0] = a; bio.a_w[1] = a + plane;
+    bio.out[0] = out; bio.out[1] = out + plane;
+    bio.qd = qd;
+    bio.cpitch = W;
+    bio.S = p->scale;
+    if (getenv("VFCP_CHAIN_STAMPS")) {
+      CK(sc.get(&bio.stamps, (size_t)2 * nby * 3));
+      CK(sc.get(&bio.phase, (size_t)nby * 8));
+    }
+    cls_stats = getenv("VFCP_CLS_STATS") != nullptr;
+    bio.dbg_skip_interior = getenv("VFCP_CHAIN_ONLY") != nullptr;
+    bio.vec4 = sizeof(F) == 4 && (W & 3) == 0 &&
+               (((uintptr_t)u | (uintptr_t)v | (uintptr_t)qd) & 15) == 0;
+    return VFCP_OK;
   }
-  const bool cls_stats = getenv("VFCP_CLS_STATS") != nullptr;
-  bio.dbg_skip_interior = getenv("VFCP_CHAIN_ONLY") != nullptr;
-  bio.vec4 = sizeof(F) == 4 && (W & 3) == 0 &&
-             (((uintptr_t)u | (uintptr_t)v | (uintptr_t)qd) & 15) == 0;
-  for (int t = 0; t < T; t++) {
+
+  int frame(int t) override {
+    const vfcp_params* p = &P;
+    if (t < 0 || t >= T) return fail(VFCP_EINVAL, "frame out of range");
+    if (!prefix_all)
+      LAUNCH(K_SCAN, st,
+             launch_chunk_prefix<uint16_t>(codes + (size_t)t * HW, nullptr,
+                                           nullptr, (int64_t)H, W, nchunks,
+                                           p->tau, pre_nl + (size_t)t * cplane,
+                                           nullptr, st));
     const PrepParams pp = prep_params(p, t, lad);
     int32_t* rprev = rec + 2 * plane * ((t + 1) & 1);
     int32_t* rcur = rec + 2 * plane * (t & 1);
@@ -649,16 +701,31 @@ int encode_fast(const vfcp_params* p, const F* u, const F* v,
                   reinterpret_cast<const int2*>(rcur), H, W, Wp, t,
                   (int64_t)H * W * T, recon),
               cudaGetLastError()));
-    {
-      int rch = ho->frame(t, qd, st);
-      if (rch) return rch;
-    }
+    return VFCP_OK;
   }
-  int h_ovf = 0;
-  CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  *overflowed = h_ovf != 0;
-  return VFCP_OK;
+
+  int end(bool* overflowed) override {
+    int h_ovf = 0;
+    CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *overflowed = h_ovf != 0;
+    return VFCP_OK;
+  }
+};
+
+template <typename F>
+int encode_fast(const vfcp_params* p, const F* u, const F* v,
+                const uint8_t* codes, const int64_t* qd_row_off, uint16_t* qd,
+                uint8_t* modes, int32_t* row_ll, int64_t* recon,
+                cudaStream_t st, bool* overflowed, HostOut* ho) {
+  EncFrames<F> ef(p, u, v, codes, qd_row_off, qd, modes, row_ll, recon, st);
+  int rc = ef.begin(true);
+  if (rc) return rc;
+  for (int t = 0; t < p->T; t++) {
+    if ((rc = ef.frame(t))) return rc;
+    if ((rc = ho->frame(t, qd, st))) return rc;
+  }
+  return ef.end(overflowed);
 }
 
 // Per-frame copies of the float64 output to (pinned) host memory on a side
@@ -906,6 +973,103 @@ int vfcp_value_range(const void* u, const void* v, int dtype, int64_t n,
   }
   out3[0] = lo; out3[1] = hi; out3[2] = ma;
   return VFCP_OK;
+}
+
+// ---- frame streaming (compress of a field still crossing PCIe)
+
+int vfcp_value_range_part(const void* u, const void* v, int dtype, int64_t n,
+                          double* part, int nb, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0 || nb <= 0) return fail(VFCP_EINVAL, "empty field");
+  if (dtype == VFCP_F32)
+    LAUNCH(K_RANGE, st, launch_range((const float*)u, (const float*)v, n, part, nb, st));
+  else
+    LAUNCH(K_RANGE, st, launch_range((const double*)u, (const double*)v, n, part, nb, st));
+  return VFCP_OK;
+}
+
+int vfcp_analyze_slab(const vfcp_params* p, const void* u, const void* v,
+                      int dtype, int t0, int t1, uint8_t* codes,
+                      uint32_t* ld_words, uint16_t* mask, int32_t* row_n31,
+                      uint64_t* list, int64_t cap, unsigned long long* count,
+                      int* ovf, void* stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (t0 < 0 || t1 > p->T || t0 >= t1)
+    return fail(VFCP_EINVAL, "vfcp_analyze_slab: bad frame range");
+  if (p->tau <= 0 || cap <= 0)
+    return fail(VFCP_EINVAL, "vfcp_analyze_slab: needs tau' > 0 and a list");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nsm = nsm_of();
+  if (dtype == VFCP_F32)
+    LAUNCH(K_ANALYZE, st,
+           launch_analyze_slab((const float*)u, (const float*)v, p->H, p->W,
+                               p->T, t0, t1, p->scale, p->tau, codes, ld_words,
+                               mask, row_n31, list, count, ovf,
+                               (unsigned long long)cap, nsm, st));
+  else
+    LAUNCH(K_ANALYZE, st,
+           launch_analyze_slab((const double*)u, (const double*)v, p->H, p->W,
+                               p->T, t0, t1, p->scale, p->tau, codes, ld_words,
+                               mask, row_n31, list, count, ovf,
+                               (unsigned long long)cap, nsm, st));
+  return VFCP_OK;
+}
+
+int vfcp_qd_offsets_upto(const vfcp_params* p, int nframes,
+                         const int32_t* row_n31, int64_t* qd_row_off,
+                         int64_t* total_dev_to_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nframes < 1 || nframes > p->T)
+    return fail(VFCP_EINVAL, "vfcp_qd_offsets_upto: bad frame count");
+  const int64_t nrows = (int64_t)nframes * p->H;
+  LAUNCH(K_SCAN, st, launch_row_scan(row_n31, nrows, p->W, 2, qd_row_off, st));
+  CK(cudaMemcpyAsync(total_dev_to_host, qd_row_off + nrows, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  return VFCP_OK;
+}
+
+int vfcp_encode_stream_begin(const vfcp_params* p, const void* u,
+                             const void* v, int dtype, const uint8_t* codes,
+                             const int64_t* qd_row_off, void* qd,
+                             uint8_t* modes, int32_t* row_ll, void* stream,
+                             void** handle) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (!handle) return fail(VFCP_EINVAL, "null handle");
+  *handle = nullptr;
+  if (!fast_ok(p) || getenv("VFCP_SLOW_PATH"))
+    return fail(VFCP_EINVAL,
+                "vfcp_encode_stream: configuration outside the block path");
+  cudaStream_t st = (cudaStream_t)stream;
+  EncFramesBase* ef;
+  if (dtype == VFCP_F32)
+    ef = new EncFrames<float>(p, (const float*)u, (const float*)v, codes,
+                              qd_row_off, (uint16_t*)qd, modes, row_ll,
+                              nullptr, st);
+  else
+    ef = new EncFrames<double>(p, (const double*)u, (const double*)v, codes,
+                               qd_row_off, (uint16_t*)qd, modes, row_ll,
+                               nullptr, st);
+  rc = ef->begin(false);
+  if (rc) { delete ef; return rc; }
+  *handle = ef;
+  return VFCP_OK;
+}
+
+int vfcp_encode_stream_frame(void* handle, int t) {
+  if (!handle) return fail(VFCP_EINVAL, "null handle");
+  return static_cast<EncFramesBase*>(handle)->frame(t);
+}
+
+int vfcp_encode_stream_end(void* handle, int* overflowed) {
+  if (!handle) return fail(VFCP_EINVAL, "null handle");
+  EncFramesBase* ef = static_cast<EncFramesBase*>(handle);
+  bool ovf = false;
+  const int rc = ef->end(&ovf);
+  if (overflowed) *overflowed = ovf ? 1 : 0;
+  delete ef;
+  return rc;
 }
 
 int vfcp_analyze(const vfcp_params* p, const void* u, const void* v,

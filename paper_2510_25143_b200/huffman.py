@@ -150,8 +150,11 @@ class PendingBlob:
 
 def encode_device_many(sections) -> list:
     """encode() of several CUDA uint8 / uint16 tensors, given as
-    (symbols, alphabet_size, window_base) (window_base: first symbol of the
-    shared-memory histogram window, the symbols' mode).  All histograms run
+    (symbols, alphabet_size, window_base[, counts]) (window_base: first symbol
+    of the shared-memory histogram window, the symbols' mode; counts: the
+    symbols' device histogram when the caller already has it -- the
+    frame-streamed compress counts each frame as it is encoded).  All
+    histograms run
     before the one host synchronisation (code lengths are built on the
     host), then every section is packed and copied to pinned memory
     asynchronously: the returned PendingBlob.result()s give the bytes."""
@@ -159,7 +162,11 @@ def encode_device_many(sections) -> list:
     L = _lib.lib()
     st = _lib.stream_ptr()
     counts = []
-    for sym, alpha, base in sections:
+    for sec in sections:
+        sym, alpha, base = sec[:3]
+        if len(sec) > 3 and sec[3] is not None:
+            counts.append(sec[3])
+            continue
         c = torch.zeros(alpha, dtype=torch.int64, device=sym.device)
         if sym.numel():
             _lib.check(L.vfcp_huff_hist_dev(sym.data_ptr(), sym.element_size(),
@@ -169,7 +176,8 @@ def encode_device_many(sections) -> list:
         counts.append(c)
     counts = [c.cpu().numpy() for c in counts]   # one synchronisation
     out = []
-    for (sym, alpha, _), counts_h in zip(sections, counts):
+    for sec, counts_h in zip(sections, counts):
+        sym, alpha = sec[0], sec[1]
         n = int(sym.numel())
         lens = code_lengths(counts_h)
         total_bits = int((counts_h * lens.astype(np.int64)).sum())

@@ -1,0 +1,186 @@
+"""The frame-streamed compress path (page-locked host input, frames analysed
+and encoded while later frames cross PCIe: codec._compress_streamed) against
+the reference's golden sections and against the whole-field device path
+(bit-exact: every stream, the archive bytes, the host copies)."""
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+_TOOK = {}
+
+
+def _cfg(g, **kw):
+    import paper_2510_25143_b200 as vg
+    return vg.Config(predictor=str(g["predictor"]), bx=int(g["bx"]),
+                     by=int(g["by"]), stride=int(g["stride"]),
+                     lam=float(g["lam"]), theta=float(g["theta"]),
+                     radius=int(g["radius"]), d_max=float(g["d_max"]),
+                     n_max=int(g["n_max"]), **kw)
+
+
+def _pinned_field(H, W, T, dx, dy, dt, u, v):
+    import torch
+    import paper_2510_25143_b200 as vg
+    up = torch.from_numpy(np.ascontiguousarray(u)).pin_memory()
+    vp = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+    return vg.FieldSeries(H, W, T, dx, dy, dt, up, vp)
+
+
+def _golden_field(g):
+    return _pinned_field(int(g["H"]), int(g["W"]), int(g["T"]),
+                         float(g["dx"]), float(g["dy"]), float(g["dt"]),
+                         g["u"], g["v"])
+
+
+def _streamable(g):
+    return (int(g["bx"]) == 32 and int(g["by"]) == 32 and
+            int(g["radius"]) <= 32768 and int(g["stride"]) >= 2 and
+            0 < int(g["tau"]) < (1 << 29))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_streamed_matches_reference(name, monkeypatch):
+    """Pinned host input: the streamed path (or, for configurations outside
+    the block path, its hand-over to the whole-field path) reproduces the
+    reference's sections."""
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import codec
+    g = load_golden(name)
+    f = _golden_field(g)
+    cfg = _cfg(g)
+    took = []
+    orig = codec._compress_streamed
+
+    def spy(*a, **k):
+        r = orig(*a, **k)
+        took.append(isinstance(r, codec.DeviceStreams))
+        return r
+
+    monkeypatch.setattr(codec, "_compress_streamed", spy)
+    s = vg.compress_device(f, float(g["eps"]), cfg,
+                           relative=bool(g["relative"]), host_out=True)
+    if _streamable(g) and codec._stream_ok(f, cfg, False):
+        # (a golden whose R0 overflows int32 is handed to the whole-field
+        # path after the stream: still the reference's sections below)
+        _TOOK[name] = bool(took and took[0])
+    assert s.scale == float(g["scale"])
+    assert s.tau == int(g["tau"])
+    assert s.eps == float(g["eps_abs"])
+    np.testing.assert_array_equal(s.codes.cpu().numpy(), g["codes"])
+    np.testing.assert_array_equal(s.ld.cpu().numpy(), g["ld"])
+    np.testing.assert_array_equal(s.modes.cpu().numpy(), g["modes"].reshape(-1))
+    np.testing.assert_array_equal(s.qd.cpu().numpy().astype(np.int32), g["qd"])
+    np.testing.assert_array_equal(s.ll.cpu().numpy(), g["ll"])
+    h = codec.streams_to_host(s)
+    np.testing.assert_array_equal(h["codes"], g["codes"])
+    np.testing.assert_array_equal(h["ld"], g["ld"])
+    np.testing.assert_array_equal(h["qd"].astype(np.int32), g["qd"])
+    np.testing.assert_array_equal(h["ll"], g["ll"])
+    np.testing.assert_array_equal(h["modes"], g["modes"].reshape(-1))
+    a = vg.compress(f, float(g["eps"]), cfg, relative=bool(g["relative"]))
+    assert a.to_bytes() == bytes(g["archive"])
+
+
+def test_goldens_did_stream():
+    """Most streamable goldens went through the streamed path itself."""
+    if not _TOOK:
+        pytest.skip("golden cases not run")
+    assert sum(_TOOK.values()) * 2 >= len(_TOOK), _TOOK
+
+
+def _synthetic(H, W, T, seed, dtype):
+    rng = np.random.default_rng(seed)
+    y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+    u = np.empty((T, H, W))
+    v = np.empty((T, H, W))
+    for t in range(T):
+        ph = 0.37 * t
+        u[t] = np.sin(2 * np.pi * (x - 1.3 * t) / 61.0 + ph) * np.cos(2 * np.pi * y / 47.0)
+        v[t] = np.cos(2 * np.pi * (y + 0.9 * t) / 53.0) * np.sin(2 * np.pi * x / 71.0 + ph)
+    u += 0.01 * rng.standard_normal(u.shape)
+    v += 0.01 * rng.standard_normal(v.shape)
+    return u.reshape(-1).astype(dtype), v.reshape(-1).astype(dtype)
+
+
+@pytest.mark.parametrize("H,W,T,eps,dtype,pred", [
+    (256, 320, 6, 1e-3, np.float32, "mop"),
+    (200, 333, 5, 1e-2, np.float32, "mop"),       # ragged blocks, H*W % 32 != 0
+    (192, 256, 4, 1e-3, np.float64, "mop"),
+    (256, 256, 3, 1e-4, np.float32, "lorenzo"),
+    (160, 224, 4, 1e-2, np.float32, "sl"),
+    (1024, 1536, 8, 1e-3, np.float32, "mop"),     # multi-CTA chains
+])
+def test_streamed_equals_whole_field(H, W, T, eps, dtype, pred, monkeypatch):
+    import torch
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import codec
+    u, v = _synthetic(H, W, T, 7 * H + T, dtype)
+    cfg = vg.Config(predictor=pred)
+    f_host = _pinned_field(H, W, T, 1.0, 1.0, 1.0, u, v)
+    f_dev = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0,
+                           torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+    took = []
+    orig = codec._compress_streamed
+
+    def spy(*a, **k):
+        r = orig(*a, **k)
+        took.append(isinstance(r, codec.DeviceStreams))
+        return r
+
+    monkeypatch.setattr(codec, "_compress_streamed", spy)
+    ref = vg.compress_device(f_dev, eps, cfg, relative=True)
+    assert not took
+    for host_out in (False, True):
+        s = vg.compress_device(f_host, eps, cfg, relative=True, host_out=host_out)
+        assert took and took[-1], "streamed path not taken"
+        assert (s.eps, s.scale, s.tau) == (ref.eps, ref.scale, ref.tau)
+        for k in ("codes", "ld", "qd", "ll", "modes"):
+            assert torch.equal(getattr(s, k), getattr(ref, k)), k
+        if host_out:
+            h = codec.streams_to_host(s)
+            for k in ("codes", "ld", "qd", "ll", "modes"):
+                np.testing.assert_array_equal(h[k], getattr(ref, k).cpu().numpy(), k)
+    # the archive of the streamed path decodes to the same reconstruction
+    a_host = vg.compress(f_host, eps, cfg, relative=True)
+    a_dev = vg.compress(f_dev, eps, cfg, relative=True)
+    assert a_host.to_bytes() == a_dev.to_bytes()
+
+
+def test_streamed_hands_over_outside_block_path():
+    """tau' = 0 (eps = 0) and a non-default block grid: pinned input still
+    compresses, through the whole-field path."""
+    import torch
+    import paper_2510_25143_b200 as vg
+    H, W, T = 96, 128, 3
+    u, v = _synthetic(H, W, T, 5, np.float32)
+    f_host = _pinned_field(H, W, T, 1.0, 1.0, 1.0, u, v)
+    f_dev = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0,
+                           torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+    for eps, cfg in ((0.0, vg.Config()), (1e-3, vg.Config(bx=16, by=16))):
+        a = vg.compress_device(f_host, eps, cfg, relative=True)
+        b = vg.compress_device(f_dev, eps, cfg, relative=True)
+        for k in ("codes", "ld", "qd", "ll", "modes"):
+            assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_host_range_matches_device():
+    import ctypes
+    import torch
+    from paper_2510_25143_b200 import _lib, field
+    rng = np.random.default_rng(3)
+    for dtype, code in ((np.float32, _lib.VFCP_F32), (np.float64, _lib.VFCP_F64)):
+        for n in (1, 17, 65536, 3 * (1 << 20) + 5):
+            u = (rng.standard_normal(n) * 3).astype(dtype)
+            v = (rng.standard_normal(n) * 5 - 1).astype(dtype)
+            out = np.zeros(3)
+            _lib.check(_lib.lib().vfcp_host_range(
+                u.ctypes.data, v.ctypes.data, code, n, 7, out.ctypes.data), "host range")
+            lo = float(min(u.min(), v.min()))
+            hi = float(max(u.max(), v.max()))
+            ma = float(max(np.abs(u).max(), np.abs(v).max()))
+            assert tuple(out) == (lo, hi, ma)
+            if n > 1:
+                d = field.device_range(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+                assert d == (lo, hi, ma)

@@ -105,3 +105,23 @@ def test_archive_errors():
     bad[4] = 9
     with pytest.raises(ValueError):
         Archive.from_bytes(bytes(bad))
+
+
+def test_host_range_exact():
+    """vfcp_host_range (the streamed path's early value range) equals
+    numpy's min / max / max|x| on both dtypes, any length and thread count."""
+    from paper_2510_25143_b200 import _lib
+    rng = np.random.default_rng(11)
+    for dtype, code in ((np.float32, _lib.VFCP_F32), (np.float64, _lib.VFCP_F64)):
+        for n, nt in ((1, 4), (15, 1), (4097, 3), (2 * (1 << 20) + 3, 8)):
+            u = (rng.standard_normal(n) * 3).astype(dtype)
+            v = (rng.standard_normal(n) * 5 - 1).astype(dtype)
+            out = np.zeros(3)
+            _lib.check(_lib.lib().vfcp_host_range(
+                u.ctypes.data, v.ctypes.data, code, n, nt, out.ctypes.data),
+                "host range")
+            assert out[0] == min(u.min(), v.min())
+            assert out[1] == max(u.max(), v.max())
+            assert out[2] == max(np.abs(u).max(), np.abs(v).max())
+    out = np.zeros(3)
+    assert _lib.lib().vfcp_host_range(None, None, 0, 0, 1, out.ctypes.data) != 0
