@@ -674,7 +674,15 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         # (the codes' section is built after the frames: its kernels, run
         # beside the frame loop on a side stream, take issue slots from the
         # block-scan chain and the call ends later)
+        timing = bool(os.environ.get("VFCP_ARCHIVE_TIMES"))
+        if timing:
+            import time
+            tm = [time.perf_counter()]
+            mark = lambda: tm.append(time.perf_counter())   # noqa: E731
+        else:
+            mark = lambda: None   # noqa: E731
         s = compress_device(f, eps, cfg, relative, want_hist=True)
+        mark()
         hq, hc = (s.hist["qd"], s.hist["codes"]) if s.hist else (None, None)
         # the small sections go to pinned memory on a side stream while
         # the symbol section is histogrammed and packed
@@ -688,18 +696,28 @@ def compress(f: FieldSeries, eps: float, config: Config | None = None,
         pending = huffman.encode_device_many([
             (s.qd, 2 * cfg.radius, max(0, cfg.radius - 4096), hq),
             (s.codes, EB_ALPHABET, 0, hc)])
+        mark()
+        side.synchronize()
+        l_d = memoryview(h_ld.numpy())     # page-locked, no second copy
+        mark()
         q_d = pending[0].result()
         q_xi = pending[1].result()
-        side.synchronize()
-        l_d = huffman.new_bytearray(h_ld.numel())
-        huffman.host_copy(np.frombuffer(l_d, dtype=np.uint8), h_ld.numpy())
-        return Archive(
+        mark()
+        a = Archive(
             H=f.H, W=f.W, T=f.T, dx=f.dx, dy=f.dy, dt=f.dt, scale=s.scale,
             eps=s.eps, tau_prime=s.tau, config=cfg, q_xi=q_xi, q_d=q_d,
             l_d=l_d,
             lossless_stream=h_ll.numpy().astype("<i8", copy=False).tobytes(),
             mode_bitmap=np.packbits(h_modes.numpy()).tobytes(),
         )
+        if timing:
+            mark()
+            import sys
+            d = [1e3 * (tm[i + 1] - tm[i]) for i in range(len(tm) - 1)]
+            print(f"[archive] compress_device {d[0]:.1f} | small D2H + pack "
+                  f"enqueue {d[1]:.1f} | l_d bytes {d[2]:.1f} | q_d, q_xi "
+                  f"bytes {d[3]:.1f} | Archive {d[4]:.1f} ms", file=sys.stderr)
+        return a
     s = compress_device(f, eps, cfg, relative, want_mask=cfg.stats,
                         host_out=True)
     host = streams_to_host(s)

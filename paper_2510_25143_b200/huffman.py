@@ -124,27 +124,19 @@ def host_touch(dst: np.ndarray) -> list:
 
 
 class PendingBlob:
-    """A device-packed section on its way to pinned host memory: the
-    destination bytes are allocated (and their pages touched, on host
-    threads) while the device packs and copies."""
+    """A device-packed section on its way to page-locked host memory: header
+    and packed bits land in one pinned buffer, and result() is a memoryview
+    of it (no second copy of a section of hundreds of megabytes; the buffer
+    returns to torch's caching host allocator when the section is dropped)."""
 
-    def __init__(self, head, nbytes, host, words, event):
-        self._head, self._nbytes = head, nbytes
+    def __init__(self, nbytes, host, words, event):
+        self._nbytes = nbytes
         self._host, self._words, self._event = host, words, event
-        self._blob = new_bytearray(len(head) + nbytes)
-        self._blob[:len(head)] = head
-        self._touch = host_touch(np.frombuffer(self._blob, dtype=np.uint8)[len(head):])
 
-    def result(self) -> bytearray:
-        blob, head = self._blob, self._head
-        if self._nbytes:
-            for t in self._touch:
-                t.result()
-            self._event.synchronize()
-            host_copy(np.frombuffer(blob, dtype=np.uint8)[len(head):],
-                      self._host.numpy().view(np.uint8)[:self._nbytes])
-        self._host = self._words = self._blob = None
-        self._touch = []
+    def result(self) -> memoryview:
+        self._event.synchronize()
+        blob = memoryview(self._host.numpy())[:self._nbytes]
+        self._host = self._words = None
         return blob
 
 
@@ -188,21 +180,24 @@ def encode_device_many(sections) -> list:
                                             n, lens.ctypes.data, alpha,
                                             words.data_ptr(), n_words, st),
                        "huffman pack (device)")
-        h = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
-        h.copy_(words, non_blocking=True)
+        head = _HDR.pack(alpha, n, total_bits) + lens.tobytes()
+        h = torch.empty(len(head) + 4 * n_words, dtype=torch.uint8,
+                        pin_memory=True)
+        h.numpy()[:len(head)] = np.frombuffer(head, dtype=np.uint8)
+        h[len(head):].copy_(words.view(torch.uint8), non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        head = _HDR.pack(alpha, n, total_bits) + lens.tobytes()
-        out.append(PendingBlob(head, (total_bits + 7) // 8, h, words, ev))
+        out.append(PendingBlob(len(head) + (total_bits + 7) // 8, h, words, ev))
     return out
 
 
-def encode_device(symbols, alphabet_size: int, window_base: int = 0) -> bytes:
+def encode_device(symbols, alphabet_size: int, window_base: int = 0):
     """encode() of a CUDA uint8 / uint16 tensor: the same bytes.
 
     window_base: first symbol of the shared-memory histogram window (the
     symbols' mode; radius - 4096 for the residual stream)."""
     return encode_device_many([(symbols, alphabet_size, window_base)])[0].result()
+
 
 
 def alphabet_of(blob) -> int:
