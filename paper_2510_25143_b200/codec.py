@@ -393,6 +393,14 @@ def _finish_streams(f, cfg, p, du, dv, dt_code, eps, S, tau, codes, ld_words,
         recon=recon, host=host)
 
 
+# Below this many input bytes per frame the frame-streamed path's per-frame
+# launches and host hand-shakes cost more than the overlap saves (configs 1-3:
+# 0.1 - 2 MB frames, hundreds of frames; measured in
+# profiles/bench_matrix_r02.json): such fields take the whole-field path.
+STREAM_MIN_FRAME_BYTES = int(os.environ.get("VFCP_STREAM_MIN_FRAME_BYTES",
+                                            str(16 << 20)))
+
+
 def _stream_ok(f, cfg: Config, extras: bool) -> bool:
     """Whether compress_device may take the frame-streamed path: page-locked
     host tensors of one float dtype and a configuration of the block path
@@ -410,6 +418,8 @@ def _stream_ok(f, cfg: Config, extras: bool) -> bool:
         return False
     if not (u.is_pinned() and v.is_pinned() and u.is_contiguous()
             and v.is_contiguous()):
+        return False
+    if 2 * f.H * f.W * u.element_size() < STREAM_MIN_FRAME_BYTES:
         return False
     return (cfg.bx == 32 and cfg.by == 32 and cfg.radius <= 32768
             and cfg.stride >= 2 and f.H <= 65535 and f.T >= 2)

@@ -168,6 +168,7 @@ def encode_device_many(sections) -> list:
         counts.append(c)
     counts = [c.cpu().numpy() for c in counts]   # one synchronisation
     out = []
+    side = torch.cuda.Stream()
     for sec, counts_h in zip(sections, counts):
         sym, alpha = sec[0], sec[1]
         n = int(sym.numel())
@@ -184,9 +185,16 @@ def encode_device_many(sections) -> list:
         h = torch.empty(len(head) + 4 * n_words, dtype=torch.uint8,
                         pin_memory=True)
         h.numpy()[:len(head)] = np.frombuffer(head, dtype=np.uint8)
-        h[len(head):].copy_(words.view(torch.uint8), non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        # the copy goes to a side stream: the next section's pack kernels
+        # run under it
+        packed = torch.cuda.Event()
+        packed.record()
+        side.wait_event(packed)
+        with torch.cuda.stream(side):
+            h[len(head):].copy_(words.view(torch.uint8), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        words.record_stream(side)
         out.append(PendingBlob(len(head) + (total_bits + 7) // 8, h, words, ev))
     return out
 

@@ -11,6 +11,14 @@ pytestmark = pytest.mark.gpu
 _TOOK = {}
 
 
+@pytest.fixture(autouse=True)
+def _stream_small_frames(monkeypatch):
+    """The test fields are far below the frame size from which compress_device
+    streams by default: lift the threshold."""
+    from paper_2510_25143_b200 import codec
+    monkeypatch.setattr(codec, "STREAM_MIN_FRAME_BYTES", 0)
+
+
 def _cfg(g, **kw):
     import paper_2510_25143_b200 as vg
     return vg.Config(predictor=str(g["predictor"]), bx=int(g["bx"]),
@@ -163,6 +171,19 @@ def test_streamed_hands_over_outside_block_path():
         b = vg.compress_device(f_dev, eps, cfg, relative=True)
         for k in ("codes", "ld", "qd", "ll", "modes"):
             assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_small_frames_take_whole_field_by_default(monkeypatch):
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import codec
+    monkeypatch.setattr(codec, "STREAM_MIN_FRAME_BYTES", 16 << 20)
+    u, v = _synthetic(64, 96, 3, 1, np.float32)
+    f = _pinned_field(64, 96, 3, 1.0, 1.0, 1.0, u, v)
+    assert not codec._stream_ok(f, vg.Config(), False)
+    monkeypatch.setattr(codec, "STREAM_MIN_FRAME_BYTES", 0)
+    assert codec._stream_ok(f, vg.Config(), False)
+    assert not codec._stream_ok(f, vg.Config(), True)
+    assert not codec._stream_ok(f, vg.Config(bx=16, by=16), False)
 
 
 def test_host_range_matches_device():
