@@ -298,6 +298,26 @@ def run(config: int, eps: float, predictor: str = "mop", H=None, W=None,
     arch_ok["l_d"] = bytes(a.l_d) == g_ld.tobytes()
     arch_ok["lossless_stream"] = a.lossless_stream == g_ll.astype("<i8").tobytes()
     arch_ok["mode_bitmap"] = a.mode_bitmap == np.packbits(g_modes).tobytes()
+    # the frame-streamed path (page-locked host input, frames analysed and
+    # encoded while later frames cross PCIe: codec._compress_streamed) must
+    # give these very streams and archive sections
+    codec.STREAM_MIN_FRAME_BYTES = 0
+    fp = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0,
+                        torch.from_numpy(u).pin_memory(),
+                        torch.from_numpy(v).pin_memory())
+    stream_ok = {"taken": bool(codec._stream_ok(fp, cfg, False))}
+    hs = codec.streams_to_host(codec.compress_device(fp, eps, cfg, relative=True,
+                                                     host_out=True))
+    for k in ("codes", "ld", "qd", "ll", "modes"):
+        stream_ok[k] = bool(np.array_equal(hs[k], host[k]))
+    del hs
+    a2 = vg.compress(fp, eps, cfg, relative=True)
+    for k in ("q_xi", "q_d", "l_d", "lossless_stream", "mode_bitmap"):
+        stream_ok["archive_" + k] = bytes(getattr(a2, k)) == bytes(getattr(a, k))
+    del a2, fp
+    arch_ok.update({"streamed_" + k: v for k, v in stream_ok.items()
+                    if k != "taken"})
+    rep["streamed_path"] = stream_ok
     del s
     torch.cuda.empty_cache()
     # decompress: the archive decodes to the encoder's reconstruction, or
