@@ -479,13 +479,51 @@ def _compress_streamed(f: FieldSeries, eps: float, cfg: Config,
         main.wait_stream(copy)
         return du, dv
 
-    out3 = np.zeros(3, np.float64)
-    # (more threads finish sooner but take memory bandwidth from the DMA:
-    # the streams' D2H of host_out can only start once the range is known)
+    # The value range.  The device reduces every frame as it arrives (its own
+    # stream, partial triples to page-locked memory); host threads reduce the
+    # frames from the back of the field until they meet it: the frames the
+    # DMA has not delivered yet are the ones only the host can see.
+    # (More threads finish sooner but take memory bandwidth from the DMA; the
+    # streams' D2H of host_out can only start once the range is known.)
     nthr = int(os.environ.get("VFCP_RANGE_THREADS", "0")) or \
         min(_lib.host_threads(), 16 if host_out else 8)
-    _lib.check(L.vfcp_host_range(hu.data_ptr(), hv.data_ptr(), dt_code, N,
-                                 nthr, out3.ctypes.data), "host range")
+    nb = 8 * torch.cuda.get_device_properties(dev).multi_processor_count
+    parts = torch.empty((T, nb, 3), dtype=torch.float64, device=dev)
+    h_parts = torch.empty((T, nb, 3), dtype=torch.float64, pin_memory=True)
+    esz = du.element_size()
+    rstream = torch.cuda.Stream()
+    rstream.wait_stream(main)
+    rdone = []
+    with torch.cuda.stream(rstream):
+        for t in range(T):
+            rstream.wait_event(arrived[t])
+            _lib.check(L.vfcp_value_range_part(
+                du.data_ptr() + t * HW * esz, dv.data_ptr() + t * HW * esz,
+                dt_code, HW, parts[t].data_ptr(), nb, rstream.cuda_stream),
+                "value_range part")
+            h_parts[t].copy_(parts[t], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(rstream)
+            rdone.append(ev)
+    for x in (du, dv, parts):
+        x.record_stream(rstream)
+    hp = h_parts.numpy()
+    out3 = np.zeros(3, np.float64)
+    lo, hi, ma = math.inf, -math.inf, 0.0
+    k = T
+    while k > 0 and not rdone[k - 1].query():
+        k -= 1
+        _lib.check(L.vfcp_host_range(hu.data_ptr() + k * HW * esz,
+                                     hv.data_ptr() + k * HW * esz, dt_code,
+                                     HW, nthr, out3.ctypes.data), "host range")
+        lo, hi, ma = min(lo, out3[0]), max(hi, out3[1]), max(ma, out3[2])
+    host_frames = T - k
+    if k > 0:
+        rdone[k - 1].synchronize()
+        lo = min(lo, hp[:k, :, 0].min())
+        hi = max(hi, hp[:k, :, 1].max())
+        ma = max(ma, hp[:k, :, 2].max())
+    out3[:] = (lo, hi, ma)
     if timing:
         w1 = time.perf_counter()
     lo, hi, ma = float(out3[0]), float(out3[1]), float(out3[2])
@@ -505,8 +543,6 @@ def _compress_streamed(f: FieldSeries, eps: float, cfg: Config,
     lst = torch.empty(cap, dtype=torch.int64, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
-    nb = 8 * torch.cuda.get_device_properties(dev).multi_processor_count
-    parts = torch.empty((T, nb, 3), dtype=torch.float64, device=dev)
     qd_row_off = torch.empty(T * H + 1, dtype=torch.int64, device=dev)
     qd = torch.empty(2 * N, dtype=torch.uint16, device=dev)
     nby, nbx = _mode_grid_shape(H, W, cfg)
@@ -533,20 +569,11 @@ def _compress_streamed(f: FieldSeries, eps: float, cfg: Config,
         pp, du.data_ptr(), dv.data_ptr(), dt_code, codes.data_ptr(),
         qd_row_off.data_ptr(), qd.data_ptr(), modes.data_ptr(),
         row_ll.data_ptr(), st, ctypes.byref(handle)), "encode stream begin")
-    esz = du.element_size()
-
-    def range_part(t):
-        _lib.check(L.vfcp_value_range_part(
-            du.data_ptr() + t * HW * esz, dv.data_ptr() + t * HW * esz,
-            dt_code, HW, parts[t].data_ptr(), nb, st), "value_range part")
-
     try:
         main.wait_event(arrived[0])
-        range_part(0)
         for t in range(T):
             if t + 1 < T:
                 main.wait_event(arrived[t + 1])
-                range_part(t + 1)
             # the anchors of frame t (frames t, t + 1): frame t's codes final
             _lib.check(L.vfcp_analyze_slab(
                 pp, du.data_ptr(), dv.data_ptr(), dt_code, t, t + 1,
@@ -591,29 +618,28 @@ def _compress_streamed(f: FieldSeries, eps: float, cfg: Config,
     except BaseException:
         L.vfcp_encode_stream_end(handle, None)
         raise
-    # the device's own range of every frame against the host's
-    pr = parts.view(-1, 3)
-    chk = torch.stack([pr[:, 0].min(), pr[:, 1].max(), pr[:, 2].max(),
-                       ovf[0].to(torch.float64)])
-    h_chk = torch.empty(4, dtype=torch.float64, pin_memory=True)
-    h_chk.copy_(chk, non_blocking=True)
+    h_ovf = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    h_ovf.copy_(ovf, non_blocking=True)
     enc_ovf = ctypes.c_int(0)
     _lib.check(L.vfcp_encode_stream_end(handle, ctypes.byref(enc_ovf)),
                "encode stream end")      # synchronises the main stream
     if timing:
         w2 = time.perf_counter()
         import sys
-        print(f"[stream] host range {1e3 * (w1 - w0):.1f} ms ({nthr} threads); "
+        print(f"[stream] range known after {1e3 * (w1 - w0):.1f} ms ({nthr} "
+              f"threads took the last {host_frames} frames); "
               f"frames on device at "
               + " ".join(f"{e0.elapsed_time(a):.0f}" for a in arrived)
               + f" ms; main stream done {1e3 * (w2 - w0):.1f} ms",
               file=sys.stderr)
-    c = h_chk.numpy()
-    if (float(c[0]), float(c[1]), float(c[2])) != (lo, hi, ma):
+    # the device's own range of every frame against the one used above
+    rdone[T - 1].synchronize()
+    c = (float(hp[:, :, 0].min()), float(hp[:, :, 1].max()),
+         float(hp[:, :, 2].max()))
+    if c != (lo, hi, ma):
         raise _lib.VfcpError(
-            "host and device value ranges disagree: "
-            f"{(lo, hi, ma)} vs {tuple(float(x) for x in c[:3])}")
-    if enc_ovf.value or c[3] != 0.0:
+            f"host and device value ranges disagree: {(lo, hi, ma)} vs {c}")
+    if enc_ovf.value or int(h_ovf[0]) != 0:
         if side is not None:
             side.synchronize()
         return whole_field()

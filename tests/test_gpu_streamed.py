@@ -173,6 +173,36 @@ def test_streamed_hands_over_outside_block_path():
             assert torch.equal(getattr(a, k), getattr(b, k)), k
 
 
+@pytest.mark.parametrize("host_all", [True, False])
+def test_range_split_between_host_and_device(host_all, monkeypatch):
+    """The value range: host threads take frames from the back until they
+    meet the device's per-frame reduction.  Both extremes (the host sees every
+    frame first / the device does) give the whole-field path's eps and scale."""
+    import torch
+    import paper_2510_25143_b200 as vg
+    H, W, T = 128, 160, 6
+    u, v = _synthetic(H, W, T, 21, np.float32)
+    u[5 * H * W + 17] = 9.5          # extremes in the last and the first frame
+    v[3] = -7.25
+    f_host = _pinned_field(H, W, T, 1.0, 1.0, 1.0, u, v)
+    f_dev = vg.FieldSeries(H, W, T, 1.0, 1.0, 1.0,
+                           torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+    ref = vg.compress_device(f_dev, 1e-3, vg.Config(), relative=True)
+    if host_all:
+        monkeypatch.setattr(torch.cuda.Event, "query", lambda self: False)
+    else:
+        real = torch.cuda.Event.query
+
+        def wait_then_true(self):
+            self.synchronize()
+            return real(self)
+        monkeypatch.setattr(torch.cuda.Event, "query", wait_then_true)
+    s = vg.compress_device(f_host, 1e-3, vg.Config(), relative=True)
+    assert (s.eps, s.scale, s.tau) == (ref.eps, ref.scale, ref.tau)
+    for k in ("codes", "ld", "qd", "ll", "modes"):
+        assert torch.equal(getattr(s, k), getattr(ref, k)), k
+
+
 def test_small_frames_take_whole_field_by_default(monkeypatch):
     import paper_2510_25143_b200 as vg
     from paper_2510_25143_b200 import codec
