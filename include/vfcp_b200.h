@@ -116,8 +116,10 @@ int vfcp_encode_host(const vfcp_params* p, const void* u, const void* v,
 /* field.py:69-73 value_range + choose_scale's max|x| on HOST memory (u, v:
  * host arrays of n values), reduced by nthreads host threads: the scale and a
  * relative eps must be known before the first frame can be converted, i.e.
- * before the data has crossed PCIe.  out3 = {min, max, max|x|}.  A hint the
- * device range (vfcp_value_range_part over every frame) is checked against. */
+ * before the data has crossed PCIe.  out3 = {min, max, max|x|}.  Meant for
+ * the spans the DMA delivers last (the device reduces the frames that have
+ * arrived); a hint the device range (vfcp_value_range_part over every frame)
+ * is checked against. */
 int vfcp_host_range(const void* u, const void* v, int dtype, int64_t n,
                     int nthreads, double* out3);
 

@@ -4,9 +4,12 @@
 // the same bytes cross PCIe.  The reference's global scale S and a relative
 // eps need these three numbers before any vertex can be converted to fixed
 // point, so a compress() of host data can only overlap its H2D copy with
-// device work if they are known early.  The result is a *hint*: the device
-// range kernel (analyze.cu range_kernel) still reduces every frame as it
-// arrives and the caller compares the two (codec.py _compress_streamed).
+// device work if they are known early.  The caller (codec.py
+// _compress_streamed) hands this function the frames from the back of the
+// field, which the DMA delivers last, while the device range kernel
+// (analyze.cu range_kernel) reduces the frames that have arrived; the result
+// is a *hint*: the device ends up reducing every frame and the caller
+// compares the two.
 //
 // Minima and maxima of finite values are exact in any order; FieldSeries has
 // already rejected NaN / Inf (field.py:37-51), so the comparisons need no
