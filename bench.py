@@ -541,7 +541,7 @@ def main():
         sweep[str(e_x)] = ent
         del sx
 
-    e2e_s = arc_s = ent_s = None
+    e2e_s = arc_s = ent_s = dec_e2e_s = None
     d2h = arc_bytes = 0
     dent = None
     if not args.quick:
@@ -580,6 +580,20 @@ def main():
         torch.cuda.synchronize()
         arc_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
         arc_bytes = sum(len(x) for x in arc.sections)
+        # the way back: decompress() of that Archive (sections in host
+        # memory) to float64 u, v in host memory, every frame's output copied
+        # while later frames decode
+        for _ in range(max(1, args.warmup)):
+            back = None
+            back = vg.decompress(arc)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            back = None
+            back = vg.decompress(arc)
+        torch.cuda.synchronize()
+        dec_e2e_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
+        del back
         del arc
         # host entropy backend (Huffman + zlib), timed on frame 0's streams
         nq0 = 2 * (H * W) if s.qd.numel() >= 2 * H * W else s.qd.numel()
@@ -670,6 +684,11 @@ def main():
             "api": "compress() -> Archive sections",
             "path": "frame-streamed + device entropy stage",
             "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": arc_bytes}
+        line["e2e_decompress"] = {
+            "value": round(8.0 * N * world / dec_e2e_s / 1e9, 3), "unit": UNIT,
+            "ms_per_step": round(dec_e2e_s * 1e3, 1),
+            "api": "decompress(Archive) -> float64 u, v in host memory",
+            "h2d_bytes_per_step": arc_bytes, "d2h_bytes_per_step": 16 * N}
         line["device_entropy"] = dent
         line["host_entropy"] = {
             "sample": "frame 0 codes + qd: Huffman + zlib(6)",
