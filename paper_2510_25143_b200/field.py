@@ -51,8 +51,9 @@ class FieldSeries:
         for name, arr in (("u", self.u), ("v", self.v)):
             if _is_torch(arr):
                 import torch
-                bad = torch.nonzero(~torch.isfinite(arr))
-                if bad.numel():
+                # (one reduction; the index list only for a field that fails)
+                if not bool(torch.isfinite(arr).all()):
+                    bad = torch.nonzero(~torch.isfinite(arr))
                     raise FieldError(
                         f"non-finite sample in {name} at index {int(bad[0, 0])}")
             else:

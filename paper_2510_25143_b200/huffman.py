@@ -254,7 +254,9 @@ def decode_device(blob, out_dtype=np.uint16):
     n_words = (total_bits + 31) // 32 + 2
     hw = torch.empty(n_words, dtype=torch.int32, pin_memory=True)
     hb = hw.numpy().view(np.uint8)
-    hb[:nbytes] = np.frombuffer(blob, dtype=np.uint8, count=nbytes, offset=off)
+    # (hundreds of megabytes: the copy is split over the host threads)
+    host_copy(hb[:nbytes],
+              np.frombuffer(blob, dtype=np.uint8, count=nbytes, offset=off))
     hb[nbytes:] = 0
     words = hw.cuda(non_blocking=True)
     out = torch.empty(n_symbols, dtype=tdt, device="cuda")
