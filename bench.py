@@ -541,7 +541,7 @@ def main():
         sweep[str(e_x)] = ent
         del sx
 
-    e2e_s = arc_s = ent_s = dec_e2e_s = None
+    e2e_s = arc_s = ent_s = dec_e2e_s = dec_err = None
     d2h = arc_bytes = 0
     dent = None
     if not args.quick:
@@ -583,16 +583,25 @@ def main():
         # the way back: decompress() of that Archive (sections in host
         # memory) to float64 u, v in host memory, every frame's output copied
         # while later frames decode
-        for _ in range(max(1, args.warmup)):
-            back = None
-            back = vg.decompress(arc)
+        dec_err = None
         barrier()
-        t0 = time.perf_counter()
-        for _ in range(max(1, args.steps)):
-            back = None
-            back = vg.decompress(arc)
-        torch.cuda.synchronize()
-        dec_e2e_s = max_over_ranks((time.perf_counter() - t0) / max(1, args.steps))
+        try:
+            for _ in range(max(1, args.warmup)):
+                back = None
+                back = vg.decompress(arc)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(max(1, args.steps)):
+                back = None
+                back = vg.decompress(arc)
+            torch.cuda.synchronize()
+            dec_local = (time.perf_counter() - t0) / max(1, args.steps)
+        except (RuntimeError, MemoryError) as err:
+            # (its 16 N bytes of page-locked output are the largest host
+            # allocation of the bench: reported, not fatal)
+            dec_local, dec_err = float("inf"), str(err).splitlines()[0][:200]
+        back = None
+        dec_e2e_s = max_over_ranks(dec_local)
         del back
         del arc
         # host entropy backend (Huffman + zlib), timed on frame 0's streams
@@ -684,11 +693,12 @@ def main():
             "api": "compress() -> Archive sections",
             "path": "frame-streamed + device entropy stage",
             "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": arc_bytes}
-        line["e2e_decompress"] = {
+        line["e2e_decompress"] = ({
             "value": round(8.0 * N * world / dec_e2e_s / 1e9, 3), "unit": UNIT,
             "ms_per_step": round(dec_e2e_s * 1e3, 1),
             "api": "decompress(Archive) -> float64 u, v in host memory",
             "h2d_bytes_per_step": arc_bytes, "d2h_bytes_per_step": 16 * N}
+            if dec_e2e_s != float("inf") else {"error": dec_err})
         line["device_entropy"] = dent
         line["host_entropy"] = {
             "sample": "frame 0 codes + qd: Huffman + zlib(6)",
