@@ -235,3 +235,87 @@ def test_host_range_matches_device():
             if n > 1:
                 d = field.device_range(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
                 assert d == (lo, hi, ma)
+
+
+@pytest.mark.parametrize("H,W,T,seed", [(96, 160, 7, 0), (130, 75, 5, 1),
+                                         (64, 64, 2, 2), (257, 300, 9, 3)])
+def test_analyze_slab_any_partition(H, W, T, seed):
+    """include/vfcp_b200.h: any partition of [0, T) into anchor slabs, run in
+    any order, leaves vfcp_analyze's codes / l_d / row counts / face mask;
+    vfcp_qd_offsets_upto is the prefix of vfcp_qd_offsets."""
+    import ctypes
+    import torch
+    import paper_2510_25143_b200 as vg
+    from paper_2510_25143_b200 import _lib, codec, field
+    rng = np.random.default_rng(seed)
+    u, v = _synthetic(H, W, T, 40 + seed, np.float32)
+    # critical points and degenerate faces: a few exact zeros and repeats
+    idx = rng.integers(0, u.size, 200)
+    u[idx] = 0.0
+    v[idx[::2]] = 0.0
+    du, dv = torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda()
+    lo, hi, ma = field.device_range(du, dv)
+    S = field.scale_for(ma)
+    tau = codec.tau_from_eps(1e-2 * (hi - lo), S)
+    assert tau > 0
+    p = codec.make_params(H, W, T, 1.0, 1.0, 1.0, S, tau, vg.Config())
+    pp = ctypes.byref(p)
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    N = H * W * T
+
+    def arrays():
+        return (torch.zeros(N, dtype=torch.uint8, device="cuda"),
+                torch.zeros((N + 31) // 32, dtype=torch.int32, device="cuda"),
+                torch.zeros(N + 1, dtype=torch.int16, device="cuda"),
+                torch.zeros(T * H, dtype=torch.int32, device="cuda"))
+
+    c0, l0, m0, r0 = arrays()
+    _lib.check(L.vfcp_analyze(pp, du.data_ptr(), dv.data_ptr(), 0, c0.data_ptr(),
+                              l0.data_ptr(), m0.data_ptr(), r0.data_ptr(), st),
+               "analyze")
+    off0 = torch.empty(T * H + 1, dtype=torch.int64, device="cuda")
+    tot = ctypes.c_int64(0)
+    _lib.check(L.vfcp_qd_offsets(pp, r0.data_ptr(), off0.data_ptr(),
+                                 ctypes.addressof(tot), st), "qd offsets")
+    cap = H * W * T
+    lst = torch.empty(cap, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for trial in range(3):
+        cuts = sorted(set(rng.integers(1, T, rng.integers(0, T)).tolist())) if T > 2 else []
+        bounds = [0] + cuts + [T]
+        slabs = list(zip(bounds[:-1], bounds[1:]))
+        rng.shuffle(slabs)
+        c1, l1, m1, r1 = arrays()
+        ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for a, b in slabs:
+            _lib.check(L.vfcp_analyze_slab(
+                pp, du.data_ptr(), dv.data_ptr(), 0, int(a), int(b), c1.data_ptr(),
+                l1.data_ptr(), m1.data_ptr(), r1.data_ptr(), lst.data_ptr(), cap,
+                cnt.data_ptr(), ovf.data_ptr(), st), "analyze slab")
+        assert int(ovf[0]) == 0
+        assert torch.equal(c1, c0), (trial, slabs)
+        assert torch.equal(l1, l0)
+        assert torch.equal(m1, m0)
+        assert torch.equal(r1, r0)
+    for nf in range(1, T + 1):
+        off1 = torch.zeros(T * H + 1, dtype=torch.int64, device="cuda")
+        h_tot = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        _lib.check(L.vfcp_qd_offsets_upto(pp, nf, r0.data_ptr(), off1.data_ptr(),
+                                          h_tot.data_ptr(), st), "offsets upto")
+        torch.cuda.synchronize()
+        assert torch.equal(off1[:nf * H + 1], off0[:nf * H + 1])
+        assert int(h_tot[0]) == int(off0[nf * H])
+    # a list that is too small raises the flag instead of dropping anchors
+    c1, l1, m1, r1 = arrays()
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(L.vfcp_analyze_slab(
+        pp, du.data_ptr(), dv.data_ptr(), 0, 0, T, c1.data_ptr(), l1.data_ptr(),
+        m1.data_ptr(), r1.data_ptr(), lst.data_ptr(), 1, cnt.data_ptr(),
+        ovf.data_ptr(), st), "analyze slab")
+    assert int(ovf[0]) == 1
+    # bad ranges
+    assert L.vfcp_analyze_slab(pp, du.data_ptr(), dv.data_ptr(), 0, 2, 2,
+                               c1.data_ptr(), l1.data_ptr(), None, r1.data_ptr(),
+                               lst.data_ptr(), cap, cnt.data_ptr(), ovf.data_ptr(),
+                               st) == -1
