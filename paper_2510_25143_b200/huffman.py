@@ -68,21 +68,6 @@ def encode(symbols, alphabet_size: int) -> bytes:
 
 
 _POOL = None
-_BA_NEW = None
-
-
-def new_bytearray(n: int) -> bytearray:
-    """A bytearray of n bytes WITHOUT bytearray(n)'s zero fill (which
-    touches every page of a fresh mapping single-threaded): the caller
-    overwrites all of it, with host_copy."""
-    global _BA_NEW
-    if _BA_NEW is None:
-        import ctypes
-        f = ctypes.pythonapi.PyByteArray_FromStringAndSize
-        f.restype = ctypes.py_object
-        f.argtypes = (ctypes.c_void_p, ctypes.c_ssize_t)
-        _BA_NEW = f
-    return _BA_NEW(None, n)
 
 
 def _pool():
@@ -108,19 +93,6 @@ def host_copy(dst: np.ndarray, src: np.ndarray) -> None:
     def part(o):
         dst[o:o + _STEP] = src[o:o + _STEP]
     list(_pool().map(part, range(0, n, _STEP)))
-
-
-def host_touch(dst: np.ndarray) -> list:
-    """First-touch the pages of a fresh destination on the host threads (one
-    write per page); returns the futures.  Started while the device still
-    packs, it takes the page faults out of the copy that follows."""
-    n = dst.size
-    if n <= _STEP:
-        return []
-
-    def part(o):
-        dst[o:o + _STEP:4096] = 0
-    return [_pool().submit(part, o) for o in range(0, n, _STEP)]
 
 
 class PendingBlob:
