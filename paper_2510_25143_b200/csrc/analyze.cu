@@ -420,10 +420,11 @@ cube_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
       uint32_t w = 0;
       const float xs[4] = {ru[q].x, ru[q].y, ru[q].z, ru[q].w};
       const float ys[4] = {rv[q].x, rv[q].y, rv[q].z, rv[q].w};
+      const bool inside = gi < H && gj + 3 < W;   // the usual group
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         uint32_t c = 0xffu;
-        if (gi < H && gj + e < W) {
+        if (inside || (gi < H && gj + e < W)) {
           if (sizeof(F) == 4) {
             c = cls_nib(xs[e], ys[e], (float)Tq);
           } else {
@@ -465,6 +466,9 @@ cube_kernel(const F* __restrict__ u, const F* __restrict__ v, int H, int W,
       for (int e = 0; e < 4; e++)
         if (((need >> (8 * e)) & 1u) && gi < H && j0 + 4 * g + e < W) m4 |= 1u << e;
       const int n = __popc(m4);
+      // (almost every row of 128 anchors lists nothing: one vote instead of
+      // the scan)
+      if (!__any_sync(FULL, n != 0)) continue;
       int incl = n;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
